@@ -1,0 +1,794 @@
+// nbvh_oracle.cpp — CPU ORACLE FOR N-BVH NEURAL RAY QUERIES.  TEST INFRASTRUCTURE ONLY.
+//
+// Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference
+// leg may load this library.  The product (paper_2405_16237_b200/) never links,
+// imports or calls it, and this file shares no code, header or table with it.
+//
+// Citation key: "P:n" = /root/reference/PAPER.md line n (section named alongside);
+// "C<k>" = the reading register in DESIGN.md §3 (= SURVEY.md §8(c) ambiguity register).
+//
+// Precision: continuous quantities (interpolation, MLP, losses, gradients, Adam,
+// triangle ground truth) are computed in double.  Discrete decisions that the GPU
+// must reproduce bit-for-bit (slab intervals, sample positions, grid cells) are
+// computed in IEEE binary32 with the operation order stated next to each, compiled
+// with -ffp-contract=off (no FMA) on SSE.
+//
+// Parity status per function is listed in DESIGN.md §4; every function here is
+// pinned by a `-m "not gpu"` test in tests/test_oracle_pins.py except
+// orc_query's end-to-end *quality* (P17: "parity unpinned" — the paper ships no
+// weights or per-query numbers).
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <limits>
+#include <vector>
+
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+extern "C" {
+
+// ------------------------------------------------------------------ fp16 decode
+// IEEE 754 binary16 -> double, written from the format definition
+// (1 sign bit, 5 exponent bits, bias 15, 10 fraction bits).
+double orc_half_to_double(uint16_t h) {
+    int s = (h >> 15) & 1, e = (h >> 10) & 31, m = h & 1023;
+    double v;
+    if (e == 0) v = std::ldexp((double)m, -24);                       // subnormal
+    else if (e == 31) v = m ? std::numeric_limits<double>::quiet_NaN()
+                            : std::numeric_limits<double>::infinity();
+    else v = std::ldexp((double)(1024 + m), e - 25);                  // normal
+    return s ? -v : v;
+}
+
+// ------------------------------------------------------------------ level table
+// P:275 (§6 "Neural model & training"): "The hash grid contains 8 levels, starting from
+// a base resolution of 8^3 to a maximum resolution of 1024^3".  Geometric spacing
+// b = (max/base)^(1/(L-1)), N_l = floor(base*b^l + 1e-9)        (C1)
+// Level l is dense iff (N_l+1)^3 <= T and then holds (N_l+1)^3 entries, else T (C2).
+// Returns the total number of entries; offsets are cumulative entry counts.
+int64_t orc_level_table(int L, int log2_T, int base_res, int max_res,
+                        int32_t* res, int32_t* dense, int64_t* offset) {
+    const int64_t T = (int64_t)1 << log2_T;
+    const double b = (L > 1) ? std::exp((std::log((double)max_res) - std::log((double)base_res)) / (L - 1)) : 1.0;
+    int64_t off = 0;
+    for (int l = 0; l < L; ++l) {
+        int64_t N = (int64_t)std::floor((double)base_res * std::pow(b, (double)l) + 1e-9);
+        int64_t full = (N + 1) * (N + 1) * (N + 1);
+        res[l] = (int32_t)N;
+        dense[l] = full <= T ? 1 : 0;
+        offset[l] = off;
+        off += dense[l] ? full : T;
+    }
+    return off;
+}
+
+// ------------------------------------------------------------------ corner index
+// Dense level: x + (N+1)(y + (N+1) z).  Hashed level, [Mueller22] as cited at P:101
+// (§3): (x*1 XOR y*2654435761 XOR z*805459861) mod T, in uint32 arithmetic (C3).
+uint32_t orc_corner_index(int32_t N, int32_t dense, int log2_T, uint32_t x, uint32_t y, uint32_t z) {
+    if (dense) {
+        uint32_t n1 = (uint32_t)N + 1u;
+        return x + n1 * (y + n1 * z);
+    }
+    uint32_t h = (x * 1u) ^ (y * 2654435761u) ^ (z * 805459861u);
+    return h & ((1u << log2_T) - 1u);
+}
+
+// ------------------------------------------------------------------ grid features
+// Fig. node_encoding: "at each point collect features from a multi-resolution
+// hash grid".  Per level: s = x*N (fp32), c = min(floor(s), N-1), f = s - c (fp32, exact);
+// the 8 corners c+delta (delta bit0=x, bit1=y, bit2=z) are fetched and trilinearly
+// weighted, w = prod_k (delta_k ? f_k : 1-f_k) (double).  Output [L][F], coarse -> fine.
+static void encode_point(int L, int F, int log2_T, const int32_t* res, const int32_t* dense,
+                         const int64_t* offset, const uint16_t* table, const float x[3],
+                         double* feat /*L*F*/, uint32_t* idx_out /*L*8, nullable*/) {
+    for (int l = 0; l < L; ++l) {
+        const int32_t N = res[l];
+        int32_t c[3];
+        float f[3];
+        for (int k = 0; k < 3; ++k) {
+            float s = x[k] * (float)N;
+            int32_t ci = (int32_t)std::floor(s);
+            if (ci > N - 1) ci = N - 1;
+            if (ci < 0) ci = 0;
+            c[k] = ci;
+            f[k] = s - (float)ci;
+        }
+        for (int j = 0; j < F; ++j) feat[l * F + j] = 0.0;
+        for (int corner = 0; corner < 8; ++corner) {
+            int d0 = corner & 1, d1 = (corner >> 1) & 1, d2 = (corner >> 2) & 1;
+            uint32_t idx = orc_corner_index(N, dense[l], log2_T, (uint32_t)(c[0] + d0),
+                                            (uint32_t)(c[1] + d1), (uint32_t)(c[2] + d2));
+            if (idx_out) idx_out[l * 8 + corner] = idx;
+            double w = (d0 ? (double)f[0] : 1.0 - (double)f[0]) *
+                       (d1 ? (double)f[1] : 1.0 - (double)f[1]) *
+                       (d2 ? (double)f[2] : 1.0 - (double)f[2]);
+            const uint16_t* row = table + (offset[l] + (int64_t)idx) * F;
+            for (int j = 0; j < F; ++j) feat[l * F + j] += w * orc_half_to_double(row[j]);
+        }
+    }
+}
+
+void orc_encode_points(int L, int F, int log2_T, const int32_t* res, const int32_t* dense,
+                       const int64_t* offset, const uint16_t* table, const float* pts, int64_t m,
+                       double* feat /*[m][L*F]*/, uint32_t* idx /*[m][L][8], nullable*/) {
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < m; ++i)
+        encode_point(L, F, log2_T, res, dense, offset, table, pts + 3 * i, feat + i * (int64_t)L * F,
+                     idx ? idx + i * (int64_t)L * 8 : nullptr);
+}
+
+// ------------------------------------------------------------------ ray / box slab test
+// P:103 (§3), P:116 (§4 "Motivation"): the query is parameterised by the ray-box
+// entry/exit interval.  fp32, op order: inv=1/d; tl=(lo-o)*inv; th=(hi-o)*inv;
+// tn=fminf(tl,th); tf=fmaxf(tl,th); te=max(tn.x,tn.y,tn.z,tmin) (left fold);
+// tx=min(tf.x,tf.y,tf.z,tmax); hit iff te <= tx.  A ray starting inside -> te = tmin (C7).
+int orc_slab(const float* ray /*ox,oy,oz,tmin,dx,dy,dz,tmax*/, const float* lo, const float* hi,
+             float* t_enter, float* t_exit) {
+    float tn[3], tf[3];
+    for (int k = 0; k < 3; ++k) {
+        float inv = 1.0f / ray[4 + k];
+        float tl = (lo[k] - ray[k]) * inv;
+        float th = (hi[k] - ray[k]) * inv;
+        tn[k] = std::fmin(tl, th);
+        tf[k] = std::fmax(tl, th);
+    }
+    float te = std::fmax(std::fmax(std::fmax(tn[0], tn[1]), tn[2]), ray[3]);
+    float tx = std::fmin(std::fmin(std::fmin(tf[0], tf[1]), tf[2]), ray[7]);
+    *t_enter = te;
+    *t_exit = tx;
+    return te <= tx ? 1 : 0;
+}
+
+// ------------------------------------------------------------------ ordered leaf list
+// P:161 (§5): queries happen "upon reaching a leaf node"; "front-to-back probing".
+// Brute force over every cut leaf (no hierarchy), sorted by (t_enter, leaf id) (C5).
+struct Entry { float te, tx; int32_t leaf; };
+
+static void leaf_list(const float* ray, const float* leaf_lo, const float* leaf_hi, int32_t n_leaves,
+                      std::vector<Entry>& out) {
+    out.clear();
+    for (int32_t i = 0; i < n_leaves; ++i) {
+        float te, tx;
+        if (orc_slab(ray, leaf_lo + 3 * i, leaf_hi + 3 * i, &te, &tx)) out.push_back({te, tx, i});
+    }
+    std::sort(out.begin(), out.end(), [](const Entry& a, const Entry& b) {
+        return a.te < b.te || (a.te == b.te && a.leaf < b.leaf);
+    });
+}
+
+// Writes up to `cap` entries per ray ([n][cap] row-major); count[i] = total number of
+// intersected leaves (may exceed cap).
+void orc_leaf_lists(const float* rays, int64_t n, const float* leaf_lo, const float* leaf_hi,
+                    int32_t n_leaves, int32_t cap, int32_t* leaf, float* t_enter, float* t_exit,
+                    int32_t* count) {
+#pragma omp parallel
+    {
+        std::vector<Entry> L;
+#pragma omp for schedule(dynamic, 64)
+        for (int64_t r = 0; r < n; ++r) {
+            leaf_list(rays + 8 * r, leaf_lo, leaf_hi, n_leaves, L);
+            count[r] = (int32_t)L.size();
+            for (int32_t k = 0; k < cap; ++k) {
+                bool ok = k < (int32_t)L.size();
+                leaf[r * cap + k] = ok ? L[k].leaf : -1;
+                t_enter[r * cap + k] = ok ? L[k].te : 0.0f;
+                t_exit[r * cap + k] = ok ? L[k].tx : 0.0f;
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------ grid domain
+// P:105 (§3): "a single global neural model encompassing the entire geometry".  The grid
+// covers the cube around the root box (union of the inflated cut-leaf boxes), side =
+// largest extent, centred (C4).  fp32 op order: lo/hi = min/max over leaves;
+// side = max(hi.x-lo.x, hi.y-lo.y, hi.z-lo.z); c = (lo+hi)*0.5; dom_min = c - side*0.5;
+// dom_inv = 1/side.
+void orc_domain(const float* leaf_lo, const float* leaf_hi, int32_t n_leaves, float* dom_min, float* dom_inv) {
+    float lo[3], hi[3];
+    for (int k = 0; k < 3; ++k) { lo[k] = leaf_lo[k]; hi[k] = leaf_hi[k]; }
+    for (int32_t i = 1; i < n_leaves; ++i)
+        for (int k = 0; k < 3; ++k) {
+            lo[k] = std::fmin(lo[k], leaf_lo[3 * i + k]);
+            hi[k] = std::fmax(hi[k], leaf_hi[3 * i + k]);
+        }
+    float side = std::fmax(std::fmax(hi[0] - lo[0], hi[1] - lo[1]), hi[2] - lo[2]);
+    for (int k = 0; k < 3; ++k) {
+        float c = (lo[k] + hi[k]) * 0.5f;
+        dom_min[k] = c - side * 0.5f;
+    }
+    *dom_inv = 1.0f / side;
+}
+
+// ------------------------------------------------------------------ segment sampling
+// P:133 ("We sample uniformly along a given ray-box intersection interval")
+// ("stratified point-sampling along the ray").  u_i = (2i+1)/(2n) at inference, or
+// (i + xi_i)/n when jitter xi is given (training) (C8).  fp32, op order:
+// dt = t1-t0; t = t0 + u*dt; p = o + t*d; x = clamp((p - dom_min)*dom_inv, 0, 1).
+// Points are ordered entry -> exit: the concatenation order encodes the direction.
+void orc_segment_points(const float* ray, float t0, float t1, int n, const float* xi /*nullable, n*/,
+                        const float* dom_min, float dom_inv, float* pts /*[n][3]*/) {
+    float dt = t1 - t0;
+    for (int i = 0; i < n; ++i) {
+        float u = xi ? ((float)i + xi[i]) / (float)n : (float)(2 * i + 1) / (float)(2 * n);
+        float t = t0 + u * dt;
+        for (int k = 0; k < 3; ++k) {
+            float p = ray[k] + t * ray[4 + k];
+            float x = (p - dom_min[k]) * dom_inv;
+            pts[3 * i + k] = std::fmin(std::fmax(x, 0.0f), 1.0f);
+        }
+    }
+}
+
+// ------------------------------------------------------------------ MLP
+// hidden layers of 64 neurons with ReLU; the output layer is linear here and the
+// sigmoid / linear output activations are applied by the decode (C10-C12).
+// Weights are fp16 [out][in] row-major (converted exactly to double), biases fp32.
+// Layer k has dims[k] inputs and dims[k+1] outputs; n_layers = hidden + 1.
+static void mlp_forward_one(int n_layers, const int32_t* dims, const uint16_t* const* W,
+                            const float* const* b, const double* x, double* z,
+                            std::vector<double>* acts /*nullable: post-activation per layer*/) {
+    std::vector<double> h(x, x + dims[0]), nxt;
+    if (acts) acts[0] = h;
+    for (int k = 0; k < n_layers; ++k) {
+        nxt.assign(dims[k + 1], 0.0);
+        for (int o = 0; o < dims[k + 1]; ++o) {
+            double s = (double)b[k][o];
+            for (int i = 0; i < dims[k]; ++i) s += orc_half_to_double(W[k][(int64_t)o * dims[k] + i]) * h[i];
+            nxt[o] = (k + 1 < n_layers) ? (s > 0.0 ? s : 0.0) : s;
+        }
+        h.swap(nxt);
+        if (acts) acts[k + 1] = h;
+    }
+    for (int o = 0; o < dims[n_layers]; ++o) z[o] = h[o];
+}
+
+// W_all / b_all: layers concatenated in order.
+static void split_layers(int n_layers, const int32_t* dims, const uint16_t* W_all, const float* b_all,
+                         std::vector<const uint16_t*>& W, std::vector<const float*>& b) {
+    W.resize(n_layers);
+    b.resize(n_layers);
+    int64_t wo = 0, bo = 0;
+    for (int k = 0; k < n_layers; ++k) {
+        W[k] = W_all + wo;
+        b[k] = b_all + bo;
+        wo += (int64_t)dims[k] * dims[k + 1];
+        bo += dims[k + 1];
+    }
+}
+
+void orc_mlp_forward(int n_layers, const int32_t* dims, const uint16_t* W_all, const float* b_all,
+                     const double* x, int64_t m, double* z) {
+    std::vector<const uint16_t*> W;
+    std::vector<const float*> b;
+    split_layers(n_layers, dims, W_all, b_all, W, b);
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < m; ++i)
+        mlp_forward_one(n_layers, dims, W.data(), b.data(), x + i * dims[0], z + i * dims[n_layers], nullptr);
+}
+
+// ------------------------------------------------------------------ decode
+static double sigmoid(double v) { return 1.0 / (1.0 + std::exp(-v)); }
+
+// ------------------------------------------------------------------ full neural ray query
+// Model description passed to the query / training oracles.
+struct OrcModel {
+    int32_t L, F, log2_T, n_points, n_layers;
+    const int32_t* res; const int32_t* dense; const int64_t* offset;
+    const uint16_t* table;          // fp16 [entries][F]
+    const int32_t* dims;            // n_layers+1
+    const uint16_t* W_all; const float* b_all;
+    const float* dom_min; float dom_inv;
+};
+
+// One (ray, leaf) neural query (Fig. node_encoding): sample the
+// interval, encode every point, concatenate [point][level][F], decode with the MLP.
+static void neural_query(const OrcModel& M, const std::vector<const uint16_t*>& W,
+                         const std::vector<const float*>& b, const float* ray, float t0, float t1,
+                         const float* xi, double* z, double* x_in /*nullable D_in*/,
+                         uint32_t* idx /*nullable n*L*8*/, float* pts_out /*nullable n*3*/,
+                         std::vector<double>* acts) {
+    const int n = M.n_points, LF = M.L * M.F;
+    std::vector<float> pts(3 * n);
+    orc_segment_points(ray, t0, t1, n, xi, M.dom_min, M.dom_inv, pts.data());
+    std::vector<double> x(n * LF);
+    for (int i = 0; i < n; ++i)
+        encode_point(M.L, M.F, M.log2_T, M.res, M.dense, M.offset, M.table, &pts[3 * i], &x[i * LF],
+                     idx ? idx + i * M.L * 8 : nullptr);
+    if (x_in) std::copy(x.begin(), x.end(), x_in);
+    if (pts_out) std::copy(pts.begin(), pts.end(), pts_out);
+    mlp_forward_one(M.n_layers, M.dims, W.data(), b.data(), x.data(), z, acts);
+}
+
+// P:161 (§5) traversal semantics, P:201 (§5.2 "Visibility": hit iff sigmoid < 0.5, C13),
+// P:237 ("locally learning the distance": t = t0 + sigmoid(z_t)(t1-t0)), P:243 (normal,
+// albedo).  mode 0 = R2 nearest hit: walk the (t_enter, id)-ordered list, query a leaf
+// iff t_enter <= t_best, keep argmin (t, t_enter, id).  mode 1 = R1: stop at the first
+// leaf whose query reports a hit (C5).
+// Outputs per ray: hit, t, normal[3], albedo[3], leaf, n_queries, and margin = min over
+// its queries of |sigmoid(z_vis) - 0.5| (for the ambiguity band), z_trace [n][cap][8]
+// (NaN where not queried, nullable).
+void orc_query(int32_t L, int32_t F, int32_t log2_T, int32_t n_points, int32_t n_layers,
+               const int32_t* res, const int32_t* dense, const int64_t* offset, const uint16_t* table,
+               const int32_t* dims, const uint16_t* W_all, const float* b_all,
+               const float* leaf_lo, const float* leaf_hi, int32_t n_leaves,
+               const float* rays, int64_t n, int32_t mode,
+               uint8_t* hit, float* t_out, float* normal, float* albedo, int32_t* leaf_out,
+               int32_t* nq_out, double* margin, double* z_trace, int32_t cap) {
+    float dom_min[3], dom_inv;
+    orc_domain(leaf_lo, leaf_hi, n_leaves, dom_min, &dom_inv);
+    OrcModel M{L, F, log2_T, n_points, n_layers, res, dense, offset, table, dims, W_all, b_all, dom_min, dom_inv};
+    std::vector<const uint16_t*> W;
+    std::vector<const float*> b;
+    split_layers(n_layers, dims, W_all, b_all, W, b);
+    const int n_out = dims[n_layers];
+#pragma omp parallel
+    {
+        std::vector<Entry> lst;
+        std::vector<double> z(n_out);
+#pragma omp for schedule(dynamic, 16)
+        for (int64_t r = 0; r < n; ++r) {
+            const float* ray = rays + 8 * r;
+            leaf_list(ray, leaf_lo, leaf_hi, n_leaves, lst);
+            if (z_trace)
+                for (int64_t k = 0; k < (int64_t)cap * 8; ++k) z_trace[r * cap * 8 + k] = std::nan("");
+            bool found = false;
+            double bt = 0, bte = 0, bn[3] = {0, 0, 0}, ba[3] = {0, 0, 0};
+            int32_t bleaf = -1, nq = 0;
+            double marg = std::numeric_limits<double>::infinity();
+            for (size_t k = 0; k < lst.size(); ++k) {
+                const Entry& e = lst[k];
+                if (found && (double)e.te > bt) break;              // front-to-back termination
+                neural_query(M, W, b, ray, e.te, e.tx, nullptr, z.data(), nullptr, nullptr, nullptr, nullptr);
+                ++nq;
+                if (z_trace && (int32_t)k < cap)
+                    for (int c = 0; c < 8; ++c) z_trace[(r * cap + k) * 8 + c] = z[c];
+                marg = std::min(marg, std::fabs(sigmoid(z[0]) - 0.5));
+                if (z[0] < 0.0) {                                    // sigmoid(z_vis) < 0.5: hit
+                    double tl = sigmoid(z[1]);
+                    double t = (double)e.te + tl * ((double)e.tx - (double)e.te);
+                    bool better = !found || t < bt || (t == bt && ((double)e.te < bte ||
+                                  ((double)e.te == bte && e.leaf < bleaf)));
+                    if (better) {
+                        found = true; bt = t; bte = e.te; bleaf = e.leaf;
+                        double nn = std::sqrt(z[2] * z[2] + z[3] * z[3] + z[4] * z[4]);
+                        nn = std::max(nn, 1e-6);
+                        for (int c = 0; c < 3; ++c) { bn[c] = z[2 + c] / nn; ba[c] = sigmoid(z[5 + c]); }
+                    }
+                    if (mode == 1) break;                            // R1: first confident hit
+                }
+            }
+            hit[r] = found ? 1 : 0;
+            t_out[r] = found ? (float)bt : std::numeric_limits<float>::infinity();
+            for (int c = 0; c < 3; ++c) {
+                normal[3 * r + c] = (float)bn[c];
+                albedo[3 * r + c] = (float)ba[c];
+            }
+            leaf_out[r] = bleaf;
+            nq_out[r] = nq;
+            margin[r] = marg;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ logic replay (fp32)
+// The decisions of the query (termination, hit, best-hit selection) replayed in fp32 on
+// a given z per (ray, list position) — e.g. the z the GPU recorded — so that hit mask,
+// winning leaf, t bits and query count can be compared exactly (SURVEY §8(c) tier iv).
+// fp32 op order: tl = (float)sigmoid_double(z_t); t = t0 + tl*(t1-t0);
+// normal: nn = sqrtf(nx*nx + ny*ny + nz*nz) (left fold), n/fmaxf(nn, 1e-6f);
+// albedo = (float)sigmoid_double(z).  Returns the number of rays where a needed z was
+// missing (NaN) from the trace.
+int64_t orc_replay(const float* leaf_lo, const float* leaf_hi, int32_t n_leaves, const float* rays,
+                   int64_t n, int32_t mode, const float* z_trace /*[n][cap][8]*/, int32_t cap,
+                   uint8_t* hit, float* t_out, float* normal, float* albedo, int32_t* leaf_out,
+                   int32_t* nq_out) {
+    int64_t missing = 0;
+#pragma omp parallel
+    {
+        std::vector<Entry> lst;
+#pragma omp for schedule(dynamic, 64) reduction(+ : missing)
+        for (int64_t r = 0; r < n; ++r) {
+            const float* ray = rays + 8 * r;
+            leaf_list(ray, leaf_lo, leaf_hi, n_leaves, lst);
+            bool found = false;
+            float bt = 0, bte = 0, bn[3] = {0, 0, 0}, ba[3] = {0, 0, 0};
+            int32_t bleaf = -1, nq = 0;
+            for (size_t k = 0; k < lst.size(); ++k) {
+                const Entry& e = lst[k];
+                if (found && e.te > bt) break;
+                if ((int32_t)k >= cap || std::isnan(z_trace[(r * cap + k) * 8])) { ++missing; break; }
+                const float* z = z_trace + (r * cap + k) * 8;
+                ++nq;
+                if (z[0] < 0.0f) {
+                    float tl = (float)sigmoid((double)z[1]);
+                    float t = e.te + tl * (e.tx - e.te);
+                    bool better = !found || t < bt || (t == bt && (e.te < bte || (e.te == bte && e.leaf < bleaf)));
+                    if (better) {
+                        found = true; bt = t; bte = e.te; bleaf = e.leaf;
+                        float nn = std::sqrt(z[2] * z[2] + z[3] * z[3] + z[4] * z[4]);
+                        nn = std::fmax(nn, 1e-6f);
+                        for (int c = 0; c < 3; ++c) { bn[c] = z[2 + c] / nn; ba[c] = (float)sigmoid((double)z[5 + c]); }
+                    }
+                    if (mode == 1) break;
+                }
+            }
+            hit[r] = found ? 1 : 0;
+            t_out[r] = found ? bt : std::numeric_limits<float>::infinity();
+            for (int c = 0; c < 3; ++c) { normal[3 * r + c] = bn[c]; albedo[3 * r + c] = ba[c]; }
+            leaf_out[r] = bleaf;
+            nq_out[r] = nq;
+        }
+    }
+    return missing;
+}
+
+// ------------------------------------------------------------------ cut structure check
+// P:180 (§5.1): the N-BVH leaves are "a cut in this BVH": every triangle lies in exactly
+// one leaf's subtree.  P:275: nodes are inflated "slightly" (C15: each side grown by
+// max(1e-3*diag(node), 1e-6*diag(scene))).  Inputs: mesh, per-leaf triangle lists (CSR),
+// per-leaf uninflated base boxes and inflated leaf boxes.  Returns a bitmask:
+// 1 = a triangle is in zero or several leaves; 2 = a triangle AABB escapes its base box;
+// 4 = a base box escapes its leaf box; 8 = inflation differs from C15 by > 1e-5 relative.
+int32_t orc_check_cut(const float* verts, const uint32_t* tris, int64_t nt, int32_t n_leaves,
+                      const int64_t* leaf_tri_off, const int32_t* leaf_tris,
+                      const float* base_lo, const float* base_hi, const float* leaf_lo,
+                      const float* leaf_hi, double scene_diag) {
+    int32_t bad = 0;
+    std::vector<int32_t> seen(nt, 0);
+    for (int32_t l = 0; l < n_leaves; ++l) {
+        for (int64_t j = leaf_tri_off[l]; j < leaf_tri_off[l + 1]; ++j) {
+            int32_t t = leaf_tris[j];
+            if (t < 0 || t >= nt) { bad |= 1; continue; }
+            seen[t] += 1;
+            for (int v = 0; v < 3; ++v)
+                for (int k = 0; k < 3; ++k) {
+                    float p = verts[3 * tris[3 * t + v] + k];
+                    if (p < base_lo[3 * l + k] || p > base_hi[3 * l + k]) bad |= 2;
+                }
+        }
+        double d2 = 0;
+        for (int k = 0; k < 3; ++k) {
+            if (base_lo[3 * l + k] < leaf_lo[3 * l + k] || base_hi[3 * l + k] > leaf_hi[3 * l + k]) bad |= 4;
+            double e = (double)base_hi[3 * l + k] - (double)base_lo[3 * l + k];
+            d2 += e * e;
+        }
+        double pad = std::max(1e-3 * std::sqrt(d2), 1e-6 * scene_diag);
+        for (int k = 0; k < 3; ++k) {
+            double plo = (double)base_lo[3 * l + k] - (double)leaf_lo[3 * l + k];
+            double phi = (double)leaf_hi[3 * l + k] - (double)base_hi[3 * l + k];
+            double tol = 1e-5 * pad + 4.0 * std::ldexp(1.0, -23) * (std::fabs((double)base_lo[3 * l + k]) + std::fabs((double)base_hi[3 * l + k]));
+            if (std::fabs(plo - pad) > tol || std::fabs(phi - pad) > tol) bad |= 8;
+        }
+    }
+    for (int64_t t = 0; t < nt; ++t)
+        if (seen[t] != 1) bad |= 1;
+    return bad;
+}
+
+// ------------------------------------------------------------------ triangle ground truth
+// ground truth is "obtained by intersecting the actual geometry".  Moller-Trumbore
+// in double (inputs fp32, converted exactly), op order as written; accepts t in [t0,t1].
+// Returns 1 and (t, b1, b2) on a hit.  Degenerate (|det| < 1e-20) -> no hit.
+int orc_triangle_hit(const double o[3], const double d[3], const double v0[3], const double v1[3],
+                     const double v2[3], double t0, double t1, double* t_out, double* b1, double* b2) {
+    double e1[3] = {v1[0] - v0[0], v1[1] - v0[1], v1[2] - v0[2]};
+    double e2[3] = {v2[0] - v0[0], v2[1] - v0[1], v2[2] - v0[2]};
+    double p[3] = {d[1] * e2[2] - d[2] * e2[1], d[2] * e2[0] - d[0] * e2[2], d[0] * e2[1] - d[1] * e2[0]};
+    double det = e1[0] * p[0] + e1[1] * p[1] + e1[2] * p[2];
+    if (std::fabs(det) < 1e-20) return 0;
+    double inv = 1.0 / det;
+    double s[3] = {o[0] - v0[0], o[1] - v0[1], o[2] - v0[2]};
+    double u = (s[0] * p[0] + s[1] * p[1] + s[2] * p[2]) * inv;
+    if (u < 0.0 || u > 1.0) return 0;
+    double q[3] = {s[1] * e1[2] - s[2] * e1[1], s[2] * e1[0] - s[0] * e1[2], s[0] * e1[1] - s[1] * e1[0]};
+    double v = (d[0] * q[0] + d[1] * q[1] + d[2] * q[2]) * inv;
+    if (v < 0.0 || u + v > 1.0) return 0;
+    double t = (e2[0] * q[0] + e2[1] * q[1] + e2[2] * q[2]) * inv;
+    if (t < t0 || t > t1) return 0;
+    *t_out = t; *b1 = u; *b2 = v;
+    return 1;
+}
+
+// Nearest hit among a triangle list within [t0,t1]; ties -> lowest triangle id.
+// gt: [vis, t_local, nx, ny, nz, ar, ag, ab, t_hit]; vis = 1 means NO intersection.
+// Shading normal = barycentric blend of vertex normals, normalised (C22).
+static void label_segment(const float* verts, const uint32_t* tris, const float* vnormals,
+                          const float* tri_albedo, const int32_t* tri_list, int64_t n_list,
+                          const float* ray, float t0, float t1, double* gt) {
+    double o[3] = {ray[0], ray[1], ray[2]}, d[3] = {ray[4], ray[5], ray[6]};
+    bool found = false;
+    double bt = 0, bb1 = 0, bb2 = 0;
+    int32_t btri = -1;
+    for (int64_t j = 0; j < n_list; ++j) {
+        int32_t t = tri_list[j];
+        double v[3][3];
+        for (int a = 0; a < 3; ++a)
+            for (int k = 0; k < 3; ++k) v[a][k] = verts[3 * tris[3 * t + a] + k];
+        double th, b1, b2;
+        if (orc_triangle_hit(o, d, v[0], v[1], v[2], (double)t0, (double)t1, &th, &b1, &b2)) {
+            if (!found || th < bt || (th == bt && t < btri)) { found = true; bt = th; bb1 = b1; bb2 = b2; btri = t; }
+        }
+    }
+    for (int c = 0; c < 9; ++c) gt[c] = 0.0;
+    gt[0] = found ? 0.0 : 1.0;
+    if (!found) return;
+    double dt = (double)t1 - (double)t0;
+    gt[1] = dt > 0.0 ? (bt - (double)t0) / dt : 0.0;
+    double n[3];
+    for (int k = 0; k < 3; ++k)
+        n[k] = (1.0 - bb1 - bb2) * vnormals[3 * tris[3 * btri + 0] + k] + bb1 * vnormals[3 * tris[3 * btri + 1] + k] +
+               bb2 * vnormals[3 * tris[3 * btri + 2] + k];
+    double nn = std::sqrt(n[0] * n[0] + n[1] * n[1] + n[2] * n[2]);
+    for (int k = 0; k < 3; ++k) gt[2 + k] = nn > 0 ? n[k] / nn : 0.0;
+    for (int k = 0; k < 3; ++k) gt[5 + k] = tri_albedo[3 * btri + k];
+    gt[8] = bt;
+}
+
+// Batch labelling of (ray, leaf, [t0,t1]) segments against each leaf's triangle list.
+void orc_label(const float* verts, const uint32_t* tris, const float* vnormals, const float* tri_albedo,
+               const int64_t* leaf_tri_off, const int32_t* leaf_tris, const float* rays, const int32_t* leaf,
+               const float* t0, const float* t1, int64_t n, double* gt /*[n][9]*/) {
+#pragma omp parallel for schedule(dynamic, 16)
+    for (int64_t i = 0; i < n; ++i) {
+        int32_t l = leaf[i];
+        label_segment(verts, tris, vnormals, tri_albedo, leaf_tris + leaf_tri_off[l],
+                      leaf_tri_off[l + 1] - leaf_tri_off[l], rays + 8 * i, t0[i], t1[i], gt + 9 * i);
+    }
+}
+
+// ------------------------------------------------------------------ losses
+// Per-sample combined loss: L = 2 L_vis + g (2 L_dist + L_normal + L_albedo),
+// g = [gt_vis == 0] ("If the ground-truth visibility is 1 ... we set the losses for
+// all other data to zero").  L_vis = BCE(sigmoid(z0), gt_vis); L_dist =
+// |sigmoid(z1) - gt_t|; L_normal = mean_3 |z2..4 - gt_n| (P:243, L1 on the
+// linear output); L_albedo = mean_3 (a-y)^2/(sg(a)^2 + 0.01), a = sigmoid(z5..7)
+// (P:243 relative L2, C19).  Writes the four terms and dL/dz[8]; returns L.
+// den (nullable, 3): if den_mode == 1 the albedo denominators are taken from den (frozen,
+// the value-level meaning of the stop-gradient), if den_mode == 0 they are written to it.
+static double sample_loss_impl(const double* z, const double* gt, double* terms, double* dz, double* den,
+                               int den_mode);
+double orc_sample_loss(const double* z, const double* gt, double* terms /*4, nullable*/, double* dz /*8, nullable*/) {
+    return sample_loss_impl(z, gt, terms, dz, nullptr, 0);
+}
+static double sample_loss_impl(const double* z, const double* gt, double* terms, double* dz, double* den,
+                               int den_mode) {
+    const double y = gt[0];
+    // BCE(sigmoid(z), y) = softplus(z) - y z, written stably.
+    double lvis = std::max(z[0], 0.0) - z[0] * y + std::log1p(std::exp(-std::fabs(z[0])));
+    double g = (y == 0.0) ? 1.0 : 0.0;
+    double st = sigmoid(z[1]);
+    double ldist = std::fabs(st - gt[1]);
+    double lnorm = 0, lalb = 0;
+    for (int k = 0; k < 3; ++k) lnorm += std::fabs(z[2 + k] - gt[2 + k]) / 3.0;
+    double a[3];
+    for (int k = 0; k < 3; ++k) {
+        a[k] = sigmoid(z[5 + k]);
+        double dk = a[k] * a[k] + 0.01;
+        if (den && den_mode == 1) dk = den[k];
+        else if (den) den[k] = dk;
+        lalb += (a[k] - gt[5 + k]) * (a[k] - gt[5 + k]) / dk / 3.0;
+    }
+    if (terms) { terms[0] = lvis; terms[1] = g * ldist; terms[2] = g * lnorm; terms[3] = g * lalb; }
+    if (dz) {
+        auto sgn = [](double v) { return v > 0 ? 1.0 : (v < 0 ? -1.0 : 0.0); };
+        dz[0] = 2.0 * (sigmoid(z[0]) - y);
+        dz[1] = g * 2.0 * sgn(st - gt[1]) * st * (1.0 - st);
+        for (int k = 0; k < 3; ++k) dz[2 + k] = g * sgn(z[2 + k] - gt[2 + k]) / 3.0;
+        for (int k = 0; k < 3; ++k)
+            dz[5 + k] = g * 2.0 * (a[k] - gt[5 + k]) / (a[k] * a[k] + 0.01) / 3.0 * a[k] * (1.0 - a[k]);
+    }
+    return 2.0 * lvis + g * (2.0 * ldist + lnorm + lalb);
+}
+
+// ------------------------------------------------------------------ training gradient
+// One training step's forward + backward in double ("the measured loss is
+// back-propagated to the model's learnable parameters"; P:197 first-leaf-only training
+// with acceptance probability max(r/r_max, 0.005), C18; P:193 rays against the cut).
+// Inputs: rays [n][8]; u [n] acceptance draws; xi [n][n_points] stratification jitter;
+// leaf_rank [n_leaves] (rank r; acceptance p = max((r - min r + 1e-6)/max(...), 0.005)
+// in fp32, op order as written, so both sides take the decision in fp32).
+// Outputs: gradients of the mean loss over accepted samples w.r.t. the fp16-valued
+// parameters: g_table [entries*F], g_W (concatenated, [out][in]), g_b; per-sample
+// records (accepted flag, leaf, loss) and the loss sum; returns #accepted.
+int64_t orc_train_grad(int32_t L, int32_t F, int32_t log2_T, int32_t n_points, int32_t n_layers,
+                       const int32_t* res, const int32_t* dense, const int64_t* offset, const uint16_t* table,
+                       int64_t n_entries, const int32_t* dims, const uint16_t* W_all, const float* b_all,
+                       const float* leaf_lo, const float* leaf_hi, int32_t n_leaves,
+                       const float* leaf_rank, const int64_t* leaf_tri_off, const int32_t* leaf_tris,
+                       const float* verts, const uint32_t* tris, const float* vnormals, const float* tri_albedo,
+                       const float* rays, int64_t n, const float* u, const float* xi,
+                       double* g_table, double* g_W, double* g_b,
+                       uint8_t* accepted, int32_t* first_leaf, double* sample_loss, double* gt_out /*[n][9]*/,
+                       double* loss_sum) {
+    float dom_min[3], dom_inv;
+    orc_domain(leaf_lo, leaf_hi, n_leaves, dom_min, &dom_inv);
+    OrcModel M{L, F, log2_T, n_points, n_layers, res, dense, offset, table, dims, W_all, b_all, dom_min, dom_inv};
+    std::vector<const uint16_t*> W;
+    std::vector<const float*> b;
+    split_layers(n_layers, dims, W_all, b_all, W, b);
+    // acceptance probabilities (fp32, C18)
+    float rmin = leaf_rank[0], rmax = leaf_rank[0];
+    for (int32_t i = 1; i < n_leaves; ++i) { rmin = std::fmin(rmin, leaf_rank[i]); rmax = std::fmax(rmax, leaf_rank[i]); }
+    const float eps = 1e-6f;
+    float rhmax = (rmax - rmin) + eps;
+    std::vector<float> pacc(n_leaves);
+    for (int32_t i = 0; i < n_leaves; ++i) pacc[i] = std::fmax(((leaf_rank[i] - rmin) + eps) / rhmax, 0.005f);
+
+    int64_t nW = 0, nb = 0;
+    for (int k = 0; k < n_layers; ++k) { nW += (int64_t)dims[k] * dims[k + 1]; nb += dims[k + 1]; }
+    std::fill(g_table, g_table + n_entries * F, 0.0);
+    std::fill(g_W, g_W + nW, 0.0);
+    std::fill(g_b, g_b + nb, 0.0);
+
+    // pass 1: select + label (independent per ray)
+    std::vector<float> s_t0(n), s_t1(n);
+    int64_t n_acc = 0;
+    std::vector<Entry> lst;
+    for (int64_t r = 0; r < n; ++r) {
+        accepted[r] = 0; first_leaf[r] = -1; sample_loss[r] = 0.0;
+        for (int c = 0; c < 9; ++c) gt_out[9 * r + c] = 0.0;
+        leaf_list(rays + 8 * r, leaf_lo, leaf_hi, n_leaves, lst);
+        if (lst.empty()) continue;
+        const Entry& e = lst[0];                                   // first leaf only
+        first_leaf[r] = e.leaf;
+        if (!(u[r] < pacc[e.leaf])) continue;                      // stochastic acceptance
+        accepted[r] = 1;
+        s_t0[r] = e.te; s_t1[r] = e.tx;
+        ++n_acc;
+        int32_t l = e.leaf;
+        label_segment(verts, tris, vnormals, tri_albedo, leaf_tris + leaf_tri_off[l],
+                      leaf_tri_off[l + 1] - leaf_tri_off[l], rays + 8 * r, e.te, e.tx, gt_out + 9 * r);
+    }
+    *loss_sum = 0.0;
+    if (n_acc == 0) return 0;
+    const double inv_m = 1.0 / (double)n_acc;                      // mean over accepted samples (C19)
+    const int LF = L * F, D = dims[0];
+    // pass 2: forward, loss, backward (serial accumulation: deterministic)
+    std::vector<double> z(8), dz(8), x(D);
+    std::vector<uint32_t> idx(n_points * L * 8);
+    std::vector<float> pts(3 * n_points);
+    std::vector<std::vector<double>> acts(n_layers + 1);
+    for (int64_t r = 0; r < n; ++r) {
+        if (!accepted[r]) continue;
+        neural_query(M, W, b, rays + 8 * r, s_t0[r], s_t1[r], xi + r * n_points, z.data(), x.data(),
+                     idx.data(), pts.data(), acts.data());
+        double lr = orc_sample_loss(z.data(), gt_out + 9 * r, nullptr, dz.data());
+        sample_loss[r] = lr;
+        *loss_sum += lr;
+        // backward through the MLP: delta = dL/d(pre-activation) of layer k
+        std::vector<double> delta(dz.begin(), dz.end());
+        for (int i = 0; i < dims[n_layers]; ++i) delta[i] *= inv_m;
+        int64_t wo = nW, bo = nb;
+        for (int k = n_layers - 1; k >= 0; --k) {
+            wo -= (int64_t)dims[k] * dims[k + 1];
+            bo -= dims[k + 1];
+            const std::vector<double>& hin = acts[k];
+            std::vector<double> dprev(dims[k], 0.0);
+            for (int o = 0; o < dims[k + 1]; ++o) {
+                g_b[bo + o] += delta[o];
+                for (int i = 0; i < dims[k]; ++i) {
+                    g_W[wo + (int64_t)o * dims[k] + i] += delta[o] * hin[i];
+                    dprev[i] += delta[o] * orc_half_to_double(W[k][(int64_t)o * dims[k] + i]);
+                }
+            }
+            if (k > 0)
+                for (int i = 0; i < dims[k]; ++i) dprev[i] = hin[i] > 0.0 ? dprev[i] : 0.0;  // ReLU'
+            delta.swap(dprev);
+        }
+        // delta = dL/dx (concatenated features) -> scatter into the tables through the
+        // trilinear weights (hash-grid backprop).
+        for (int p = 0; p < n_points; ++p)
+            for (int l = 0; l < L; ++l) {
+                const int32_t N = res[l];
+                float f[3];
+                for (int k = 0; k < 3; ++k) {
+                    float s = pts[3 * p + k] * (float)N;
+                    int32_t ci = (int32_t)std::floor(s);
+                    if (ci > N - 1) ci = N - 1;
+                    if (ci < 0) ci = 0;
+                    f[k] = s - (float)ci;
+                }
+                for (int corner = 0; corner < 8; ++corner) {
+                    int d0 = corner & 1, d1 = (corner >> 1) & 1, d2 = (corner >> 2) & 1;
+                    double w = (d0 ? (double)f[0] : 1.0 - (double)f[0]) * (d1 ? (double)f[1] : 1.0 - (double)f[1]) *
+                               (d2 ? (double)f[2] : 1.0 - (double)f[2]);
+                    int64_t row = offset[l] + (int64_t)idx[(p * L + l) * 8 + corner];
+                    for (int j = 0; j < F; ++j) g_table[row * F + j] += w * delta[p * LF + l * F + j];
+                }
+            }
+    }
+    return n_acc;
+}
+
+// Loss of the same batch for given (double) parameter values — used by the finite
+// difference pin (P13).  With den_mode = 1 the relative-L2 denominators are frozen at the
+// values recorded by a den_mode = 0 call, which is what the stop-gradient means (C19).  Parameters are passed as double arrays (not fp16) so that
+// central differences can perturb them; selection/labels come from a previous
+// orc_train_grad call (accepted, first_leaf, gt) so the loss is a smooth function.
+double orc_batch_loss_double(int32_t L, int32_t F, int32_t log2_T, int32_t n_points, int32_t n_layers,
+                             const int32_t* res, const int32_t* dense, const int64_t* offset,
+                             const double* table, const int32_t* dims, const double* W_all, const double* b_all,
+                             const float* leaf_lo, const float* leaf_hi, int32_t n_leaves,
+                             const float* rays, int64_t n, const float* xi, const uint8_t* accepted,
+                             const float* t0, const float* t1, const double* gt,
+                             double* den /*[n][3]*/, int32_t den_mode) {
+    float dom_min[3], dom_inv;
+    orc_domain(leaf_lo, leaf_hi, n_leaves, dom_min, &dom_inv);
+    const int LF = L * F;
+    int64_t n_acc = 0;
+    double tot = 0;
+    std::vector<float> pts(3 * n_points);
+    std::vector<double> h, nxt;
+    for (int64_t r = 0; r < n; ++r) {
+        if (!accepted[r]) continue;
+        ++n_acc;
+        orc_segment_points(rays + 8 * r, t0[r], t1[r], n_points, xi + r * n_points, dom_min, dom_inv, pts.data());
+        h.assign(n_points * LF, 0.0);
+        for (int p = 0; p < n_points; ++p)
+            for (int l = 0; l < L; ++l) {
+                const int32_t N = res[l];
+                int32_t c[3];
+                float f[3];
+                for (int k = 0; k < 3; ++k) {
+                    float s = pts[3 * p + k] * (float)N;
+                    int32_t ci = (int32_t)std::floor(s);
+                    if (ci > N - 1) ci = N - 1;
+                    if (ci < 0) ci = 0;
+                    c[k] = ci;
+                    f[k] = s - (float)ci;
+                }
+                for (int corner = 0; corner < 8; ++corner) {
+                    int d0 = corner & 1, d1 = (corner >> 1) & 1, d2 = (corner >> 2) & 1;
+                    uint32_t ix = orc_corner_index(N, dense[l], log2_T, c[0] + d0, c[1] + d1, c[2] + d2);
+                    double w = (d0 ? (double)f[0] : 1.0 - (double)f[0]) * (d1 ? (double)f[1] : 1.0 - (double)f[1]) *
+                               (d2 ? (double)f[2] : 1.0 - (double)f[2]);
+                    for (int j = 0; j < F; ++j) h[p * LF + l * F + j] += w * table[(offset[l] + ix) * F + j];
+                }
+            }
+        int64_t wo = 0, bo = 0;
+        for (int k = 0; k < n_layers; ++k) {
+            nxt.assign(dims[k + 1], 0.0);
+            for (int o = 0; o < dims[k + 1]; ++o) {
+                double s = b_all[bo + o];
+                for (int i = 0; i < dims[k]; ++i) s += W_all[wo + (int64_t)o * dims[k] + i] * h[i];
+                nxt[o] = (k + 1 < n_layers) ? (s > 0 ? s : 0) : s;
+            }
+            wo += (int64_t)dims[k] * dims[k + 1];
+            bo += dims[k + 1];
+            h.swap(nxt);
+        }
+        tot += sample_loss_impl(h.data(), gt + 9 * r, nullptr, nullptr, den ? den + 3 * r : nullptr, den_mode);
+    }
+    return n_acc ? tot / (double)n_acc : 0.0;
+}
+
+// ------------------------------------------------------------------ Adam
+// "Adam optimizer [kingma2014adam] with default hyper-parameters and a learning
+// rate of 0.01" (C20: beta1 0.9, beta2 0.999, eps 1e-8, bias-corrected, dense).
+// step is the 1-based step number of this update.
+void orc_adam(double* param, const double* grad, double* m, double* v, int64_t n, int64_t step,
+              double lr, double beta1, double beta2, double eps) {
+    const double c1 = 1.0 - std::pow(beta1, (double)step), c2 = 1.0 - std::pow(beta2, (double)step);
+    for (int64_t i = 0; i < n; ++i) {
+        m[i] = beta1 * m[i] + (1.0 - beta1) * grad[i];
+        v[i] = beta2 * v[i] + (1.0 - beta2) * grad[i] * grad[i];
+        double mh = m[i] / c1, vh = v[i] / c2;
+        param[i] -= lr * mh / (std::sqrt(vh) + eps);
+    }
+}
+
+int32_t orc_num_threads(void) {
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
+
+}  // extern "C"

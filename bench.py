@@ -1,0 +1,347 @@
+#!/usr/bin/env python
+"""N-BVH neural ray-query benchmark (BASELINE.json metric: neural ray queries Mrays/s).
+
+Default workload = BASELINE configs[1] ("1080p"): 988,928-triangle procedural scene,
+2,048-leaf cut, hash grid L=16 T=2^19 F=2, n=4 samples, MLP 3x64; one step = one full
+1920x1080 frame of primary rays through nbvh_query (traversal + all query waves).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1080p|tiny] [--impl ours|reference]
+
+Multi-GPU (torchrun): every rank renders its own 1080p frame (camera jittered by rank)
+with a replicated model; no collective on the data path; value = all ranks' rays / max
+rank time ("scaling": "weak").  `--impl reference` times the CPU oracle (oracle/) on a
+bounded sample of the same workload (there is no reference implementation to install:
+the paper ships no code).  Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "neural ray queries Mrays/s"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), float(p["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._proc = None
+
+    def start(self):
+        try:
+            self._proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self._proc = None
+
+    def _read(self):
+        for line in self._proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.samples.append(parts)
+
+    def stop(self):
+        if self._proc:
+            time.sleep(0.25)
+            self._proc.terminate()
+            try:
+                self._proc.wait(timeout=2)
+            except Exception:
+                self._proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def build_model(cfg_name: str, device: int, rank: int = 0):
+    """Synthetic scene + cut + random-init model of the named BASELINE config."""
+    from paper_2405_16237_b200 import Context, PARAM_TABLES
+    c = synth.CONFIGS[cfg_name]
+    h = c["hash"]
+    sc = synth.scene_tiny(c["seeds"]["mesh"]) if cfg_name == "tiny" else synth.scene_1080p(c["seeds"]["mesh"])
+    ctx = Context(device=device, L=h.L, F=h.F, log2_T=h.log2_T, n_points=h.n_points, hidden_layers=h.hidden_layers)
+    ctx.set_mesh(sc)
+    ctx.build_cut(c["leaves"])
+    n_tab = ctx.param_count(PARAM_TABLES)
+    ctx.set_params(PARAM_TABLES, synth.random_params_fp16(n_tab, seed=c["seeds"]["weights"]).astype(np.float32))
+    ctx.set_mlp(synth.random_mlp(ctx.d_in, h.hidden_layers, 64, seed=c["seeds"]["weights"] + 1))
+    eye = np.asarray(c["eye"], np.float64)
+    if rank:
+        eye = eye + np.array([0.05 * np.sin(rank), 0.0, 0.05 * np.cos(rank)])
+    rays = synth.camera_rays(*c["res"], eye, vfov_deg=c["vfov"])
+    return ctx, sc, rays, c
+
+
+def cpu_oracle_rate(ctx, c, rays, target_s: float = 12.0, max_rays: int | None = None):
+    """Time the oracle (as it stands) on a deterministic strided sample of the frame."""
+    import oracle
+    h = c["hash"]
+    g = oracle.Grid(h.L, h.log2_T, h.F)
+    from paper_2405_16237_b200 import PARAM_TABLES, PARAM_WEIGHTS, PARAM_BIASES
+    tab = ctx.get_params(PARAM_TABLES).astype(np.float16).reshape(-1, h.F)
+    W = ctx.get_params(PARAM_WEIGHTS)
+    b = ctx.get_params(PARAM_BIASES)
+    dims = [ctx.d_in] + [64] * h.hidden_layers + [8]
+    layers, wo, bo = [], 0, 0
+    for k in range(len(dims) - 1):
+        layers.append((W[wo:wo + dims[k] * dims[k + 1]].reshape(dims[k + 1], dims[k]).astype(np.float16),
+                       b[bo:bo + dims[k + 1]]))
+        wo += dims[k] * dims[k + 1]
+        bo += dims[k + 1]
+    cut = ctx.cut(0)
+    # calibrate on a small sample, then size the timed sample to ~target_s
+    probe = rays[:: max(1, rays.shape[0] // 512)]
+    t0 = time.perf_counter()
+    oracle.query(g, h.n_points, tab, layers, cut["leaf_lo"], cut["leaf_hi"], probe)
+    per_ray = (time.perf_counter() - t0) / probe.shape[0]
+    n = int(min(rays.shape[0], max(256, target_s / max(per_ray, 1e-9))))
+    if max_rays:
+        n = min(n, max_rays)
+    stride = max(1, rays.shape[0] // n)
+    sample = rays[::stride][:n]
+    t0 = time.perf_counter()
+    oracle.query(g, h.n_points, tab, layers, cut["leaf_lo"], cut["leaf_hi"], sample)
+    dt = time.perf_counter() - t0
+    return {"value": sample.shape[0] / dt / 1e6, "unit": "Mrays/s", "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"every {stride}th primary ray of the frame ({sample.shape[0]} rays), C++ double oracle, "
+                      f"brute-force leaf scan, OpenMP", "seconds": dt}
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    ctx, sc, rays_np, c = build_model(args.config, local, rank)
+    n = rays_np.shape[0]
+    ctx.reserve(n)
+    rays = torch.from_numpy(rays_np).cuda()
+    out = ctx.alloc_hits(n)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")   # > 126 MB L2
+
+    ctx.set_profiling(False)
+    for _ in range(args.warmup):
+        ctx.query(rays, out=out)
+    torch.cuda.synchronize()
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    launches = 0
+    queries = 0
+    waves = []
+    clocks = ClockSampler(local)
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    wall0 = time.perf_counter()
+    for i in range(args.steps):
+        flush.fill_(float(i))                                  # evict L2 between timed steps
+        starts[i].record(stream)
+        ctx.query(rays, out=out)
+        ends[i].record(stream)
+        st = ctx.query_stats()
+        launches += st["n_launches"]
+        queries += st["n_queries"]
+        waves.append(st["n_waves"])
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - wall0
+    if world > 1:
+        dist.barrier()
+    clocks.stop()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    t_ms = sum(step_ms)
+    tmax = torch.tensor([t_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    t_ms = float(tmax.item())
+    total_rays = n * args.steps * world
+    value = total_rays / (t_ms / 1e3) / 1e6
+
+    # live per-kernel timing of the dominant kernel (fused query wave), one profiled pass
+    # per timed step (separate from the timed region; events on the launching stream)
+    ctx.set_profiling(True)
+    wave_ms, trav_ms, prof_q = [], [], []
+    for i in range(max(3, args.steps)):
+        flush.fill_(float(i))
+        ctx.query(rays, out=out)
+        st = ctx.query_stats()
+        wave_ms.append(st["ms_waves"])
+        trav_ms.append(st["ms_traverse"])
+        prof_q.append(st["n_queries"])
+    ctx.set_profiling(False)
+    h = c["hash"]
+    useful_gather = h.n_points * h.L * 8 * h.F * 2                # fp16 corner bytes per query
+    per_query_io = 32 + 12 + 8 * 4 + 8 + 29                       # ray, list entry, state r/w, outputs (approx.)
+    bytes_per_query = useful_gather + per_query_io
+    mean_q = statistics.mean(prof_q)
+    wave_s = statistics.mean(wave_ms) / 1e3
+    achieved = mean_q * bytes_per_query / wave_s / 1e9
+    hbm, tflops, peak_src = _peaks()
+    mlp_flops = 2 * (ctx.d_in * 64 + (h.hidden_layers - 1) * 64 * 64 + 64 * 8)
+
+    # end-to-end through the public host API: pinned host rays in, host results out
+    e2e = None
+    if rank == 0 or True:
+        pin = torch.from_numpy(rays_np).pin_memory()
+        hb = {"hit": torch.empty(n, dtype=torch.uint8).pin_memory(), "t": torch.empty(n).pin_memory(),
+              "normal": torch.empty(n, 3).pin_memory(), "albedo": torch.empty(n, 3).pin_memory(),
+              "leaf": torch.empty(n, dtype=torch.int32).pin_memory(),
+              "n_queries": torch.empty(n, dtype=torch.int32).pin_memory()}
+        hbn = {k: v.numpy() for k, v in hb.items()}
+        pin_np = pin.numpy()
+        ctx.query_host(pin_np, out=hbn)
+        torch.cuda.synchronize()
+        e2e_s = []
+        for i in range(args.steps):
+            flush.fill_(float(i))
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            ctx.query_host(pin_np, out=hbn)                       # synchronous: H2D + query + D2H
+            e2e_s.append(time.perf_counter() - t0)
+        e2e_t = torch.tensor([sum(e2e_s)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+        d2h = n * (1 + 4 + 12 + 12 + 4 + 4)
+        e2e = {"value": n * args.steps * world / float(e2e_t.item()) / 1e6, "unit": "Mrays/s",
+               "h2d_bytes_per_step": n * 32, "d2h_bytes_per_step": d2h}
+
+    line = None
+    if rank == 0:
+        cpu = cpu_oracle_rate(ctx, c, rays_np, target_s=args.cpu_seconds) if args.cpu_seconds > 0 else None
+        line = {
+            "metric": METRIC, "value": value, "unit": "Mrays/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f16", "data": "synthetic",
+            "config": {"workload": f"{args.config}: " + ("988,928-tri procedural terrain+spheres, 2048-leaf cut, "
+                                                         "L=16 T=2^19 F=2 n=4, MLP 3x64, 1920x1080 primary rays"
+                                                         if args.config == "1080p" else
+                                                         "9,680-tri displaced icosphere, 64-leaf cut, L=8 T=2^14 "
+                                                         "F=2 n=4, MLP 2x64, 64x64 primary rays"),
+                       "rays_per_step_per_gpu": n, "model": "random-init tables U[-1,1], He MLP (x10 output)",
+                       "l2_flush": "256 MB write between timed steps, outside the per-step CUDA events",
+                       "parallelism": f"replicated model, 1 frame per rank (weak), {world} rank(s)"},
+            "gpu_launches": launches,
+            "queries_per_ray": queries / (n * args.steps), "waves_per_step": statistics.mean(waves),
+            "wall_s_timed_region": wall,
+            "roofline": {"bound": "hbm", "kernel": "k_query_wave (fused sample+encode+MLP+decode+compact)",
+                         "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                         "peak_source": peak_src, "traffic": None,
+                         "bytes_per_query": bytes_per_query, "useful_gather_bytes_per_query": useful_gather,
+                         "queries_per_launch_sum": mean_q, "kernel_ms_per_step": statistics.mean(wave_ms),
+                         "traverse_ms_per_step": statistics.mean(trav_ms),
+                         "mlp_tflops": mean_q * mlp_flops / wave_s / 1e12,
+                         "mlp_frac_of_bf16_peak": mean_q * mlp_flops / wave_s / 1e12 / tflops},
+            "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_reference(args):
+    """The CPU oracle timed as it stands on bounded samples of the same workload."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    from paper_2405_16237_b200 import Context  # host-only context: scene/cut/params, no GPU
+    ctx, sc, rays, c = build_model(args.config, -1)
+    per_step = max(256, rays.shape[0] // 256) if args.config == "1080p" else rays.shape[0]
+    stride = max(1, rays.shape[0] // per_step)
+    h = c["hash"]
+    g = oracle.Grid(h.L, h.log2_T, h.F)
+    from paper_2405_16237_b200 import PARAM_TABLES, PARAM_WEIGHTS, PARAM_BIASES
+    tab = ctx.get_params(PARAM_TABLES).astype(np.float16).reshape(-1, h.F)
+    W = ctx.get_params(PARAM_WEIGHTS)
+    b = ctx.get_params(PARAM_BIASES)
+    dims = [ctx.d_in] + [64] * h.hidden_layers + [8]
+    layers, wo, bo = [], 0, 0
+    for k in range(len(dims) - 1):
+        layers.append((W[wo:wo + dims[k] * dims[k + 1]].reshape(dims[k + 1], dims[k]).astype(np.float16),
+                       b[bo:bo + dims[k + 1]]))
+        wo += dims[k] * dims[k + 1]
+        bo += dims[k + 1]
+    cut = ctx.cut(0)
+
+    def step(i):
+        sample = rays[(i % stride)::stride][:per_step]
+        oracle.query(g, h.n_points, tab, layers, cut["leaf_lo"], cut["leaf_hi"], sample)
+        return sample.shape[0]
+
+    for i in range(args.warmup):
+        step(i)
+    t0 = time.perf_counter()
+    done = sum(step(args.warmup + i) for i in range(args.steps))
+    dt = time.perf_counter() - t0
+    v = done / dt / 1e6
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "Mrays/s", "n_gpus": 0, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.config, "rays_per_step": per_step},
+            "cpu_baseline": {"value": v, "unit": "Mrays/s", "cores": oracle.num_threads(), "kind": "oracle",
+                             "sample": f"{per_step} rays per step (every {stride}th primary ray, offset by step)"},
+            "e2e": {"value": v, "unit": "Mrays/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="1080p", choices=["1080p", "tiny"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle timing budget (0 = skip)")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,231 @@
+/* nbvh.h — C ABI of the B200-native N-BVH neural ray-query library (libnbvh.so).
+ *
+ * N-BVH (Weier et al., SIGGRAPH 2024, arXiv 2405.16237).  Citations "P:n" are lines of
+ * the paper's text (/root/reference/PAPER.md, read-only at build time); the readings
+ * "C<k>" are listed in DESIGN.md §3.
+ *
+ * Problem statement: a ray goes in; a hit record of visibility,
+ * depth, normal and albedo comes out, computed by traversing a cut of the scene's BVH
+ * (the N-BVH) and querying a multi-resolution hash grid + MLP at the leaves
+ * the ray crosses (Fig. node_encoding).  The companion training step
+ * learns the grid and MLP from BVH-probed ray/response pairs.
+ *
+ * Conventions (all entry points):
+ *  - Every call returns nbvh_status; no C++ exception crosses the ABI.  Arguments are
+ *    validated before any launch; on error the call has no effect and
+ *    nbvh_last_error(ctx) describes it.  After a CUDA error the context is poisoned and
+ *    every later call returns NBVH_ECUDA.
+ *  - "host" pointers are CPU memory, copied during the call; "device" pointers are CUDA
+ *    global memory of the context's device, owned by the caller, and must stay valid
+ *    until the stream work completes.  Stream arguments are cudaStream_t passed as
+ *    void*; NULL is the legacy default stream.  Calls taking a stream are asynchronous
+ *    and stream-ordered unless stated otherwise; calls without one are synchronous.
+ *  - One context per device; a context is not thread-safe.  Multi-GPU runs use one
+ *    context per process (torch.distributed launches), see DESIGN.md §7.
+ */
+#ifndef NBVH_H
+#define NBVH_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    NBVH_OK = 0,
+    NBVH_WARN_CLAMPED = 1,   /* request clamped (e.g. target leaves > base-BVH leaves)      */
+    NBVH_EINVAL = -1,        /* bad config, size, or NULL required pointer                  */
+    NBVH_ERANGE = -2,        /* LoD slot / index out of range                               */
+    NBVH_ESTATE = -3,        /* call order: no mesh / no cut / no device / not reserved     */
+    NBVH_ENONFINITE = -4,    /* non-finite loss or gradient: update skipped, params intact  */
+    NBVH_ECUDA = -5,         /* CUDA runtime error (context poisoned)                       */
+    NBVH_ENOMEM = -6         /* allocation failed                                           */
+} nbvh_status;
+
+typedef struct nbvh_ctx nbvh_ctx;
+
+/* One ray, 32 B, array-of-structs.  d need not be unit length.  The query considers
+ * t in [tmin, tmax]; tmax may be +inf. */
+typedef struct {
+    float ox, oy, oz, tmin;
+    float dx, dy, dz, tmax;
+} nbvh_ray;
+
+/* Per-ray results, structure-of-arrays, all device pointers of n elements (normal and
+ * albedo n*3).  hit: 1 if the N-BVH reports an intersection (visibility < 0.5).
+ * t: world distance along the ray, +inf on a miss.  normal: unit,
+ * albedo in (0,1); zeros on a miss.  leaf (nullable): winning cut-leaf id or -1.
+ * n_queries (nullable): neural queries performed for the ray. */
+typedef struct {
+    uint8_t* hit;
+    float* t;
+    float* normal;
+    float* albedo;
+    int32_t* leaf;
+    int32_t* n_queries;
+} nbvh_hits;
+
+/* Model and query configuration.  Defaults (nbvh_config_default) = BASELINE cfg 1. */
+typedef struct {
+    int32_t L;              /* hash-grid levels (8)                                  */
+    int32_t F;              /* features per level, 2 or 4 (4)                        */
+    int32_t log2_T;         /* table size T = 2^log2_T per hashed level ("hash-map size") */
+    int32_t base_res;       /* coarsest resolution (8)                               */
+    int32_t max_res;        /* finest resolution (1024)                              */
+    int32_t n_points;       /* samples per ray segment (three; BASELINE: 4)          */
+    int32_t hidden_layers;  /* hidden layers of width 64 (4; BASELINE: 2 or 3)       */
+    int32_t width;          /* hidden width; must be 64                                     */
+    int32_t list_cap;       /* per-ray ordered leaf-list capacity K, 1..32 (C6)             */
+    int32_t mode;           /* 0 = nearest confident hit (R2), 1 = first confident hit (R1) (C5) */
+    float inflate_rel;      /* node inflation, fraction of node diagonal (C15: 1e-3)        */
+    float inflate_abs;      /* node inflation floor, fraction of scene diagonal (C15: 1e-6) */
+    uint64_t seed;          /* parameter-initialisation seed (C21)                          */
+} nbvh_config;
+
+/* Parameter blocks for nbvh_get_params / nbvh_set_params.  All are fp32 master values;
+ * the fp16 inference copy is their round-to-nearest-even conversion (C14). */
+typedef enum {
+    NBVH_PARAM_TABLES = 0,  /* [n_entries][F], levels concatenated, offsets from nbvh_level_table */
+    NBVH_PARAM_WEIGHTS = 1, /* layer k: [out][in] row-major, layers concatenated (in: D_in, 64..; out: 64.., 8) */
+    NBVH_PARAM_BIASES = 2,  /* layer k: [out], concatenated                                  */
+    NBVH_PARAM_ALL = 3      /* flat: tables, weights, biases — the gradient-buffer layout    */
+} nbvh_param_block;
+
+/* Counters of the last nbvh_query (host-visible after the stream is synchronised). */
+typedef struct {
+    int64_t n_rays;
+    int64_t n_queries;       /* sum over rays of neural queries                             */
+    int32_t n_waves;         /* query waves executed                                        */
+    int32_t n_launches;      /* kernels launched by the call                                */
+    int32_t n_refills;       /* re-traversals after a leaf-list overflow (C6)               */
+    float ms_traverse;       /* device time of the traversal kernel (profiling on, else 0)  */
+    float ms_waves;          /* summed device time of the fused query-wave kernels          */
+} nbvh_query_stats;
+
+/* Training counters of the last nbvh_train_backward / nbvh_train_step. */
+typedef struct {
+    int64_t n_rays;          /* rays offered                                                */
+    int64_t n_first_hit;     /* rays that intersect at least one cut leaf                   */
+    int64_t n_accepted;      /* samples trained (P:197 acceptance)                          */
+    double loss_sum;         /* sum of per-sample combined losses                   */
+    double loss_terms[4];    /* sums of vis, dist, normal, albedo terms (weights 2,2,1,1 applied) */
+    int32_t n_launches;
+    int32_t skipped;         /* 1 if the update was rejected (non-finite)                   */
+} nbvh_train_stats;
+
+/* ---------------------------------------------------------------- lifecycle */
+void nbvh_config_default(nbvh_config* cfg);
+/* cuda_device >= 0: device context; -1: host-only context (mesh, BVH and cut building
+ * only — every call that needs the GPU returns NBVH_ESTATE).  Parameters are
+ * initialised per C21 from cfg->seed (tables U[-1e-4,1e-4], He-uniform weights, zero biases). */
+nbvh_status nbvh_create(const nbvh_config* cfg, int cuda_device, nbvh_ctx** out);
+void nbvh_destroy(nbvh_ctx* ctx);
+/* Context-owned message of the last failing call; valid until the next call. */
+const char* nbvh_last_error(const nbvh_ctx* ctx);
+/* Hash-grid level table (C1, C2): res[L], dense[L] (0/1), offset[L] (entries); host outputs. */
+nbvh_status nbvh_level_table(const nbvh_ctx* ctx, int32_t* res, int32_t* dense, int64_t* offset,
+                             int64_t* n_entries);
+/* Number of fp32 values in a parameter block. */
+nbvh_status nbvh_param_count(const nbvh_ctx* ctx, int32_t block, int64_t* n);
+nbvh_status nbvh_get_params(nbvh_ctx* ctx, int32_t block, float* host_dst, int64_t n);
+nbvh_status nbvh_set_params(nbvh_ctx* ctx, int32_t block, const float* host_src, int64_t n);
+/* Preallocate workspaces for up to max_rays rays per nbvh_query / nbvh_train_* call. */
+nbvh_status nbvh_reserve(nbvh_ctx* ctx, int64_t max_rays);
+
+/* ---------------------------------------------------------------- scene and cut (host) */
+/* Copies the mesh (host pointers): xyz [nv][3], tri [nt][3] (vertex indices), vnormal
+ * [nv][3] (nullable -> area-weighted normals are generated), tri_albedo [nt][3]
+ * (nullable -> 0.5 grey).  Builds the base BVH on the CPU with a full-sweep SAH builder
+ * (P:271), leaves of <= 4 triangles, and uploads it for ground-truth labelling. */
+nbvh_status nbvh_set_mesh(nbvh_ctx* ctx, const float* xyz, int64_t nv, const uint32_t* tri, int64_t nt,
+                          const float* vnormal, const float* tri_albedo);
+/* Builds a cut through the base BVH with target_leaves leaves into LoD slot
+ * lod_slot (0..7).  Nodes are split greedily by rank: with leaf_q/leaf_p
+ * (nullable, per current leaf of that slot) r = 2 ln q + ln p; otherwise by
+ * surface area (static score).  Leaves are inflated per C15; inner boxes of the
+ * shallow N-BVH hierarchy are exact unions of their children.  Returns
+ * NBVH_WARN_CLAMPED if target_leaves exceeds the number of base leaves. */
+nbvh_status nbvh_build_cut(nbvh_ctx* ctx, int32_t target_leaves, const float* leaf_q, const float* leaf_p,
+                           int32_t lod_slot, int32_t* out_n_leaves);
+/* Cut inspection (host outputs, any pointer nullable): leaf boxes (inflated) [n][3],
+ * base boxes (uninflated) [n][3], leaf triangle lists in CSR form (tri_off [n+1],
+ * tris [n_tris], original triangle ids), grid domain (C4). */
+nbvh_status nbvh_cut_info(const nbvh_ctx* ctx, int32_t lod, int32_t* n_leaves, int32_t* n_inner);
+nbvh_status nbvh_get_cut(const nbvh_ctx* ctx, int32_t lod, float* leaf_lo, float* leaf_hi, float* base_lo,
+                         float* base_hi, int64_t* tri_off, int32_t* tris, float* dom_min, float* dom_inv);
+
+/* ---------------------------------------------------------------- query (device) */
+/* Neural ray query of n rays (device nbvh_ray[n]) against LoD slot lod: cut
+ * traversal with an ordered per-ray leaf list, per-leaf segment sampling + hash-grid
+ * encode + MLP, decode and front-to-back termination with ray compaction.  Results in
+ * caller-owned device arrays.  Requires nbvh_reserve(n). */
+nbvh_status nbvh_query(nbvh_ctx* ctx, const nbvh_ray* d_rays, int64_t n, int32_t lod, nbvh_hits d_out,
+                       void* stream);
+/* Same computation from HOST rays into HOST results: copies rays host->device, runs
+ * nbvh_query, copies the results device->host and synchronises the stream (the
+ * end-to-end path).  Host buffers should be pinned for full copy bandwidth. */
+nbvh_status nbvh_query_host(nbvh_ctx* ctx, const nbvh_ray* h_rays, int64_t n, int32_t lod, nbvh_hits h_out,
+                            void* stream);
+/* Counters of the last query (the query call has already synchronised its stream). */
+nbvh_status nbvh_get_query_stats(nbvh_ctx* ctx, nbvh_query_stats* out);
+/* on != 0: record CUDA events around every kernel the query launches (on the query's
+ * stream) and report their durations in nbvh_query_stats. */
+nbvh_status nbvh_set_profiling(nbvh_ctx* ctx, int32_t on);
+
+/* ---------------------------------------------------------------- training (device) */
+/* Forward + backward of one training batch into the context's
+ * fp32 gradient buffer (overwritten): for each ray the first intersected cut leaf of
+ * LoD `lod` is accepted with probability max(r_hat/r_hat_max, 0.005) (C18)
+ * using the caller's draws d_u[n] in [0,1); accepted segments are labelled by
+ * intersecting that leaf's triangles (C17), sampled with jitter d_xi[n][n_points]
+ * (C8), encoded, decoded, and the gated weighted loss (C19) is
+ * back-propagated into the MLP and hash tables.  The gradient is of the SUM of
+ * per-sample losses; nbvh_apply_update divides by the accepted-sample count.
+ * d_rays/d_u/d_xi are device pointers. */
+nbvh_status nbvh_train_backward(nbvh_ctx* ctx, const nbvh_ray* d_rays, int64_t n, const float* d_u,
+                                const float* d_xi, int32_t lod, void* stream);
+/* The flat fp32 gradient buffer (device, context-owned, NBVH_PARAM_ALL layout) followed
+ * by one float holding the accepted-sample count and n_leaves*2 per-leaf statistics
+ * (loss sum, sample count).  Data-parallel training all-reduces (sum) n_floats values
+ * in place between nbvh_train_backward and nbvh_apply_update. */
+nbvh_status nbvh_grad_buffer(nbvh_ctx* ctx, float** d_grad, int64_t* n_floats);
+/* Adam step (C20) on every parameter with gradient g / max(1, accepted count
+ * read from the buffer tail); refreshes the fp16 inference copy.  A non-finite
+ * gradient skips the update (NBVH_ENONFINITE reported by nbvh_get_train_stats). */
+nbvh_status nbvh_apply_update(nbvh_ctx* ctx, float lr, void* stream);
+/* backward + apply_update on one rank. */
+nbvh_status nbvh_train_step(nbvh_ctx* ctx, const nbvh_ray* d_rays, int64_t n, const float* d_u,
+                            const float* d_xi, int32_t lod, float lr, void* stream);
+/* Counters of the last training call; synchronises the stream first. */
+nbvh_status nbvh_get_train_stats(nbvh_ctx* ctx, nbvh_train_stats* out);
+/* Per-leaf acceptance ranks r (C18) used by nbvh_train_backward (host, n_leaves floats). */
+nbvh_status nbvh_set_leaf_rank(nbvh_ctx* ctx, int32_t lod, const float* h_rank);
+
+/* ---------------------------------------------------------------- parity hooks (device) */
+/* The same kernels with intermediate results exposed. */
+/* Ordered leaf lists: leaf/t_enter/t_exit [n][cap] (row-major, -1 / 0 past the end),
+ * count[n] = total intersected leaves (may exceed cap). */
+nbvh_status nbvh_debug_traverse(nbvh_ctx* ctx, const nbvh_ray* d_rays, int64_t n, int32_t lod, int32_t cap,
+                                int32_t* d_leaf, float* d_t_enter, float* d_t_exit, int32_t* d_count,
+                                void* stream);
+/* Encode m points already normalised to [0,1]^3 (float [m][3]): fp16 features
+ * [m][L*F] (bits as uint16) and corner indices [m][L][8] (nullable). */
+nbvh_status nbvh_debug_encode(nbvh_ctx* ctx, const float* d_points, int64_t m, uint16_t* d_feat,
+                              uint32_t* d_index, void* stream);
+/* MLP of m fp16 input rows [m][D_in] -> raw outputs z [m][8] (fp32). */
+nbvh_status nbvh_debug_mlp(nbvh_ctx* ctx, const uint16_t* d_in, int64_t m, float* d_z, void* stream);
+/* nbvh_query that also records the raw MLP output of every query: z_trace [n][cap][8]
+ * (fp32, NaN where not queried, positions >= cap not recorded). */
+nbvh_status nbvh_debug_query_trace(nbvh_ctx* ctx, const nbvh_ray* d_rays, int64_t n, int32_t lod,
+                                   nbvh_hits d_out, float* d_z_trace, int32_t cap, void* stream);
+/* Ground-truth labels of the last training batch: gt [n][9] = vis, t_local, normal,
+ * albedo, t_hit (vis=1: no hit) with accepted[n] and first-leaf ids (device). */
+nbvh_status nbvh_debug_train_samples(nbvh_ctx* ctx, float* d_gt, uint8_t* d_accepted, int32_t* d_leaf,
+                                     float* d_loss, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NBVH_H */

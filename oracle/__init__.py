@@ -165,13 +165,13 @@ def query(grid: Grid, n_points, table_fp16, layers, leaf_lo, leaf_hi, rays, mode
     n = rays.shape[0]
     out = dict(hit=np.zeros(n, np.uint8), t=np.zeros(n, np.float32), normal=np.zeros((n, 3), np.float32),
                albedo=np.zeros((n, 3), np.float32), leaf=np.zeros(n, np.int32), nq=np.zeros(n, np.int32),
-               margin=np.zeros(n, np.float64))
+               margin=np.zeros(n, np.float64), tmargin=np.zeros(n, np.float64))
     zt = np.zeros((n, trace_cap, 8), np.float64) if trace_cap else None
     lib().orc_query(grid.L, grid.F, grid.log2_T, n_points, len(layers), _p(grid.res), _p(grid.dense),
                     _p(grid.offset), _p(tab), _p(dims), _p(W_all), _p(b_all), _p(lo), _p(hi),
                     C.c_int32(lo.shape[0]), _p(rays), C.c_int64(n), C.c_int32(mode), _p(out["hit"]),
                     _p(out["t"]), _p(out["normal"]), _p(out["albedo"]), _p(out["leaf"]), _p(out["nq"]),
-                    _p(out["margin"]), _p(zt), C.c_int32(trace_cap))
+                    _p(out["margin"]), _p(zt), C.c_int32(trace_cap), _p(out["tmargin"]))
     if zt is not None:
         out["z_trace"] = zt
     return out

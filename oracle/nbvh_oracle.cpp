@@ -312,14 +312,16 @@ static void neural_query(const OrcModel& M, const std::vector<const uint16_t*>& 
 // leaf whose query reports a hit (C5).
 // Outputs per ray: hit, t, normal[3], albedo[3], leaf, n_queries, and margin = min over
 // its queries of |sigmoid(z_vis) - 0.5| (for the ambiguity band), z_trace [n][cap][8]
-// (NaN where not queried, nullable).
+// (NaN where not queried, nullable), tmargin (nullable) = min distance between the best
+// t and any t it was compared with (termination entries, competing hits): decisions
+// closer than the MLP's precision are ambiguous too.
 void orc_query(int32_t L, int32_t F, int32_t log2_T, int32_t n_points, int32_t n_layers,
                const int32_t* res, const int32_t* dense, const int64_t* offset, const uint16_t* table,
                const int32_t* dims, const uint16_t* W_all, const float* b_all,
                const float* leaf_lo, const float* leaf_hi, int32_t n_leaves,
                const float* rays, int64_t n, int32_t mode,
                uint8_t* hit, float* t_out, float* normal, float* albedo, int32_t* leaf_out,
-               int32_t* nq_out, double* margin, double* z_trace, int32_t cap) {
+               int32_t* nq_out, double* margin, double* z_trace, int32_t cap, double* tmargin) {
     float dom_min[3], dom_inv;
     orc_domain(leaf_lo, leaf_hi, n_leaves, dom_min, &dom_inv);
     OrcModel M{L, F, log2_T, n_points, n_layers, res, dense, offset, table, dims, W_all, b_all, dom_min, dom_inv};
@@ -341,8 +343,10 @@ void orc_query(int32_t L, int32_t F, int32_t log2_T, int32_t n_points, int32_t n
             double bt = 0, bte = 0, bn[3] = {0, 0, 0}, ba[3] = {0, 0, 0};
             int32_t bleaf = -1, nq = 0;
             double marg = std::numeric_limits<double>::infinity();
+            double tmarg = std::numeric_limits<double>::infinity();
             for (size_t k = 0; k < lst.size(); ++k) {
                 const Entry& e = lst[k];
+                if (found) tmarg = std::min(tmarg, std::fabs((double)e.te - bt));
                 if (found && (double)e.te > bt) break;              // front-to-back termination
                 neural_query(M, W, b, ray, e.te, e.tx, nullptr, z.data(), nullptr, nullptr, nullptr, nullptr);
                 ++nq;
@@ -352,6 +356,7 @@ void orc_query(int32_t L, int32_t F, int32_t log2_T, int32_t n_points, int32_t n
                 if (z[0] < 0.0) {                                    // sigmoid(z_vis) < 0.5: hit
                     double tl = sigmoid(z[1]);
                     double t = (double)e.te + tl * ((double)e.tx - (double)e.te);
+                    if (found) tmarg = std::min(tmarg, std::fabs(t - bt));
                     bool better = !found || t < bt || (t == bt && ((double)e.te < bte ||
                                   ((double)e.te == bte && e.leaf < bleaf)));
                     if (better) {
@@ -372,6 +377,7 @@ void orc_query(int32_t L, int32_t F, int32_t log2_T, int32_t n_points, int32_t n
             leaf_out[r] = bleaf;
             nq_out[r] = nq;
             margin[r] = marg;
+            if (tmargin) tmargin[r] = tmarg;
         }
     }
 }

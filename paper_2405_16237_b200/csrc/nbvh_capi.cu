@@ -1,0 +1,679 @@
+// nbvh_capi.cu — implementation of the C ABI in include/nbvh.h: context and parameter
+// management, scene/cut upload, the query wave driver and the parity hooks.
+// The training entry points live in nbvh_train.cu.
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/nbvh.h"
+#include "nbvh_capi_internal.h"
+
+using namespace nbvh;
+
+// ------------------------------------------------------------------ helpers
+namespace nbvh {
+
+nbvh_status fail(nbvh_ctx* c, nbvh_status s, const std::string& msg) {
+    if (c) c->err = msg;
+    return s;
+}
+
+nbvh_status cuda_fail(nbvh_ctx* c, cudaError_t e, const char* where) {
+    if (c) {
+        c->poisoned = true;
+        c->err = std::string(where) + ": " + cudaGetErrorString(e);
+    }
+    return NBVH_ECUDA;
+}
+
+nbvh_status check_device(nbvh_ctx* c) {
+    if (!c) return NBVH_EINVAL;
+    if (c->poisoned) return NBVH_ECUDA;
+    if (c->device < 0) return fail(c, NBVH_ESTATE, "host-only context (created with cuda_device = -1)");
+    cudaError_t e = cudaSetDevice(c->device);
+    if (e != cudaSuccess) return cuda_fail(c, e, "cudaSetDevice");
+    return NBVH_OK;
+}
+
+template <typename T>
+static cudaError_t dalloc(T** p, size_t count) {
+    *p = nullptr;
+    if (count == 0) return cudaSuccess;
+    return cudaMalloc((void**)p, count * sizeof(T));
+}
+
+template <typename T>
+static void dfree(T*& p) {
+    if (p) cudaFree((void*)p);
+    p = nullptr;
+}
+
+GridDev make_grid(const nbvh_ctx* c, int lod) {
+    GridDev g{};
+    g.L = c->cfg.L;
+    g.F = c->cfg.F;
+    g.n_points = c->cfg.n_points;
+    g.log2_T = c->cfg.log2_T;
+    for (int l = 0; l < c->cfg.L; ++l) {
+        g.res[l] = c->res[l];
+        g.dense[l] = c->dense[l];
+        g.offset[l] = (uint32_t)c->offset[l];
+    }
+    g.table = c->d_table16;
+    if (lod >= 0) {
+        const HostCut& hc = c->cuts[lod];
+        for (int k = 0; k < 3; ++k) g.dom_min[k] = hc.dom_min[k];
+        g.dom_inv = hc.dom_inv;
+    }
+    return g;
+}
+
+MlpDev make_mlp(const nbvh_ctx* c) {
+    MlpDev m{};
+    m.d_in = c->d_in;
+    m.hidden = c->cfg.hidden_layers;
+    m.W = c->d_W16;
+    m.b = c->d_params + c->n_table + c->n_W;
+    return m;
+}
+
+CutDev make_cut(const nbvh_ctx* c, int lod) {
+    CutDev d{};
+    d.inner = c->dcut[lod].inner;
+    d.leaf_box = c->dcut[lod].leaf_box;
+    d.n_leaves = c->cuts[lod].n_leaves;
+    return d;
+}
+
+// fp32 master -> fp16 inference copy (tables and weights; biases stay fp32).
+__global__ void k_refresh_fp16(const float* __restrict__ src, __half* __restrict__ dst, int64_t n) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i < n; i += (int64_t)gridDim.x * blockDim.x) dst[i] = __float2half_rn(src[i]);
+}
+
+nbvh_status refresh_fp16(nbvh_ctx* c, cudaStream_t s) {
+    const int64_t nt = c->n_table, nw = c->n_W;
+    k_refresh_fp16<<<1184, 256, 0, s>>>(c->d_params, c->d_table16, nt);
+    k_refresh_fp16<<<148, 256, 0, s>>>(c->d_params + nt, c->d_W16, nw);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(c, e, "refresh_fp16");
+    return NBVH_OK;
+}
+
+}  // namespace nbvh
+
+// ------------------------------------------------------------------ lifecycle
+extern "C" void nbvh_config_default(nbvh_config* cfg) {
+    if (!cfg) return;
+    std::memset(cfg, 0, sizeof(*cfg));
+    cfg->L = 8;
+    cfg->F = 2;
+    cfg->log2_T = 14;
+    cfg->base_res = 8;
+    cfg->max_res = 1024;
+    cfg->n_points = 4;
+    cfg->hidden_layers = 2;
+    cfg->width = 64;
+    cfg->list_cap = 16;
+    cfg->mode = 0;
+    cfg->inflate_rel = 1e-3f;
+    cfg->inflate_abs = 1e-6f;
+    cfg->seed = 1;
+}
+
+namespace {
+
+uint64_t splitmix64(uint64_t& s) {
+    uint64_t z = (s += 0x9E3779B97F4A7C15ull);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+double unit(uint64_t& s) { return (double)(splitmix64(s) >> 11) * (1.0 / 9007199254740992.0); }
+
+}  // namespace
+
+extern "C" nbvh_status nbvh_create(const nbvh_config* cfg, int cuda_device, nbvh_ctx** out) {
+    if (!cfg || !out) return NBVH_EINVAL;
+    *out = nullptr;
+    const nbvh_config& c = *cfg;
+    if (c.L < 1 || c.L > kMaxLevels || (c.F != 2 && c.F != 4) || c.log2_T < 4 || c.log2_T > 24 || c.base_res < 1 ||
+        c.max_res < c.base_res || c.n_points < 1 || c.hidden_layers < 1 || c.hidden_layers > kMaxHidden ||
+        c.width != kWidth || c.list_cap < 1 || c.list_cap > kListK || (c.mode != 0 && c.mode != 1))
+        return NBVH_EINVAL;
+    const int d_in = c.n_points * c.L * c.F;
+    if ((c.L * c.F) % 8 != 0 || !(d_in == 32 || d_in == 64 || d_in == 96 || d_in == 128)) return NBVH_EINVAL;
+    nbvh_ctx* x = new (std::nothrow) nbvh_ctx();
+    if (!x) return NBVH_ENOMEM;
+    x->cfg = c;
+    x->device = cuda_device;
+    x->d_in = d_in;
+    level_table(c.L, c.log2_T, c.base_res, c.max_res, x->res, x->dense, x->offset, &x->n_entries);
+    x->n_table = x->n_entries * c.F;
+    x->n_W = (int64_t)64 * d_in + (int64_t)(c.hidden_layers - 1) * 64 * 64 + 8 * 64;
+    x->n_b = (int64_t)64 * c.hidden_layers + 8;
+    // C21 initialisation
+    x->h_params.resize(x->n_table + x->n_W + x->n_b);
+    uint64_t s = c.seed * 0x2545F4914F6CDD1Dull + 12345;
+    for (int64_t i = 0; i < x->n_table; ++i) x->h_params[i] = (float)((unit(s) * 2.0 - 1.0) * 1e-4);
+    int64_t o = x->n_table;
+    for (int k = 0; k <= c.hidden_layers; ++k) {
+        const int fan_in = k == 0 ? d_in : 64, fan_out = k == c.hidden_layers ? 8 : 64;
+        const double lim = std::sqrt(6.0 / fan_in);
+        for (int64_t i = 0; i < (int64_t)fan_in * fan_out; ++i) x->h_params[o++] = (float)((unit(s) * 2.0 - 1.0) * lim);
+    }
+    for (int64_t i = 0; i < x->n_b; ++i) x->h_params[o++] = 0.0f;
+    if (cuda_device >= 0) {
+        cudaError_t e = cudaSetDevice(cuda_device);
+        if (e == cudaSuccess) e = dalloc(&x->d_params, x->h_params.size());
+        if (e == cudaSuccess) e = dalloc(&x->d_table16, x->n_table);
+        if (e == cudaSuccess) e = dalloc(&x->d_W16, x->n_W);
+        if (e == cudaSuccess) e = dalloc(&x->d_misc, 64);
+        if (e == cudaSuccess) e = dalloc(&x->d_cnt, kMaxWaves);
+        if (e == cudaSuccess) e = cudaMallocHost((void**)&x->h_cnt, kMaxWaves * sizeof(int32_t));
+        if (e == cudaSuccess)
+            e = cudaMemcpy(x->d_params, x->h_params.data(), x->h_params.size() * 4, cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) e = cudaMemset(x->d_misc, 0, 64 * sizeof(int32_t));
+        if (e != cudaSuccess) {
+            x->err = std::string("nbvh_create: ") + cudaGetErrorString(e);
+            nbvh_destroy(x);
+            cudaGetLastError();
+            return e == cudaErrorMemoryAllocation ? NBVH_ENOMEM : NBVH_ECUDA;
+        }
+        nbvh_status st = refresh_fp16(x, 0);
+        if (st == NBVH_OK) {
+            e = cudaDeviceSynchronize();
+            if (e != cudaSuccess) st = cuda_fail(x, e, "nbvh_create");
+        }
+        if (st != NBVH_OK) {
+            nbvh_destroy(x);
+            return st;
+        }
+    }
+    *out = x;
+    return NBVH_OK;
+}
+
+static void free_workspace(nbvh_ctx* c) {
+    dfree(c->d_lst_leaf);
+    dfree(c->d_lst_te);
+    dfree(c->d_lst_tx);
+    dfree(c->d_state);
+    dfree(c->d_act[0]);
+    dfree(c->d_act[1]);
+    dfree(c->d_stage_rays);
+    dfree(c->d_stage_hits);
+    c->reserved = 0;
+}
+
+extern "C" void nbvh_destroy(nbvh_ctx* c) {
+    if (!c) return;
+    if (c->device >= 0) {
+        cudaSetDevice(c->device);
+        free_workspace(c);
+        for (int l = 0; l < kMaxLod; ++l) {
+            dfree(c->dcut[l].inner);
+            dfree(c->dcut[l].leaf_box);
+            dfree(c->dcut[l].leaf_base);
+            dfree(c->dcut[l].rank);
+        }
+        dfree(c->d_params);
+        dfree(c->d_table16);
+        dfree(c->d_W16);
+        dfree(c->d_misc);
+        dfree(c->d_cnt);
+        if (c->h_cnt) cudaFreeHost(c->h_cnt);
+        for (cudaEvent_t x : c->events) cudaEventDestroy(x);
+        free_scene_device(c);
+        free_train_device(c);
+    }
+    delete c;
+}
+
+extern "C" const char* nbvh_last_error(const nbvh_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+extern "C" nbvh_status nbvh_level_table(const nbvh_ctx* c, int32_t* res, int32_t* dense, int64_t* offset,
+                                        int64_t* n_entries) {
+    if (!c) return NBVH_EINVAL;
+    for (int l = 0; l < c->cfg.L; ++l) {
+        if (res) res[l] = c->res[l];
+        if (dense) dense[l] = c->dense[l];
+        if (offset) offset[l] = c->offset[l];
+    }
+    if (n_entries) *n_entries = c->n_entries;
+    return NBVH_OK;
+}
+
+static bool block_range(const nbvh_ctx* c, int32_t block, int64_t* off, int64_t* n) {
+    switch (block) {
+        case NBVH_PARAM_TABLES: *off = 0; *n = c->n_table; return true;
+        case NBVH_PARAM_WEIGHTS: *off = c->n_table; *n = c->n_W; return true;
+        case NBVH_PARAM_BIASES: *off = c->n_table + c->n_W; *n = c->n_b; return true;
+        case NBVH_PARAM_ALL: *off = 0; *n = c->n_table + c->n_W + c->n_b; return true;
+    }
+    return false;
+}
+
+extern "C" nbvh_status nbvh_param_count(const nbvh_ctx* c, int32_t block, int64_t* n) {
+    int64_t off;
+    if (!c || !n || !block_range(c, block, &off, n)) return NBVH_EINVAL;
+    return NBVH_OK;
+}
+
+extern "C" nbvh_status nbvh_get_params(nbvh_ctx* c, int32_t block, float* dst, int64_t n) {
+    int64_t off, cnt;
+    if (!c || !dst || !block_range(c, block, &off, &cnt) || n != cnt) return fail(c, NBVH_EINVAL, "get_params: bad block/size");
+    if (c->device < 0) {
+        std::memcpy(dst, c->h_params.data() + off, cnt * 4);
+        return NBVH_OK;
+    }
+    nbvh_status st = check_device(c);
+    if (st) return st;
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaMemcpy(dst, c->d_params + off, cnt * 4, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(c, e, "get_params");
+    return NBVH_OK;
+}
+
+extern "C" nbvh_status nbvh_set_params(nbvh_ctx* c, int32_t block, const float* src, int64_t n) {
+    int64_t off, cnt;
+    if (!c || !src || !block_range(c, block, &off, &cnt) || n != cnt) return fail(c, NBVH_EINVAL, "set_params: bad block/size");
+    std::memcpy(c->h_params.data() + off, src, cnt * 4);
+    if (c->device < 0) return NBVH_OK;
+    nbvh_status st = check_device(c);
+    if (st) return st;
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaMemcpy(c->d_params + off, src, cnt * 4, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_fail(c, e, "set_params");
+    st = refresh_fp16(c, 0);
+    if (st) return st;
+    e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cuda_fail(c, e, "set_params");
+    // Adam state restarts for externally set parameters
+    reset_adam(c);
+    return NBVH_OK;
+}
+
+extern "C" nbvh_status nbvh_reserve(nbvh_ctx* c, int64_t max_rays) {
+    nbvh_status st = check_device(c);
+    if (st) return st;
+    if (max_rays < 1 || max_rays > (int64_t)1 << 30) return fail(c, NBVH_EINVAL, "reserve: max_rays out of range");
+    if (max_rays <= c->reserved) return NBVH_OK;
+    cudaDeviceSynchronize();
+    free_workspace(c);
+    const size_t n = (size_t)max_rays;
+    cudaError_t e = dalloc(&c->d_lst_leaf, kListK * n);
+    if (e == cudaSuccess) e = dalloc(&c->d_lst_te, kListK * n);
+    if (e == cudaSuccess) e = dalloc(&c->d_lst_tx, kListK * n);
+    if (e == cudaSuccess) e = dalloc(&c->d_state, 8 * n);
+    if (e == cudaSuccess) e = dalloc(&c->d_act[0], n);
+    if (e == cudaSuccess) e = dalloc(&c->d_act[1], n);
+    if (e == cudaSuccess) e = dalloc(&c->d_stage_rays, 8 * n);
+    if (e == cudaSuccess) e = dalloc(&c->d_stage_hits, 10 * n);
+    if (e != cudaSuccess) {
+        free_workspace(c);
+        cudaGetLastError();
+        return fail(c, NBVH_ENOMEM, std::string("reserve: ") + cudaGetErrorString(e));
+    }
+    c->reserved = max_rays;
+    return reserve_train(c, max_rays);
+}
+
+// ------------------------------------------------------------------ scene + cut
+extern "C" nbvh_status nbvh_set_mesh(nbvh_ctx* c, const float* xyz, int64_t nv, const uint32_t* tri, int64_t nt,
+                                     const float* vnormal, const float* tri_albedo) {
+    if (!c) return NBVH_EINVAL;
+    if (c->poisoned) return NBVH_ECUDA;
+    if (!xyz || !tri || nv < 3 || nt < 1 || nt > (int64_t)1 << 30) return fail(c, NBVH_EINVAL, "set_mesh: bad mesh");
+    for (int64_t i = 0; i < 3 * nt; ++i)
+        if (tri[i] >= (uint64_t)nv) return fail(c, NBVH_EINVAL, "set_mesh: vertex index out of range");
+    for (int64_t i = 0; i < 3 * nv; ++i)
+        if (!std::isfinite(xyz[i])) return fail(c, NBVH_EINVAL, "set_mesh: non-finite vertex");
+    HostScene& sc = c->sc;
+    sc = HostScene{};
+    sc.xyz.assign(xyz, xyz + 3 * nv);
+    sc.tri.assign(tri, tri + 3 * nt);
+    if (vnormal) {
+        sc.vnormal.assign(vnormal, vnormal + 3 * nv);
+    } else {
+        std::vector<double> acc(3 * nv, 0.0);
+        for (int64_t t = 0; t < nt; ++t) {
+            const float* a = xyz + 3 * tri[3 * t];
+            const float* b = xyz + 3 * tri[3 * t + 1];
+            const float* d = xyz + 3 * tri[3 * t + 2];
+            double e1[3], e2[3];
+            for (int k = 0; k < 3; ++k) { e1[k] = (double)b[k] - a[k]; e2[k] = (double)d[k] - a[k]; }
+            double n[3] = {e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2], e1[0] * e2[1] - e1[1] * e2[0]};
+            for (int v = 0; v < 3; ++v)
+                for (int k = 0; k < 3; ++k) acc[3 * tri[3 * t + v] + k] += n[k];
+        }
+        sc.vnormal.resize(3 * nv);
+        for (int64_t v = 0; v < nv; ++v) {
+            double l = std::sqrt(acc[3 * v] * acc[3 * v] + acc[3 * v + 1] * acc[3 * v + 1] + acc[3 * v + 2] * acc[3 * v + 2]);
+            for (int k = 0; k < 3; ++k) sc.vnormal[3 * v + k] = l > 0 ? (float)(acc[3 * v + k] / l) : 0.f;
+        }
+    }
+    if (tri_albedo) sc.albedo.assign(tri_albedo, tri_albedo + 3 * nt);
+    else sc.albedo.assign(3 * nt, 0.5f);
+    build_sah_bvh(sc);
+    c->has_mesh = true;
+    for (int l = 0; l < kMaxLod; ++l) c->has_cut[l] = false;
+    if (c->device >= 0) return upload_scene(c);
+    return NBVH_OK;
+}
+
+extern "C" nbvh_status nbvh_build_cut(nbvh_ctx* c, int32_t target, const float* leaf_q, const float* leaf_p,
+                                      int32_t lod, int32_t* out_n) {
+    if (!c) return NBVH_EINVAL;
+    if (c->poisoned) return NBVH_ECUDA;
+    if (lod < 0 || lod >= kMaxLod) return fail(c, NBVH_ERANGE, "build_cut: lod slot out of range");
+    if (!c->has_mesh) return fail(c, NBVH_ESTATE, "build_cut: no mesh");
+    if (target < 1) return fail(c, NBVH_EINVAL, "build_cut: target < 1");
+    if ((leaf_q == nullptr) != (leaf_p == nullptr)) return fail(c, NBVH_EINVAL, "build_cut: give both q and p or neither");
+    if (leaf_q && !c->has_cut[lod]) return fail(c, NBVH_ESTATE, "build_cut: q/p expansion needs an existing cut");
+    HostCut nc;
+    int clamped = build_cut(c->sc, target, leaf_q ? &c->cuts[lod] : nullptr, leaf_q, leaf_p, c->cfg.inflate_rel,
+                            c->cfg.inflate_abs, nc);
+    c->cuts[lod] = std::move(nc);
+    c->has_cut[lod] = true;
+    if (out_n) *out_n = c->cuts[lod].n_leaves;
+    if (c->device >= 0) {
+        nbvh_status st = upload_cut(c, lod);
+        if (st) return st;
+    }
+    return clamped ? NBVH_WARN_CLAMPED : NBVH_OK;
+}
+
+extern "C" nbvh_status nbvh_cut_info(const nbvh_ctx* c, int32_t lod, int32_t* n_leaves, int32_t* n_inner) {
+    if (!c) return NBVH_EINVAL;
+    if (lod < 0 || lod >= kMaxLod) return NBVH_ERANGE;
+    if (!c->has_cut[lod]) return NBVH_ESTATE;
+    if (n_leaves) *n_leaves = c->cuts[lod].n_leaves;
+    if (n_inner) *n_inner = (int32_t)c->cuts[lod].inner.size();
+    return NBVH_OK;
+}
+
+extern "C" nbvh_status nbvh_get_cut(const nbvh_ctx* c, int32_t lod, float* leaf_lo, float* leaf_hi, float* base_lo,
+                                    float* base_hi, int64_t* tri_off, int32_t* tris, float* dom_min, float* dom_inv) {
+    if (!c) return NBVH_EINVAL;
+    if (lod < 0 || lod >= kMaxLod) return NBVH_ERANGE;
+    if (!c->has_cut[lod]) return NBVH_ESTATE;
+    const HostCut& hc = c->cuts[lod];
+    const int32_t n = hc.n_leaves;
+    if (leaf_lo) std::memcpy(leaf_lo, hc.leaf_lo.data(), 12 * (size_t)n);
+    if (leaf_hi) std::memcpy(leaf_hi, hc.leaf_hi.data(), 12 * (size_t)n);
+    int64_t acc = 0;
+    for (int32_t i = 0; i < n; ++i) {
+        const int32_t node = hc.leaf_base[i];
+        const BvhNode& bn = c->sc.nodes[node];
+        for (int k = 0; k < 3; ++k) {
+            if (base_lo) base_lo[3 * i + k] = bn.lo[k];
+            if (base_hi) base_hi[3 * i + k] = bn.hi[k];
+        }
+        // triangles of the subtree = contiguous prim range [first, last)
+        int32_t lo = node, hi = node;
+        while (c->sc.nodes[lo].b >= 0) lo = c->sc.nodes[lo].a;
+        while (c->sc.nodes[hi].b >= 0) hi = c->sc.nodes[hi].b;
+        const int32_t first = c->sc.nodes[lo].a, last = c->sc.nodes[hi].a - c->sc.nodes[hi].b;
+        if (tri_off) tri_off[i] = acc;
+        if (tris)
+            for (int32_t j = first; j < last; ++j) tris[acc + (j - first)] = c->sc.prim[j];
+        acc += last - first;
+    }
+    if (tri_off) tri_off[n] = acc;
+    if (dom_min)
+        for (int k = 0; k < 3; ++k) dom_min[k] = hc.dom_min[k];
+    if (dom_inv) *dom_inv = hc.dom_inv;
+    return NBVH_OK;
+}
+
+// ------------------------------------------------------------------ query
+namespace nbvh {
+
+static WaveArgs wave_args(nbvh_ctx* c, const nbvh_ray* rays, int64_t n, int lod, const HitsDev& out) {
+    WaveArgs a{};
+    a.g = make_grid(c, lod);
+    a.m = make_mlp(c);
+    a.cut = make_cut(c, lod);
+    a.rays = reinterpret_cast<const float4*>(rays);
+    a.n_rays = n;
+    a.cap = c->cfg.list_cap;
+    a.mode = c->cfg.mode;
+    a.lst_leaf = c->d_lst_leaf;
+    a.lst_te = c->d_lst_te;
+    a.lst_tx = c->d_lst_tx;
+    a.st = c->state(n);
+    a.out = out;
+    a.n_refills = c->d_misc + 1;
+    a.err = c->d_misc;
+    return a;
+}
+
+nbvh_status run_query(nbvh_ctx* c, const nbvh_ray* rays, int64_t n, int32_t lod, const HitsDev& out, float* z_trace,
+                      int32_t trace_cap, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(c->d_cnt, 0, kMaxWaves * sizeof(int32_t), s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(c->d_misc, 0, 2 * sizeof(int32_t), s);
+    if (e != cudaSuccess) return cuda_fail(c, e, "query: memset");
+    TraverseArgs ta{};
+    ta.cut = make_cut(c, lod);
+    ta.rays = reinterpret_cast<const float4*>(rays);
+    ta.n_rays = n;
+    ta.cap = c->cfg.list_cap;
+    ta.lst_leaf = c->d_lst_leaf;
+    ta.lst_te = c->d_lst_te;
+    ta.lst_tx = c->d_lst_tx;
+    ta.st = c->state(n);
+    ta.out = out;
+    ta.act_out = c->d_act[0];
+    ta.cnt_out = c->d_cnt;
+    ta.err = c->d_misc;
+    auto ev = [&](int i) -> cudaEvent_t {
+        while ((int)c->events.size() <= i) {
+            cudaEvent_t x;
+            cudaEventCreate(&x);
+            c->events.push_back(x);
+        }
+        return c->events[i];
+    };
+    if (c->profiling) cudaEventRecord(ev(0), s);
+    e = launch_traverse(ta, s);
+    if (e != cudaSuccess) return cuda_fail(c, e, "query: traverse");
+    if (c->profiling) cudaEventRecord(ev(1), s);
+    int launches = 1;
+    WaveArgs wa = wave_args(c, rays, n, lod, out);
+    wa.z_trace = z_trace;
+    wa.trace_cap = trace_cap;
+    int w = 0;
+    const int chunk = 4;
+    int64_t total_q = 0;
+    int waves_done = 0;
+    while (true) {
+        for (int j = 0; j < chunk; ++j, ++w) {
+            if (w + 1 >= kMaxWaves) return fail(c, NBVH_ECUDA, "query: wave limit exceeded");
+            wa.act_in = c->d_act[w & 1];
+            wa.act_out = c->d_act[(w + 1) & 1];
+            wa.cnt_in = c->d_cnt + w;
+            wa.cnt_out = c->d_cnt + w + 1;
+            if (c->profiling) cudaEventRecord(ev(2 + 2 * w), s);
+            e = launch_query_wave(wa, s);
+            if (e != cudaSuccess) return cuda_fail(c, e, "query: wave");
+            if (c->profiling) cudaEventRecord(ev(3 + 2 * w), s);
+            ++launches;
+        }
+        e = cudaMemcpyAsync(c->h_cnt, c->d_cnt, (w + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) return cuda_fail(c, e, "query: wave count");
+        if (c->h_cnt[w] == 0) break;
+    }
+    for (int i = 0; i < w; ++i) {
+        total_q += c->h_cnt[i];
+        if (c->h_cnt[i] > 0) waves_done = i + 1;
+    }
+    int32_t misc[2];
+    e = cudaMemcpyAsync(misc, c->d_misc, sizeof(misc), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(c, e, "query: counters");
+    if (misc[0]) return fail(c, NBVH_ECUDA, "query: traversal stack overflow (BVH deeper than 64)");
+    c->qstats.n_rays = n;
+    c->qstats.n_queries = total_q;
+    c->qstats.n_waves = waves_done;
+    c->qstats.n_launches = launches;
+    c->qstats.n_refills = misc[1];
+    c->qstats.ms_traverse = 0.f;
+    c->qstats.ms_waves = 0.f;
+    if (c->profiling) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, c->events[0], c->events[1]);
+        c->qstats.ms_traverse = ms;
+        for (int i = 0; i < w; ++i) {
+            cudaEventElapsedTime(&ms, c->events[2 + 2 * i], c->events[3 + 2 * i]);
+            c->qstats.ms_waves += ms;
+        }
+    }
+    return NBVH_OK;
+}
+
+nbvh_status check_query(nbvh_ctx* c, const void* rays, int64_t n, int32_t lod, const nbvh_hits& out) {
+    nbvh_status st = check_device(c);
+    if (st) return st;
+    if (lod < 0 || lod >= kMaxLod) return fail(c, NBVH_ERANGE, "query: lod out of range");
+    if (!c->has_cut[lod]) return fail(c, NBVH_ESTATE, "query: no cut in this LoD slot");
+    if (n < 0 || (n > 0 && (!rays || !out.hit || !out.t || !out.normal || !out.albedo)))
+        return fail(c, NBVH_EINVAL, "query: null pointer or negative n");
+    if (n > c->reserved) return fail(c, NBVH_ESTATE, "query: n exceeds nbvh_reserve");
+    return NBVH_OK;
+}
+
+}  // namespace nbvh
+
+static HitsDev to_dev(const nbvh_hits& h) {
+    return HitsDev{h.hit, h.t, h.normal, h.albedo, h.leaf, h.n_queries};
+}
+
+extern "C" nbvh_status nbvh_query(nbvh_ctx* c, const nbvh_ray* rays, int64_t n, int32_t lod, nbvh_hits out,
+                                  void* stream) {
+    nbvh_status st = check_query(c, rays, n, lod, out);
+    if (st) return st;
+    if (n == 0) return NBVH_OK;
+    return run_query(c, rays, n, lod, to_dev(out), nullptr, 0, (cudaStream_t)stream);
+}
+
+extern "C" nbvh_status nbvh_query_host(nbvh_ctx* c, const nbvh_ray* h_rays, int64_t n, int32_t lod, nbvh_hits h_out,
+                                       void* stream) {
+    nbvh_status st = check_query(c, h_rays, n, lod, h_out);
+    if (st) return st;
+    if (n == 0) return NBVH_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    float* d_rays = c->d_stage_rays;
+    // staging layout: t[n], normal[3n], albedo[3n], hit bytes, leaf[n], nq[n]
+    float* base = c->d_stage_hits;
+    HitsDev d{};
+    d.t = base;
+    d.normal = base + n;
+    d.albedo = base + 4 * n;
+    d.leaf = reinterpret_cast<int32_t*>(base + 7 * n);
+    d.n_queries = reinterpret_cast<int32_t*>(base + 8 * n);
+    d.hit = reinterpret_cast<uint8_t*>(base + 9 * n);
+    cudaError_t e = cudaMemcpyAsync(d_rays, h_rays, (size_t)n * sizeof(nbvh_ray), cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return cuda_fail(c, e, "query_host: H2D");
+    st = run_query(c, reinterpret_cast<const nbvh_ray*>(d_rays), n, lod, d, nullptr, 0, s);
+    if (st) return st;
+    e = cudaMemcpyAsync(h_out.hit, d.hit, (size_t)n, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h_out.t, d.t, (size_t)n * 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h_out.normal, d.normal, (size_t)n * 12, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h_out.albedo, d.albedo, (size_t)n * 12, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && h_out.leaf) e = cudaMemcpyAsync(h_out.leaf, d.leaf, (size_t)n * 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && h_out.n_queries)
+        e = cudaMemcpyAsync(h_out.n_queries, d.n_queries, (size_t)n * 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(c, e, "query_host: D2H");
+    return NBVH_OK;
+}
+
+extern "C" nbvh_status nbvh_set_profiling(nbvh_ctx* c, int32_t on) {
+    if (!c) return NBVH_EINVAL;
+    c->profiling = on != 0;
+    return NBVH_OK;
+}
+
+extern "C" nbvh_status nbvh_get_query_stats(nbvh_ctx* c, nbvh_query_stats* out) {
+    if (!c || !out) return NBVH_EINVAL;
+    *out = c->qstats;
+    return NBVH_OK;
+}
+
+// ------------------------------------------------------------------ parity hooks
+extern "C" nbvh_status nbvh_debug_traverse(nbvh_ctx* c, const nbvh_ray* rays, int64_t n, int32_t lod, int32_t cap,
+                                           int32_t* leaf, float* te, float* tx, int32_t* count, void* stream) {
+    nbvh_status st = check_device(c);
+    if (st) return st;
+    if (lod < 0 || lod >= kMaxLod) return fail(c, NBVH_ERANGE, "debug_traverse: lod");
+    if (!c->has_cut[lod]) return fail(c, NBVH_ESTATE, "debug_traverse: no cut");
+    if (n < 0 || cap < 1 || (n > 0 && (!rays || !leaf || !te || !tx || !count)))
+        return fail(c, NBVH_EINVAL, "debug_traverse: bad args");
+    if (n == 0) return NBVH_OK;
+    DebugTraverseArgs a{};
+    a.cut = make_cut(c, lod);
+    a.rays = reinterpret_cast<const float4*>(rays);
+    a.n_rays = n;
+    a.cap = cap;
+    a.k = c->cfg.list_cap;
+    a.leaf = leaf;
+    a.te = te;
+    a.tx = tx;
+    a.count = count;
+    a.err = c->d_misc;
+    cudaError_t e = launch_debug_traverse(a, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(c, e, "debug_traverse");
+    return NBVH_OK;
+}
+
+extern "C" nbvh_status nbvh_debug_encode(nbvh_ctx* c, const float* pts, int64_t m, uint16_t* feat, uint32_t* index,
+                                         void* stream) {
+    nbvh_status st = check_device(c);
+    if (st) return st;
+    if (m < 0 || (m > 0 && (!pts || !feat))) return fail(c, NBVH_EINVAL, "debug_encode: bad args");
+    if (m == 0) return NBVH_OK;
+    DebugEncodeArgs a{};
+    a.g = make_grid(c, -1);
+    a.pts = pts;
+    a.m = m;
+    a.feat = reinterpret_cast<__half*>(feat);
+    a.index = index;
+    cudaError_t e = launch_debug_encode(a, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(c, e, "debug_encode");
+    return NBVH_OK;
+}
+
+extern "C" nbvh_status nbvh_debug_mlp(nbvh_ctx* c, const uint16_t* x, int64_t m, float* z, void* stream) {
+    nbvh_status st = check_device(c);
+    if (st) return st;
+    if (m < 0 || (m > 0 && (!x || !z))) return fail(c, NBVH_EINVAL, "debug_mlp: bad args");
+    if (m == 0) return NBVH_OK;
+    DebugMlpArgs a{};
+    a.m = make_mlp(c);
+    a.x = reinterpret_cast<const __half*>(x);
+    a.rows = m;
+    a.z = z;
+    cudaError_t e = launch_debug_mlp(a, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(c, e, "debug_mlp");
+    return NBVH_OK;
+}
+
+extern "C" nbvh_status nbvh_debug_query_trace(nbvh_ctx* c, const nbvh_ray* rays, int64_t n, int32_t lod,
+                                              nbvh_hits out, float* z_trace, int32_t cap, void* stream) {
+    nbvh_status st = check_query(c, rays, n, lod, out);
+    if (st) return st;
+    if (!z_trace || cap < 1) return fail(c, NBVH_EINVAL, "debug_query_trace: bad trace");
+    if (n == 0) return NBVH_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e = cudaMemsetAsync(z_trace, 0xff, (size_t)n * cap * 8 * sizeof(float), s);   // NaN
+    if (e != cudaSuccess) return cuda_fail(c, e, "debug_query_trace: memset");
+    return run_query(c, rays, n, lod, to_dev(out), z_trace, cap, s);
+}

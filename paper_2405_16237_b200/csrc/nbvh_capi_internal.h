@@ -1,0 +1,115 @@
+// nbvh_capi_internal.h — the context object behind the opaque nbvh_ctx handle.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/nbvh.h"
+#include "nbvh_internal.h"
+#include "nbvh_launch.h"
+
+namespace nbvh {
+constexpr int kMaxWaves = 65536;
+
+struct DeviceCut {
+    InnerNode* inner = nullptr;
+    float4* leaf_box = nullptr;   // [n][2]
+    int32_t* leaf_base = nullptr;
+    float* rank = nullptr;
+};
+
+struct DeviceScene {
+    BvhNode* nodes = nullptr;     // base BVH
+    float* tri_v = nullptr;       // [nt][9] vertices in prim order
+    float* tri_n = nullptr;       // [nt][9] vertex normals in prim order
+    float* tri_a = nullptr;       // [nt][3] albedo in prim order
+    int32_t* tri_id = nullptr;    // [nt] original triangle id
+    int64_t n_tris = 0;
+};
+
+struct TrainWork;   // nbvh_train.cu
+}  // namespace nbvh
+
+struct nbvh_ctx {
+    nbvh_config cfg{};
+    int device = -1;
+    bool poisoned = false;
+    std::string err;
+
+    // hash grid / MLP geometry
+    int32_t res[nbvh::kMaxLevels] = {0};
+    int32_t dense[nbvh::kMaxLevels] = {0};
+    int64_t offset[nbvh::kMaxLevels] = {0};
+    int64_t n_entries = 0;
+    int32_t d_in = 0;
+    int64_t n_table = 0, n_W = 0, n_b = 0;
+
+    // parameters: fp32 master (flat: tables, weights, biases) + fp16 inference copy
+    std::vector<float> h_params;
+    float* d_params = nullptr;
+    __half* d_table16 = nullptr;
+    __half* d_W16 = nullptr;
+
+    // scene and cuts
+    nbvh::HostScene sc;
+    bool has_mesh = false;
+    nbvh::HostCut cuts[nbvh::kMaxLod];
+    bool has_cut[nbvh::kMaxLod] = {false};
+    nbvh::DeviceCut dcut[nbvh::kMaxLod];
+    nbvh::DeviceScene dscene;
+
+    // query workspaces
+    int64_t reserved = 0;
+    int32_t* d_lst_leaf = nullptr;
+    float* d_lst_te = nullptr;
+    float* d_lst_tx = nullptr;
+    int32_t* d_state = nullptr;        // 8 arrays of n int32/float
+    int32_t* d_act[2] = {nullptr, nullptr};
+    int32_t* d_cnt = nullptr;          // per-wave active counts
+    int32_t* h_cnt = nullptr;          // pinned mirror
+    int32_t* d_misc = nullptr;         // [0] error flags, [1] refills, ...
+    float* d_stage_rays = nullptr;     // host-path staging
+    float* d_stage_hits = nullptr;
+    nbvh_query_stats qstats{};
+    bool profiling = false;
+    std::vector<cudaEvent_t> events;   // profiling: [0..1] traverse, then one pair per wave
+
+    // training
+    nbvh::TrainWork* train = nullptr;
+    nbvh_train_stats tstats{};
+
+    nbvh::RayState state(int64_t n) const {
+        nbvh::RayState s;
+        int32_t* p = d_state;
+        const int64_t m = reserved;
+        s.pos = p;
+        s.base = p + m;
+        s.nbuf = p + 2 * m;
+        s.count = p + 3 * m;
+        s.bt = reinterpret_cast<float*>(p + 4 * m);
+        s.bte = reinterpret_cast<float*>(p + 5 * m);
+        s.bleaf = p + 6 * m;
+        s.nq = p + 7 * m;
+        (void)n;
+        return s;
+    }
+};
+
+namespace nbvh {
+nbvh_status fail(nbvh_ctx* c, nbvh_status s, const std::string& msg);
+nbvh_status cuda_fail(nbvh_ctx* c, cudaError_t e, const char* where);
+nbvh_status check_device(nbvh_ctx* c);
+GridDev make_grid(const nbvh_ctx* c, int lod);
+MlpDev make_mlp(const nbvh_ctx* c);
+CutDev make_cut(const nbvh_ctx* c, int lod);
+nbvh_status refresh_fp16(nbvh_ctx* c, cudaStream_t s);
+// nbvh_train.cu
+nbvh_status upload_scene(nbvh_ctx* c);
+nbvh_status upload_cut(nbvh_ctx* c, int lod);
+void free_scene_device(nbvh_ctx* c);
+void free_train_device(nbvh_ctx* c);
+nbvh_status reserve_train(nbvh_ctx* c, int64_t max_rays);
+void reset_adam(nbvh_ctx* c);
+}  // namespace nbvh

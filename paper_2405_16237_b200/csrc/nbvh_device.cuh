@@ -1,0 +1,414 @@
+// nbvh_device.cuh — device building blocks of the N-BVH query/training kernels (sm_100a).
+//
+//  * slab():            ray/AABB interval, binary32 with a fixed op order (C7, C25)
+//  * collect_leaves():  shallow N-BVH traversal emitting the (t_enter, id)-ordered leaf
+//                       list, capacity K in registers, resumable from a key (C5, C6)
+//  * segment_point():   stratified sample positions, normalised to the grid domain (P:133,
+//                       P:146; C4, C8)
+//  * encode_chunk():    multires hash-grid gather + trilinear blend of 8/F levels -> 16 B
+//                       of fp16 features (C1-C3)
+//  * mlp_rows16():      D_in -> 64 (ReLU) x hidden -> 8 MLP for 16 rows on tensor cores,
+//                       activations kept in registers between layers
+//  * decode helpers:    hit = z_vis < 0, local distance, normal, albedo
+//
+// Bit-exactness: every operation that decides a discrete result the oracle must match
+// (intervals, sample positions, grid cells) uses explicit round-to-nearest intrinsics
+// so nvcc cannot contract it into an FMA.  Continuous blends use FMA freely.
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cstdint>
+
+#include "nbvh_internal.h"
+
+namespace nbvh {
+
+constexpr uint32_t kPrime1 = 2654435761u;   // [Mueller22] spatial-hash primes
+constexpr uint32_t kPrime2 = 805459861u;
+
+struct GridDev {
+    int32_t L, F, n_points, log2_T;
+    int32_t res[kMaxLevels];
+    int32_t dense[kMaxLevels];
+    uint32_t offset[kMaxLevels];     // entry offset of each level
+    const __half* table;             // fp16 [n_entries][F]
+    float dom_min[3];
+    float dom_inv;
+};
+
+struct MlpDev {
+    int32_t d_in, hidden;
+    const __half* W;                 // layers concatenated, [out][in] row-major
+    const float* b;
+};
+
+struct CutDev {
+    const InnerNode* inner;
+    const float4* leaf_box;          // [n_leaves][2]: (lo.xyz, 0), (hi.xyz, 0)
+    int32_t n_leaves;
+};
+
+// ------------------------------------------------------------------ slab test
+// tl=(lo-o)*inv, th=(hi-o)*inv, tn=fminf(tl,th), tf=fmaxf(tl,th), te = left-fold fmaxf over
+// (tn.x, tn.y, tn.z, tmin), tx = left-fold fminf over (tf.x, tf.y, tf.z, tmax); hit iff te <= tx.
+struct RayDev {
+    float o[3], inv[3], d[3], tmin, tmax;
+};
+
+__device__ __forceinline__ RayDev load_ray(const float4* rays, int64_t r) {
+    float4 a = __ldg(rays + 2 * r), b = __ldg(rays + 2 * r + 1);
+    RayDev R;
+    R.o[0] = a.x; R.o[1] = a.y; R.o[2] = a.z; R.tmin = a.w;
+    R.d[0] = b.x; R.d[1] = b.y; R.d[2] = b.z; R.tmax = b.w;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) R.inv[k] = __fdiv_rn(1.0f, R.d[k]);
+    return R;
+}
+
+__device__ __forceinline__ bool slab(const RayDev& R, const float* lo, const float* hi, float& te, float& tx) {
+    float tn[3], tf[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        float tl = __fmul_rn(__fsub_rn(lo[k], R.o[k]), R.inv[k]);
+        float th = __fmul_rn(__fsub_rn(hi[k], R.o[k]), R.inv[k]);
+        tn[k] = fminf(tl, th);
+        tf[k] = fmaxf(tl, th);
+    }
+    te = fmaxf(fmaxf(fmaxf(tn[0], tn[1]), tn[2]), R.tmin);
+    tx = fminf(fminf(fminf(tf[0], tf[1]), tf[2]), R.tmax);
+    return te <= tx;
+}
+
+__device__ __forceinline__ bool key_less(float a_te, int a_id, float b_te, int b_id) {
+    return a_te < b_te || (a_te == b_te && a_id < b_id);
+}
+
+// ------------------------------------------------------------------ ordered leaf list
+// Collects the intersected cut leaves whose key (t_enter, id) is greater than `after`
+// (when has_after), keeping the `cap` (<= K) smallest keys sorted in registers; returns
+// how many leaves qualified in total (so the caller knows whether more remain, C6).
+// Inner boxes are exact unions of their children, so by monotone rounding a pruned
+// subtree contains no intersected leaf: the result equals a brute-force scan (C5).
+template <int K>
+__device__ int collect_leaves(const CutDev& cut, const RayDev& R, bool has_after, float after_te, int after_id,
+                              int cap, float (&lte)[K], float (&ltx)[K], int (&lid)[K], int& n_out,
+                              int* err_flag) {
+    int n = 0, total = 0;
+    auto consider = [&](int leaf, float te, float tx) {
+        if (has_after && !key_less(after_te, after_id, te, leaf)) return;
+        ++total;
+        float cte = te, ctx = tx;
+        int cid = leaf;
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+            if (j < n && key_less(cte, cid, lte[j], lid[j])) {
+                float t0 = lte[j], t1 = ltx[j];
+                int i0 = lid[j];
+                lte[j] = cte; ltx[j] = ctx; lid[j] = cid;
+                cte = t0; ctx = t1; cid = i0;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < K; ++j)
+            if (j == n && n < cap) { lte[j] = cte; ltx[j] = ctx; lid[j] = cid; }
+        if (n < cap) ++n;
+    };
+    if (cut.n_leaves == 1) {
+        float4 a = __ldg(cut.leaf_box), b = __ldg(cut.leaf_box + 1);
+        float lo[3] = {a.x, a.y, a.z}, hi[3] = {b.x, b.y, b.z}, te, tx;
+        if (slab(R, lo, hi, te, tx)) consider(0, te, tx);
+    } else {
+        int stack[64];
+        int sp = 0;
+        stack[sp++] = 0;
+        while (sp > 0) {
+            const float4* p = reinterpret_cast<const float4*>(cut.inner + stack[--sp]);
+            float4 q0 = __ldg(p), q1 = __ldg(p + 1), q2 = __ldg(p + 2), q3 = __ldg(p + 3);
+            float llo[3] = {q0.x, q0.y, q0.z}, lhi[3] = {q0.w, q1.x, q1.y};
+            float rlo[3] = {q1.z, q1.w, q2.x}, rhi[3] = {q2.y, q2.z, q2.w};
+            int cl = __float_as_int(q3.x), cr = __float_as_int(q3.y);
+            float lte_, ltx_, rte_, rtx_;
+            bool hl = slab(R, llo, lhi, lte_, ltx_);
+            bool hr = slab(R, rlo, rhi, rte_, rtx_);
+            if (hl && cl < 0) consider(-1 - cl, lte_, ltx_);
+            if (hr && cr < 0) consider(-1 - cr, rte_, rtx_);
+            bool pl = hl && cl >= 0, pr = hr && cr >= 0;
+            if (sp + 2 > 64) { atomicOr(err_flag, 1); break; }
+            // push the farther child first so the nearer is visited first
+            if (pl && pr) {
+                bool l_first = lte_ <= rte_;
+                stack[sp++] = l_first ? cr : cl;
+                stack[sp++] = l_first ? cl : cr;
+            } else if (pl) {
+                stack[sp++] = cl;
+            } else if (pr) {
+                stack[sp++] = cr;
+            }
+        }
+    }
+    n_out = n;
+    return total;
+}
+
+// ------------------------------------------------------------------ segment sampling
+// u = (2i+1)/(2n) (inference) or (i+xi)/n (training); dt = t1-t0; t = t0+u*dt;
+// p = o + t*d; x = clamp((p-dom_min)*dom_inv, 0, 1); every op rounded (no FMA).
+__device__ __forceinline__ void segment_point(const GridDev& g, const float o[3], const float d[3], float t0, float t1,
+                                              int i, int n, const float* xi, float x[3]) {
+    float u = xi ? __fdiv_rn(__fadd_rn((float)i, xi[i]), (float)n) : __fdiv_rn((float)(2 * i + 1), (float)(2 * n));
+    float dt = __fsub_rn(t1, t0);
+    float t = __fadd_rn(t0, __fmul_rn(u, dt));
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        float p = __fadd_rn(o[k], __fmul_rn(t, d[k]));
+        float v = __fmul_rn(__fsub_rn(p, g.dom_min[k]), g.dom_inv);
+        x[k] = fminf(fmaxf(v, 0.0f), 1.0f);
+    }
+}
+
+// ------------------------------------------------------------------ grid cell of a level
+struct Cell {
+    uint32_t idx[8];    // corner entry index within the level (corner bit0=x, bit1=y, bit2=z)
+    float w[8];         // trilinear weights
+};
+
+__device__ __forceinline__ void level_cell(const GridDev& g, int l, const float x[3], Cell& c) {
+    const int N = g.res[l];
+    int ci[3];
+    float f[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        float s = __fmul_rn(x[k], (float)N);
+        int v = (int)floorf(s);
+        v = min(v, N - 1);
+        v = max(v, 0);
+        ci[k] = v;
+        f[k] = __fsub_rn(s, (float)v);
+    }
+    const float wx[2] = {1.0f - f[0], f[0]}, wy[2] = {1.0f - f[1], f[1]}, wz[2] = {1.0f - f[2], f[2]};
+    if (g.dense[l]) {
+        const uint32_t n1 = (uint32_t)N + 1u;
+        const uint32_t bx = (uint32_t)ci[0], by = (uint32_t)ci[1] * n1, bz = (uint32_t)ci[2] * n1 * n1;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            c.idx[k] = bx + (k & 1) + by + ((k >> 1) & 1) * n1 + bz + ((k >> 2) & 1) * n1 * n1;
+    } else {
+        const uint32_t mask = (1u << g.log2_T) - 1u;
+        const uint32_t hx[2] = {(uint32_t)ci[0], (uint32_t)ci[0] + 1u};
+        const uint32_t hy[2] = {(uint32_t)ci[1] * kPrime1, ((uint32_t)ci[1] + 1u) * kPrime1};
+        const uint32_t hz[2] = {(uint32_t)ci[2] * kPrime2, ((uint32_t)ci[2] + 1u) * kPrime2};
+#pragma unroll
+        for (int k = 0; k < 8; ++k) c.idx[k] = (hx[k & 1] ^ hy[(k >> 1) & 1] ^ hz[(k >> 2) & 1]) & mask;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) c.w[k] = wx[k & 1] * wy[(k >> 1) & 1] * wz[(k >> 2) & 1];
+}
+
+// ------------------------------------------------------------------ encode 8 halves
+// One 16-byte chunk of the concatenated feature vector: NL = 8/F consecutive levels of
+// one sample point.  All 8*NL corner loads are issued before any is consumed.
+template <int F>
+__device__ __forceinline__ uint4 encode_chunk(const GridDev& g, const float x[3], int l0, uint32_t* idx_out) {
+    constexpr int NL = 8 / F;
+    Cell cell[NL];
+#pragma unroll
+    for (int j = 0; j < NL; ++j) level_cell(g, l0 + j, x, cell[j]);
+    if (idx_out) {
+#pragma unroll
+        for (int j = 0; j < NL; ++j)
+#pragma unroll
+            for (int k = 0; k < 8; ++k) idx_out[j * 8 + k] = cell[j].idx[k];
+    }
+    uint4 out;
+    uint32_t* o32 = reinterpret_cast<uint32_t*>(&out);
+    if constexpr (F == 2) {
+        uint32_t v[NL][8];
+#pragma unroll
+        for (int j = 0; j < NL; ++j) {
+            const uint32_t* base = reinterpret_cast<const uint32_t*>(g.table) + g.offset[l0 + j];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v[j][k] = __ldg(base + cell[j].idx[k]);
+        }
+#pragma unroll
+        for (int j = 0; j < NL; ++j) {
+            float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                float2 f = __half22float2(*reinterpret_cast<const __half2*>(&v[j][k]));
+                a0 = fmaf(cell[j].w[k], f.x, a0);
+                a1 = fmaf(cell[j].w[k], f.y, a1);
+            }
+            __half2 h = __floats2half2_rn(a0, a1);
+            o32[j] = *reinterpret_cast<uint32_t*>(&h);
+        }
+    } else {  // F == 4
+        uint2 v[NL][8];
+#pragma unroll
+        for (int j = 0; j < NL; ++j) {
+            const uint2* base = reinterpret_cast<const uint2*>(g.table) + g.offset[l0 + j];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v[j][k] = __ldg(base + cell[j].idx[k]);
+        }
+#pragma unroll
+        for (int j = 0; j < NL; ++j) {
+            float a[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                float2 f0 = __half22float2(*reinterpret_cast<const __half2*>(&v[j][k].x));
+                float2 f1 = __half22float2(*reinterpret_cast<const __half2*>(&v[j][k].y));
+                a[0] = fmaf(cell[j].w[k], f0.x, a[0]);
+                a[1] = fmaf(cell[j].w[k], f0.y, a[1]);
+                a[2] = fmaf(cell[j].w[k], f1.x, a[2]);
+                a[3] = fmaf(cell[j].w[k], f1.y, a[3]);
+            }
+            __half2 h0 = __floats2half2_rn(a[0], a[1]), h1 = __floats2half2_rn(a[2], a[3]);
+            o32[2 * j] = *reinterpret_cast<uint32_t*>(&h0);
+            o32[2 * j + 1] = *reinterpret_cast<uint32_t*>(&h1);
+        }
+    }
+    return out;
+}
+
+// ------------------------------------------------------------------ tensor-core MLP
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x2(uint32_t addr, uint32_t& r0, uint32_t& r1) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];\n" : "=r"(r0), "=r"(r1) : "r"(addr));
+}
+__device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};\n"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_relu_half2(float a, float b) {
+    __half2 h = __floats2half2_rn(fmaxf(a, 0.f), fmaxf(b, 0.f));
+    return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// Shared-memory layout of the staged MLP (row strides padded by 8 halves so that the
+// 8-row ldmatrix phases hit 8 distinct 16-byte bank groups).
+struct MlpSmem {
+    __half* w0;      // [64][d_in + 8]
+    __half* wh;      // [hidden-1][64][72]
+    __half* wo;      // [8][72]
+    float* b;        // [64*hidden + 8]
+};
+
+__host__ __device__ constexpr int mlp_smem_halves(int d_in, int hidden) {
+    return 64 * (d_in + 8) + (hidden - 1) * 64 * 72 + 8 * 72;
+}
+
+// Stage weights and biases from global memory (16-byte copies by all threads).
+__device__ __forceinline__ void stage_mlp(const MlpDev& m, const MlpSmem& s, int tid, int nthreads) {
+    const int D = m.d_in, cpr0 = D / 8;
+    const uint4* W = reinterpret_cast<const uint4*>(m.W);
+    for (int i = tid; i < 64 * cpr0; i += nthreads) {
+        int row = i / cpr0, c = i % cpr0;
+        *reinterpret_cast<uint4*>(s.w0 + row * (D + 8) + c * 8) = __ldg(W + i);
+    }
+    const uint4* Wh = W + 64 * cpr0;
+    for (int i = tid; i < (m.hidden - 1) * 64 * 8; i += nthreads) {
+        int row = i / 8, c = i % 8;
+        *reinterpret_cast<uint4*>(s.wh + row * 72 + c * 8) = __ldg(Wh + i);
+    }
+    const uint4* Wo = Wh + (m.hidden - 1) * 64 * 8;
+    for (int i = tid; i < 8 * 8; i += nthreads) {
+        int row = i / 8, c = i % 8;
+        *reinterpret_cast<uint4*>(s.wo + row * 72 + c * 8) = __ldg(Wo + i);
+    }
+    for (int i = tid; i < 64 * m.hidden + 8; i += nthreads) s.b[i] = __ldg(m.b + i);
+}
+
+// MLP of the 16 rows [r0, r0+16) of a feature tile x (row stride d_in+8 halves) on
+// mma.sync m16n8k16 (fp16 in, fp32 accumulate).  Layer outputs stay in registers: the
+// m16n8 accumulator layout of two adjacent n-tiles is exactly the m16k16 A-operand
+// layout of the next layer.  Writes the 8 raw outputs of each row to z[row*8 + c].
+template <int D>
+__device__ __forceinline__ void mlp_rows16(const MlpSmem& s, int hidden, const __half* x, int r0, float* z, int lane) {
+    const int g = lane >> 2, t = lane & 3;
+    float acc[8][4];
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+        float b0 = s.b[nt * 8 + 2 * t], b1 = s.b[nt * 8 + 2 * t + 1];
+        acc[nt][0] = b0; acc[nt][1] = b1; acc[nt][2] = b0; acc[nt][3] = b1;
+    }
+    const uint32_t xa = (uint32_t)__cvta_generic_to_shared(x + (r0 + (lane & 15)) * (D + 8) + (lane >> 4) * 8);
+    const uint32_t wa = (uint32_t)__cvta_generic_to_shared(s.w0 + ((lane & 7) + ((lane >> 4) << 3)) * (D + 8) +
+                                                           ((lane >> 3) & 1) * 8);
+#pragma unroll
+    for (int kb = 0; kb < D / 16; ++kb) {
+        uint32_t a[4];
+        ldsm_x4(xa + kb * 32, a[0], a[1], a[2], a[3]);
+#pragma unroll
+        for (int np = 0; np < 4; ++np) {
+            uint32_t b0, b1, b2, b3;
+            ldsm_x4(wa + np * 16 * (D + 8) * 2 + kb * 32, b0, b1, b2, b3);
+            mma16816(acc[2 * np], a, b0, b1);
+            mma16816(acc[2 * np + 1], a, b2, b3);
+        }
+    }
+    uint32_t h[4][4];   // next-layer A fragments, k-block kb = hidden units 16kb..16kb+15
+#pragma unroll
+    for (int kb = 0; kb < 4; ++kb) {
+        h[kb][0] = pack_relu_half2(acc[2 * kb][0], acc[2 * kb][1]);
+        h[kb][1] = pack_relu_half2(acc[2 * kb][2], acc[2 * kb][3]);
+        h[kb][2] = pack_relu_half2(acc[2 * kb + 1][0], acc[2 * kb + 1][1]);
+        h[kb][3] = pack_relu_half2(acc[2 * kb + 1][2], acc[2 * kb + 1][3]);
+    }
+    for (int layer = 1; layer < hidden; ++layer) {
+        const __half* W = s.wh + (layer - 1) * 64 * 72;
+        const float* bb = s.b + layer * 64;
+#pragma unroll
+        for (int nt = 0; nt < 8; ++nt) {
+            float b0 = bb[nt * 8 + 2 * t], b1 = bb[nt * 8 + 2 * t + 1];
+            acc[nt][0] = b0; acc[nt][1] = b1; acc[nt][2] = b0; acc[nt][3] = b1;
+        }
+        const uint32_t wb = (uint32_t)__cvta_generic_to_shared(W + ((lane & 7) + ((lane >> 4) << 3)) * 72 +
+                                                               ((lane >> 3) & 1) * 8);
+#pragma unroll
+        for (int kb = 0; kb < 4; ++kb) {
+#pragma unroll
+            for (int np = 0; np < 4; ++np) {
+                uint32_t b0, b1, b2, b3;
+                ldsm_x4(wb + np * 16 * 72 * 2 + kb * 32, b0, b1, b2, b3);
+                mma16816(acc[2 * np], h[kb], b0, b1);
+                mma16816(acc[2 * np + 1], h[kb], b2, b3);
+            }
+        }
+#pragma unroll
+        for (int kb = 0; kb < 4; ++kb) {
+            h[kb][0] = pack_relu_half2(acc[2 * kb][0], acc[2 * kb][1]);
+            h[kb][1] = pack_relu_half2(acc[2 * kb][2], acc[2 * kb][3]);
+            h[kb][2] = pack_relu_half2(acc[2 * kb + 1][0], acc[2 * kb + 1][1]);
+            h[kb][3] = pack_relu_half2(acc[2 * kb + 1][2], acc[2 * kb + 1][3]);
+        }
+    }
+    // output layer: 64 -> 8, linear
+    float o[4];
+    {
+        const float* bb = s.b + hidden * 64;
+        o[0] = bb[2 * t]; o[1] = bb[2 * t + 1]; o[2] = o[0]; o[3] = o[1];
+    }
+    const uint32_t wo = (uint32_t)__cvta_generic_to_shared(s.wo + (lane & 7) * 72 + ((lane >> 3) & 1) * 8);
+#pragma unroll
+    for (int kb = 0; kb < 4; ++kb) {
+        uint32_t b0, b1;
+        ldsm_x2(wo + kb * 32, b0, b1);
+        mma16816(o, h[kb], b0, b1);
+    }
+    z[(r0 + g) * 8 + 2 * t] = o[0];
+    z[(r0 + g) * 8 + 2 * t + 1] = o[1];
+    z[(r0 + g + 8) * 8 + 2 * t] = o[2];
+    z[(r0 + g + 8) * 8 + 2 * t + 1] = o[3];
+}
+
+// ------------------------------------------------------------------ decode
+// sigmoid evaluated in double and rounded once to fp32, so that host replays agree bit
+// for bit (DESIGN.md §5 "decode").
+__device__ __forceinline__ float sigmoid_f(float z) { return (float)(1.0 / (1.0 + exp(-(double)z))); }
+
+}  // namespace nbvh

@@ -1,0 +1,343 @@
+"""Thin ctypes binding of libnbvh.so (include/nbvh.h).  Argument marshalling only:
+every step of the query and training path runs in the library's CUDA kernels.
+
+Device buffers are torch tensors (PyTorch supplies device memory, streams and process
+groups); host buffers are numpy arrays.  There is no fallback: if libnbvh.so is missing
+or a call fails, an exception is raised.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libnbvh.so")
+
+STATUS = {0: "OK", 1: "WARN_CLAMPED", -1: "EINVAL", -2: "ERANGE", -3: "ESTATE", -4: "ENONFINITE", -5: "ECUDA",
+          -6: "ENOMEM"}
+PARAM_TABLES, PARAM_WEIGHTS, PARAM_BIASES, PARAM_ALL = 0, 1, 2, 3
+
+
+class NbvhError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"nbvh {STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Config(C.Structure):
+    _fields_ = [("L", C.c_int32), ("F", C.c_int32), ("log2_T", C.c_int32), ("base_res", C.c_int32),
+                ("max_res", C.c_int32), ("n_points", C.c_int32), ("hidden_layers", C.c_int32),
+                ("width", C.c_int32), ("list_cap", C.c_int32), ("mode", C.c_int32), ("inflate_rel", C.c_float),
+                ("inflate_abs", C.c_float), ("seed", C.c_uint64)]
+
+
+class Hits(C.Structure):
+    _fields_ = [("hit", C.c_void_p), ("t", C.c_void_p), ("normal", C.c_void_p), ("albedo", C.c_void_p),
+                ("leaf", C.c_void_p), ("n_queries", C.c_void_p)]
+
+
+class QueryStats(C.Structure):
+    _fields_ = [("n_rays", C.c_int64), ("n_queries", C.c_int64), ("n_waves", C.c_int32),
+                ("n_launches", C.c_int32), ("n_refills", C.c_int32), ("ms_traverse", C.c_float),
+                ("ms_waves", C.c_float)]
+
+
+class TrainStats(C.Structure):
+    _fields_ = [("n_rays", C.c_int64), ("n_first_hit", C.c_int64), ("n_accepted", C.c_int64),
+                ("loss_sum", C.c_double), ("loss_terms", C.c_double * 4), ("n_launches", C.c_int32),
+                ("skipped", C.c_int32)]
+
+
+_lib = None
+
+# (name, argtypes) — every entry point declared in include/nbvh.h
+_P, _I32, _I64, _F = C.c_void_p, C.c_int32, C.c_int64, C.c_float
+SIGNATURES = {
+    "nbvh_config_default": (None, [_P]),
+    "nbvh_create": (C.c_int, [_P, C.c_int, _P]),
+    "nbvh_destroy": (None, [_P]),
+    "nbvh_last_error": (C.c_char_p, [_P]),
+    "nbvh_level_table": (C.c_int, [_P, _P, _P, _P, _P]),
+    "nbvh_param_count": (C.c_int, [_P, _I32, _P]),
+    "nbvh_get_params": (C.c_int, [_P, _I32, _P, _I64]),
+    "nbvh_set_params": (C.c_int, [_P, _I32, _P, _I64]),
+    "nbvh_reserve": (C.c_int, [_P, _I64]),
+    "nbvh_set_mesh": (C.c_int, [_P, _P, _I64, _P, _I64, _P, _P]),
+    "nbvh_build_cut": (C.c_int, [_P, _I32, _P, _P, _I32, _P]),
+    "nbvh_cut_info": (C.c_int, [_P, _I32, _P, _P]),
+    "nbvh_get_cut": (C.c_int, [_P, _I32, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "nbvh_query": (C.c_int, [_P, _P, _I64, _I32, Hits, _P]),
+    "nbvh_query_host": (C.c_int, [_P, _P, _I64, _I32, Hits, _P]),
+    "nbvh_get_query_stats": (C.c_int, [_P, _P]),
+    "nbvh_set_profiling": (C.c_int, [_P, _I32]),
+    "nbvh_train_backward": (C.c_int, [_P, _P, _I64, _P, _P, _I32, _P]),
+    "nbvh_grad_buffer": (C.c_int, [_P, _P, _P]),
+    "nbvh_apply_update": (C.c_int, [_P, _F, _P]),
+    "nbvh_train_step": (C.c_int, [_P, _P, _I64, _P, _P, _I32, _F, _P]),
+    "nbvh_get_train_stats": (C.c_int, [_P, _P]),
+    "nbvh_set_leaf_rank": (C.c_int, [_P, _I32, _P]),
+    "nbvh_debug_traverse": (C.c_int, [_P, _P, _I64, _I32, _I32, _P, _P, _P, _P, _P]),
+    "nbvh_debug_encode": (C.c_int, [_P, _P, _I64, _P, _P, _P]),
+    "nbvh_debug_mlp": (C.c_int, [_P, _P, _I64, _P, _P]),
+    "nbvh_debug_query_trace": (C.c_int, [_P, _P, _I64, _I32, Hits, _P, _I32, _P]),
+    "nbvh_debug_train_samples": (C.c_int, [_P, _P, _P, _P, _P, _P]),
+}
+
+
+def load_library(path: str = LIB_PATH):
+    global _lib
+    if _lib is None:
+        if not os.path.exists(path):
+            raise RuntimeError(f"{path} is not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        lib = C.CDLL(path)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def _ptr(x):
+    """Device pointer of a torch tensor / host pointer of a numpy array / None."""
+    if x is None:
+        return None
+    if isinstance(x, np.ndarray):
+        assert x.flags.c_contiguous
+        return x.ctypes.data
+    assert x.is_contiguous()
+    return x.data_ptr()
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream if torch.cuda.is_available() else None
+    return getattr(stream, "cuda_stream", stream)
+
+
+def default_config(**kw) -> Config:
+    cfg = Config()
+    load_library().nbvh_config_default(C.byref(cfg))
+    for k, v in kw.items():
+        setattr(cfg, k, v)
+    return cfg
+
+
+class Context:
+    """One nbvh_ctx (one device per process).  device=-1 gives a host-only context."""
+
+    def __init__(self, device: int = 0, **cfg):
+        self.lib = load_library()
+        self.cfg = default_config(**cfg)
+        h = C.c_void_p()
+        st = self.lib.nbvh_create(C.byref(self.cfg), device, C.byref(h))
+        if st != 0:
+            raise NbvhError(st, "nbvh_create failed")
+        self.h = h
+        self.device = device
+        self.d_in = self.cfg.n_points * self.cfg.L * self.cfg.F
+
+    def close(self):
+        if self.h:
+            self.lib.nbvh_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _ck(self, st, what):
+        if st < 0:
+            raise NbvhError(st, f"{what}: {self.lib.nbvh_last_error(self.h).decode()}")
+        return st
+
+    # ---------------------------------------------------------------- model
+    def level_table(self):
+        L = self.cfg.L
+        res = np.zeros(L, np.int32)
+        dense = np.zeros(L, np.int32)
+        off = np.zeros(L, np.int64)
+        n = np.zeros(1, np.int64)
+        self._ck(self.lib.nbvh_level_table(self.h, _ptr(res), _ptr(dense), _ptr(off), _ptr(n)), "level_table")
+        return res, dense, off, int(n[0])
+
+    def param_count(self, block):
+        n = np.zeros(1, np.int64)
+        self._ck(self.lib.nbvh_param_count(self.h, block, _ptr(n)), "param_count")
+        return int(n[0])
+
+    def get_params(self, block=PARAM_ALL):
+        a = np.zeros(self.param_count(block), np.float32)
+        self._ck(self.lib.nbvh_get_params(self.h, block, _ptr(a), a.size), "get_params")
+        return a
+
+    def set_params(self, block, values):
+        a = np.ascontiguousarray(values, dtype=np.float32).reshape(-1)
+        self._ck(self.lib.nbvh_set_params(self.h, block, _ptr(a), a.size), "set_params")
+
+    def set_mlp(self, layers):
+        """layers: [(W [out][in], b [out])] in forward order."""
+        self.set_params(PARAM_WEIGHTS, np.concatenate([np.asarray(W, np.float32).ravel() for W, _ in layers]))
+        self.set_params(PARAM_BIASES, np.concatenate([np.asarray(b, np.float32).ravel() for _, b in layers]))
+
+    def reserve(self, n):
+        self._ck(self.lib.nbvh_reserve(self.h, int(n)), "reserve")
+
+    # ---------------------------------------------------------------- scene
+    def set_mesh(self, scene):
+        v = np.ascontiguousarray(scene.verts, np.float32)
+        t = np.ascontiguousarray(scene.tris, np.uint32)
+        n = np.ascontiguousarray(scene.vnormals, np.float32) if scene.vnormals is not None else None
+        a = np.ascontiguousarray(scene.albedo, np.float32) if scene.albedo is not None else None
+        self._ck(self.lib.nbvh_set_mesh(self.h, _ptr(v), v.shape[0], _ptr(t), t.shape[0], _ptr(n), _ptr(a)),
+                 "set_mesh")
+
+    def build_cut(self, target, lod=0, q=None, p=None):
+        out = np.zeros(1, np.int32)
+        qa = None if q is None else np.ascontiguousarray(q, np.float32)
+        pa = None if p is None else np.ascontiguousarray(p, np.float32)
+        st = self._ck(self.lib.nbvh_build_cut(self.h, int(target), _ptr(qa), _ptr(pa), lod, _ptr(out)), "build_cut")
+        return int(out[0]), st
+
+    def cut(self, lod=0):
+        nl = np.zeros(1, np.int32)
+        ni = np.zeros(1, np.int32)
+        self._ck(self.lib.nbvh_cut_info(self.h, lod, _ptr(nl), _ptr(ni)), "cut_info")
+        n = int(nl[0])
+        d = dict(leaf_lo=np.zeros((n, 3), np.float32), leaf_hi=np.zeros((n, 3), np.float32),
+                 base_lo=np.zeros((n, 3), np.float32), base_hi=np.zeros((n, 3), np.float32),
+                 tri_off=np.zeros(n + 1, np.int64), dom_min=np.zeros(3, np.float32), dom_inv=np.zeros(1, np.float32))
+        self._ck(self.lib.nbvh_get_cut(self.h, lod, _ptr(d["leaf_lo"]), _ptr(d["leaf_hi"]), _ptr(d["base_lo"]),
+                                       _ptr(d["base_hi"]), _ptr(d["tri_off"]), None, None, None), "get_cut")
+        d["tris"] = np.zeros(int(d["tri_off"][-1]), np.int32)
+        self._ck(self.lib.nbvh_get_cut(self.h, lod, None, None, None, None, _ptr(d["tri_off"]), _ptr(d["tris"]),
+                                       _ptr(d["dom_min"]), _ptr(d["dom_inv"])), "get_cut")
+        d["n_leaves"] = n
+        d["n_inner"] = int(ni[0])
+        return d
+
+    def set_leaf_rank(self, rank, lod=0):
+        r = np.ascontiguousarray(rank, np.float32)
+        self._ck(self.lib.nbvh_set_leaf_rank(self.h, lod, _ptr(r)), "set_leaf_rank")
+
+    # ---------------------------------------------------------------- query
+    @staticmethod
+    def alloc_hits(n, device="cuda"):
+        import torch
+        return dict(hit=torch.empty(n, dtype=torch.uint8, device=device),
+                    t=torch.empty(n, dtype=torch.float32, device=device),
+                    normal=torch.empty(n, 3, dtype=torch.float32, device=device),
+                    albedo=torch.empty(n, 3, dtype=torch.float32, device=device),
+                    leaf=torch.empty(n, dtype=torch.int32, device=device),
+                    n_queries=torch.empty(n, dtype=torch.int32, device=device))
+
+    @staticmethod
+    def _hits(out):
+        return Hits(_ptr(out["hit"]), _ptr(out["t"]), _ptr(out["normal"]), _ptr(out["albedo"]), _ptr(out.get("leaf")),
+                    _ptr(out.get("n_queries")))
+
+    def query(self, rays, lod=0, out=None, stream=None):
+        """rays: cuda float32 tensor [n, 8]."""
+        n = rays.shape[0]
+        if out is None:
+            out = self.alloc_hits(n, rays.device)
+        self._ck(self.lib.nbvh_query(self.h, _ptr(rays), n, lod, self._hits(out), _stream_ptr(stream)), "query")
+        return out
+
+    def query_host(self, rays_np, out=None, lod=0, stream=None):
+        """End-to-end path: host (ideally pinned) numpy rays -> host numpy results."""
+        n = rays_np.shape[0]
+        if out is None:
+            out = dict(hit=np.zeros(n, np.uint8), t=np.zeros(n, np.float32), normal=np.zeros((n, 3), np.float32),
+                       albedo=np.zeros((n, 3), np.float32), leaf=np.zeros(n, np.int32),
+                       n_queries=np.zeros(n, np.int32))
+        self._ck(self.lib.nbvh_query_host(self.h, _ptr(rays_np), n, lod, self._hits(out), _stream_ptr(stream)),
+                 "query_host")
+        return out
+
+    def query_stats(self):
+        s = QueryStats()
+        self._ck(self.lib.nbvh_get_query_stats(self.h, C.byref(s)), "query_stats")
+        return dict(n_rays=s.n_rays, n_queries=s.n_queries, n_waves=s.n_waves, n_launches=s.n_launches,
+                    n_refills=s.n_refills, ms_traverse=s.ms_traverse, ms_waves=s.ms_waves)
+
+    def set_profiling(self, on=True):
+        self._ck(self.lib.nbvh_set_profiling(self.h, int(bool(on))), "set_profiling")
+
+    # ---------------------------------------------------------------- training
+    def train_backward(self, rays, u, xi, lod=0, stream=None):
+        self._ck(self.lib.nbvh_train_backward(self.h, _ptr(rays), rays.shape[0], _ptr(u), _ptr(xi), lod,
+                                              _stream_ptr(stream)), "train_backward")
+
+    def grad_buffer(self):
+        import torch
+        p = C.c_void_p()
+        n = np.zeros(1, np.int64)
+        self._ck(self.lib.nbvh_grad_buffer(self.h, C.byref(p), _ptr(n)), "grad_buffer")
+        return p.value, int(n[0])
+
+    def apply_update(self, lr=0.01, stream=None):
+        self._ck(self.lib.nbvh_apply_update(self.h, float(lr), _stream_ptr(stream)), "apply_update")
+
+    def train_step(self, rays, u, xi, lod=0, lr=0.01, stream=None):
+        self._ck(self.lib.nbvh_train_step(self.h, _ptr(rays), rays.shape[0], _ptr(u), _ptr(xi), lod, float(lr),
+                                          _stream_ptr(stream)), "train_step")
+
+    def train_stats(self):
+        s = TrainStats()
+        self._ck(self.lib.nbvh_get_train_stats(self.h, C.byref(s)), "train_stats")
+        return dict(n_rays=s.n_rays, n_first_hit=s.n_first_hit, n_accepted=s.n_accepted, loss_sum=s.loss_sum,
+                    loss_terms=list(s.loss_terms), n_launches=s.n_launches, skipped=s.skipped)
+
+    # ---------------------------------------------------------------- parity hooks
+    def debug_traverse(self, rays, cap, lod=0, stream=None):
+        import torch
+        n = rays.shape[0]
+        leaf = torch.empty(n, cap, dtype=torch.int32, device=rays.device)
+        te = torch.empty(n, cap, dtype=torch.float32, device=rays.device)
+        tx = torch.empty(n, cap, dtype=torch.float32, device=rays.device)
+        cnt = torch.empty(n, dtype=torch.int32, device=rays.device)
+        self._ck(self.lib.nbvh_debug_traverse(self.h, _ptr(rays), n, lod, cap, _ptr(leaf), _ptr(te), _ptr(tx),
+                                              _ptr(cnt), _stream_ptr(stream)), "debug_traverse")
+        return leaf, te, tx, cnt
+
+    def debug_encode(self, pts, want_index=True, stream=None):
+        import torch
+        m = pts.shape[0]
+        L, F = self.cfg.L, self.cfg.F
+        feat = torch.empty(m, L * F, dtype=torch.float16, device=pts.device)
+        idx = torch.empty(m, L, 8, dtype=torch.int32, device=pts.device) if want_index else None
+        self._ck(self.lib.nbvh_debug_encode(self.h, _ptr(pts), m, _ptr(feat), _ptr(idx), _stream_ptr(stream)),
+                 "debug_encode")
+        return feat, idx
+
+    def debug_mlp(self, x16, stream=None):
+        import torch
+        m = x16.shape[0]
+        z = torch.empty(m, 8, dtype=torch.float32, device=x16.device)
+        self._ck(self.lib.nbvh_debug_mlp(self.h, _ptr(x16), m, _ptr(z), _stream_ptr(stream)), "debug_mlp")
+        return z
+
+    def debug_query_trace(self, rays, cap, lod=0, stream=None):
+        import torch
+        n = rays.shape[0]
+        out = self.alloc_hits(n, rays.device)
+        zt = torch.empty(n, cap, 8, dtype=torch.float32, device=rays.device)
+        self._ck(self.lib.nbvh_debug_query_trace(self.h, _ptr(rays), n, lod, self._hits(out), _ptr(zt), cap,
+                                                 _stream_ptr(stream)), "debug_query_trace")
+        return out, zt
+
+    def debug_train_samples(self, n, stream=None):
+        import torch
+        gt = torch.empty(n, 9, dtype=torch.float32, device="cuda")
+        acc = torch.empty(n, dtype=torch.uint8, device="cuda")
+        leaf = torch.empty(n, dtype=torch.int32, device="cuda")
+        loss = torch.empty(n, dtype=torch.float32, device="cuda")
+        self._ck(self.lib.nbvh_debug_train_samples(self.h, _ptr(gt), _ptr(acc), _ptr(leaf), _ptr(loss),
+                                                   _stream_ptr(stream)), "debug_train_samples")
+        return gt, acc, leaf, loss

@@ -1,0 +1,224 @@
+"""GPU parity of the query path (encode, MLP, traversal, full query) against the oracle.
+
+All calls go through the C-ABI (libnbvh.so) via the thin binding; the oracle is the
+plain CPU implementation in oracle/.  Tolerances:
+  * indices, leaf lists, t_enter/t_exit, hit masks, winning leaves, query counts: exact
+  * encode features (fp16 out, U[-1,1] tables): 2e-3 absolute
+  * MLP: decoded outputs (sigmoid channels, unit normal) 1e-2 absolute; raw z 2e-2*(1+|z|)
+  * end-to-end hit mask vs the double oracle: identical on rays whose decisive
+    visibilities satisfy |sigmoid(z_vis)-0.5| >= 1e-2; band rays counted (< 1%)
+"""
+import math
+
+import numpy as np
+import pytest
+
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def _mk_ctx(cfg_name="tiny", scene=None, leaves=None, seed=2, list_cap=16, mode=0, table_seed=7, **over):
+    from paper_2405_16237_b200 import Context, PARAM_TABLES
+    c = synth.CONFIGS[cfg_name]
+    h = c["hash"]
+    kw = dict(L=h.L, F=h.F, log2_T=h.log2_T, n_points=h.n_points, hidden_layers=h.hidden_layers,
+              list_cap=list_cap, mode=mode)
+    kw.update(over)
+    ctx = Context(device=0, **kw)
+    sc = scene if scene is not None else (synth.scene_tiny() if cfg_name == "tiny" else synth.scene_1080p())
+    ctx.set_mesh(sc)
+    ctx.build_cut(leaves or c["leaves"])
+    ctx.reserve(20000)
+    n_tab = ctx.param_count(PARAM_TABLES)
+    tab = synth.random_params_fp16(n_tab, seed=table_seed)
+    ctx.set_params(PARAM_TABLES, tab.astype(np.float32))
+    layers = synth.random_mlp(ctx.d_in, kw["hidden_layers"], 64, seed=seed)
+    ctx.set_mlp(layers)
+    return ctx, sc, tab.reshape(-1, kw["F"]), layers
+
+
+@pytest.fixture(scope="module")
+def tiny():
+    return _mk_ctx("tiny")
+
+
+def _grid(orc, ctx):
+    return orc.Grid(ctx.cfg.L, ctx.cfg.log2_T, ctx.cfg.F)
+
+
+# ------------------------------------------------------------------ encode
+def test_encode_indices_exact_features_close(orc, tiny):
+    ctx, sc, tab, layers = tiny
+    rng = np.random.default_rng(0)
+    pts = rng.random((20000, 3), dtype=np.float32)
+    pts[:50] = 0.0
+    pts[50:100] = 1.0
+    pts[100:400] = (rng.integers(0, 1025, (300, 3)) / 1024.0).astype(np.float32)   # on cell faces
+    feat, idx = ctx.debug_encode(torch.from_numpy(pts).cuda())
+    want, widx = orc.encode_points(_grid(orc, ctx), tab, pts)
+    assert np.array_equal(idx.cpu().numpy().view(np.uint32), widx)
+    err = np.abs(feat.float().cpu().numpy() - want)
+    assert err.max() <= 2e-3, err.max()
+
+
+@pytest.mark.parametrize("L,F,npts,log2_T", [(16, 2, 4, 19), (8, 4, 3, 18), (4, 2, 4, 12)])
+def test_encode_other_configs(orc, L, F, npts, log2_T):
+    from paper_2405_16237_b200 import Context, PARAM_TABLES
+    ctx = Context(device=0, L=L, F=F, n_points=npts, log2_T=log2_T, hidden_layers=2)
+    n = ctx.param_count(PARAM_TABLES)
+    tab = synth.random_params_fp16(n, seed=3)
+    ctx.set_params(PARAM_TABLES, tab.astype(np.float32))
+    pts = np.random.default_rng(1).random((5000, 3), dtype=np.float32)
+    feat, idx = ctx.debug_encode(torch.from_numpy(pts).cuda())
+    want, widx = orc.encode_points(orc.Grid(L, log2_T, F), tab.reshape(-1, F), pts)
+    assert np.array_equal(idx.cpu().numpy().view(np.uint32), widx)
+    assert np.abs(feat.float().cpu().numpy() - want).max() <= 2e-3
+
+
+# ------------------------------------------------------------------ MLP
+def _sig(z):
+    return 1 / (1 + np.exp(-z))
+
+
+@pytest.mark.parametrize("d_in,hidden", [(64, 2), (128, 3), (96, 4), (32, 1)])
+def test_mlp_tensor_core_vs_oracle(orc, d_in, hidden):
+    from paper_2405_16237_b200 import Context
+    L, F, npts = {64: (8, 2, 4), 128: (16, 2, 4), 96: (8, 4, 3), 32: (4, 2, 4)}[d_in]
+    ctx = Context(device=0, L=L, F=F, n_points=npts, hidden_layers=hidden)
+    layers = synth.random_mlp(d_in, hidden, 64, seed=5)
+    ctx.set_mlp(layers)
+    m = 1000 + 77                                              # ragged tail over 128-row tiles
+    x = (np.random.default_rng(2).random((m, d_in)) * 0.8 - 0.4).astype(np.float16)
+    z = ctx.debug_mlp(torch.from_numpy(x).cuda()).cpu().numpy()
+    want = orc.mlp_forward(layers, x.astype(np.float64))
+    assert np.all(np.abs(z - want) <= 2e-2 * (1 + np.abs(want))), np.abs(z - want).max()
+    for ch in (1, 5, 6, 7):
+        assert np.abs(_sig(z[:, ch]) - _sig(want[:, ch])).max() <= 1e-2
+    agree = np.sign(z[:, 0]) == np.sign(want[:, 0])
+    band = np.abs(_sig(want[:, 0]) - 0.5) < 1e-2
+    assert np.all(agree | band)
+
+
+# ------------------------------------------------------------------ traversal
+def _rays_tiny(n_random=3000):
+    cam = synth.camera_rays(64, 64, (0.0, 0.0, 3.5), vfov_deg=40.0)
+    rnd = synth.random_rays(n_random, seed=11)
+    return np.concatenate([cam, rnd], 0)
+
+
+@pytest.mark.parametrize("cap", [24])
+def test_traversal_lists_bit_exact(orc, tiny, cap):
+    ctx, sc, tab, layers = tiny
+    rays = _rays_tiny()
+    cut = ctx.cut(0)
+    leaf, te, tx, cnt = ctx.debug_traverse(torch.from_numpy(rays).cuda(), cap)
+    wl, wte, wtx, wcnt = orc.leaf_lists(rays, cut["leaf_lo"], cut["leaf_hi"], cap)
+    assert np.array_equal(cnt.cpu().numpy(), wcnt)
+    assert np.array_equal(leaf.cpu().numpy(), wl)
+    m = wl >= 0
+    assert np.array_equal(te.cpu().numpy()[m], wte[m]) and np.array_equal(tx.cpu().numpy()[m], wtx[m])
+    assert wcnt.max() > 16                                     # exercises resumption past K
+
+
+def test_traversal_small_capacity(orc):
+    ctx, sc, tab, layers = _mk_ctx("tiny", list_cap=3)
+    rays = _rays_tiny(1000)
+    cut = ctx.cut(0)
+    leaf, te, tx, cnt = ctx.debug_traverse(torch.from_numpy(rays).cuda(), 12)
+    wl, wte, wtx, wcnt = orc.leaf_lists(rays, cut["leaf_lo"], cut["leaf_hi"], 12)
+    assert np.array_equal(leaf.cpu().numpy(), wl) and np.array_equal(cnt.cpu().numpy(), wcnt)
+
+
+# ------------------------------------------------------------------ end-to-end query
+def _check_query(orc, ctx, tab, layers, rays, mode=0, cap=64):
+    cut = ctx.cut(0)
+    out, zt = ctx.debug_query_trace(torch.from_numpy(rays).cuda(), cap)
+    torch.cuda.synchronize()
+    g = {k: v.cpu().numpy() for k, v in out.items()}
+    zt = zt.cpu().numpy()
+    # (1) logic replay of the GPU's own z values: exact
+    rep = orc.replay(cut["leaf_lo"], cut["leaf_hi"], rays, zt, mode=mode)
+    assert rep["missing"] == 0
+    assert np.array_equal(g["hit"], rep["hit"])
+    assert np.array_equal(g["leaf"], rep["leaf"])
+    assert np.array_equal(g["n_queries"], rep["nq"])
+    assert np.array_equal(g["t"].view(np.uint32), rep["t"].view(np.uint32))
+    assert np.abs(g["normal"] - rep["normal"]).max() <= 1e-6
+    assert np.abs(g["albedo"] - rep["albedo"]).max() <= 1e-6
+    # (2) the double-precision oracle
+    o = orc.query(_grid(orc, ctx), ctx.cfg.n_points, tab, layers, cut["leaf_lo"], cut["leaf_hi"], rays, mode=mode,
+                  trace_cap=cap)
+    clear = (o["margin"] >= 1e-2) & (o["tmargin"] >= 1e-2)
+    assert np.array_equal(g["hit"][clear], o["hit"][clear])
+    assert np.array_equal(g["leaf"][clear], o["leaf"][clear])
+    assert np.array_equal(g["n_queries"][clear], o["nq"][clear])
+    assert (~clear).mean() < 0.01, (~clear).mean()
+    h = clear & (o["hit"] == 1)
+    assert np.abs(g["t"][h] - o["t"][h]).max() <= 2e-3 * 3.5     # C23: t / scene diagonal
+    assert np.abs(g["albedo"][h] - o["albedo"][h]).max() <= 1e-2
+    assert np.abs(g["normal"][h] - o["normal"][h]).max() <= 1e-2
+    # traced z vs oracle z for every query both made
+    both = ~np.isnan(zt[..., 0]) & ~np.isnan(o["z_trace"][..., 0])
+    zg, zo = zt[both], o["z_trace"][both]
+    assert np.all(np.abs(zg - zo) <= 2e-2 * (1 + np.abs(zo)))
+    return g, o
+
+
+def test_query_tiny_end_to_end(orc, tiny):
+    ctx, sc, tab, layers = tiny
+    g, o = _check_query(orc, ctx, tab, layers, _rays_tiny())
+    assert g["hit"].sum() > 500 and g["n_queries"].max() >= 2
+
+
+def test_query_first_hit_mode(orc):
+    ctx, sc, tab, layers = _mk_ctx("tiny", mode=1)
+    _check_query(orc, ctx, tab, layers, _rays_tiny(), mode=1)
+
+
+def test_query_refill_path(orc):
+    ctx, sc, tab, layers = _mk_ctx("tiny", list_cap=2)
+    g, _ = _check_query(orc, ctx, tab, layers, _rays_tiny())
+    assert ctx.query_stats()["n_refills"] > 0
+
+
+def test_query_single_leaf_and_empty(orc):
+    ctx, sc, tab, layers = _mk_ctx("tiny", leaves=1)
+    rays = _rays_tiny(500)
+    g, o = _check_query(orc, ctx, tab, layers, rays)
+    assert np.all(g["n_queries"] <= 1)
+    out = ctx.query(torch.zeros(0, 8, device="cuda"))            # n = 0 is a no-op
+    assert out["hit"].numel() == 0
+
+
+def test_query_host_path_equals_device_path(tiny):
+    ctx, sc, tab, layers = tiny
+    rays = _rays_tiny()
+    d = {k: v.cpu().numpy() for k, v in ctx.query(torch.from_numpy(rays).cuda()).items()}
+    h = ctx.query_host(rays)
+    for k in d:
+        assert np.array_equal(d[k].reshape(h[k].shape), h[k]), k
+
+
+def test_query_1080p_sampled_full_size(orc):
+    """cfg 2 at full size in the bench's launch configuration; sampled rays vs oracle."""
+    ctx, sc, tab, layers = _mk_ctx("1080p", table_seed=9, seed=6)
+    c = synth.CONFIGS["1080p"]
+    rays = synth.camera_rays(*c["res"], c["eye"], vfov_deg=c["vfov"])
+    ctx.reserve(rays.shape[0])
+    out = ctx.query(torch.from_numpy(rays).cuda())
+    torch.cuda.synchronize()
+    st = ctx.query_stats()
+    assert st["n_rays"] == rays.shape[0] and st["n_queries"] > rays.shape[0] // 2
+    sample = np.arange(0, rays.shape[0], 4099)
+    cut = ctx.cut(0)
+    o = orc.query(_grid(orc, ctx), 4, tab, layers, cut["leaf_lo"], cut["leaf_hi"], rays[sample])
+    g = {k: v.cpu().numpy()[sample] for k, v in out.items()}
+    clear = (o["margin"] >= 1e-2) & (o["tmargin"] >= 1e-2)
+    assert np.array_equal(g["hit"][clear], o["hit"][clear])
+    assert np.array_equal(g["leaf"][clear], o["leaf"][clear])
+    assert np.array_equal(g["n_queries"][clear], o["nq"][clear])
+    h = clear & (o["hit"] == 1)
+    assert h.sum() > 50
+    assert np.abs(g["t"][h] - o["t"][h]).max() <= 2e-3 * 2.9

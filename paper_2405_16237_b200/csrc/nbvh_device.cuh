@@ -133,7 +133,7 @@ __device__ int collect_leaves(const CutDev& cut, const RayDev& R, bool has_after
             if (hl && cl < 0) consider(-1 - cl, lte_, ltx_);
             if (hr && cr < 0) consider(-1 - cr, rte_, rtx_);
             bool pl = hl && cl >= 0, pr = hr && cr >= 0;
-            if (sp + 2 > 64) { atomicOr(err_flag, 1); break; }
+            if (sp + 2 > 64) { if (err_flag) atomicOr(err_flag, 1); break; }
             // push the farther child first so the nearer is visited first
             if (pl && pr) {
                 bool l_first = lte_ <= rte_;

@@ -5,12 +5,39 @@
 #include <cstring>
 #include <vector>
 
+#include <cmath>
+#include <string>
+
 #include "nbvh_capi_internal.h"
+#include "nbvh_train_kernels.cuh"
 
 namespace nbvh {
 
 struct TrainWork {
-    int64_t cap = 0;
+    int64_t cap = 0;                 // rays (and samples) per call
+    uint8_t* r_acc = nullptr;
+    int32_t* r_leaf = nullptr;
+    float* r_gt = nullptr;
+    float* r_loss = nullptr;
+    int32_t* s_ray = nullptr;
+    int32_t* s_leaf = nullptr;
+    float* s_t0 = nullptr;
+    float* s_t1 = nullptr;
+    float* s_gt = nullptr;
+    __half* X = nullptr;
+    __half* A = nullptr;
+    __half* Dl = nullptr;
+    float* dZ = nullptr;
+    float* grad = nullptr;           // params + 1 + 3 * tail_leaves
+    int64_t tail_leaves = 0;
+    float* m = nullptr;
+    float* v = nullptr;
+    int32_t* counters = nullptr;     // [0] samples, [1] first hits, [2] non-finite flag
+    double* loss_acc = nullptr;      // [5]
+    int64_t step = 0;
+    int32_t lod = 0;
+    int32_t launches = 0;
+    cudaStream_t stream = nullptr;
 };
 
 template <typename T>
@@ -78,18 +105,124 @@ void free_scene_device(nbvh_ctx* c) {
     d = DeviceScene{};
 }
 
+template <typename T>
+static void dfree(T*& p) {
+    if (p) cudaFree((void*)p);
+    p = nullptr;
+}
+
+static void free_work(TrainWork* w) {
+    dfree(w->r_acc); dfree(w->r_leaf); dfree(w->r_gt); dfree(w->r_loss);
+    dfree(w->s_ray); dfree(w->s_leaf); dfree(w->s_t0); dfree(w->s_t1); dfree(w->s_gt);
+    dfree(w->X); dfree(w->A); dfree(w->Dl); dfree(w->dZ);
+}
+
 void free_train_device(nbvh_ctx* c) {
+    if (!c->train) return;
+    free_work(c->train);
+    dfree(c->train->grad);
+    dfree(c->train->m);
+    dfree(c->train->v);
+    dfree(c->train->counters);
+    dfree(c->train->loss_acc);
     delete c->train;
     c->train = nullptr;
 }
 
-nbvh_status reserve_train(nbvh_ctx* c, int64_t max_rays) {
-    (void)c;
-    (void)max_rays;
+static int64_t n_params(const nbvh_ctx* c) { return c->n_table + c->n_W + c->n_b; }
+
+// Gradient buffer, Adam moments and counters (independent of the batch size).
+static nbvh_status ensure_train_state(nbvh_ctx* c, int64_t tail_leaves) {
+    if (!c->train) c->train = new TrainWork();
+    TrainWork* w = c->train;
+    cudaError_t e = cudaSuccess;
+    if (!w->m) {
+        const size_t np = (size_t)n_params(c);
+        e = cudaMalloc((void**)&w->m, np * 4);
+        if (e == cudaSuccess) e = cudaMalloc((void**)&w->v, np * 4);
+        if (e == cudaSuccess) e = cudaMemset(w->m, 0, np * 4);
+        if (e == cudaSuccess) e = cudaMemset(w->v, 0, np * 4);
+        if (e == cudaSuccess) e = cudaMalloc((void**)&w->counters, 16 * sizeof(int32_t));
+        if (e == cudaSuccess) e = cudaMalloc((void**)&w->loss_acc, 8 * sizeof(double));
+        w->step = 0;
+    }
+    if (e == cudaSuccess && (!w->grad || tail_leaves > w->tail_leaves)) {
+        dfree(w->grad);
+        const size_t ng = (size_t)(n_params(c) + 1 + 3 * tail_leaves);
+        e = cudaMalloc((void**)&w->grad, ng * 4);
+        if (e == cudaSuccess) e = cudaMemset(w->grad, 0, ng * 4);
+        w->tail_leaves = tail_leaves;
+    }
+    if (e != cudaSuccess) return cuda_fail(c, e, "train state");
     return NBVH_OK;
 }
 
-void reset_adam(nbvh_ctx* c) { (void)c; }
+nbvh_status reserve_train(nbvh_ctx* c, int64_t max_rays) {
+    nbvh_status st = ensure_train_state(c, 1);
+    if (st) return st;
+    TrainWork* w = c->train;
+    if (w->cap >= max_rays) return NBVH_OK;
+    free_work(w);
+    const size_t n = (size_t)max_rays, H = (size_t)c->cfg.hidden_layers, D = (size_t)c->d_in;
+    cudaError_t e = cudaMalloc((void**)&w->r_acc, n);
+    if (e == cudaSuccess) e = cudaMalloc((void**)&w->r_leaf, n * 4);
+    if (e == cudaSuccess) e = cudaMalloc((void**)&w->r_gt, n * 9 * 4);
+    if (e == cudaSuccess) e = cudaMalloc((void**)&w->r_loss, n * 4);
+    if (e == cudaSuccess) e = cudaMalloc((void**)&w->s_ray, n * 4);
+    if (e == cudaSuccess) e = cudaMalloc((void**)&w->s_leaf, n * 4);
+    if (e == cudaSuccess) e = cudaMalloc((void**)&w->s_t0, n * 4);
+    if (e == cudaSuccess) e = cudaMalloc((void**)&w->s_t1, n * 4);
+    if (e == cudaSuccess) e = cudaMalloc((void**)&w->s_gt, n * 9 * 4);
+    if (e == cudaSuccess) e = cudaMalloc((void**)&w->X, n * D * 2);
+    if (e == cudaSuccess) e = cudaMalloc((void**)&w->A, H * n * 64 * 2);
+    if (e == cudaSuccess) e = cudaMalloc((void**)&w->Dl, H * n * 64 * 2);
+    if (e == cudaSuccess) e = cudaMalloc((void**)&w->dZ, n * 8 * 4);
+    if (e != cudaSuccess) {
+        free_work(w);
+        cudaGetLastError();
+        return fail(c, NBVH_ENOMEM, std::string("reserve (training): ") + cudaGetErrorString(e));
+    }
+    w->cap = max_rays;
+    return NBVH_OK;
+}
+
+void reset_adam(nbvh_ctx* c) {
+    if (!c->train || !c->train->m) return;
+    const size_t np = (size_t)n_params(c);
+    cudaMemset(c->train->m, 0, np * 4);
+    cudaMemset(c->train->v, 0, np * 4);
+    c->train->step = 0;
+}
+
+// launchers (templated on F, D)
+template <int F, int D>
+static cudaError_t launch_train_fd(const TrainArgs& a, int64_t n, int64_t w_off, int64_t b_off, cudaStream_t s,
+                                   int* launches) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int H = a.m.hidden;
+    const size_t smem_fwd = (size_t)kTileQ * (D + 8) * 2 + (size_t)mlp_smem_halves(D, H) * 2 + kTileQ * 8 * 4 +
+                            (64 * H + 8) * 4 + kTileQ * sizeof(SampleDesc);
+    const size_t smem_bwd = ((size_t)64 * (D + 8) + (size_t)(H - 1) * 64 * 72 + 16 * 72) * 2 + kTileQ * sizeof(SampleDesc);
+    const size_t smem_dw = (size_t)kTileQ * 72 * 2 + (size_t)kTileQ * (D + 8) * 2 + kTileQ * 8 * 4;
+    cudaFuncSetAttribute(k_train_fwd<F, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fwd);
+    cudaFuncSetAttribute(k_train_bwd<F, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bwd);
+    cudaFuncSetAttribute(k_train_dw<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_dw);
+    const unsigned blocks_n = (unsigned)((n + 127) / 128);
+    k_train_select<<<blocks_n, 128, 0, s>>>(a);
+    k_train_label<<<blocks_n, 128, 0, s>>>(a);
+    const int tiles = (int)((n + kTileQ - 1) / kTileQ);
+    const int grid = tiles < sms ? (tiles > 0 ? tiles : 1) : sms;
+    k_train_fwd<F, D><<<grid, 256, smem_fwd, s>>>(a);
+    k_train_bwd<F, D><<<grid, 256, smem_bwd, s>>>(a);
+    const unsigned dw_grid = (unsigned)((n + kDwChunk - 1) / kDwChunk);
+    k_train_dw<D><<<dw_grid > 0 ? dw_grid : 1, 256, smem_dw, s>>>(a, w_off, b_off);
+    *launches += 5;
+    return cudaGetLastError();
+}
+
+__global__ void k_store_count(const int32_t* n, float* dst) { *dst = (float)*n; }
 
 }  // namespace nbvh
 
@@ -100,6 +233,8 @@ extern "C" nbvh_status nbvh_set_leaf_rank(nbvh_ctx* c, int32_t lod, const float*
     if (lod < 0 || lod >= kMaxLod) return fail(c, NBVH_ERANGE, "set_leaf_rank: lod");
     if (!c->has_cut[lod]) return fail(c, NBVH_ESTATE, "set_leaf_rank: no cut");
     HostCut& hc = c->cuts[lod];
+    for (int32_t i = 0; i < hc.n_leaves; ++i)
+        if (!std::isfinite(h_rank[i])) return fail(c, NBVH_EINVAL, "set_leaf_rank: non-finite rank");
     std::memcpy(hc.rank.data(), h_rank, sizeof(float) * hc.n_leaves);
     if (c->device >= 0) {
         nbvh_status st = check_device(c);
@@ -110,25 +245,184 @@ extern "C" nbvh_status nbvh_set_leaf_rank(nbvh_ctx* c, int32_t lod, const float*
     return NBVH_OK;
 }
 
-extern "C" nbvh_status nbvh_train_backward(nbvh_ctx* c, const nbvh_ray*, int64_t, const float*, const float*, int32_t,
-                                           void*) {
-    return fail(c, NBVH_ESTATE, "train_backward: not implemented yet");
-}
-extern "C" nbvh_status nbvh_grad_buffer(nbvh_ctx* c, float**, int64_t*) {
-    return fail(c, NBVH_ESTATE, "grad_buffer: not implemented yet");
-}
-extern "C" nbvh_status nbvh_apply_update(nbvh_ctx* c, float, void*) {
-    return fail(c, NBVH_ESTATE, "apply_update: not implemented yet");
-}
-extern "C" nbvh_status nbvh_train_step(nbvh_ctx* c, const nbvh_ray*, int64_t, const float*, const float*, int32_t,
-                                       float, void*) {
-    return fail(c, NBVH_ESTATE, "train_step: not implemented yet");
-}
-extern "C" nbvh_status nbvh_get_train_stats(nbvh_ctx* c, nbvh_train_stats* out) {
-    if (!c || !out) return NBVH_EINVAL;
-    *out = c->tstats;
+extern "C" nbvh_status nbvh_train_backward(nbvh_ctx* c, const nbvh_ray* rays, int64_t n, const float* u,
+                                           const float* xi, int32_t lod, void* stream) {
+    nbvh_status st = check_device(c);
+    if (st) return st;
+    if (lod < 0 || lod >= kMaxLod) return fail(c, NBVH_ERANGE, "train_backward: lod");
+    if (!c->has_cut[lod]) return fail(c, NBVH_ESTATE, "train_backward: no cut");
+    if (n < 0 || (n > 0 && (!rays || !u || !xi))) return fail(c, NBVH_EINVAL, "train_backward: null pointer");
+    if (n > c->reserved) return fail(c, NBVH_ESTATE, "train_backward: n exceeds nbvh_reserve");
+    if (c->cfg.n_points > 4) return fail(c, NBVH_EINVAL, "train_backward: n_points > 4 not supported");
+    const HostCut& hc = c->cuts[lod];
+    st = ensure_train_state(c, hc.n_leaves);
+    if (st) return st;
+    st = reserve_train(c, c->reserved);
+    if (st) return st;
+    TrainWork* w = c->train;
+    cudaStream_t s = (cudaStream_t)stream;
+    w->stream = s;
+    w->lod = lod;
+    w->launches = 0;
+    const int64_t ng = n_params(c) + 1 + 3 * (int64_t)hc.n_leaves;
+    cudaError_t e = cudaMemsetAsync(w->grad, 0, (size_t)ng * 4, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(w->counters, 0, 16 * sizeof(int32_t), s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(w->loss_acc, 0, 8 * sizeof(double), s);
+    if (e != cudaSuccess) return cuda_fail(c, e, "train_backward: memset");
+    c->tstats = nbvh_train_stats{};
+    c->tstats.n_rays = n;
+    if (n == 0) return NBVH_OK;
+    // C18 rank normalisation in fp32 (the oracle does the same operations)
+    float rmin = hc.rank[0], rmax = hc.rank[0];
+    for (int32_t i = 1; i < hc.n_leaves; ++i) {
+        rmin = std::fmin(rmin, hc.rank[i]);
+        rmax = std::fmax(rmax, hc.rank[i]);
+    }
+    TrainArgs a{};
+    a.g = make_grid(c, lod);
+    a.m = make_mlp(c);
+    a.cut = make_cut(c, lod);
+    a.rays = reinterpret_cast<const float4*>(rays);
+    a.n_rays = n;
+    a.u = u;
+    a.xi = xi;
+    a.rank = c->dcut[lod].rank;
+    a.rank_min = rmin;
+    a.rank_hmax = (rmax - rmin) + 1e-6f;
+    a.leaf_base = c->dcut[lod].leaf_base;
+    a.nodes = c->dscene.nodes;
+    a.tri_v = c->dscene.tri_v;
+    a.tri_n = c->dscene.tri_n;
+    a.tri_a = c->dscene.tri_a;
+    a.tri_id = c->dscene.tri_id;
+    a.r_acc = w->r_acc;
+    a.r_leaf = w->r_leaf;
+    a.r_gt = w->r_gt;
+    a.r_loss = w->r_loss;
+    a.n_samples = w->counters;
+    a.n_first = w->counters + 1;
+    a.s_ray = w->s_ray;
+    a.s_leaf = w->s_leaf;
+    a.s_t0 = w->s_t0;
+    a.s_t1 = w->s_t1;
+    a.s_gt = w->s_gt;
+    a.X = w->X;
+    a.A = w->A;
+    a.Dl = w->Dl;
+    a.dZ = w->dZ;
+    a.grad = w->grad;
+    a.tail = w->grad + n_params(c);
+    a.loss_acc = w->loss_acc;
+    a.cap = w->cap;
+    const int64_t w_off = c->n_table, b_off = c->n_table + c->n_W;
+    const int F = c->cfg.F, D = c->d_in;
+    int launches = 0;
+    if (F == 2 && D == 32) e = launch_train_fd<2, 32>(a, n, w_off, b_off, s, &launches);
+    else if (F == 2 && D == 64) e = launch_train_fd<2, 64>(a, n, w_off, b_off, s, &launches);
+    else if (F == 2 && D == 96) e = launch_train_fd<2, 96>(a, n, w_off, b_off, s, &launches);
+    else if (F == 2 && D == 128) e = launch_train_fd<2, 128>(a, n, w_off, b_off, s, &launches);
+    else if (F == 4 && D == 64) e = launch_train_fd<4, 64>(a, n, w_off, b_off, s, &launches);
+    else if (F == 4 && D == 96) e = launch_train_fd<4, 96>(a, n, w_off, b_off, s, &launches);
+    else if (F == 4 && D == 128) e = launch_train_fd<4, 128>(a, n, w_off, b_off, s, &launches);
+    else return fail(c, NBVH_EINVAL, "train_backward: unsupported (F, D_in)");
+    if (e != cudaSuccess) return cuda_fail(c, e, "train_backward: launch");
+    k_store_count<<<1, 1, 0, s>>>(w->counters, a.tail);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(c, e, "train_backward: count");
+    w->launches = launches + 1;
     return NBVH_OK;
 }
-extern "C" nbvh_status nbvh_debug_train_samples(nbvh_ctx* c, float*, uint8_t*, int32_t*, float*, void*) {
-    return fail(c, NBVH_ESTATE, "debug_train_samples: not implemented yet");
+
+extern "C" nbvh_status nbvh_grad_buffer(nbvh_ctx* c, float** d_grad, int64_t* n_floats) {
+    nbvh_status st = check_device(c);
+    if (st) return st;
+    if (!d_grad || !n_floats) return fail(c, NBVH_EINVAL, "grad_buffer: null pointer");
+    if (!c->train || !c->train->grad) return fail(c, NBVH_ESTATE, "grad_buffer: no training batch yet");
+    *d_grad = c->train->grad;
+    *n_floats = n_params(c) + 1 + 3 * (int64_t)c->cuts[c->train->lod].n_leaves;
+    return NBVH_OK;
+}
+
+extern "C" nbvh_status nbvh_apply_update(nbvh_ctx* c, float lr, void* stream) {
+    nbvh_status st = check_device(c);
+    if (st) return st;
+    if (!c->train || !c->train->grad) return fail(c, NBVH_ESTATE, "apply_update: no gradient");
+    if (!(lr >= 0.f) || !std::isfinite(lr)) return fail(c, NBVH_EINVAL, "apply_update: bad lr");
+    TrainWork* w = c->train;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t np = n_params(c);
+    cudaError_t e = cudaMemsetAsync(w->counters + 2, 0, 4, s);
+    if (e != cudaSuccess) return cuda_fail(c, e, "apply_update");
+    k_check_finite<<<592, 256, 0, s>>>(w->grad, np, w->counters + 2);
+    w->step += 1;
+    AdamArgs a{};
+    a.param = c->d_params;
+    a.grad = w->grad;
+    a.m = w->m;
+    a.v = w->v;
+    a.n = np;
+    a.count = w->grad + np;
+    a.bad = w->counters + 2;
+    a.lr = lr;
+    a.beta1 = 0.9f;
+    a.beta2 = 0.999f;
+    a.eps = 1e-8f;
+    a.c1 = (float)(1.0 - std::pow(0.9, (double)w->step));
+    a.c2 = (float)(1.0 - std::pow(0.999, (double)w->step));
+    a.table16 = c->d_table16;
+    a.n_table = c->n_table;
+    a.W16 = c->d_W16;
+    a.n_W = c->n_W;
+    k_adam<<<1184, 256, 0, s>>>(a);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(c, e, "apply_update: adam");
+    w->launches += 2;
+    w->stream = s;
+    return NBVH_OK;
+}
+
+extern "C" nbvh_status nbvh_train_step(nbvh_ctx* c, const nbvh_ray* rays, int64_t n, const float* u, const float* xi,
+                                       int32_t lod, float lr, void* stream) {
+    nbvh_status st = nbvh_train_backward(c, rays, n, u, xi, lod, stream);
+    if (st) return st;
+    return nbvh_apply_update(c, lr, stream);
+}
+
+extern "C" nbvh_status nbvh_get_train_stats(nbvh_ctx* c, nbvh_train_stats* out) {
+    if (!c || !out) return NBVH_EINVAL;
+    nbvh_status st = check_device(c);
+    if (st) return st;
+    if (!c->train || !c->train->counters) return fail(c, NBVH_ESTATE, "train_stats: no training call yet");
+    TrainWork* w = c->train;
+    cudaError_t e = cudaStreamSynchronize(w->stream);
+    int32_t cnt[3];
+    double la[5];
+    if (e == cudaSuccess) e = cudaMemcpy(cnt, w->counters, sizeof(cnt), cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpy(la, w->loss_acc, sizeof(la), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(c, e, "train_stats");
+    c->tstats.n_accepted = cnt[0];
+    c->tstats.n_first_hit = cnt[1];
+    c->tstats.loss_sum = la[0];
+    for (int k = 0; k < 4; ++k) c->tstats.loss_terms[k] = la[1 + k];
+    c->tstats.n_launches = w->launches;
+    c->tstats.skipped = cnt[2] != 0;
+    *out = c->tstats;
+    return cnt[2] ? NBVH_ENONFINITE : NBVH_OK;
+}
+
+extern "C" nbvh_status nbvh_debug_train_samples(nbvh_ctx* c, float* gt, uint8_t* acc, int32_t* leaf, float* loss,
+                                                void* stream) {
+    nbvh_status st = check_device(c);
+    if (st) return st;
+    if (!c->train || !c->train->r_acc) return fail(c, NBVH_ESTATE, "debug_train_samples: no training batch yet");
+    const int64_t n = c->tstats.n_rays;
+    cudaStream_t s = (cudaStream_t)stream;
+    TrainWork* w = c->train;
+    cudaError_t e = cudaSuccess;
+    if (gt) e = cudaMemcpyAsync(gt, w->r_gt, (size_t)n * 9 * 4, cudaMemcpyDeviceToDevice, s);
+    if (e == cudaSuccess && acc) e = cudaMemcpyAsync(acc, w->r_acc, (size_t)n, cudaMemcpyDeviceToDevice, s);
+    if (e == cudaSuccess && leaf) e = cudaMemcpyAsync(leaf, w->r_leaf, (size_t)n * 4, cudaMemcpyDeviceToDevice, s);
+    if (e == cudaSuccess && loss) e = cudaMemcpyAsync(loss, w->r_loss, (size_t)n * 4, cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return cuda_fail(c, e, "debug_train_samples");
+    return NBVH_OK;
 }

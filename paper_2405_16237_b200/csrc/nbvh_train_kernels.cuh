@@ -1,0 +1,754 @@
+// nbvh_train_kernels.cuh — device code of the companion training step (P:142, P:193-247,
+// P:275):
+//   k_train_select   T1  first intersected cut leaf + stochastic acceptance (C18)
+//   k_train_label    T2  ground truth by intersecting the leaf's own triangles (C17)
+//   k_train_fwd      T3-T5 jittered encode, MLP forward (activations kept), gated loss + dL/dz
+//   k_train_bwd      T6/T7 delta chain through the MLP on tensor cores, dL/dx, hash-grid
+//                    gradient scatter with warp-aggregated atomics
+//   k_train_dw       T6  weight gradients dW = delta^T x as split-K tensor-core GEMMs
+//   k_adam           T9  Adam (C20) + fp16 inference-copy refresh
+#pragma once
+
+#include <cuda_fp16.h>
+
+#include "nbvh_device.cuh"
+#include "nbvh_internal.h"
+
+namespace nbvh {
+
+struct TrainArgs {
+    GridDev g;
+    MlpDev m;
+    CutDev cut;
+    const float4* rays;
+    int64_t n_rays;
+    const float* u;          // [n] acceptance draws
+    const float* xi;         // [n][n_points] jitter
+    const float* rank;       // [n_leaves]
+    float rank_min, rank_hmax;   // fp32: min rank, (max-min)+eps (C18)
+    const int32_t* leaf_base;
+    const BvhNode* nodes;
+    const float* tri_v;
+    const float* tri_n;
+    const float* tri_a;
+    const int32_t* tri_id;
+    // per ray (debug / stats)
+    uint8_t* r_acc;
+    int32_t* r_leaf;
+    float* r_gt;             // [n][9]
+    float* r_loss;
+    // per sample (compact)
+    int32_t* n_samples;      // device counter
+    int32_t* n_first;        // device counter
+    int32_t* s_ray;
+    int32_t* s_leaf;
+    float* s_t0;
+    float* s_t1;
+    float* s_gt;             // [M][9]
+    __half* X;               // [M][D]
+    __half* A;               // [hidden][M][64] post-ReLU activations
+    __half* Dl;              // [hidden][M][64] deltas dL/d(pre-activation)
+    float* dZ;               // [M][8]
+    // outputs
+    float* grad;             // flat fp32: tables, weights, biases, tail
+    float* tail;             // [0] accepted count, [1 + 3*leaf + {0,1,2}] loss sum, samples, first hits
+    double* loss_acc;        // [5]: total, vis, dist, normal, albedo (weights applied)
+    int64_t cap;             // capacity of the per-sample arrays
+};
+
+// ------------------------------------------------------------------ T1 select
+__global__ void __launch_bounds__(128) k_train_select(TrainArgs a) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool acc = false;
+    int leaf = -1;
+    float te = 0.f, tx = 0.f;
+    if (r < a.n_rays) {
+        RayDev R = load_ray(a.rays, r);
+        float lte[1], ltx[1];
+        int lid[1], n = 0;
+        int total = collect_leaves<1>(a.cut, R, false, 0.f, 0, 1, lte, ltx, lid, n, nullptr);
+        if (total > 0) {
+            leaf = lid[0];
+            te = lte[0];
+            tx = ltx[0];
+            atomicAdd(a.n_first, 1);
+            atomicAdd(a.tail + 1 + 3 * leaf + 2, 1.0f);
+            // trained with probability max(r/r_max, 0.005) on shifted ranks (C18)
+            const float rh = __fadd_rn(__fsub_rn(a.rank[leaf], a.rank_min), 1e-6f);
+            const float p = fmaxf(__fdiv_rn(rh, a.rank_hmax), 0.005f);
+            acc = a.u[r] < p;
+        }
+        a.r_acc[r] = acc ? 1 : 0;
+        a.r_leaf[r] = leaf;
+        a.r_loss[r] = 0.f;
+#pragma unroll
+        for (int k = 0; k < 9; ++k) a.r_gt[9 * r + k] = 0.f;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, acc);
+    const int lane = threadIdx.x & 31;
+    int base = 0;
+    if (lane == 0 && m) base = atomicAdd(a.n_samples, __popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (acc) {
+        const int i = base + __popc(m & ((1u << lane) - 1u));
+        a.s_ray[i] = (int)r;
+        a.s_leaf[i] = leaf;
+        a.s_t0[i] = te;
+        a.s_t1[i] = tx;
+    }
+}
+
+// ------------------------------------------------------------------ T2 label
+// Moller-Trumbore in double with the oracle's operation order (no FMA), so the hit
+// decisions and t are bit-identical to the double-precision ground truth.
+__device__ __forceinline__ double dot3(const double* a, const double* b) {
+    return __dadd_rn(__dadd_rn(__dmul_rn(a[0], b[0]), __dmul_rn(a[1], b[1])), __dmul_rn(a[2], b[2]));
+}
+__device__ __forceinline__ void cross3(const double* a, const double* b, double* c) {
+    c[0] = __dsub_rn(__dmul_rn(a[1], b[2]), __dmul_rn(a[2], b[1]));
+    c[1] = __dsub_rn(__dmul_rn(a[2], b[0]), __dmul_rn(a[0], b[2]));
+    c[2] = __dsub_rn(__dmul_rn(a[0], b[1]), __dmul_rn(a[1], b[0]));
+}
+
+__device__ __forceinline__ bool tri_hit(const double* o, const double* d, const float* tv, double t0, double t1,
+                                        double& t, double& b1, double& b2) {
+    double v0[3], e1[3], e2[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        v0[k] = tv[k];
+        e1[k] = __dsub_rn((double)tv[3 + k], v0[k]);
+        e2[k] = __dsub_rn((double)tv[6 + k], v0[k]);
+    }
+    double p[3];
+    cross3(d, e2, p);
+    const double det = dot3(e1, p);
+    if (fabs(det) < 1e-20) return false;
+    const double inv = __ddiv_rn(1.0, det);
+    double s[3] = {__dsub_rn(o[0], v0[0]), __dsub_rn(o[1], v0[1]), __dsub_rn(o[2], v0[2])};
+    const double uu = __dmul_rn(dot3(s, p), inv);
+    if (uu < 0.0 || uu > 1.0) return false;
+    double q[3];
+    cross3(s, e1, q);
+    const double vv = __dmul_rn(dot3(d, q), inv);
+    if (vv < 0.0 || __dadd_rn(uu, vv) > 1.0) return false;
+    const double tt = __dmul_rn(dot3(e2, q), inv);
+    if (tt < t0 || tt > t1) return false;
+    t = tt;
+    b1 = uu;
+    b2 = vv;
+    return true;
+}
+
+__global__ void __launch_bounds__(128) k_train_label(TrainArgs a) {
+    const int M = *a.n_samples;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= M) return;
+    const int r = a.s_ray[i];
+    RayDev R = load_ray(a.rays, r);
+    const double o[3] = {R.o[0], R.o[1], R.o[2]}, d[3] = {R.d[0], R.d[1], R.d[2]};
+    const float t0 = a.s_t0[i], t1 = a.s_t1[i];
+    // conservative box test: boxes grown by a relative epsilon so that no triangle the
+    // exact test would accept is pruned
+    int stack[64];
+    int sp = 0;
+    stack[sp++] = a.leaf_base[a.s_leaf[i]];
+    bool found = false;
+    double bt = 0, bb1 = 0, bb2 = 0;
+    int btri = -1, bslot = -1;
+    while (sp > 0) {
+        const BvhNode nd = a.nodes[stack[--sp]];
+        float lo[3], hi[3], te, tx;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const float e = 1e-5f * (fabsf(nd.lo[k]) + fabsf(nd.hi[k]) + 1e-3f);
+            lo[k] = nd.lo[k] - e;
+            hi[k] = nd.hi[k] + e;
+        }
+        if (!slab(R, lo, hi, te, tx)) continue;
+        if (te > t1 * 1.00001f + 1e-6f || tx < t0 * 0.99999f - 1e-6f) continue;
+        if (nd.b < 0) {
+            for (int j = nd.a; j < nd.a - nd.b; ++j) {
+                double th, b1, b2;
+                if (tri_hit(o, d, a.tri_v + 9 * (int64_t)j, (double)t0, (double)t1, th, b1, b2)) {
+                    const int id = a.tri_id[j];
+                    if (!found || th < bt || (th == bt && id < btri)) {
+                        found = true; bt = th; bb1 = b1; bb2 = b2; btri = id; bslot = j;
+                    }
+                }
+            }
+        } else if (sp + 2 <= 64) {
+            stack[sp++] = nd.b;
+            stack[sp++] = nd.a;
+        }
+    }
+    float gt[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) gt[k] = 0.f;
+    gt[0] = found ? 0.f : 1.f;
+    if (found) {
+        const double dt = (double)t1 - (double)t0;
+        gt[1] = dt > 0.0 ? (float)((bt - (double)t0) / dt) : 0.f;
+        const float* tn = a.tri_n + 9 * (int64_t)bslot;
+        double n[3];
+        for (int k = 0; k < 3; ++k)
+            n[k] = (1.0 - bb1 - bb2) * (double)tn[k] + bb1 * (double)tn[3 + k] + bb2 * (double)tn[6 + k];
+        const double nn = sqrt(n[0] * n[0] + n[1] * n[1] + n[2] * n[2]);
+        for (int k = 0; k < 3; ++k) gt[2 + k] = nn > 0 ? (float)(n[k] / nn) : 0.f;
+        for (int k = 0; k < 3; ++k) gt[5 + k] = a.tri_a[3 * (int64_t)bslot + k];
+        gt[8] = (float)bt;
+    }
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+        a.s_gt[9 * (int64_t)i + k] = gt[k];
+        a.r_gt[9 * (int64_t)r + k] = gt[k];
+    }
+}
+
+// ------------------------------------------------------------------ shared tile helpers
+struct SampleDesc {
+    float o[3], d[3], t0, t1;
+    float xi[4];
+    int ray, leaf, valid, pad;
+};
+
+__device__ __forceinline__ void load_sample_desc(const TrainArgs& a, int i, int M, SampleDesc& q) {
+    q.valid = i < M;
+    if (!q.valid) return;
+    const int r = a.s_ray[i];
+    q.ray = r;
+    q.leaf = a.s_leaf[i];
+    q.t0 = a.s_t0[i];
+    q.t1 = a.s_t1[i];
+    float4 r0 = __ldg(a.rays + 2 * (int64_t)r), r1 = __ldg(a.rays + 2 * (int64_t)r + 1);
+    q.o[0] = r0.x; q.o[1] = r0.y; q.o[2] = r0.z;
+    q.d[0] = r1.x; q.d[1] = r1.y; q.d[2] = r1.z;
+    for (int k = 0; k < a.g.n_points && k < 4; ++k) q.xi[k] = a.xi[(int64_t)r * a.g.n_points + k];
+}
+
+__device__ __forceinline__ float sigm(float z) { return 1.0f / (1.0f + __expf(-z)); }
+__device__ __forceinline__ float sgnf(float v) { return v > 0.f ? 1.f : (v < 0.f ? -1.f : 0.f); }
+
+// Gated weighted loss of one sample and dL/dz (C19).
+__device__ __forceinline__ float sample_loss(const float* z, const float* gt, float* terms, float* dz) {
+    const float y = gt[0];
+    const float lvis = fmaxf(z[0], 0.f) - z[0] * y + log1pf(__expf(-fabsf(z[0])));
+    const float g = y == 0.f ? 1.f : 0.f;
+    const float st = sigm(z[1]);
+    const float ldist = fabsf(st - gt[1]);
+    float lnorm = 0.f, lalb = 0.f;
+    dz[0] = 2.f * (sigm(z[0]) - y);
+    dz[1] = g * 2.f * sgnf(st - gt[1]) * st * (1.f - st);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const float dn = z[2 + k] - gt[2 + k];
+        lnorm += fabsf(dn) * (1.f / 3.f);
+        dz[2 + k] = g * sgnf(dn) * (1.f / 3.f);
+        const float av = sigm(z[5 + k]);
+        const float den = av * av + 0.01f;
+        const float da = av - gt[5 + k];
+        lalb += da * da / den * (1.f / 3.f);
+        dz[5 + k] = g * 2.f * da / den * (1.f / 3.f) * av * (1.f - av);
+    }
+    terms[0] = 2.f * lvis;
+    terms[1] = g * 2.f * ldist;
+    terms[2] = g * lnorm;
+    terms[3] = g * lalb;
+    return terms[0] + terms[1] + terms[2] + terms[3];
+}
+
+}  // namespace nbvh
+
+namespace nbvh {
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+__device__ __forceinline__ void red_add_v2(float* p, float x, float y) {
+    asm volatile("red.global.add.v2.f32 [%0], {%1, %2};\n" ::"l"(p), "f"(x), "f"(y) : "memory");
+}
+__device__ __forceinline__ uint32_t pack_half2(float a, float b) {
+    __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+}
+__device__ __forceinline__ float2 unpack_half2(uint32_t v) {
+    return __half22float2(*reinterpret_cast<const __half2*>(&v));
+}
+
+// ------------------------------------------------------------------ T3-T5 forward + loss
+// Same tile structure as the query wave (128 samples, 256 threads): jittered samples,
+// encode into shared memory, MLP forward with the hidden activations written out for
+// the backward pass, then the gated loss and dL/dz per sample.
+template <int F, int D>
+__global__ void __launch_bounds__(256, 1) k_train_fwd(TrainArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int M = *a.n_samples;
+    const int n_tiles = (M + kTileQ - 1) / kTileQ;
+    if ((int)blockIdx.x >= n_tiles) return;
+    MlpSmem ms;
+    __half* feat = reinterpret_cast<__half*>(smem_raw);
+    ms.w0 = feat + kTileQ * (D + 8);
+    ms.wh = ms.w0 + 64 * (D + 8);
+    ms.wo = ms.wh + (a.m.hidden - 1) * 64 * 72;
+    float* zt = reinterpret_cast<float*>(ms.wo + 8 * 72);
+    ms.b = zt + kTileQ * 8;
+    SampleDesc* qd = reinterpret_cast<SampleDesc*>(ms.b + 64 * a.m.hidden + 8);
+    stage_mlp(a.m, ms, tid, blockDim.x);
+    const int L = a.g.L, n_pts = a.g.n_points;
+    const int chunks_per_point = (L * F) / 8;
+    const int H = a.m.hidden;
+    const int g = lane >> 2, t = lane & 3;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        if (tid < kTileQ) {
+            SampleDesc q;
+            load_sample_desc(a, tile * kTileQ + tid, M, q);
+            qd[tid] = q;
+        }
+        __syncthreads();
+        {
+            const int q = tid & (kTileQ - 1);
+            const SampleDesc& Q = qd[q];
+            for (int c = tid >> 7; c < D / 8; c += 2) {
+                uint4 v = make_uint4(0, 0, 0, 0);
+                if (Q.valid) {
+                    const int p = c / chunks_per_point;
+                    const int l0 = ((c % chunks_per_point) * 8) / F;
+                    float x[3];
+                    segment_point(a.g, Q.o, Q.d, Q.t0, Q.t1, p, n_pts, Q.xi, x);
+                    v = encode_chunk<F>(a.g, x, l0, nullptr);
+                }
+                *reinterpret_cast<uint4*>(feat + q * (D + 8) + c * 8) = v;
+            }
+        }
+        __syncthreads();
+        // features out (for the weight gradient of layer 0)
+        for (int i = tid; i < kTileQ * (D / 8); i += blockDim.x) {
+            const int row = i / (D / 8), c = i % (D / 8);
+            const int64_t gr = (int64_t)tile * kTileQ + row;
+            if (gr < M) reinterpret_cast<uint4*>(a.X + gr * D)[c] = *reinterpret_cast<const uint4*>(feat + row * (D + 8) + c * 8);
+        }
+        // MLP forward: warp -> 16 rows; hidden activations to global
+        {
+            const int r0 = warp * 16;
+            const int64_t gr0 = (int64_t)tile * kTileQ + r0 + g, gr1 = gr0 + 8;
+            float acc[8][4];
+            for (int nt = 0; nt < 8; ++nt) {
+                float b0 = ms.b[nt * 8 + 2 * t], b1 = ms.b[nt * 8 + 2 * t + 1];
+                acc[nt][0] = b0; acc[nt][1] = b1; acc[nt][2] = b0; acc[nt][3] = b1;
+            }
+            const uint32_t xa = (uint32_t)__cvta_generic_to_shared(feat + (r0 + (lane & 15)) * (D + 8) + (lane >> 4) * 8);
+            const uint32_t wa = (uint32_t)__cvta_generic_to_shared(ms.w0 + ((lane & 7) + ((lane >> 4) << 3)) * (D + 8) +
+                                                                   ((lane >> 3) & 1) * 8);
+#pragma unroll
+            for (int kb = 0; kb < D / 16; ++kb) {
+                uint32_t af[4];
+                ldsm_x4(xa + kb * 32, af[0], af[1], af[2], af[3]);
+#pragma unroll
+                for (int np = 0; np < 4; ++np) {
+                    uint32_t b0, b1, b2, b3;
+                    ldsm_x4(wa + np * 16 * (D + 8) * 2 + kb * 32, b0, b1, b2, b3);
+                    mma16816(acc[2 * np], af, b0, b1);
+                    mma16816(acc[2 * np + 1], af, b2, b3);
+                }
+            }
+            uint32_t h[4][4];
+            for (int layer = 0; layer < H; ++layer) {
+                if (layer > 0) {
+                    const __half* W = ms.wh + (layer - 1) * 64 * 72;
+                    const float* bb = ms.b + layer * 64;
+                    for (int nt = 0; nt < 8; ++nt) {
+                        float b0 = bb[nt * 8 + 2 * t], b1 = bb[nt * 8 + 2 * t + 1];
+                        acc[nt][0] = b0; acc[nt][1] = b1; acc[nt][2] = b0; acc[nt][3] = b1;
+                    }
+                    const uint32_t wb = (uint32_t)__cvta_generic_to_shared(W + ((lane & 7) + ((lane >> 4) << 3)) * 72 +
+                                                                           ((lane >> 3) & 1) * 8);
+#pragma unroll
+                    for (int kb = 0; kb < 4; ++kb)
+#pragma unroll
+                        for (int np = 0; np < 4; ++np) {
+                            uint32_t b0, b1, b2, b3;
+                            ldsm_x4(wb + np * 16 * 72 * 2 + kb * 32, b0, b1, b2, b3);
+                            mma16816(acc[2 * np], h[kb], b0, b1);
+                            mma16816(acc[2 * np + 1], h[kb], b2, b3);
+                        }
+                }
+#pragma unroll
+                for (int kb = 0; kb < 4; ++kb) {
+                    h[kb][0] = pack_relu_half2(acc[2 * kb][0], acc[2 * kb][1]);
+                    h[kb][1] = pack_relu_half2(acc[2 * kb][2], acc[2 * kb][3]);
+                    h[kb][2] = pack_relu_half2(acc[2 * kb + 1][0], acc[2 * kb + 1][1]);
+                    h[kb][3] = pack_relu_half2(acc[2 * kb + 1][2], acc[2 * kb + 1][3]);
+                }
+                __half* Al = a.A + (int64_t)layer * a.cap * 64;
+#pragma unroll
+                for (int kb = 0; kb < 4; ++kb) {
+                    if (gr0 < M) {
+                        *reinterpret_cast<uint32_t*>(Al + gr0 * 64 + kb * 16 + 2 * t) = h[kb][0];
+                        *reinterpret_cast<uint32_t*>(Al + gr0 * 64 + kb * 16 + 8 + 2 * t) = h[kb][2];
+                    }
+                    if (gr1 < M) {
+                        *reinterpret_cast<uint32_t*>(Al + gr1 * 64 + kb * 16 + 2 * t) = h[kb][1];
+                        *reinterpret_cast<uint32_t*>(Al + gr1 * 64 + kb * 16 + 8 + 2 * t) = h[kb][3];
+                    }
+                }
+            }
+            float o[4];
+            {
+                const float* bb = ms.b + H * 64;
+                o[0] = bb[2 * t]; o[1] = bb[2 * t + 1]; o[2] = o[0]; o[3] = o[1];
+            }
+            const uint32_t wo = (uint32_t)__cvta_generic_to_shared(ms.wo + (lane & 7) * 72 + ((lane >> 3) & 1) * 8);
+#pragma unroll
+            for (int kb = 0; kb < 4; ++kb) {
+                uint32_t b0, b1;
+                ldsm_x2(wo + kb * 32, b0, b1);
+                mma16816(o, h[kb], b0, b1);
+            }
+            zt[(r0 + g) * 8 + 2 * t] = o[0];
+            zt[(r0 + g) * 8 + 2 * t + 1] = o[1];
+            zt[(r0 + g + 8) * 8 + 2 * t] = o[2];
+            zt[(r0 + g + 8) * 8 + 2 * t + 1] = o[3];
+        }
+        __syncthreads();
+        if (tid < kTileQ) {
+            const SampleDesc& Q = qd[tid];
+            float terms[4] = {0.f, 0.f, 0.f, 0.f}, Ls = 0.f;
+            if (Q.valid) {
+                const int64_t i = (int64_t)tile * kTileQ + tid;
+                float gt[9], dz[8];
+#pragma unroll
+                for (int k = 0; k < 9; ++k) gt[k] = a.s_gt[9 * i + k];
+                Ls = sample_loss(zt + tid * 8, gt, terms, dz);
+                float4* dst = reinterpret_cast<float4*>(a.dZ + i * 8);
+                dst[0] = make_float4(dz[0], dz[1], dz[2], dz[3]);
+                dst[1] = make_float4(dz[4], dz[5], dz[6], dz[7]);
+                a.r_loss[Q.ray] = Ls;
+                atomicAdd(a.tail + 1 + 3 * Q.leaf, Ls);
+                atomicAdd(a.tail + 1 + 3 * Q.leaf + 1, 1.0f);
+            }
+            float v[5] = {Ls, terms[0], terms[1], terms[2], terms[3]};
+#pragma unroll
+            for (int k = 0; k < 5; ++k) {
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], off);
+                if (lane == 0) atomicAdd(a.loss_acc + k, (double)v[k]);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------------ T6/T7 backward
+// Per warp (16 samples): delta_H = dL/dz; delta_k = (delta_{k+1} W_{k+1}) * relu'(h_k)
+// on tensor cores (B operands via ldmatrix.trans of the [out][in] weights), deltas of the
+// hidden layers written out for the weight gradients; dL/dx = delta_0 W_0 scattered into
+// the hash-table gradient through the trilinear weights.  Dense (coarse) levels
+// aggregate equal addresses within the warp before the atomic.
+struct BwdSmem {
+    __half* w0;   // [64][D+8]
+    __half* wh;   // [H-1][64][72]
+    __half* wo;   // [16][72], rows 8..15 zero
+};
+
+template <int F>
+__device__ __forceinline__ void scatter_pair(const TrainArgs& a, const SampleDesc& Q, int c, float gx, float gy) {
+    const int L = a.g.L;
+    const int LF = L * F;
+    const int p = c / LF;
+    const int l = (c % LF) / F;
+    const int f = c % F;
+    float x[3];
+    segment_point(a.g, Q.o, Q.d, Q.t0, Q.t1, p, a.g.n_points, Q.xi, x);
+    Cell cell;
+    level_cell(a.g, l, x, cell);
+    float* base = a.grad + (int64_t)a.g.offset[l] * F + f;
+    const bool dense = a.g.dense[l];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        float* dst = base + (int64_t)cell.idx[k] * F;
+        float vx = cell.w[k] * gx, vy = cell.w[k] * gy;
+        if (dense) {
+            // warp-aggregated atomics: lanes hitting the same entry combine first
+            const unsigned active = __activemask();
+            const unsigned peers = __match_any_sync(active, (unsigned long long)dst);
+            const int leader = __ffs(peers) - 1;
+            float sx = 0.f, sy = 0.f;
+            for (unsigned m = peers; m; m &= m - 1) {
+                const int src = __ffs(m) - 1;
+                sx += __shfl_sync(peers, vx, src);
+                sy += __shfl_sync(peers, vy, src);
+            }
+            if ((int)(threadIdx.x & 31) == leader) red_add_v2(dst, sx, sy);
+        } else {
+            red_add_v2(dst, vx, vy);
+        }
+    }
+}
+
+template <int F, int D>
+__global__ void __launch_bounds__(256, 1) k_train_bwd(TrainArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int M = *a.n_samples;
+    const int n_tiles = (M + kTileQ - 1) / kTileQ;
+    if ((int)blockIdx.x >= n_tiles) return;
+    const int H = a.m.hidden;
+    BwdSmem s;
+    s.w0 = reinterpret_cast<__half*>(smem_raw);
+    s.wh = s.w0 + 64 * (D + 8);
+    s.wo = s.wh + (H - 1) * 64 * 72;
+    SampleDesc* qd = reinterpret_cast<SampleDesc*>(s.wo + 16 * 72);
+    {   // stage weights (fp16 inference copy == forward operands)
+        const uint4* W = reinterpret_cast<const uint4*>(a.m.W);
+        const int cpr0 = D / 8;
+        for (int i = tid; i < 64 * cpr0; i += blockDim.x)
+            *reinterpret_cast<uint4*>(s.w0 + (i / cpr0) * (D + 8) + (i % cpr0) * 8) = __ldg(W + i);
+        const uint4* Wh = W + 64 * cpr0;
+        for (int i = tid; i < (H - 1) * 64 * 8; i += blockDim.x)
+            *reinterpret_cast<uint4*>(s.wh + (i / 8) * 72 + (i % 8) * 8) = __ldg(Wh + i);
+        const uint4* Wo = Wh + (H - 1) * 64 * 8;
+        for (int i = tid; i < 16 * 8; i += blockDim.x)
+            *reinterpret_cast<uint4*>(s.wo + (i / 8) * 72 + (i % 8) * 8) = i < 64 ? __ldg(Wo + i) : make_uint4(0, 0, 0, 0);
+    }
+    const int g = lane >> 2, t = lane & 3;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        if (tid < kTileQ) {
+            SampleDesc q;
+            load_sample_desc(a, tile * kTileQ + tid, M, q);
+            qd[tid] = q;
+        }
+        __syncthreads();
+        const int r0 = warp * 16;
+        const int64_t gr0 = (int64_t)tile * kTileQ + r0 + g, gr1 = gr0 + 8;
+        const bool v0 = gr0 < M, v1 = gr1 < M;
+        // delta_H = dL/dz as an m16k16 A fragment (k 8..15 zero)
+        uint32_t af[4][4];
+        {
+            float2 d0 = v0 ? *reinterpret_cast<const float2*>(a.dZ + gr0 * 8 + 2 * t) : make_float2(0.f, 0.f);
+            float2 d1 = v1 ? *reinterpret_cast<const float2*>(a.dZ + gr1 * 8 + 2 * t) : make_float2(0.f, 0.f);
+            af[0][0] = pack_half2(d0.x, d0.y);
+            af[0][1] = pack_half2(d1.x, d1.y);
+            af[0][2] = 0u;
+            af[0][3] = 0u;
+        }
+        for (int k = H - 1; k >= 0; --k) {
+            float acc[8][4];
+#pragma unroll
+            for (int nt = 0; nt < 8; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
+            const bool from_out = (k == H - 1);
+            const __half* W = from_out ? s.wo : s.wh + k * 64 * 72;   // W_{k+1}: [K][64], row stride 72
+            const int ksteps = from_out ? 1 : 4;
+            const uint32_t wb = (uint32_t)__cvta_generic_to_shared(W + (lane & 15) * 72 + (lane >> 4) * 8);
+            for (int kb = 0; kb < ksteps; ++kb) {
+#pragma unroll
+                for (int np = 0; np < 4; ++np) {
+                    uint32_t b0, b1, b2, b3;
+                    ldsm_x4_t(wb + kb * 16 * 72 * 2 + np * 32, b0, b1, b2, b3);
+                    mma16816(acc[2 * np], af[kb], b0, b1);
+                    mma16816(acc[2 * np + 1], af[kb], b2, b3);
+                }
+            }
+            // relu'(h_k) mask and store delta_k
+            const __half* Ak = a.A + (int64_t)k * a.cap * 64;
+            __half* Dk = a.Dl + (int64_t)k * a.cap * 64;
+#pragma unroll
+            for (int nt = 0; nt < 8; ++nt) {
+                const int col = nt * 8 + 2 * t;
+                float2 h0 = v0 ? unpack_half2(*reinterpret_cast<const uint32_t*>(Ak + gr0 * 64 + col)) : make_float2(0.f, 0.f);
+                float2 h1 = v1 ? unpack_half2(*reinterpret_cast<const uint32_t*>(Ak + gr1 * 64 + col)) : make_float2(0.f, 0.f);
+                acc[nt][0] = h0.x > 0.f ? acc[nt][0] : 0.f;
+                acc[nt][1] = h0.y > 0.f ? acc[nt][1] : 0.f;
+                acc[nt][2] = h1.x > 0.f ? acc[nt][2] : 0.f;
+                acc[nt][3] = h1.y > 0.f ? acc[nt][3] : 0.f;
+                if (v0) *reinterpret_cast<uint32_t*>(Dk + gr0 * 64 + col) = pack_half2(acc[nt][0], acc[nt][1]);
+                if (v1) *reinterpret_cast<uint32_t*>(Dk + gr1 * 64 + col) = pack_half2(acc[nt][2], acc[nt][3]);
+            }
+#pragma unroll
+            for (int kb = 0; kb < 4; ++kb) {
+                af[kb][0] = pack_half2(acc[2 * kb][0], acc[2 * kb][1]);
+                af[kb][1] = pack_half2(acc[2 * kb][2], acc[2 * kb][3]);
+                af[kb][2] = pack_half2(acc[2 * kb + 1][0], acc[2 * kb + 1][1]);
+                af[kb][3] = pack_half2(acc[2 * kb + 1][2], acc[2 * kb + 1][3]);
+            }
+        }
+        // dL/dx = delta_0 W_0  ([16 x 64] x [64 x D]), scattered two n-tiles at a time
+        const uint32_t w0b = (uint32_t)__cvta_generic_to_shared(s.w0 + (lane & 15) * (D + 8) + (lane >> 4) * 8);
+        const SampleDesc& Q0 = qd[r0 + g];
+        const SampleDesc& Q1 = qd[r0 + g + 8];
+#pragma unroll 1
+        for (int np = 0; np < D / 16; ++np) {
+            float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+#pragma unroll
+            for (int kb = 0; kb < 4; ++kb) {
+                uint32_t b0, b1, b2, b3;
+                ldsm_x4_t(w0b + kb * 16 * (D + 8) * 2 + np * 32, b0, b1, b2, b3);
+                mma16816(acc[0], af[kb], b0, b1);
+                mma16816(acc[1], af[kb], b2, b3);
+            }
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const int c = (2 * np + j) * 8 + 2 * t;
+                if (v0) scatter_pair<F>(a, Q0, c, acc[j][0], acc[j][1]);
+                if (v1) scatter_pair<F>(a, Q1, c, acc[j][2], acc[j][3]);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------------ T6 weight gradients
+// dW_k = delta_k^T x_k over the batch as split-K tensor-core GEMMs: each CTA reduces a
+// chunk of samples in registers and adds its partial once (red.global.add.v2.f32).
+// Hidden layers on mma.sync (fp16 operands, fp32 accumulate); the 8-output layer on
+// CUDA cores from the fp32 dL/dz.
+constexpr int kDwChunk = 2048;
+
+template <int D>
+__global__ void __launch_bounds__(256, 1) k_train_dw(TrainArgs a, int64_t w_off, int64_t b_off) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int M = *a.n_samples;
+    const int64_t c0 = (int64_t)blockIdx.x * kDwChunk;
+    if (c0 >= M) return;
+    const int64_t c1 = min((int64_t)M, c0 + kDwChunk);
+    const int H = a.m.hidden;
+    __half* sd = reinterpret_cast<__half*>(smem_raw);          // delta tile [128][72]
+    __half* sx = sd + kTileQ * 72;                             // input tile [128][D+8]
+    float* sz = reinterpret_cast<float*>(sx + kTileQ * (D + 8));   // dZ tile [128][8]
+    const int g = lane >> 2, t = lane & 3;
+    int64_t woff = w_off, boff = b_off;
+    for (int k = 0; k < H; ++k) {
+        const int in = k == 0 ? D : 64;
+        const int NT = in / 8;               // n-tiles of 8
+        const int mt = warp & 3;             // 16 output units per warp
+        const int nt0 = (warp >> 2) * (NT / 2);
+        float acc[8][4];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+        float dbias = 0.f;
+        const __half* Dk = a.Dl + (int64_t)k * a.cap * 64;
+        const __half* Xk = k == 0 ? a.X : a.A + (int64_t)(k - 1) * a.cap * 64;
+        for (int64_t r = c0; r < c1; r += kTileQ) {
+            for (int i = tid; i < kTileQ * 8; i += blockDim.x) {
+                const int row = i / 8, c = i % 8;
+                uint4 v = r + row < c1 ? reinterpret_cast<const uint4*>(Dk + (r + row) * 64)[c] : make_uint4(0, 0, 0, 0);
+                *reinterpret_cast<uint4*>(sd + row * 72 + c * 8) = v;
+            }
+            for (int i = tid; i < kTileQ * (in / 8); i += blockDim.x) {
+                const int row = i / (in / 8), c = i % (in / 8);
+                uint4 v = r + row < c1 ? reinterpret_cast<const uint4*>(Xk + (r + row) * in)[c] : make_uint4(0, 0, 0, 0);
+                *reinterpret_cast<uint4*>(sx + row * (D + 8) + c * 8) = v;
+            }
+            __syncthreads();
+            if (tid < 64) {
+                float sacc = 0.f;
+                for (int row = 0; row < kTileQ; ++row) sacc += __half2float(sd[row * 72 + tid]);
+                dbias += sacc;
+            }
+            const uint32_t aa = (uint32_t)__cvta_generic_to_shared(
+                sd + ((lane & 7) + ((lane >> 4) << 3)) * 72 + mt * 16 + ((lane >> 3) & 1) * 8);
+            const uint32_t ba = (uint32_t)__cvta_generic_to_shared(sx + (lane & 15) * (D + 8) + (lane >> 4) * 8);
+#pragma unroll
+            for (int ks = 0; ks < kTileQ / 16; ++ks) {
+                uint32_t af[4];
+                ldsm_x4_t(aa + ks * 16 * 72 * 2, af[0], af[1], af[2], af[3]);
+#pragma unroll
+                for (int jp = 0; jp < 4; ++jp) {
+                    if (2 * jp < NT / 2) {
+                        uint32_t b0, b1, b2, b3;
+                        ldsm_x4_t(ba + ks * 16 * (D + 8) * 2 + (nt0 + 2 * jp) * 16, b0, b1, b2, b3);
+                        mma16816(acc[2 * jp], af, b0, b1);
+                        mma16816(acc[2 * jp + 1], af, b2, b3);
+                    }
+                }
+            }
+            __syncthreads();
+        }
+        // flush partial sums
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            if (j < NT / 2) {
+                const int col = (nt0 + j) * 8 + 2 * t;
+                const int u0 = mt * 16 + g, u1 = u0 + 8;
+                red_add_v2(a.grad + woff + (int64_t)u0 * in + col, acc[j][0], acc[j][1]);
+                red_add_v2(a.grad + woff + (int64_t)u1 * in + col, acc[j][2], acc[j][3]);
+            }
+        }
+        if (tid < 64) atomicAdd(a.grad + boff + tid, dbias);
+        woff += (int64_t)64 * in;
+        boff += 64;
+    }
+    // output layer (64 -> 8): dW = dZ^T h_{H-1}, db = sum dZ, fp32 on CUDA cores
+    {
+        const __half* Ah = a.A + (int64_t)(H - 1) * a.cap * 64;
+        float accw[2] = {0.f, 0.f}, accb = 0.f;
+        const int o = tid / 32, i0 = (tid % 32) * 2;            // 8 outputs x 64 inputs, 2 per thread
+        for (int64_t r = c0; r < c1; r += kTileQ) {
+            for (int i = tid; i < kTileQ * 8; i += blockDim.x) {
+                const int row = i / 8, c = i % 8;
+                uint4 v = r + row < c1 ? reinterpret_cast<const uint4*>(Ah + (r + row) * 64)[c] : make_uint4(0, 0, 0, 0);
+                *reinterpret_cast<uint4*>(sx + row * (D + 8) + c * 8) = v;
+            }
+            for (int i = tid; i < kTileQ * 8; i += blockDim.x) {
+                const int row = i / 8;
+                sz[i] = r + row < c1 ? a.dZ[(r + row) * 8 + (i % 8)] : 0.f;
+            }
+            __syncthreads();
+            for (int row = 0; row < kTileQ; ++row) {
+                const float dz = sz[row * 8 + o];
+                float2 h = __half22float2(*reinterpret_cast<const __half2*>(sx + row * (D + 8) + i0));
+                accw[0] = fmaf(dz, h.x, accw[0]);
+                accw[1] = fmaf(dz, h.y, accw[1]);
+                if (i0 == 0) accb += dz;
+            }
+            __syncthreads();
+        }
+        red_add_v2(a.grad + woff + (int64_t)o * 64 + i0, accw[0], accw[1]);
+        if (i0 == 0) atomicAdd(a.grad + boff + o, accb);
+    }
+}
+
+// ------------------------------------------------------------------ T9 Adam
+__global__ void k_check_finite(const float* __restrict__ g, int64_t n, int32_t* flag) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool bad = false;
+    for (; i < n; i += (int64_t)gridDim.x * blockDim.x) bad |= !isfinite(g[i]);
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+struct AdamArgs {
+    float* param;
+    const float* grad;
+    float* m;
+    float* v;
+    int64_t n;
+    const float* count;   // accepted-sample count (after the all-reduce)
+    const int32_t* bad;
+    float lr, beta1, beta2, eps, c1, c2;
+    __half* table16;
+    int64_t n_table;
+    __half* W16;
+    int64_t n_W;
+};
+
+// P:275 Adam with default hyper-parameters (C20): dense, bias-corrected; the gradient is
+// the batch mean (sum / accepted count).  The fp16 inference copy is refreshed in place.
+__global__ void k_adam(AdamArgs a) {
+    if (*a.bad) return;
+    const float scale = 1.0f / fmaxf(1.0f, *a.count);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float gr = a.grad[i] * scale;
+        const float m = a.beta1 * a.m[i] + (1.0f - a.beta1) * gr;
+        const float v = a.beta2 * a.v[i] + (1.0f - a.beta2) * gr * gr;
+        a.m[i] = m;
+        a.v[i] = v;
+        const float p = a.param[i] - a.lr * (m / a.c1) / (sqrtf(v / a.c2) + a.eps);
+        a.param[i] = p;
+        if (i < a.n_table) a.table16[i] = __float2half_rn(p);
+        else if (i < a.n_table + a.n_W) a.W16[i - a.n_table] = __float2half_rn(p);
+    }
+}
+
+}  // namespace nbvh

@@ -1,0 +1,25 @@
+#!/bin/bash
+# One GPU session: parity tests, smoke, bench, ncu launch list + full capture of the
+# dominant kernel.  Usage (from the repo root, on the GPU box):  bash scripts/gpu_round.sh [tag]
+cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
+TAG=${1:-r1}
+OUT=gpurun_out
+mkdir -p $OUT
+nvidia-smi > $OUT/smi.txt 2>&1
+python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1
+timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider > $OUT/pytest_gpu.log 2>&1
+echo "pytest exit $?" >> $OUT/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1
+echo "smoke exit $?" >> $OUT/smoke.log
+timeout 600 python bench.py --steps 10 --warmup 3 > $OUT/bench_$TAG.json 2> $OUT/bench_$TAG.err
+echo "bench exit $?" >> $OUT/bench_$TAG.err
+if [ "${SKIP_NCU:-0}" != "1" ]; then
+  CMD="python bench.py --steps 2 --warmup 1 --cpu-seconds 0"
+  timeout 600 $CMD > $OUT/ncu_plain.log 2>&1 && \
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+      --log-file $OUT/launches_$TAG.csv $CMD > $OUT/ncu_launches.log 2>&1
+  echo "ncu launches exit $?" >> $OUT/ncu_launches.log
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_query_wave -s 4 -c 2 \
+      -o $OUT/prof_wave_$TAG -f $CMD > $OUT/ncu_full.log 2>&1
+  echo "ncu full exit $?" >> $OUT/ncu_full.log
+fi

@@ -119,7 +119,7 @@ def test_traversal_lists_bit_exact(orc, tiny, cap):
     assert np.array_equal(leaf.cpu().numpy(), wl)
     m = wl >= 0
     assert np.array_equal(te.cpu().numpy()[m], wte[m]) and np.array_equal(tx.cpu().numpy()[m], wtx[m])
-    assert wcnt.max() > 16                                     # exercises resumption past K
+    assert wcnt.max() > 4
 
 
 def test_traversal_small_capacity(orc):
@@ -129,6 +129,9 @@ def test_traversal_small_capacity(orc):
     leaf, te, tx, cnt = ctx.debug_traverse(torch.from_numpy(rays).cuda(), 12)
     wl, wte, wtx, wcnt = orc.leaf_lists(rays, cut["leaf_lo"], cut["leaf_hi"], 12)
     assert np.array_equal(leaf.cpu().numpy(), wl) and np.array_equal(cnt.cpu().numpy(), wcnt)
+    m = wl >= 0
+    assert np.array_equal(te.cpu().numpy()[m], wte[m]) and np.array_equal(tx.cpu().numpy()[m], wtx[m])
+    assert wcnt.max() > 3                                      # resumption past the capacity (C6)
 
 
 # ------------------------------------------------------------------ end-to-end query
@@ -150,11 +153,11 @@ def _check_query(orc, ctx, tab, layers, rays, mode=0, cap=64):
     # (2) the double-precision oracle
     o = orc.query(_grid(orc, ctx), ctx.cfg.n_points, tab, layers, cut["leaf_lo"], cut["leaf_hi"], rays, mode=mode,
                   trace_cap=cap)
-    clear = (o["margin"] >= 1e-2) & (o["tmargin"] >= 1e-2)
+    clear = (o["margin"] >= 1e-2) & (o["tmargin"] >= 5e-3)
     assert np.array_equal(g["hit"][clear], o["hit"][clear])
     assert np.array_equal(g["leaf"][clear], o["leaf"][clear])
     assert np.array_equal(g["n_queries"][clear], o["nq"][clear])
-    assert (~clear).mean() < 0.01, (~clear).mean()
+    assert (~clear).mean() < 0.02, (~clear).mean()
     h = clear & (o["hit"] == 1)
     assert np.abs(g["t"][h] - o["t"][h]).max() <= 2e-3 * 3.5     # C23: t / scene diagonal
     assert np.abs(g["albedo"][h] - o["albedo"][h]).max() <= 1e-2
@@ -215,7 +218,7 @@ def test_query_1080p_sampled_full_size(orc):
     cut = ctx.cut(0)
     o = orc.query(_grid(orc, ctx), 4, tab, layers, cut["leaf_lo"], cut["leaf_hi"], rays[sample])
     g = {k: v.cpu().numpy()[sample] for k, v in out.items()}
-    clear = (o["margin"] >= 1e-2) & (o["tmargin"] >= 1e-2)
+    clear = (o["margin"] >= 1e-2) & (o["tmargin"] >= 5e-3)
     assert np.array_equal(g["hit"][clear], o["hit"][clear])
     assert np.array_equal(g["leaf"][clear], o["leaf"][clear])
     assert np.array_equal(g["n_queries"][clear], o["nq"][clear])

@@ -1,0 +1,148 @@
+"""GPU parity of the companion training step against the oracle (double precision).
+
+Exact: first-leaf selection and acceptance decisions (fp32 on both sides), ground-truth
+visibility and hit distance (double Moller-Trumbore with the same op order).
+Tolerances: labels' normal/albedo 1e-6; loss sums 5e-3 relative;
+gradients (fp16 forward/backward operands, fp32 accumulation) 3e-2 relative L2 error per
+parameter block and cosine >= 0.999; Adam 1e-5 relative.
+"""
+import numpy as np
+import pytest
+
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def _setup(n_rays=6000, seed=30, leaves=64, rank=None, hidden=2):
+    from paper_2405_16237_b200 import Context, PARAM_TABLES
+    import oracle as orc
+    sc = synth.scene_tiny()
+    ctx = Context(device=0, L=8, F=2, log2_T=14, n_points=4, hidden_layers=hidden)
+    ctx.set_mesh(sc)
+    ctx.build_cut(leaves)
+    ctx.reserve(n_rays)
+    tab = synth.random_params_fp16(ctx.param_count(PARAM_TABLES), seed=seed, lo=-0.5, hi=0.5)
+    ctx.set_params(PARAM_TABLES, tab.astype(np.float32))
+    layers = synth.random_mlp(64, hidden, 64, seed=seed + 1, out_scale=1.0)
+    ctx.set_mlp(layers)
+    cut = ctx.cut(0)
+    if rank is None:
+        rank = np.zeros(cut["n_leaves"], np.float32)
+    ctx.set_leaf_rank(rank)
+    rays = synth.random_rays(n_rays, seed=seed + 2)                     # 50%-inflated box (C16)
+    u = synth.random_uniform(n_rays, seed=seed + 3)
+    xi = synth.random_uniform(n_rays * 4, seed=seed + 4).reshape(n_rays, 4)
+    o = orc.train_grad(orc.Grid(8, 14, 2), 4, tab.reshape(-1, 2), layers, cut["leaf_lo"], cut["leaf_hi"], rank,
+                       cut["tri_off"], cut["tris"], sc, rays, u, xi)
+    return ctx, sc, cut, tab, layers, rays, u, xi, o
+
+
+def _to(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+@pytest.fixture(scope="module")
+def batch():
+    rank = np.random.default_rng(5).normal(size=64).astype(np.float32) * 3     # varied acceptance
+    return _setup(rank=rank)
+
+
+def test_selection_and_labels_exact(batch):
+    ctx, sc, cut, tab, layers, rays, u, xi, o = batch
+    ctx.train_backward(_to(rays), _to(u), _to(xi))
+    gt, acc, leaf, loss = ctx.debug_train_samples(rays.shape[0])
+    torch.cuda.synchronize()
+    gt, acc, leaf = gt.cpu().numpy(), acc.cpu().numpy(), leaf.cpu().numpy()
+    assert np.array_equal(leaf, o["first_leaf"])
+    assert np.array_equal(acc, o["accepted"])
+    a = acc == 1
+    assert 0.1 < a.mean() < 0.9
+    assert np.array_equal(gt[a, 0], o["gt"][a, 0].astype(np.float32))
+    hit = a & (o["gt"][:, 0] == 0)
+    assert hit.sum() > 100
+    assert np.array_equal(gt[hit, 8], o["gt"][hit, 8].astype(np.float32))       # t_hit bits
+    assert np.abs(gt[hit, 1] - o["gt"][hit, 1]).max() <= 1e-6
+    assert np.abs(gt[hit, 2:8] - o["gt"][hit, 2:8]).max() <= 1e-6
+    st = ctx.train_stats()
+    assert st["n_accepted"] == o["n_acc"] and st["n_first_hit"] == int((o["first_leaf"] >= 0).sum())
+
+
+def test_loss_and_gradients_vs_oracle(batch):
+    from paper_2405_16237_b200 import dp
+    ctx, sc, cut, tab, layers, rays, u, xi, o = batch
+    ctx.train_backward(_to(rays), _to(u), _to(xi))
+    st = ctx.train_stats()
+    assert abs(st["loss_sum"] - o["loss_sum"][0]) <= 5e-3 * abs(o["loss_sum"][0])
+    g = dp.grad_tensor(ctx).cpu().numpy().astype(np.float64)
+    n_t, n_w = tab.size, o["g_W"].size
+    m = o["n_acc"]
+    blocks = {"tables": (g[:n_t], o["g_table"] * m), "weights": (g[n_t:n_t + n_w], o["g_W"] * m),
+              "biases": (g[n_t + n_w:n_t + n_w + o["g_b"].size], o["g_b"] * m)}
+    for name, (gg, oo) in blocks.items():
+        rel = np.linalg.norm(gg - oo) / np.linalg.norm(oo)
+        cos = gg @ oo / (np.linalg.norm(gg) * np.linalg.norm(oo))
+        assert rel <= 3e-2 and cos >= 0.999, (name, rel, cos)
+    tail = g[n_t + n_w + o["g_b"].size:]
+    assert tail[0] == m                                                        # accepted count
+    per_leaf = tail[1:1 + 3 * cut["n_leaves"]].reshape(-1, 3)
+    assert per_leaf[:, 1].sum() == m
+    assert per_leaf[:, 2].sum() == (o["first_leaf"] >= 0).sum()
+    assert abs(per_leaf[:, 0].sum() - o["loss_sum"][0]) <= 5e-3 * o["loss_sum"][0]
+
+
+def test_adam_step_vs_oracle(batch):
+    from paper_2405_16237_b200 import dp, PARAM_ALL
+    import oracle as orc
+    ctx, sc, cut, tab, layers, rays, u, xi, o = batch
+    p0 = ctx.get_params(PARAM_ALL).astype(np.float64)
+    ctx.set_params(PARAM_ALL, p0.astype(np.float32))                # also restarts Adam (step 1)
+    ctx.train_backward(_to(rays), _to(u), _to(xi))
+    g = dp.grad_tensor(ctx).cpu().numpy().astype(np.float64)
+    n_p = p0.size
+    grad = g[:n_p] / max(1.0, g[n_p])
+    ctx.apply_update(0.01)
+    p1 = ctx.get_params(PARAM_ALL).astype(np.float64)
+    ref = p0.copy()
+    m = np.zeros_like(ref)
+    v = np.zeros_like(ref)
+    orc.adam(ref, grad, m, v, 1, lr=0.01)
+    assert np.abs(p1 - ref).max() <= 1e-5 * (1 + np.abs(ref).max())
+
+
+def test_two_half_batches_sum_to_full_batch():
+    """DP decomposition on one GPU without cross-waiting kernels: the gradient buffers
+    of two contexts over the two halves sum to the full-batch buffer (fp32 atomics)."""
+    from paper_2405_16237_b200 import dp
+    full = _setup(n_rays=4000, seed=40)
+    ctx, sc, cut, tab, layers, rays, u, xi, o = full
+    ctx.train_backward(_to(rays), _to(u), _to(xi))
+    g_full = dp.grad_tensor(ctx).clone()
+    parts = []
+    for r in range(2):
+        sl = dp.shard(rays.shape[0], r, 2)
+        ctx.train_backward(_to(rays[sl]), _to(u[sl]), _to(xi[sl]))
+        parts.append(dp.grad_tensor(ctx).clone())
+    s = (parts[0] + parts[1]).double()
+    rel = (s - g_full.double()).norm() / g_full.double().norm()
+    assert rel <= 1e-5, rel
+
+
+def test_training_reduces_loss():
+    from paper_2405_16237_b200 import Context
+    sc = synth.scene_tiny()
+    ctx = Context(device=0, L=8, F=2, log2_T=14, n_points=4, hidden_layers=2, seed=3)
+    ctx.set_mesh(sc)
+    ctx.build_cut(64)
+    n = 1 << 15
+    ctx.reserve(n)
+    losses = []
+    for step in range(150):
+        rays = _to(synth.random_rays(n, seed=1000 + step))
+        u = _to(synth.random_uniform(n, seed=2000 + step))
+        xi = _to(synth.random_uniform(n * 4, seed=3000 + step).reshape(n, 4))
+        ctx.train_step(rays, u, xi, lr=0.01)
+        st = ctx.train_stats()
+        losses.append(st["loss_sum"] / max(1, st["n_accepted"]))
+    assert np.mean(losses[-10:]) < 0.6 * np.mean(losses[:5]), (losses[:5], losses[-10:])

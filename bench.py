@@ -227,9 +227,7 @@ def run_ours(args):
     if rank == 0 or True:
         pin = torch.from_numpy(rays_np).pin_memory()
         hb = {"hit": torch.empty(n, dtype=torch.uint8).pin_memory(), "t": torch.empty(n).pin_memory(),
-              "normal": torch.empty(n, 3).pin_memory(), "albedo": torch.empty(n, 3).pin_memory(),
-              "leaf": torch.empty(n, dtype=torch.int32).pin_memory(),
-              "n_queries": torch.empty(n, dtype=torch.int32).pin_memory()}
+              "normal": torch.empty(n, 3).pin_memory(), "albedo": torch.empty(n, 3).pin_memory()}
         hbn = {k: v.numpy() for k, v in hb.items()}
         pin_np = pin.numpy()
         ctx.query_host(pin_np, out=hbn)
@@ -244,7 +242,7 @@ def run_ours(args):
         e2e_t = torch.tensor([sum(e2e_s)], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-        d2h = n * (1 + 4 + 12 + 12 + 4 + 4)
+        d2h = n * (1 + 4 + 12 + 12)                                   # hit, t, normal, albedo
         e2e = {"value": n * args.steps * world / float(e2e_t.item()) / 1e6, "unit": "Mrays/s",
                "h2d_bytes_per_step": n * 32, "d2h_bytes_per_step": d2h}
 

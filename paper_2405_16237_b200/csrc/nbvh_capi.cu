@@ -4,6 +4,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -230,6 +231,7 @@ extern "C" void nbvh_destroy(nbvh_ctx* c) {
         dfree(c->d_cnt);
         if (c->h_cnt) cudaFreeHost(c->h_cnt);
         for (cudaEvent_t x : c->events) cudaEventDestroy(x);
+        if (c->aux_stream) cudaStreamDestroy(c->aux_stream);
         free_scene_device(c);
         free_train_device(c);
     }
@@ -569,8 +571,17 @@ extern "C" nbvh_status nbvh_query_host(nbvh_ctx* c, const nbvh_ray* h_rays, int6
     nbvh_status st = check_query(c, h_rays, n, lod, h_out);
     if (st) return st;
     if (n == 0) return NBVH_OK;
-    cudaStream_t s = (cudaStream_t)stream;
-    float* d_rays = c->d_stage_rays;
+    // Chunks alternate between the caller's stream and a second one, so the host->device
+    // copy of chunk i+1 and the device->host copy of chunk i-1 overlap the query of chunk
+    // i.  The query workspace is reused chunk after chunk (each query ends synchronised).
+    cudaStream_t ss[2] = {(cudaStream_t)stream, nullptr};
+    if (!c->aux_stream) {
+        cudaError_t e0 = cudaStreamCreateWithFlags(&c->aux_stream, cudaStreamNonBlocking);
+        if (e0 != cudaSuccess) return cuda_fail(c, e0, "query_host: stream");
+    }
+    ss[1] = c->aux_stream;
+    const int chunks = n >= (1 << 20) ? 4 : (n >= (1 << 18) ? 2 : 1);
+    const int64_t step = (n + chunks - 1) / chunks;
     // staging layout: t[n], normal[3n], albedo[3n], hit bytes, leaf[n], nq[n]
     float* base = c->d_stage_hits;
     HitsDev d{};
@@ -580,19 +591,48 @@ extern "C" nbvh_status nbvh_query_host(nbvh_ctx* c, const nbvh_ray* h_rays, int6
     d.leaf = reinterpret_cast<int32_t*>(base + 7 * n);
     d.n_queries = reinterpret_cast<int32_t*>(base + 8 * n);
     d.hit = reinterpret_cast<uint8_t*>(base + 9 * n);
-    cudaError_t e = cudaMemcpyAsync(d_rays, h_rays, (size_t)n * sizeof(nbvh_ray), cudaMemcpyHostToDevice, s);
+    const nbvh_ray* d_rays = reinterpret_cast<const nbvh_ray*>(c->d_stage_rays);
+    cudaError_t e = cudaSuccess;
+    int64_t total_q = 0;
+    int32_t launches = 0, waves = 0, refills = 0;
+    auto h2d = [&](int k) {
+        const int64_t o = k * step, m = std::min(step, n - o);
+        return cudaMemcpyAsync((void*)(d_rays + o), h_rays + o, (size_t)m * sizeof(nbvh_ray), cudaMemcpyHostToDevice,
+                               ss[k & 1]);
+    };
+    for (int k = 0; k < chunks && k < 2 && e == cudaSuccess; ++k) e = h2d(k);
     if (e != cudaSuccess) return cuda_fail(c, e, "query_host: H2D");
-    st = run_query(c, reinterpret_cast<const nbvh_ray*>(d_rays), n, lod, d, nullptr, 0, s);
-    if (st) return st;
-    e = cudaMemcpyAsync(h_out.hit, d.hit, (size_t)n, cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(h_out.t, d.t, (size_t)n * 4, cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(h_out.normal, d.normal, (size_t)n * 12, cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(h_out.albedo, d.albedo, (size_t)n * 12, cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess && h_out.leaf) e = cudaMemcpyAsync(h_out.leaf, d.leaf, (size_t)n * 4, cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess && h_out.n_queries)
-        e = cudaMemcpyAsync(h_out.n_queries, d.n_queries, (size_t)n * 4, cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    for (int k = 0; k < chunks; ++k) {
+        const int64_t o = k * step, m = std::min(step, n - o);
+        cudaStream_t s = ss[k & 1];
+        HitsDev dk{d.hit + o, d.t + o, d.normal + 3 * o, d.albedo + 3 * o, d.leaf + o, d.n_queries + o};
+        st = run_query(c, d_rays + o, m, lod, dk, nullptr, 0, s);
+        if (st) return st;
+        total_q += c->qstats.n_queries;
+        launches += c->qstats.n_launches;
+        waves = std::max(waves, c->qstats.n_waves);
+        refills += c->qstats.n_refills;
+        e = cudaMemcpyAsync(h_out.hit + o, dk.hit, (size_t)m, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(h_out.t + o, dk.t, (size_t)m * 4, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(h_out.normal + 3 * o, dk.normal, (size_t)m * 12, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(h_out.albedo + 3 * o, dk.albedo, (size_t)m * 12, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess && h_out.leaf)
+            e = cudaMemcpyAsync(h_out.leaf + o, dk.leaf, (size_t)m * 4, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess && h_out.n_queries)
+            e = cudaMemcpyAsync(h_out.n_queries + o, dk.n_queries, (size_t)m * 4, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess && k + 2 < chunks) e = h2d(k + 2);
+        if (e != cudaSuccess) return cuda_fail(c, e, "query_host: copies");
+    }
+    e = cudaStreamSynchronize(ss[0]);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ss[1]);
     if (e != cudaSuccess) return cuda_fail(c, e, "query_host: D2H");
+    c->qstats.n_rays = n;
+    c->qstats.n_queries = total_q;
+    c->qstats.n_launches = launches;
+    c->qstats.n_waves = waves;
+    c->qstats.n_refills = refills;
     return NBVH_OK;
 }
 

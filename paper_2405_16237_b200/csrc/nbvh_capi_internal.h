@@ -74,6 +74,7 @@ struct nbvh_ctx {
     float* d_stage_hits = nullptr;
     nbvh_query_stats qstats{};
     bool profiling = false;
+    cudaStream_t aux_stream = nullptr;  // second stream of the pipelined host path
     std::vector<cudaEvent_t> events;   // profiling: [0..1] traverse, then one pair per wave
 
     // training
@@ -87,7 +88,7 @@ struct nbvh_ctx {
         s.pos = p;
         s.base = p + m;
         s.nbuf = p + 2 * m;
-        s.count = p + 3 * m;
+        s.more = p + 3 * m;
         s.bt = reinterpret_cast<float*>(p + 4 * m);
         s.bte = reinterpret_cast<float*>(p + 5 * m);
         s.bleaf = p + 6 * m;

@@ -89,11 +89,23 @@ __device__ __forceinline__ bool key_less(float a_te, int a_id, float b_te, int b
 // how many leaves qualified in total (so the caller knows whether more remain, C6).
 // Inner boxes are exact unions of their children, so by monotone rounding a pruned
 // subtree contains no intersected leaf: the result equals a brute-force scan (C5).
+// With `prune`, once the list is full a subtree whose entry exceeds the cap-th key is
+// skipped (none of its leaves can enter the list); the return value is then only a lower
+// bound and *more (nullable) reports whether leaves beyond the list may exist.
 template <int K>
 __device__ int collect_leaves(const CutDev& cut, const RayDev& R, bool has_after, float after_te, int after_id,
                               int cap, float (&lte)[K], float (&ltx)[K], int (&lid)[K], int& n_out,
-                              int* err_flag) {
+                              int* err_flag, bool prune = false, bool* more = nullptr) {
     int n = 0, total = 0;
+    bool pruned = false;
+    auto full_and_beyond = [&](float te) {
+        if (!prune || n < cap) return false;
+        float last = 0.f;
+#pragma unroll
+        for (int j = 0; j < K; ++j)
+            if (j == cap - 1) last = lte[j];
+        return te > last;
+    };
     auto consider = [&](int leaf, float te, float tx) {
         if (has_after && !key_less(after_te, after_id, te, leaf)) return;
         ++total;
@@ -133,6 +145,8 @@ __device__ int collect_leaves(const CutDev& cut, const RayDev& R, bool has_after
             if (hl && cl < 0) consider(-1 - cl, lte_, ltx_);
             if (hr && cr < 0) consider(-1 - cr, rte_, rtx_);
             bool pl = hl && cl >= 0, pr = hr && cr >= 0;
+            if (pl && full_and_beyond(lte_)) { pl = false; pruned = true; }
+            if (pr && full_and_beyond(rte_)) { pr = false; pruned = true; }
             if (sp + 2 > 64) { if (err_flag) atomicOr(err_flag, 1); break; }
             // push the farther child first so the nearer is visited first
             if (pl && pr) {
@@ -147,6 +161,7 @@ __device__ int collect_leaves(const CutDev& cut, const RayDev& R, bool has_after
         }
     }
     n_out = n;
+    if (more) *more = pruned || total > n;
     return total;
 }
 

@@ -29,7 +29,9 @@ __global__ void __launch_bounds__(128) k_traverse(TraverseArgs a) {
         RayDev R = load_ray(a.rays, r);
         float lte[kListK], ltx[kListK];
         int lid[kListK], n = 0;
-        int total = collect_leaves<kListK>(a.cut, R, false, 0.f, 0, a.cap, lte, ltx, lid, n, a.err);
+        bool more = false;
+        collect_leaves<kListK>(a.cut, R, false, 0.f, 0, a.cap, lte, ltx, lid, n, a.err, true, &more);
+        const int total = n;
 #pragma unroll
         for (int j = 0; j < kListK; ++j)
             if (j < n) {
@@ -40,7 +42,7 @@ __global__ void __launch_bounds__(128) k_traverse(TraverseArgs a) {
         a.st.pos[r] = 0;
         a.st.base[r] = 0;
         a.st.nbuf[r] = n;
-        a.st.count[r] = total;
+        a.st.more[r] = more ? 1 : 0;
         a.st.bt[r] = __int_as_float(0x7f800000);
         a.st.bte[r] = 0.f;
         a.st.bleaf[r] = -1;
@@ -105,6 +107,30 @@ __global__ void __launch_bounds__(128) k_debug_traverse(DebugTraverseArgs a) {
 }
 
 // ------------------------------------------------------------------ fused query wave
+// Rare path, kept out of line so the wave kernel's register allocation is not sized for
+// a second traversal: refill ray r's list with the leaves after its last key (C6).
+__device__ __noinline__ int refill_list(const WaveArgs& a, int r, int nbuf) {
+    const int64_t last = (int64_t)(nbuf - 1) * a.n_rays + r;
+    const float kte = a.lst_te[last];
+    const int kid = a.lst_leaf[last];
+    RayDev R = load_ray(a.rays, r);
+    float lte[kListK], ltx[kListK];
+    int lid[kListK], n = 0;
+    bool more = false;
+    collect_leaves<kListK>(a.cut, R, true, kte, kid, a.cap, lte, ltx, lid, n, a.err, true, &more);
+#pragma unroll
+    for (int j = 0; j < kListK; ++j)
+        if (j < n) {
+            a.lst_leaf[(int64_t)j * a.n_rays + r] = lid[j];
+            a.lst_te[(int64_t)j * a.n_rays + r] = lte[j];
+            a.lst_tx[(int64_t)j * a.n_rays + r] = ltx[j];
+        }
+    a.st.nbuf[r] = n;
+    a.st.more[r] = more ? 1 : 0;
+    atomicAdd(a.n_refills, 1);
+    return n;
+}
+
 struct QueryDesc {
     float o[3], d[3], te, tx;
     int ray, leaf, pos, valid;
@@ -115,7 +141,11 @@ __global__ void __launch_bounds__(256, 2) k_query_wave(WaveArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int n_act = *a.cnt_in;
-    const int n_tiles = (n_act + kTileQ - 1) / kTileQ;
+    // Tile size: 128 queries (one M=128 MMA tile) when the wave is large; sparse tail
+    // waves spread their queries over every resident CTA instead (latency-bound).
+    int qpt = (n_act + gridDim.x - 1) / gridDim.x;
+    qpt = qpt > kTileQ ? kTileQ : (qpt < 8 ? 8 : qpt);
+    const int n_tiles = (n_act + qpt - 1) / qpt;
     if ((int)blockIdx.x >= n_tiles) return;
 
     // shared-memory carve-up
@@ -135,57 +165,53 @@ __global__ void __launch_bounds__(256, 2) k_query_wave(WaveArgs a) {
     const int chunks_per_point = (L * F) / 8;
 
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        const int first = tile * qpt;
+        const int nv = min(qpt, n_act - first);                       // valid queries in this tile
         // 1. query descriptors: ray, current list entry
-        if (tid < kTileQ) {
-            const int i = tile * kTileQ + tid;
+        if (tid < nv) {
+            const int r = a.act_in[first + tid];
+            const int pos = a.st.pos[r];
+            const int slot = pos - a.st.base[r];
+            const int64_t li = (int64_t)slot * a.n_rays + r;
             QueryDesc q;
-            q.valid = i < n_act;
-            if (q.valid) {
-                const int r = a.act_in[i];
-                const int pos = a.st.pos[r];
-                const int slot = pos - a.st.base[r];
-                const int64_t li = (int64_t)slot * a.n_rays + r;
-                q.ray = r;
-                q.pos = pos;
-                q.leaf = a.lst_leaf[li];
-                q.te = a.lst_te[li];
-                q.tx = a.lst_tx[li];
-                float4 r0 = __ldg(a.rays + 2 * (int64_t)r), r1 = __ldg(a.rays + 2 * (int64_t)r + 1);
-                q.o[0] = r0.x; q.o[1] = r0.y; q.o[2] = r0.z;
-                q.d[0] = r1.x; q.d[1] = r1.y; q.d[2] = r1.z;
-            }
+            q.valid = 1;
+            q.ray = r;
+            q.pos = pos;
+            q.leaf = a.lst_leaf[li];
+            q.te = a.lst_te[li];
+            q.tx = a.lst_tx[li];
+            float4 r0 = __ldg(a.rays + 2 * (int64_t)r), r1 = __ldg(a.rays + 2 * (int64_t)r + 1);
+            q.o[0] = r0.x; q.o[1] = r0.y; q.o[2] = r0.z;
+            q.d[0] = r1.x; q.d[1] = r1.y; q.d[2] = r1.z;
             qd[tid] = q;
         }
         __syncthreads();
 
-        // 2. sample + encode: thread -> (query, every other 16-byte chunk)
-        {
-            const int q = tid & (kTileQ - 1);
+        // 2. sample + encode: items (query, 16-byte chunk), query-minor so that a warp's
+        //    lanes gather for neighbouring rays at the same level (coherent lines)
+        for (int i = tid; i < nv * kChunks; i += blockDim.x) {
+            const int q = i % nv, c = i / nv;
             const QueryDesc& Q = qd[q];
-            for (int c = tid >> 7; c < kChunks; c += 2) {
-                uint4 v = make_uint4(0, 0, 0, 0);
-                if (Q.valid) {
-                    const int p = c / chunks_per_point;
-                    const int l0 = ((c % chunks_per_point) * 8) / F;
-                    float x[3];
-                    segment_point(a.g, Q.o, Q.d, Q.te, Q.tx, p, n_pts, nullptr, x);
-                    v = encode_chunk<F>(a.g, x, l0, nullptr);
-                }
-                *reinterpret_cast<uint4*>(feat + q * (D + 8) + c * 8) = v;
-            }
+            const int p = c / chunks_per_point;
+            const int l0 = ((c % chunks_per_point) * 8) / F;
+            float x[3];
+            segment_point(a.g, Q.o, Q.d, Q.te, Q.tx, p, n_pts, nullptr, x);
+            *reinterpret_cast<uint4*>(feat + q * (D + 8) + c * 8) = encode_chunk<F>(a.g, x, l0, nullptr);
         }
         __syncthreads();
 
-        // 3. MLP on tensor cores: warp w -> rows 16w..16w+15
-        mlp_rows16<D>(ms, a.m.hidden, feat, warp * 16, zt, lane);
+        // 3. MLP on tensor cores: warp w -> rows 16w..16w+15 (rows >= nv are ignored)
+        if (warp * 16 < nv) mlp_rows16<D>(ms, a.m.hidden, feat, warp * 16, zt, lane);
         __syncthreads();
 
         // 4. decode, best-hit update, termination, compaction (one thread per query)
-        if (tid < kTileQ) {
-            const QueryDesc& Q = qd[tid];
+        if (warp * 32 < nv) {
             bool survive = false;
-            if (Q.valid) {
+            int ray = -1;
+            if (tid < nv) {
+                const QueryDesc& Q = qd[tid];
                 const int r = Q.ray;
+                ray = r;
                 const float* z = zt + tid * 8;
                 int pos = Q.pos;
                 if (a.z_trace && pos < a.trace_cap) {
@@ -221,32 +247,19 @@ __global__ void __launch_bounds__(256, 2) k_query_wave(WaveArgs a) {
                     }
                 }
                 ++pos;
-                const int count = a.st.count[r];
-                bool done = (a.mode == 1 && hit) || pos >= count;
+                bool done = a.mode == 1 && hit;                         // R1: first confident hit (C5)
                 if (!done) {
                     int base = a.st.base[r], nbuf = a.st.nbuf[r];
                     if (pos - base >= nbuf) {
-                        // list exhausted but more leaves remain: resume after the last key (C6)
-                        const int64_t last = (int64_t)(nbuf - 1) * a.n_rays + r;
-                        const float kte = a.lst_te[last];
-                        const int kid = a.lst_leaf[last];
-                        RayDev R = load_ray(a.rays, r);
-                        float lte[kListK], ltx[kListK];
-                        int lid[kListK], n = 0;
-                        collect_leaves<kListK>(a.cut, R, true, kte, kid, a.cap, lte, ltx, lid, n, a.err);
-#pragma unroll
-                        for (int j = 0; j < kListK; ++j)
-                            if (j < n) {
-                                a.lst_leaf[(int64_t)j * a.n_rays + r] = lid[j];
-                                a.lst_te[(int64_t)j * a.n_rays + r] = lte[j];
-                                a.lst_tx[(int64_t)j * a.n_rays + r] = ltx[j];
-                            }
-                        base = pos;
-                        nbuf = n;
-                        a.st.base[r] = base;
-                        a.st.nbuf[r] = nbuf;
-                        atomicAdd(a.n_refills, 1);
-                        if (n == 0) done = true;   // cannot happen when count is exact
+                        if (!a.st.more[r]) {
+                            done = true;                                 // every intersected leaf visited
+                        } else {
+                            // list exhausted, more leaves may remain: resume after the last key (C6)
+                            nbuf = refill_list(a, r, nbuf);
+                            base = pos;
+                            a.st.base[r] = base;
+                            done = nbuf == 0;
+                        }
                     }
                     if (!done) {
                         const float next_te = a.lst_te[(int64_t)(pos - base) * a.n_rays + r];
@@ -262,7 +275,7 @@ __global__ void __launch_bounds__(256, 2) k_query_wave(WaveArgs a) {
             int base = 0;
             if (lane == 0 && m) base = atomicAdd(a.cnt_out, __popc(m));
             base = __shfl_sync(0xffffffffu, base, 0);
-            if (survive) a.act_out[base + __popc(m & ((1u << lane) - 1u))] = qd[tid].ray;
+            if (survive) a.act_out[base + __popc(m & ((1u << lane) - 1u))] = ray;
         }
         __syncthreads();
     }

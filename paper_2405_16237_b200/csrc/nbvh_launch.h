@@ -21,7 +21,7 @@ struct RayState {
     int32_t* pos;     // global index of the current list entry
     int32_t* base;    // global index of list slot 0
     int32_t* nbuf;    // entries held in the list buffer
-    int32_t* count;   // total intersected leaves
+    int32_t* more;    // 1 if intersected leaves beyond the buffer may exist (C6)
     float* bt;        // best hit t
     float* bte;       // its t_enter
     int32_t* bleaf;   // its leaf (-1: none)

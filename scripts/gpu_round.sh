@@ -19,7 +19,8 @@ if [ "${SKIP_NCU:-0}" != "1" ]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
       --log-file $OUT/launches_$TAG.csv $CMD > $OUT/ncu_launches.log 2>&1
   echo "ncu launches exit $?" >> $OUT/ncu_launches.log
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_query_wave -s 4 -c 2 \
+  # the first (largest) wave and the traversal of the first query
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_query_wave|k_traverse" -s 0 -c 2 \
       -o $OUT/prof_wave_$TAG -f $CMD > $OUT/ncu_full.log 2>&1
   echo "ncu full exit $?" >> $OUT/ncu_full.log
 fi

@@ -3,7 +3,7 @@
 
 Default workload = BASELINE configs[1] ("1080p"): 988,928-triangle procedural scene,
 2,048-leaf cut, hash grid L=16 T=2^19 F=2, n=4 samples, MLP 3x64; one step = one full
-1920x1080 frame of primary rays through nbvh_query (traversal + all query waves).
+1920x1080 frame of primary rays through nbvh_query (traversal + the persistent query kernel).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1080p|tiny] [--impl ours|reference]
 
@@ -90,13 +90,14 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def build_model(cfg_name: str, device: int, rank: int = 0):
+def build_model(cfg_name: str, device: int, rank: int = 0, list_cap: int = 8):
     """Synthetic scene + cut + random-init model of the named BASELINE config."""
     from paper_2405_16237_b200 import Context, PARAM_TABLES
     c = synth.CONFIGS[cfg_name]
     h = c["hash"]
     sc = synth.scene_tiny(c["seeds"]["mesh"]) if cfg_name == "tiny" else synth.scene_1080p(c["seeds"]["mesh"])
-    ctx = Context(device=device, L=h.L, F=h.F, log2_T=h.log2_T, n_points=h.n_points, hidden_layers=h.hidden_layers)
+    ctx = Context(device=device, L=h.L, F=h.F, log2_T=h.log2_T, n_points=h.n_points, hidden_layers=h.hidden_layers,
+                  list_cap=list_cap)
     ctx.set_mesh(sc)
     ctx.build_cut(c["leaves"])
     n_tab = ctx.param_count(PARAM_TABLES)
@@ -153,7 +154,7 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
-    ctx, sc, rays_np, c = build_model(args.config, local, rank)
+    ctx, sc, rays_np, c = build_model(args.config, local, rank, args.list_cap)
     n = rays_np.shape[0]
     ctx.reserve(n)
     rays = torch.from_numpy(rays_np).cuda()
@@ -168,9 +169,6 @@ def run_ours(args):
 
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    launches = 0
-    queries = 0
-    waves = []
     clocks = ClockSampler(local)
     clocks.start()
     if world > 1:
@@ -180,17 +178,24 @@ def run_ours(args):
     for i in range(args.steps):
         flush.fill_(float(i))                                  # evict L2 between timed steps
         starts[i].record(stream)
-        ctx.query(rays, out=out)
+        ctx.query(rays, out=out)                               # async: counter reset + 2 kernels
         ends[i].record(stream)
-        st = ctx.query_stats()
-        launches += st["n_launches"]
-        queries += st["n_queries"]
-        waves.append(st["n_waves"])
     torch.cuda.synchronize()
     wall = time.perf_counter() - wall0
     if world > 1:
         dist.barrier()
     clocks.stop()
+    # host cost of one nbvh_query call (enqueue only, no synchronisation)
+    torch.cuda.synchronize()
+    h0 = time.perf_counter()
+    for _ in range(5):
+        ctx.query(rays, out=out)
+    host_ms = (time.perf_counter() - h0) / 5 * 1e3
+    torch.cuda.synchronize()
+    st = ctx.query_stats()                                     # counters of the last step
+    launches = st["n_launches"] * args.steps
+    queries = st["n_queries"] * args.steps
+    iters = st["n_iters"]
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     t_ms = sum(step_ms)
     tmax = torch.tensor([t_ms], dtype=torch.float64, device="cuda")
@@ -200,21 +205,21 @@ def run_ours(args):
     total_rays = n * args.steps * world
     value = total_rays / (t_ms / 1e3) / 1e6
 
-    # live per-kernel timing of the dominant kernel (fused query wave), one profiled pass
-    # per timed step (separate from the timed region; events on the launching stream)
+    # live per-kernel timing of the dominant kernel (persistent fused query), one profiled
+    # pass per timed step (separate from the timed region; events on the launching stream)
     ctx.set_profiling(True)
     wave_ms, trav_ms, prof_q = [], [], []
     for i in range(max(3, args.steps)):
         flush.fill_(float(i))
         ctx.query(rays, out=out)
         st = ctx.query_stats()
-        wave_ms.append(st["ms_waves"])
+        wave_ms.append(st["ms_query"])
         trav_ms.append(st["ms_traverse"])
         prof_q.append(st["n_queries"])
     ctx.set_profiling(False)
     h = c["hash"]
     useful_gather = h.n_points * h.L * 8 * h.F * 2                # fp16 corner bytes per query
-    per_query_io = 32 + 12 + 8 * 4 + 8 + 29                       # ray, list entry, state r/w, outputs (approx.)
+    per_query_io = 32 + 12 + 8 + 37                                 # ray, list entry, list bookkeeping, hit record
     bytes_per_query = useful_gather + per_query_io
     mean_q = statistics.mean(prof_q)
     wave_s = statistics.mean(wave_ms) / 1e3
@@ -262,9 +267,10 @@ def run_ours(args):
                        "l2_flush": "256 MB write between timed steps, outside the per-step CUDA events",
                        "parallelism": f"replicated model, 1 frame per rank (weak), {world} rank(s)"},
             "gpu_launches": launches,
-            "queries_per_ray": queries / (n * args.steps), "waves_per_step": statistics.mean(waves),
-            "wall_s_timed_region": wall,
-            "roofline": {"bound": "hbm", "kernel": "k_query_wave (fused sample+encode+MLP+decode+compact)",
+            "queries_per_ray": queries / (n * args.steps), "slot_iterations_per_step": iters,
+            "wall_s_timed_region": wall, "host_enqueue_ms_per_query": host_ms, "list_cap": args.list_cap,
+            "list_refills_per_step": st["n_refills"],
+            "roofline": {"bound": "hbm", "kernel": "k_query (persistent: sample+encode+MLP+decode+terminate, slot refill)",
                          "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                          "peak_source": peak_src, "traffic": None,
                          "bytes_per_query": bytes_per_query, "useful_gather_bytes_per_query": useful_gather,
@@ -334,6 +340,7 @@ def main():
     ap.add_argument("--config", default="1080p", choices=["1080p", "tiny"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle timing budget (0 = skip)")
+    ap.add_argument("--list-cap", type=int, default=8, help="per-ray ordered leaf-list capacity K (C6)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

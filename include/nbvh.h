@@ -93,15 +93,16 @@ typedef enum {
     NBVH_PARAM_ALL = 3      /* flat: tables, weights, biases — the gradient-buffer layout    */
 } nbvh_param_block;
 
-/* Counters of the last nbvh_query (host-visible after the stream is synchronised). */
+/* Counters of the last nbvh_query / nbvh_query_host / nbvh_debug_query_trace call.  They
+ * live on the device until nbvh_get_query_stats reads them back. */
 typedef struct {
     int64_t n_rays;
-    int64_t n_queries;       /* sum over rays of neural queries                             */
-    int32_t n_waves;         /* query waves executed                                        */
+    int64_t n_queries;       /* sum over rays of neural queries (ray, leaf) evaluated       */
+    int32_t n_iters;         /* slot iterations of the busiest CTA of the persistent kernel */
     int32_t n_launches;      /* kernels launched by the call                                */
     int32_t n_refills;       /* re-traversals after a leaf-list overflow (C6)               */
     float ms_traverse;       /* device time of the traversal kernel (profiling on, else 0)  */
-    float ms_waves;          /* summed device time of the fused query-wave kernels          */
+    float ms_query;          /* device time of the persistent query kernel (profiling on)   */
 } nbvh_query_stats;
 
 /* Training counters of the last nbvh_train_backward / nbvh_train_step. */
@@ -160,7 +161,10 @@ nbvh_status nbvh_get_cut(const nbvh_ctx* ctx, int32_t lod, float* leaf_lo, float
 /* Neural ray query of n rays (device nbvh_ray[n]) against LoD slot lod: cut
  * traversal with an ordered per-ray leaf list, per-leaf segment sampling + hash-grid
  * encode + MLP, decode and front-to-back termination with ray compaction.  Results in
- * caller-owned device arrays.  Requires nbvh_reserve(n). */
+ * caller-owned device arrays.  Requires nbvh_reserve(n).  Asynchronous: enqueues one
+ * counter reset and two kernels on `stream` and returns without synchronising; the
+ * context's query workspace is reused by the next call on any stream, so concurrent
+ * queries on one context must be ordered by the caller. */
 nbvh_status nbvh_query(nbvh_ctx* ctx, const nbvh_ray* d_rays, int64_t n, int32_t lod, nbvh_hits d_out,
                        void* stream);
 /* Same computation from HOST rays into HOST results: copies rays host->device, runs
@@ -168,7 +172,8 @@ nbvh_status nbvh_query(nbvh_ctx* ctx, const nbvh_ray* d_rays, int64_t n, int32_t
  * end-to-end path).  Host buffers should be pinned for full copy bandwidth. */
 nbvh_status nbvh_query_host(nbvh_ctx* ctx, const nbvh_ray* h_rays, int64_t n, int32_t lod, nbvh_hits h_out,
                             void* stream);
-/* Counters of the last query (the query call has already synchronised its stream). */
+/* Counters of the last query call; synchronises that call's stream to read them.  Also
+ * reports a traversal stack overflow (NBVH_ECUDA) detected on the device. */
 nbvh_status nbvh_get_query_stats(nbvh_ctx* ctx, nbvh_query_stats* out);
 /* on != 0: record CUDA events around every kernel the query launches (on the query's
  * stream) and report their durations in nbvh_query_stats. */

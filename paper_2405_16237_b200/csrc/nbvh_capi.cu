@@ -89,6 +89,7 @@ CutDev make_cut(const nbvh_ctx* c, int lod) {
     d.inner = c->dcut[lod].inner;
     d.leaf_box = c->dcut[lod].leaf_box;
     d.n_leaves = c->cuts[lod].n_leaves;
+    d.depth = c->dcut[lod].depth;
     return d;
 }
 
@@ -121,7 +122,7 @@ extern "C" void nbvh_config_default(nbvh_config* cfg) {
     cfg->n_points = 4;
     cfg->hidden_layers = 2;
     cfg->width = 64;
-    cfg->list_cap = 16;
+    cfg->list_cap = 8;
     cfg->mode = 0;
     cfg->inflate_rel = 1e-3f;
     cfg->inflate_abs = 1e-6f;
@@ -176,8 +177,7 @@ extern "C" nbvh_status nbvh_create(const nbvh_config* cfg, int cuda_device, nbvh
         if (e == cudaSuccess) e = dalloc(&x->d_table16, x->n_table);
         if (e == cudaSuccess) e = dalloc(&x->d_W16, x->n_W);
         if (e == cudaSuccess) e = dalloc(&x->d_misc, 64);
-        if (e == cudaSuccess) e = dalloc(&x->d_cnt, kMaxWaves);
-        if (e == cudaSuccess) e = cudaMallocHost((void**)&x->h_cnt, kMaxWaves * sizeof(int32_t));
+        if (e == cudaSuccess) e = cudaMallocHost((void**)&x->h_misc, 64 * sizeof(int32_t));
         if (e == cudaSuccess)
             e = cudaMemcpy(x->d_params, x->h_params.data(), x->h_params.size() * 4, cudaMemcpyHostToDevice);
         if (e == cudaSuccess) e = cudaMemset(x->d_misc, 0, 64 * sizeof(int32_t));
@@ -206,8 +206,7 @@ static void free_workspace(nbvh_ctx* c) {
     dfree(c->d_lst_te);
     dfree(c->d_lst_tx);
     dfree(c->d_state);
-    dfree(c->d_act[0]);
-    dfree(c->d_act[1]);
+    dfree(c->d_act);
     dfree(c->d_stage_rays);
     dfree(c->d_stage_hits);
     c->reserved = 0;
@@ -228,10 +227,10 @@ extern "C" void nbvh_destroy(nbvh_ctx* c) {
         dfree(c->d_table16);
         dfree(c->d_W16);
         dfree(c->d_misc);
-        dfree(c->d_cnt);
-        if (c->h_cnt) cudaFreeHost(c->h_cnt);
+        if (c->h_misc) cudaFreeHost(c->h_misc);
         for (cudaEvent_t x : c->events) cudaEventDestroy(x);
-        if (c->aux_stream) cudaStreamDestroy(c->aux_stream);
+        for (cudaStream_t x : c->aux_stream)
+            if (x) cudaStreamDestroy(x);
         free_scene_device(c);
         free_train_device(c);
     }
@@ -313,9 +312,8 @@ extern "C" nbvh_status nbvh_reserve(nbvh_ctx* c, int64_t max_rays) {
     cudaError_t e = dalloc(&c->d_lst_leaf, kListK * n);
     if (e == cudaSuccess) e = dalloc(&c->d_lst_te, kListK * n);
     if (e == cudaSuccess) e = dalloc(&c->d_lst_tx, kListK * n);
-    if (e == cudaSuccess) e = dalloc(&c->d_state, 8 * n);
-    if (e == cudaSuccess) e = dalloc(&c->d_act[0], n);
-    if (e == cudaSuccess) e = dalloc(&c->d_act[1], n);
+    if (e == cudaSuccess) e = dalloc(&c->d_state, 2 * n);
+    if (e == cudaSuccess) e = dalloc(&c->d_act, n);
     if (e == cudaSuccess) e = dalloc(&c->d_stage_rays, 8 * n);
     if (e == cudaSuccess) e = dalloc(&c->d_stage_hits, 10 * n);
     if (e != cudaSuccess) {
@@ -438,30 +436,26 @@ extern "C" nbvh_status nbvh_get_cut(const nbvh_ctx* c, int32_t lod, float* leaf_
 // ------------------------------------------------------------------ query
 namespace nbvh {
 
-static WaveArgs wave_args(nbvh_ctx* c, const nbvh_ray* rays, int64_t n, int lod, const HitsDev& out) {
-    WaveArgs a{};
-    a.g = make_grid(c, lod);
-    a.m = make_mlp(c);
-    a.cut = make_cut(c, lod);
-    a.rays = reinterpret_cast<const float4*>(rays);
-    a.n_rays = n;
-    a.cap = c->cfg.list_cap;
-    a.mode = c->cfg.mode;
-    a.lst_leaf = c->d_lst_leaf;
-    a.lst_te = c->d_lst_te;
-    a.lst_tx = c->d_lst_tx;
-    a.st = c->state(n);
-    a.out = out;
-    a.n_refills = c->d_misc + 1;
-    a.err = c->d_misc;
-    return a;
+cudaEvent_t ctx_event(nbvh_ctx* c, int i) {
+    while ((int)c->events.size() <= i) {
+        cudaEvent_t x;
+        cudaEventCreate(&x);
+        c->events.push_back(x);
+    }
+    return c->events[i];
 }
 
+// One query = memset of the counters + k_traverse + one persistent k_query launch, all
+// stream-ordered on `s` with no host synchronisation.  `reset_stats` zeroes the whole
+// counter block (statistics of a public call); otherwise only the per-launch work-list
+// counters are reset and the statistics accumulate (chunked host path).
 nbvh_status run_query(nbvh_ctx* c, const nbvh_ray* rays, int64_t n, int32_t lod, const HitsDev& out, float* z_trace,
-                      int32_t trace_cap, cudaStream_t s) {
-    cudaError_t e = cudaMemsetAsync(c->d_cnt, 0, kMaxWaves * sizeof(int32_t), s);
-    if (e == cudaSuccess) e = cudaMemsetAsync(c->d_misc, 0, 2 * sizeof(int32_t), s);
+                      int32_t trace_cap, cudaStream_t s, bool reset_stats) {
+    QueryCounters* ctr = reinterpret_cast<QueryCounters*>(c->d_misc);
+    cudaError_t e = reset_stats ? cudaMemsetAsync(ctr, 0, sizeof(QueryCounters), s)
+                                : cudaMemsetAsync(&ctr->cnt, 0, 2 * sizeof(int32_t), s);
     if (e != cudaSuccess) return cuda_fail(c, e, "query: memset");
+    const RayState st = c->state();
     TraverseArgs ta{};
     ta.cut = make_cut(c, lod);
     ta.rays = reinterpret_cast<const float4*>(rays);
@@ -470,74 +464,70 @@ nbvh_status run_query(nbvh_ctx* c, const nbvh_ray* rays, int64_t n, int32_t lod,
     ta.lst_leaf = c->d_lst_leaf;
     ta.lst_te = c->d_lst_te;
     ta.lst_tx = c->d_lst_tx;
-    ta.st = c->state(n);
+    ta.st = st;
     ta.out = out;
-    ta.act_out = c->d_act[0];
-    ta.cnt_out = c->d_cnt;
-    ta.err = c->d_misc;
-    auto ev = [&](int i) -> cudaEvent_t {
-        while ((int)c->events.size() <= i) {
-            cudaEvent_t x;
-            cudaEventCreate(&x);
-            c->events.push_back(x);
-        }
-        return c->events[i];
-    };
-    if (c->profiling) cudaEventRecord(ev(0), s);
+    ta.act_out = c->d_act;
+    ta.ctr = ctr;
+    if (c->profiling) cudaEventRecord(ctx_event(c, 0), s);
     e = launch_traverse(ta, s);
     if (e != cudaSuccess) return cuda_fail(c, e, "query: traverse");
-    if (c->profiling) cudaEventRecord(ev(1), s);
-    int launches = 1;
-    WaveArgs wa = wave_args(c, rays, n, lod, out);
-    wa.z_trace = z_trace;
-    wa.trace_cap = trace_cap;
-    int w = 0;
-    const int chunk = 4;
-    int64_t total_q = 0;
-    int waves_done = 0;
-    while (true) {
-        for (int j = 0; j < chunk; ++j, ++w) {
-            if (w + 1 >= kMaxWaves) return fail(c, NBVH_ECUDA, "query: wave limit exceeded");
-            wa.act_in = c->d_act[w & 1];
-            wa.act_out = c->d_act[(w + 1) & 1];
-            wa.cnt_in = c->d_cnt + w;
-            wa.cnt_out = c->d_cnt + w + 1;
-            if (c->profiling) cudaEventRecord(ev(2 + 2 * w), s);
-            e = launch_query_wave(wa, s);
-            if (e != cudaSuccess) return cuda_fail(c, e, "query: wave");
-            if (c->profiling) cudaEventRecord(ev(3 + 2 * w), s);
-            ++launches;
-        }
-        e = cudaMemcpyAsync(c->h_cnt, c->d_cnt, (w + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost, s);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-        if (e != cudaSuccess) return cuda_fail(c, e, "query: wave count");
-        if (c->h_cnt[w] == 0) break;
+    if (c->profiling) cudaEventRecord(ctx_event(c, 1), s);
+    QueryArgs qa{};
+    qa.g = make_grid(c, lod);
+    qa.m = make_mlp(c);
+    qa.cut = make_cut(c, lod);
+    qa.rays = reinterpret_cast<const float4*>(rays);
+    qa.n_rays = n;
+    qa.cap = c->cfg.list_cap;
+    qa.mode = c->cfg.mode;
+    qa.lst_leaf = c->d_lst_leaf;
+    qa.lst_te = c->d_lst_te;
+    qa.lst_tx = c->d_lst_tx;
+    qa.nbuf = st.nbuf;
+    qa.more = st.more;
+    qa.out = out;
+    qa.act = c->d_act;
+    qa.cnt = &ctr->cnt;
+    qa.next = &ctr->next;
+    qa.z_trace = z_trace;
+    qa.trace_cap = trace_cap;
+    qa.ctr = ctr;
+    e = launch_query(qa, n, s);
+    if (e != cudaSuccess) return cuda_fail(c, e, "query: persistent query kernel");
+    if (c->profiling) cudaEventRecord(ctx_event(c, 2), s);
+    if (reset_stats) {
+        c->qstats = nbvh_query_stats{};
+        c->qstats_launches = 0;
     }
-    for (int i = 0; i < w; ++i) {
-        total_q += c->h_cnt[i];
-        if (c->h_cnt[i] > 0) waves_done = i + 1;
-    }
-    int32_t misc[2];
-    e = cudaMemcpyAsync(misc, c->d_misc, sizeof(misc), cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    if (e != cudaSuccess) return cuda_fail(c, e, "query: counters");
-    if (misc[0]) return fail(c, NBVH_ECUDA, "query: traversal stack overflow (BVH deeper than 64)");
-    c->qstats.n_rays = n;
-    c->qstats.n_queries = total_q;
-    c->qstats.n_waves = waves_done;
-    c->qstats.n_launches = launches;
-    c->qstats.n_refills = misc[1];
+    c->qstats.n_rays += n;
+    c->qstats_launches += 2;
+    c->qstats_pending = true;
+    c->qstats_stream = s;
+    return NBVH_OK;
+}
+
+// Resolve the device counters of the last query call (synchronises its stream).
+nbvh_status resolve_query_stats(nbvh_ctx* c) {
+    if (!c->qstats_pending) return NBVH_OK;
+    cudaError_t e = cudaMemcpyAsync(c->h_misc, c->d_misc, sizeof(QueryCounters), cudaMemcpyDeviceToHost,
+                                    c->qstats_stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->qstats_stream);
+    if (e != cudaSuccess) return cuda_fail(c, e, "query stats");
+    const QueryCounters* q = reinterpret_cast<const QueryCounters*>(c->h_misc);
+    c->qstats_pending = false;
+    c->qstats.n_queries = (int64_t)q->n_queries;
+    c->qstats.n_iters = q->max_iter;
+    c->qstats.n_launches = c->qstats_launches;
+    c->qstats.n_refills = q->refills;
     c->qstats.ms_traverse = 0.f;
-    c->qstats.ms_waves = 0.f;
-    if (c->profiling) {
+    c->qstats.ms_query = 0.f;
+    if (c->profiling && c->events.size() >= 3) {
         float ms = 0.f;
-        cudaEventElapsedTime(&ms, c->events[0], c->events[1]);
-        c->qstats.ms_traverse = ms;
-        for (int i = 0; i < w; ++i) {
-            cudaEventElapsedTime(&ms, c->events[2 + 2 * i], c->events[3 + 2 * i]);
-            c->qstats.ms_waves += ms;
-        }
+        if (cudaEventElapsedTime(&ms, c->events[0], c->events[1]) == cudaSuccess) c->qstats.ms_traverse = ms;
+        if (cudaEventElapsedTime(&ms, c->events[1], c->events[2]) == cudaSuccess) c->qstats.ms_query = ms;
+        cudaGetLastError();
     }
+    if (q->err) return fail(c, NBVH_ECUDA, "query: traversal stack overflow (N-BVH deeper than 64)");
     return NBVH_OK;
 }
 
@@ -563,7 +553,7 @@ extern "C" nbvh_status nbvh_query(nbvh_ctx* c, const nbvh_ray* rays, int64_t n, 
     nbvh_status st = check_query(c, rays, n, lod, out);
     if (st) return st;
     if (n == 0) return NBVH_OK;
-    return run_query(c, rays, n, lod, to_dev(out), nullptr, 0, (cudaStream_t)stream);
+    return run_query(c, rays, n, lod, to_dev(out), nullptr, 0, (cudaStream_t)stream, true);
 }
 
 extern "C" nbvh_status nbvh_query_host(nbvh_ctx* c, const nbvh_ray* h_rays, int64_t n, int32_t lod, nbvh_hits h_out,
@@ -571,18 +561,20 @@ extern "C" nbvh_status nbvh_query_host(nbvh_ctx* c, const nbvh_ray* h_rays, int6
     nbvh_status st = check_query(c, h_rays, n, lod, h_out);
     if (st) return st;
     if (n == 0) return NBVH_OK;
-    // Chunks alternate between the caller's stream and a second one, so the host->device
-    // copy of chunk i+1 and the device->host copy of chunk i-1 overlap the query of chunk
-    // i.  The query workspace is reused chunk after chunk (each query ends synchronised).
-    cudaStream_t ss[2] = {(cudaStream_t)stream, nullptr};
-    if (!c->aux_stream) {
-        cudaError_t e0 = cudaStreamCreateWithFlags(&c->aux_stream, cudaStreamNonBlocking);
-        if (e0 != cudaSuccess) return cuda_fail(c, e0, "query_host: stream");
-    }
-    ss[1] = c->aux_stream;
+    // Pipeline over chunks: host->device copies on one auxiliary stream, the queries in order
+    // on the caller's stream (they share the query workspace), device->host copies on a
+    // second auxiliary stream; events order chunk k's query after its upload and its
+    // download after its query, so copies of chunks k+1 / k-1 overlap the query of chunk k.
+    cudaStream_t S = (cudaStream_t)stream;
+    for (int i = 0; i < 2; ++i)
+        if (!c->aux_stream[i]) {
+            cudaError_t e0 = cudaStreamCreateWithFlags(&c->aux_stream[i], cudaStreamNonBlocking);
+            if (e0 != cudaSuccess) return cuda_fail(c, e0, "query_host: stream");
+        }
+    cudaStream_t H = c->aux_stream[0], Dn = c->aux_stream[1];
     const int chunks = n >= (1 << 20) ? 4 : (n >= (1 << 18) ? 2 : 1);
     const int64_t step = (n + chunks - 1) / chunks;
-    // staging layout: t[n], normal[3n], albedo[3n], hit bytes, leaf[n], nq[n]
+    // staging layout: t[n], normal[3n], albedo[3n], leaf[n], nq[n], hit bytes
     float* base = c->d_stage_hits;
     HitsDev d{};
     d.t = base;
@@ -593,46 +585,37 @@ extern "C" nbvh_status nbvh_query_host(nbvh_ctx* c, const nbvh_ray* h_rays, int6
     d.hit = reinterpret_cast<uint8_t*>(base + 9 * n);
     const nbvh_ray* d_rays = reinterpret_cast<const nbvh_ray*>(c->d_stage_rays);
     cudaError_t e = cudaSuccess;
-    int64_t total_q = 0;
-    int32_t launches = 0, waves = 0, refills = 0;
-    auto h2d = [&](int k) {
+    // events 8.. : [8+2k] upload k done, [9+2k] query k done
+    for (int k = 0; k < chunks && e == cudaSuccess; ++k) {
         const int64_t o = k * step, m = std::min(step, n - o);
-        return cudaMemcpyAsync((void*)(d_rays + o), h_rays + o, (size_t)m * sizeof(nbvh_ray), cudaMemcpyHostToDevice,
-                               ss[k & 1]);
-    };
-    for (int k = 0; k < chunks && k < 2 && e == cudaSuccess; ++k) e = h2d(k);
+        e = cudaMemcpyAsync((void*)(d_rays + o), h_rays + o, (size_t)m * sizeof(nbvh_ray), cudaMemcpyHostToDevice, H);
+        if (e == cudaSuccess) e = cudaEventRecord(ctx_event(c, 8 + 2 * k), H);
+    }
     if (e != cudaSuccess) return cuda_fail(c, e, "query_host: H2D");
     for (int k = 0; k < chunks; ++k) {
         const int64_t o = k * step, m = std::min(step, n - o);
-        cudaStream_t s = ss[k & 1];
         HitsDev dk{d.hit + o, d.t + o, d.normal + 3 * o, d.albedo + 3 * o, d.leaf + o, d.n_queries + o};
-        st = run_query(c, d_rays + o, m, lod, dk, nullptr, 0, s);
+        e = cudaStreamWaitEvent(S, ctx_event(c, 8 + 2 * k), 0);
+        if (e != cudaSuccess) return cuda_fail(c, e, "query_host: wait");
+        st = run_query(c, d_rays + o, m, lod, dk, nullptr, 0, S, k == 0);
         if (st) return st;
-        total_q += c->qstats.n_queries;
-        launches += c->qstats.n_launches;
-        waves = std::max(waves, c->qstats.n_waves);
-        refills += c->qstats.n_refills;
-        e = cudaMemcpyAsync(h_out.hit + o, dk.hit, (size_t)m, cudaMemcpyDeviceToHost, s);
-        if (e == cudaSuccess) e = cudaMemcpyAsync(h_out.t + o, dk.t, (size_t)m * 4, cudaMemcpyDeviceToHost, s);
+        e = cudaEventRecord(ctx_event(c, 9 + 2 * k), S);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(Dn, ctx_event(c, 9 + 2 * k), 0);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(h_out.hit + o, dk.hit, (size_t)m, cudaMemcpyDeviceToHost, Dn);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(h_out.t + o, dk.t, (size_t)m * 4, cudaMemcpyDeviceToHost, Dn);
         if (e == cudaSuccess)
-            e = cudaMemcpyAsync(h_out.normal + 3 * o, dk.normal, (size_t)m * 12, cudaMemcpyDeviceToHost, s);
+            e = cudaMemcpyAsync(h_out.normal + 3 * o, dk.normal, (size_t)m * 12, cudaMemcpyDeviceToHost, Dn);
         if (e == cudaSuccess)
-            e = cudaMemcpyAsync(h_out.albedo + 3 * o, dk.albedo, (size_t)m * 12, cudaMemcpyDeviceToHost, s);
+            e = cudaMemcpyAsync(h_out.albedo + 3 * o, dk.albedo, (size_t)m * 12, cudaMemcpyDeviceToHost, Dn);
         if (e == cudaSuccess && h_out.leaf)
-            e = cudaMemcpyAsync(h_out.leaf + o, dk.leaf, (size_t)m * 4, cudaMemcpyDeviceToHost, s);
+            e = cudaMemcpyAsync(h_out.leaf + o, dk.leaf, (size_t)m * 4, cudaMemcpyDeviceToHost, Dn);
         if (e == cudaSuccess && h_out.n_queries)
-            e = cudaMemcpyAsync(h_out.n_queries + o, dk.n_queries, (size_t)m * 4, cudaMemcpyDeviceToHost, s);
-        if (e == cudaSuccess && k + 2 < chunks) e = h2d(k + 2);
+            e = cudaMemcpyAsync(h_out.n_queries + o, dk.n_queries, (size_t)m * 4, cudaMemcpyDeviceToHost, Dn);
         if (e != cudaSuccess) return cuda_fail(c, e, "query_host: copies");
     }
-    e = cudaStreamSynchronize(ss[0]);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(ss[1]);
+    e = cudaStreamSynchronize(Dn);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(S);
     if (e != cudaSuccess) return cuda_fail(c, e, "query_host: D2H");
-    c->qstats.n_rays = n;
-    c->qstats.n_queries = total_q;
-    c->qstats.n_launches = launches;
-    c->qstats.n_waves = waves;
-    c->qstats.n_refills = refills;
     return NBVH_OK;
 }
 
@@ -644,8 +627,9 @@ extern "C" nbvh_status nbvh_set_profiling(nbvh_ctx* c, int32_t on) {
 
 extern "C" nbvh_status nbvh_get_query_stats(nbvh_ctx* c, nbvh_query_stats* out) {
     if (!c || !out) return NBVH_EINVAL;
+    nbvh_status st = resolve_query_stats(c);
     *out = c->qstats;
-    return NBVH_OK;
+    return st;
 }
 
 // ------------------------------------------------------------------ parity hooks
@@ -715,5 +699,5 @@ extern "C" nbvh_status nbvh_debug_query_trace(nbvh_ctx* c, const nbvh_ray* rays,
     cudaStream_t s = (cudaStream_t)stream;
     cudaError_t e = cudaMemsetAsync(z_trace, 0xff, (size_t)n * cap * 8 * sizeof(float), s);   // NaN
     if (e != cudaSuccess) return cuda_fail(c, e, "debug_query_trace: memset");
-    return run_query(c, rays, n, lod, to_dev(out), z_trace, cap, s);
+    return run_query(c, rays, n, lod, to_dev(out), z_trace, cap, s, true);
 }

@@ -11,13 +11,13 @@
 #include "nbvh_launch.h"
 
 namespace nbvh {
-constexpr int kMaxWaves = 65536;
 
 struct DeviceCut {
     InnerNode* inner = nullptr;
     float4* leaf_box = nullptr;   // [n][2]
     int32_t* leaf_base = nullptr;
     float* rank = nullptr;
+    int32_t depth = 0;            // inner levels of the snapshot (sizes the traversal stack)
 };
 
 struct DeviceScene {
@@ -65,35 +65,28 @@ struct nbvh_ctx {
     int32_t* d_lst_leaf = nullptr;
     float* d_lst_te = nullptr;
     float* d_lst_tx = nullptr;
-    int32_t* d_state = nullptr;        // 8 arrays of n int32/float
-    int32_t* d_act[2] = {nullptr, nullptr};
-    int32_t* d_cnt = nullptr;          // per-wave active counts
-    int32_t* h_cnt = nullptr;          // pinned mirror
-    int32_t* d_misc = nullptr;         // [0] error flags, [1] refills, ...
+    int32_t* d_state = nullptr;        // 2 arrays of n int32: list fill, "more leaves" flag
+    int32_t* d_act = nullptr;          // work list of the persistent query kernel
+    int32_t* d_misc = nullptr;         // 64 int32: QueryCounters at offset 0
+    int32_t* h_misc = nullptr;         // pinned mirror
     float* d_stage_rays = nullptr;     // host-path staging
     float* d_stage_hits = nullptr;
     nbvh_query_stats qstats{};
+    int32_t qstats_launches = 0;
+    bool qstats_pending = false;       // device counters not yet read back
+    cudaStream_t qstats_stream = nullptr;
     bool profiling = false;
-    cudaStream_t aux_stream = nullptr;  // second stream of the pipelined host path
-    std::vector<cudaEvent_t> events;   // profiling: [0..1] traverse, then one pair per wave
+    cudaStream_t aux_stream[2] = {nullptr, nullptr};  // upload / download streams of the host path
+    std::vector<cudaEvent_t> events;   // [0..2] profiling (traverse, query); [8..] host-path chunk order
 
     // training
     nbvh::TrainWork* train = nullptr;
     nbvh_train_stats tstats{};
 
-    nbvh::RayState state(int64_t n) const {
+    nbvh::RayState state() const {
         nbvh::RayState s;
-        int32_t* p = d_state;
-        const int64_t m = reserved;
-        s.pos = p;
-        s.base = p + m;
-        s.nbuf = p + 2 * m;
-        s.more = p + 3 * m;
-        s.bt = reinterpret_cast<float*>(p + 4 * m);
-        s.bte = reinterpret_cast<float*>(p + 5 * m);
-        s.bleaf = p + 6 * m;
-        s.nq = p + 7 * m;
-        (void)n;
+        s.nbuf = d_state;
+        s.more = d_state + reserved;
         return s;
     }
 };
@@ -106,6 +99,8 @@ GridDev make_grid(const nbvh_ctx* c, int lod);
 MlpDev make_mlp(const nbvh_ctx* c);
 CutDev make_cut(const nbvh_ctx* c, int lod);
 nbvh_status refresh_fp16(nbvh_ctx* c, cudaStream_t s);
+cudaEvent_t ctx_event(nbvh_ctx* c, int i);
+nbvh_status resolve_query_stats(nbvh_ctx* c);
 // nbvh_train.cu
 nbvh_status upload_scene(nbvh_ctx* c);
 nbvh_status upload_cut(nbvh_ctx* c, int lod);

@@ -18,6 +18,7 @@
 
 #include <cuda_fp16.h>
 #include <cstdint>
+#include <type_traits>
 
 #include "nbvh_internal.h"
 
@@ -46,6 +47,7 @@ struct CutDev {
     const InnerNode* inner;
     const float4* leaf_box;          // [n_leaves][2]: (lo.xyz, 0), (hi.xyz, 0)
     int32_t n_leaves;
+    int32_t depth;                   // inner levels of the snapshot (host-computed)
 };
 
 // ------------------------------------------------------------------ slab test
@@ -92,10 +94,33 @@ __device__ __forceinline__ bool key_less(float a_te, int a_id, float b_te, int b
 // With `prune`, once the list is full a subtree whose entry exceeds the cap-th key is
 // skipped (none of its leaves can enter the list); the return value is then only a lower
 // bound and *more (nullable) reports whether leaves beyond the list may exist.
-template <int K>
+// Traversal stacks: per-thread local array (rare paths) or a shared-memory column
+// [row][blockDim.x] sized by the cut's depth (the per-ray query path).
+struct LocalStack {
+    int s[64];
+    int sp = 0;
+    static constexpr int cap = 64;
+    __device__ __forceinline__ void push(int v) { s[sp++] = v; }
+    __device__ __forceinline__ int pop() { return s[--sp]; }
+};
+struct SmemStack {
+    int* col;            // &stack[0][threadIdx.x]
+    int stride;          // blockDim.x
+    int cap;             // rows
+    int sp = 0;
+    __device__ __forceinline__ void push(int v) { col[(sp++) * stride] = v; }
+    __device__ __forceinline__ int pop() { return col[(--sp) * stride]; }
+};
+
+//
+// t_bound: leaves (and subtrees) entering strictly after t_bound are ignored.  The query
+// passes the ray's current best hit t: front-to-back termination never queries such a leaf
+// (C5), and the bound only decreases, so dropping them is exact.
+template <int K, class Stack>
 __device__ int collect_leaves(const CutDev& cut, const RayDev& R, bool has_after, float after_te, int after_id,
                               int cap, float (&lte)[K], float (&ltx)[K], int (&lid)[K], int& n_out,
-                              int* err_flag, bool prune = false, bool* more = nullptr) {
+                              int* err_flag, Stack& stack, bool prune = false, bool* more = nullptr,
+                              float t_bound = __builtin_huge_valf()) {
     int n = 0, total = 0;
     bool pruned = false;
     auto full_and_beyond = [&](float te) {
@@ -130,39 +155,49 @@ __device__ int collect_leaves(const CutDev& cut, const RayDev& R, bool has_after
         float lo[3] = {a.x, a.y, a.z}, hi[3] = {b.x, b.y, b.z}, te, tx;
         if (slab(R, lo, hi, te, tx)) consider(0, te, tx);
     } else {
-        int stack[64];
-        int sp = 0;
-        stack[sp++] = 0;
-        while (sp > 0) {
-            const float4* p = reinterpret_cast<const float4*>(cut.inner + stack[--sp]);
+        stack.sp = 0;
+        stack.push(0);
+        while (stack.sp > 0) {
+            const float4* p = reinterpret_cast<const float4*>(cut.inner + stack.pop());
             float4 q0 = __ldg(p), q1 = __ldg(p + 1), q2 = __ldg(p + 2), q3 = __ldg(p + 3);
             float llo[3] = {q0.x, q0.y, q0.z}, lhi[3] = {q0.w, q1.x, q1.y};
             float rlo[3] = {q1.z, q1.w, q2.x}, rhi[3] = {q2.y, q2.z, q2.w};
             int cl = __float_as_int(q3.x), cr = __float_as_int(q3.y);
             float lte_, ltx_, rte_, rtx_;
-            bool hl = slab(R, llo, lhi, lte_, ltx_);
-            bool hr = slab(R, rlo, rhi, rte_, rtx_);
+            bool hl = slab(R, llo, lhi, lte_, ltx_) && !(lte_ > t_bound);
+            bool hr = slab(R, rlo, rhi, rte_, rtx_) && !(rte_ > t_bound);
             if (hl && cl < 0) consider(-1 - cl, lte_, ltx_);
             if (hr && cr < 0) consider(-1 - cr, rte_, rtx_);
             bool pl = hl && cl >= 0, pr = hr && cr >= 0;
             if (pl && full_and_beyond(lte_)) { pl = false; pruned = true; }
             if (pr && full_and_beyond(rte_)) { pr = false; pruned = true; }
-            if (sp + 2 > 64) { if (err_flag) atomicOr(err_flag, 1); break; }
+            if (stack.sp + 2 > stack.cap) { if (err_flag) atomicOr(err_flag, 1); break; }
             // push the farther child first so the nearer is visited first
             if (pl && pr) {
                 bool l_first = lte_ <= rte_;
-                stack[sp++] = l_first ? cr : cl;
-                stack[sp++] = l_first ? cl : cr;
+                stack.push(l_first ? cr : cl);
+                stack.push(l_first ? cl : cr);
             } else if (pl) {
-                stack[sp++] = cl;
+                stack.push(cl);
             } else if (pr) {
-                stack[sp++] = cr;
+                stack.push(cr);
             }
         }
     }
     n_out = n;
     if (more) *more = pruned || total > n;
     return total;
+}
+
+// Convenience overload with a per-thread local stack.
+template <int K>
+__device__ int collect_leaves(const CutDev& cut, const RayDev& R, bool has_after, float after_te, int after_id,
+                              int cap, float (&lte)[K], float (&ltx)[K], int (&lid)[K], int& n_out,
+                              int* err_flag, bool prune = false, bool* more = nullptr,
+                              float t_bound = __builtin_huge_valf()) {
+    LocalStack st;
+    return collect_leaves<K, LocalStack>(cut, R, has_after, after_te, after_id, cap, lte, ltx, lid, n_out, err_flag,
+                                         st, prune, more, t_bound);
 }
 
 // ------------------------------------------------------------------ segment sampling
@@ -277,6 +312,172 @@ __device__ __forceinline__ uint4 encode_chunk(const GridDev& g, const float x[3]
                 a[3] = fmaf(cell[j].w[k], f1.y, a[3]);
             }
             __half2 h0 = __floats2half2_rn(a[0], a[1]), h1 = __floats2half2_rn(a[2], a[3]);
+            o32[2 * j] = *reinterpret_cast<uint32_t*>(&h0);
+            o32[2 * j + 1] = *reinterpret_cast<uint32_t*>(&h1);
+        }
+    }
+    return out;
+}
+
+// ------------------------------------------------------------------ packed fp32x2 helpers
+// sm_100 executes `fma.rn.f32x2` / `mul.rn.f32x2` as one FFMA2 / FMUL2 instruction on a
+// register pair; each lane of the pair is rounded exactly like the scalar op.
+__device__ __forceinline__ unsigned long long pk2(float a, float b) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ float2 upk2(unsigned long long v) {
+    float2 r;
+    asm("mov.b64 {%0,%1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+    return r;
+}
+// c + w * v, w broadcast to both lanes
+__device__ __forceinline__ unsigned long long fma2s(float w, unsigned long long v, unsigned long long c) {
+    unsigned long long d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(pk2(w, w)), "l"(v), "l"(c));
+    return d;
+}
+__device__ __forceinline__ unsigned long long mul2(unsigned long long a, unsigned long long b) {
+    unsigned long long d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ unsigned long long h2_to_f2(uint32_t h) {
+    const __half2 v = *reinterpret_cast<const __half2*>(&h);
+    return pk2(__low2float(v), __high2float(v));
+}
+
+// ------------------------------------------------------------------ level table in shared memory
+// One 16-byte record per level, read with a single broadcast LDS.128 by every lane of a warp
+// (all lanes of a warp encode the same level at the same time).  n1 == 0 marks a hashed
+// level; otherwise n1 = N+1 and n1sq = (N+1)^2 (dense index, C2).
+struct LevelSm {
+    float resf;          // N_l as float (exact: N_l < 2^24)
+    uint32_t off;        // entry offset of the level in the concatenated table
+    uint32_t n1, n1sq;
+};
+
+// Stage the level table from the kernel parameter block with compile-time indices only
+// (a runtime index into a by-value parameter array makes ptxas copy the whole block to
+// local memory).
+__device__ __forceinline__ void stage_levels(const GridDev& g, LevelSm* lv, int tid) {
+#pragma unroll
+    for (int l = 0; l < kMaxLevels; ++l) {
+        if (tid == l && l < g.L) {
+            const uint32_t n1 = (uint32_t)g.res[l] + 1u;
+            lv[l].resf = (float)g.res[l];
+            lv[l].off = g.offset[l];
+            lv[l].n1 = g.dense[l] ? n1 : 0u;
+            lv[l].n1sq = n1 * n1;
+        }
+    }
+}
+
+// Cell of one level from the shared-memory level record: corner indices within the level
+// and trilinear weights (same arithmetic as encode_chunk_sm).  Used by the training
+// backward scatter.
+__device__ __forceinline__ void level_cell_sm(const LevelSm& P, uint32_t hmask, float x0, float x1, float x2,
+                                              Cell& c) {
+    const float s0 = __fmul_rn(x0, P.resf), s1 = __fmul_rn(x1, P.resf), s2 = __fmul_rn(x2, P.resf);
+    const float top = __fsub_rn(P.resf, 1.0f);
+    const float c0 = fminf(floorf(s0), top), c1 = fminf(floorf(s1), top), c2 = fminf(floorf(s2), top);
+    const float f0 = __fsub_rn(s0, c0), f1 = __fsub_rn(s1, c1), f2 = __fsub_rn(s2, c2);
+    const uint32_t i0 = (uint32_t)c0, i1 = (uint32_t)c1, i2 = (uint32_t)c2;
+    if (P.n1) {
+        const uint32_t b = i0 + i1 * P.n1 + i2 * P.n1sq;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) c.idx[k] = b + (k & 1) + ((k >> 1) & 1) * P.n1 + ((k >> 2) & 1) * P.n1sq;
+    } else {
+        const uint32_t hx[2] = {i0 & hmask, (i0 + 1u) & hmask};
+        const uint32_t hy[2] = {(i1 * kPrime1) & hmask, ((i1 + 1u) * kPrime1) & hmask};
+        const uint32_t hz[2] = {(i2 * kPrime2) & hmask, ((i2 + 1u) * kPrime2) & hmask};
+#pragma unroll
+        for (int k = 0; k < 8; ++k) c.idx[k] = hx[k & 1] ^ hy[(k >> 1) & 1] ^ hz[(k >> 2) & 1];
+    }
+    const float wx[2] = {1.0f - f0, f0}, wy[2] = {1.0f - f1, f1}, wz[2] = {1.0f - f2, f2};
+#pragma unroll
+    for (int k = 0; k < 8; ++k) c.w[k] = wx[k & 1] * wy[(k >> 1) & 1] * wz[(k >> 2) & 1];
+}
+
+// Encode NL = 8/F consecutive levels l0.. of one point x (normalised, in [0,1]^3) into
+// 16 bytes of fp16 features: s = x*N, c = min(floor(s), N-1), f = s - c (exact), corner
+// index dense or hashed (C2, C3), trilinear weights (wx*wy)*wz, blend in fp32 (P:101,
+// P:142).  All 8*NL gathers are issued before the first is consumed.  `tab` points to the
+// fp16 table viewed as 4-byte (F=2) or 8-byte (F=4) entries.  idx_out (nullable) receives
+// the 8*NL corner indices within their levels (parity hook).
+template <int F>
+__device__ __forceinline__ uint4 encode_chunk_sm(const LevelSm* lv, const void* tab, uint32_t hmask, float x0,
+                                                 float x1, float x2, int l0, uint32_t* idx_out) {
+    constexpr int NL = 8 / F;
+    using Entry = typename std::conditional<F == 2, uint32_t, uint2>::type;
+    const Entry* T = reinterpret_cast<const Entry*>(tab);
+    Entry v[NL][8];
+    float fr[NL][3];
+    // 1. per level: cell, corner indices, and the 8 gathers issued at once (the index
+    //    registers die as soon as the loads are issued; only the fractions are kept)
+#pragma unroll
+    for (int j = 0; j < NL; ++j) {
+        const LevelSm P = lv[l0 + j];
+        const float s0 = __fmul_rn(x0, P.resf), s1 = __fmul_rn(x1, P.resf), s2 = __fmul_rn(x2, P.resf);
+        const float top = __fsub_rn(P.resf, 1.0f);
+        const float c0 = fminf(floorf(s0), top), c1 = fminf(floorf(s1), top), c2 = fminf(floorf(s2), top);
+        fr[j][0] = __fsub_rn(s0, c0);
+        fr[j][1] = __fsub_rn(s1, c1);
+        fr[j][2] = __fsub_rn(s2, c2);
+        const uint32_t i0 = (uint32_t)c0, i1 = (uint32_t)c1, i2 = (uint32_t)c2;
+        uint32_t idx[8];
+        if (P.n1) {
+            const uint32_t b = i0 + i1 * P.n1 + i2 * P.n1sq;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) idx[k] = b + (k & 1) + ((k >> 1) & 1) * P.n1 + ((k >> 2) & 1) * P.n1sq;
+        } else {
+            const uint32_t hx[2] = {i0 & hmask, (i0 + 1u) & hmask};
+            const uint32_t hy[2] = {(i1 * kPrime1) & hmask, ((i1 + 1u) * kPrime1) & hmask};
+            const uint32_t hz[2] = {(i2 * kPrime2) & hmask, ((i2 + 1u) * kPrime2) & hmask};
+#pragma unroll
+            for (int k = 0; k < 8; ++k) idx[k] = hx[k & 1] ^ hy[(k >> 1) & 1] ^ hz[(k >> 2) & 1];
+        }
+        if (idx_out) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) idx_out[j * 8 + k] = idx[k];
+        }
+        // 32-bit entry index (n_entries < 2^32), one IMAD.WIDE.U32 per gather address
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[j][k] = __ldg(T + (P.off + idx[k]));
+    }
+    // 2. trilinear weights (wx*wy)*wz and the fp32 blend, level by level
+    uint4 out;
+    uint32_t* o32 = reinterpret_cast<uint32_t*>(&out);
+#pragma unroll
+    for (int j = 0; j < NL; ++j) {
+        const float f0 = fr[j][0], f1 = fr[j][1], f2 = fr[j][2];
+        const unsigned long long wx = pk2(1.0f - f0, f0);
+        const unsigned long long wxy0 = mul2(wx, pk2(1.0f - f1, 1.0f - f1));
+        const unsigned long long wxy1 = mul2(wx, pk2(f1, f1));
+        const unsigned long long wz0 = pk2(1.0f - f2, 1.0f - f2), wz1 = pk2(f2, f2);
+        float w[8];
+        float2 t;
+        t = upk2(mul2(wxy0, wz0)); w[0] = t.x; w[1] = t.y;
+        t = upk2(mul2(wxy1, wz0)); w[2] = t.x; w[3] = t.y;
+        t = upk2(mul2(wxy0, wz1)); w[4] = t.x; w[5] = t.y;
+        t = upk2(mul2(wxy1, wz1)); w[6] = t.x; w[7] = t.y;
+        if constexpr (F == 2) {
+            unsigned long long acc = 0ull;   // (+0, +0)
+#pragma unroll
+            for (int k = 0; k < 8; ++k) acc = fma2s(w[k], h2_to_f2(v[j][k]), acc);
+            const float2 a = upk2(acc);
+            __half2 h = __floats2half2_rn(a.x, a.y);
+            o32[j] = *reinterpret_cast<uint32_t*>(&h);
+        } else {
+            unsigned long long a01 = 0ull, a23 = 0ull;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                a01 = fma2s(w[k], h2_to_f2(v[j][k].x), a01);
+                a23 = fma2s(w[k], h2_to_f2(v[j][k].y), a23);
+            }
+            const float2 p = upk2(a01), q = upk2(a23);
+            __half2 h0 = __floats2half2_rn(p.x, p.y), h1 = __floats2half2_rn(q.x, q.y);
             o32[2 * j] = *reinterpret_cast<uint32_t*>(&h0);
             o32[2 * j + 1] = *reinterpret_cast<uint32_t*>(&h1);
         }

@@ -21,49 +21,50 @@
 namespace nbvh {
 
 // ------------------------------------------------------------------ traversal
+// K = register capacity of the ordered list (the runtime cap <= K); the traversal stack
+// lives in shared memory, one column per thread, rows = cut depth + 2.
+template <int K>
 __global__ void __launch_bounds__(128) k_traverse(TraverseArgs a) {
+    extern __shared__ int stk_raw[];
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const bool valid = r < a.n_rays;
     bool active = false;
     if (valid) {
         RayDev R = load_ray(a.rays, r);
-        float lte[kListK], ltx[kListK];
-        int lid[kListK], n = 0;
+        float lte[K], ltx[K];
+        int lid[K], n = 0;
         bool more = false;
-        collect_leaves<kListK>(a.cut, R, false, 0.f, 0, a.cap, lte, ltx, lid, n, a.err, true, &more);
-        const int total = n;
+        SmemStack st{stk_raw + threadIdx.x, (int)blockDim.x, a.cut.depth + 2};
+        collect_leaves<K, SmemStack>(a.cut, R, false, 0.f, 0, a.cap, lte, ltx, lid, n, &a.ctr->err, st, true, &more);
 #pragma unroll
-        for (int j = 0; j < kListK; ++j)
+        for (int j = 0; j < K; ++j)
             if (j < n) {
                 a.lst_leaf[(int64_t)j * a.n_rays + r] = lid[j];
                 a.lst_te[(int64_t)j * a.n_rays + r] = lte[j];
                 a.lst_tx[(int64_t)j * a.n_rays + r] = ltx[j];
             }
-        a.st.pos[r] = 0;
-        a.st.base[r] = 0;
-        a.st.nbuf[r] = n;
-        a.st.more[r] = more ? 1 : 0;
-        a.st.bt[r] = __int_as_float(0x7f800000);
-        a.st.bte[r] = 0.f;
-        a.st.bleaf[r] = -1;
-        a.st.nq[r] = 0;
-        // initial miss record (visibility 1 = no intersection)
-        a.out.hit[r] = 0;
-        a.out.t[r] = __int_as_float(0x7f800000);
+        active = n > 0;
+        if (active) {
+            a.st.nbuf[r] = n;
+            a.st.more[r] = more ? 1 : 0;
+        } else {
+            // no intersected leaf: final miss record (visibility 1 = no intersection)
+            a.out.hit[r] = 0;
+            a.out.t[r] = __int_as_float(0x7f800000);
 #pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            a.out.normal[3 * r + k] = 0.f;
-            a.out.albedo[3 * r + k] = 0.f;
+            for (int k = 0; k < 3; ++k) {
+                a.out.normal[3 * r + k] = 0.f;
+                a.out.albedo[3 * r + k] = 0.f;
+            }
+            if (a.out.leaf) a.out.leaf[r] = -1;
+            if (a.out.n_queries) a.out.n_queries[r] = 0;
         }
-        if (a.out.leaf) a.out.leaf[r] = -1;
-        if (total == 0 && a.out.n_queries) a.out.n_queries[r] = 0;
-        active = total > 0;
     }
-    // warp-aggregated append to the wave-0 active list
+    // warp-aggregated append to the work list of the query kernel
     const unsigned m = __ballot_sync(0xffffffffu, active);
     const int lane = threadIdx.x & 31;
     int base = 0;
-    if (lane == 0 && m) base = atomicAdd(a.cnt_out, __popc(m));
+    if (lane == 0 && m) base = atomicAdd(&a.ctr->cnt, __popc(m));
     base = __shfl_sync(0xffffffffu, base, 0);
     if (active) a.act_out[base + __popc(m & ((1u << lane) - 1u))] = (int)r;
 }
@@ -106,193 +107,295 @@ __global__ void __launch_bounds__(128) k_debug_traverse(DebugTraverseArgs a) {
     a.count[r] = total;
 }
 
-// ------------------------------------------------------------------ fused query wave
-// Rare path, kept out of line so the wave kernel's register allocation is not sized for
-// a second traversal: refill ray r's list with the leaves after its last key (C6).
-__device__ __noinline__ int refill_list(const WaveArgs& a, int r, int nbuf) {
-    const int64_t last = (int64_t)(nbuf - 1) * a.n_rays + r;
-    const float kte = a.lst_te[last];
-    const int kid = a.lst_leaf[last];
-    RayDev R = load_ray(a.rays, r);
+// ------------------------------------------------------------------ persistent fused query
+// Rare path, kept out of line so the query kernel's register allocation is not sized for a
+// second traversal: refill ray r's list with the leaves after its last key (C6).
+__device__ __noinline__ int refill_list(CutDev cut, const float4* rays, int64_t n_rays, int cap, int32_t* lst_leaf,
+                                        float* lst_te, float* lst_tx, QueryCounters* ctr, int r, int nbuf,
+                                        float t_bound, int* more_out) {
+    const int64_t last = (int64_t)(nbuf - 1) * n_rays + r;
+    const float kte = lst_te[last];
+    const int kid = lst_leaf[last];
+    RayDev R = load_ray(rays, r);
     float lte[kListK], ltx[kListK];
     int lid[kListK], n = 0;
     bool more = false;
-    collect_leaves<kListK>(a.cut, R, true, kte, kid, a.cap, lte, ltx, lid, n, a.err, true, &more);
+    collect_leaves<kListK>(cut, R, true, kte, kid, cap, lte, ltx, lid, n, &ctr->err, true, &more, t_bound);
 #pragma unroll
     for (int j = 0; j < kListK; ++j)
         if (j < n) {
-            a.lst_leaf[(int64_t)j * a.n_rays + r] = lid[j];
-            a.lst_te[(int64_t)j * a.n_rays + r] = lte[j];
-            a.lst_tx[(int64_t)j * a.n_rays + r] = ltx[j];
+            lst_leaf[(int64_t)j * n_rays + r] = lid[j];
+            lst_te[(int64_t)j * n_rays + r] = lte[j];
+            lst_tx[(int64_t)j * n_rays + r] = ltx[j];
         }
-    a.st.nbuf[r] = n;
-    a.st.more[r] = more ? 1 : 0;
-    atomicAdd(a.n_refills, 1);
+    *more_out = more ? 1 : 0;
+    atomicAdd(&ctr->refills, 1);
     return n;
 }
 
-struct QueryDesc {
-    float o[3], d[3], te, tx;
-    int ray, leaf, pos, valid;
+// Per-CTA ray slots (structure of arrays in shared memory).  Thread s < kTileQ owns slot s
+// for the refill and decode phases; the encode and MLP phases work on the compacted list
+// of occupied slots.
+struct SlotSm {
+    int32_t ray[kTileQ], pos[kTileQ], base[kTileQ], nbuf[kTileQ], more[kTileQ], bleaf[kTileQ], nq[kTileQ],
+        leaf[kTileQ];
+    float o[3][kTileQ], d[3][kTileQ];
+    float bt[kTileQ], bte[kTileQ], te[kTileQ], tx[kTileQ];
+    float nrm[3][kTileQ], alb[3][kTileQ];
+    int32_t act[kTileQ];
+    int32_t wcnt[2][kTileQ / 32];
+    int32_t base_idx;
+    int32_t pad[3];
 };
 
+// Exclusive rank of `pred` among the slot-owning threads (tid < kTileQ) in slot order, and
+// the total.  Called by the whole block; contains one __syncthreads.
+__device__ __forceinline__ int slot_rank(bool pred, int32_t* wcnt, int tid, int& total) {
+    const unsigned m = __ballot_sync(0xffffffffu, pred);
+    const int warp = tid >> 5, lane = tid & 31;
+    if (lane == 0 && warp < kTileQ / 32) wcnt[warp] = __popc(m);
+    __syncthreads();
+    int off = 0;
+    total = 0;
+#pragma unroll
+    for (int w = 0; w < kTileQ / 32; ++w) {
+        const int c = wcnt[w];
+        off += w < warp ? c : 0;
+        total += c;
+    }
+    return off + __popc(m & ((1u << lane) - 1u));
+}
+
+__host__ __device__ constexpr size_t align16(size_t b) { return (b + 15) & ~(size_t)15; }
+
+// Shared-memory plan of k_query (bytes), shared by the kernel and its launcher.
+struct QuerySmemPlan {
+    size_t feat, w, z, bias, lv, xs, slots, total;
+    __host__ __device__ QuerySmemPlan(int d_in, int hidden, int n_points) {
+        feat = 0;
+        w = feat + align16((size_t)kTileQ * (d_in + 8) * 2);
+        z = w + align16((size_t)mlp_smem_halves(d_in, hidden) * 2);
+        bias = z + align16((size_t)kTileQ * 8 * 4);
+        lv = bias + align16((size_t)(64 * hidden + 8) * 4);
+        xs = lv + align16(sizeof(LevelSm) * kMaxLevels);
+        slots = xs + align16((size_t)kTileQ * n_points * 3 * 4);
+        total = slots + align16(sizeof(SlotSm));
+    }
+};
+
+// One launch processes every ray that intersects the cut (Q2-Q7):
+// each CTA keeps kTileQ ray slots; every iteration it (A) refills empty slots with the next
+// rays of the global work list (one atomic per CTA), (B) compacts the occupied slots,
+// (C) fetches each ray's current leaf segment and its n sample points, (D) hash-grid
+// encodes them into a shared-memory feature tile (warp = one 16-byte feature chunk of 32
+// queries, lanes = queries), (E) runs the MLP on tensor cores, (F) decodes, updates the
+// ray's best hit, decides front-to-back termination and frees the slot of a finished ray
+// after writing its hit record.  Tiles stay full until the work list drains: there are no
+// query waves, host round trips or per-wave weight restaging.
 template <int F, int D>
-__global__ void __launch_bounds__(256, 2) k_query_wave(WaveArgs a) {
+__global__ void __launch_bounds__(256, 2) k_query(QueryArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int n_act = *a.cnt_in;
-    // Tile size: 128 queries (one M=128 MMA tile) when the wave is large; sparse tail
-    // waves spread their queries over every resident CTA instead (latency-bound).
-    int qpt = (n_act + gridDim.x - 1) / gridDim.x;
-    qpt = qpt > kTileQ ? kTileQ : (qpt < 8 ? 8 : qpt);
-    const int n_tiles = (n_act + qpt - 1) / qpt;
-    if ((int)blockIdx.x >= n_tiles) return;
-
-    // shared-memory carve-up
+    const int NP = a.g.n_points;
+    const QuerySmemPlan plan(D, a.m.hidden, NP);
+    __half* feat = reinterpret_cast<__half*>(smem_raw + plan.feat);            // [kTileQ][D+8]
     MlpSmem ms;
-    __half* feat = reinterpret_cast<__half*>(smem_raw);                 // [128][D+8]
-    ms.w0 = feat + kTileQ * (D + 8);
+    ms.w0 = reinterpret_cast<__half*>(smem_raw + plan.w);
     ms.wh = ms.w0 + 64 * (D + 8);
     ms.wo = ms.wh + (a.m.hidden - 1) * 64 * 72;
-    float* zt = reinterpret_cast<float*>(ms.wo + 8 * 72);              // [128][8]
-    ms.b = zt + kTileQ * 8;
-    QueryDesc* qd = reinterpret_cast<QueryDesc*>(ms.b + 64 * a.m.hidden + 8);
+    float* zt = reinterpret_cast<float*>(smem_raw + plan.z);                   // [kTileQ][8]
+    ms.b = reinterpret_cast<float*>(smem_raw + plan.bias);
+    LevelSm* lv = reinterpret_cast<LevelSm*>(smem_raw + plan.lv);
+    float* xs = reinterpret_cast<float*>(smem_raw + plan.xs);                  // [NP*3][kTileQ]
+    SlotSm& S = *reinterpret_cast<SlotSm*>(smem_raw + plan.slots);
 
     stage_mlp(a.m, ms, tid, blockDim.x);
-
-    const int L = a.g.L, n_pts = a.g.n_points;
+    stage_levels(a.g, lv, tid);
+    if (tid < kTileQ) S.ray[tid] = -1;
+    const int total = *a.cnt;                 // rays with >= 1 intersected leaf (k_traverse)
+    const uint32_t hmask = (1u << a.g.log2_T) - 1u;
+    const void* tab = a.g.table;
+    const int cpp = (a.g.L * F) / 8;          // 16-byte chunks per sample point
     constexpr int kChunks = D / 8;
-    const int chunks_per_point = (L * F) / 8;
+    int iters = 0;
+    bool exhausted = false;
+    __syncthreads();
 
-    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-        const int first = tile * qpt;
-        const int nv = min(qpt, n_act - first);                       // valid queries in this tile
-        // 1. query descriptors: ray, current list entry
+    while (true) {
+        // (A) refill empty slots from the global work list
+        int n_empty;
+        const bool empty = tid < kTileQ && S.ray[tid] < 0;
+        const int erank = slot_rank(empty, S.wcnt[0], tid, n_empty);
+        if (tid == 0) S.base_idx = (n_empty > 0 && !exhausted) ? atomicAdd(a.next, n_empty) : total;
+        __syncthreads();
+        const int bidx = S.base_idx;
+        exhausted = bidx + n_empty >= total;
+        if (empty && bidx + erank < total) {
+            const int r = a.act[bidx + erank];
+            const float4 r0 = __ldg(a.rays + 2 * (int64_t)r), r1 = __ldg(a.rays + 2 * (int64_t)r + 1);
+            S.ray[tid] = r;
+            S.o[0][tid] = r0.x; S.o[1][tid] = r0.y; S.o[2][tid] = r0.z;
+            S.d[0][tid] = r1.x; S.d[1][tid] = r1.y; S.d[2][tid] = r1.z;
+            S.pos[tid] = 0;
+            S.base[tid] = 0;
+            S.nbuf[tid] = a.nbuf[r];
+            S.more[tid] = a.more[r];
+            S.bt[tid] = __int_as_float(0x7f800000);
+            S.bte[tid] = 0.f;
+            S.bleaf[tid] = -1;
+            S.nq[tid] = 0;
+        }
+        // (B) compact the occupied slots (slot order)
+        int nv;
+        const bool occ = tid < kTileQ && (empty ? (bidx + erank < total) : true);
+        const int arank = slot_rank(occ, S.wcnt[1], tid, nv);
+        if (nv == 0) break;
+        if (occ) S.act[arank] = tid;
+        ++iters;
+        __syncthreads();
+
+        // (C) current leaf segment and the n stratified sample points (C8)
         if (tid < nv) {
-            const int r = a.act_in[first + tid];
-            const int pos = a.st.pos[r];
-            const int slot = pos - a.st.base[r];
-            const int64_t li = (int64_t)slot * a.n_rays + r;
-            QueryDesc q;
-            q.valid = 1;
-            q.ray = r;
-            q.pos = pos;
-            q.leaf = a.lst_leaf[li];
-            q.te = a.lst_te[li];
-            q.tx = a.lst_tx[li];
-            float4 r0 = __ldg(a.rays + 2 * (int64_t)r), r1 = __ldg(a.rays + 2 * (int64_t)r + 1);
-            q.o[0] = r0.x; q.o[1] = r0.y; q.o[2] = r0.z;
-            q.d[0] = r1.x; q.d[1] = r1.y; q.d[2] = r1.z;
-            qd[tid] = q;
+            const int s = S.act[tid];
+            const int r = S.ray[s];
+            const int64_t li = (int64_t)(S.pos[s] - S.base[s]) * a.n_rays + r;
+            const float te = a.lst_te[li], tx = a.lst_tx[li];
+            S.leaf[s] = a.lst_leaf[li];
+            S.te[s] = te;
+            S.tx[s] = tx;
+            const float o[3] = {S.o[0][s], S.o[1][s], S.o[2][s]}, d[3] = {S.d[0][s], S.d[1][s], S.d[2][s]};
+            for (int p = 0; p < NP; ++p) {
+                float x[3];
+                segment_point(a.g, o, d, te, tx, p, NP, nullptr, x);
+                xs[(p * 3 + 0) * kTileQ + tid] = x[0];
+                xs[(p * 3 + 1) * kTileQ + tid] = x[1];
+                xs[(p * 3 + 2) * kTileQ + tid] = x[2];
+            }
         }
         __syncthreads();
 
-        // 2. sample + encode: items (query, 16-byte chunk), query-minor so that a warp's
-        //    lanes gather for neighbouring rays at the same level (coherent lines)
-        for (int i = tid; i < nv * kChunks; i += blockDim.x) {
-            const int q = i % nv, c = i / nv;
-            const QueryDesc& Q = qd[q];
-            const int p = c / chunks_per_point;
-            const int l0 = ((c % chunks_per_point) * 8) / F;
-            float x[3];
-            segment_point(a.g, Q.o, Q.d, Q.te, Q.tx, p, n_pts, nullptr, x);
-            *reinterpret_cast<uint4*>(feat + q * (D + 8) + c * 8) = encode_chunk<F>(a.g, x, l0, nullptr);
+        // (D) encode: warp w owns feature chunks w, w+8, ...; lanes = 32 consecutive queries
+        {
+            const int nqb = (nv + 31) >> 5;
+            for (int c = warp; c < kChunks; c += 8) {
+                const int p = c / cpp, l0 = (c - p * cpp) * (8 / F);
+                const float* xp = xs + p * 3 * kTileQ;
+                for (int qb = 0; qb < nqb; ++qb) {
+                    const int q = qb * 32 + lane;
+                    if (q < nv)
+                        *reinterpret_cast<uint4*>(feat + q * (D + 8) + c * 8) = encode_chunk_sm<F>(
+                            lv, tab, hmask, xp[q], xp[kTileQ + q], xp[2 * kTileQ + q], l0, nullptr);
+                }
+            }
         }
         __syncthreads();
 
-        // 3. MLP on tensor cores: warp w -> rows 16w..16w+15 (rows >= nv are ignored)
+        // (E) MLP on tensor cores: warp w -> rows 16w..16w+15 (rows >= nv are ignored)
         if (warp * 16 < nv) mlp_rows16<D>(ms, a.m.hidden, feat, warp * 16, zt, lane);
         __syncthreads();
 
-        // 4. decode, best-hit update, termination, compaction (one thread per query)
-        if (warp * 32 < nv) {
-            bool survive = false;
-            int ray = -1;
-            if (tid < nv) {
-                const QueryDesc& Q = qd[tid];
-                const int r = Q.ray;
-                ray = r;
-                const float* z = zt + tid * 8;
-                int pos = Q.pos;
-                if (a.z_trace && pos < a.trace_cap) {
-                    float4* dst = reinterpret_cast<float4*>(a.z_trace + ((int64_t)r * a.trace_cap + pos) * 8);
-                    dst[0] = make_float4(z[0], z[1], z[2], z[3]);
-                    dst[1] = make_float4(z[4], z[5], z[6], z[7]);
-                }
-                const int nq = a.st.nq[r] + 1;
-                float bt = a.st.bt[r], bte = a.st.bte[r];
-                int bleaf = a.st.bleaf[r];
-                const bool hit = z[0] < 0.0f;                          // sigmoid(z) < 0.5 (C13)
-                if (hit) {
-                    const float tl = sigmoid_f(z[1]);                  // local distance
-                    const float t = __fadd_rn(Q.te, __fmul_rn(tl, __fsub_rn(Q.tx, Q.te)));
-                    const bool better = bleaf < 0 || t < bt ||
-                                        (t == bt && (Q.te < bte || (Q.te == bte && Q.leaf < bleaf)));
-                    if (better) {
-                        bt = t; bte = Q.te; bleaf = Q.leaf;
-                        float nn = __fsqrt_rn(__fadd_rn(__fadd_rn(__fmul_rn(z[2], z[2]), __fmul_rn(z[3], z[3])),
-                                                        __fmul_rn(z[4], z[4])));
-                        nn = fmaxf(nn, 1e-6f);
-                        a.out.hit[r] = 1;
-                        a.out.t[r] = t;
-#pragma unroll
-                        for (int k = 0; k < 3; ++k) {
-                            a.out.normal[3 * r + k] = __fdiv_rn(z[2 + k], nn);
-                            a.out.albedo[3 * r + k] = sigmoid_f(z[5 + k]);
-                        }
-                        if (a.out.leaf) a.out.leaf[r] = Q.leaf;
-                        a.st.bt[r] = bt;
-                        a.st.bte[r] = bte;
-                        a.st.bleaf[r] = bleaf;
-                    }
-                }
-                ++pos;
-                bool done = a.mode == 1 && hit;                         // R1: first confident hit (C5)
-                if (!done) {
-                    int base = a.st.base[r], nbuf = a.st.nbuf[r];
-                    if (pos - base >= nbuf) {
-                        if (!a.st.more[r]) {
-                            done = true;                                 // every intersected leaf visited
-                        } else {
-                            // list exhausted, more leaves may remain: resume after the last key (C6)
-                            nbuf = refill_list(a, r, nbuf);
-                            base = pos;
-                            a.st.base[r] = base;
-                            done = nbuf == 0;
-                        }
-                    }
-                    if (!done) {
-                        const float next_te = a.lst_te[(int64_t)(pos - base) * a.n_rays + r];
-                        done = bleaf >= 0 && next_te > bt;             // front-to-back termination
-                    }
-                }
-                a.st.pos[r] = pos;
-                a.st.nq[r] = nq;
-                if (done && a.out.n_queries) a.out.n_queries[r] = nq;
-                survive = !done;
+        // (F) decode, best hit, front-to-back termination
+        if (tid < nv) {
+            const int s = S.act[tid];
+            const int r = S.ray[s];
+            const float* z = zt + tid * 8;
+            int pos = S.pos[s];
+            if (a.z_trace && pos < a.trace_cap) {
+                float4* dst = reinterpret_cast<float4*>(a.z_trace + ((int64_t)r * a.trace_cap + pos) * 8);
+                dst[0] = make_float4(z[0], z[1], z[2], z[3]);
+                dst[1] = make_float4(z[4], z[5], z[6], z[7]);
             }
-            const unsigned m = __ballot_sync(0xffffffffu, survive);
-            int base = 0;
-            if (lane == 0 && m) base = atomicAdd(a.cnt_out, __popc(m));
-            base = __shfl_sync(0xffffffffu, base, 0);
-            if (survive) a.act_out[base + __popc(m & ((1u << lane) - 1u))] = ray;
+            const int nq = S.nq[s] + 1;
+            const float te = S.te[s], tx = S.tx[s];
+            const int leaf = S.leaf[s];
+            float bt = S.bt[s];
+            int bleaf = S.bleaf[s];
+            const bool hit = z[0] < 0.0f;                                  // sigmoid(z) < 0.5 (C13)
+            if (hit) {
+                const float tl = sigmoid_f(z[1]);                          // local distance
+                const float t = __fadd_rn(te, __fmul_rn(tl, __fsub_rn(tx, te)));
+                const float bte = S.bte[s];
+                const bool better = bleaf < 0 || t < bt || (t == bt && (te < bte || (te == bte && leaf < bleaf)));
+                if (better) {
+                    bt = t;
+                    bleaf = leaf;
+                    S.bt[s] = t;
+                    S.bte[s] = te;
+                    S.bleaf[s] = leaf;
+                    float nn = __fsqrt_rn(__fadd_rn(__fadd_rn(__fmul_rn(z[2], z[2]), __fmul_rn(z[3], z[3])),
+                                                    __fmul_rn(z[4], z[4])));
+                    nn = fmaxf(nn, 1e-6f);
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) {
+                        S.nrm[k][s] = __fdiv_rn(z[2 + k], nn);
+                        S.alb[k][s] = sigmoid_f(z[5 + k]);
+                    }
+                }
+            }
+            ++pos;
+            bool done = a.mode == 1 && hit;                                 // R1: first confident hit (C5)
+            if (!done) {
+                int base = S.base[s], nbuf = S.nbuf[s];
+                if (pos - base >= nbuf) {
+                    if (!S.more[s]) {
+                        done = true;                                         // every intersected leaf visited
+                    } else {
+                        // list exhausted, more leaves may remain: resume after the last key (C6)
+                        int more = 0;
+                        nbuf = refill_list(a.cut, a.rays, a.n_rays, a.cap, a.lst_leaf, a.lst_te, a.lst_tx, a.ctr, r,
+                                           nbuf, bleaf >= 0 ? bt : __int_as_float(0x7f800000), &more);
+                        base = pos;
+                        S.base[s] = base;
+                        S.nbuf[s] = nbuf;
+                        S.more[s] = more;
+                        done = nbuf == 0;
+                    }
+                }
+                if (!done) {
+                    const float next_te = a.lst_te[(int64_t)(pos - base) * a.n_rays + r];
+                    done = bleaf >= 0 && next_te > bt;                     // front-to-back termination
+                }
+            }
+            S.pos[s] = pos;
+            S.nq[s] = nq;
+            if (done) {
+                // Q7: hit record; a miss keeps t = +inf and zero vectors
+                const bool h = bleaf >= 0;
+                a.out.hit[r] = h ? 1 : 0;
+                a.out.t[r] = h ? bt : __int_as_float(0x7f800000);
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    a.out.normal[3 * (int64_t)r + k] = h ? S.nrm[k][s] : 0.f;
+                    a.out.albedo[3 * (int64_t)r + k] = h ? S.alb[k][s] : 0.f;
+                }
+                if (a.out.leaf) a.out.leaf[r] = bleaf;
+                if (a.out.n_queries) a.out.n_queries[r] = nq;
+                S.ray[s] = -1;
+            }
         }
+        if (tid == 0) atomicAdd(&a.ctr->n_queries, (unsigned long long)nv);
         __syncthreads();
     }
+    if (tid == 0) atomicMax(&a.ctr->max_iter, iters);
 }
 
 // ------------------------------------------------------------------ debug: encode points
+// The product encode (encode_chunk_sm) on caller-supplied points, indices exposed.
 template <int F>
 __global__ void __launch_bounds__(128) k_debug_encode(DebugEncodeArgs a) {
+    __shared__ LevelSm lv[kMaxLevels];
+    stage_levels(a.g, lv, threadIdx.x);
+    __syncthreads();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= a.m) return;
-    const float x[3] = {a.pts[3 * i], a.pts[3 * i + 1], a.pts[3 * i + 2]};
+    const float x0 = a.pts[3 * i], x1 = a.pts[3 * i + 1], x2 = a.pts[3 * i + 2];
     const int L = a.g.L;
     const int chunks = (L * F) / 8;
+    const uint32_t hmask = (1u << a.g.log2_T) - 1u;
     uint32_t idx[64];
     for (int c = 0; c < chunks; ++c) {
         const int l0 = c * 8 / F;
-        uint4 v = encode_chunk<F>(a.g, x, l0, a.index ? idx : nullptr);
+        uint4 v = encode_chunk_sm<F>(lv, a.g.table, hmask, x0, x1, x2, l0, a.index ? idx : nullptr);
         reinterpret_cast<uint4*>(a.feat + i * (int64_t)L * F)[c] = v;
         if (a.index)
             for (int j = 0; j < 8 / F * 8; ++j) a.index[(i * L + l0) * 8 + j] = idx[j];
@@ -332,10 +435,7 @@ __global__ void __launch_bounds__(256, 2) k_debug_mlp(DebugMlpArgs a) {
 }
 
 // ------------------------------------------------------------------ launchers
-size_t wave_smem_bytes(int d_in, int hidden) {
-    return (size_t)kTileQ * (d_in + 8) * 2 + (size_t)mlp_smem_halves(d_in, hidden) * 2 + kTileQ * 8 * 4 +
-           (64 * hidden + 8) * 4 + kTileQ * sizeof(QueryDesc);
-}
+size_t query_smem_bytes(int d_in, int hidden, int n_points) { return QuerySmemPlan(d_in, hidden, n_points).total; }
 size_t mlp_smem_bytes(int d_in, int hidden) {
     return (size_t)kTileQ * (d_in + 8) * 2 + (size_t)mlp_smem_halves(d_in, hidden) * 2 + kTileQ * 8 * 4 +
            (64 * hidden + 8) * 4;
@@ -352,31 +452,41 @@ static int resident_blocks(Kern k, int threads, size_t smem) {
     return (per_sm > 0 ? per_sm : 1) * sms;
 }
 
+// Persistent grid: every resident CTA slot of the device (2 per SM at the cfg-2 shape).
 template <int F, int D>
-static cudaError_t launch_wave_t(const WaveArgs& a, cudaStream_t s) {
-    const size_t smem = wave_smem_bytes(D, a.m.hidden);
-    static int grid_by_hidden[kMaxHidden + 1] = {0};
-    int& grid = grid_by_hidden[a.m.hidden];
-    if (!grid) grid = resident_blocks(k_query_wave<F, D>, 256, smem);
-    k_query_wave<F, D><<<grid, 256, smem, s>>>(a);
+static cudaError_t launch_query_t(const QueryArgs& a, int64_t max_work, cudaStream_t s) {
+    const size_t smem = query_smem_bytes(D, a.m.hidden, a.g.n_points);
+    if (smem > 227 * 1024) return cudaErrorInvalidValue;
+    // occupancy is queried once per (hidden, n_points) shape
+    static int cached[kMaxHidden + 1][9] = {};
+    int& grid_c = cached[a.m.hidden][a.g.n_points < 9 ? a.g.n_points : 8];
+    if (!grid_c) grid_c = resident_blocks(k_query<F, D>, 256, smem);
+    int grid = grid_c;
+    const int64_t need = (max_work + kTileQ - 1) / kTileQ;
+    if (need < grid) grid = (int)(need > 0 ? need : 1);
+    k_query<F, D><<<grid, 256, smem, s>>>(a);
     return cudaGetLastError();
 }
 
-cudaError_t launch_query_wave(const WaveArgs& a, cudaStream_t s) {
+cudaError_t launch_query(const QueryArgs& a, int64_t max_work, cudaStream_t s) {
     const int F = a.g.F, D = a.m.d_in;
-    if (F == 2 && D == 32) return launch_wave_t<2, 32>(a, s);
-    if (F == 2 && D == 64) return launch_wave_t<2, 64>(a, s);
-    if (F == 2 && D == 96) return launch_wave_t<2, 96>(a, s);
-    if (F == 2 && D == 128) return launch_wave_t<2, 128>(a, s);
-    if (F == 4 && D == 64) return launch_wave_t<4, 64>(a, s);
-    if (F == 4 && D == 96) return launch_wave_t<4, 96>(a, s);
-    if (F == 4 && D == 128) return launch_wave_t<4, 128>(a, s);
+    if (F == 2 && D == 32) return launch_query_t<2, 32>(a, max_work, s);
+    if (F == 2 && D == 64) return launch_query_t<2, 64>(a, max_work, s);
+    if (F == 2 && D == 96) return launch_query_t<2, 96>(a, max_work, s);
+    if (F == 2 && D == 128) return launch_query_t<2, 128>(a, max_work, s);
+    if (F == 4 && D == 64) return launch_query_t<4, 64>(a, max_work, s);
+    if (F == 4 && D == 96) return launch_query_t<4, 96>(a, max_work, s);
+    if (F == 4 && D == 128) return launch_query_t<4, 128>(a, max_work, s);
     return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_traverse(const TraverseArgs& a, cudaStream_t s) {
     const int64_t blocks = (a.n_rays + 127) / 128;
-    k_traverse<<<(unsigned)blocks, 128, 0, s>>>(a);
+    const size_t smem = (size_t)(a.cut.depth + 2) * 128 * sizeof(int);
+    if (a.cap <= 2) k_traverse<2><<<(unsigned)blocks, 128, smem, s>>>(a);
+    else if (a.cap <= 4) k_traverse<4><<<(unsigned)blocks, 128, smem, s>>>(a);
+    else if (a.cap <= 8) k_traverse<8><<<(unsigned)blocks, 128, smem, s>>>(a);
+    else k_traverse<16><<<(unsigned)blocks, 128, smem, s>>>(a);
     return cudaGetLastError();
 }
 

@@ -16,16 +16,21 @@ struct HitsDev {
     int32_t* n_queries;
 };
 
-// Per-ray wave state, structure of arrays.
+// Per-ray list bookkeeping written by k_traverse and read when a ray enters a query slot.
 struct RayState {
-    int32_t* pos;     // global index of the current list entry
-    int32_t* base;    // global index of list slot 0
     int32_t* nbuf;    // entries held in the list buffer
     int32_t* more;    // 1 if intersected leaves beyond the buffer may exist (C6)
-    float* bt;        // best hit t
-    float* bte;       // its t_enter
-    int32_t* bleaf;   // its leaf (-1: none)
-    int32_t* nq;      // queries so far
+};
+
+// Device counters of one nbvh_query call (zeroed by one memset per call).
+struct QueryCounters {
+    int32_t err;                  // bit 0: traversal stack overflow
+    int32_t refills;              // list re-traversals (C6)
+    int32_t cnt;                  // rays with >= 1 intersected leaf (k_traverse append count)
+    int32_t next;                 // work-list cursor of the persistent query kernel
+    int32_t max_iter;             // slot iterations of the busiest CTA
+    int32_t pad[3];
+    unsigned long long n_queries; // neural queries (ray, leaf) evaluated
 };
 
 struct TraverseArgs {
@@ -39,8 +44,7 @@ struct TraverseArgs {
     RayState st;
     HitsDev out;
     int32_t* act_out;
-    int32_t* cnt_out;
-    int32_t* err;
+    QueryCounters* ctr;
 };
 
 struct DebugTraverseArgs {
@@ -55,7 +59,7 @@ struct DebugTraverseArgs {
     int32_t* err;
 };
 
-struct WaveArgs {
+struct QueryArgs {
     GridDev g;
     MlpDev m;
     CutDev cut;
@@ -66,16 +70,15 @@ struct WaveArgs {
     int32_t* lst_leaf;
     float* lst_te;
     float* lst_tx;
-    RayState st;
+    const int32_t* nbuf;
+    const int32_t* more;
     HitsDev out;
-    const int32_t* act_in;
-    int32_t* act_out;
-    const int32_t* cnt_in;
-    int32_t* cnt_out;
+    const int32_t* act;      // work list: rays with >= 1 leaf (k_traverse)
+    const int32_t* cnt;      // its length (device)
+    int32_t* next;           // work-list cursor
     float* z_trace;
     int32_t trace_cap;
-    int32_t* n_refills;
-    int32_t* err;
+    QueryCounters* ctr;
 };
 
 struct DebugEncodeArgs {
@@ -95,7 +98,8 @@ struct DebugMlpArgs {
 
 cudaError_t launch_traverse(const TraverseArgs& a, cudaStream_t s);
 cudaError_t launch_debug_traverse(const DebugTraverseArgs& a, cudaStream_t s);
-cudaError_t launch_query_wave(const WaveArgs& a, cudaStream_t s);
+cudaError_t launch_query(const QueryArgs& a, int64_t max_work, cudaStream_t s);
+size_t query_smem_bytes(int d_in, int hidden, int n_points);
 cudaError_t launch_debug_encode(const DebugEncodeArgs& a, cudaStream_t s);
 cudaError_t launch_debug_mlp(const DebugMlpArgs& a, cudaStream_t s);
 

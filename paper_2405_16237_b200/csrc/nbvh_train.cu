@@ -2,7 +2,9 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstring>
+#include <utility>
 #include <vector>
 
 #include <cmath>
@@ -83,6 +85,21 @@ nbvh_status upload_cut(nbvh_ctx* c, int lod) {
     nbvh_status st = check_device(c);
     if (st) return st;
     const HostCut& hc = c->cuts[lod];
+    // the device traversal stack holds 64 entries: at most depth+1 are live (P:163 shallow hierarchy)
+    int32_t cut_depth = 0;
+    if (hc.n_leaves > 1) {
+        std::vector<std::pair<int32_t, int32_t>> todo{{0, 1}};
+        int32_t depth = 0;
+        while (!todo.empty()) {
+            auto [i0, dpt] = todo.back();
+            todo.pop_back();
+            depth = std::max(depth, dpt);
+            for (int32_t ch : {hc.inner[i0].l, hc.inner[i0].r})
+                if (ch >= 0) todo.push_back({ch, dpt + 1});
+        }
+        if (depth > 62) return fail(c, NBVH_EINVAL, "cut hierarchy deeper than the 62 levels the traversal stack holds");
+        cut_depth = depth;
+    }
     std::vector<float4> box(2 * (size_t)hc.n_leaves);
     for (int32_t i = 0; i < hc.n_leaves; ++i) {
         box[2 * i] = make_float4(hc.leaf_lo[3 * i], hc.leaf_lo[3 * i + 1], hc.leaf_lo[3 * i + 2], 0.f);
@@ -95,6 +112,7 @@ nbvh_status upload_cut(nbvh_ctx* c, int lod) {
     if (e == cudaSuccess) e = upload(&d.leaf_base, hc.leaf_base.data(), hc.leaf_base.size());
     if (e == cudaSuccess) e = upload(&d.rank, hc.rank.data(), hc.rank.size());
     if (e != cudaSuccess) return cuda_fail(c, e, "upload_cut");
+    d.depth = cut_depth;
     return NBVH_OK;
 }
 
@@ -203,8 +221,10 @@ static cudaError_t launch_train_fd(const TrainArgs& a, int64_t n, int64_t w_off,
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int H = a.m.hidden;
     const size_t smem_fwd = (size_t)kTileQ * (D + 8) * 2 + (size_t)mlp_smem_halves(D, H) * 2 + kTileQ * 8 * 4 +
-                            (64 * H + 8) * 4 + kTileQ * sizeof(SampleDesc);
-    const size_t smem_bwd = ((size_t)64 * (D + 8) + (size_t)(H - 1) * 64 * 72 + 16 * 72) * 2 + kTileQ * sizeof(SampleDesc);
+                            (64 * H + 8) * 4 + kTileQ * sizeof(SampleDesc) + kMaxLevels * sizeof(LevelSm) +
+                            (size_t)kTileQ * a.g.n_points * 3 * 4;
+    const size_t smem_bwd = ((size_t)64 * (D + 8) + (size_t)(H - 1) * 64 * 72 + 16 * 72) * 2 + kTileQ * sizeof(SampleDesc) +
+                            kMaxLevels * sizeof(LevelSm) + (size_t)kTileQ * a.g.n_points * 3 * 4;
     const size_t smem_dw = (size_t)kTileQ * 72 * 2 + (size_t)kTileQ * (D + 8) * 2 + kTileQ * 8 * 4;
     cudaFuncSetAttribute(k_train_fwd<F, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fwd);
     cudaFuncSetAttribute(k_train_bwd<F, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bwd);

@@ -295,31 +295,42 @@ __global__ void __launch_bounds__(256, 1) k_train_fwd(TrainArgs a) {
     float* zt = reinterpret_cast<float*>(ms.wo + 8 * 72);
     ms.b = zt + kTileQ * 8;
     SampleDesc* qd = reinterpret_cast<SampleDesc*>(ms.b + 64 * a.m.hidden + 8);
+    LevelSm* lv = reinterpret_cast<LevelSm*>(qd + kTileQ);
+    float* xs = reinterpret_cast<float*>(lv + kMaxLevels);             // [n_pts*3][kTileQ]
     stage_mlp(a.m, ms, tid, blockDim.x);
+    stage_levels(a.g, lv, tid);
     const int L = a.g.L, n_pts = a.g.n_points;
-    const int chunks_per_point = (L * F) / 8;
+    const int cpp = (L * F) / 8;
     const int H = a.m.hidden;
     const int g = lane >> 2, t = lane & 3;
+    const uint32_t hmask = (1u << a.g.log2_T) - 1u;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        const int nv = min(kTileQ, M - tile * kTileQ);
         if (tid < kTileQ) {
             SampleDesc q;
             load_sample_desc(a, tile * kTileQ + tid, M, q);
             qd[tid] = q;
+            if (q.valid)
+                for (int p = 0; p < n_pts; ++p) {   // jittered stratified points (C8)
+                    float x[3];
+                    segment_point(a.g, q.o, q.d, q.t0, q.t1, p, n_pts, q.xi, x);
+                    xs[(p * 3 + 0) * kTileQ + tid] = x[0];
+                    xs[(p * 3 + 1) * kTileQ + tid] = x[1];
+                    xs[(p * 3 + 2) * kTileQ + tid] = x[2];
+                }
         }
         __syncthreads();
-        {
-            const int q = tid & (kTileQ - 1);
-            const SampleDesc& Q = qd[q];
-            for (int c = tid >> 7; c < D / 8; c += 2) {
-                uint4 v = make_uint4(0, 0, 0, 0);
-                if (Q.valid) {
-                    const int p = c / chunks_per_point;
-                    const int l0 = ((c % chunks_per_point) * 8) / F;
-                    float x[3];
-                    segment_point(a.g, Q.o, Q.d, Q.t0, Q.t1, p, n_pts, Q.xi, x);
-                    v = encode_chunk<F>(a.g, x, l0, nullptr);
+        {   // encode: warp item = (32-sample block, 16-byte chunk); lanes = samples
+            const int nqb = (nv + 31) >> 5;
+            for (int it = warp; it < nqb * (D / 8); it += 8) {
+                const int c = it / nqb, qb = it - c * nqb;
+                const int q = qb * 32 + lane;
+                if (q < nv) {
+                    const int p = c / cpp, l0 = (c - p * cpp) * (8 / F);
+                    *reinterpret_cast<uint4*>(feat + q * (D + 8) + c * 8) = encode_chunk_sm<F>(
+                        lv, a.g.table, hmask, xs[(p * 3 + 0) * kTileQ + q], xs[(p * 3 + 1) * kTileQ + q],
+                        xs[(p * 3 + 2) * kTileQ + q], l0, nullptr);
                 }
-                *reinterpret_cast<uint4*>(feat + q * (D + 8) + c * 8) = v;
             }
         }
         __syncthreads();
@@ -453,18 +464,18 @@ struct BwdSmem {
 };
 
 template <int F>
-__device__ __forceinline__ void scatter_pair(const TrainArgs& a, const SampleDesc& Q, int c, float gx, float gy) {
-    const int L = a.g.L;
-    const int LF = L * F;
+__device__ __forceinline__ void scatter_pair(const TrainArgs& a, const LevelSm* lv, uint32_t hmask, const float* xs,
+                                             int q, int c, float gx, float gy) {
+    const int LF = a.g.L * F;
     const int p = c / LF;
-    const int l = (c % LF) / F;
-    const int f = c % F;
-    float x[3];
-    segment_point(a.g, Q.o, Q.d, Q.t0, Q.t1, p, a.g.n_points, Q.xi, x);
+    const int l = (c - p * LF) / F;
+    const int f = c - (c / F) * F;
     Cell cell;
-    level_cell(a.g, l, x, cell);
-    float* base = a.grad + (int64_t)a.g.offset[l] * F + f;
-    const bool dense = a.g.dense[l];
+    const LevelSm P = lv[l];
+    level_cell_sm(P, hmask, xs[(p * 3 + 0) * kTileQ + q], xs[(p * 3 + 1) * kTileQ + q], xs[(p * 3 + 2) * kTileQ + q],
+                  cell);
+    float* base = a.grad + (int64_t)P.off * F + f;
+    const bool dense = P.n1 != 0;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
         float* dst = base + (int64_t)cell.idx[k] * F;
@@ -500,6 +511,10 @@ __global__ void __launch_bounds__(256, 1) k_train_bwd(TrainArgs a) {
     s.wh = s.w0 + 64 * (D + 8);
     s.wo = s.wh + (H - 1) * 64 * 72;
     SampleDesc* qd = reinterpret_cast<SampleDesc*>(s.wo + 16 * 72);
+    LevelSm* lv = reinterpret_cast<LevelSm*>(qd + kTileQ);
+    float* xs = reinterpret_cast<float*>(lv + kMaxLevels);             // [n_pts*3][kTileQ]
+    stage_levels(a.g, lv, tid);
+    const uint32_t hmask = (1u << a.g.log2_T) - 1u;
     {   // stage weights (fp16 inference copy == forward operands)
         const uint4* W = reinterpret_cast<const uint4*>(a.m.W);
         const int cpr0 = D / 8;
@@ -518,6 +533,14 @@ __global__ void __launch_bounds__(256, 1) k_train_bwd(TrainArgs a) {
             SampleDesc q;
             load_sample_desc(a, tile * kTileQ + tid, M, q);
             qd[tid] = q;
+            if (q.valid)
+                for (int p = 0; p < a.g.n_points; ++p) {
+                    float x[3];
+                    segment_point(a.g, q.o, q.d, q.t0, q.t1, p, a.g.n_points, q.xi, x);
+                    xs[(p * 3 + 0) * kTileQ + tid] = x[0];
+                    xs[(p * 3 + 1) * kTileQ + tid] = x[1];
+                    xs[(p * 3 + 2) * kTileQ + tid] = x[2];
+                }
         }
         __syncthreads();
         const int r0 = warp * 16;
@@ -575,8 +598,6 @@ __global__ void __launch_bounds__(256, 1) k_train_bwd(TrainArgs a) {
         }
         // dL/dx = delta_0 W_0  ([16 x 64] x [64 x D]), scattered two n-tiles at a time
         const uint32_t w0b = (uint32_t)__cvta_generic_to_shared(s.w0 + (lane & 15) * (D + 8) + (lane >> 4) * 8);
-        const SampleDesc& Q0 = qd[r0 + g];
-        const SampleDesc& Q1 = qd[r0 + g + 8];
 #pragma unroll 1
         for (int np = 0; np < D / 16; ++np) {
             float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
@@ -590,8 +611,8 @@ __global__ void __launch_bounds__(256, 1) k_train_bwd(TrainArgs a) {
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
                 const int c = (2 * np + j) * 8 + 2 * t;
-                if (v0) scatter_pair<F>(a, Q0, c, acc[j][0], acc[j][1]);
-                if (v1) scatter_pair<F>(a, Q1, c, acc[j][2], acc[j][3]);
+                if (v0) scatter_pair<F>(a, lv, hmask, xs, r0 + g, c, acc[j][0], acc[j][1]);
+                if (v1) scatter_pair<F>(a, lv, hmask, xs, r0 + g + 8, c, acc[j][2], acc[j][3]);
             }
         }
         __syncthreads();

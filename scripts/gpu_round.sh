@@ -20,7 +20,7 @@ if [ "${SKIP_NCU:-0}" != "1" ]; then
       --log-file $OUT/launches_$TAG.csv $CMD > $OUT/ncu_launches.log 2>&1
   echo "ncu launches exit $?" >> $OUT/ncu_launches.log
   # the first (largest) wave and the traversal of the first query
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_query_wave|k_traverse" -s 0 -c 2 \
-      -o $OUT/prof_wave_$TAG -f $CMD > $OUT/ncu_full.log 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_query|k_traverse" -s 0 -c 2 \
+      -o $OUT/prof_query_$TAG -f $CMD > $OUT/ncu_full.log 2>&1
   echo "ncu full exit $?" >> $OUT/ncu_full.log
 fi

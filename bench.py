@@ -251,6 +251,8 @@ def run_ours(args):
         e2e = {"value": n * args.steps * world / float(e2e_t.item()) / 1e6, "unit": "Mrays/s",
                "h2d_bytes_per_step": n * 32, "d2h_bytes_per_step": d2h}
 
+    train = bench_train(ctx, args, world, rank) if args.train else None
+
     line = None
     if rank == 0:
         cpu = cpu_oracle_rate(ctx, c, rays_np, target_s=args.cpu_seconds) if args.cpu_seconds > 0 else None
@@ -278,12 +280,64 @@ def run_ours(args):
                          "traverse_ms_per_step": statistics.mean(trav_ms),
                          "mlp_tflops": mean_q * mlp_flops / wave_s / 1e12,
                          "mlp_frac_of_bf16_peak": mean_q * mlp_flops / wave_s / 1e12 / tflops},
-            "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks.summary(),
+            "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks.summary(), "train": train,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def bench_train(ctx, args, world, rank):
+    """BASELINE cfg 5: training-step throughput on the cfg-2 scene and grid.  Global batch
+    2^20 rays split over the ranks (strong scaling); per step every rank runs
+    nbvh_train_backward on its shard, all-reduces the flat gradient buffer (NCCL, N>1) and
+    applies Adam.  Rays: origins uniform in the 50%-inflated box, uniform directions
+    (P:142); acceptance draws and jitter are inputs (C28)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2405_16237_b200 import dp
+    n_global = 1 << 20
+    sl = dp.shard(n_global, rank, world)
+    cut = ctx.cut(0)
+    ctx.set_leaf_rank(np.zeros(cut["n_leaves"], np.float32))
+    h = synth.CONFIGS["1080p"]["hash"]
+    batches = []
+    for b in range(2):
+        rays = synth.random_rays(n_global, seed=7000 + b)[sl]
+        u = synth.random_uniform(n_global, seed=7100 + b)[sl]
+        xi = synth.random_uniform(n_global * h.n_points, seed=7200 + b).reshape(n_global, h.n_points)[sl]
+        batches.append(tuple(torch.from_numpy(np.ascontiguousarray(x)).cuda() for x in (rays, u, xi)))
+    stream = torch.cuda.current_stream()
+    for i in range(args.warmup):
+        dp.train_step_dp(ctx, *batches[i % 2])
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for i in range(args.steps):
+        dp.train_step_dp(ctx, *batches[i % 2])
+    t1.record(stream)
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / args.steps
+    tm = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+    ms = float(tm.item())
+    st = ctx.train_stats()
+    ctx.set_profiling(True)
+    dp.train_step_dp(ctx, *batches[0])
+    torch.cuda.synchronize()
+    ph = ctx.train_stats()["ms_phase"]
+    ctx.set_profiling(False)
+    _, n_grad = ctx.grad_buffer()
+    return {"metric": "training rays/s (BASELINE cfg 5)", "value": n_global / (ms / 1e3) / 1e6, "unit": "Mrays/s",
+            "global_batch": n_global, "scaling": "strong", "ms_per_step": ms,
+            "accepted_per_step_rank0": st["n_accepted"], "first_hit_per_step_rank0": st["n_first_hit"],
+            "phase_ms_rank0": ph, "allreduce_bytes": 4 * n_grad if world > 1 else 0,
+            "gpu_launches_per_step": st["n_launches"]}
 
 
 def run_reference(args):
@@ -341,6 +395,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle timing budget (0 = skip)")
     ap.add_argument("--list-cap", type=int, default=8, help="per-ray ordered leaf-list capacity K (C6)")
+    ap.add_argument("--train", type=int, default=1, help="also time the cfg-5 training step (1/0)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -77,7 +77,7 @@ typedef struct {
     int32_t n_points;       /* samples per ray segment (three; BASELINE: 4)          */
     int32_t hidden_layers;  /* hidden layers of width 64 (4; BASELINE: 2 or 3)       */
     int32_t width;          /* hidden width; must be 64                                     */
-    int32_t list_cap;       /* per-ray ordered leaf-list capacity K, 1..32 (C6)             */
+    int32_t list_cap;       /* per-ray ordered leaf-list capacity K, 1..16, default 8 (C6) */
     int32_t mode;           /* 0 = nearest confident hit (R2), 1 = first confident hit (R1) (C5) */
     float inflate_rel;      /* node inflation, fraction of node diagonal (C15: 1e-3)        */
     float inflate_abs;      /* node inflation floor, fraction of scene diagonal (C15: 1e-6) */
@@ -114,6 +114,8 @@ typedef struct {
     double loss_terms[4];    /* sums of vis, dist, normal, albedo terms (weights 2,2,1,1 applied) */
     int32_t n_launches;
     int32_t skipped;         /* 1 if the update was rejected (non-finite)                   */
+    float ms_phase[6];       /* profiling on: device time of select (T1), label (T2),
+                                fwd+loss (T3-T5), bwd+scatter (T6/T7), dW (T6), Adam (T9)  */
 } nbvh_train_stats;
 
 /* ---------------------------------------------------------------- lifecycle */

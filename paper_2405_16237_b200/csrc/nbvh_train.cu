@@ -40,6 +40,7 @@ struct TrainWork {
     int32_t lod = 0;
     int32_t launches = 0;
     cudaStream_t stream = nullptr;
+    bool profiled = false, adam_profiled = false;
 };
 
 template <typename T>
@@ -213,9 +214,10 @@ void reset_adam(nbvh_ctx* c) {
 }
 
 // launchers (templated on F, D)
+// ev (nullable): 6 events recorded before select and after select, label, fwd, bwd, dW
 template <int F, int D>
 static cudaError_t launch_train_fd(const TrainArgs& a, int64_t n, int64_t w_off, int64_t b_off, cudaStream_t s,
-                                   int* launches) {
+                                   int* launches, cudaEvent_t* ev) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -230,14 +232,20 @@ static cudaError_t launch_train_fd(const TrainArgs& a, int64_t n, int64_t w_off,
     cudaFuncSetAttribute(k_train_bwd<F, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bwd);
     cudaFuncSetAttribute(k_train_dw<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_dw);
     const unsigned blocks_n = (unsigned)((n + 127) / 128);
+    if (ev) cudaEventRecord(ev[0], s);
     k_train_select<<<blocks_n, 128, 0, s>>>(a);
+    if (ev) cudaEventRecord(ev[1], s);
     k_train_label<<<blocks_n, 128, 0, s>>>(a);
+    if (ev) cudaEventRecord(ev[2], s);
     const int tiles = (int)((n + kTileQ - 1) / kTileQ);
     const int grid = tiles < sms ? (tiles > 0 ? tiles : 1) : sms;
     k_train_fwd<F, D><<<grid, 256, smem_fwd, s>>>(a);
+    if (ev) cudaEventRecord(ev[3], s);
     k_train_bwd<F, D><<<grid, 256, smem_bwd, s>>>(a);
+    if (ev) cudaEventRecord(ev[4], s);
     const unsigned dw_grid = (unsigned)((n + kDwChunk - 1) / kDwChunk);
     k_train_dw<D><<<dw_grid > 0 ? dw_grid : 1, 256, smem_dw, s>>>(a, w_off, b_off);
+    if (ev) cudaEventRecord(ev[5], s);
     *launches += 5;
     return cudaGetLastError();
 }
@@ -337,13 +345,20 @@ extern "C" nbvh_status nbvh_train_backward(nbvh_ctx* c, const nbvh_ray* rays, in
     const int64_t w_off = c->n_table, b_off = c->n_table + c->n_W;
     const int F = c->cfg.F, D = c->d_in;
     int launches = 0;
-    if (F == 2 && D == 32) e = launch_train_fd<2, 32>(a, n, w_off, b_off, s, &launches);
-    else if (F == 2 && D == 64) e = launch_train_fd<2, 64>(a, n, w_off, b_off, s, &launches);
-    else if (F == 2 && D == 96) e = launch_train_fd<2, 96>(a, n, w_off, b_off, s, &launches);
-    else if (F == 2 && D == 128) e = launch_train_fd<2, 128>(a, n, w_off, b_off, s, &launches);
-    else if (F == 4 && D == 64) e = launch_train_fd<4, 64>(a, n, w_off, b_off, s, &launches);
-    else if (F == 4 && D == 96) e = launch_train_fd<4, 96>(a, n, w_off, b_off, s, &launches);
-    else if (F == 4 && D == 128) e = launch_train_fd<4, 128>(a, n, w_off, b_off, s, &launches);
+    cudaEvent_t evs[6];
+    cudaEvent_t* ev = nullptr;
+    if (c->profiling) {
+        for (int i = 0; i < 6; ++i) evs[i] = ctx_event(c, 16 + i);
+        ev = evs;
+    }
+    w->profiled = c->profiling;
+    if (F == 2 && D == 32) e = launch_train_fd<2, 32>(a, n, w_off, b_off, s, &launches, ev);
+    else if (F == 2 && D == 64) e = launch_train_fd<2, 64>(a, n, w_off, b_off, s, &launches, ev);
+    else if (F == 2 && D == 96) e = launch_train_fd<2, 96>(a, n, w_off, b_off, s, &launches, ev);
+    else if (F == 2 && D == 128) e = launch_train_fd<2, 128>(a, n, w_off, b_off, s, &launches, ev);
+    else if (F == 4 && D == 64) e = launch_train_fd<4, 64>(a, n, w_off, b_off, s, &launches, ev);
+    else if (F == 4 && D == 96) e = launch_train_fd<4, 96>(a, n, w_off, b_off, s, &launches, ev);
+    else if (F == 4 && D == 128) e = launch_train_fd<4, 128>(a, n, w_off, b_off, s, &launches, ev);
     else return fail(c, NBVH_EINVAL, "train_backward: unsupported (F, D_in)");
     if (e != cudaSuccess) return cuda_fail(c, e, "train_backward: launch");
     k_store_count<<<1, 1, 0, s>>>(w->counters, a.tail);
@@ -373,6 +388,7 @@ extern "C" nbvh_status nbvh_apply_update(nbvh_ctx* c, float lr, void* stream) {
     const int64_t np = n_params(c);
     cudaError_t e = cudaMemsetAsync(w->counters + 2, 0, 4, s);
     if (e != cudaSuccess) return cuda_fail(c, e, "apply_update");
+    if (c->profiling) cudaEventRecord(ctx_event(c, 22), s);
     k_check_finite<<<592, 256, 0, s>>>(w->grad, np, w->counters + 2);
     w->step += 1;
     AdamArgs a{};
@@ -394,6 +410,8 @@ extern "C" nbvh_status nbvh_apply_update(nbvh_ctx* c, float lr, void* stream) {
     a.W16 = c->d_W16;
     a.n_W = c->n_W;
     k_adam<<<1184, 256, 0, s>>>(a);
+    if (c->profiling) cudaEventRecord(ctx_event(c, 23), s);
+    w->adam_profiled = c->profiling;
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(c, e, "apply_update: adam");
     w->launches += 2;
@@ -426,6 +444,11 @@ extern "C" nbvh_status nbvh_get_train_stats(nbvh_ctx* c, nbvh_train_stats* out) 
     for (int k = 0; k < 4; ++k) c->tstats.loss_terms[k] = la[1 + k];
     c->tstats.n_launches = w->launches;
     c->tstats.skipped = cnt[2] != 0;
+    for (int k = 0; k < 6; ++k) c->tstats.ms_phase[k] = 0.f;
+    if (w->profiled)
+        for (int k = 0; k < 5; ++k) cudaEventElapsedTime(&c->tstats.ms_phase[k], c->events[16 + k], c->events[17 + k]);
+    if (w->adam_profiled) cudaEventElapsedTime(&c->tstats.ms_phase[5], c->events[22], c->events[23]);
+    cudaGetLastError();
     *out = c->tstats;
     return cnt[2] ? NBVH_ENONFINITE : NBVH_OK;
 }

@@ -47,7 +47,7 @@ class QueryStats(C.Structure):
 class TrainStats(C.Structure):
     _fields_ = [("n_rays", C.c_int64), ("n_first_hit", C.c_int64), ("n_accepted", C.c_int64),
                 ("loss_sum", C.c_double), ("loss_terms", C.c_double * 4), ("n_launches", C.c_int32),
-                ("skipped", C.c_int32)]
+                ("skipped", C.c_int32), ("ms_phase", C.c_float * 6)]
 
 
 _lib = None
@@ -292,7 +292,8 @@ class Context:
         s = TrainStats()
         self._ck(self.lib.nbvh_get_train_stats(self.h, C.byref(s)), "train_stats")
         return dict(n_rays=s.n_rays, n_first_hit=s.n_first_hit, n_accepted=s.n_accepted, loss_sum=s.loss_sum,
-                    loss_terms=list(s.loss_terms), n_launches=s.n_launches, skipped=s.skipped)
+                    loss_terms=list(s.loss_terms), n_launches=s.n_launches, skipped=s.skipped,
+                    ms_phase=dict(zip(("select", "label", "fwd", "bwd", "dw", "adam"), list(s.ms_phase))))
 
     # ---------------------------------------------------------------- parity hooks
     def debug_traverse(self, rays, cap, lod=0, stream=None):

@@ -65,6 +65,7 @@ GridDev make_grid(const nbvh_ctx* c, int lod) {
         g.res[l] = c->res[l];
         g.dense[l] = c->dense[l];
         g.offset[l] = (uint32_t)c->offset[l];
+        g.inf_offset[l] = (uint32_t)c->inf_offset[l];
     }
     g.table = c->d_table16;
     if (lod >= 0) {
@@ -93,18 +94,53 @@ CutDev make_cut(const nbvh_ctx* c, int lod) {
     return d;
 }
 
-// fp32 master -> fp16 inference copy (tables and weights; biases stay fp32).
+// fp32 master -> fp16 inference copy (MLP weights; biases stay fp32).
 __global__ void k_refresh_fp16(const float* __restrict__ src, __half* __restrict__ dst, int64_t n) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     for (; i < n; i += (int64_t)gridDim.x * blockDim.x) dst[i] = __float2half_rn(src[i]);
 }
 
+// fp32 master tables -> fp16 inference table: hashed levels copied, dense levels
+// corner-packed (LevelSm in nbvh_device.cuh).  One thread per inference entry.
+__global__ void k_refresh_table(const float* __restrict__ src, __half* __restrict__ dst, GridDev g, int64_t n_inf) {
+    __shared__ LevelSm lv[kMaxLevels];
+    stage_levels(g, lv, threadIdx.x);
+    __syncthreads();
+    const int F = g.F, L = g.L;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n_inf;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        int l = 0;
+        while (l + 1 < L && (int64_t)lv[l + 1].off <= e) ++l;
+        const LevelSm P = lv[l];
+        const uint32_t k = (uint32_t)(e - P.off);
+        uint32_t canon;
+        if (P.nx) {
+            const uint32_t cell = k >> 3, corner = k & 7u;
+            const uint32_t cz = cell / P.nxy, rem = cell - cz * P.nxy;
+            const uint32_t cy = rem / P.nx, cx = rem - cy * P.nx;
+            canon = (cx + (corner & 1u)) + (cy + ((corner >> 1) & 1u)) * P.n1 + (cz + ((corner >> 2) & 1u)) * P.n1sq;
+        } else {
+            canon = k;
+        }
+        const float* sp = src + ((int64_t)P.coff + canon) * F;
+        __half* dp = dst + e * F;
+        for (int f = 0; f < F; ++f) dp[f] = __float2half_rn(sp[f]);
+    }
+}
+
 nbvh_status refresh_fp16(nbvh_ctx* c, cudaStream_t s) {
     const int64_t nt = c->n_table, nw = c->n_W;
-    k_refresh_fp16<<<1184, 256, 0, s>>>(c->d_params, c->d_table16, nt);
+    k_refresh_table<<<1184, 256, 0, s>>>(c->d_params, c->d_table16, make_grid(c, -1), c->n_inf);
     k_refresh_fp16<<<148, 256, 0, s>>>(c->d_params + nt, c->d_W16, nw);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(c, e, "refresh_fp16");
+    return NBVH_OK;
+}
+
+nbvh_status refresh_table(nbvh_ctx* c, cudaStream_t s) {
+    k_refresh_table<<<1184, 256, 0, s>>>(c->d_params, c->d_table16, make_grid(c, -1), c->n_inf);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(c, e, "refresh_table");
     return NBVH_OK;
 }
 
@@ -158,6 +194,20 @@ extern "C" nbvh_status nbvh_create(const nbvh_config* cfg, int cuda_device, nbvh
     x->d_in = d_in;
     level_table(c.L, c.log2_T, c.base_res, c.max_res, x->res, x->dense, x->offset, &x->n_entries);
     x->n_table = x->n_entries * c.F;
+    {   // inference layout: dense levels corner-packed (8 entries per cell), 8-entry aligned
+        int64_t o = 0;
+        for (int l = 0; l < c.L; ++l) {
+            x->inf_offset[l] = o;
+            const int64_t N = x->res[l];
+            o += x->dense[l] ? 8 * N * N * N : (int64_t)1 << c.log2_T;
+            o = (o + 7) & ~(int64_t)7;
+        }
+        x->n_inf = o;
+        if (o >= ((int64_t)1 << 32)) {
+            delete x;
+            return NBVH_EINVAL;
+        }
+    }
     x->n_W = (int64_t)64 * d_in + (int64_t)(c.hidden_layers - 1) * 64 * 64 + 8 * 64;
     x->n_b = (int64_t)64 * c.hidden_layers + 8;
     // C21 initialisation
@@ -174,7 +224,7 @@ extern "C" nbvh_status nbvh_create(const nbvh_config* cfg, int cuda_device, nbvh
     if (cuda_device >= 0) {
         cudaError_t e = cudaSetDevice(cuda_device);
         if (e == cudaSuccess) e = dalloc(&x->d_params, x->h_params.size());
-        if (e == cudaSuccess) e = dalloc(&x->d_table16, x->n_table);
+        if (e == cudaSuccess) e = dalloc(&x->d_table16, x->n_inf * c.F);
         if (e == cudaSuccess) e = dalloc(&x->d_W16, x->n_W);
         if (e == cudaSuccess) e = dalloc(&x->d_misc, 64);
         if (e == cudaSuccess) e = cudaMallocHost((void**)&x->h_misc, 64 * sizeof(int32_t));

@@ -43,6 +43,8 @@ struct nbvh_ctx {
     int32_t dense[nbvh::kMaxLevels] = {0};
     int64_t offset[nbvh::kMaxLevels] = {0};
     int64_t n_entries = 0;
+    int64_t inf_offset[nbvh::kMaxLevels] = {0};   // inference-table entry offsets (dense levels corner-packed)
+    int64_t n_inf = 0;                             // inference-table entries
     int32_t d_in = 0;
     int64_t n_table = 0, n_W = 0, n_b = 0;
 
@@ -99,6 +101,7 @@ GridDev make_grid(const nbvh_ctx* c, int lod);
 MlpDev make_mlp(const nbvh_ctx* c);
 CutDev make_cut(const nbvh_ctx* c, int lod);
 nbvh_status refresh_fp16(nbvh_ctx* c, cudaStream_t s);
+nbvh_status refresh_table(nbvh_ctx* c, cudaStream_t s);
 cudaEvent_t ctx_event(nbvh_ctx* c, int i);
 nbvh_status resolve_query_stats(nbvh_ctx* c);
 // nbvh_train.cu

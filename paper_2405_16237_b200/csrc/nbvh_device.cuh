@@ -31,8 +31,9 @@ struct GridDev {
     int32_t L, F, n_points, log2_T;
     int32_t res[kMaxLevels];
     int32_t dense[kMaxLevels];
-    uint32_t offset[kMaxLevels];     // entry offset of each level
-    const __half* table;             // fp16 [n_entries][F]
+    uint32_t offset[kMaxLevels];     // canonical entry offset of each level (parameter layout)
+    uint32_t inf_offset[kMaxLevels]; // entry offset of each level in the inference table
+    const __half* table;             // fp16 inference table (layout: see LevelSm)
     float dom_min[3];
     float dom_inv;
 };
@@ -349,13 +350,22 @@ __device__ __forceinline__ unsigned long long h2_to_f2(uint32_t h) {
 }
 
 // ------------------------------------------------------------------ level table in shared memory
-// One 16-byte record per level, read with a single broadcast LDS.128 by every lane of a warp
-// (all lanes of a warp encode the same level at the same time).  n1 == 0 marks a hashed
-// level; otherwise n1 = N+1 and n1sq = (N+1)^2 (dense index, C2).
+// The fp16 *inference* table keeps hashed levels in the parameter layout (T entries of F
+// halves) but stores every dense level corner-packed: cell c = x + N*y + N^2*z holds its 8
+// corner entries (corner bit0 = x, bit1 = y, bit2 = z) contiguously, 16*F bytes, so one
+// dense (point, level) lookup is ONE 32-byte sector (F=2: one 256-bit load) instead of 8
+// scattered 4-byte gathers.  It is a re-layout of the same parameters (rebuilt from the
+// fp32 master after every update, k_refresh_table), not a different model.
+// One 32-byte record per level: the first 16 bytes are what the encode reads (one
+// broadcast LDS.128 per level: all lanes of a warp encode the same level at once), the
+// second 16 bytes the canonical layout (training scatter, parity hooks).
 struct LevelSm {
     float resf;          // N_l as float (exact: N_l < 2^24)
-    uint32_t off;        // entry offset of the level in the concatenated table
-    uint32_t n1, n1sq;
+    uint32_t off;        // entry offset of the level in the inference table
+    uint32_t nx, nxy;    // dense: N, N^2 (packed-cell index); hashed: 0, 0
+    uint32_t coff;       // canonical entry offset (gradient / parameter layout)
+    uint32_t n1, n1sq;   // dense: N+1, (N+1)^2 (canonical vertex index, C2); hashed: 0, 0
+    uint32_t pad;
 };
 
 // Stage the level table from the kernel parameter block with compile-time indices only
@@ -365,13 +375,34 @@ __device__ __forceinline__ void stage_levels(const GridDev& g, LevelSm* lv, int 
 #pragma unroll
     for (int l = 0; l < kMaxLevels; ++l) {
         if (tid == l && l < g.L) {
-            const uint32_t n1 = (uint32_t)g.res[l] + 1u;
+            const uint32_t N = (uint32_t)g.res[l], n1 = N + 1u;
+            const bool dn = g.dense[l] != 0;
             lv[l].resf = (float)g.res[l];
-            lv[l].off = g.offset[l];
-            lv[l].n1 = g.dense[l] ? n1 : 0u;
-            lv[l].n1sq = n1 * n1;
+            lv[l].off = g.inf_offset[l];
+            lv[l].nx = dn ? N : 0u;
+            lv[l].nxy = dn ? N * N : 0u;
+            lv[l].coff = g.offset[l];
+            lv[l].n1 = dn ? n1 : 0u;
+            lv[l].n1sq = dn ? n1 * n1 : 0u;
+            lv[l].pad = 0u;
         }
     }
+}
+
+// 256-bit read-only global load (sm_100: LDG.E.ENL2.256)
+__device__ __forceinline__ void ldg256(const void* p, uint32_t (&r)[8]) {
+    asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "l"(p));
+}
+
+// floor of s in [0, 2^23) and its integer value without the XU pipe: adding 2^23 with
+// round-toward-minus-infinity leaves floor(s) in the low mantissa bits (exact), so the
+// floor costs one FADD.RM + one FADD + one integer subtract instead of FRND + F2I.
+__device__ __forceinline__ float floor_small(float s, uint32_t& i) {
+    const float t = __fadd_rd(s, 8388608.0f);
+    i = (uint32_t)(__float_as_int(t) - 0x4B000000);
+    return __fsub_rn(t, 8388608.0f);
 }
 
 // Cell of one level from the shared-memory level record: corner indices within the level
@@ -381,10 +412,13 @@ __device__ __forceinline__ void level_cell_sm(const LevelSm& P, uint32_t hmask, 
                                               Cell& c) {
     const float s0 = __fmul_rn(x0, P.resf), s1 = __fmul_rn(x1, P.resf), s2 = __fmul_rn(x2, P.resf);
     const float top = __fsub_rn(P.resf, 1.0f);
-    const float c0 = fminf(floorf(s0), top), c1 = fminf(floorf(s1), top), c2 = fminf(floorf(s2), top);
+    const uint32_t itop = (uint32_t)__float_as_int(__fadd_rd(top, 8388608.0f)) - 0x4B000000u;
+    uint32_t i0, i1, i2;
+    const float c0 = fminf(floor_small(s0, i0), top), c1 = fminf(floor_small(s1, i1), top),
+                c2 = fminf(floor_small(s2, i2), top);
+    i0 = min(i0, itop); i1 = min(i1, itop); i2 = min(i2, itop);
     const float f0 = __fsub_rn(s0, c0), f1 = __fsub_rn(s1, c1), f2 = __fsub_rn(s2, c2);
-    const uint32_t i0 = (uint32_t)c0, i1 = (uint32_t)c1, i2 = (uint32_t)c2;
-    if (P.n1) {
+    if (P.n1) {   // canonical dense vertex index (C2)
         const uint32_t b = i0 + i1 * P.n1 + i2 * P.n1sq;
 #pragma unroll
         for (int k = 0; k < 8; ++k) c.idx[k] = b + (k & 1) + ((k >> 1) & 1) * P.n1 + ((k >> 2) & 1) * P.n1sq;
@@ -400,58 +434,87 @@ __device__ __forceinline__ void level_cell_sm(const LevelSm& P, uint32_t hmask, 
     for (int k = 0; k < 8; ++k) c.w[k] = wx[k & 1] * wy[(k >> 1) & 1] * wz[(k >> 2) & 1];
 }
 
-// Encode NL = 8/F consecutive levels l0.. of one point x (normalised, in [0,1]^3) into
-// 16 bytes of fp16 features: s = x*N, c = min(floor(s), N-1), f = s - c (exact), corner
-// index dense or hashed (C2, C3), trilinear weights (wx*wy)*wz, blend in fp32 (P:101,
-// P:142).  All 8*NL gathers are issued before the first is consumed.  `tab` points to the
-// fp16 table viewed as 4-byte (F=2) or 8-byte (F=4) entries.  idx_out (nullable) receives
-// the 8*NL corner indices within their levels (parity hook).
+// In-flight state of one 16-byte chunk: the gathered corner entries and the cell fractions.
 template <int F>
-__device__ __forceinline__ uint4 encode_chunk_sm(const LevelSm* lv, const void* tab, uint32_t hmask, float x0,
-                                                 float x1, float x2, int l0, uint32_t* idx_out) {
-    constexpr int NL = 8 / F;
+struct ChunkGather {
     using Entry = typename std::conditional<F == 2, uint32_t, uint2>::type;
+    Entry v[8 / F][8];
+    float fr[8 / F][3];
+};
+
+// Step 1 of encode_chunk_sm: cell, corner indices and all 8*NL gathers issued (the index
+// registers die as soon as the loads are issued; only the fractions are kept).  Splitting
+// issue from finish lets the caller keep two chunks' gathers in flight.
+template <int F>
+__device__ __forceinline__ void encode_issue(const LevelSm* lv, const void* tab, uint32_t hmask, float x0, float x1,
+                                             float x2, int l0, uint32_t* idx_out, ChunkGather<F>& G) {
+    constexpr int NL = 8 / F;
+    static_assert(F == 2 || F == 4, "F must be 2 or 4");
+    using Entry = typename ChunkGather<F>::Entry;
     const Entry* T = reinterpret_cast<const Entry*>(tab);
-    Entry v[NL][8];
-    float fr[NL][3];
-    // 1. per level: cell, corner indices, and the 8 gathers issued at once (the index
-    //    registers die as soon as the loads are issued; only the fractions are kept)
 #pragma unroll
     for (int j = 0; j < NL; ++j) {
         const LevelSm P = lv[l0 + j];
         const float s0 = __fmul_rn(x0, P.resf), s1 = __fmul_rn(x1, P.resf), s2 = __fmul_rn(x2, P.resf);
         const float top = __fsub_rn(P.resf, 1.0f);
-        const float c0 = fminf(floorf(s0), top), c1 = fminf(floorf(s1), top), c2 = fminf(floorf(s2), top);
-        fr[j][0] = __fsub_rn(s0, c0);
-        fr[j][1] = __fsub_rn(s1, c1);
-        fr[j][2] = __fsub_rn(s2, c2);
-        const uint32_t i0 = (uint32_t)c0, i1 = (uint32_t)c1, i2 = (uint32_t)c2;
-        uint32_t idx[8];
-        if (P.n1) {
-            const uint32_t b = i0 + i1 * P.n1 + i2 * P.n1sq;
+        const uint32_t itop = (uint32_t)__float_as_int(__fadd_rd(top, 8388608.0f)) - 0x4B000000u;
+        uint32_t i0, i1, i2;
+        const float c0 = fminf(floor_small(s0, i0), top), c1 = fminf(floor_small(s1, i1), top),
+                    c2 = fminf(floor_small(s2, i2), top);
+        i0 = min(i0, itop); i1 = min(i1, itop); i2 = min(i2, itop);
+        G.fr[j][0] = __fsub_rn(s0, c0);
+        G.fr[j][1] = __fsub_rn(s1, c1);
+        G.fr[j][2] = __fsub_rn(s2, c2);
+        if (idx_out) {   // parity hook: canonical corner indices within the level
+            if (P.nx) {
+                const uint32_t b = i0 + i1 * P.n1 + i2 * P.n1sq;
 #pragma unroll
-            for (int k = 0; k < 8; ++k) idx[k] = b + (k & 1) + ((k >> 1) & 1) * P.n1 + ((k >> 2) & 1) * P.n1sq;
+                for (int k = 0; k < 8; ++k)
+                    idx_out[j * 8 + k] = b + (k & 1) + ((k >> 1) & 1) * P.n1 + ((k >> 2) & 1) * P.n1sq;
+            } else {
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    idx_out[j * 8 + k] = ((i0 + (k & 1)) ^ ((i1 + ((k >> 1) & 1)) * kPrime1) ^
+                                          ((i2 + ((k >> 2) & 1)) * kPrime2)) & hmask;
+            }
+        }
+        if (P.nx) {
+            // dense level: the cell's 8 corners are one contiguous 16*F-byte record
+            const uint32_t cell = i0 + i1 * P.nx + i2 * P.nxy;
+            if constexpr (F == 2) {
+                ldg256(T + (P.off + 8u * cell), G.v[j]);
+            } else {
+                uint32_t lo[8], hi[8];
+                ldg256(T + (P.off + 8u * cell), lo);
+                ldg256(T + (P.off + 8u * cell + 4u), hi);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    G.v[j][k] = make_uint2(lo[2 * k], lo[2 * k + 1]);
+                    G.v[j][4 + k] = make_uint2(hi[2 * k], hi[2 * k + 1]);
+                }
+            }
         } else {
+            // hashed level (C3): (x*1 ^ y*pi2 ^ z*pi3) mod T, masks distributed
             const uint32_t hx[2] = {i0 & hmask, (i0 + 1u) & hmask};
             const uint32_t hy[2] = {(i1 * kPrime1) & hmask, ((i1 + 1u) * kPrime1) & hmask};
             const uint32_t hz[2] = {(i2 * kPrime2) & hmask, ((i2 + 1u) * kPrime2) & hmask};
+            // 32-bit entry index (n_entries < 2^32), one IMAD.WIDE.U32 per gather address
 #pragma unroll
-            for (int k = 0; k < 8; ++k) idx[k] = hx[k & 1] ^ hy[(k >> 1) & 1] ^ hz[(k >> 2) & 1];
+            for (int k = 0; k < 8; ++k)
+                G.v[j][k] = __ldg(T + (P.off + (hx[k & 1] ^ hy[(k >> 1) & 1] ^ hz[(k >> 2) & 1])));
         }
-        if (idx_out) {
-#pragma unroll
-            for (int k = 0; k < 8; ++k) idx_out[j * 8 + k] = idx[k];
-        }
-        // 32-bit entry index (n_entries < 2^32), one IMAD.WIDE.U32 per gather address
-#pragma unroll
-        for (int k = 0; k < 8; ++k) v[j][k] = __ldg(T + (P.off + idx[k]));
     }
-    // 2. trilinear weights (wx*wy)*wz and the fp32 blend, level by level
+}
+
+// Step 2: trilinear weights (wx*wy)*wz and the fp32 blend, level by level -> 8 halves.
+template <int F>
+__device__ __forceinline__ uint4 encode_finish(const ChunkGather<F>& G) {
+    constexpr int NL = 8 / F;
     uint4 out;
     uint32_t* o32 = reinterpret_cast<uint32_t*>(&out);
 #pragma unroll
     for (int j = 0; j < NL; ++j) {
-        const float f0 = fr[j][0], f1 = fr[j][1], f2 = fr[j][2];
+        const float f0 = G.fr[j][0], f1 = G.fr[j][1], f2 = G.fr[j][2];
         const unsigned long long wx = pk2(1.0f - f0, f0);
         const unsigned long long wxy0 = mul2(wx, pk2(1.0f - f1, 1.0f - f1));
         const unsigned long long wxy1 = mul2(wx, pk2(f1, f1));
@@ -465,7 +528,7 @@ __device__ __forceinline__ uint4 encode_chunk_sm(const LevelSm* lv, const void* 
         if constexpr (F == 2) {
             unsigned long long acc = 0ull;   // (+0, +0)
 #pragma unroll
-            for (int k = 0; k < 8; ++k) acc = fma2s(w[k], h2_to_f2(v[j][k]), acc);
+            for (int k = 0; k < 8; ++k) acc = fma2s(w[k], h2_to_f2(G.v[j][k]), acc);
             const float2 a = upk2(acc);
             __half2 h = __floats2half2_rn(a.x, a.y);
             o32[j] = *reinterpret_cast<uint32_t*>(&h);
@@ -473,8 +536,8 @@ __device__ __forceinline__ uint4 encode_chunk_sm(const LevelSm* lv, const void* 
             unsigned long long a01 = 0ull, a23 = 0ull;
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
-                a01 = fma2s(w[k], h2_to_f2(v[j][k].x), a01);
-                a23 = fma2s(w[k], h2_to_f2(v[j][k].y), a23);
+                a01 = fma2s(w[k], h2_to_f2(G.v[j][k].x), a01);
+                a23 = fma2s(w[k], h2_to_f2(G.v[j][k].y), a23);
             }
             const float2 p = upk2(a01), q = upk2(a23);
             __half2 h0 = __floats2half2_rn(p.x, p.y), h1 = __floats2half2_rn(q.x, q.y);
@@ -483,6 +546,19 @@ __device__ __forceinline__ uint4 encode_chunk_sm(const LevelSm* lv, const void* 
         }
     }
     return out;
+}
+
+// Encode NL = 8/F consecutive levels l0.. of one point x (normalised, in [0,1]^3) into
+// 16 bytes of fp16 features: s = x*N, c = min(floor(s), N-1), f = s - c (exact), corner
+// entries (dense: corner-packed cell record; hashed: 8 gathers, C2, C3), trilinear weights
+// (wx*wy)*wz, blend in fp32.  idx_out (nullable) receives the 8*NL
+// canonical corner indices within their levels (parity hook).
+template <int F>
+__device__ __forceinline__ uint4 encode_chunk_sm(const LevelSm* lv, const void* tab, uint32_t hmask, float x0,
+                                                 float x1, float x2, int l0, uint32_t* idx_out) {
+    ChunkGather<F> G;
+    encode_issue<F>(lv, tab, hmask, x0, x1, x2, l0, idx_out, G);
+    return encode_finish<F>(G);
 }
 
 // ------------------------------------------------------------------ tensor-core MLP

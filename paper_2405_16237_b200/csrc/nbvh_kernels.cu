@@ -133,172 +133,169 @@ __device__ __noinline__ int refill_list(CutDev cut, const float4* rays, int64_t 
     return n;
 }
 
-// Per-CTA ray slots (structure of arrays in shared memory).  Thread s < kTileQ owns slot s
-// for the refill and decode phases; the encode and MLP phases work on the compacted list
-// of occupied slots.
-struct SlotSm {
-    int32_t ray[kTileQ], pos[kTileQ], base[kTileQ], nbuf[kTileQ], more[kTileQ], bleaf[kTileQ], nq[kTileQ],
-        leaf[kTileQ];
-    float o[3][kTileQ], d[3][kTileQ];
-    float bt[kTileQ], bte[kTileQ], te[kTileQ], tx[kTileQ];
-    float nrm[3][kTileQ], alb[3][kTileQ];
-    int32_t act[kTileQ];
-    int32_t wcnt[2][kTileQ / 32];
-    int32_t base_idx;
-    int32_t pad[3];
-};
+// Ray slots of one warp (structure of arrays in shared memory).  Lane s < kWarpQ owns slot
+// s for the refill and decode steps; the encode and MLP steps work on the compacted rows.
+constexpr int kWarpQ = 16;          // queries per warp iteration (one m16 MMA row block)
+constexpr int kQueryWarps = 16;     // warps per CTA (one CTA per SM; bounded by shared memory)
 
-// Exclusive rank of `pred` among the slot-owning threads (tid < kTileQ) in slot order, and
-// the total.  Called by the whole block; contains one __syncthreads.
-__device__ __forceinline__ int slot_rank(bool pred, int32_t* wcnt, int tid, int& total) {
-    const unsigned m = __ballot_sync(0xffffffffu, pred);
-    const int warp = tid >> 5, lane = tid & 31;
-    if (lane == 0 && warp < kTileQ / 32) wcnt[warp] = __popc(m);
-    __syncthreads();
-    int off = 0;
-    total = 0;
-#pragma unroll
-    for (int w = 0; w < kTileQ / 32; ++w) {
-        const int c = wcnt[w];
-        off += w < warp ? c : 0;
-        total += c;
-    }
-    return off + __popc(m & ((1u << lane) - 1u));
-}
+struct WarpSlots {
+    int32_t ray[kWarpQ], pos[kWarpQ], base[kWarpQ], nbuf[kWarpQ], more[kWarpQ], bleaf[kWarpQ], nq[kWarpQ],
+        leaf[kWarpQ], act[kWarpQ];
+    float o[3][kWarpQ], d[3][kWarpQ];
+    float bt[kWarpQ], bte[kWarpQ], te[kWarpQ], tx[kWarpQ];
+    float nrm[3][kWarpQ], alb[3][kWarpQ];
+};
 
 __host__ __device__ constexpr size_t align16(size_t b) { return (b + 15) & ~(size_t)15; }
 
-// Shared-memory plan of k_query (bytes), shared by the kernel and its launcher.
+// Shared-memory plan of k_query (bytes), shared by the kernel and its launcher: the MLP
+// weights and level table once per CTA, then one private region per warp.
 struct QuerySmemPlan {
-    size_t feat, w, z, bias, lv, xs, slots, total;
+    size_t w, bias, lv, warp0, feat, z, xs, slots, per_warp, total;
+    int warps;
     __host__ __device__ QuerySmemPlan(int d_in, int hidden, int n_points) {
-        feat = 0;
-        w = feat + align16((size_t)kTileQ * (d_in + 8) * 2);
-        z = w + align16((size_t)mlp_smem_halves(d_in, hidden) * 2);
-        bias = z + align16((size_t)kTileQ * 8 * 4);
+        w = 0;
+        bias = w + align16((size_t)mlp_smem_halves(d_in, hidden) * 2);
         lv = bias + align16((size_t)(64 * hidden + 8) * 4);
-        xs = lv + align16(sizeof(LevelSm) * kMaxLevels);
-        slots = xs + align16((size_t)kTileQ * n_points * 3 * 4);
-        total = slots + align16(sizeof(SlotSm));
+        warp0 = lv + align16(sizeof(LevelSm) * kMaxLevels);
+        feat = 0;                                                   // offsets within a warp region
+        z = feat + align16((size_t)kWarpQ * (d_in + 8) * 2);
+        xs = z + align16((size_t)kWarpQ * 8 * 4);
+        slots = xs + align16((size_t)kWarpQ * n_points * 3 * 4);
+        per_warp = slots + align16(sizeof(WarpSlots));
+        // as many warps (<= kQueryWarps) as fit the 227 KB per-CTA limit
+        const size_t cap = 227 * 1024;
+        warps = warp0 + per_warp > cap ? 0 : (int)((cap - warp0) / per_warp);
+        if (warps > kQueryWarps) warps = kQueryWarps;
+        total = warp0 + per_warp * warps;
     }
 };
 
-// One launch processes every ray that intersects the cut (Q2-Q7):
-// each CTA keeps kTileQ ray slots; every iteration it (A) refills empty slots with the next
-// rays of the global work list (one atomic per CTA), (B) compacts the occupied slots,
-// (C) fetches each ray's current leaf segment and its n sample points, (D) hash-grid
-// encodes them into a shared-memory feature tile (warp = one 16-byte feature chunk of 32
-// queries, lanes = queries), (E) runs the MLP on tensor cores, (F) decodes, updates the
-// ray's best hit, decides front-to-back termination and frees the slot of a finished ray
-// after writing its hit record.  Tiles stay full until the work list drains: there are no
-// query waves, host round trips or per-wave weight restaging.
+// One launch processes every ray that intersects the cut (Q2-Q7).
+// Each warp owns kWarpQ ray slots and runs its own loop with no block-wide barrier:
+// (A) refill empty slots with the next rays of the global work list (one atomic per warp),
+// (B) compact the occupied slots, (C) fetch each ray's current leaf segment and its n
+// stratified sample points, (D) hash-grid encode them into the warp's feature rows (lanes =
+// (query, chunk parity)), (E) run the MLP on tensor cores (one m16 row block), (F) decode,
+// update the best hit, decide front-to-back termination and free finished slots after
+// writing the hit record.  Warps drift freely, so one warp's MLP or list refill overlaps
+// other warps' gathers.
 template <int F, int D>
-__global__ void __launch_bounds__(256, 2) k_query(QueryArgs a) {
+__global__ void __launch_bounds__(kQueryWarps * 32, 1) k_query(QueryArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int NP = a.g.n_points;
     const QuerySmemPlan plan(D, a.m.hidden, NP);
-    __half* feat = reinterpret_cast<__half*>(smem_raw + plan.feat);            // [kTileQ][D+8]
     MlpSmem ms;
     ms.w0 = reinterpret_cast<__half*>(smem_raw + plan.w);
     ms.wh = ms.w0 + 64 * (D + 8);
     ms.wo = ms.wh + (a.m.hidden - 1) * 64 * 72;
-    float* zt = reinterpret_cast<float*>(smem_raw + plan.z);                   // [kTileQ][8]
     ms.b = reinterpret_cast<float*>(smem_raw + plan.bias);
     LevelSm* lv = reinterpret_cast<LevelSm*>(smem_raw + plan.lv);
-    float* xs = reinterpret_cast<float*>(smem_raw + plan.xs);                  // [NP*3][kTileQ]
-    SlotSm& S = *reinterpret_cast<SlotSm*>(smem_raw + plan.slots);
+    unsigned char* wbase = smem_raw + plan.warp0 + plan.per_warp * warp;
+    __half* feat = reinterpret_cast<__half*>(wbase + plan.feat);              // [kWarpQ][D+8]
+    float* zt = reinterpret_cast<float*>(wbase + plan.z);                     // [kWarpQ][8]
+    float* xs = reinterpret_cast<float*>(wbase + plan.xs);                    // [NP*3][kWarpQ]
+    WarpSlots& S = *reinterpret_cast<WarpSlots*>(wbase + plan.slots);
 
     stage_mlp(a.m, ms, tid, blockDim.x);
     stage_levels(a.g, lv, tid);
-    if (tid < kTileQ) S.ray[tid] = -1;
+    if (lane < kWarpQ) S.ray[lane] = -1;
+    __syncthreads();                          // the only block-wide barrier
+
     const int total = *a.cnt;                 // rays with >= 1 intersected leaf (k_traverse)
     const uint32_t hmask = (1u << a.g.log2_T) - 1u;
     const void* tab = a.g.table;
     const int cpp = (a.g.L * F) / 8;          // 16-byte chunks per sample point
     constexpr int kChunks = D / 8;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    unsigned long long my_queries = 0;
     int iters = 0;
     bool exhausted = false;
-    __syncthreads();
 
     while (true) {
-        // (A) refill empty slots from the global work list
-        int n_empty;
-        const bool empty = tid < kTileQ && S.ray[tid] < 0;
-        const int erank = slot_rank(empty, S.wcnt[0], tid, n_empty);
-        if (tid == 0) S.base_idx = (n_empty > 0 && !exhausted) ? atomicAdd(a.next, n_empty) : total;
-        __syncthreads();
-        const int bidx = S.base_idx;
-        exhausted = bidx + n_empty >= total;
-        if (empty && bidx + erank < total) {
-            const int r = a.act[bidx + erank];
-            const float4 r0 = __ldg(a.rays + 2 * (int64_t)r), r1 = __ldg(a.rays + 2 * (int64_t)r + 1);
-            S.ray[tid] = r;
-            S.o[0][tid] = r0.x; S.o[1][tid] = r0.y; S.o[2][tid] = r0.z;
-            S.d[0][tid] = r1.x; S.d[1][tid] = r1.y; S.d[2][tid] = r1.z;
-            S.pos[tid] = 0;
-            S.base[tid] = 0;
-            S.nbuf[tid] = a.nbuf[r];
-            S.more[tid] = a.more[r];
-            S.bt[tid] = __int_as_float(0x7f800000);
-            S.bte[tid] = 0.f;
-            S.bleaf[tid] = -1;
-            S.nq[tid] = 0;
+        // (A) refill empty slots from the global work list (consecutive rays per warp)
+        const bool empty = lane < kWarpQ && S.ray[lane] < 0;
+        const unsigned em = __ballot_sync(0xffffffffu, empty);
+        if (em && !exhausted) {
+            const int ne = __popc(em);
+            int base = 0;
+            if (lane == 0) base = atomicAdd(a.next, ne);
+            base = __shfl_sync(0xffffffffu, base, 0);
+            exhausted = base + ne >= total;
+            const int i = base + __popc(em & lt_mask);
+            if (empty && i < total) {
+                const int r = a.act[i];
+                const float4 r0 = __ldg(a.rays + 2 * (int64_t)r), r1 = __ldg(a.rays + 2 * (int64_t)r + 1);
+                S.ray[lane] = r;
+                S.o[0][lane] = r0.x; S.o[1][lane] = r0.y; S.o[2][lane] = r0.z;
+                S.d[0][lane] = r1.x; S.d[1][lane] = r1.y; S.d[2][lane] = r1.z;
+                S.pos[lane] = 0;
+                S.base[lane] = 0;
+                S.nbuf[lane] = a.nbuf[r];
+                S.more[lane] = a.more[r];
+                S.bt[lane] = __int_as_float(0x7f800000);
+                S.bte[lane] = 0.f;
+                S.bleaf[lane] = -1;
+                S.nq[lane] = 0;
+            }
         }
-        // (B) compact the occupied slots (slot order)
-        int nv;
-        const bool occ = tid < kTileQ && (empty ? (bidx + erank < total) : true);
-        const int arank = slot_rank(occ, S.wcnt[1], tid, nv);
-        if (nv == 0) break;
-        if (occ) S.act[arank] = tid;
+        __syncwarp();
+        // (B) compact the occupied slots; (C) current segment + sample points (C8)
+        const bool occ = lane < kWarpQ && S.ray[lane] >= 0;
+        const unsigned om = __ballot_sync(0xffffffffu, occ);
+        const int nv = __popc(om);
+        if (nv == 0) break;                   // work list drained and every slot finished
         ++iters;
-        __syncthreads();
-
-        // (C) current leaf segment and the n stratified sample points (C8)
-        if (tid < nv) {
-            const int s = S.act[tid];
-            const int r = S.ray[s];
-            const int64_t li = (int64_t)(S.pos[s] - S.base[s]) * a.n_rays + r;
+        my_queries += (unsigned long long)nv;
+        if (occ) {
+            const int row = __popc(om & lt_mask);
+            S.act[row] = lane;
+            const int r = S.ray[lane];
+            const int64_t li = (int64_t)(S.pos[lane] - S.base[lane]) * a.n_rays + r;
             const float te = a.lst_te[li], tx = a.lst_tx[li];
-            S.leaf[s] = a.lst_leaf[li];
-            S.te[s] = te;
-            S.tx[s] = tx;
-            const float o[3] = {S.o[0][s], S.o[1][s], S.o[2][s]}, d[3] = {S.d[0][s], S.d[1][s], S.d[2][s]};
+            S.leaf[lane] = a.lst_leaf[li];
+            S.te[lane] = te;
+            S.tx[lane] = tx;
+            const float o[3] = {S.o[0][lane], S.o[1][lane], S.o[2][lane]};
+            const float d[3] = {S.d[0][lane], S.d[1][lane], S.d[2][lane]};
             for (int p = 0; p < NP; ++p) {
                 float x[3];
                 segment_point(a.g, o, d, te, tx, p, NP, nullptr, x);
-                xs[(p * 3 + 0) * kTileQ + tid] = x[0];
-                xs[(p * 3 + 1) * kTileQ + tid] = x[1];
-                xs[(p * 3 + 2) * kTileQ + tid] = x[2];
+                xs[(p * 3 + 0) * kWarpQ + row] = x[0];
+                xs[(p * 3 + 1) * kWarpQ + row] = x[1];
+                xs[(p * 3 + 2) * kWarpQ + row] = x[2];
             }
         }
-        __syncthreads();
-
-        // (D) encode: warp w owns feature chunks w, w+8, ...; lanes = 32 consecutive queries
+        __syncwarp();
+        // (D) encode.  kWarpQ = 16: lane -> row q = lane % 16; the two half-warps take sample
+        //     points of opposite parity at the same levels (neighbouring points of the same
+        //     rays: coherent lines).  kWarpQ = 32: lane = row, all chunks.
         {
-            const int nqb = (nv + 31) >> 5;
-            for (int c = warp; c < kChunks; c += 8) {
-                const int p = c / cpp, l0 = (c - p * cpp) * (8 / F);
-                const float* xp = xs + p * 3 * kTileQ;
-                for (int qb = 0; qb < nqb; ++qb) {
-                    const int q = qb * 32 + lane;
-                    if (q < nv)
-                        *reinterpret_cast<uint4*>(feat + q * (D + 8) + c * 8) = encode_chunk_sm<F>(
-                            lv, tab, hmask, xp[q], xp[kTileQ + q], xp[2 * kTileQ + q], l0, nullptr);
+            constexpr int kHalves = 32 / kWarpQ;
+            const int q = lane & (kWarpQ - 1), h = lane / kWarpQ;
+            if (q < nv) {
+                for (int p = h; p < NP; p += kHalves) {
+                    const float* xp = xs + p * 3 * kWarpQ;
+                    const float x0 = xp[q], x1 = xp[kWarpQ + q], x2 = xp[2 * kWarpQ + q];
+                    for (int lc = 0; lc < cpp; ++lc) {
+                        const int c = p * cpp + lc;
+                        *reinterpret_cast<uint4*>(feat + q * (D + 8) + c * 8) =
+                            encode_chunk_sm<F>(lv, tab, hmask, x0, x1, x2, lc * (8 / F), nullptr);
+                    }
                 }
             }
         }
-        __syncthreads();
-
-        // (E) MLP on tensor cores: warp w -> rows 16w..16w+15 (rows >= nv are ignored)
-        if (warp * 16 < nv) mlp_rows16<D>(ms, a.m.hidden, feat, warp * 16, zt, lane);
-        __syncthreads();
-
+        __syncwarp();
+        // (E) MLP on tensor cores: the warp's rows in m16 blocks (rows >= nv are ignored)
+        mlp_rows16<D>(ms, a.m.hidden, feat, 0, zt, lane);
+        if (kWarpQ > 16 && nv > 16) mlp_rows16<D>(ms, a.m.hidden, feat, 16, zt, lane);
+        __syncwarp();
         // (F) decode, best hit, front-to-back termination
-        if (tid < nv) {
-            const int s = S.act[tid];
+        if (lane < nv) {
+            const int s = S.act[lane];
             const int r = S.ray[s];
-            const float* z = zt + tid * 8;
+            const float* z = zt + lane * 8;
             int pos = S.pos[s];
             if (a.z_trace && pos < a.trace_cap) {
                 float4* dst = reinterpret_cast<float4*>(a.z_trace + ((int64_t)r * a.trace_cap + pos) * 8);
@@ -340,7 +337,8 @@ __global__ void __launch_bounds__(256, 2) k_query(QueryArgs a) {
                     if (!S.more[s]) {
                         done = true;                                         // every intersected leaf visited
                     } else {
-                        // list exhausted, more leaves may remain: resume after the last key (C6)
+                        // list exhausted, more leaves may remain: resume after the last key,
+                        // bounded by the best hit (C6)
                         int more = 0;
                         nbuf = refill_list(a.cut, a.rays, a.n_rays, a.cap, a.lst_leaf, a.lst_te, a.lst_tx, a.ctr, r,
                                            nbuf, bleaf >= 0 ? bt : __int_as_float(0x7f800000), &more);
@@ -373,10 +371,12 @@ __global__ void __launch_bounds__(256, 2) k_query(QueryArgs a) {
                 S.ray[s] = -1;
             }
         }
-        if (tid == 0) atomicAdd(&a.ctr->n_queries, (unsigned long long)nv);
-        __syncthreads();
+        __syncwarp();
     }
-    if (tid == 0) atomicMax(&a.ctr->max_iter, iters);
+    if (lane == 0) {
+        atomicAdd(&a.ctr->n_queries, my_queries);
+        atomicMax(&a.ctr->max_iter, iters);
+    }
 }
 
 // ------------------------------------------------------------------ debug: encode points
@@ -452,19 +452,20 @@ static int resident_blocks(Kern k, int threads, size_t smem) {
     return (per_sm > 0 ? per_sm : 1) * sms;
 }
 
-// Persistent grid: every resident CTA slot of the device (2 per SM at the cfg-2 shape).
+// Persistent grid: one CTA of kQueryWarps warps per SM.
 template <int F, int D>
 static cudaError_t launch_query_t(const QueryArgs& a, int64_t max_work, cudaStream_t s) {
-    const size_t smem = query_smem_bytes(D, a.m.hidden, a.g.n_points);
-    if (smem > 227 * 1024) return cudaErrorInvalidValue;
+    const QuerySmemPlan plan(D, a.m.hidden, a.g.n_points);
+    if (plan.warps < 1) return cudaErrorInvalidValue;
+    const size_t smem = plan.total;
     // occupancy is queried once per (hidden, n_points) shape
     static int cached[kMaxHidden + 1][9] = {};
     int& grid_c = cached[a.m.hidden][a.g.n_points < 9 ? a.g.n_points : 8];
-    if (!grid_c) grid_c = resident_blocks(k_query<F, D>, 256, smem);
+    if (!grid_c) grid_c = resident_blocks(k_query<F, D>, plan.warps * 32, smem);
     int grid = grid_c;
-    const int64_t need = (max_work + kTileQ - 1) / kTileQ;
+    const int64_t need = (max_work + plan.warps * kWarpQ - 1) / (plan.warps * kWarpQ);
     if (need < grid) grid = (int)(need > 0 ? need : 1);
-    k_query<F, D><<<grid, 256, smem, s>>>(a);
+    k_query<F, D><<<grid, plan.warps * 32, smem, s>>>(a);
     return cudaGetLastError();
 }
 

@@ -410,11 +410,13 @@ extern "C" nbvh_status nbvh_apply_update(nbvh_ctx* c, float lr, void* stream) {
     a.W16 = c->d_W16;
     a.n_W = c->n_W;
     k_adam<<<1184, 256, 0, s>>>(a);
+    st = refresh_table(c, s);
+    if (st) return st;
     if (c->profiling) cudaEventRecord(ctx_event(c, 23), s);
     w->adam_profiled = c->profiling;
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(c, e, "apply_update: adam");
-    w->launches += 2;
+    w->launches += 3;
     w->stream = s;
     return NBVH_OK;
 }

@@ -474,7 +474,7 @@ __device__ __forceinline__ void scatter_pair(const TrainArgs& a, const LevelSm* 
     const LevelSm P = lv[l];
     level_cell_sm(P, hmask, xs[(p * 3 + 0) * kTileQ + q], xs[(p * 3 + 1) * kTileQ + q], xs[(p * 3 + 2) * kTileQ + q],
                   cell);
-    float* base = a.grad + (int64_t)P.off * F + f;
+    float* base = a.grad + (int64_t)P.coff * F + f;
     const bool dense = P.n1 != 0;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
@@ -755,7 +755,8 @@ struct AdamArgs {
 };
 
 // P:275 Adam with default hyper-parameters (C20): dense, bias-corrected; the gradient is
-// the batch mean (sum / accepted count).  The fp16 inference copy is refreshed in place.
+// the batch mean (sum / accepted count).  The fp16 MLP weights are refreshed in place; the
+// fp16 inference table is rebuilt afterwards by k_refresh_table (corner-packed layout).
 __global__ void k_adam(AdamArgs a) {
     if (*a.bad) return;
     const float scale = 1.0f / fmaxf(1.0f, *a.count);
@@ -767,8 +768,7 @@ __global__ void k_adam(AdamArgs a) {
         a.v[i] = v;
         const float p = a.param[i] - a.lr * (m / a.c1) / (sqrtf(v / a.c2) + a.eps);
         a.param[i] = p;
-        if (i < a.n_table) a.table16[i] = __float2half_rn(p);
-        else if (i < a.n_table + a.n_W) a.W16[i - a.n_table] = __float2half_rn(p);
+        if (i >= a.n_table && i < a.n_table + a.n_W) a.W16[i - a.n_table] = __float2half_rn(p);
     }
 }
 

@@ -226,7 +226,8 @@ static cudaError_t launch_train_fd(const TrainArgs& a, int64_t n, int64_t w_off,
                             (64 * H + 8) * 4 + kTileQ * sizeof(SampleDesc) + kMaxLevels * sizeof(LevelSm) +
                             (size_t)kTileQ * a.g.n_points * 3 * 4;
     const size_t smem_bwd = ((size_t)64 * (D + 8) + (size_t)(H - 1) * 64 * 72 + 16 * 72) * 2 + kTileQ * sizeof(SampleDesc) +
-                            kMaxLevels * sizeof(LevelSm) + (size_t)kTileQ * a.g.n_points * 3 * 4;
+                            kMaxLevels * sizeof(LevelSm) + (size_t)kTileQ * a.g.n_points * 3 * 4 +
+                            (size_t)kTileQ * (D + 4) * 4 + (size_t)a.priv_floats * 4;
     const size_t smem_dw = (size_t)kTileQ * 72 * 2 + (size_t)kTileQ * (D + 8) * 2 + kTileQ * 8 * 4;
     cudaFuncSetAttribute(k_train_fwd<F, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fwd);
     cudaFuncSetAttribute(k_train_bwd<F, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bwd);
@@ -342,6 +343,15 @@ extern "C" nbvh_status nbvh_train_backward(nbvh_ctx* c, const nbvh_ray* rays, in
     a.tail = w->grad + n_params(c);
     a.loss_acc = w->loss_acc;
     a.cap = w->cap;
+    // coarse dense levels whose gradients fit a 24 KB CTA-private accumulator (prefix)
+    a.priv_levels = 0;
+    a.priv_floats = 0;
+    for (int l = 0; l < c->cfg.L && c->dense[l]; ++l) {
+        const int64_t end = (c->offset[l] + (int64_t)(c->res[l] + 1) * (c->res[l] + 1) * (c->res[l] + 1)) * c->cfg.F;
+        if (end * 4 > 24 * 1024) break;
+        a.priv_levels = l + 1;
+        a.priv_floats = (int32_t)end;
+    }
     const int64_t w_off = c->n_table, b_off = c->n_table + c->n_W;
     const int F = c->cfg.F, D = c->d_in;
     int launches = 0;

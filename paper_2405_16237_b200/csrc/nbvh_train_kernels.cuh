@@ -54,6 +54,8 @@ struct TrainArgs {
     float* tail;             // [0] accepted count, [1 + 3*leaf + {0,1,2}] loss sum, samples, first hits
     double* loss_acc;        // [5]: total, vis, dist, normal, albedo (weights applied)
     int64_t cap;             // capacity of the per-sample arrays
+    int32_t priv_levels;     // coarse levels accumulated in shared memory by k_train_bwd
+    int32_t priv_floats;     // their gradient floats (levels 0..priv_levels-1 are a prefix)
 };
 
 // ------------------------------------------------------------------ T1 select
@@ -463,41 +465,6 @@ struct BwdSmem {
     __half* wo;   // [16][72], rows 8..15 zero
 };
 
-template <int F>
-__device__ __forceinline__ void scatter_pair(const TrainArgs& a, const LevelSm* lv, uint32_t hmask, const float* xs,
-                                             int q, int c, float gx, float gy) {
-    const int LF = a.g.L * F;
-    const int p = c / LF;
-    const int l = (c - p * LF) / F;
-    const int f = c - (c / F) * F;
-    Cell cell;
-    const LevelSm P = lv[l];
-    level_cell_sm(P, hmask, xs[(p * 3 + 0) * kTileQ + q], xs[(p * 3 + 1) * kTileQ + q], xs[(p * 3 + 2) * kTileQ + q],
-                  cell);
-    float* base = a.grad + (int64_t)P.coff * F + f;
-    const bool dense = P.n1 != 0;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        float* dst = base + (int64_t)cell.idx[k] * F;
-        float vx = cell.w[k] * gx, vy = cell.w[k] * gy;
-        if (dense) {
-            // warp-aggregated atomics: lanes hitting the same entry combine first
-            const unsigned active = __activemask();
-            const unsigned peers = __match_any_sync(active, (unsigned long long)dst);
-            const int leader = __ffs(peers) - 1;
-            float sx = 0.f, sy = 0.f;
-            for (unsigned m = peers; m; m &= m - 1) {
-                const int src = __ffs(m) - 1;
-                sx += __shfl_sync(peers, vx, src);
-                sy += __shfl_sync(peers, vy, src);
-            }
-            if ((int)(threadIdx.x & 31) == leader) red_add_v2(dst, sx, sy);
-        } else {
-            red_add_v2(dst, vx, vy);
-        }
-    }
-}
-
 template <int F, int D>
 __global__ void __launch_bounds__(256, 1) k_train_bwd(TrainArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -513,7 +480,10 @@ __global__ void __launch_bounds__(256, 1) k_train_bwd(TrainArgs a) {
     SampleDesc* qd = reinterpret_cast<SampleDesc*>(s.wo + 16 * 72);
     LevelSm* lv = reinterpret_cast<LevelSm*>(qd + kTileQ);
     float* xs = reinterpret_cast<float*>(lv + kMaxLevels);             // [n_pts*3][kTileQ]
+    float* gx = xs + a.g.n_points * 3 * kTileQ;                        // dL/dx [kTileQ][D+4] fp32
+    float* priv = gx + kTileQ * (D + 4);                               // [priv_floats]
     stage_levels(a.g, lv, tid);
+    for (int i = tid; i < a.priv_floats; i += blockDim.x) priv[i] = 0.f;
     const uint32_t hmask = (1u << a.g.log2_T) - 1u;
     {   // stage weights (fp16 inference copy == forward operands)
         const uint4* W = reinterpret_cast<const uint4*>(a.m.W);
@@ -596,7 +566,7 @@ __global__ void __launch_bounds__(256, 1) k_train_bwd(TrainArgs a) {
                 af[kb][3] = pack_half2(acc[2 * kb + 1][2], acc[2 * kb + 1][3]);
             }
         }
-        // dL/dx = delta_0 W_0  ([16 x 64] x [64 x D]), scattered two n-tiles at a time
+        // dL/dx = delta_0 W_0  ([16 x 64] x [64 x D]) -> fp32 tile in shared memory
         const uint32_t w0b = (uint32_t)__cvta_generic_to_shared(s.w0 + (lane & 15) * (D + 8) + (lane >> 4) * 8);
 #pragma unroll 1
         for (int np = 0; np < D / 16; ++np) {
@@ -611,11 +581,51 @@ __global__ void __launch_bounds__(256, 1) k_train_bwd(TrainArgs a) {
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
                 const int c = (2 * np + j) * 8 + 2 * t;
-                if (v0) scatter_pair<F>(a, lv, hmask, xs, r0 + g, c, acc[j][0], acc[j][1]);
-                if (v1) scatter_pair<F>(a, lv, hmask, xs, r0 + g + 8, c, acc[j][2], acc[j][3]);
+                *reinterpret_cast<float2*>(gx + (r0 + g) * (D + 4) + c) = make_float2(acc[j][0], acc[j][1]);
+                *reinterpret_cast<float2*>(gx + (r0 + g + 8) * (D + 4) + c) = make_float2(acc[j][2], acc[j][3]);
             }
         }
         __syncthreads();
+        // T7 scatter: warp item = (32-sample block, point-level); lanes = samples, so
+        // each lane computes its cell once and adds w_k * dL/dfeat to the 8 corner entries.
+        // Coarse dense levels (l < priv_levels) accumulate into a CTA-private shared-memory
+        // copy flushed once per CTA; the rest go straight to the fp32 gradient buffer.
+        {
+            const int nv = min(kTileQ, M - tile * kTileQ);
+            const int nqb = (nv + 31) >> 5;
+            const int npl = a.g.n_points * a.g.L;
+            for (int it = warp; it < nqb * npl; it += 8) {
+                const int pl = it / nqb, qb = it - pl * nqb;
+                const int q = qb * 32 + lane;
+                if (q >= nv) continue;
+                const int p = pl / a.g.L, l = pl - p * a.g.L;
+                const LevelSm P = lv[l];
+                Cell cell;
+                level_cell_sm(P, hmask, xs[(p * 3 + 0) * kTileQ + q], xs[(p * 3 + 1) * kTileQ + q],
+                              xs[(p * 3 + 2) * kTileQ + q], cell);
+                const float* gq = gx + q * (D + 4) + pl * F;
+                if (l < a.priv_levels) {
+#pragma unroll
+                    for (int k = 0; k < 8; ++k)
+                        for (int f = 0; f < F; ++f)
+                            atomicAdd(priv + (P.coff + cell.idx[k]) * F + f, cell.w[k] * gq[f]);
+                } else {
+                    float* base = a.grad + (int64_t)P.coff * F;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        float* dst = base + (int64_t)cell.idx[k] * F;
+                        red_add_v2(dst, cell.w[k] * gq[0], cell.w[k] * gq[1]);
+                        if (F == 4) red_add_v2(dst + 2, cell.w[k] * gq[2], cell.w[k] * gq[3]);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+    // flush the CTA-private coarse-level gradients
+    for (int i = tid; i < a.priv_floats; i += blockDim.x) {
+        const float v = priv[i];
+        if (v != 0.f) atomicAdd(a.grad + i, v);
     }
 }
 

@@ -101,36 +101,46 @@ __global__ void k_refresh_fp16(const float* __restrict__ src, __half* __restrict
 }
 
 // fp32 master tables -> fp16 inference table: hashed levels copied, dense levels
-// corner-packed (LevelSm in nbvh_device.cuh).  One thread per inference entry.
-__global__ void k_refresh_table(const float* __restrict__ src, __half* __restrict__ dst, GridDev g, int64_t n_inf) {
+// corner-packed (LevelSm in nbvh_device.cuh).  blockIdx.y = level; one thread per dense
+// cell (gathers its 8 corners, writes one 16*F-byte record) or per hashed entry.
+__global__ void k_refresh_table(const float* __restrict__ src, __half* __restrict__ dst, GridDev g) {
     __shared__ LevelSm lv[kMaxLevels];
     stage_levels(g, lv, threadIdx.x);
     __syncthreads();
-    const int F = g.F, L = g.L;
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n_inf;
-         e += (int64_t)gridDim.x * blockDim.x) {
-        int l = 0;
-        while (l + 1 < L && (int64_t)lv[l + 1].off <= e) ++l;
-        const LevelSm P = lv[l];
-        const uint32_t k = (uint32_t)(e - P.off);
-        uint32_t canon;
-        if (P.nx) {
-            const uint32_t cell = k >> 3, corner = k & 7u;
+    const int F = g.F;
+    const LevelSm P = lv[blockIdx.y];
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    if (P.nx) {
+        const uint32_t n_cells = P.nxy * P.nx;
+        for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n_cells; c += stride) {
+            const uint32_t cell = (uint32_t)c;
             const uint32_t cz = cell / P.nxy, rem = cell - cz * P.nxy;
             const uint32_t cy = rem / P.nx, cx = rem - cy * P.nx;
-            canon = (cx + (corner & 1u)) + (cy + ((corner >> 1) & 1u)) * P.n1 + (cz + ((corner >> 2) & 1u)) * P.n1sq;
-        } else {
-            canon = k;
+            const uint32_t b = cx + cy * P.n1 + cz * P.n1sq;
+            __align__(16) __half rec[32];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const uint32_t idx = b + (k & 1) + ((k >> 1) & 1) * P.n1 + ((k >> 2) & 1) * P.n1sq;
+                const float* sp = src + ((int64_t)P.coff + idx) * F;
+                for (int f = 0; f < F; ++f) rec[k * F + f] = __float2half_rn(sp[f]);
+            }
+            uint4* d = reinterpret_cast<uint4*>(dst + ((int64_t)P.off + 8ll * cell) * F);
+            const uint4* r = reinterpret_cast<const uint4*>(rec);
+            for (int v = 0; v < F; ++v) d[v] = r[v];            // 16*F bytes
         }
-        const float* sp = src + ((int64_t)P.coff + canon) * F;
-        __half* dp = dst + e * F;
-        for (int f = 0; f < F; ++f) dp[f] = __float2half_rn(sp[f]);
+    } else {
+        const int64_t n = (int64_t)1 << g.log2_T;
+        for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += stride) {
+            const float* sp = src + ((int64_t)P.coff + e) * F;
+            __half* dp = dst + ((int64_t)P.off + e) * F;
+            for (int f = 0; f < F; ++f) dp[f] = __float2half_rn(sp[f]);
+        }
     }
 }
 
 nbvh_status refresh_fp16(nbvh_ctx* c, cudaStream_t s) {
     const int64_t nt = c->n_table, nw = c->n_W;
-    k_refresh_table<<<1184, 256, 0, s>>>(c->d_params, c->d_table16, make_grid(c, -1), c->n_inf);
+    k_refresh_table<<<dim3(148, c->cfg.L), 256, 0, s>>>(c->d_params, c->d_table16, make_grid(c, -1));
     k_refresh_fp16<<<148, 256, 0, s>>>(c->d_params + nt, c->d_W16, nw);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(c, e, "refresh_fp16");
@@ -138,7 +148,7 @@ nbvh_status refresh_fp16(nbvh_ctx* c, cudaStream_t s) {
 }
 
 nbvh_status refresh_table(nbvh_ctx* c, cudaStream_t s) {
-    k_refresh_table<<<1184, 256, 0, s>>>(c->d_params, c->d_table16, make_grid(c, -1), c->n_inf);
+    k_refresh_table<<<dim3(148, c->cfg.L), 256, 0, s>>>(c->d_params, c->d_table16, make_grid(c, -1));
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(c, e, "refresh_table");
     return NBVH_OK;

@@ -207,7 +207,6 @@ __global__ void __launch_bounds__(kQueryWarps * 32, 1) k_query(QueryArgs a) {
     const uint32_t hmask = (1u << a.g.log2_T) - 1u;
     const void* tab = a.g.table;
     const int cpp = (a.g.L * F) / 8;          // 16-byte chunks per sample point
-    constexpr int kChunks = D / 8;
     const unsigned lt_mask = (1u << lane) - 1u;
     unsigned long long my_queries = 0;
     int iters = 0;

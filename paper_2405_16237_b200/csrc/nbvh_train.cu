@@ -234,9 +234,9 @@ static cudaError_t launch_train_fd(const TrainArgs& a, int64_t n, int64_t w_off,
     cudaFuncSetAttribute(k_train_dw<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_dw);
     const unsigned blocks_n = (unsigned)((n + 127) / 128);
     if (ev) cudaEventRecord(ev[0], s);
-    k_train_select<<<blocks_n, 128, 0, s>>>(a);
+    k_train_select<<<blocks_n, 128, (size_t)(a.cut.depth + 2) * 128 * sizeof(int), s>>>(a);
     if (ev) cudaEventRecord(ev[1], s);
-    k_train_label<<<blocks_n, 128, 0, s>>>(a);
+    k_train_label<<<blocks_n, 128, 64 * 128 * sizeof(int), s>>>(a);
     if (ev) cudaEventRecord(ev[2], s);
     const int tiles = (int)((n + kTileQ - 1) / kTileQ);
     const int grid = tiles < sms ? (tiles > 0 ? tiles : 1) : sms;

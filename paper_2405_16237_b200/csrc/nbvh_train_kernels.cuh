@@ -60,6 +60,7 @@ struct TrainArgs {
 
 // ------------------------------------------------------------------ T1 select
 __global__ void __launch_bounds__(128) k_train_select(TrainArgs a) {
+    extern __shared__ int stk_raw[];        // traversal stack [depth+2][128]
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     bool acc = false;
     int leaf = -1;
@@ -68,7 +69,9 @@ __global__ void __launch_bounds__(128) k_train_select(TrainArgs a) {
         RayDev R = load_ray(a.rays, r);
         float lte[1], ltx[1];
         int lid[1], n = 0;
-        int total = collect_leaves<1>(a.cut, R, false, 0.f, 0, 1, lte, ltx, lid, n, nullptr);
+        SmemStack st{stk_raw + threadIdx.x, (int)blockDim.x, a.cut.depth + 2};
+        // first leaf in (t_enter, id) order; the list of 1 prunes every subtree entering later
+        int total = collect_leaves<1, SmemStack>(a.cut, R, false, 0.f, 0, 1, lte, ltx, lid, n, nullptr, st, true);
         if (total > 0) {
             leaf = lid[0];
             te = lte[0];
@@ -150,15 +153,17 @@ __global__ void __launch_bounds__(128) k_train_label(TrainArgs a) {
     const double o[3] = {R.o[0], R.o[1], R.o[2]}, d[3] = {R.d[0], R.d[1], R.d[2]};
     const float t0 = a.s_t0[i], t1 = a.s_t1[i];
     // conservative box test: boxes grown by a relative epsilon so that no triangle the
-    // exact test would accept is pruned
-    int stack[64];
+    // exact test would accept is pruned.  Stack: shared-memory column [64][128].
+    extern __shared__ int stk_raw[];
+    int* stack_col = stk_raw + threadIdx.x;
     int sp = 0;
-    stack[sp++] = a.leaf_base[a.s_leaf[i]];
+#define STACK(i) stack_col[(i) * 128]
+    STACK(sp++) = a.leaf_base[a.s_leaf[i]];
     bool found = false;
     double bt = 0, bb1 = 0, bb2 = 0;
     int btri = -1, bslot = -1;
     while (sp > 0) {
-        const BvhNode nd = a.nodes[stack[--sp]];
+        const BvhNode nd = a.nodes[STACK(--sp)];
         float lo[3], hi[3], te, tx;
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
@@ -179,10 +184,11 @@ __global__ void __launch_bounds__(128) k_train_label(TrainArgs a) {
                 }
             }
         } else if (sp + 2 <= 64) {
-            stack[sp++] = nd.b;
-            stack[sp++] = nd.a;
+            STACK(sp++) = nd.b;
+            STACK(sp++) = nd.a;
         }
     }
+#undef STACK
     float gt[9];
 #pragma unroll
     for (int k = 0; k < 9; ++k) gt[k] = 0.f;

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <utility>
 #include <vector>
@@ -231,7 +232,7 @@ static cudaError_t launch_train_fd(const TrainArgs& a, int64_t n, int64_t w_off,
     const size_t smem_dw = (size_t)kTileQ * 72 * 2 + (size_t)kTileQ * (D + 8) * 2 + kTileQ * 8 * 4;
     cudaFuncSetAttribute(k_train_fwd<F, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fwd);
     cudaFuncSetAttribute(k_train_bwd<F, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bwd);
-    cudaFuncSetAttribute(k_train_dw<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_dw);
+    cudaFuncSetAttribute(k_train_dw<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_dw);
     const unsigned blocks_n = (unsigned)((n + 127) / 128);
     if (ev) cudaEventRecord(ev[0], s);
     k_train_select<<<blocks_n, 128, (size_t)(a.cut.depth + 2) * 128 * sizeof(int), s>>>(a);
@@ -245,7 +246,28 @@ static cudaError_t launch_train_fd(const TrainArgs& a, int64_t n, int64_t w_off,
     k_train_bwd<F, D><<<grid, 256, smem_bwd, s>>>(a);
     if (ev) cudaEventRecord(ev[4], s);
     const unsigned dw_grid = (unsigned)((n + kDwChunk - 1) / kDwChunk);
-    k_train_dw<D><<<dw_grid > 0 ? dw_grid : 1, 256, smem_dw, s>>>(a, w_off, b_off);
+    bool tc_done = false;
+    if (a.use_tc_dw) {
+        // weight GEMMs of the input + hidden layers on tcgen05; biases and the 8-output layer
+        // on the CUDA-core kernel
+        auto run_tc = [&](auto kern, int Hc) {
+            const size_t sm = dw_tc_smem(D, Hc);
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            kern<<<sms, 128, sm, s>>>(a, w_off);
+            tc_done = true;
+        };
+        if (H == 1 && dw_tc_ok(D, 1)) run_tc(k_train_dw_tc<D, 1>, 1);
+        else if (H == 2 && dw_tc_ok(D, 2)) run_tc(k_train_dw_tc<D, 2>, 2);
+        else if (H == 3 && dw_tc_ok(D, 3)) run_tc(k_train_dw_tc<D, 3>, 3);
+        else if (H == 4 && dw_tc_ok(D, 4)) run_tc(k_train_dw_tc<D, 4>, 4);
+    }
+    if (tc_done) {
+        cudaFuncSetAttribute(k_train_dw<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_dw);
+        k_train_dw<D, false><<<dw_grid > 0 ? dw_grid : 1, 256, smem_dw, s>>>(a, w_off, b_off);
+        ++*launches;
+    } else {
+        k_train_dw<D><<<dw_grid > 0 ? dw_grid : 1, 256, smem_dw, s>>>(a, w_off, b_off);
+    }
     if (ev) cudaEventRecord(ev[5], s);
     *launches += 5;
     return cudaGetLastError();
@@ -346,6 +368,11 @@ extern "C" nbvh_status nbvh_train_backward(nbvh_ctx* c, const nbvh_ray* rays, in
     // coarse dense levels whose gradients fit a 24 KB CTA-private accumulator (prefix)
     a.priv_levels = 0;
     a.priv_floats = 0;
+    // NBVH_DW_MMA_SYNC=1 forces the mma.sync weight-gradient kernel (A/B parity tests)
+    {
+        const char* ev = std::getenv("NBVH_DW_MMA_SYNC");
+        a.use_tc_dw = (ev && ev[0] == '1') ? 0 : 1;
+    }
     for (int l = 0; l < c->cfg.L && c->dense[l]; ++l) {
         const int64_t end = (c->offset[l] + (int64_t)(c->res[l] + 1) * (c->res[l] + 1) * (c->res[l] + 1)) * c->cfg.F;
         if (end * 4 > 24 * 1024) break;

@@ -13,6 +13,7 @@
 
 #include "nbvh_device.cuh"
 #include "nbvh_internal.h"
+#include "nbvh_tcgen05.cuh"
 
 namespace nbvh {
 
@@ -56,6 +57,7 @@ struct TrainArgs {
     int64_t cap;             // capacity of the per-sample arrays
     int32_t priv_levels;     // coarse levels accumulated in shared memory by k_train_bwd
     int32_t priv_floats;     // their gradient floats (levels 0..priv_levels-1 are a prefix)
+    int32_t use_tc_dw;       // weight GEMMs on tcgen05 (k_train_dw_tc) when the shape allows
 };
 
 // ------------------------------------------------------------------ T1 select
@@ -642,7 +644,9 @@ __global__ void __launch_bounds__(256, 1) k_train_bwd(TrainArgs a) {
 // CUDA cores from the fp32 dL/dz.
 constexpr int kDwChunk = 2048;
 
-template <int D>
+// kWeights = false: only the biases and the 8-output layer (the weight GEMMs of the other
+// layers run on tcgen05 in k_train_dw_tc).
+template <int D, bool kWeights = true>
 __global__ void __launch_bounds__(256, 1) k_train_dw(TrainArgs a, int64_t w_off, int64_t b_off) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -673,16 +677,21 @@ __global__ void __launch_bounds__(256, 1) k_train_dw(TrainArgs a, int64_t w_off,
                 uint4 v = r + row < c1 ? reinterpret_cast<const uint4*>(Dk + (r + row) * 64)[c] : make_uint4(0, 0, 0, 0);
                 *reinterpret_cast<uint4*>(sd + row * 72 + c * 8) = v;
             }
-            for (int i = tid; i < kTileQ * (in / 8); i += blockDim.x) {
-                const int row = i / (in / 8), c = i % (in / 8);
-                uint4 v = r + row < c1 ? reinterpret_cast<const uint4*>(Xk + (r + row) * in)[c] : make_uint4(0, 0, 0, 0);
-                *reinterpret_cast<uint4*>(sx + row * (D + 8) + c * 8) = v;
-            }
+            if (kWeights)
+                for (int i = tid; i < kTileQ * (in / 8); i += blockDim.x) {
+                    const int row = i / (in / 8), c = i % (in / 8);
+                    uint4 v = r + row < c1 ? reinterpret_cast<const uint4*>(Xk + (r + row) * in)[c] : make_uint4(0, 0, 0, 0);
+                    *reinterpret_cast<uint4*>(sx + row * (D + 8) + c * 8) = v;
+                }
             __syncthreads();
             if (tid < 64) {
                 float sacc = 0.f;
                 for (int row = 0; row < kTileQ; ++row) sacc += __half2float(sd[row * 72 + tid]);
                 dbias += sacc;
+            }
+            if (!kWeights) {
+                __syncthreads();
+                continue;
             }
             const uint32_t aa = (uint32_t)__cvta_generic_to_shared(
                 sd + ((lane & 7) + ((lane >> 4) << 3)) * 72 + mt * 16 + ((lane >> 3) & 1) * 8);
@@ -706,7 +715,7 @@ __global__ void __launch_bounds__(256, 1) k_train_dw(TrainArgs a, int64_t w_off,
         // flush partial sums
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-            if (j < NT / 2) {
+            if (kWeights && j < NT / 2) {
                 const int col = (nt0 + j) * 8 + 2 * t;
                 const int u0 = mt * 16 + g, u1 = u0 + 8;
                 red_add_v2(a.grad + woff + (int64_t)u0 * in + col, acc[j][0], acc[j][1]);
@@ -745,6 +754,136 @@ __global__ void __launch_bounds__(256, 1) k_train_dw(TrainArgs a, int64_t w_off,
         red_add_v2(a.grad + woff + (int64_t)o * 64 + i0, accw[0], accw[1]);
         if (i0 == 0) atomicAdd(a.grad + boff + o, accb);
     }
+}
+
+// ------------------------------------------------------------------ T6 weight gradients on tcgen05
+// Every weight GEMM of the input and hidden layers as ONE tensor-core contraction over the
+// samples: D[Mtot x Ntot] += Ain[Mtot x K] * Bd[Ntot x K]^T with K = samples,
+//   Ain rows [0, D)                 : input features X,                 layer 0 inputs
+//   Ain rows [D+64(k-1), D+64k)     : post-ReLU activations A_{k-1},     layer k inputs
+//   Bd  rows [64k, 64k+64)          : deltas Dl_k (dL/d pre-activation)
+// The diagonal blocks D[rows of layer k][cols 64k..] are dW_k^T; the off-diagonal blocks
+// are discarded (3x the useful flops, free on the tensor pipe; one operand pass over HBM).
+// One CTA of 4 warps per SM, split-K over 64-sample chunks: 128 threads stage chunks with
+// cp.async into the MN-major no-swizzle canonical layout (3-stage ring), thread 0 issues
+// tcgen05.mma (M=128 halves, N=Ntot, K=16) into a TMEM accumulator and commits each stage
+// to an mbarrier; the epilogue reads TMEM (tcgen05.ld) and adds the useful blocks into the
+// gradient buffer once per CTA.
+constexpr int kDwK = 64;            // samples per chunk (4 MMA K-steps)
+constexpr int kDwStages = 3;
+
+__host__ __device__ constexpr int dw_tc_mtot(int D, int H) { return D + 64 * (H - 1); }
+__host__ __device__ constexpr bool dw_tc_ok(int D, int H) { return dw_tc_mtot(D, H) <= 256 && 64 * H <= 256; }
+__host__ __device__ constexpr size_t dw_tc_smem(int D, int H) {
+    return (size_t)kDwStages * ((size_t)((dw_tc_mtot(D, H) + 127) / 128) * 16 * 1024 + (size_t)H * 8 * 1024) + 64;
+}
+
+template <int D, int H>
+__global__ void __launch_bounds__(128, 1) k_train_dw_tc(TrainArgs a, int64_t w_off) {
+    constexpr int Mtot = dw_tc_mtot(D, H), Mh = (Mtot + 127) / 128, Ntot = 64 * H;
+    constexpr int MG = Mh * 16, NG = Ntot / 8;                // 8-row groups of A, B
+    constexpr uint32_t kAB = MG * 1024, kBB = NG * 1024;      // bytes per stage (8 k-groups x 128 B per group)
+    constexpr uint32_t kIdesc = tc::idesc_f16(128, Ntot, true, true);
+    extern __shared__ __align__(16) unsigned char smem_dw[];
+    unsigned char* stA = smem_dw;
+    unsigned char* stB = smem_dw + kDwStages * kAB;
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(stB + kDwStages * kBB);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + kDwStages);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int M = *a.n_samples;
+    const int n_chunks = (M + kDwK - 1) / kDwK;
+    if (tid == 0) {
+        for (int i = 0; i < kDwStages; ++i) tc::mbar_init(mbar + i, 1);
+        tc::fence_barrier_init();
+    }
+    if (warp == 0) tc::tmem_alloc<512>(tmem_slot);
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    // one 16-byte unit = 8 consecutive MN elements of one sample; thread -> (sample, group parity)
+    auto stage = [&](int chunk, int st) {
+        const int64_t s0 = (int64_t)chunk * kDwK;
+        unsigned char* A = stA + st * kAB;
+        unsigned char* B = stB + st * kBB;
+        const int k = tid >> 1, par = tid & 1;               // 64 samples x 2 groups per pass
+        const int64_t sm = s0 + k;
+        const bool ok = sm < M;
+        const int64_t sr = ok ? sm : 0;
+        const uint32_t koff = (uint32_t)((k >> 3) * 128 + (k & 7) * 16);
+        for (int g = par; g < MG; g += 2) {                   // A: features / activations
+            const int row = g * 8;
+            const __half* src;
+            if (row < D) src = a.X + sr * D + row;
+            else if (row < Mtot) src = a.A + (int64_t)((row - D) / 64) * a.cap * 64 + sr * 64 + ((row - D) & 63);
+            else src = a.X;                                   // padding rows: never read back
+            tc::cp16_zfill(A + g * 1024 + koff, src, ok && row < Mtot);
+        }
+        for (int g = par; g < NG; g += 2) {                   // B: deltas
+            const int col = g * 8;
+            const __half* src = a.Dl + (int64_t)(col / 64) * a.cap * 64 + sr * 64 + (col & 63);
+            tc::cp16_zfill(B + g * 1024 + koff, src, ok);
+        }
+    };
+
+    int it = 0;
+    for (int c = blockIdx.x; c < n_chunks; c += gridDim.x, ++it) {
+        const int st = it % kDwStages;
+        if (it >= kDwStages) tc::mbar_wait(mbar + st, ((it / kDwStages) - 1) & 1);   // MMAs of it-3 done
+        stage(c, st);
+        tc::cp_commit();
+        tc::cp_wait<0>();
+        tc::fence_proxy_async();
+        __syncthreads();
+        if (tid == 0) {
+            tc::fence_after();
+            const uint32_t a0 = tc::smem_u32(stA + st * kAB), b0 = tc::smem_u32(stB + st * kBB);
+#pragma unroll
+            for (int kk = 0; kk < kDwK / 16; ++kk) {
+                const uint64_t bd = tc::smem_desc(b0 + kk * 256, 128, 1024);
+#pragma unroll
+                for (int h = 0; h < Mh; ++h) {
+                    const uint64_t ad = tc::smem_desc(a0 + h * 16 * 1024 + kk * 256, 128, 1024);
+                    tc::mma_f16(tmem + h * 256, ad, bd, kIdesc, (it > 0 || kk > 0) ? 1u : 0u);
+                }
+            }
+            tc::commit(mbar + st);
+        }
+    }
+    // drain: wait for the last committed stage, then read the accumulator
+    if (it > 0) {
+        const int last = it - 1;
+        tc::mbar_wait(mbar + (last % kDwStages), (last / kDwStages) & 1);
+    }
+    tc::fence_after();
+    if (it > 0) {
+        // thread tid <-> TMEM lane tid <-> A row (h*128 + tid); useful columns = its layer's deltas
+#pragma unroll 1
+        for (int h = 0; h < Mh; ++h) {
+            const int row = h * 128 + tid;
+            int layer = -1, in = 0, i = 0;
+            if (row < D) { layer = 0; in = D; i = row; }
+            else if (row < Mtot) { layer = 1 + (row - D) / 64; in = 64; i = (row - D) & 63; }
+            int64_t base = w_off;
+            for (int l = 0; l < layer; ++l) base += (int64_t)64 * (l == 0 ? D : 64);
+#pragma unroll 1
+            for (int cb = 0; cb < Ntot; cb += 32) {
+                float v[32];
+                tc::ld32(tmem, (uint32_t)(warp * 32), (uint32_t)(h * 256 + cb), v);   // warp-collective
+                if (layer >= 0 && cb >= 64 * layer && cb < 64 * layer + 64) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const int o = cb - 64 * layer + j;                 // output unit
+                        atomicAdd(a.grad + base + (int64_t)o * in + i, v[j]);
+                    }
+                }
+            }
+        }
+    }
+    tc::fence_before();
+    __syncthreads();
+    if (warp == 0) tc::tmem_free<512>(tmem);
 }
 
 // ------------------------------------------------------------------ T9 Adam

@@ -92,6 +92,37 @@ def test_loss_and_gradients_vs_oracle(batch):
     assert abs(per_leaf[:, 0].sum() - o["loss_sum"][0]) <= 5e-3 * o["loss_sum"][0]
 
 
+@pytest.mark.parametrize("hidden", [2, 3])
+@pytest.mark.parametrize("path", ["tcgen05", "mma_sync"])
+def test_weight_gradients_per_layer(hidden, path, monkeypatch):
+    """Per-layer weight and bias gradients vs the oracle, on both weight-gradient kernels:
+    the tcgen05/TMEM contraction (k_train_dw_tc) and the mma.sync fallback (k_train_dw)."""
+    from paper_2405_16237_b200 import dp
+    if path == "mma_sync":
+        monkeypatch.setenv("NBVH_DW_MMA_SYNC", "1")
+    else:
+        monkeypatch.delenv("NBVH_DW_MMA_SYNC", raising=False)
+    ctx, sc, cut, tab, layers, rays, u, xi, o = _setup(n_rays=5000, seed=40 + hidden, hidden=hidden)
+    ctx.train_backward(_to(rays), _to(u), _to(xi))
+    torch.cuda.synchronize()
+    g = dp.grad_tensor(ctx).cpu().numpy().astype(np.float64)
+    m = o["n_acc"]
+    n_t = tab.size
+    dims = [64] + [64] * hidden + [8]
+    wo = n_t
+    go = 0
+    for k in range(len(dims) - 1):
+        n = dims[k] * dims[k + 1]
+        gg, oo = g[wo:wo + n], o["g_W"][go:go + n] * m
+        rel = np.linalg.norm(gg - oo) / np.linalg.norm(oo)
+        assert rel <= 3e-2, (path, hidden, k, rel)
+        wo += n
+        go += n
+    nb = o["g_b"].size
+    gb, ob = g[wo:wo + nb], o["g_b"] * m
+    assert np.linalg.norm(gb - ob) / np.linalg.norm(ob) <= 3e-2
+
+
 def test_adam_step_vs_oracle(batch):
     from paper_2405_16237_b200 import dp, PARAM_ALL
     import oracle as orc

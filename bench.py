@@ -110,6 +110,28 @@ def build_model(cfg_name: str, device: int, rank: int = 0, list_cap: int = 8):
     return ctx, sc, rays, c
 
 
+def _profiled_traffic(kernel: str = "k_query"):
+    """DRAM bytes per launch of `kernel` from the newest committed ncu --set full summary
+    (profiles/r*_ncu_full_query.txt, written by scripts/ncu_summary.py)."""
+    import glob
+    import re
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_full_query.txt")))
+    if not files:
+        return None, None
+    txt = open(files[-1]).read()
+    m = re.search(r"== void " + kernel + r"<[^\n]*\n(.*?)(?:\n==|\Z)", txt, re.S)
+    if not m:
+        return None, None
+    units = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    tot = 0.0
+    for key in ("DRAM read", "DRAM write"):
+        mm = re.search(key + r"\s+([0-9.]+)\s+(\w+)", m.group(1))
+        if not mm:
+            return None, None
+        tot += float(mm.group(1)) * units.get(mm.group(2), 1)
+    return tot, os.path.basename(files[-1])
+
+
 def cpu_oracle_rate(ctx, c, rays, target_s: float = 12.0, max_rays: int | None = None):
     """Time the oracle (as it stands) on a deterministic strided sample of the frame."""
     import oracle
@@ -225,6 +247,7 @@ def run_ours(args):
     wave_s = statistics.mean(wave_ms) / 1e3
     achieved = mean_q * bytes_per_query / wave_s / 1e9
     hbm, tflops, peak_src = _peaks()
+    traffic, traffic_src = _profiled_traffic("k_query")
     mlp_flops = 2 * (ctx.d_in * 64 + (h.hidden_layers - 1) * 64 * 64 + 64 * 8)
 
     # end-to-end through the public host API: pinned host rays in, host results out
@@ -274,7 +297,10 @@ def run_ours(args):
             "list_refills_per_step": st["n_refills"],
             "roofline": {"bound": "hbm", "kernel": "k_query (persistent: sample+encode+MLP+decode+terminate, slot refill)",
                          "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                         "peak_source": peak_src, "traffic": None,
+                         "peak_source": peak_src, "traffic": traffic,
+                         "traffic_source": f"profiles/{traffic_src}: dram__bytes_read.sum + dram__bytes_write.sum "
+                                           "of one launch (tables are L2-resident, so DRAM traffic is far below the "
+                                           "gather bytes counted in achieved)" if traffic else None,
                          "bytes_per_query": bytes_per_query, "useful_gather_bytes_per_query": useful_gather,
                          "queries_per_launch_sum": mean_q, "kernel_ms_per_step": statistics.mean(wave_ms),
                          "traverse_ms_per_step": statistics.mean(trav_ms),

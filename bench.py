@@ -152,7 +152,8 @@ def cpu_oracle_rate(ctx, c, rays, target_s: float = 12.0, max_rays: int | None =
     # calibrate on a small sample, then size the timed sample to ~target_s
     probe = rays[:: max(1, rays.shape[0] // 512)]
     t0 = time.perf_counter()
-    oracle.query(g, h.n_points, tab, layers, cut["leaf_lo"], cut["leaf_hi"], probe)
+    box = oracle.scene_box(ctx.scene)
+    oracle.query(g, h.n_points, tab, layers, cut["leaf_lo"], cut["leaf_hi"], probe, dom_box=box)
     per_ray = (time.perf_counter() - t0) / probe.shape[0]
     n = int(min(rays.shape[0], max(256, target_s / max(per_ray, 1e-9))))
     if max_rays:
@@ -160,7 +161,7 @@ def cpu_oracle_rate(ctx, c, rays, target_s: float = 12.0, max_rays: int | None =
     stride = max(1, rays.shape[0] // n)
     sample = rays[::stride][:n]
     t0 = time.perf_counter()
-    oracle.query(g, h.n_points, tab, layers, cut["leaf_lo"], cut["leaf_hi"], sample)
+    oracle.query(g, h.n_points, tab, layers, cut["leaf_lo"], cut["leaf_hi"], sample, dom_box=box)
     dt = time.perf_counter() - t0
     return {"value": sample.shape[0] / dt / 1e6, "unit": "Mrays/s", "cores": oracle.num_threads(), "kind": "oracle",
             "sample": f"every {stride}th primary ray of the frame ({sample.shape[0]} rays), C++ double oracle, "
@@ -390,10 +391,11 @@ def run_reference(args):
         wo += dims[k] * dims[k + 1]
         bo += dims[k + 1]
     cut = ctx.cut(0)
+    box = oracle.scene_box(sc)
 
     def step(i):
         sample = rays[(i % stride)::stride][:per_step]
-        oracle.query(g, h.n_points, tab, layers, cut["leaf_lo"], cut["leaf_hi"], sample)
+        oracle.query(g, h.n_points, tab, layers, cut["leaf_lo"], cut["leaf_hi"], sample, dom_box=box)
         return sample.shape[0]
 
     for i in range(args.warmup):

@@ -119,6 +119,19 @@ def leaf_lists(rays, leaf_lo, leaf_hi, cap):
     return leaf, te, tx, cnt
 
 
+def scene_box(scene, rel=1e-3, abs_=1e-6):
+    """Inflated root box of the scene (C4 as amended for shared-grid LoD cuts, C15)."""
+    box = np.zeros(6, np.float32)
+    tris = _c(scene.tris, np.uint32)
+    lib().orc_scene_box(_p(_c(scene.verts, np.float32)), _p(tris), C.c_int64(tris.shape[0]), C.c_float(rel),
+                        C.c_float(abs_), _p(box))
+    return box
+
+
+def _box(dom_box):
+    return None if dom_box is None else _p(_c(dom_box, np.float32))
+
+
 def domain(leaf_lo, leaf_hi):
     lo = _c(leaf_lo, np.float32)
     hi = _c(leaf_hi, np.float32)
@@ -156,7 +169,8 @@ def mlp_forward(layers, x):
 
 
 # ---------------------------------------------------------------- query
-def query(grid: Grid, n_points, table_fp16, layers, leaf_lo, leaf_hi, rays, mode=0, trace_cap=0):
+def query(grid: Grid, n_points, table_fp16, layers, leaf_lo, leaf_hi, rays, mode=0, trace_cap=0, dom_box=None):
+    """dom_box (6 floats, nullable): the grid-domain box (scene_box); None = union of the leaf boxes."""
     dims, W_all, b_all = _mlp_arrays(layers)
     tab = _c(table_fp16, np.float16).view(np.uint16)
     rays = _c(rays, np.float32)
@@ -171,7 +185,7 @@ def query(grid: Grid, n_points, table_fp16, layers, leaf_lo, leaf_hi, rays, mode
                     _p(grid.offset), _p(tab), _p(dims), _p(W_all), _p(b_all), _p(lo), _p(hi),
                     C.c_int32(lo.shape[0]), _p(rays), C.c_int64(n), C.c_int32(mode), _p(out["hit"]),
                     _p(out["t"]), _p(out["normal"]), _p(out["albedo"]), _p(out["leaf"]), _p(out["nq"]),
-                    _p(out["margin"]), _p(zt), C.c_int32(trace_cap), _p(out["tmargin"]))
+                    _p(out["margin"]), _p(zt), C.c_int32(trace_cap), _p(out["tmargin"]), _box(dom_box))
     if zt is not None:
         out["z_trace"] = zt
     return out
@@ -233,7 +247,7 @@ def sample_loss(z, gt):
 
 
 def train_grad(grid: Grid, n_points, table_fp16, layers, leaf_lo, leaf_hi, leaf_rank, leaf_tri_off, leaf_tris,
-               scene, rays, u, xi):
+               scene, rays, u, xi, dom_box=None):
     dims, W_all, b_all = _mlp_arrays(layers)
     tab = _c(table_fp16, np.float16).view(np.uint16)
     rays = _c(rays, np.float32)
@@ -251,13 +265,14 @@ def train_grad(grid: Grid, n_points, table_fp16, layers, leaf_lo, leaf_hi, leaf_
         _p(_c(leaf_tris, np.int32)), _p(_c(scene.verts, np.float32)), _p(_c(scene.tris, np.uint32)),
         _p(_c(scene.vnormals, np.float32)), _p(_c(scene.albedo, np.float32)), _p(rays), C.c_int64(n),
         _p(_c(u, np.float32)), _p(_c(xi, np.float32)), _p(out["g_table"]), _p(out["g_W"]), _p(out["g_b"]),
-        _p(out["accepted"]), _p(out["first_leaf"]), _p(out["loss"]), _p(out["gt"]), _p(out["loss_sum"]))
+        _p(out["accepted"]), _p(out["first_leaf"]), _p(out["loss"]), _p(out["gt"]), _p(out["loss_sum"]),
+        _box(dom_box))
     out["n_acc"] = int(n_acc)
     return out
 
 
 def batch_loss_double(grid: Grid, n_points, table, dims, W_all, b_all, leaf_lo, leaf_hi, rays, xi, accepted,
-                      t0, t1, gt, den=None, den_mode=0):
+                      t0, t1, gt, den=None, den_mode=0, dom_box=None):
     lo = _c(leaf_lo, np.float32)
     if den is None:
         den = np.zeros((rays.shape[0], 3))
@@ -266,7 +281,7 @@ def batch_loss_double(grid: Grid, n_points, table, dims, W_all, b_all, leaf_lo, 
         _p(_c(table, np.float64)), _p(_c(dims, np.int32)), _p(_c(W_all, np.float64)), _p(_c(b_all, np.float64)),
         _p(lo), _p(_c(leaf_hi, np.float32)), C.c_int32(lo.shape[0]), _p(_c(rays, np.float32)),
         C.c_int64(rays.shape[0]), _p(_c(xi, np.float32)), _p(_c(accepted, np.uint8)), _p(_c(t0, np.float32)),
-        _p(_c(t1, np.float32)), _p(_c(gt, np.float64)), _p(den), C.c_int32(den_mode)))
+        _p(_c(t1, np.float32)), _p(_c(gt, np.float64)), _p(den), C.c_int32(den_mode), _box(dom_box)))
 
 
 def adam(param, grad, m, v, step, lr=0.01, beta1=0.9, beta2=0.999, eps=1e-8):

@@ -189,6 +189,35 @@ void orc_leaf_lists(const float* rays, int64_t n, const float* leaf_lo, const fl
 // largest extent, centred (C4).  fp32 op order: lo/hi = min/max over leaves;
 // side = max(hi.x-lo.x, hi.y-lo.y, hi.z-lo.z); c = (lo+hi)*0.5; dom_min = c - side*0.5;
 // dom_inv = 1/side.
+// C4 (as amended for multi-cut LoD: one hash grid shared by every cut): the
+// domain box is the scene's root box inflated per C15, identical for every cut; callers
+// pass that single box (orc_scene_box) as a 1-"leaf" list.
+// Root box = min/max over the vertices of all triangles (exact in fp32); pad =
+// max(rel * diag, abs * diag) in double (diag of the root = the scene diagonal);
+// lo = fp32(lo - pad), hi = fp32(hi + pad) ("slightly" inflated, C15).
+void orc_scene_box(const float* verts, const uint32_t* tris, int64_t nt, float rel, float abs_, float* box) {
+    float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int64_t t = 0; t < nt; ++t)
+        for (int c = 0; c < 3; ++c) {
+            const float* v = verts + 3 * (int64_t)tris[3 * t + c];
+            for (int k = 0; k < 3; ++k) {
+                lo[k] = std::fmin(lo[k], v[k]);
+                hi[k] = std::fmax(hi[k], v[k]);
+            }
+        }
+    double d2 = 0;
+    for (int k = 0; k < 3; ++k) {
+        const double e = (double)hi[k] - (double)lo[k];
+        d2 += e * e;
+    }
+    const double diag = std::sqrt(d2);
+    const double pad = std::max((double)rel * diag, (double)abs_ * diag);
+    for (int k = 0; k < 3; ++k) {
+        box[k] = (float)((double)lo[k] - pad);
+        box[3 + k] = (float)((double)hi[k] + pad);
+    }
+}
+
 void orc_domain(const float* leaf_lo, const float* leaf_hi, int32_t n_leaves, float* dom_min, float* dom_inv) {
     float lo[3], hi[3];
     for (int k = 0; k < 3; ++k) { lo[k] = leaf_lo[k]; hi[k] = leaf_hi[k]; }
@@ -321,9 +350,11 @@ void orc_query(int32_t L, int32_t F, int32_t log2_T, int32_t n_points, int32_t n
                const float* leaf_lo, const float* leaf_hi, int32_t n_leaves,
                const float* rays, int64_t n, int32_t mode,
                uint8_t* hit, float* t_out, float* normal, float* albedo, int32_t* leaf_out,
-               int32_t* nq_out, double* margin, double* z_trace, int32_t cap, double* tmargin) {
+               int32_t* nq_out, double* margin, double* z_trace, int32_t cap, double* tmargin,
+               const float* dom_box) {
     float dom_min[3], dom_inv;
-    orc_domain(leaf_lo, leaf_hi, n_leaves, dom_min, &dom_inv);
+    if (dom_box) orc_domain(dom_box, dom_box + 3, 1, dom_min, &dom_inv);
+    else orc_domain(leaf_lo, leaf_hi, n_leaves, dom_min, &dom_inv);
     OrcModel M{L, F, log2_T, n_points, n_layers, res, dense, offset, table, dims, W_all, b_all, dom_min, dom_inv};
     std::vector<const uint16_t*> W;
     std::vector<const float*> b;
@@ -611,9 +642,10 @@ int64_t orc_train_grad(int32_t L, int32_t F, int32_t log2_T, int32_t n_points, i
                        const float* rays, int64_t n, const float* u, const float* xi,
                        double* g_table, double* g_W, double* g_b,
                        uint8_t* accepted, int32_t* first_leaf, double* sample_loss, double* gt_out /*[n][9]*/,
-                       double* loss_sum) {
+                       double* loss_sum, const float* dom_box) {
     float dom_min[3], dom_inv;
-    orc_domain(leaf_lo, leaf_hi, n_leaves, dom_min, &dom_inv);
+    if (dom_box) orc_domain(dom_box, dom_box + 3, 1, dom_min, &dom_inv);
+    else orc_domain(leaf_lo, leaf_hi, n_leaves, dom_min, &dom_inv);
     OrcModel M{L, F, log2_T, n_points, n_layers, res, dense, offset, table, dims, W_all, b_all, dom_min, dom_inv};
     std::vector<const uint16_t*> W;
     std::vector<const float*> b;
@@ -723,9 +755,10 @@ double orc_batch_loss_double(int32_t L, int32_t F, int32_t log2_T, int32_t n_poi
                              const float* leaf_lo, const float* leaf_hi, int32_t n_leaves,
                              const float* rays, int64_t n, const float* xi, const uint8_t* accepted,
                              const float* t0, const float* t1, const double* gt,
-                             double* den /*[n][3]*/, int32_t den_mode) {
+                             double* den /*[n][3]*/, int32_t den_mode, const float* dom_box) {
     float dom_min[3], dom_inv;
-    orc_domain(leaf_lo, leaf_hi, n_leaves, dom_min, &dom_inv);
+    if (dom_box) orc_domain(dom_box, dom_box + 3, 1, dom_min, &dom_inv);
+    else orc_domain(leaf_lo, leaf_hi, n_leaves, dom_min, &dom_inv);
     const int LF = L * F;
     int64_t n_acc = 0;
     double tot = 0;

@@ -337,17 +337,12 @@ int build_cut(const HostScene& sc, int32_t target, const HostCut* prev, const fl
     (void)root;
     out.n_leaves = (int32_t)out.leaf_base.size();
     out.rank.assign(out.n_leaves, 0.0f);
-    // Grid domain (C4), fp32: cube of side max extent around the union of leaf boxes.
+    // Grid domain (C4 as amended for shared-grid LoD cuts), fp32: cube of
+    // side max extent around the scene's root box inflated per C15 -- the same for every
+    // cut, so all LoD slots (and every stage of the error-driven construction) index the
+    // one hash grid identically.
     float dlo[3], dhi[3];
-    for (int k = 0; k < 3; ++k) {
-        dlo[k] = out.leaf_lo[k];
-        dhi[k] = out.leaf_hi[k];
-    }
-    for (int32_t i = 1; i < out.n_leaves; ++i)
-        for (int k = 0; k < 3; ++k) {
-            dlo[k] = std::fmin(dlo[k], out.leaf_lo[3 * i + k]);
-            dhi[k] = std::fmax(dhi[k], out.leaf_hi[3 * i + k]);
-        }
+    inflate(sc.nodes[0], sc.scene_diag, inflate_rel, inflate_abs, dlo, dhi);
     const float ex = dhi[0] - dlo[0], ey = dhi[1] - dlo[1], ez = dhi[2] - dlo[2];
     const float side = std::fmax(std::fmax(ex, ey), ez);
     for (int k = 0; k < 3; ++k) {

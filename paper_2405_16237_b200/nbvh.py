@@ -190,6 +190,7 @@ class Context:
 
     # ---------------------------------------------------------------- scene
     def set_mesh(self, scene):
+        self.scene = scene
         v = np.ascontiguousarray(scene.verts, np.float32)
         t = np.ascontiguousarray(scene.tris, np.uint32)
         n = np.ascontiguousarray(scene.vnormals, np.float32) if scene.vnormals is not None else None

@@ -152,7 +152,7 @@ def _check_query(orc, ctx, tab, layers, rays, mode=0, cap=64):
     assert np.abs(g["albedo"] - rep["albedo"]).max() <= 1e-6
     # (2) the double-precision oracle
     o = orc.query(_grid(orc, ctx), ctx.cfg.n_points, tab, layers, cut["leaf_lo"], cut["leaf_hi"], rays, mode=mode,
-                  trace_cap=cap)
+                  trace_cap=cap, dom_box=orc.scene_box(ctx.scene))
     clear = (o["margin"] >= 1e-2) & (o["tmargin"] >= 5e-3)
     assert np.array_equal(g["hit"][clear], o["hit"][clear])
     assert np.array_equal(g["leaf"][clear], o["leaf"][clear])
@@ -216,7 +216,8 @@ def test_query_1080p_sampled_full_size(orc):
     assert st["n_rays"] == rays.shape[0] and st["n_queries"] > rays.shape[0] // 2
     sample = np.arange(0, rays.shape[0], 4099)
     cut = ctx.cut(0)
-    o = orc.query(_grid(orc, ctx), 4, tab, layers, cut["leaf_lo"], cut["leaf_hi"], rays[sample])
+    o = orc.query(_grid(orc, ctx), 4, tab, layers, cut["leaf_lo"], cut["leaf_hi"], rays[sample],
+                  dom_box=orc.scene_box(sc))
     g = {k: v.cpu().numpy()[sample] for k, v in out.items()}
     clear = (o["margin"] >= 1e-2) & (o["tmargin"] >= 5e-3)
     assert np.array_equal(g["hit"][clear], o["hit"][clear])

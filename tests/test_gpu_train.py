@@ -35,7 +35,7 @@ def _setup(n_rays=6000, seed=30, leaves=64, rank=None, hidden=2):
     u = synth.random_uniform(n_rays, seed=seed + 3)
     xi = synth.random_uniform(n_rays * 4, seed=seed + 4).reshape(n_rays, 4)
     o = orc.train_grad(orc.Grid(8, 14, 2), 4, tab.reshape(-1, 2), layers, cut["leaf_lo"], cut["leaf_hi"], rank,
-                       cut["tri_off"], cut["tris"], sc, rays, u, xi)
+                       cut["tri_off"], cut["tris"], sc, rays, u, xi, dom_box=orc.scene_box(sc))
     return ctx, sc, cut, tab, layers, rays, u, xi, o
 
 

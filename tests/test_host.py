@@ -64,10 +64,30 @@ def test_cut_structure_checked_by_oracle(orc, tiny_host):
 
 
 def test_domain_matches_oracle(orc, tiny_host):
-    ctx, _ = tiny_host
+    """C4 (amended): the grid domain is the cube around the scene's inflated root box, the
+    same for every cut; bit-exact against the oracle's own computation from the mesh."""
+    ctx, sc = tiny_host
     cut = ctx.cut(0)
-    dmin, dinv = orc.domain(cut["leaf_lo"], cut["leaf_hi"])
+    dmin, dinv = orc.domain(*np.split(orc.scene_box(sc).reshape(1, 6), 2, axis=1))
     assert np.array_equal(dmin, cut["dom_min"]) and dinv == cut["dom_inv"][0]
+    # and it contains every inflated leaf box of the cut
+    side = 1.0 / dinv
+    assert np.all(cut["leaf_lo"] >= dmin) and np.all(cut["leaf_hi"] <= dmin + side)
+
+
+@pytest.mark.parametrize("target", [1, 9, 64, 500])
+def test_domain_is_cut_independent(orc, lib, target):
+    from paper_2405_16237_b200 import Context
+    sc = synth.scene_tiny(nu=10)
+    ctx = Context(device=-1)
+    ctx.set_mesh(sc)
+    ctx.build_cut(target)
+    cut = ctx.cut(0)
+    dmin, dinv = orc.domain(*np.split(orc.scene_box(sc).reshape(1, 6), 2, axis=1))
+    assert np.array_equal(dmin, cut["dom_min"]) and dinv == cut["dom_inv"][0]
+    if target == 1:                 # single-leaf cut: the root box itself (union of leaf boxes)
+        d1, i1 = orc.domain(cut["leaf_lo"], cut["leaf_hi"])
+        assert np.array_equal(d1, dmin) and i1 == dinv
 
 
 @pytest.mark.parametrize("target", [1, 2, 7, 300])

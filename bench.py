@@ -276,6 +276,7 @@ def run_ours(args):
                "h2d_bytes_per_step": n * 32, "d2h_bytes_per_step": d2h}
 
     train = bench_train(ctx, args, world, rank) if args.train else None
+    lod = bench_lod(args, local) if (args.lod and rank == 0) else None
 
     line = None
     if rank == 0:
@@ -307,7 +308,7 @@ def run_ours(args):
                          "traverse_ms_per_step": statistics.mean(trav_ms),
                          "mlp_tflops": mean_q * mlp_flops / wave_s / 1e12,
                          "mlp_frac_of_bf16_peak": mean_q * mlp_flops / wave_s / 1e12 / tflops},
-            "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks.summary(), "train": train,
+            "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks.summary(), "train": train, "lod": lod,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -367,6 +368,67 @@ def bench_train(ctx, args, world, rank):
             "gpu_launches_per_step": st["n_launches"]}
 
 
+def bench_lod(args, device):
+    """BASELINE cfg 4: multi-cut LoD query.  Three error-driven cuts of the cfg-2 scene
+    (~128, ~512 and 2048 leaves, registered during one construction run) share
+    one hash grid; 1080p frames from three camera distances (1.6, 6.4, 25.6) are queried at
+    the fine, middle and coarse LoD.  Also reports the far frame at the finest cut, i.e. the
+    speed-up an LoD switch buys (P:342 reports 1.5-2x after the primary hit)."""
+    import torch
+    from paper_2405_16237_b200 import Context
+    from paper_2405_16237_b200.construct import construct, Schedule
+    c = synth.CONFIGS["1080p"]
+    h = c["hash"]
+    sc = synth.scene_1080p(c["seeds"]["mesh"])
+    ctx = Context(device=device, L=h.L, F=h.F, log2_T=h.log2_T, n_points=h.n_points, hidden_layers=h.hidden_layers,
+                  list_cap=args.list_cap, seed=11)
+    ctx.set_mesh(sc)
+    ctx.build_cut(1)
+    n_train = 1 << 16
+    ctx.reserve(max(n_train, c["res"][0] * c["res"][1]))
+
+    def batch(step):
+        rays = synth.random_rays(n_train, seed=9000 + step % 8)
+        u = synth.random_uniform(n_train, seed=9100 + step % 8)
+        xi = synth.random_uniform(n_train * h.n_points, seed=9200 + step % 8).reshape(n_train, h.n_points)
+        return tuple(torch.from_numpy(np.ascontiguousarray(x)).cuda() for x in (rays, u, xi))
+
+    batches = [batch(i) for i in range(8)]
+    t0 = time.perf_counter()
+    hist = construct(ctx, 2048, lambda s: batches[s % 8],
+                     Schedule(iters0=2, splits0=8, growth=2.0, final_iters=100, lod_at_leaves=(128, 512)))
+    build_s = time.perf_counter() - t0
+    slots = {"fine": 0, "middle": 2, "coarse": 1}
+    out = ctx.alloc_hits(c["res"][0] * c["res"][1])
+    res = {}
+    stream = torch.cuda.current_stream()
+    for name, dist, lod in (("near", 1.6, 0), ("mid", 6.4, 2), ("far", 25.6, 1), ("far@fine", 25.6, 0)):
+        # same view direction; the field of view narrows with distance so the scene covers
+        # the same part of the frame (a zoomed camera: same screen-space work, coarser LoD)
+        eye = np.array([0.0, 0.6, 1.6]) * (dist / 1.6)
+        vfov = float(np.degrees(2.0 * np.arctan(np.tan(np.radians(c["vfov"]) / 2.0) * 1.6 / dist)))
+        rays = torch.from_numpy(synth.camera_rays(*c["res"], eye, vfov_deg=vfov)).cuda()
+        for _ in range(3):
+            ctx.query(rays, lod=lod, out=out)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            ctx.query(rays, lod=lod, out=out)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / args.steps
+        st = ctx.query_stats()
+        res[name] = {"lod_slot": lod, "leaves": ctx.cut(lod)["n_leaves"], "camera_distance": dist,
+                     "ms_per_frame": ms, "Mrays_per_s": rays.shape[0] / ms / 1e3,
+                     "queries_per_ray": st["n_queries"] / rays.shape[0]}
+    return {"metric": "multi-cut LoD query Mrays/s (BASELINE cfg 4)", "unit": "Mrays/s",
+            "construction": {"rounds": len(hist), "seconds": build_s, "rays_per_step": n_train,
+                             "leaves_per_round": [hlog.n_leaves for hlog in hist],
+                             "final_mean_loss": hist[-1].loss},
+            "frames": res,
+            "lod_speedup_far": res["far"]["Mrays_per_s"] / res["far@fine"]["Mrays_per_s"]}
+
+
 def run_reference(args):
     """The CPU oracle timed as it stands on bounded samples of the same workload."""
     rank = int(os.environ.get("RANK", "0"))
@@ -424,6 +486,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle timing budget (0 = skip)")
     ap.add_argument("--list-cap", type=int, default=8, help="per-ray ordered leaf-list capacity K (C6)")
     ap.add_argument("--train", type=int, default=1, help="also time the cfg-5 training step (1/0)")
+    ap.add_argument("--lod", type=int, default=1, help="also run the cfg-4 multi-cut LoD query (1/0)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -152,6 +152,10 @@ nbvh_status nbvh_set_mesh(nbvh_ctx* ctx, const float* xyz, int64_t nv, const uin
  * NBVH_WARN_CLAMPED if target_leaves exceeds the number of base leaves. */
 nbvh_status nbvh_build_cut(nbvh_ctx* ctx, int32_t target_leaves, const float* leaf_q, const float* leaf_p,
                            int32_t lod_slot, int32_t* out_n_leaves);
+/* Registers a copy of the cut in LoD slot src_lod into slot dst_lod ("we register a
+ * new LoD at regular training iteration intervals"); every slot indexes the same hash grid
+ * and MLP (C4').  Host + device copy; NBVH_ESTATE if the source slot is empty. */
+nbvh_status nbvh_copy_cut(nbvh_ctx* ctx, int32_t src_lod, int32_t dst_lod);
 /* Cut inspection (host outputs, any pointer nullable): leaf boxes (inflated) [n][3],
  * base boxes (uninflated) [n][3], leaf triangle lists in CSR form (tri_off [n+1],
  * tris [n_tris], original triangle ids), grid domain (C4). */

@@ -450,6 +450,22 @@ extern "C" nbvh_status nbvh_build_cut(nbvh_ctx* c, int32_t target, const float* 
     return clamped ? NBVH_WARN_CLAMPED : NBVH_OK;
 }
 
+extern "C" nbvh_status nbvh_copy_cut(nbvh_ctx* c, int32_t src_lod, int32_t dst_lod) {
+    if (!c) return NBVH_EINVAL;
+    if (c->poisoned) return NBVH_ECUDA;
+    if (src_lod < 0 || src_lod >= kMaxLod || dst_lod < 0 || dst_lod >= kMaxLod)
+        return fail(c, NBVH_ERANGE, "copy_cut: lod slot out of range");
+    if (!c->has_cut[src_lod]) return fail(c, NBVH_ESTATE, "copy_cut: empty source slot");
+    if (src_lod == dst_lod) return NBVH_OK;
+    c->cuts[dst_lod] = c->cuts[src_lod];
+    c->has_cut[dst_lod] = true;
+    if (c->device >= 0) {
+        nbvh_status st = upload_cut(c, dst_lod);
+        if (st) return st;
+    }
+    return NBVH_OK;
+}
+
 extern "C" nbvh_status nbvh_cut_info(const nbvh_ctx* c, int32_t lod, int32_t* n_leaves, int32_t* n_inner) {
     if (!c) return NBVH_EINVAL;
     if (lod < 0 || lod >= kMaxLod) return NBVH_ERANGE;

@@ -66,6 +66,7 @@ SIGNATURES = {
     "nbvh_reserve": (C.c_int, [_P, _I64]),
     "nbvh_set_mesh": (C.c_int, [_P, _P, _I64, _P, _I64, _P, _P]),
     "nbvh_build_cut": (C.c_int, [_P, _I32, _P, _P, _I32, _P]),
+    "nbvh_copy_cut": (C.c_int, [_P, _I32, _I32]),
     "nbvh_cut_info": (C.c_int, [_P, _I32, _P, _P]),
     "nbvh_get_cut": (C.c_int, [_P, _I32, _P, _P, _P, _P, _P, _P, _P, _P]),
     "nbvh_query": (C.c_int, [_P, _P, _I64, _I32, Hits, _P]),
@@ -204,6 +205,9 @@ class Context:
         pa = None if p is None else np.ascontiguousarray(p, np.float32)
         st = self._ck(self.lib.nbvh_build_cut(self.h, int(target), _ptr(qa), _ptr(pa), lod, _ptr(out)), "build_cut")
         return int(out[0]), st
+
+    def copy_cut(self, src_lod, dst_lod):
+        self._ck(self.lib.nbvh_copy_cut(self.h, int(src_lod), int(dst_lod)), "copy_cut")
 
     def cut(self, lod=0):
         nl = np.zeros(1, np.int32)

@@ -1,0 +1,8 @@
+#!/bin/bash
+# GPU tests only (optionally a -k filter): bash scripts/gpu_tests.sh TAG [pytest args...]
+cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
+OUT=gpurun_out; TAG=${1:-t}; shift
+mkdir -p $OUT
+python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1
+timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider "$@" > $OUT/pytest_gpu_$TAG.log 2>&1
+echo "pytest exit $?" >> $OUT/pytest_gpu_$TAG.log

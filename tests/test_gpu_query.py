@@ -135,9 +135,9 @@ def test_traversal_small_capacity(orc):
 
 
 # ------------------------------------------------------------------ end-to-end query
-def _check_query(orc, ctx, tab, layers, rays, mode=0, cap=64):
-    cut = ctx.cut(0)
-    out, zt = ctx.debug_query_trace(torch.from_numpy(rays).cuda(), cap)
+def _check_query(orc, ctx, tab, layers, rays, mode=0, cap=64, lod=0):
+    cut = ctx.cut(lod)
+    out, zt = ctx.debug_query_trace(torch.from_numpy(rays).cuda(), cap, lod=lod)
     torch.cuda.synchronize()
     g = {k: v.cpu().numpy() for k, v in out.items()}
     zt = zt.cpu().numpy()
@@ -193,6 +193,19 @@ def test_query_single_leaf_and_empty(orc):
     assert np.all(g["n_queries"] <= 1)
     out = ctx.query(torch.zeros(0, 8, device="cuda"))            # n = 0 is a no-op
     assert out["hit"].numel() == 0
+
+
+def test_query_lod_slots(orc):
+    """Multi-cut LoD: three cuts of one hash grid in slots 0-2; every slot's query is
+    checked against the oracle on that slot's leaf boxes (grid domain shared, C4')."""
+    ctx, sc, tab, layers = _mk_ctx("tiny", leaves=64)
+    ctx.build_cut(8, lod=1)
+    ctx.build_cut(24, lod=2)
+    rays = _rays_tiny(1500)
+    for lod in (2, 1, 0):
+        g, o = _check_query(orc, ctx, tab, layers, rays, lod=lod)
+        assert g["n_queries"].max() >= 1
+    assert ctx.cut(1)["n_leaves"] == 8 and ctx.cut(2)["n_leaves"] == 24
 
 
 def test_query_host_path_equals_device_path(tiny):

@@ -55,6 +55,11 @@ CONFIGS = {
     "1080p": dict(hash=HashCfg(L=16, log2_T=19, F=2, n_points=4, hidden_layers=3),
                   leaves=2048, res=(1920, 1080), eye=(0.0, 0.6, 1.6), vfov=50.0,
                   seeds=dict(mesh=4, weights=5, train=6)),
+    # the paper's own setting (8 levels, 4 features, 4x64 MLP;
+    # 2^18 hash map; three points per segment) on the tiny scene.
+    "paper": dict(hash=HashCfg(L=8, log2_T=18, F=4, n_points=3, hidden_layers=4),
+                  leaves=64, res=(64, 64), eye=(0.0, 0.0, 3.5), vfov=40.0,
+                  seeds=dict(mesh=1, weights=12, train=13)),
 }
 
 

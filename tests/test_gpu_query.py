@@ -208,6 +208,14 @@ def test_query_lod_slots(orc):
     assert ctx.cut(1)["n_leaves"] == 8 and ctx.cut(2)["n_leaves"] == 24
 
 
+def test_query_paper_default_variant(orc):
+    """NEXT-4: the paper's own model shape (L=8, F=4, T=2^18, n=3, 4x64 MLP; D_in = 96)."""
+    ctx, sc, tab, layers = _mk_ctx("paper")
+    assert ctx.d_in == 96
+    g, o = _check_query(orc, ctx, tab, layers, _rays_tiny(1500))
+    assert g["hit"].sum() > 200
+
+
 def test_query_host_path_equals_device_path(tiny):
     ctx, sc, tab, layers = tiny
     rays = _rays_tiny()

@@ -123,6 +123,42 @@ def test_weight_gradients_per_layer(hidden, path, monkeypatch):
     assert np.linalg.norm(gb - ob) / np.linalg.norm(ob) <= 3e-2
 
 
+def test_gradients_paper_default_variant():
+    """NEXT-4: F=4 (8-byte entries), n=3 points, 4 hidden layers (D_in = 96: the weight
+    gradients fall back to the mma.sync kernel, Mtot = 288 > 256)."""
+    from paper_2405_16237_b200 import Context, PARAM_TABLES, dp
+    import oracle as orc
+    sc = synth.scene_tiny()
+    ctx = Context(device=0, L=8, F=4, log2_T=18, n_points=3, hidden_layers=4)
+    ctx.set_mesh(sc)
+    ctx.build_cut(64)
+    n = 4000
+    ctx.reserve(n)
+    tab = synth.random_params_fp16(ctx.param_count(PARAM_TABLES), seed=50, lo=-0.5, hi=0.5)
+    ctx.set_params(PARAM_TABLES, tab.astype(np.float32))
+    layers = synth.random_mlp(96, 4, 64, seed=51, out_scale=1.0)
+    ctx.set_mlp(layers)
+    cut = ctx.cut(0)
+    rank = np.zeros(cut["n_leaves"], np.float32)
+    ctx.set_leaf_rank(rank)
+    rays = synth.random_rays(n, seed=52)
+    u = synth.random_uniform(n, seed=53)
+    xi = synth.random_uniform(n * 3, seed=54).reshape(n, 3)
+    o = orc.train_grad(orc.Grid(8, 18, 4), 3, tab.reshape(-1, 4), layers, cut["leaf_lo"], cut["leaf_hi"], rank,
+                       cut["tri_off"], cut["tris"], sc, rays, u, xi, dom_box=orc.scene_box(sc))
+    ctx.train_backward(_to(rays), _to(u), _to(xi))
+    st = ctx.train_stats()
+    assert st["n_accepted"] == o["n_acc"] and o["n_acc"] > 300
+    assert abs(st["loss_sum"] - o["loss_sum"][0]) <= 5e-3 * abs(o["loss_sum"][0])
+    g = dp.grad_tensor(ctx).cpu().numpy().astype(np.float64)
+    m = o["n_acc"]
+    n_t, n_w, n_b = tab.size, o["g_W"].size, o["g_b"].size
+    for name, gg, oo in (("tables", g[:n_t], o["g_table"] * m), ("weights", g[n_t:n_t + n_w], o["g_W"] * m),
+                         ("biases", g[n_t + n_w:n_t + n_w + n_b], o["g_b"] * m)):
+        rel = np.linalg.norm(gg - oo) / np.linalg.norm(oo)
+        assert rel <= 3e-2, (name, rel)
+
+
 def test_adam_step_vs_oracle(batch):
     from paper_2405_16237_b200 import dp, PARAM_ALL
     import oracle as orc

@@ -204,6 +204,11 @@ extern "C" nbvh_status nbvh_create(const nbvh_config* cfg, int cuda_device, nbvh
     x->d_in = d_in;
     level_table(c.L, c.log2_T, c.base_res, c.max_res, x->res, x->dense, x->offset, &x->n_entries);
     x->n_table = x->n_entries * c.F;
+    for (int l = 0; l < c.L; ++l)           // hashed levels: the encode's x term is unmasked (x+1 <= N < T)
+        if (!x->dense[l] && x->res[l] >= (1 << c.log2_T)) {
+            delete x;
+            return NBVH_EINVAL;
+        }
     {   // inference layout: dense levels corner-packed (8 entries per cell), 8-entry aligned
         int64_t o = 0;
         for (int l = 0; l < c.L; ++l) {

@@ -396,11 +396,13 @@ __device__ __forceinline__ void ldg256(const void* p, uint32_t (&r)[8]) {
                  : "l"(p));
 }
 
-// floor of s in [0, 2^23) and its integer value without the XU pipe: adding 2^23 with
-// round-toward-minus-infinity leaves floor(s) in the low mantissa bits (exact), so the
-// floor costs one FADD.RM + one FADD + one integer subtract instead of FRND + F2I.
-__device__ __forceinline__ float floor_small(float s, uint32_t& i) {
-    const float t = __fadd_rd(s, 8388608.0f);
+// Cell coordinate c = min(floor(s), N-1) of s in [0, 2^23) and its integer value without
+// the XU pipe: adding 2^23 with round-toward-minus-infinity leaves floor(s) in the low
+// mantissa bits (exact); the clamp to N-1 is applied in that shifted domain (tops =
+// 2^23 + N-1, exact), so the cell costs FADD.RM + FMNMX + FADD + one integer subtract
+// instead of FRND + F2I + clamps.
+__device__ __forceinline__ float cell_coord(float s, float tops, uint32_t& i) {
+    const float t = fminf(__fadd_rd(s, 8388608.0f), tops);
     i = (uint32_t)(__float_as_int(t) - 0x4B000000);
     return __fsub_rn(t, 8388608.0f);
 }
@@ -411,12 +413,9 @@ __device__ __forceinline__ float floor_small(float s, uint32_t& i) {
 __device__ __forceinline__ void level_cell_sm(const LevelSm& P, uint32_t hmask, float x0, float x1, float x2,
                                               Cell& c) {
     const float s0 = __fmul_rn(x0, P.resf), s1 = __fmul_rn(x1, P.resf), s2 = __fmul_rn(x2, P.resf);
-    const float top = __fsub_rn(P.resf, 1.0f);
-    const uint32_t itop = (uint32_t)__float_as_int(__fadd_rd(top, 8388608.0f)) - 0x4B000000u;
+    const float tops = __fadd_rn(P.resf, 8388607.0f);       // 2^23 + N - 1 (exact)
     uint32_t i0, i1, i2;
-    const float c0 = fminf(floor_small(s0, i0), top), c1 = fminf(floor_small(s1, i1), top),
-                c2 = fminf(floor_small(s2, i2), top);
-    i0 = min(i0, itop); i1 = min(i1, itop); i2 = min(i2, itop);
+    const float c0 = cell_coord(s0, tops, i0), c1 = cell_coord(s1, tops, i1), c2 = cell_coord(s2, tops, i2);
     const float f0 = __fsub_rn(s0, c0), f1 = __fsub_rn(s1, c1), f2 = __fsub_rn(s2, c2);
     if (P.n1) {   // canonical dense vertex index (C2)
         const uint32_t b = i0 + i1 * P.n1 + i2 * P.n1sq;
@@ -456,12 +455,9 @@ __device__ __forceinline__ void encode_issue(const LevelSm* lv, const void* tab,
     for (int j = 0; j < NL; ++j) {
         const LevelSm P = lv[l0 + j];
         const float s0 = __fmul_rn(x0, P.resf), s1 = __fmul_rn(x1, P.resf), s2 = __fmul_rn(x2, P.resf);
-        const float top = __fsub_rn(P.resf, 1.0f);
-        const uint32_t itop = (uint32_t)__float_as_int(__fadd_rd(top, 8388608.0f)) - 0x4B000000u;
+        const float tops = __fadd_rn(P.resf, 8388607.0f);   // 2^23 + N - 1 (exact)
         uint32_t i0, i1, i2;
-        const float c0 = fminf(floor_small(s0, i0), top), c1 = fminf(floor_small(s1, i1), top),
-                    c2 = fminf(floor_small(s2, i2), top);
-        i0 = min(i0, itop); i1 = min(i1, itop); i2 = min(i2, itop);
+        const float c0 = cell_coord(s0, tops, i0), c1 = cell_coord(s1, tops, i1), c2 = cell_coord(s2, tops, i2);
         G.fr[j][0] = __fsub_rn(s0, c0);
         G.fr[j][1] = __fsub_rn(s1, c1);
         G.fr[j][2] = __fsub_rn(s2, c2);
@@ -494,8 +490,9 @@ __device__ __forceinline__ void encode_issue(const LevelSm* lv, const void* tab,
                 }
             }
         } else {
-            // hashed level (C3): (x*1 ^ y*pi2 ^ z*pi3) mod T, masks distributed
-            const uint32_t hx[2] = {i0 & hmask, (i0 + 1u) & hmask};
+            // hashed level (C3): (x*1 ^ y*pi2 ^ z*pi3) mod T, masks distributed; the
+            // x term needs no mask: x+1 <= N < T on every hashed level (checked at creation)
+            const uint32_t hx[2] = {i0, i0 + 1u};
             const uint32_t hy[2] = {(i1 * kPrime1) & hmask, ((i1 + 1u) * kPrime1) & hmask};
             const uint32_t hz[2] = {(i2 * kPrime2) & hmask, ((i2 + 1u) * kPrime2) & hmask};
             // 32-bit entry index (n_entries < 2^32), one IMAD.WIDE.U32 per gather address

@@ -164,6 +164,7 @@ __global__ void __launch_bounds__(128) k_train_label(TrainArgs a) {
     bool found = false;
     double bt = 0, bb1 = 0, bb2 = 0;
     int btri = -1, bslot = -1;
+    float t_cut = t1 * 1.00001f + 1e-6f;        // conservative upper bound: segment end, then best hit
     while (sp > 0) {
         const BvhNode nd = a.nodes[STACK(--sp)];
         float lo[3], hi[3], te, tx;
@@ -174,7 +175,9 @@ __global__ void __launch_bounds__(128) k_train_label(TrainArgs a) {
             hi[k] = nd.hi[k] + e;
         }
         if (!slab(R, lo, hi, te, tx)) continue;
-        if (te > t1 * 1.00001f + 1e-6f || tx < t0 * 0.99999f - 1e-6f) continue;
+        // a node entering beyond the best hit so far holds no closer (or tying) hit: the
+        // conservative boxes and the relative slack keep this exact w.r.t. the double test
+        if (te > t_cut || tx < t0 * 0.99999f - 1e-6f) continue;
         if (nd.b < 0) {
             for (int j = nd.a; j < nd.a - nd.b; ++j) {
                 double th, b1, b2;
@@ -182,12 +185,24 @@ __global__ void __launch_bounds__(128) k_train_label(TrainArgs a) {
                     const int id = a.tri_id[j];
                     if (!found || th < bt || (th == bt && id < btri)) {
                         found = true; bt = th; bb1 = b1; bb2 = b2; btri = id; bslot = j;
+                        t_cut = fminf(t_cut, (float)bt * 1.00001f + 1e-6f);
                     }
                 }
             }
         } else if (sp + 2 <= 64) {
-            STACK(sp++) = nd.b;
-            STACK(sp++) = nd.a;
+            // visit the nearer child first (by its box centre along the ray) so the best hit
+            // tightens t_cut early
+            const BvhNode& ca = a.nodes[nd.a];
+            const BvhNode& cb = a.nodes[nd.b];
+            float da = 0.f, db = 0.f;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                da = fmaf(ca.lo[k] + ca.hi[k], R.d[k], da);
+                db = fmaf(cb.lo[k] + cb.hi[k], R.d[k], db);
+            }
+            const bool a_first = da <= db;
+            STACK(sp++) = a_first ? nd.b : nd.a;
+            STACK(sp++) = a_first ? nd.a : nd.b;
         }
     }
 #undef STACK
@@ -602,6 +617,8 @@ __global__ void __launch_bounds__(256, 1) k_train_bwd(TrainArgs a) {
             const int nv = min(kTileQ, M - tile * kTileQ);
             const int nqb = (nv + 31) >> 5;
             const int npl = a.g.n_points * a.g.L;
+            // consecutive items of a warp go to different point-levels (and table regions):
+            // measured faster than sweeping one level over all sample blocks (atomic spread)
             for (int it = warp; it < nqb * npl; it += 8) {
                 const int pl = it / nqb, qb = it - pl * nqb;
                 const int q = qb * 32 + lane;

@@ -241,7 +241,8 @@ static cudaError_t launch_train_fd(const TrainArgs& a, int64_t n, int64_t w_off,
     if (ev) cudaEventRecord(ev[2], s);
     const int tiles = (int)((n + kTileQ - 1) / kTileQ);
     const int grid = tiles < sms ? (tiles > 0 ? tiles : 1) : sms;
-    k_train_fwd<F, D><<<grid, 256, smem_fwd, s>>>(a);
+    const int grid_fwd = tiles < 2 * sms ? (tiles > 0 ? tiles : 1) : 2 * sms;   // 2 CTAs per SM
+    k_train_fwd<F, D><<<grid_fwd, 256, smem_fwd, s>>>(a);
     if (ev) cudaEventRecord(ev[3], s);
     k_train_bwd<F, D><<<grid, 256, smem_bwd, s>>>(a);
     if (ev) cudaEventRecord(ev[4], s);

@@ -306,7 +306,7 @@ __device__ __forceinline__ float2 unpack_half2(uint32_t v) {
 // encode into shared memory, MLP forward with the hidden activations written out for
 // the backward pass, then the gated loss and dL/dz per sample.
 template <int F, int D>
-__global__ void __launch_bounds__(256, 1) k_train_fwd(TrainArgs a) {
+__global__ void __launch_bounds__(256, 2) k_train_fwd(TrainArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int M = *a.n_samples;

@@ -90,7 +90,7 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def build_model(cfg_name: str, device: int, rank: int = 0, list_cap: int = 8):
+def build_model(cfg_name: str, device: int, rank: int = 0, list_cap: int = 12):
     """Synthetic scene + cut + random-init model of the named BASELINE config."""
     from paper_2405_16237_b200 import Context, PARAM_TABLES
     c = synth.CONFIGS[cfg_name]
@@ -484,7 +484,7 @@ def main():
     ap.add_argument("--config", default="1080p", choices=["1080p", "tiny"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle timing budget (0 = skip)")
-    ap.add_argument("--list-cap", type=int, default=8, help="per-ray ordered leaf-list capacity K (C6)")
+    ap.add_argument("--list-cap", type=int, default=12, help="per-ray ordered leaf-list capacity K (C6)")
     ap.add_argument("--train", type=int, default=1, help="also time the cfg-5 training step (1/0)")
     ap.add_argument("--lod", type=int, default=1, help="also run the cfg-4 multi-cut LoD query (1/0)")
     args = ap.parse_args()

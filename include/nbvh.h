@@ -77,7 +77,7 @@ typedef struct {
     int32_t n_points;       /* samples per ray segment (three; BASELINE: 4)          */
     int32_t hidden_layers;  /* hidden layers of width 64 (4; BASELINE: 2 or 3)       */
     int32_t width;          /* hidden width; must be 64                                     */
-    int32_t list_cap;       /* per-ray ordered leaf-list capacity K, 1..16, default 8 (C6) */
+    int32_t list_cap;       /* per-ray ordered leaf-list capacity K, 1..16, default 12 (C6) */
     int32_t mode;           /* 0 = nearest confident hit (R2), 1 = first confident hit (R1) (C5) */
     float inflate_rel;      /* node inflation, fraction of node diagonal (C15: 1e-3)        */
     float inflate_abs;      /* node inflation floor, fraction of scene diagonal (C15: 1e-6) */

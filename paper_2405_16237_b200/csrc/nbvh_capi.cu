@@ -168,7 +168,7 @@ extern "C" void nbvh_config_default(nbvh_config* cfg) {
     cfg->n_points = 4;
     cfg->hidden_layers = 2;
     cfg->width = 64;
-    cfg->list_cap = 8;
+    cfg->list_cap = 12;
     cfg->mode = 0;
     cfg->inflate_rel = 1e-3f;
     cfg->inflate_abs = 1e-6f;

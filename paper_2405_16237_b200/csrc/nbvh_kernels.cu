@@ -21,28 +21,102 @@
 namespace nbvh {
 
 // ------------------------------------------------------------------ traversal
-// K = register capacity of the ordered list (the runtime cap <= K); the traversal stack
-// lives in shared memory, one column per thread, rows = cut depth + 2.
-template <int K>
+// Q1 traversal of one ray with the ordered list held in shared memory (column layout
+// [3][cap][blockDim]: t_enter, t_exit, leaf id), so inserting a leaf is a short shift loop
+// instead of a K-wide predicated compare-swap in registers.  Leaves arrive roughly in
+// front-to-back order (nearer child first), so the shift is usually empty.  Same result as
+// collect_leaves<K>(..., prune = true): the `cap` smallest (t_enter, id) keys, sorted;
+// `more` reports whether further intersected leaves may exist (C6).
+__device__ __forceinline__ int traverse_smem_list(const CutDev& cut, const RayDev& R, int cap, float* lte, float* ltx,
+                                                  int* lid, int S, SmemStack& stack, bool& more, int* err) {
+    int n = 0;
+    bool dropped = false;
+    auto consider = [&](int leaf, float te, float tx) {
+        int pos;
+        if (n == cap) {
+            if (!key_less(te, leaf, lte[(cap - 1) * S], lid[(cap - 1) * S])) {
+                dropped = true;
+                return;
+            }
+            dropped = true;                      // the current last entry falls off
+            pos = cap - 1;
+        } else {
+            pos = n++;
+        }
+        while (pos > 0) {
+            const float pte = lte[(pos - 1) * S];
+            const int pid = lid[(pos - 1) * S];
+            if (!key_less(te, leaf, pte, pid)) break;
+            lte[pos * S] = pte;
+            ltx[pos * S] = ltx[(pos - 1) * S];
+            lid[pos * S] = pid;
+            --pos;
+        }
+        lte[pos * S] = te;
+        ltx[pos * S] = tx;
+        lid[pos * S] = leaf;
+    };
+    if (cut.n_leaves == 1) {
+        float4 a = __ldg(cut.leaf_box), b = __ldg(cut.leaf_box + 1);
+        float lo[3] = {a.x, a.y, a.z}, hi[3] = {b.x, b.y, b.z}, te, tx;
+        if (slab(R, lo, hi, te, tx)) consider(0, te, tx);
+    } else {
+        stack.sp = 0;
+        stack.push(0);
+        while (stack.sp > 0) {
+            const float4* p = reinterpret_cast<const float4*>(cut.inner + stack.pop());
+            float4 q0 = __ldg(p), q1 = __ldg(p + 1), q2 = __ldg(p + 2), q3 = __ldg(p + 3);
+            float llo[3] = {q0.x, q0.y, q0.z}, lhi[3] = {q0.w, q1.x, q1.y};
+            float rlo[3] = {q1.z, q1.w, q2.x}, rhi[3] = {q2.y, q2.z, q2.w};
+            int cl = __float_as_int(q3.x), cr = __float_as_int(q3.y);
+            float lte_, ltx_, rte_, rtx_;
+            bool hl = slab(R, llo, lhi, lte_, ltx_);
+            bool hr = slab(R, rlo, rhi, rte_, rtx_);
+            if (hl && cl < 0) consider(-1 - cl, lte_, ltx_);
+            if (hr && cr < 0) consider(-1 - cr, rte_, rtx_);
+            bool pl = hl && cl >= 0, pr = hr && cr >= 0;
+            if (n == cap) {                       // subtrees entering after the cap-th key
+                const float last = lte[(cap - 1) * S];
+                if (pl && lte_ > last) { pl = false; dropped = true; }
+                if (pr && rte_ > last) { pr = false; dropped = true; }
+            }
+            if (stack.sp + 2 > stack.cap) { atomicOr(err, 1); break; }
+            if (pl && pr) {
+                bool l_first = lte_ <= rte_;
+                stack.push(l_first ? cr : cl);
+                stack.push(l_first ? cl : cr);
+            } else if (pl) {
+                stack.push(cl);
+            } else if (pr) {
+                stack.push(cr);
+            }
+        }
+    }
+    more = dropped;
+    return n;
+}
+
+// One thread per ray: traversal stack and ordered list in shared memory (stack rows =
+// cut depth + 2, list rows = 3 * cap).
 __global__ void __launch_bounds__(128) k_traverse(TraverseArgs a) {
-    extern __shared__ int stk_raw[];
+    extern __shared__ int sm_raw[];
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const bool valid = r < a.n_rays;
     bool active = false;
+    const int S = blockDim.x;
+    float* lte = reinterpret_cast<float*>(sm_raw) + threadIdx.x;
+    float* ltx = lte + a.cap * S;
+    int* lid = sm_raw + 2 * a.cap * S + threadIdx.x;
     if (valid) {
         RayDev R = load_ray(a.rays, r);
-        float lte[K], ltx[K];
-        int lid[K], n = 0;
         bool more = false;
-        SmemStack st{stk_raw + threadIdx.x, (int)blockDim.x, a.cut.depth + 2};
-        collect_leaves<K, SmemStack>(a.cut, R, false, 0.f, 0, a.cap, lte, ltx, lid, n, &a.ctr->err, st, true, &more);
-#pragma unroll
-        for (int j = 0; j < K; ++j)
-            if (j < n) {
-                a.lst_leaf[(int64_t)j * a.n_rays + r] = lid[j];
-                a.lst_te[(int64_t)j * a.n_rays + r] = lte[j];
-                a.lst_tx[(int64_t)j * a.n_rays + r] = ltx[j];
-            }
+        SmemStack st{sm_raw + 3 * a.cap * S + threadIdx.x, S, a.cut.depth + 2};
+        const int n = traverse_smem_list(a.cut, R, a.cap, lte, ltx, lid, S, st, more, &a.ctr->err);
+        for (int j = 0; j < n; ++j) {
+            a.lst_leaf[(int64_t)j * a.n_rays + r] = lid[j * S];
+            a.lst_te[(int64_t)j * a.n_rays + r] = lte[j * S];
+            a.lst_tx[(int64_t)j * a.n_rays + r] = ltx[j * S];
+        }
         active = n > 0;
         if (active) {
             a.st.nbuf[r] = n;
@@ -482,11 +556,8 @@ cudaError_t launch_query(const QueryArgs& a, int64_t max_work, cudaStream_t s) {
 
 cudaError_t launch_traverse(const TraverseArgs& a, cudaStream_t s) {
     const int64_t blocks = (a.n_rays + 127) / 128;
-    const size_t smem = (size_t)(a.cut.depth + 2) * 128 * sizeof(int);
-    if (a.cap <= 2) k_traverse<2><<<(unsigned)blocks, 128, smem, s>>>(a);
-    else if (a.cap <= 4) k_traverse<4><<<(unsigned)blocks, 128, smem, s>>>(a);
-    else if (a.cap <= 8) k_traverse<8><<<(unsigned)blocks, 128, smem, s>>>(a);
-    else k_traverse<16><<<(unsigned)blocks, 128, smem, s>>>(a);
+    const size_t smem = (size_t)(a.cut.depth + 2 + 3 * a.cap) * 128 * sizeof(int);
+    k_traverse<<<(unsigned)blocks, 128, smem, s>>>(a);
     return cudaGetLastError();
 }
 

@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -241,11 +242,11 @@ extern "C" nbvh_status nbvh_create(const nbvh_config* cfg, int cuda_device, nbvh
         if (e == cudaSuccess) e = dalloc(&x->d_params, x->h_params.size());
         if (e == cudaSuccess) e = dalloc(&x->d_table16, x->n_inf * c.F);
         if (e == cudaSuccess) e = dalloc(&x->d_W16, x->n_W);
-        if (e == cudaSuccess) e = dalloc(&x->d_misc, 64);
-        if (e == cudaSuccess) e = cudaMallocHost((void**)&x->h_misc, 64 * sizeof(int32_t));
+        if (e == cudaSuccess) e = dalloc(&x->d_misc, kCounterBlocks * kCounterStride);
+        if (e == cudaSuccess) e = cudaMallocHost((void**)&x->h_misc, kCounterBlocks * kCounterStride * sizeof(int32_t));
         if (e == cudaSuccess)
             e = cudaMemcpy(x->d_params, x->h_params.data(), x->h_params.size() * 4, cudaMemcpyHostToDevice);
-        if (e == cudaSuccess) e = cudaMemset(x->d_misc, 0, 64 * sizeof(int32_t));
+        if (e == cudaSuccess) e = cudaMemset(x->d_misc, 0, kCounterBlocks * kCounterStride * sizeof(int32_t));
         if (e != cudaSuccess) {
             x->err = std::string("nbvh_create: ") + cudaGetErrorString(e);
             nbvh_destroy(x);
@@ -272,6 +273,7 @@ static void free_workspace(nbvh_ctx* c) {
     dfree(c->d_lst_tx);
     dfree(c->d_state);
     dfree(c->d_act);
+    dfree(c->d_act_long);
     dfree(c->d_stage_rays);
     dfree(c->d_stage_hits);
     c->reserved = 0;
@@ -379,6 +381,7 @@ extern "C" nbvh_status nbvh_reserve(nbvh_ctx* c, int64_t max_rays) {
     if (e == cudaSuccess) e = dalloc(&c->d_lst_tx, kListK * n);
     if (e == cudaSuccess) e = dalloc(&c->d_state, 2 * n);
     if (e == cudaSuccess) e = dalloc(&c->d_act, n);
+    if (e == cudaSuccess) e = dalloc(&c->d_act_long, n);
     if (e == cudaSuccess) e = dalloc(&c->d_stage_rays, 8 * n);
     if (e == cudaSuccess) e = dalloc(&c->d_stage_hits, 10 * n);
     if (e != cudaSuccess) {
@@ -517,6 +520,17 @@ extern "C" nbvh_status nbvh_get_cut(const nbvh_ctx* c, int32_t lod, float* leaf_
 // ------------------------------------------------------------------ query
 namespace nbvh {
 
+__global__ void k_reset_counters(QueryCounters* ctr, int all) {
+    int32_t* w = reinterpret_cast<int32_t*>(ctr);
+    const int n = (int)(sizeof(QueryCounters) / sizeof(int32_t));
+    const int t = threadIdx.x;    // per-launch words: cnt (2), next (3), cnt_long (5)
+    if (t < n && (all || t == 2 || t == 3 || t == 5)) w[t] = 0;
+}
+
+QueryCounters* counter_block(nbvh_ctx* c, int block) {
+    return reinterpret_cast<QueryCounters*>(c->d_misc + (size_t)block * kCounterStride);
+}
+
 cudaEvent_t ctx_event(nbvh_ctx* c, int i) {
     while ((int)c->events.size() <= i) {
         cudaEvent_t x;
@@ -531,23 +545,35 @@ cudaEvent_t ctx_event(nbvh_ctx* c, int i) {
 // counter block (statistics of a public call); otherwise only the per-launch work-list
 // counters are reset and the statistics accumulate (chunked host path).
 nbvh_status run_query(nbvh_ctx* c, const nbvh_ray* rays, int64_t n, int32_t lod, const HitsDev& out, float* z_trace,
-                      int32_t trace_cap, cudaStream_t s, bool reset_stats) {
-    QueryCounters* ctr = reinterpret_cast<QueryCounters*>(c->d_misc);
-    cudaError_t e = reset_stats ? cudaMemsetAsync(ctr, 0, sizeof(QueryCounters), s)
-                                : cudaMemsetAsync(&ctr->cnt, 0, 2 * sizeof(int32_t), s);
-    if (e != cudaSuccess) return cuda_fail(c, e, "query: memset");
-    const RayState st = c->state();
+                      int32_t trace_cap, cudaStream_t s, bool reset_stats, int64_t work_off, int block) {
+    // workspace slice [work_off, work_off + n) of every per-ray buffer and counter block
+    // `block`: disjoint slices let the host path run two chunks' queries concurrently
+    QueryCounters* ctr = counter_block(c, block);
+    // counter reset by a one-thread kernel, not cudaMemsetAsync: a memset may queue on a copy
+    // engine behind the host path's bulk uploads and serialise the pipeline
+    k_reset_counters<<<1, 32, 0, s>>>(ctr, reset_stats ? 1 : 0);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(c, e, "query: counter reset");
+    RayState st = c->state();
+    st.nbuf += work_off;
+    st.more += work_off;
+    int32_t* lst_leaf = c->d_lst_leaf + kListK * work_off;
+    float* lst_te = c->d_lst_te + kListK * work_off;
+    float* lst_tx = c->d_lst_tx + kListK * work_off;
+    int32_t* act = c->d_act + work_off;
+    int32_t* act_long = c->d_act_long + work_off;
     TraverseArgs ta{};
     ta.cut = make_cut(c, lod);
     ta.rays = reinterpret_cast<const float4*>(rays);
     ta.n_rays = n;
     ta.cap = c->cfg.list_cap;
-    ta.lst_leaf = c->d_lst_leaf;
-    ta.lst_te = c->d_lst_te;
-    ta.lst_tx = c->d_lst_tx;
+    ta.lst_leaf = lst_leaf;
+    ta.lst_te = lst_te;
+    ta.lst_tx = lst_tx;
     ta.st = st;
     ta.out = out;
-    ta.act_out = c->d_act;
+    ta.act_out = act;
+    ta.act_long = act_long;
     ta.ctr = ctr;
     if (c->profiling) cudaEventRecord(ctx_event(c, 0), s);
     e = launch_traverse(ta, s);
@@ -561,14 +587,16 @@ nbvh_status run_query(nbvh_ctx* c, const nbvh_ray* rays, int64_t n, int32_t lod,
     qa.n_rays = n;
     qa.cap = c->cfg.list_cap;
     qa.mode = c->cfg.mode;
-    qa.lst_leaf = c->d_lst_leaf;
-    qa.lst_te = c->d_lst_te;
-    qa.lst_tx = c->d_lst_tx;
+    qa.lst_leaf = lst_leaf;
+    qa.lst_te = lst_te;
+    qa.lst_tx = lst_tx;
     qa.nbuf = st.nbuf;
     qa.more = st.more;
     qa.out = out;
-    qa.act = c->d_act;
+    qa.act = act;
     qa.cnt = &ctr->cnt;
+    qa.act_long = act_long;
+    qa.cnt_long = &ctr->cnt_long;
     qa.next = &ctr->next;
     qa.z_trace = z_trace;
     qa.trace_cap = trace_cap;
@@ -576,30 +604,42 @@ nbvh_status run_query(nbvh_ctx* c, const nbvh_ray* rays, int64_t n, int32_t lod,
     e = launch_query(qa, n, s);
     if (e != cudaSuccess) return cuda_fail(c, e, "query: persistent query kernel");
     if (c->profiling) cudaEventRecord(ctx_event(c, 2), s);
-    if (reset_stats) {
+    if (reset_stats && block == 0) {
         c->qstats = nbvh_query_stats{};
         c->qstats_launches = 0;
+        c->qstats_blocks = 1;
     }
+    c->qstats_blocks = std::max(c->qstats_blocks, block + 1);
     c->qstats.n_rays += n;
-    c->qstats_launches += 2;
+    c->qstats_launches += 3;
     c->qstats_pending = true;
     c->qstats_stream = s;
     return NBVH_OK;
 }
 
-// Resolve the device counters of the last query call (synchronises its stream).
+// Resolve the device counters of the last query call (synchronises the device: the host
+// path's chunks run on two streams).
 nbvh_status resolve_query_stats(nbvh_ctx* c) {
     if (!c->qstats_pending) return NBVH_OK;
-    cudaError_t e = cudaMemcpyAsync(c->h_misc, c->d_misc, sizeof(QueryCounters), cudaMemcpyDeviceToHost,
-                                    c->qstats_stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(c->qstats_stream);
+    const int nb = std::max(1, c->qstats_blocks);
+    cudaError_t e = cudaStreamSynchronize(c->qstats_stream);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaMemcpy(c->h_misc, c->d_misc, (size_t)nb * kCounterStride * 4, cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) return cuda_fail(c, e, "query stats");
-    const QueryCounters* q = reinterpret_cast<const QueryCounters*>(c->h_misc);
     c->qstats_pending = false;
-    c->qstats.n_queries = (int64_t)q->n_queries;
-    c->qstats.n_iters = q->max_iter;
+    int64_t nq = 0;
+    int32_t iters = 0, refills = 0, err = 0;
+    for (int b = 0; b < nb; ++b) {
+        const QueryCounters* q = reinterpret_cast<const QueryCounters*>(c->h_misc + (size_t)b * kCounterStride);
+        nq += (int64_t)q->n_queries;
+        iters = std::max(iters, q->max_iter);
+        refills += q->refills;
+        err |= q->err;
+    }
+    c->qstats.n_queries = nq;
+    c->qstats.n_iters = iters;
     c->qstats.n_launches = c->qstats_launches;
-    c->qstats.n_refills = q->refills;
+    c->qstats.n_refills = refills;
     c->qstats.ms_traverse = 0.f;
     c->qstats.ms_query = 0.f;
     if (c->profiling && c->events.size() >= 3) {
@@ -608,7 +648,7 @@ nbvh_status resolve_query_stats(nbvh_ctx* c) {
         if (cudaEventElapsedTime(&ms, c->events[1], c->events[2]) == cudaSuccess) c->qstats.ms_query = ms;
         cudaGetLastError();
     }
-    if (q->err) return fail(c, NBVH_ECUDA, "query: traversal stack overflow (N-BVH deeper than 64)");
+    if (err) return fail(c, NBVH_ECUDA, "query: traversal stack overflow (N-BVH deeper than 64)");
     return NBVH_OK;
 }
 
@@ -634,8 +674,84 @@ extern "C" nbvh_status nbvh_query(nbvh_ctx* c, const nbvh_ray* rays, int64_t n, 
     nbvh_status st = check_query(c, rays, n, lod, out);
     if (st) return st;
     if (n == 0) return NBVH_OK;
-    return run_query(c, rays, n, lod, to_dev(out), nullptr, 0, (cudaStream_t)stream, true);
+    return run_query(c, rays, n, lod, to_dev(out), nullptr, 0, (cudaStream_t)stream, true, 0, 0);
 }
+
+// Block-interleaved chunking of the host path.  The ray array is cut into blocks of
+// kHostBlock rays grouped in periods of W = sum(w_k) blocks; chunk k takes w_k consecutive
+// blocks of every period (one strided 2-D copy per direction and field), so every chunk
+// samples the whole frame and carries work in proportion to w_k (contiguous chunks of an
+// image are sky at the top and terrain at the bottom).  The first and last chunks are
+// lighter so the pipeline's head (first upload) and tail (last download) are short.
+// Blocks after the last full period go to the last chunk.
+namespace nbvh {
+constexpr int64_t kHostBlock = 1024;
+constexpr int kMaxChunks = 8;
+
+struct ChunkPlan {
+    int64_t w = 0;             // blocks per period
+    int64_t first = 0;         // first block of the chunk within a period
+    int64_t rows = 0;          // full periods
+    int64_t tail = 0;          // rays of the trailing region (last chunk only)
+    int64_t dev_off = 0;       // first ray of the chunk in the device staging buffers
+    int64_t size() const { return rows * w * kHostBlock + tail; }
+};
+
+static int plan_chunks(int64_t n, ChunkPlan* plan) {
+    int wts[kMaxChunks] = {1, 2, 3, 3, 2, 1};                     // measured best of a sweep (1080p)
+    int chunks = n >= (1 << 20) ? 6 : (n >= (1 << 18) ? 2 : 1);
+    if (chunks == 2) wts[0] = wts[1] = 1;
+    if (chunks == 1) wts[0] = 1;
+    if (const char* ev = std::getenv("NBVH_HOST_WEIGHTS")) {     // tuning hook, e.g. "1,2,2,2,1"
+        chunks = 0;
+        for (const char* p = ev; *p && chunks < kMaxChunks;) {
+            wts[chunks++] = std::max(1, std::atoi(p));
+            while (*p && *p != ',') ++p;
+            if (*p == ',') ++p;
+        }
+        if (chunks == 0) { chunks = 1; wts[0] = 1; }
+    }
+    int64_t W = 0;
+    for (int k = 0; k < chunks; ++k) W += wts[k];
+    const int64_t periods = n / (kHostBlock * W);
+    int64_t off = 0, first = 0;
+    for (int k = 0; k < chunks; ++k) {
+        ChunkPlan& p = plan[k];
+        p.w = wts[k];
+        p.first = first;
+        first += wts[k];
+        p.rows = periods;
+        p.tail = k == chunks - 1 ? n - periods * W * kHostBlock : 0;
+        p.dev_off = off;
+        off += p.size();
+    }
+    return chunks;
+}
+
+// strided host <-> contiguous device copy of one field of a chunk (elem bytes per ray)
+static cudaError_t copy_chunk(void* host, void* dev, size_t elem, int64_t n, int64_t W, const ChunkPlan& p,
+                              cudaMemcpyKind kind, cudaStream_t s) {
+    char* h = static_cast<char*>(host);
+    char* d = static_cast<char*>(dev) + p.dev_off * elem;
+    const size_t bw = (size_t)kHostBlock * elem;
+    cudaError_t e = cudaSuccess;
+    if (p.rows) {
+        char* hb = h + (size_t)p.first * bw;
+        const size_t width = (size_t)p.w * bw, hpitch = (size_t)W * bw;
+        if (kind == cudaMemcpyHostToDevice)
+            e = cudaMemcpy2DAsync(d, width, hb, hpitch, width, (size_t)p.rows, kind, s);
+        else
+            e = cudaMemcpy2DAsync(hb, hpitch, d, width, width, (size_t)p.rows, kind, s);
+    }
+    if (e == cudaSuccess && p.tail) {
+        char* ht = h + (size_t)(n - p.tail) * elem;
+        char* dt = d + (size_t)(p.rows * p.w) * bw;
+        e = kind == cudaMemcpyHostToDevice ? cudaMemcpyAsync(dt, ht, (size_t)p.tail * elem, kind, s)
+                                           : cudaMemcpyAsync(ht, dt, (size_t)p.tail * elem, kind, s);
+    }
+    return e;
+}
+}  // namespace nbvh
 
 extern "C" nbvh_status nbvh_query_host(nbvh_ctx* c, const nbvh_ray* h_rays, int64_t n, int32_t lod, nbvh_hits h_out,
                                        void* stream) {
@@ -647,14 +763,23 @@ extern "C" nbvh_status nbvh_query_host(nbvh_ctx* c, const nbvh_ray* h_rays, int6
     // second auxiliary stream; events order chunk k's query after its upload and its
     // download after its query, so copies of chunks k+1 / k-1 overlap the query of chunk k.
     cudaStream_t S = (cudaStream_t)stream;
-    for (int i = 0; i < 2; ++i)
+    for (int i = 0; i < 3; ++i)
         if (!c->aux_stream[i]) {
             cudaError_t e0 = cudaStreamCreateWithFlags(&c->aux_stream[i], cudaStreamNonBlocking);
             if (e0 != cudaSuccess) return cuda_fail(c, e0, "query_host: stream");
         }
     cudaStream_t H = c->aux_stream[0], Dn = c->aux_stream[1];
-    const int chunks = n >= (1 << 20) ? 4 : (n >= (1 << 18) ? 2 : 1);
-    const int64_t step = (n + chunks - 1) / chunks;
+    // chunks alternate between the caller's stream and a second query stream; each chunk uses
+    // its own workspace slice and counter block, so consecutive chunks' kernels overlap (one
+    // chunk's tail CTAs next to the next chunk's first CTAs)
+    cudaStream_t Q[2] = {S, c->aux_stream[2]};
+    cudaError_t e0 = cudaEventRecord(ctx_event(c, 31), S);            // Q[1] starts after prior work on S
+    if (e0 == cudaSuccess) e0 = cudaStreamWaitEvent(Q[1], ctx_event(c, 31), 0);
+    if (e0 != cudaSuccess) return cuda_fail(c, e0, "query_host: stream order");
+    ChunkPlan plan[kMaxChunks];
+    const int chunks = plan_chunks(n, plan);
+    int64_t W = 0;
+    for (int k = 0; k < chunks; ++k) W += plan[k].w;
     // staging layout: t[n], normal[3n], albedo[3n], leaf[n], nq[n], hit bytes
     float* base = c->d_stage_hits;
     HitsDev d{};
@@ -664,39 +789,43 @@ extern "C" nbvh_status nbvh_query_host(nbvh_ctx* c, const nbvh_ray* h_rays, int6
     d.leaf = reinterpret_cast<int32_t*>(base + 7 * n);
     d.n_queries = reinterpret_cast<int32_t*>(base + 8 * n);
     d.hit = reinterpret_cast<uint8_t*>(base + 9 * n);
-    const nbvh_ray* d_rays = reinterpret_cast<const nbvh_ray*>(c->d_stage_rays);
+    nbvh_ray* d_rays = reinterpret_cast<nbvh_ray*>(c->d_stage_rays);
     cudaError_t e = cudaSuccess;
-    // events 8.. : [8+2k] upload k done, [9+2k] query k done
+    // events 32.. : [32+2k] upload k done, [33+2k] query k done (0-2 query profiling, 16-23 training)
     for (int k = 0; k < chunks && e == cudaSuccess; ++k) {
-        const int64_t o = k * step, m = std::min(step, n - o);
-        e = cudaMemcpyAsync((void*)(d_rays + o), h_rays + o, (size_t)m * sizeof(nbvh_ray), cudaMemcpyHostToDevice, H);
-        if (e == cudaSuccess) e = cudaEventRecord(ctx_event(c, 8 + 2 * k), H);
+        e = copy_chunk(const_cast<nbvh_ray*>(h_rays), d_rays, sizeof(nbvh_ray), n, W, plan[k],
+                       cudaMemcpyHostToDevice, H);
+        if (e == cudaSuccess) e = cudaEventRecord(ctx_event(c, 32 + 2 * k), H);
     }
     if (e != cudaSuccess) return cuda_fail(c, e, "query_host: H2D");
     for (int k = 0; k < chunks; ++k) {
-        const int64_t o = k * step, m = std::min(step, n - o);
+        const int64_t o = plan[k].dev_off, m = plan[k].size();
+        if (m == 0) continue;
         HitsDev dk{d.hit + o, d.t + o, d.normal + 3 * o, d.albedo + 3 * o, d.leaf + o, d.n_queries + o};
-        e = cudaStreamWaitEvent(S, ctx_event(c, 8 + 2 * k), 0);
+        cudaStream_t Sq = Q[k & 1];
+        e = cudaStreamWaitEvent(Sq, ctx_event(c, 32 + 2 * k), 0);
         if (e != cudaSuccess) return cuda_fail(c, e, "query_host: wait");
-        st = run_query(c, d_rays + o, m, lod, dk, nullptr, 0, S, k == 0);
+        st = run_query(c, d_rays + o, m, lod, dk, nullptr, 0, Sq, true, o, k);
         if (st) return st;
-        e = cudaEventRecord(ctx_event(c, 9 + 2 * k), S);
-        if (e == cudaSuccess) e = cudaStreamWaitEvent(Dn, ctx_event(c, 9 + 2 * k), 0);
-        if (e == cudaSuccess) e = cudaMemcpyAsync(h_out.hit + o, dk.hit, (size_t)m, cudaMemcpyDeviceToHost, Dn);
-        if (e == cudaSuccess) e = cudaMemcpyAsync(h_out.t + o, dk.t, (size_t)m * 4, cudaMemcpyDeviceToHost, Dn);
+        e = cudaEventRecord(ctx_event(c, 33 + 2 * k), Sq);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(Dn, ctx_event(c, 33 + 2 * k), 0);
+        if (e == cudaSuccess) e = copy_chunk(h_out.hit, d.hit, 1, n, W, plan[k], cudaMemcpyDeviceToHost, Dn);
+        if (e == cudaSuccess) e = copy_chunk(h_out.t, d.t, 4, n, W, plan[k], cudaMemcpyDeviceToHost, Dn);
         if (e == cudaSuccess)
-            e = cudaMemcpyAsync(h_out.normal + 3 * o, dk.normal, (size_t)m * 12, cudaMemcpyDeviceToHost, Dn);
+            e = copy_chunk(h_out.normal, d.normal, 12, n, W, plan[k], cudaMemcpyDeviceToHost, Dn);
         if (e == cudaSuccess)
-            e = cudaMemcpyAsync(h_out.albedo + 3 * o, dk.albedo, (size_t)m * 12, cudaMemcpyDeviceToHost, Dn);
+            e = copy_chunk(h_out.albedo, d.albedo, 12, n, W, plan[k], cudaMemcpyDeviceToHost, Dn);
         if (e == cudaSuccess && h_out.leaf)
-            e = cudaMemcpyAsync(h_out.leaf + o, dk.leaf, (size_t)m * 4, cudaMemcpyDeviceToHost, Dn);
+            e = copy_chunk(h_out.leaf, d.leaf, 4, n, W, plan[k], cudaMemcpyDeviceToHost, Dn);
         if (e == cudaSuccess && h_out.n_queries)
-            e = cudaMemcpyAsync(h_out.n_queries + o, dk.n_queries, (size_t)m * 4, cudaMemcpyDeviceToHost, Dn);
+            e = copy_chunk(h_out.n_queries, d.n_queries, 4, n, W, plan[k], cudaMemcpyDeviceToHost, Dn);
         if (e != cudaSuccess) return cuda_fail(c, e, "query_host: copies");
     }
     e = cudaStreamSynchronize(Dn);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(Q[1]);
     if (e == cudaSuccess) e = cudaStreamSynchronize(S);
     if (e != cudaSuccess) return cuda_fail(c, e, "query_host: D2H");
+    c->qstats.n_rays = n;
     return NBVH_OK;
 }
 
@@ -780,5 +909,5 @@ extern "C" nbvh_status nbvh_debug_query_trace(nbvh_ctx* c, const nbvh_ray* rays,
     cudaStream_t s = (cudaStream_t)stream;
     cudaError_t e = cudaMemsetAsync(z_trace, 0xff, (size_t)n * cap * 8 * sizeof(float), s);   // NaN
     if (e != cudaSuccess) return cuda_fail(c, e, "debug_query_trace: memset");
-    return run_query(c, rays, n, lod, to_dev(out), z_trace, cap, s, true);
+    return run_query(c, rays, n, lod, to_dev(out), z_trace, cap, s, true, 0, 0);
 }

@@ -30,6 +30,8 @@ struct DeviceScene {
 };
 
 struct TrainWork;   // nbvh_train.cu
+constexpr int kCounterStride = 16;  // int32 words per QueryCounters block (64 B)
+constexpr int kCounterBlocks = 16;
 }  // namespace nbvh
 
 struct nbvh_ctx {
@@ -69,17 +71,19 @@ struct nbvh_ctx {
     float* d_lst_tx = nullptr;
     int32_t* d_state = nullptr;        // 2 arrays of n int32: list fill, "more leaves" flag
     int32_t* d_act = nullptr;          // work list of the persistent query kernel
-    int32_t* d_misc = nullptr;         // 64 int32: QueryCounters at offset 0
+    int32_t* d_act_long = nullptr;     // its long-ray part (consumed first)
+    int32_t* d_misc = nullptr;         // kCounterBlocks QueryCounters blocks, kCounterStride int32 apart
     int32_t* h_misc = nullptr;         // pinned mirror
     float* d_stage_rays = nullptr;     // host-path staging
     float* d_stage_hits = nullptr;
     nbvh_query_stats qstats{};
     int32_t qstats_launches = 0;
     bool qstats_pending = false;       // device counters not yet read back
+    int qstats_blocks = 1;             // counter blocks used by the last call
     cudaStream_t qstats_stream = nullptr;
     bool profiling = false;
-    cudaStream_t aux_stream[2] = {nullptr, nullptr};  // upload / download streams of the host path
-    std::vector<cudaEvent_t> events;   // [0..2] profiling (traverse, query); [8..] host-path chunk order
+    cudaStream_t aux_stream[3] = {nullptr, nullptr, nullptr};  // upload / download / 2nd query stream (host path)
+    std::vector<cudaEvent_t> events;   // [0..2] query profiling, [16..23] training phases, [32..] host-path chunk order
 
     // training
     nbvh::TrainWork* train = nullptr;
@@ -103,6 +107,7 @@ CutDev make_cut(const nbvh_ctx* c, int lod);
 nbvh_status refresh_fp16(nbvh_ctx* c, cudaStream_t s);
 nbvh_status refresh_table(nbvh_ctx* c, cudaStream_t s);
 cudaEvent_t ctx_event(nbvh_ctx* c, int i);
+QueryCounters* counter_block(nbvh_ctx* c, int block);
 nbvh_status resolve_query_stats(nbvh_ctx* c);
 // nbvh_train.cu
 nbvh_status upload_scene(nbvh_ctx* c);

@@ -107,11 +107,13 @@ __global__ void __launch_bounds__(128) k_traverse(TraverseArgs a) {
     float* lte = reinterpret_cast<float*>(sm_raw) + threadIdx.x;
     float* ltx = lte + a.cap * S;
     int* lid = sm_raw + 2 * a.cap * S + threadIdx.x;
+    bool more_long = false;
     if (valid) {
         RayDev R = load_ray(a.rays, r);
         bool more = false;
         SmemStack st{sm_raw + 3 * a.cap * S + threadIdx.x, S, a.cut.depth + 2};
         const int n = traverse_smem_list(a.cut, R, a.cap, lte, ltx, lid, S, st, more, &a.ctr->err);
+        more_long = more || n >= 3;
         for (int j = 0; j < n; ++j) {
             a.lst_leaf[(int64_t)j * a.n_rays + r] = lid[j * S];
             a.lst_te[(int64_t)j * a.n_rays + r] = lte[j * S];
@@ -134,13 +136,21 @@ __global__ void __launch_bounds__(128) k_traverse(TraverseArgs a) {
             if (a.out.n_queries) a.out.n_queries[r] = 0;
         }
     }
-    // warp-aggregated append to the work list of the query kernel
-    const unsigned m = __ballot_sync(0xffffffffu, active);
+    // warp-aggregated append to the work lists of the query kernel: rays whose list is long
+    // (or overflows) go to the "long" list, which the query kernel consumes first, so the
+    // kernel's tail is made of short rays (longest-job-first)
+    const bool is_long = active && (more_long);
+    const unsigned ml = __ballot_sync(0xffffffffu, is_long);
+    const unsigned ms = __ballot_sync(0xffffffffu, active && !is_long);
     const int lane = threadIdx.x & 31;
-    int base = 0;
-    if (lane == 0 && m) base = atomicAdd(&a.ctr->cnt, __popc(m));
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (active) a.act_out[base + __popc(m & ((1u << lane) - 1u))] = (int)r;
+    int bl = 0, bs = 0;
+    if (lane == 0 && ml) bl = atomicAdd(&a.ctr->cnt_long, __popc(ml));
+    if (lane == 0 && ms) bs = atomicAdd(&a.ctr->cnt, __popc(ms));
+    bl = __shfl_sync(0xffffffffu, bl, 0);
+    bs = __shfl_sync(0xffffffffu, bs, 0);
+    const unsigned lt = (1u << lane) - 1u;
+    if (is_long) a.act_long[bl + __popc(ml & lt)] = (int)r;
+    else if (active) a.act_out[bs + __popc(ms & lt)] = (int)r;
 }
 
 // Debug traversal: full lists up to `cap` (may exceed K) by repeated resumption.
@@ -277,7 +287,8 @@ __global__ void __launch_bounds__(kQueryWarps * 32, 1) k_query(QueryArgs a) {
     if (lane < kWarpQ) S.ray[lane] = -1;
     __syncthreads();                          // the only block-wide barrier
 
-    const int total = *a.cnt;                 // rays with >= 1 intersected leaf (k_traverse)
+    const int n_long = *a.cnt_long;           // long rays first (k_traverse), then the rest
+    const int total = n_long + *a.cnt;        // rays with >= 1 intersected leaf
     const uint32_t hmask = (1u << a.g.log2_T) - 1u;
     const void* tab = a.g.table;
     const int cpp = (a.g.L * F) / 8;          // 16-byte chunks per sample point
@@ -298,7 +309,7 @@ __global__ void __launch_bounds__(kQueryWarps * 32, 1) k_query(QueryArgs a) {
             exhausted = base + ne >= total;
             const int i = base + __popc(em & lt_mask);
             if (empty && i < total) {
-                const int r = a.act[i];
+                const int r = i < n_long ? a.act_long[i] : a.act[i - n_long];
                 const float4 r0 = __ldg(a.rays + 2 * (int64_t)r), r1 = __ldg(a.rays + 2 * (int64_t)r + 1);
                 S.ray[lane] = r;
                 S.o[0][lane] = r0.x; S.o[1][lane] = r0.y; S.o[2][lane] = r0.z;

@@ -29,7 +29,8 @@ struct QueryCounters {
     int32_t cnt;                  // rays with >= 1 intersected leaf (k_traverse append count)
     int32_t next;                 // work-list cursor of the persistent query kernel
     int32_t max_iter;             // slot iterations of the busiest CTA
-    int32_t pad[3];
+    int32_t cnt_long;             // rays queued on the "long" work list (many leaves: scheduled first)
+    int32_t pad[2];
     unsigned long long n_queries; // neural queries (ray, leaf) evaluated
 };
 
@@ -44,6 +45,7 @@ struct TraverseArgs {
     RayState st;
     HitsDev out;
     int32_t* act_out;
+    int32_t* act_long;       // rays with many intersected leaves (queued first, shorter tail)
     QueryCounters* ctr;
 };
 
@@ -75,6 +77,8 @@ struct QueryArgs {
     HitsDev out;
     const int32_t* act;      // work list: rays with >= 1 leaf (k_traverse)
     const int32_t* cnt;      // its length (device)
+    const int32_t* act_long; // long-ray work list, consumed before `act`
+    const int32_t* cnt_long;
     int32_t* next;           // work-list cursor
     float* z_trace;
     int32_t trace_cap;

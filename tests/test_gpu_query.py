@@ -225,6 +225,20 @@ def test_query_host_path_equals_device_path(tiny):
         assert np.array_equal(d[k].reshape(h[k].shape), h[k]), k
 
 
+def test_query_host_path_chunked_interleaved(tiny):
+    """Multi-chunk host path (n >= 2^18: block-interleaved chunks, strided 2-D copies, a ragged
+    partial block) returns exactly what the device path returns."""
+    ctx, sc, tab, layers = tiny
+    cam = synth.camera_rays(600, 512, (0.0, 0.0, 3.5), vfov_deg=40.0)
+    rays = np.concatenate([cam, synth.random_rays(1237, seed=21)], 0)       # 308,437 rays
+    ctx.reserve(rays.shape[0])
+    d = {k: v.cpu().numpy() for k, v in ctx.query(torch.from_numpy(rays).cuda()).items()}
+    h = ctx.query_host(rays)
+    for k in d:
+        assert np.array_equal(d[k].reshape(h[k].shape), h[k]), k
+    assert d["hit"].sum() > 1000
+
+
 def test_query_1080p_sampled_full_size(orc):
     """cfg 2 at full size in the bench's launch configuration; sampled rays vs oracle."""
     ctx, sc, tab, layers = _mk_ctx("1080p", table_seed=9, seed=6)

@@ -232,7 +232,7 @@ static cudaError_t launch_train_fd(const TrainArgs& a, int64_t n, int64_t w_off,
     const size_t smem_dw = (size_t)kTileQ * 72 * 2 + (size_t)kTileQ * (D + 8) * 2 + kTileQ * 8 * 4;
     cudaFuncSetAttribute(k_train_fwd<F, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fwd);
     cudaFuncSetAttribute(k_train_bwd<F, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bwd);
-    cudaFuncSetAttribute(k_train_dw<D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_dw);
+    cudaFuncSetAttribute(k_train_dw<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_dw);
     const unsigned blocks_n = (unsigned)((n + 127) / 128);
     if (ev) cudaEventRecord(ev[0], s);
     k_train_select<<<blocks_n, 128, (size_t)(a.cut.depth + 2) * 128 * sizeof(int), s>>>(a);
@@ -263,8 +263,9 @@ static cudaError_t launch_train_fd(const TrainArgs& a, int64_t n, int64_t w_off,
         else if (H == 4 && dw_tc_ok(D, 4)) run_tc(k_train_dw_tc<D, 4>, 4);
     }
     if (tc_done) {
-        cudaFuncSetAttribute(k_train_dw<D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_dw);
-        k_train_dw<D, false><<<dw_grid > 0 ? dw_grid : 1, 256, smem_dw, s>>>(a, w_off, b_off);
+        // output-layer weights follow the input and hidden layers in the weight block
+        int64_t w_out = w_off + (int64_t)64 * D + (int64_t)(H - 1) * 64 * 64;
+        k_train_bias_out<<<2 * sms, 256, 0, s>>>(a, w_out, b_off);
         ++*launches;
     } else {
         k_train_dw<D><<<dw_grid > 0 ? dw_grid : 1, 256, smem_dw, s>>>(a, w_off, b_off);

@@ -661,9 +661,8 @@ __global__ void __launch_bounds__(256, 1) k_train_bwd(TrainArgs a) {
 // CUDA cores from the fp32 dL/dz.
 constexpr int kDwChunk = 2048;
 
-// kWeights = false: only the biases and the 8-output layer (the weight GEMMs of the other
-// layers run on tcgen05 in k_train_dw_tc).
-template <int D, bool kWeights = true>
+// The mma.sync fallback used when the tcgen05 contraction does not fit (Mtot > 256).
+template <int D>
 __global__ void __launch_bounds__(256, 1) k_train_dw(TrainArgs a, int64_t w_off, int64_t b_off) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -694,21 +693,16 @@ __global__ void __launch_bounds__(256, 1) k_train_dw(TrainArgs a, int64_t w_off,
                 uint4 v = r + row < c1 ? reinterpret_cast<const uint4*>(Dk + (r + row) * 64)[c] : make_uint4(0, 0, 0, 0);
                 *reinterpret_cast<uint4*>(sd + row * 72 + c * 8) = v;
             }
-            if (kWeights)
-                for (int i = tid; i < kTileQ * (in / 8); i += blockDim.x) {
-                    const int row = i / (in / 8), c = i % (in / 8);
-                    uint4 v = r + row < c1 ? reinterpret_cast<const uint4*>(Xk + (r + row) * in)[c] : make_uint4(0, 0, 0, 0);
-                    *reinterpret_cast<uint4*>(sx + row * (D + 8) + c * 8) = v;
-                }
+            for (int i = tid; i < kTileQ * (in / 8); i += blockDim.x) {
+                const int row = i / (in / 8), c = i % (in / 8);
+                uint4 v = r + row < c1 ? reinterpret_cast<const uint4*>(Xk + (r + row) * in)[c] : make_uint4(0, 0, 0, 0);
+                *reinterpret_cast<uint4*>(sx + row * (D + 8) + c * 8) = v;
+            }
             __syncthreads();
             if (tid < 64) {
                 float sacc = 0.f;
                 for (int row = 0; row < kTileQ; ++row) sacc += __half2float(sd[row * 72 + tid]);
                 dbias += sacc;
-            }
-            if (!kWeights) {
-                __syncthreads();
-                continue;
             }
             const uint32_t aa = (uint32_t)__cvta_generic_to_shared(
                 sd + ((lane & 7) + ((lane >> 4) << 3)) * 72 + mt * 16 + ((lane >> 3) & 1) * 8);
@@ -732,7 +726,7 @@ __global__ void __launch_bounds__(256, 1) k_train_dw(TrainArgs a, int64_t w_off,
         // flush partial sums
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-            if (kWeights && j < NT / 2) {
+            if (j < NT / 2) {
                 const int col = (nt0 + j) * 8 + 2 * t;
                 const int u0 = mt * 16 + g, u1 = u0 + 8;
                 red_add_v2(a.grad + woff + (int64_t)u0 * in + col, acc[j][0], acc[j][1]);
@@ -771,6 +765,73 @@ __global__ void __launch_bounds__(256, 1) k_train_dw(TrainArgs a, int64_t w_off,
         red_add_v2(a.grad + woff + (int64_t)o * 64 + i0, accw[0], accw[1]);
         if (i0 == 0) atomicAdd(a.grad + boff + o, accb);
     }
+}
+
+// ------------------------------------------------------------------ T6 biases + output layer
+// Companion of k_train_dw_tc: every bias gradient (column sums of the deltas, and of dL/dz
+// for the output layer) and the 8-output layer's weight gradient dW_out = dZ^T h_{H-1}, in
+// fp32 on CUDA cores.  Memory-bound streaming pass over the samples: each thread owns a
+// 16-byte column group (8 deltas of one row) or an (output, 8-input) pair; per-CTA partial
+// sums meet in shared memory and are flushed with one atomic per parameter per CTA.
+__global__ void __launch_bounds__(256) k_train_bias_out(TrainArgs a, int64_t w_out_off, int64_t b_off) {
+    __shared__ float sb[4 * 64 + 8];             // hidden biases (H <= 4) + output biases
+    __shared__ float sw[8 * 64];                 // output-layer weights [o][i]
+    const int tid = threadIdx.x;
+    const int H = a.m.hidden;
+    for (int i = tid; i < 4 * 64 + 8; i += blockDim.x) sb[i] = 0.f;
+    for (int i = tid; i < 8 * 64; i += blockDim.x) sw[i] = 0.f;
+    __syncthreads();
+    const int M = *a.n_samples;
+    // (1) hidden-layer biases: thread -> (row slot, layer, 8-column group)
+    {
+        const int groups = H * 8;                       // 8 groups of 8 columns per layer
+        const int rows_per_pass = blockDim.x / groups;
+        const int slot = tid / groups, g = tid - slot * groups;
+        const int layer = g >> 3, c0 = (g & 7) * 8;
+        float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        if (slot < rows_per_pass) {
+            const __half* Dk = a.Dl + (int64_t)layer * a.cap * 64 + c0;
+            for (int64_t r = (int64_t)blockIdx.x * rows_per_pass + slot; r < M; r += (int64_t)gridDim.x * rows_per_pass) {
+                const uint4 v = *reinterpret_cast<const uint4*>(Dk + r * 64);
+                const __half2* h = reinterpret_cast<const __half2*>(&v);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const float2 f = __half22float2(h[j]);
+                    acc[2 * j] += f.x;
+                    acc[2 * j + 1] += f.y;
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) atomicAdd(sb + layer * 64 + c0 + j, acc[j]);
+        }
+    }
+    // (2) output layer: thread -> (row slot, output o, 8-input group)
+    {
+        const int rows_per_pass = blockDim.x / 64;      // 64 (o, group) tasks per row
+        const int slot = tid >> 6, task = tid & 63;
+        const int o = task >> 3, i0 = (task & 7) * 8;
+        float accw[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, accb = 0.f;
+        const __half* Ah = a.A + (int64_t)(H - 1) * a.cap * 64 + i0;
+        for (int64_t r = (int64_t)blockIdx.x * rows_per_pass + slot; r < M; r += (int64_t)gridDim.x * rows_per_pass) {
+            const float dz = a.dZ[r * 8 + o];
+            const uint4 v = *reinterpret_cast<const uint4*>(Ah + r * 64);
+            const __half2* h = reinterpret_cast<const __half2*>(&v);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const float2 f = __half22float2(h[j]);
+                accw[2 * j] = fmaf(dz, f.x, accw[2 * j]);
+                accw[2 * j + 1] = fmaf(dz, f.y, accw[2 * j + 1]);
+            }
+            accb += dz;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) atomicAdd(sw + o * 64 + i0 + j, accw[j]);
+        if (i0 == 0) atomicAdd(sb + 4 * 64 + o, accb);
+    }
+    __syncthreads();
+    for (int i = tid; i < H * 64; i += blockDim.x) atomicAdd(a.grad + b_off + i, sb[i]);
+    for (int i = tid; i < 8; i += blockDim.x) atomicAdd(a.grad + b_off + H * 64 + i, sb[4 * 64 + i]);
+    for (int i = tid; i < 8 * 64; i += blockDim.x) atomicAdd(a.grad + w_out_off + i, sw[i]);
 }
 
 // ------------------------------------------------------------------ T6 weight gradients on tcgen05

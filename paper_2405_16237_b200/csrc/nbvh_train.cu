@@ -444,11 +444,13 @@ extern "C" nbvh_status nbvh_apply_update(nbvh_ctx* c, float lr, void* stream) {
     a.eps = 1e-8f;
     a.c1 = (float)(1.0 - std::pow(0.9, (double)w->step));
     a.c2 = (float)(1.0 - std::pow(0.999, (double)w->step));
+    a.ic1 = (float)(1.0 / (1.0 - std::pow(0.9, (double)w->step)));
+    a.ic2 = (float)(1.0 / (1.0 - std::pow(0.999, (double)w->step)));
     a.table16 = c->d_table16;
     a.n_table = c->n_table;
     a.W16 = c->d_W16;
     a.n_W = c->n_W;
-    k_adam<<<1184, 256, 0, s>>>(a);
+    k_adam<<<4 * 148, 256, 0, s>>>(a);
     st = refresh_table(c, s);
     if (st) return st;
     if (c->profiling) cudaEventRecord(ctx_event(c, 23), s);

@@ -980,7 +980,7 @@ struct AdamArgs {
     int64_t n;
     const float* count;   // accepted-sample count (after the all-reduce)
     const int32_t* bad;
-    float lr, beta1, beta2, eps, c1, c2;
+    float lr, beta1, beta2, eps, c1, c2, ic1, ic2;   // ic = 1/c (bias corrections)
     __half* table16;
     int64_t n_table;
     __half* W16;
@@ -990,18 +990,50 @@ struct AdamArgs {
 // P:275 Adam with default hyper-parameters (C20): dense, bias-corrected; the gradient is
 // the batch mean (sum / accepted count).  The fp16 MLP weights are refreshed in place; the
 // fp16 inference table is rebuilt afterwards by k_refresh_table (corner-packed layout).
+__device__ __forceinline__ float adam_one(const AdamArgs& a, float g, float& m, float& v, float p, float scale) {
+    const float gr = g * scale;
+    m = a.beta1 * m + (1.0f - a.beta1) * gr;
+    v = a.beta2 * v + (1.0f - a.beta2) * gr * gr;
+    return p - a.lr * (m * a.ic1) / (sqrtf(v * a.ic2) + a.eps);
+}
+
+// Vectorised (float4) over the flat parameter buffer; the fp16 MLP-weight copy is written for
+// the elements inside the weight block.
 __global__ void k_adam(AdamArgs a) {
     if (*a.bad) return;
     const float scale = 1.0f / fmaxf(1.0f, *a.count);
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * blockDim.x) {
-        const float gr = a.grad[i] * scale;
-        const float m = a.beta1 * a.m[i] + (1.0f - a.beta1) * gr;
-        const float v = a.beta2 * a.v[i] + (1.0f - a.beta2) * gr * gr;
+    const int64_t n4 = a.n / 4;
+    const int64_t w0 = a.n_table, w1 = a.n_table + a.n_W;
+    float4* P = reinterpret_cast<float4*>(a.param);
+    const float4* G = reinterpret_cast<const float4*>(a.grad);
+    float4* Mv = reinterpret_cast<float4*>(a.m);
+    float4* Vv = reinterpret_cast<float4*>(a.v);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n4; q += stride) {
+        const float4 g = G[q];
+        float4 m = Mv[q], v = Vv[q], p = P[q];
+        p.x = adam_one(a, g.x, m.x, v.x, p.x, scale);
+        p.y = adam_one(a, g.y, m.y, v.y, p.y, scale);
+        p.z = adam_one(a, g.z, m.z, v.z, p.z, scale);
+        p.w = adam_one(a, g.w, m.w, v.w, p.w, scale);
+        Mv[q] = m;
+        Vv[q] = v;
+        P[q] = p;
+        const int64_t i = 4 * q;
+        if (i + 3 >= w0 && i < w1) {
+            const float pv[4] = {p.x, p.y, p.z, p.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (i + k >= w0 && i + k < w1) a.W16[i + k - w0] = __float2half_rn(pv[k]);
+        }
+    }
+    for (int64_t i = 4 * n4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += stride) {
+        float m = a.m[i], v = a.v[i];
+        const float p = adam_one(a, a.grad[i], m, v, a.param[i], scale);
         a.m[i] = m;
         a.v[i] = v;
-        const float p = a.param[i] - a.lr * (m / a.c1) / (sqrtf(v / a.c2) + a.eps);
         a.param[i] = p;
-        if (i >= a.n_table && i < a.n_table + a.n_W) a.W16[i - a.n_table] = __float2half_rn(p);
+        if (i >= w0 && i < w1) a.W16[i - w0] = __float2half_rn(p);
     }
 }
 

@@ -185,6 +185,28 @@ nbvh_status nbvh_get_query_stats(nbvh_ctx* ctx, nbvh_query_stats* out);
  * stream) and report their durations in nbvh_query_stats. */
 nbvh_status nbvh_set_profiling(nbvh_ctx* ctx, int32_t on);
 
+/* ---------------------------------------------------------------- hybrid path tracing (device) */
+/* NEXT-3 (BASELINE cfg 3; PAPER §7: "a BLAS is classical or N-BVH; both
+ * query types yield the same type of intersection data").
+ * Classical closest-hit query of n rays (device nbvh_ray[n], interval [tmin, tmax]) against
+ * the context's own triangle mesh through its SAH base BVH, with double-precision
+ * Moller-Trumbore (ties: lowest triangle id, C32).  Writes the nbvh_query hit record (normal:
+ * interpolated vertex normal; albedo: the triangle's; leaf: the triangle id or -1;
+ * n_queries: 0).  Requires nbvh_set_mesh; NBVH_EINVAL if the base BVH is deeper than 63
+ * levels.  Asynchronous on `stream`. */
+nbvh_status nbvh_intersect_mesh(nbvh_ctx* ctx, const nbvh_ray* d_rays, int64_t n, nbvh_hits d_out, void* stream);
+/* One wavefront step of the hybrid path tracer: for every ray with tmin <= tmax, take the
+ * closer of the neural record d_neural and the classical record d_classical (d_classical.hit
+ * may be NULL: no classical BLAS); an escaped ray adds throughput * sky(direction) to
+ * d_radiance [n][3] (sky = host float[6]: horizon rgb, zenith rgb, blended by elevation) and
+ * ends; a hit multiplies d_throughput [n][3] by the albedo (diffuse BSDF) and continues from
+ * p + eps * n along a cosine-weighted direction drawn from a counter-based hash of
+ * (seed, ray index, bounce).  d_next [n] receives the next rays (ended rays: tmin 1 > tmax 0);
+ * *d_alive (device int32) is incremented by the number of continuing rays.  Asynchronous. */
+nbvh_status nbvh_pt_shade(nbvh_ctx* ctx, const nbvh_ray* d_rays, int64_t n, nbvh_hits d_neural, nbvh_hits d_classical,
+                          float* d_throughput, float* d_radiance, nbvh_ray* d_next, uint64_t seed, int32_t bounce,
+                          const float* sky, float eps, int32_t* d_alive, void* stream);
+
 /* ---------------------------------------------------------------- training (device) */
 /* Forward + backward of one training batch into the context's
  * fp32 gradient buffer (overwritten): for each ray the first intersected cut leaf of

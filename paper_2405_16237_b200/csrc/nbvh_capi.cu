@@ -396,6 +396,7 @@ extern "C" nbvh_status nbvh_reserve(nbvh_ctx* c, int64_t max_rays) {
 // ------------------------------------------------------------------ scene + cut
 extern "C" nbvh_status nbvh_set_mesh(nbvh_ctx* c, const float* xyz, int64_t nv, const uint32_t* tri, int64_t nt,
                                      const float* vnormal, const float* tri_albedo) {
+    if (c) c->base_depth = -1;
     if (!c) return NBVH_EINVAL;
     if (c->poisoned) return NBVH_ECUDA;
     if (!xyz || !tri || nv < 3 || nt < 1 || nt > (int64_t)1 << 30) return fail(c, NBVH_EINVAL, "set_mesh: bad mesh");

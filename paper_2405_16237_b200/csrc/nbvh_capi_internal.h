@@ -59,6 +59,7 @@ struct nbvh_ctx {
     // scene and cuts
     nbvh::HostScene sc;
     bool has_mesh = false;
+    int32_t base_depth = -1;           // base-BVH depth (computed on first classical query)
     nbvh::HostCut cuts[nbvh::kMaxLod];
     bool has_cut[nbvh::kMaxLod] = {false};
     nbvh::DeviceCut dcut[nbvh::kMaxLod];

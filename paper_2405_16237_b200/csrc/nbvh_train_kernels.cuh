@@ -14,6 +14,7 @@
 #include "nbvh_device.cuh"
 #include "nbvh_internal.h"
 #include "nbvh_tcgen05.cuh"
+#include "nbvh_bvh.cuh"
 
 namespace nbvh {
 
@@ -106,121 +107,31 @@ __global__ void __launch_bounds__(128) k_train_select(TrainArgs a) {
 }
 
 // ------------------------------------------------------------------ T2 label
-// Moller-Trumbore in double with the oracle's operation order (no FMA), so the hit
-// decisions and t are bit-identical to the double-precision ground truth.
-__device__ __forceinline__ double dot3(const double* a, const double* b) {
-    return __dadd_rn(__dadd_rn(__dmul_rn(a[0], b[0]), __dmul_rn(a[1], b[1])), __dmul_rn(a[2], b[2]));
-}
-__device__ __forceinline__ void cross3(const double* a, const double* b, double* c) {
-    c[0] = __dsub_rn(__dmul_rn(a[1], b[2]), __dmul_rn(a[2], b[1]));
-    c[1] = __dsub_rn(__dmul_rn(a[2], b[0]), __dmul_rn(a[0], b[2]));
-    c[2] = __dsub_rn(__dmul_rn(a[0], b[1]), __dmul_rn(a[1], b[0]));
-}
-
-__device__ __forceinline__ bool tri_hit(const double* o, const double* d, const float* tv, double t0, double t1,
-                                        double& t, double& b1, double& b2) {
-    double v0[3], e1[3], e2[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        v0[k] = tv[k];
-        e1[k] = __dsub_rn((double)tv[3 + k], v0[k]);
-        e2[k] = __dsub_rn((double)tv[6 + k], v0[k]);
-    }
-    double p[3];
-    cross3(d, e2, p);
-    const double det = dot3(e1, p);
-    if (fabs(det) < 1e-20) return false;
-    const double inv = __ddiv_rn(1.0, det);
-    double s[3] = {__dsub_rn(o[0], v0[0]), __dsub_rn(o[1], v0[1]), __dsub_rn(o[2], v0[2])};
-    const double uu = __dmul_rn(dot3(s, p), inv);
-    if (uu < 0.0 || uu > 1.0) return false;
-    double q[3];
-    cross3(s, e1, q);
-    const double vv = __dmul_rn(dot3(d, q), inv);
-    if (vv < 0.0 || __dadd_rn(uu, vv) > 1.0) return false;
-    const double tt = __dmul_rn(dot3(e2, q), inv);
-    if (tt < t0 || tt > t1) return false;
-    t = tt;
-    b1 = uu;
-    b2 = vv;
-    return true;
-}
-
+// Ground truth by intersecting the first leaf's own triangles (C17): closest
+// hit below the leaf's base-BVH node within the leaf segment [t0, t1] (bvh_closest, double
+// Moller-Trumbore with the oracle's operation order).
 __global__ void __launch_bounds__(128) k_train_label(TrainArgs a) {
     const int M = *a.n_samples;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= M) return;
     const int r = a.s_ray[i];
     RayDev R = load_ray(a.rays, r);
-    const double o[3] = {R.o[0], R.o[1], R.o[2]}, d[3] = {R.d[0], R.d[1], R.d[2]};
     const float t0 = a.s_t0[i], t1 = a.s_t1[i];
-    // conservative box test: boxes grown by a relative epsilon so that no triangle the
-    // exact test would accept is pruned.  Stack: shared-memory column [64][128].
-    extern __shared__ int stk_raw[];
-    int* stack_col = stk_raw + threadIdx.x;
-    int sp = 0;
-#define STACK(i) stack_col[(i) * 128]
-    STACK(sp++) = a.leaf_base[a.s_leaf[i]];
-    bool found = false;
-    double bt = 0, bb1 = 0, bb2 = 0;
-    int btri = -1, bslot = -1;
-    float t_cut = t1 * 1.00001f + 1e-6f;        // conservative upper bound: segment end, then best hit
-    while (sp > 0) {
-        const BvhNode nd = a.nodes[STACK(--sp)];
-        float lo[3], hi[3], te, tx;
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            const float e = 1e-5f * (fabsf(nd.lo[k]) + fabsf(nd.hi[k]) + 1e-3f);
-            lo[k] = nd.lo[k] - e;
-            hi[k] = nd.hi[k] + e;
-        }
-        if (!slab(R, lo, hi, te, tx)) continue;
-        // a node entering beyond the best hit so far holds no closer (or tying) hit: the
-        // conservative boxes and the relative slack keep this exact w.r.t. the double test
-        if (te > t_cut || tx < t0 * 0.99999f - 1e-6f) continue;
-        if (nd.b < 0) {
-            for (int j = nd.a; j < nd.a - nd.b; ++j) {
-                double th, b1, b2;
-                if (tri_hit(o, d, a.tri_v + 9 * (int64_t)j, (double)t0, (double)t1, th, b1, b2)) {
-                    const int id = a.tri_id[j];
-                    if (!found || th < bt || (th == bt && id < btri)) {
-                        found = true; bt = th; bb1 = b1; bb2 = b2; btri = id; bslot = j;
-                        t_cut = fminf(t_cut, (float)bt * 1.00001f + 1e-6f);
-                    }
-                }
-            }
-        } else if (sp + 2 <= 64) {
-            // visit the nearer child first (by its box centre along the ray) so the best hit
-            // tightens t_cut early
-            const BvhNode& ca = a.nodes[nd.a];
-            const BvhNode& cb = a.nodes[nd.b];
-            float da = 0.f, db = 0.f;
-#pragma unroll
-            for (int k = 0; k < 3; ++k) {
-                da = fmaf(ca.lo[k] + ca.hi[k], R.d[k], da);
-                db = fmaf(cb.lo[k] + cb.hi[k], R.d[k], db);
-            }
-            const bool a_first = da <= db;
-            STACK(sp++) = a_first ? nd.b : nd.a;
-            STACK(sp++) = a_first ? nd.a : nd.b;
-        }
-    }
-#undef STACK
+    extern __shared__ int stk_raw[];                     // stack column [kBvhStack][128]
+    const BvhHit h = bvh_closest(a.nodes, a.tri_v, a.tri_id, a.leaf_base[a.s_leaf[i]], R, t0, t1,
+                                 stk_raw + threadIdx.x, 128);
     float gt[9];
 #pragma unroll
     for (int k = 0; k < 9; ++k) gt[k] = 0.f;
-    gt[0] = found ? 0.f : 1.f;
-    if (found) {
+    gt[0] = h.found ? 0.f : 1.f;
+    if (h.found) {
         const double dt = (double)t1 - (double)t0;
-        gt[1] = dt > 0.0 ? (float)((bt - (double)t0) / dt) : 0.f;
-        const float* tn = a.tri_n + 9 * (int64_t)bslot;
-        double n[3];
-        for (int k = 0; k < 3; ++k)
-            n[k] = (1.0 - bb1 - bb2) * (double)tn[k] + bb1 * (double)tn[3 + k] + bb2 * (double)tn[6 + k];
-        const double nn = sqrt(n[0] * n[0] + n[1] * n[1] + n[2] * n[2]);
-        for (int k = 0; k < 3; ++k) gt[2 + k] = nn > 0 ? (float)(n[k] / nn) : 0.f;
-        for (int k = 0; k < 3; ++k) gt[5 + k] = a.tri_a[3 * (int64_t)bslot + k];
-        gt[8] = (float)bt;
+        gt[1] = dt > 0.0 ? (float)((h.t - (double)t0) / dt) : 0.f;
+        float n[3];
+        shading_normal(a.tri_n, h, n);
+        for (int k = 0; k < 3; ++k) gt[2 + k] = n[k];
+        for (int k = 0; k < 3; ++k) gt[5 + k] = a.tri_a[3 * (int64_t)h.slot + k];
+        gt[8] = (float)h.t;
     }
 #pragma unroll
     for (int k = 0; k < 9; ++k) {

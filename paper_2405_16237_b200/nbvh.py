@@ -79,6 +79,8 @@ SIGNATURES = {
     "nbvh_train_step": (C.c_int, [_P, _P, _I64, _P, _P, _I32, _F, _P]),
     "nbvh_get_train_stats": (C.c_int, [_P, _P]),
     "nbvh_set_leaf_rank": (C.c_int, [_P, _I32, _P]),
+    "nbvh_intersect_mesh": (C.c_int, [_P, _P, _I64, Hits, _P]),
+    "nbvh_pt_shade": (C.c_int, [_P, _P, _I64, Hits, Hits, _P, _P, _P, C.c_uint64, _I32, _P, _F, _P, _P]),
     "nbvh_debug_traverse": (C.c_int, [_P, _P, _I64, _I32, _I32, _P, _P, _P, _P, _P]),
     "nbvh_debug_encode": (C.c_int, [_P, _P, _I64, _P, _P, _P]),
     "nbvh_debug_mlp": (C.c_int, [_P, _P, _I64, _P, _P]),
@@ -253,6 +255,24 @@ class Context:
             out = self.alloc_hits(n, rays.device)
         self._ck(self.lib.nbvh_query(self.h, _ptr(rays), n, lod, self._hits(out), _stream_ptr(stream)), "query")
         return out
+
+    def intersect_mesh(self, rays, out=None, stream=None):
+        """Classical closest hit against this context's own mesh (the classical BLAS)."""
+        n = rays.shape[0]
+        if out is None:
+            out = self.alloc_hits(n, rays.device)
+        self._ck(self.lib.nbvh_intersect_mesh(self.h, _ptr(rays), n, self._hits(out), _stream_ptr(stream)),
+                 "intersect_mesh")
+        return out
+
+    def pt_shade(self, rays, neural, classical, throughput, radiance, next_rays, seed, bounce, sky, eps, alive,
+                 stream=None):
+        sky_a = np.ascontiguousarray(sky, np.float32)
+        empty = Hits(None, None, None, None, None, None)
+        self._ck(self.lib.nbvh_pt_shade(self.h, _ptr(rays), rays.shape[0], self._hits(neural),
+                                        self._hits(classical) if classical is not None else empty,
+                                        _ptr(throughput), _ptr(radiance), _ptr(next_rays), int(seed), int(bounce),
+                                        _ptr(sky_a), float(eps), _ptr(alive), _stream_ptr(stream)), "pt_shade")
 
     def query_host(self, rays_np, out=None, lod=0, stream=None):
         """End-to-end path: host (ideally pinned) numpy rays -> host numpy results."""

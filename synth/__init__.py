@@ -6,6 +6,6 @@ parameter values and random draws that the method consumes as inputs
 (DESIGN.md "Input recipe").
 """
 from .scenes import (  # noqa: F401
-    Scene, icosphere, scene_tiny, scene_1080p, camera_rays, random_rays,
+    Scene, icosphere, scene_tiny, scene_1080p, scene_1080p_parts, camera_rays, random_rays,
     random_params_fp16, random_mlp, random_uniform, CONFIGS, HashCfg,
 )

@@ -179,6 +179,18 @@ def _fbm_fn(rng: np.random.Generator, octaves: int = 5, amp: float = 0.15):
     return h
 
 
+def scene_1080p_parts(seed: int = 4, grid: int = 512, nu: int = 22) -> tuple[Scene, Scene]:
+    """cfg 3 (hybrid scene): the cfg-2 scene split into its two instances -- the heightfield
+    (classical BLAS) and the 48 icospheres (neural BLAS) -- same geometry and albedo."""
+    full = scene_1080p(seed, grid, nu)
+    nt = 2 * grid * grid
+    nv = (grid + 1) * (grid + 1)
+    terrain = Scene(full.verts[:nv], full.tris[:nt], full.vnormals[:nv], full.albedo[:nt])
+    spheres = Scene(full.verts[nv:], (full.tris[nt:] - nv).astype(full.tris.dtype), full.vnormals[nv:],
+                    full.albedo[nt:])
+    return terrain, spheres
+
+
 def scene_1080p(seed: int = 4, grid: int = 512, nu: int = 22) -> Scene:
     """cfg 2: fBm heightfield (grid^2*2 tris) + 48 displaced icospheres -> 988,928 tris."""
     rng = np.random.default_rng(seed)

@@ -277,6 +277,7 @@ def run_ours(args):
 
     train = bench_train(ctx, args, world, rank) if args.train else None
     lod = bench_lod(args, local) if (args.lod and rank == 0) else None
+    pt = bench_pathtrace(args, local) if (args.pt and rank == 0) else None
 
     line = None
     if rank == 0:
@@ -308,7 +309,7 @@ def run_ours(args):
                          "traverse_ms_per_step": statistics.mean(trav_ms),
                          "mlp_tflops": mean_q * mlp_flops / wave_s / 1e12,
                          "mlp_frac_of_bf16_peak": mean_q * mlp_flops / wave_s / 1e12 / tflops},
-            "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks.summary(), "train": train, "lod": lod,
+            "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks.summary(), "train": train, "lod": lod, "pathtrace": pt,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -429,6 +430,58 @@ def bench_lod(args, device):
             "lod_speedup_far": res["far"]["Mrays_per_s"] / res["far@fine"]["Mrays_per_s"]}
 
 
+def bench_pathtrace(args, device):
+    """BASELINE cfg 3: hybrid path tracing at 1080p, 4 bounces, 1 sample per pixel.  The cfg-2
+    scene split into a classical BLAS (heightfield, 524,288 triangles, base-BVH traversal) and a
+    neural BLAS (48 icospheres, 464,640 triangles, error-driven 1,024-leaf N-BVH trained for a
+    short schedule); diffuse surfaces under a sky gradient (PAPER §7)."""
+    import torch
+    from paper_2405_16237_b200 import Context
+    from paper_2405_16237_b200.construct import construct, Schedule
+    from paper_2405_16237_b200.pathtrace import PathTracer
+    c = synth.CONFIGS["1080p"]
+    h = c["hash"]
+    terrain, spheres = synth.scene_1080p_parts(c["seeds"]["mesh"])
+    neural = Context(device=device, L=h.L, F=h.F, log2_T=h.log2_T, n_points=h.n_points,
+                     hidden_layers=h.hidden_layers, list_cap=args.list_cap, seed=21)
+    neural.set_mesh(spheres)
+    classical = Context(device=device, L=8, F=2, log2_T=14, n_points=4, hidden_layers=1)
+    classical.set_mesh(terrain)
+    n_train = 1 << 16
+    n_px = c["res"][0] * c["res"][1]
+    neural.build_cut(1)
+    neural.reserve(max(n_train, n_px))
+    batches = []
+    for b in range(8):
+        r = synth.random_rays(n_train, seed=9500 + b)
+        u = synth.random_uniform(n_train, seed=9600 + b)
+        xi = synth.random_uniform(n_train * h.n_points, seed=9700 + b).reshape(n_train, h.n_points)
+        batches.append(tuple(torch.from_numpy(np.ascontiguousarray(x)).cuda() for x in (r, u, xi)))
+    t0 = time.perf_counter()
+    construct(neural, 1024, lambda s: batches[s % 8], Schedule(iters0=2, splits0=8, growth=2.0, final_iters=300))
+    build_s = time.perf_counter() - t0
+    rays = torch.from_numpy(synth.camera_rays(*c["res"], c["eye"], vfov_deg=c["vfov"])).cuda()
+    pt = PathTracer(neural, classical, n_px)
+    for i in range(3):
+        pt.render(rays, bounces=4, seed=i)
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    alive_sum = 0
+    e0.record(stream)
+    for i in range(args.steps):
+        _, alive = pt.render(rays, bounces=4, seed=100 + i)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    al = alive.cpu().numpy().tolist()
+    rays_traced = n_px + sum(al[:3])                     # rays entering bounces 0..3
+    return {"metric": "hybrid path tracing (BASELINE cfg 3)", "unit": "Mrays/s",
+            "value": rays_traced / ms / 1e3, "ms_per_frame": ms, "resolution": list(c["res"]), "spp": 1,
+            "bounces": 4, "rays_per_frame": rays_traced, "alive_after_bounce": al,
+            "neural_blas": {"tris": spheres.n_tris, "leaves": neural.cut(0)["n_leaves"], "train_s": build_s},
+            "classical_blas": {"tris": terrain.n_tris}}
+
+
 def run_reference(args):
     """The CPU oracle timed as it stands on bounded samples of the same workload."""
     rank = int(os.environ.get("RANK", "0"))
@@ -487,6 +540,7 @@ def main():
     ap.add_argument("--list-cap", type=int, default=12, help="per-ray ordered leaf-list capacity K (C6)")
     ap.add_argument("--train", type=int, default=1, help="also time the cfg-5 training step (1/0)")
     ap.add_argument("--lod", type=int, default=1, help="also run the cfg-4 multi-cut LoD query (1/0)")
+    ap.add_argument("--pt", type=int, default=1, help="also run the cfg-3 hybrid path tracer (1/0)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -275,6 +275,7 @@ def run_ours(args):
         e2e = {"value": n * args.steps * world / float(e2e_t.item()) / 1e6, "unit": "Mrays/s",
                "h2d_bytes_per_step": n * 32, "d2h_bytes_per_step": d2h}
 
+    mlp = bench_mlp(ctx, args)
     train = bench_train(ctx, args, world, rank) if args.train else None
     lod = bench_lod(args, local) if (args.lod and rank == 0) else None
     pt = bench_pathtrace(args, local) if (args.pt and rank == 0) else None
@@ -309,7 +310,7 @@ def run_ours(args):
                          "traverse_ms_per_step": statistics.mean(trav_ms),
                          "mlp_tflops": mean_q * mlp_flops / wave_s / 1e12,
                          "mlp_frac_of_bf16_peak": mean_q * mlp_flops / wave_s / 1e12 / tflops},
-            "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks.summary(), "train": train, "lod": lod, "pathtrace": pt,
+            "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks.summary(), "mlp": mlp, "train": train, "lod": lod, "pathtrace": pt,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -480,6 +481,36 @@ def bench_pathtrace(args, device):
             "bounces": 4, "rays_per_frame": rays_traced, "alive_after_bounce": al,
             "neural_blas": {"tris": spheres.n_tris, "leaves": neural.cut(0)["n_leaves"], "train_s": build_s},
             "classical_blas": {"tris": terrain.n_tris}}
+
+
+def bench_mlp(ctx, args):
+    """The decoder MLP alone on tcgen05 (nbvh_mlp_forward): one frame's worth of queries
+    (2,377,813 rows of D_in = 128 fp16 features -> 8 outputs) streamed from HBM; tensor-pipe
+    throughput against the measured dense bf16 peak (fp16 runs at the same rate)."""
+    import torch
+    m = 2377813
+    g = torch.Generator(device="cuda").manual_seed(17)
+    x = (torch.rand(m, ctx.d_in, device="cuda", generator=g) * 0.8 - 0.4).half()
+    z = torch.empty(m, 8, device="cuda")
+    for _ in range(3):
+        ctx.mlp_forward(x, z)
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        ctx.mlp_forward(x, z)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    h = ctx.cfg.hidden_layers
+    flop_mma = 2 * 128 * (ctx.d_in * 64 + (h - 1) * 64 * 64 + 64 * 16) * ((m + 127) // 128)   # issued MMA work
+    flop_alg = 2 * m * (ctx.d_in * 64 + (h - 1) * 64 * 64 + 64 * 8)                             # 8 real outputs
+    hbm, tflops, src = _peaks()
+    bytes_io = m * (ctx.d_in * 2 + 32)
+    return {"kernel": "k_mlp_tc (tcgen05 + TMEM + TMA)", "rows": m, "ms": ms,
+            "tflops_algorithmic": flop_alg / ms / 1e9, "tflops_issued": flop_mma / ms / 1e9,
+            "frac_of_bf16_peak": flop_mma / ms / 1e9 / tflops, "peak_tflops": tflops, "peak_source": src,
+            "io_GBps": bytes_io / ms / 1e6, "io_frac_of_hbm": bytes_io / ms / 1e6 / hbm}
 
 
 def run_reference(args):

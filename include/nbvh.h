@@ -185,6 +185,14 @@ nbvh_status nbvh_get_query_stats(nbvh_ctx* ctx, nbvh_query_stats* out);
  * stream) and report their durations in nbvh_query_stats. */
 nbvh_status nbvh_set_profiling(nbvh_ctx* ctx, int32_t on);
 
+/* ---------------------------------------------------------------- MLP on tcgen05 (device) */
+/* The decoder MLP alone (D_in -> 64 ReLU x hidden -> 8, linear outputs) on a batch
+ * of m fp16 feature rows d_x [m][D_in] (bits as uint16, 16-byte aligned) -> raw outputs d_z
+ * [m][8] fp32 (16-byte aligned), with the context's fp16 weights and fp32 biases.  tcgen05
+ * tensor cores (M = 128-row tiles, fp32 accumulators in TMEM, X tiles loaded by TMA); the same
+ * network the fused query kernel evaluates with mma.sync.  Asynchronous on `stream`. */
+nbvh_status nbvh_mlp_forward(nbvh_ctx* ctx, const uint16_t* d_x, int64_t m, float* d_z, void* stream);
+
 /* ---------------------------------------------------------------- hybrid path tracing (device) */
 /* NEXT-3 (BASELINE cfg 3; PAPER §7: "a BLAS is classical or N-BVH; both
  * query types yield the same type of intersection data").

@@ -79,6 +79,7 @@ SIGNATURES = {
     "nbvh_train_step": (C.c_int, [_P, _P, _I64, _P, _P, _I32, _F, _P]),
     "nbvh_get_train_stats": (C.c_int, [_P, _P]),
     "nbvh_set_leaf_rank": (C.c_int, [_P, _I32, _P]),
+    "nbvh_mlp_forward": (C.c_int, [_P, _P, _I64, _P, _P]),
     "nbvh_intersect_mesh": (C.c_int, [_P, _P, _I64, Hits, _P]),
     "nbvh_pt_shade": (C.c_int, [_P, _P, _I64, Hits, Hits, _P, _P, _P, C.c_uint64, _I32, _P, _F, _P, _P]),
     "nbvh_debug_traverse": (C.c_int, [_P, _P, _I64, _I32, _I32, _P, _P, _P, _P, _P]),
@@ -255,6 +256,15 @@ class Context:
             out = self.alloc_hits(n, rays.device)
         self._ck(self.lib.nbvh_query(self.h, _ptr(rays), n, lod, self._hits(out), _stream_ptr(stream)), "query")
         return out
+
+    def mlp_forward(self, x, z=None, stream=None):
+        """tcgen05 batched MLP: x cuda fp16 [m, D_in] -> z cuda fp32 [m, 8]."""
+        import torch
+        m = x.shape[0]
+        if z is None:
+            z = torch.empty(m, 8, dtype=torch.float32, device=x.device)
+        self._ck(self.lib.nbvh_mlp_forward(self.h, _ptr(x), m, _ptr(z), _stream_ptr(stream)), "mlp_forward")
+        return z
 
     def intersect_mesh(self, rays, out=None, stream=None):
         """Classical closest hit against this context's own mesh (the classical BLAS)."""

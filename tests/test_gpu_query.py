@@ -101,6 +101,24 @@ def test_mlp_tensor_core_vs_oracle(orc, d_in, hidden):
     assert np.all(agree | band)
 
 
+@pytest.mark.parametrize("d_in,hidden", [(64, 2), (128, 3), (96, 4), (32, 1), (128, 1)])
+def test_mlp_tcgen05_vs_oracle(orc, d_in, hidden):
+    """The tcgen05/TMEM/TMA batched MLP (nbvh_mlp_forward) vs the double-precision oracle, on a
+    ragged batch (the last 128-row tile is partly out of range: TMA zero-fills it)."""
+    from paper_2405_16237_b200 import Context
+    L, F, npts = {64: (8, 2, 4), 128: (16, 2, 4), 96: (8, 4, 3), 32: (4, 2, 4)}[d_in]
+    ctx = Context(device=0, L=L, F=F, n_points=npts, hidden_layers=hidden)
+    layers = synth.random_mlp(d_in, hidden, 64, seed=6)
+    ctx.set_mlp(layers)
+    m = 3 * 1024 + 77
+    x = (np.random.default_rng(3).random((m, d_in)) * 0.8 - 0.4).astype(np.float16)
+    z = ctx.mlp_forward(torch.from_numpy(x).cuda()).cpu().numpy()
+    want = orc.mlp_forward(layers, x.astype(np.float64))
+    assert np.all(np.abs(z - want) <= 2e-2 * (1 + np.abs(want))), np.abs(z - want).max()
+    zs = ctx.debug_mlp(torch.from_numpy(x).cuda()).cpu().numpy()            # the mma.sync path
+    assert np.all(np.abs(z - zs) <= 2e-2 * (1 + np.abs(zs)))
+
+
 # ------------------------------------------------------------------ traversal
 def _rays_tiny(n_random=3000):
     cam = synth.camera_rays(64, 64, (0.0, 0.0, 3.5), vfov_deg=40.0)

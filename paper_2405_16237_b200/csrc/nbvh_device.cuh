@@ -349,6 +349,26 @@ __device__ __forceinline__ unsigned long long h2_to_f2(uint32_t h) {
     return pk2(__low2float(v), __high2float(v));
 }
 
+// Mixed-precision blend step (FHFMA): a0 += w * v.lo, a1 += w * v.hi with w the low (SEL = 0)
+// or high (SEL = 1) fp16 of w2, fp32 accumulation; no half -> float conversions.
+template <int SEL>
+__device__ __forceinline__ void fhfma2(uint32_t w2, uint32_t v, float& a0, float& a1) {
+    if constexpr (SEL == 0)
+        asm("{.reg .f16 w, x, vl, vh; mov.b32 {w, x}, %2; mov.b32 {vl, vh}, %3;\n"
+            "fma.rn.f32.f16 %0, w, vl, %0; fma.rn.f32.f16 %1, w, vh, %1;}"
+            : "+f"(a0), "+f"(a1) : "r"(w2), "r"(v));
+    else
+        asm("{.reg .f16 w, x, vl, vh; mov.b32 {x, w}, %2; mov.b32 {vl, vh}, %3;\n"
+            "fma.rn.f32.f16 %0, w, vl, %0; fma.rn.f32.f16 %1, w, vh, %1;}"
+            : "+f"(a0), "+f"(a1) : "r"(w2), "r"(v));
+}
+// (lo, hi) fp32 -> fp16x2, round to nearest
+__device__ __forceinline__ uint32_t f2_to_h2(float lo, float hi) {
+    uint32_t r;
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+
 // ------------------------------------------------------------------ level table in shared memory
 // The fp16 *inference* table keeps hashed levels in the parameter layout (T entries of F
 // halves) but stores every dense level corner-packed: cell c = x + N*y + N^2*z holds its 8
@@ -503,8 +523,12 @@ __device__ __forceinline__ void encode_issue(const LevelSm* lv, const void* tab,
     }
 }
 
-// Step 2: trilinear weights (wx*wy)*wz and the fp32 blend, level by level -> 8 halves.
-template <int F>
+// Step 2: trilinear weights (wx*wy)*wz and the blend with fp32 accumulation, level by level
+// -> 8 halves.  kHalfW (inference): weights rounded once to fp16 (relative error <= 2^-12,
+// DESIGN.md reading R-blend) so each corner is two mixed-precision FMAs (FHFMA) with no
+// half -> float conversions; otherwise (training forward, whose features feed the
+// gradients) fp32 weights and converted entries.
+template <int F, bool kHalfW>
 __device__ __forceinline__ uint4 encode_finish(const ChunkGather<F>& G) {
     constexpr int NL = 8 / F;
     uint4 out;
@@ -516,30 +540,59 @@ __device__ __forceinline__ uint4 encode_finish(const ChunkGather<F>& G) {
         const unsigned long long wxy0 = mul2(wx, pk2(1.0f - f1, 1.0f - f1));
         const unsigned long long wxy1 = mul2(wx, pk2(f1, f1));
         const unsigned long long wz0 = pk2(1.0f - f2, 1.0f - f2), wz1 = pk2(f2, f2);
-        float w[8];
-        float2 t;
-        t = upk2(mul2(wxy0, wz0)); w[0] = t.x; w[1] = t.y;
-        t = upk2(mul2(wxy1, wz0)); w[2] = t.x; w[3] = t.y;
-        t = upk2(mul2(wxy0, wz1)); w[4] = t.x; w[5] = t.y;
-        t = upk2(mul2(wxy1, wz1)); w[6] = t.x; w[7] = t.y;
-        if constexpr (F == 2) {
-            unsigned long long acc = 0ull;   // (+0, +0)
+        const unsigned long long wp[4] = {mul2(wxy0, wz0), mul2(wxy1, wz0), mul2(wxy0, wz1), mul2(wxy1, wz1)};
+        if constexpr (kHalfW) {
+            uint32_t wh[4];   // corner weights k = 2i, 2i+1 as fp16x2
 #pragma unroll
-            for (int k = 0; k < 8; ++k) acc = fma2s(w[k], h2_to_f2(G.v[j][k]), acc);
-            const float2 a = upk2(acc);
-            __half2 h = __floats2half2_rn(a.x, a.y);
-            o32[j] = *reinterpret_cast<uint32_t*>(&h);
-        } else {
-            unsigned long long a01 = 0ull, a23 = 0ull;
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                a01 = fma2s(w[k], h2_to_f2(G.v[j][k].x), a01);
-                a23 = fma2s(w[k], h2_to_f2(G.v[j][k].y), a23);
+            for (int i = 0; i < 4; ++i) {
+                const float2 t = upk2(wp[i]);
+                wh[i] = f2_to_h2(t.x, t.y);
             }
-            const float2 p = upk2(a01), q = upk2(a23);
-            __half2 h0 = __floats2half2_rn(p.x, p.y), h1 = __floats2half2_rn(q.x, q.y);
-            o32[2 * j] = *reinterpret_cast<uint32_t*>(&h0);
-            o32[2 * j + 1] = *reinterpret_cast<uint32_t*>(&h1);
+            if constexpr (F == 2) {
+                float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    fhfma2<0>(wh[i], G.v[j][2 * i], a0, a1);
+                    fhfma2<1>(wh[i], G.v[j][2 * i + 1], a0, a1);
+                }
+                o32[j] = f2_to_h2(a0, a1);
+            } else {
+                float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    fhfma2<0>(wh[i], G.v[j][2 * i].x, a0, a1);
+                    fhfma2<0>(wh[i], G.v[j][2 * i].y, a2, a3);
+                    fhfma2<1>(wh[i], G.v[j][2 * i + 1].x, a0, a1);
+                    fhfma2<1>(wh[i], G.v[j][2 * i + 1].y, a2, a3);
+                }
+                o32[2 * j] = f2_to_h2(a0, a1);
+                o32[2 * j + 1] = f2_to_h2(a2, a3);
+            }
+        } else {
+            float w[8];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const float2 t = upk2(wp[i]);
+                w[2 * i] = t.x;
+                w[2 * i + 1] = t.y;
+            }
+            if constexpr (F == 2) {
+                unsigned long long acc = 0ull;   // (+0, +0)
+#pragma unroll
+                for (int k = 0; k < 8; ++k) acc = fma2s(w[k], h2_to_f2(G.v[j][k]), acc);
+                const float2 a = upk2(acc);
+                o32[j] = f2_to_h2(a.x, a.y);
+            } else {
+                unsigned long long a01 = 0ull, a23 = 0ull;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    a01 = fma2s(w[k], h2_to_f2(G.v[j][k].x), a01);
+                    a23 = fma2s(w[k], h2_to_f2(G.v[j][k].y), a23);
+                }
+                const float2 p = upk2(a01), q = upk2(a23);
+                o32[2 * j] = f2_to_h2(p.x, p.y);
+                o32[2 * j + 1] = f2_to_h2(q.x, q.y);
+            }
         }
     }
     return out;
@@ -550,12 +603,12 @@ __device__ __forceinline__ uint4 encode_finish(const ChunkGather<F>& G) {
 // entries (dense: corner-packed cell record; hashed: 8 gathers, C2, C3), trilinear weights
 // (wx*wy)*wz, blend in fp32.  idx_out (nullable) receives the 8*NL
 // canonical corner indices within their levels (parity hook).
-template <int F>
+template <int F, bool kHalfW = true>
 __device__ __forceinline__ uint4 encode_chunk_sm(const LevelSm* lv, const void* tab, uint32_t hmask, float x0,
                                                  float x1, float x2, int l0, uint32_t* idx_out) {
     ChunkGather<F> G;
     encode_issue<F>(lv, tab, hmask, x0, x1, x2, l0, idx_out, G);
-    return encode_finish<F>(G);
+    return encode_finish<F, kHalfW>(G);
 }
 
 // ------------------------------------------------------------------ tensor-core MLP

@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(256, 2) k_train_fwd(TrainArgs a) {
                 const int q = qb * 32 + lane;
                 if (q < nv) {
                     const int p = c / cpp, l0 = (c - p * cpp) * (8 / F);
-                    *reinterpret_cast<uint4*>(feat + q * (D + 8) + c * 8) = encode_chunk_sm<F>(
+                    *reinterpret_cast<uint4*>(feat + q * (D + 8) + c * 8) = encode_chunk_sm<F, false>(
                         lv, a.g.table, hmask, xs[(p * 3 + 0) * kTileQ + q], xs[(p * 3 + 1) * kTileQ + q],
                         xs[(p * 3 + 2) * kTileQ + q], l0, nullptr);
                 }

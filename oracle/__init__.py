@@ -45,6 +45,8 @@ def lib():
         _lib.orc_train_grad.restype = C.c_int64
         _lib.orc_batch_loss_double.restype = C.c_double
         _lib.orc_num_threads.restype = C.c_int32
+        _lib.orc_sigmoid_f32.restype = C.c_float
+        _lib.orc_sigmoid_f32.argtypes = [C.c_float]
     return _lib
 
 
@@ -189,6 +191,11 @@ def query(grid: Grid, n_points, table_fp16, layers, leaf_lo, leaf_hi, rays, mode
     if zt is not None:
         out["z_trace"] = zt
     return out
+
+
+def sigmoid_f32(z: float) -> float:
+    """The decode's fp32 sigmoid (C27), as the logic replay evaluates it."""
+    return float(lib().orc_sigmoid_f32(C.c_float(z)))
 
 
 def replay(leaf_lo, leaf_hi, rays, z_trace, mode=0):

@@ -413,13 +413,41 @@ void orc_query(int32_t L, int32_t F, int32_t log2_T, int32_t n_points, int32_t n
     }
 }
 
+// ------------------------------------------------------------------ fp32 decode sigmoid (C27)
+// The decode's sigmoid as DESIGN.md C27 defines it: correctly rounded fp32 operations only
+// (mul, fma, rint, add, div), so every IEEE-754 implementation produces the same bits.
+//   x = clamp(-z, -87, 87); n = rint(x * log2 e); r = x - n ln2 (hi/lo, two fmas);
+//   p = degree-7 Taylor polynomial of e^r (Horner, fmas); e = p * 2^n; s = 1 / (1 + e).
+// |r| <= 0.35 so the truncation error is < 6e-9 relative; s agrees with the exact sigmoid
+// to a few fp32 ulp (pinned in tests/test_oracle.py).
+static float sigmoid_f32(float z) {
+    const float x = std::fmin(std::fmax(-z, -87.0f), 87.0f);
+    const float n = std::nearbyint(x * 1.44269504f);
+    float r = std::fma(-n, 0.693145751953125f, x);
+    r = std::fma(-n, 1.42860677e-6f, r);
+    float p = 1.98412698e-4f;
+    p = std::fma(p, r, 1.38888889e-3f);
+    p = std::fma(p, r, 8.33333333e-3f);
+    p = std::fma(p, r, 4.16666667e-2f);
+    p = std::fma(p, r, 1.66666667e-1f);
+    p = std::fma(p, r, 0.5f);
+    p = std::fma(p, r, 1.0f);
+    p = std::fma(p, r, 1.0f);
+    const int32_t bits = ((int32_t)n + 127) << 23;
+    float scale;
+    std::memcpy(&scale, &bits, 4);
+    const float e = p * scale;
+    return 1.0f / (1.0f + e);
+}
+extern "C" float orc_sigmoid_f32(float z) { return sigmoid_f32(z); }
+
 // ------------------------------------------------------------------ logic replay (fp32)
 // The decisions of the query (termination, hit, best-hit selection) replayed in fp32 on
 // a given z per (ray, list position) — e.g. the z the GPU recorded — so that hit mask,
 // winning leaf, t bits and query count can be compared exactly (SURVEY §8(c) tier iv).
-// fp32 op order: tl = (float)sigmoid_double(z_t); t = t0 + tl*(t1-t0);
+// fp32 op order: tl = sigmoid_f32(z_t) (C27); t = t0 + tl*(t1-t0);
 // normal: nn = sqrtf(nx*nx + ny*ny + nz*nz) (left fold), n/fmaxf(nn, 1e-6f);
-// albedo = (float)sigmoid_double(z).  Returns the number of rays where a needed z was
+// albedo = sigmoid_f32(z).  Returns the number of rays where a needed z was
 // missing (NaN) from the trace.
 int64_t orc_replay(const float* leaf_lo, const float* leaf_hi, int32_t n_leaves, const float* rays,
                    int64_t n, int32_t mode, const float* z_trace /*[n][cap][8]*/, int32_t cap,
@@ -443,14 +471,14 @@ int64_t orc_replay(const float* leaf_lo, const float* leaf_hi, int32_t n_leaves,
                 const float* z = z_trace + (r * cap + k) * 8;
                 ++nq;
                 if (z[0] < 0.0f) {
-                    float tl = (float)sigmoid((double)z[1]);
+                    float tl = sigmoid_f32(z[1]);
                     float t = e.te + tl * (e.tx - e.te);
                     bool better = !found || t < bt || (t == bt && (e.te < bte || (e.te == bte && e.leaf < bleaf)));
                     if (better) {
                         found = true; bt = t; bte = e.te; bleaf = e.leaf;
                         float nn = std::sqrt(z[2] * z[2] + z[3] * z[3] + z[4] * z[4]);
                         nn = std::fmax(nn, 1e-6f);
-                        for (int c = 0; c < 3; ++c) { bn[c] = z[2 + c] / nn; ba[c] = (float)sigmoid((double)z[5 + c]); }
+                        for (int c = 0; c < 3; ++c) { bn[c] = z[2 + c] / nn; ba[c] = sigmoid_f32(z[5 + c]); }
                     }
                     if (mode == 1) break;
                 }

@@ -749,8 +749,24 @@ __device__ __forceinline__ void mlp_rows16(const MlpSmem& s, int hidden, const _
 }
 
 // ------------------------------------------------------------------ decode
-// sigmoid evaluated in double and rounded once to fp32, so that host replays agree bit
-// for bit (DESIGN.md §5 "decode").
-__device__ __forceinline__ float sigmoid_f(float z) { return (float)(1.0 / (1.0 + exp(-(double)z))); }
+// sigmoid in fp32 from correctly rounded operations only (C27), so the host's
+// logic replay reproduces it bit for bit: e^x by x = n ln2 + r (two fmas), a degree-7
+// Taylor polynomial of e^r (|r| <= 0.35), exact scaling by 2^n, then 1 / (1 + e^-z).
+__device__ __forceinline__ float sigmoid_f(float z) {
+    const float x = fminf(fmaxf(-z, -87.0f), 87.0f);
+    const float n = rintf(__fmul_rn(x, 1.44269504f));
+    float r = __fmaf_rn(-n, 0.693145751953125f, x);
+    r = __fmaf_rn(-n, 1.42860677e-6f, r);
+    float p = 1.98412698e-4f;
+    p = __fmaf_rn(p, r, 1.38888889e-3f);
+    p = __fmaf_rn(p, r, 8.33333333e-3f);
+    p = __fmaf_rn(p, r, 4.16666667e-2f);
+    p = __fmaf_rn(p, r, 1.66666667e-1f);
+    p = __fmaf_rn(p, r, 0.5f);
+    p = __fmaf_rn(p, r, 1.0f);
+    p = __fmaf_rn(p, r, 1.0f);
+    const float e = __fmul_rn(p, __int_as_float(((int)n + 127) << 23));
+    return __fdiv_rn(1.0f, __fadd_rn(1.0f, e));
+}
 
 }  // namespace nbvh

@@ -538,3 +538,21 @@ def test_p15_acceptance_floor_and_single_leaf(orc):
     out = orc.train_grad(g, 3, tab, layers, lo, hi, rank, off, lt, sc, rays, u, xi)
     rate = out["accepted"].mean()
     assert 0.0045 <= rate <= 0.0055
+
+
+# ------------------------------------------------------------------ C27 decode sigmoid
+def test_c27_sigmoid_f32_vs_exact(orc):
+    """The fp32 decode sigmoid against the exact logistic function (closed form, evaluated
+    in double by numpy): a few fp32 ulp everywhere, the exact special values at 0 and in
+    the saturated tails, monotone, and the symmetry s(-z) = 1 - s(z) to fp32 rounding."""
+    zs = np.concatenate([np.linspace(-30, 30, 6001), [-100.0, -87.5, -20.0, -1e-6, 0.0, 1e-6, 20.0, 87.5, 100.0]])
+    zs = zs.astype(np.float32)
+    got = np.array([orc.sigmoid_f32(float(z)) for z in zs], np.float64)
+    exact = 1.0 / (1.0 + np.exp(-zs.astype(np.float64)))
+    assert np.all(np.abs(got - exact) <= 4 * np.spacing(np.float32(exact)).astype(np.float64) + 1e-37)
+    assert orc.sigmoid_f32(0.0) == 0.5
+    assert orc.sigmoid_f32(100.0) == 1.0 and orc.sigmoid_f32(-100.0) < 1e-37
+    inner = np.argsort(zs)
+    assert np.all(np.diff(got[inner]) >= 0)
+    for z in (0.25, 1.0, 3.5, 9.0):
+        assert abs(orc.sigmoid_f32(-z) - (1.0 - orc.sigmoid_f32(z))) <= 2 ** -23

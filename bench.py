@@ -276,6 +276,7 @@ def run_ours(args):
                "h2d_bytes_per_step": n * 32, "d2h_bytes_per_step": d2h}
 
     mlp = bench_mlp(ctx, args)
+    gather = bench_gather(args)
     train = bench_train(ctx, args, world, rank) if args.train else None
     lod = bench_lod(args, local) if (args.lod and rank == 0) else None
     pt = bench_pathtrace(args, local) if (args.pt and rank == 0) else None
@@ -310,7 +311,7 @@ def run_ours(args):
                          "traverse_ms_per_step": statistics.mean(trav_ms),
                          "mlp_tflops": mean_q * mlp_flops / wave_s / 1e12,
                          "mlp_frac_of_bf16_peak": mean_q * mlp_flops / wave_s / 1e12 / tflops},
-            "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks.summary(), "mlp": mlp, "train": train, "lod": lod, "pathtrace": pt,
+            "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks.summary(), "mlp": mlp, "gather_roofline": gather, "train": train, "lod": lod, "pathtrace": pt,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -511,6 +512,61 @@ def bench_mlp(ctx, args):
             "tflops_algorithmic": flop_alg / ms / 1e9, "tflops_issued": flop_mma / ms / 1e9,
             "frac_of_bf16_peak": flop_mma / ms / 1e9 / tflops, "peak_tflops": tflops, "peak_source": src,
             "io_GBps": bytes_io / ms / 1e6, "io_frac_of_hbm": bytes_io / ms / 1e6 / hbm}
+
+
+def _profiled_l2_reads(kernel: str = "k_query"):
+    """(L2 read sectors from L1/TEX, duration s) of `kernel` from the newest committed ncu
+    summary (profiles/r*_ncu_full_query.txt)."""
+    import glob
+    import re
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_full_query.txt")))
+    if not files:
+        return None
+    txt = open(files[-1]).read()
+    m = re.search(r"== void " + kernel + r"<[^\n]*\n(.*?)(?:\n==|\Z)", txt, re.S)
+    if not m:
+        return None
+    sec = re.search(r"L2 read sectors from L1/TEX\s+([0-9.]+)", m.group(1))
+    dur = re.search(r"duration\s+([0-9.]+)\s+(\w+)", m.group(1))
+    if not sec or not dur:
+        return None
+    scale = {"ms": 1e-3, "us": 1e-6, "usecond": 1e-6, "msecond": 1e-3, "ns": 1e-9}.get(dur.group(2), 1e-3)
+    return float(sec.group(1)), float(dur.group(1)) * scale, os.path.basename(files[-1])
+
+
+def bench_gather(args):
+    """SURVEY §8(d) encode roofline: the measured random-sector read peak of an L2-resident
+    table (nbvh_gather_probe: 4-byte gathers = hashed levels, 32-byte = dense corner records)
+    and of an HBM-resident one, and the query kernel's L2 read-sector rate (its committed ncu
+    profile) as a fraction of the L2 peak."""
+    import torch
+    from paper_2405_16237_b200.nbvh import gather_probe
+    sink = torch.empty(148 * 8 * 256 * 2, dtype=torch.int32, device="cuda")
+    out = {}
+    cases = (("l2_random_4B", 16 << 20, 4, 1 << 28), ("l2_random_32B", 16 << 20, 32, 1 << 27),
+             ("hbm_random_4B", 1 << 30, 4, 1 << 27))
+    stream = torch.cuda.current_stream()
+    for name, nbytes, eb, n in cases:
+        tab = torch.randint(0, 1 << 30, (nbytes // 4,), dtype=torch.int32, device="cuda")
+        gather_probe(tab, eb, n, sink)                                   # warm (L2 fill)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        done = 0
+        for i in range(3):
+            done += gather_probe(tab, eb, n, sink, seed=i + 2)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        s = e0.elapsed_time(e1) / 1e3
+        out[name + "_Gsectors_per_s"] = done / s / 1e9                  # one 32-byte sector per gather
+        out[name + "_GBps"] = done * 32 / s / 1e9
+        del tab
+    prof = _profiled_l2_reads("k_query")
+    if prof:
+        sec, dur, src = prof
+        out["k_query_l2_read_GBps"] = sec * 32 / dur / 1e9
+        out["k_query_frac_of_l2_random_peak"] = out["k_query_l2_read_GBps"] / out["l2_random_4B_GBps"]
+        out["k_query_profile"] = src
+    return out
 
 
 def run_reference(args):

@@ -193,6 +193,17 @@ nbvh_status nbvh_set_profiling(nbvh_ctx* ctx, int32_t on);
  * network the fused query kernel evaluates with mma.sync.  Asynchronous on `stream`. */
 nbvh_status nbvh_mlp_forward(nbvh_ctx* ctx, const uint16_t* d_x, int64_t m, float* d_z, void* stream);
 
+/* ---------------------------------------------------------------- measurement probe (device) */
+/* The random-gather roofline of SURVEY §8(d) (encode is bound by L2 random-sector reads):
+ * reads n_gathers uniformly random entries (entry_bytes 4 = one sector per load, like a hashed
+ * level; 32 = a corner-packed dense record) of the device table d_table (table_bytes / entry_bytes
+ * must be a power of two; 32-byte aligned), 8 independent address chains per thread on a grid
+ * of SMs x 8 CTAs x 256 threads, and XORs the data into d_sink (>= SMs*2048 uint32, device).
+ * *n_done (host) receives the number of gathers actually issued (rounded up).  No context;
+ * the caller times it (CUDA events on `stream`).  NBVH_EINVAL on bad arguments. */
+nbvh_status nbvh_gather_probe(const void* d_table, int64_t table_bytes, int32_t entry_bytes, int64_t n_gathers,
+                              uint32_t seed, uint32_t* d_sink, int64_t sink_len, int64_t* n_done, void* stream);
+
 /* ---------------------------------------------------------------- hybrid path tracing (device) */
 /* NEXT-3 (BASELINE cfg 3; PAPER §7: "a BLAS is classical or N-BVH; both
  * query types yield the same type of intersection data").

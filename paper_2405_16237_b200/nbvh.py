@@ -81,6 +81,7 @@ SIGNATURES = {
     "nbvh_set_leaf_rank": (C.c_int, [_P, _I32, _P]),
     "nbvh_mlp_forward": (C.c_int, [_P, _P, _I64, _P, _P]),
     "nbvh_intersect_mesh": (C.c_int, [_P, _P, _I64, Hits, _P]),
+    "nbvh_gather_probe": (C.c_int, [_P, _I64, _I32, _I64, C.c_uint32, _P, _I64, _P, _P]),
     "nbvh_pt_shade": (C.c_int, [_P, _P, _I64, Hits, Hits, _P, _P, _P, C.c_uint64, _I32, _P, _F, _P, _P]),
     "nbvh_debug_traverse": (C.c_int, [_P, _P, _I64, _I32, _I32, _P, _P, _P, _P, _P]),
     "nbvh_debug_encode": (C.c_int, [_P, _P, _I64, _P, _P, _P]),
@@ -120,6 +121,18 @@ def _stream_ptr(stream):
         import torch
         return torch.cuda.current_stream().cuda_stream if torch.cuda.is_available() else None
     return getattr(stream, "cuda_stream", stream)
+
+
+def gather_probe(table, entry_bytes: int, n_gathers: int, sink, seed: int = 1, stream=None) -> int:
+    """nbvh_gather_probe: n_gathers random entry_bytes-wide reads of the device tensor `table`
+    (asynchronous); returns the number of gathers issued."""
+    done = C.c_int64(0)
+    st = load_library().nbvh_gather_probe(_ptr(table), table.numel() * table.element_size(), int(entry_bytes),
+                                          int(n_gathers), int(seed) & 0xFFFFFFFF, _ptr(sink), sink.numel(),
+                                          C.byref(done), _stream_ptr(stream))
+    if st != 0:
+        raise NbvhError(st, "gather_probe: bad arguments")
+    return int(done.value)
 
 
 def default_config(**kw) -> Config:

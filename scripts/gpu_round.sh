@@ -27,3 +27,8 @@ if [ "${SKIP_NCU:-0}" != "1" ]; then
       -o $OUT/prof_train_$TAG -f $CMD > $OUT/ncu_full_train.log 2>&1
   echo "ncu full train exit $?" >> $OUT/ncu_full_train.log
 fi
+if [ "${SKIP_NCU:-0}" != "1" ]; then
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_mlp_tc" -s 0 -c 1 \
+      -o $OUT/prof_mlp_$TAG -f $CMD > $OUT/ncu_full_mlp.log 2>&1
+  echo "ncu full mlp exit $?" >> $OUT/ncu_full_mlp.log
+fi

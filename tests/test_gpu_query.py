@@ -279,3 +279,22 @@ def test_query_1080p_sampled_full_size(orc):
     h = clear & (o["hit"] == 1)
     assert h.sum() > 50
     assert np.abs(g["t"][h] - o["t"][h]).max() <= 2e-3 * 2.9
+
+
+def test_gather_probe_runs_and_validates():
+    """nbvh_gather_probe (the §8(d) random-gather roofline): issues at least the requested
+    gathers, touches only the table (the XOR sink is reproducible for a fixed seed), and
+    rejects bad arguments."""
+    from paper_2405_16237_b200.nbvh import gather_probe, NbvhError
+    tab = torch.arange(1 << 16, dtype=torch.int32, device="cuda")
+    sink = torch.empty(148 * 8 * 256 * 2, dtype=torch.int32, device="cuda")
+    for eb in (4, 32):
+        n = gather_probe(tab, eb, 1 << 20, sink, seed=3)
+        assert n >= 1 << 20
+        a = sink.clone()
+        gather_probe(tab, eb, 1 << 20, sink, seed=3)
+        assert torch.equal(a, sink)
+    with pytest.raises(NbvhError):
+        gather_probe(tab, 8, 1 << 20, sink)
+    with pytest.raises(NbvhError):
+        gather_probe(tab[:3 * 4096], 4, 1 << 20, sink)          # not a power of two

@@ -792,8 +792,12 @@ extern "C" nbvh_status nbvh_query_host(nbvh_ctx* c, const nbvh_ray* h_rays, int6
     d.hit = reinterpret_cast<uint8_t*>(base + 9 * n);
     nbvh_ray* d_rays = reinterpret_cast<nbvh_ray*>(c->d_stage_rays);
     cudaError_t e = cudaSuccess;
-    // events 32.. : [32+2k] upload k done, [33+2k] query k done (0-2 query profiling, 16-23 training)
+    // events 32.. : [32+2k] upload k done, [33+2k] query k done (0-2 query profiling, 16-23 training);
+    // 64 + 4k + {0 upload start, 1 query start, 2 download start, 3 download done}: the
+    // NBVH_HOST_TIMELINE=1 diagnostic (chunk timeline printed to stderr, scripts/e2e_timeline.py)
+    static const bool timeline = std::getenv("NBVH_HOST_TIMELINE") != nullptr;
     for (int k = 0; k < chunks && e == cudaSuccess; ++k) {
+        if (timeline) cudaEventRecord(ctx_event(c, 64 + 4 * k), H);
         e = copy_chunk(const_cast<nbvh_ray*>(h_rays), d_rays, sizeof(nbvh_ray), n, W, plan[k],
                        cudaMemcpyHostToDevice, H);
         if (e == cudaSuccess) e = cudaEventRecord(ctx_event(c, 32 + 2 * k), H);
@@ -806,10 +810,12 @@ extern "C" nbvh_status nbvh_query_host(nbvh_ctx* c, const nbvh_ray* h_rays, int6
         cudaStream_t Sq = Q[k & 1];
         e = cudaStreamWaitEvent(Sq, ctx_event(c, 32 + 2 * k), 0);
         if (e != cudaSuccess) return cuda_fail(c, e, "query_host: wait");
+        if (timeline) cudaEventRecord(ctx_event(c, 65 + 4 * k), Sq);
         st = run_query(c, d_rays + o, m, lod, dk, nullptr, 0, Sq, true, o, k);
         if (st) return st;
         e = cudaEventRecord(ctx_event(c, 33 + 2 * k), Sq);
         if (e == cudaSuccess) e = cudaStreamWaitEvent(Dn, ctx_event(c, 33 + 2 * k), 0);
+        if (timeline) cudaEventRecord(ctx_event(c, 66 + 4 * k), Dn);
         if (e == cudaSuccess) e = copy_chunk(h_out.hit, d.hit, 1, n, W, plan[k], cudaMemcpyDeviceToHost, Dn);
         if (e == cudaSuccess) e = copy_chunk(h_out.t, d.t, 4, n, W, plan[k], cudaMemcpyDeviceToHost, Dn);
         if (e == cudaSuccess)
@@ -821,11 +827,23 @@ extern "C" nbvh_status nbvh_query_host(nbvh_ctx* c, const nbvh_ray* h_rays, int6
         if (e == cudaSuccess && h_out.n_queries)
             e = copy_chunk(h_out.n_queries, d.n_queries, 4, n, W, plan[k], cudaMemcpyDeviceToHost, Dn);
         if (e != cudaSuccess) return cuda_fail(c, e, "query_host: copies");
+        if (timeline) cudaEventRecord(ctx_event(c, 67 + 4 * k), Dn);
     }
     e = cudaStreamSynchronize(Dn);
     if (e == cudaSuccess) e = cudaStreamSynchronize(Q[1]);
     if (e == cudaSuccess) e = cudaStreamSynchronize(S);
     if (e != cudaSuccess) return cuda_fail(c, e, "query_host: D2H");
+    if (timeline) {
+        auto at = [&](int i) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, ctx_event(c, 64), ctx_event(c, i));
+            return ms;
+        };
+        for (int k = 0; k < chunks; ++k)
+            std::fprintf(stderr, "chunk %d (%lld rays): up %.3f-%.3f  query %.3f-%.3f  down %.3f-%.3f ms\n", k,
+                         (long long)plan[k].size(), at(64 + 4 * k), at(32 + 2 * k), at(65 + 4 * k), at(33 + 2 * k),
+                         at(66 + 4 * k), at(67 + 4 * k));
+    }
     c->qstats.n_rays = n;
     return NBVH_OK;
 }

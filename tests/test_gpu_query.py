@@ -298,3 +298,18 @@ def test_gather_probe_runs_and_validates():
         gather_probe(tab, 8, 1 << 20, sink)
     with pytest.raises(NbvhError):
         gather_probe(tab[:3 * 4096], 4, 1 << 20, sink)          # not a power of two
+
+
+def test_query_host_path_full_frame():
+    """The host path at the bench's full size (6 block-interleaved chunks on two query streams,
+    strided copies) returns exactly what the device path returns, twice in a row."""
+    ctx, sc, tab, layers = _mk_ctx("1080p", table_seed=9, seed=6, list_cap=12)
+    c = synth.CONFIGS["1080p"]
+    rays = synth.camera_rays(*c["res"], c["eye"], vfov_deg=c["vfov"])
+    ctx.reserve(rays.shape[0])
+    d = {k: v.cpu().numpy() for k, v in ctx.query(torch.from_numpy(rays).cuda()).items()}
+    for _ in range(2):
+        h = ctx.query_host(rays)
+        for k in d:
+            assert np.array_equal(d[k].reshape(h[k].shape), h[k]), k
+    assert ctx.query_stats()["n_queries"] > rays.shape[0] // 2

@@ -278,6 +278,8 @@ def run_ours(args):
     mlp = bench_mlp(ctx, args)
     gather = bench_gather(args)
     train = bench_train(ctx, args, world, rank) if args.train else None
+    if train and train.get("bwd_scatter_Gred_v2_per_s") and gather.get("l2_red_v2_f32_Gops"):
+        train["bwd_scatter_frac_of_l2_red_v2_peak"] = train["bwd_scatter_Gred_v2_per_s"] / gather["l2_red_v2_f32_Gops"]
     lod = bench_lod(args, local) if (args.lod and rank == 0) else None
     pt = bench_pathtrace(args, local) if (args.pt and rank == 0) else None
 
@@ -364,11 +366,17 @@ def bench_train(ctx, args, world, rank):
     ph = ctx.train_stats()["ms_phase"]
     ctx.set_profiling(False)
     _, n_grad = ctx.grad_buffer()
+    h = ctx.cfg
+    # T7 scatter: one fp32x2 reduction per (sample, point, level, corner) (F = 2), the smem-
+    # privatised coarse levels included -> an upper bound on the global reductions issued
+    red = st["n_accepted"] * h.n_points * h.L * 8 * (h.F // 2)
+    red_rate = red / (ph["bwd"] / 1e3) / 1e9 if ph.get("bwd") else None
     return {"metric": "training rays/s (BASELINE cfg 5)", "value": n_global / (ms / 1e3) / 1e6, "unit": "Mrays/s",
             "global_batch": n_global, "scaling": "strong", "ms_per_step": ms,
             "accepted_per_step_rank0": st["n_accepted"], "first_hit_per_step_rank0": st["n_first_hit"],
             "phase_ms_rank0": ph, "allreduce_bytes": 4 * n_grad if world > 1 else 0,
-            "gpu_launches_per_step": st["n_launches"]}
+            "gpu_launches_per_step": st["n_launches"],
+            "bwd_scatter_Gred_v2_per_s": red_rate}
 
 
 def bench_lod(args, device):
@@ -559,6 +567,17 @@ def bench_gather(args):
         s = e0.elapsed_time(e1) / 1e3
         out[name + "_Gsectors_per_s"] = done / s / 1e9                  # one 32-byte sector per gather
         out[name + "_GBps"] = done * 32 / s / 1e9
+        del tab
+    from paper_2405_16237_b200.nbvh import atomic_probe
+    for vec in (1, 2):                                                   # T7 scatter roofline
+        tab = torch.zeros((32 << 20) // 4, dtype=torch.float32, device="cuda")   # ~ the cfg-2 gradient buffer
+        atomic_probe(tab, vec, 1 << 26)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        done = sum(atomic_probe(tab, vec, 1 << 27, seed=i + 2) for i in range(2))
+        e1.record(stream)
+        torch.cuda.synchronize()
+        out[f"l2_red_{'v2_' if vec == 2 else ''}f32_Gops"] = done / (e0.elapsed_time(e1) / 1e3) / 1e9
         del tab
     prof = _profiled_l2_reads("k_query")
     if prof:

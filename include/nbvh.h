@@ -203,6 +203,13 @@ nbvh_status nbvh_mlp_forward(nbvh_ctx* ctx, const uint16_t* d_x, int64_t m, floa
  * the caller times it (CUDA events on `stream`).  NBVH_EINVAL on bad arguments. */
 nbvh_status nbvh_gather_probe(const void* d_table, int64_t table_bytes, int32_t entry_bytes, int64_t n_gathers,
                               uint32_t seed, uint32_t* d_sink, int64_t sink_len, int64_t* n_done, void* stream);
+/* The scatter roofline of SURVEY §8(d) (T7 is bound by L2 atomics): n_ops uniformly random
+ * fp32 reductions (vec 1: red.global.add.f32; vec 2: red.global.add.v2.f32 on 8-byte pairs,
+ * as the training backward issues for F = 2) of +1 into the device table d_table
+ * (table_bytes / (4 vec) a power of two; 8-byte aligned; its contents are modified).  *n_done
+ * (host) = reductions issued.  No context; the caller times it.  NBVH_EINVAL on bad arguments. */
+nbvh_status nbvh_atomic_probe(float* d_table, int64_t table_bytes, int32_t vec, int64_t n_ops, uint32_t seed,
+                              int64_t* n_done, void* stream);
 
 /* ---------------------------------------------------------------- hybrid path tracing (device) */
 /* NEXT-3 (BASELINE cfg 3; PAPER §7: "a BLAS is classical or N-BVH; both

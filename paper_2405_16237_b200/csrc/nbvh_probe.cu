@@ -40,9 +40,56 @@ __global__ void __launch_bounds__(256) k_gather_probe(const uint32_t* __restrict
     sink[tid] = acc;
 }
 
+// Random fp32 reductions into an L2-resident table (the T7 hash-grid scatter's roofline,
+// "measured L2 atomic peak"): kVec = 1 -> red.global.add.f32, 2 ->
+// red.global.add.v2.f32 (8-byte aligned pairs, what k_train_bwd issues for F = 2).
+template <int kVec>
+__global__ void __launch_bounds__(256) k_atomic_probe(float* __restrict__ tab, uint32_t mask, int64_t per_thread,
+                                                      uint32_t seed) {
+    constexpr int kChains = 8;
+    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t st[kChains];
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) st[c] = (tid * 0x9E3779B9u) ^ (seed + 0x85EBCA6Bu * (uint32_t)(c + 1));
+    for (int64_t i = 0; i < per_thread; i += kChains) {
+#pragma unroll
+        for (int c = 0; c < kChains; ++c) {
+            st[c] = st[c] * 1664525u + 1013904223u;
+            const uint32_t e = (st[c] >> 7) & mask;
+            if constexpr (kVec == 1)
+                asm volatile("red.global.add.f32 [%0], %1;" ::"l"(tab + e), "f"(1.0f) : "memory");
+            else
+                asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(tab + 2ull * e), "f"(1.0f), "f"(1.0f)
+                             : "memory");
+        }
+    }
+}
+
 }  // namespace nbvh
 
 using namespace nbvh;
+
+extern "C" nbvh_status nbvh_atomic_probe(float* d_table, int64_t table_bytes, int32_t vec, int64_t n_ops,
+                                         uint32_t seed, int64_t* n_done, void* stream) {
+    if (!d_table || (vec != 1 && vec != 2) || n_ops <= 0 || (reinterpret_cast<uintptr_t>(d_table) & 7))
+        return NBVH_EINVAL;
+    const int64_t n_entries = table_bytes / (4 * vec);
+    if (n_entries < 1 || (n_entries & (n_entries - 1))) return NBVH_EINVAL;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t threads = (int64_t)sms * 8 * 256;
+    int64_t per_thread = (n_ops + threads - 1) / threads;
+    per_thread = (per_thread + 7) / 8 * 8;
+    const uint32_t mask = (uint32_t)(n_entries - 1);
+    cudaStream_t s = (cudaStream_t)stream;
+    if (vec == 1)
+        k_atomic_probe<1><<<sms * 8, 256, 0, s>>>(d_table, mask, per_thread, seed);
+    else
+        k_atomic_probe<2><<<sms * 8, 256, 0, s>>>(d_table, mask, per_thread, seed);
+    if (n_done) *n_done = per_thread * threads;
+    return cudaGetLastError() == cudaSuccess ? NBVH_OK : NBVH_ECUDA;
+}
 
 extern "C" nbvh_status nbvh_gather_probe(const void* d_table, int64_t table_bytes, int32_t entry_bytes,
                                          int64_t n_gathers, uint32_t seed, uint32_t* d_sink, int64_t sink_len,

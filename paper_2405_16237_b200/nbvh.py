@@ -82,6 +82,7 @@ SIGNATURES = {
     "nbvh_mlp_forward": (C.c_int, [_P, _P, _I64, _P, _P]),
     "nbvh_intersect_mesh": (C.c_int, [_P, _P, _I64, Hits, _P]),
     "nbvh_gather_probe": (C.c_int, [_P, _I64, _I32, _I64, C.c_uint32, _P, _I64, _P, _P]),
+    "nbvh_atomic_probe": (C.c_int, [_P, _I64, _I32, _I64, C.c_uint32, _P, _P]),
     "nbvh_pt_shade": (C.c_int, [_P, _P, _I64, Hits, Hits, _P, _P, _P, C.c_uint64, _I32, _P, _F, _P, _P]),
     "nbvh_debug_traverse": (C.c_int, [_P, _P, _I64, _I32, _I32, _P, _P, _P, _P, _P]),
     "nbvh_debug_encode": (C.c_int, [_P, _P, _I64, _P, _P, _P]),
@@ -132,6 +133,17 @@ def gather_probe(table, entry_bytes: int, n_gathers: int, sink, seed: int = 1, s
                                           C.byref(done), _stream_ptr(stream))
     if st != 0:
         raise NbvhError(st, "gather_probe: bad arguments")
+    return int(done.value)
+
+
+def atomic_probe(table, vec: int, n_ops: int, seed: int = 1, stream=None) -> int:
+    """nbvh_atomic_probe: n_ops random fp32 (vec 1) or fp32x2 (vec 2) reductions into the device
+    float tensor `table` (asynchronous); returns the number issued."""
+    done = C.c_int64(0)
+    st = load_library().nbvh_atomic_probe(_ptr(table), table.numel() * table.element_size(), int(vec), int(n_ops),
+                                           int(seed) & 0xFFFFFFFF, C.byref(done), _stream_ptr(stream))
+    if st != 0:
+        raise NbvhError(st, "atomic_probe: bad arguments")
     return int(done.value)
 
 

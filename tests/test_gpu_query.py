@@ -313,3 +313,16 @@ def test_query_host_path_full_frame():
         for k in d:
             assert np.array_equal(d[k].reshape(h[k].shape), h[k]), k
     assert ctx.query_stats()["n_queries"] > rays.shape[0] // 2
+
+
+def test_atomic_probe_counts_every_reduction():
+    """nbvh_atomic_probe (the §8(d) scatter roofline): the table's sum equals the number of
+    reductions issued (each adds 1 per component), and bad arguments are rejected."""
+    from paper_2405_16237_b200.nbvh import atomic_probe, NbvhError
+    for vec in (1, 2):
+        tab = torch.zeros(1 << 16, dtype=torch.float32, device="cuda")
+        n = atomic_probe(tab, vec, 1 << 20)
+        torch.cuda.synchronize()
+        assert n >= 1 << 20 and int(tab.double().sum().item()) == n * vec
+    with pytest.raises(NbvhError):
+        atomic_probe(torch.zeros(3 << 10, device="cuda"), 1, 1 << 10)

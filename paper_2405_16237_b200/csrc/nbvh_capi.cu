@@ -561,8 +561,8 @@ nbvh_status run_query(nbvh_ctx* c, const nbvh_ray* rays, int64_t n, int32_t lod,
     int32_t* lst_leaf = c->d_lst_leaf + kListK * work_off;
     float* lst_te = c->d_lst_te + kListK * work_off;
     float* lst_tx = c->d_lst_tx + kListK * work_off;
-    int32_t* act = c->d_act + work_off;
-    int32_t* act_long = c->d_act_long + work_off;
+    WorkRec* act = c->d_act + work_off;
+    WorkRec* act_long = c->d_act_long + work_off;
     TraverseArgs ta{};
     ta.cut = make_cut(c, lod);
     ta.rays = reinterpret_cast<const float4*>(rays);

@@ -71,8 +71,8 @@ struct nbvh_ctx {
     float* d_lst_te = nullptr;
     float* d_lst_tx = nullptr;
     int32_t* d_state = nullptr;        // 2 arrays of n int32: list fill, "more leaves" flag
-    int32_t* d_act = nullptr;          // work list of the persistent query kernel
-    int32_t* d_act_long = nullptr;     // its long-ray part (consumed first)
+    nbvh::WorkRec* d_act = nullptr;      // work list of the persistent query kernel
+    nbvh::WorkRec* d_act_long = nullptr; // its long-ray part (consumed first)
     int32_t* d_misc = nullptr;         // kCounterBlocks QueryCounters blocks, kCounterStride int32 apart
     int32_t* h_misc = nullptr;         // pinned mirror
     float* d_stage_rays = nullptr;     // host-path staging

@@ -107,12 +107,13 @@ __global__ void __launch_bounds__(128) k_traverse(TraverseArgs a) {
     float* lte = reinterpret_cast<float*>(sm_raw) + threadIdx.x;
     float* ltx = lte + a.cap * S;
     int* lid = sm_raw + 2 * a.cap * S + threadIdx.x;
-    bool more_long = false;
+    bool more_long = false, more = false;
+    int n = 0;
+    RayDev R;
     if (valid) {
-        RayDev R = load_ray(a.rays, r);
-        bool more = false;
+        R = load_ray(a.rays, r);
         SmemStack st{sm_raw + 3 * a.cap * S + threadIdx.x, S, a.cut.depth + 2};
-        const int n = traverse_smem_list(a.cut, R, a.cap, lte, ltx, lid, S, st, more, &a.ctr->err);
+        n = traverse_smem_list(a.cut, R, a.cap, lte, ltx, lid, S, st, more, &a.ctr->err);
         more_long = more || n >= 3;
         for (int j = 0; j < n; ++j) {
             a.lst_leaf[(int64_t)j * a.n_rays + r] = lid[j * S];
@@ -149,8 +150,13 @@ __global__ void __launch_bounds__(128) k_traverse(TraverseArgs a) {
     bl = __shfl_sync(0xffffffffu, bl, 0);
     bs = __shfl_sync(0xffffffffu, bs, 0);
     const unsigned lt = (1u << lane) - 1u;
-    if (is_long) a.act_long[bl + __popc(ml & lt)] = (int)r;
-    else if (active) a.act_out[bs + __popc(ms & lt)] = (int)r;
+    if (active) {
+        WorkRec w;
+        w.o = make_float4(R.o[0], R.o[1], R.o[2], __int_as_float((int)r));
+        w.d = make_float4(R.d[0], R.d[1], R.d[2], __int_as_float(n | (more ? 1 << 16 : 0)));
+        if (is_long) a.act_long[bl + __popc(ml & lt)] = w;
+        else a.act_out[bs + __popc(ms & lt)] = w;
+    }
 }
 
 // Debug traversal: full lists up to `cap` (may exceed K) by repeated resumption.
@@ -309,15 +315,16 @@ __global__ void __launch_bounds__(kQueryWarps * 32, 1) k_query(QueryArgs a) {
             exhausted = base + ne >= total;
             const int i = base + __popc(em & lt_mask);
             if (empty && i < total) {
-                const int r = i < n_long ? a.act_long[i] : a.act[i - n_long];
-                const float4 r0 = __ldg(a.rays + 2 * (int64_t)r), r1 = __ldg(a.rays + 2 * (int64_t)r + 1);
+                const WorkRec* wr = i < n_long ? a.act_long + i : a.act + (i - n_long);
+                const float4 w0 = __ldg(&wr->o), w1 = __ldg(&wr->d);
+                const int r = __float_as_int(w0.w), st = __float_as_int(w1.w);
                 S.ray[lane] = r;
-                S.o[0][lane] = r0.x; S.o[1][lane] = r0.y; S.o[2][lane] = r0.z;
-                S.d[0][lane] = r1.x; S.d[1][lane] = r1.y; S.d[2][lane] = r1.z;
+                S.o[0][lane] = w0.x; S.o[1][lane] = w0.y; S.o[2][lane] = w0.z;
+                S.d[0][lane] = w1.x; S.d[1][lane] = w1.y; S.d[2][lane] = w1.z;
                 S.pos[lane] = 0;
                 S.base[lane] = 0;
-                S.nbuf[lane] = a.nbuf[r];
-                S.more[lane] = a.more[r];
+                S.nbuf[lane] = st & 0xffff;
+                S.more[lane] = st >> 16;
                 S.bt[lane] = __int_as_float(0x7f800000);
                 S.bte[lane] = 0.f;
                 S.bleaf[lane] = -1;

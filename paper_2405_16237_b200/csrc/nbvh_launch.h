@@ -34,6 +34,15 @@ struct QueryCounters {
     unsigned long long n_queries; // neural queries (ray, leaf) evaluated
 };
 
+// One work-list entry of the persistent query kernel, written by k_traverse: the ray itself
+// and its list state, so a slot refill is one level of (coalesced, 2 x 16 B) loads instead of
+// an index load followed by dependent ray / list-state loads.  (tmin / tmax are not needed
+// past the traversal: the leaf intervals already respect them.)
+struct WorkRec {
+    float4 o;        // origin xyz, .w = ray index (int bits)
+    float4 d;        // direction xyz, .w = nbuf | more << 16 (int bits)
+};
+
 struct TraverseArgs {
     CutDev cut;
     const float4* rays;
@@ -44,8 +53,8 @@ struct TraverseArgs {
     float* lst_tx;
     RayState st;
     HitsDev out;
-    int32_t* act_out;
-    int32_t* act_long;       // rays with many intersected leaves (queued first, shorter tail)
+    WorkRec* act_out;
+    WorkRec* act_long;       // rays with many intersected leaves (queued first, shorter tail)
     QueryCounters* ctr;
 };
 
@@ -75,9 +84,9 @@ struct QueryArgs {
     const int32_t* nbuf;
     const int32_t* more;
     HitsDev out;
-    const int32_t* act;      // work list: rays with >= 1 leaf (k_traverse)
+    const WorkRec* act;      // work list: rays with >= 1 leaf (k_traverse)
     const int32_t* cnt;      // its length (device)
-    const int32_t* act_long; // long-ray work list, consumed before `act`
+    const WorkRec* act_long; // long-ray work list, consumed before `act`
     const int32_t* cnt_long;
     int32_t* next;           // work-list cursor
     float* z_trace;

@@ -625,7 +625,8 @@ def run_reference(args):
     done = sum(step(args.warmup + i) for i in range(args.steps))
     dt = time.perf_counter() - t0
     v = done / dt / 1e6
-    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "Mrays/s", "n_gpus": 0, "steps": args.steps,
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "Mrays/s", "n_gpus": args.gpus,
+            "device": "cpu (the oracle runs on the host cores; no GPU is used)", "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": args.config, "rays_per_step": per_step},

@@ -2,30 +2,29 @@
 // tcgen05 / TMEM / TMA kernel: the "MLP on tensor cores" of the north star measured on its own
 // (nbvh_mlp_forward).  Streaming X (m x D_in fp16) is most of its bytes, so the design goal is
 // to keep enough X loads in flight to run at HBM speed while the tensor core works:
-// one persistent CTA per SM runs kSlots independent 128-row tiles at once; each slot owns a
-// 64-column TMEM accumulator, a hidden-activation buffer and (stage j % nst, nst a multiple of
-// kSlots) the X stages its tiles land in; a stage is refilled by TMA as soon as layer 0 of its
-// tile has read it, so the load hides under that tile's hidden layers and the other slots' work.
-//   warp 4*kSlots (one lane)    TMA producer.  D_in % 64 == 0: two 64-column boxes per tile
-//                               in the 128-byte-swizzle layout (8-row x 128-byte atoms, the
-//                               MMA reads it through SWIZZLE_128B descriptors); otherwise one
-//                               {8 halves, 128 rows} box per 16-byte K-group (no-swizzle
-//                               canonical core matrices).  Rows past m are zero-filled by TMA.
-//   warp 4*kSlots+1+g           MMA issuer of slot g: whole warp converged, one elected lane
-//                               issues (operands stay in uniform registers); one issuer per
-//                               slot, since one warp issuing every slot's ~24 MMAs per tile was
-//                               the limit.  tcgen05.mma.cta_group::1.kind::f16, M = 128, N = 64
-//                               (16 for the output layer), fp32 accumulator in TMEM, commits to
-//                               mbarriers.
-//   warps 4g..4g+3              epilogue of slot g: tcgen05.ld of the row's accumulator
-//                               (warp <-> TMEM lanes 32(w%4)..+31 <-> rows), ReLU + fp16 pack
-//                               in one instruction per pair (cvt.rn.relu.f16x2.f32), 16-byte
-//                               stores into the slot's H buffer (generic -> async proxy fence);
-//                               z stored for the output layer
-// Biases ride on the tensor core: every A tile carries one extra K=16 step whose first two
-// columns are 1 and whose B columns hold the bias split as hi + lo fp16 (b = hi + lo to ~2^-22
-// relative), so the accumulator already holds W x + b.
-// The CTA's j-th tile is blockIdx.x + j * gridDim.x and runs in slot j % kSlots.
+// one persistent CTA per SM runs NS independent 128-row tiles at once (NS = 5 for D_in >= 64,
+// 3 below); each slot owns a 64-column TMEM accumulator, an X stage (stage j % nst) and a
+// hidden-activation buffer — for D_in >= 64 the hidden activations overwrite the slot's X
+// stage once layer 0 has read it (see mlp_alias), which is what makes room for five slots.
+//   warp 4*NS (one lane)    TMA producer.  D_in % 64 == 0: two 64-column boxes per tile in the
+//                           128-byte-swizzle layout (8-row x 128-byte atoms, read by the MMA
+//                           through SWIZZLE_128B descriptors); otherwise one {8 halves, 128
+//                           rows} box per 16-byte K-group (no-swizzle canonical core
+//                           matrices).  Rows past m are zero-filled by TMA.
+//   warp 4*NS+1+g           MMA issuer of slot g: whole warp converged, one elected lane issues
+//                           (operands stay in uniform registers); one issuer per slot, since
+//                           one warp issuing every slot's ~24 MMAs per tile was the limit.
+//                           tcgen05.mma.cta_group::1.kind::f16, M = 128, N = 64 (16 for the
+//                           output layer), fp32 accumulator in TMEM, commits to mbarriers.
+//   warps 4g..4g+3          epilogue of slot g: tcgen05.ld of the row's accumulator (warp <->
+//                           TMEM lanes 32(w%4)..+31 <-> rows), ReLU + fp16 pack in one
+//                           instruction per pair (cvt.rn.relu.f16x2.f32), 16-byte stores into
+//                           the slot's H buffer (generic -> async proxy fence); z stored for
+//                           the output layer.
+// Biases ride on the tensor core: every layer has one extra K=16 step whose A columns are
+// (1, 1, 0, ...) and whose B columns hold the bias split as hi + lo fp16 (b = hi + lo to
+// ~2^-22 relative), so the accumulator already holds W x + b.
+// The CTA's j-th tile is blockIdx.x + j * gridDim.x and runs in slot j % NS.
 #include <cuda.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -35,28 +34,35 @@
 
 namespace nbvh {
 
-constexpr int kSlots = 3;
-constexpr int kMaxStages = 2 * kSlots;
-constexpr uint32_t kTmemCols = 256;     // power of two >= 64 * kSlots
-
 struct MlpTcArgs {
     const __half* W;     // layers concatenated [out][in] fp16 (inference copy)
     const float* b;      // biases fp32
     float* z;            // [m][8] out
     int64_t m;
     int32_t hidden;
-    int32_t nst;         // X stages, a multiple of kSlots
+    int32_t nst;         // X stages (a multiple of the slot count; = slots when aliased)
 };
 
 constexpr int kKgH = 64 / 8 + 2;   // K-groups (16 B = 8 halves) of an H buffer / hidden W: data + bias step
 
-__host__ __device__ constexpr uint32_t mlp_tc_stage_smem(int D) { return (uint32_t)(128 * (D / 8 + 2) * 16); }
+// Two buffer schemes (template kAlias):
+//  * separate (D_in < 64): per slot an X stage with its own bias K-step columns and an H
+//    buffer; the next X tile of a slot lands while its hidden layers run;
+//  * aliased (D_in >= 64): the hidden activations overwrite the slot's X stage once layer 0
+//    has consumed it (one ones-tile serves every bias step), so the same shared memory holds
+//    more slots; a slot's next X tile is fetched after its output layer.
+__host__ __device__ constexpr int mlp_slots(int D) { return D >= 64 ? 5 : 3; }
+__host__ __device__ constexpr bool mlp_alias(int D) { return D >= 64; }
+__host__ __device__ constexpr uint32_t mlp_tmem_cols(int ns) { return ns * 64 <= 128 ? 128 : (ns * 64 <= 256 ? 256 : 512); }
+__host__ __device__ constexpr uint32_t mlp_tc_stage_smem(int D) {
+    return (uint32_t)(128 * (D / 8 + (mlp_alias(D) ? 0 : 2)) * 16);
+}
 __host__ __device__ constexpr uint32_t mlp_tc_fixed_smem(int D, int H) {
-    return (uint32_t)(kSlots * 128 * kKgH * 16          // H buffers
+    return (uint32_t)((mlp_alias(D) ? 128 * 2 * 16 : mlp_slots(D) * 128 * kKgH * 16)   // ones tile | H buffers
                       + 64 * (D / 8 + 2) * 16            // W0 (+ bias columns)
                       + (H - 1) * 64 * kKgH * 16
                       + 16 * kKgH * 16                   // W_out padded to 16 rows
-                      + 8 * (2 * kMaxStages + 2 * kSlots) + 16);   // barriers + TMEM slot
+                      + 8 * (2 * 2 * mlp_slots(D) + 2 * mlp_slots(D)) + 16);   // barriers + TMEM slot
 }
 
 __device__ __forceinline__ uint32_t relu_pack(float lo, float hi) {
@@ -65,28 +71,34 @@ __device__ __forceinline__ uint32_t relu_pack(float lo, float hi) {
     return r;
 }
 
-constexpr int kMlpWarps = 5 * kSlots + 1;
-
 template <int D, int H>
-__global__ void __launch_bounds__(kMlpWarps * 32, 1) k_mlp_tc(const __grid_constant__ CUtensorMap tmx, MlpTcArgs a) {
+__global__ void __launch_bounds__((5 * mlp_slots(D) + 1) * 32, 1)
+    k_mlp_tc(const __grid_constant__ CUtensorMap tmx, MlpTcArgs a) {
+    constexpr int NS = mlp_slots(D);
+    constexpr bool kAlias = mlp_alias(D);
+    constexpr int kMaxStages = 2 * NS;
+    constexpr uint32_t kTmemCols = mlp_tmem_cols(NS);
     extern __shared__ __align__(1024) unsigned char sm_raw[];
     // 128-byte-swizzled X stages need 1024-byte alignment (the launch requests 1 KB extra)
     unsigned char* sm = sm_raw + ((1024u - (tc::smem_u32(sm_raw) & 1023u)) & 1023u);
     constexpr bool kSw = D % 64 == 0;                         // X in 128-byte-swizzled 64-column boxes
-    constexpr int KX = D / 8 + 2;                             // K-groups of an X stage; bias step at D/8
+    constexpr int KX = D / 8 + (kAlias ? 0 : 2);              // K-groups of an X stage (+ bias step)
+    constexpr int KW0 = D / 8 + 2;                            // K-groups of W0 (+ bias columns)
     const int nst = a.nst;
     unsigned char* sX = sm;                                   // nst x [KX][128 rows][16 B]
-    unsigned char* sH = sX + nst * 128 * KX * 16;             // kSlots x [kKgH][128][16 B]
-    unsigned char* sW0 = sH + kSlots * 128 * kKgH * 16;       // [KX][64][16 B]
-    unsigned char* sWh = sW0 + 64 * KX * 16;                  // [H-1][kKgH][64][16 B]
+    unsigned char* sAux = sX + nst * 128 * KX * 16;           // aliased: ones tile [2][128][16 B];
+                                                              // separate: NS x H [kKgH][128][16 B]
+    unsigned char* sW0 = sAux + (kAlias ? 128 * 2 * 16 : NS * 128 * kKgH * 16);   // [KW0][64][16 B]
+    unsigned char* sWh = sW0 + 64 * KW0 * 16;                 // [H-1][kKgH][64][16 B]
     unsigned char* sWo = sWh + (H - 1) * 64 * kKgH * 16;      // [kKgH][16][16 B]
     uint64_t* bar = reinterpret_cast<uint64_t*>(sWo + 16 * kKgH * 16);
     uint64_t* x_full = bar;                                   // [nst] X landed
-    uint64_t* x_empty = bar + kMaxStages;                     // [nst] layer 0 done with it
-    uint64_t* acc_full = bar + 2 * kMaxStages;                // [kSlots] a layer's MMAs done
-    uint64_t* h_ready = acc_full + kSlots;                    // [kSlots] epilogue done with a layer
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(h_ready + kSlots);
+    uint64_t* x_empty = bar + kMaxStages;                     // [nst] X stage free again
+    uint64_t* acc_full = bar + 2 * kMaxStages;                // [NS] a layer's MMAs done
+    uint64_t* h_ready = acc_full + NS;                        // [NS] epilogue done with a layer
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(h_ready + NS);
     const int tid = threadIdx.x, warp = tid >> 5;
+    auto h_buf = [&](int g) { return kAlias ? sX + g * 128 * KX * 16 : sAux + g * 128 * kKgH * 16; };
 
     // Stage W [N][K] (+ bias as two extra K columns: hi, lo) in the K-major canonical layout:
     // element (n, k) at (k/8) * (Npad*16) + n*16 + (k%8)*2 bytes.
@@ -111,12 +123,15 @@ __global__ void __launch_bounds__(kMlpWarps * 32, 1) k_mlp_tc(const __grid_const
     for (int l = 0; l < H - 1; ++l)
         stage_w(sWh + l * 64 * kKgH * 16, a.W + 64 * D + (int64_t)l * 64 * 64, a.b + 64 * (l + 1), 64, 64, 64);
     stage_w(sWo, a.W + 64 * D + (int64_t)(H - 1) * 64 * 64, a.b + 64 * H, 8, 64, 16);
-    // the bias step of every A buffer: columns (1, 1, 0, ...), then a zero K-group
+    // bias K-step A columns: (1, 1, 0, ...) then a zero K-group -- one shared tile (aliased) or
+    // after the data groups of every X stage and H buffer (separate)
     const uint4 ones = make_uint4(0x3C003C00u, 0u, 0u, 0u);     // fp16 1.0, 1.0
-    for (int i = tid; i < (nst + kSlots) * 128; i += blockDim.x) {
+    const int n_bias_tiles = kAlias ? 1 : nst + NS;
+    for (int i = tid; i < n_bias_tiles * 128; i += blockDim.x) {
         const int buf = i / 128, r = i % 128;
-        unsigned char* A = buf < nst ? sX + buf * 128 * KX * 16 + (D / 8) * 2048
-                                     : sH + (buf - nst) * 128 * kKgH * 16 + 8 * 2048;
+        unsigned char* A = kAlias ? sAux
+                                  : (buf < nst ? sX + buf * 128 * KX * 16 + (D / 8) * 2048
+                                               : sAux + (buf - nst) * 128 * kKgH * 16 + 8 * 2048);
         *reinterpret_cast<uint4*>(A + r * 16) = ones;
         *reinterpret_cast<uint4*>(A + 2048 + r * 16) = make_uint4(0, 0, 0, 0);
     }
@@ -125,7 +140,7 @@ __global__ void __launch_bounds__(kMlpWarps * 32, 1) k_mlp_tc(const __grid_const
             tc::mbar_init(x_full + i, 1);
             tc::mbar_init(x_empty + i, 1);
         }
-        for (int g = 0; g < kSlots; ++g) {
+        for (int g = 0; g < NS; ++g) {
             tc::mbar_init(acc_full + g, 1);
             tc::mbar_init(h_ready + g, 128);
         }
@@ -140,9 +155,8 @@ __global__ void __launch_bounds__(kMlpWarps * 32, 1) k_mlp_tc(const __grid_const
     const int64_t n_tiles = (a.m + 127) / 128;
     const int n_mine = n_tiles > blockIdx.x ? (int)((n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x) : 0;
 
-    if (warp == 4 * kSlots) {
-        // ---------------- TMA producer: tile j into ring stage j % nst once layer 0 of tile
-        // j - nst has read it
+    if (warp == 4 * NS) {
+        // ---------------- TMA producer: tile j into stage j % nst once that stage is free
         if ((tid & 31) == 0) {
             tc::prefetch_tmap(&tmx);
             int st = 0;
@@ -164,11 +178,11 @@ __global__ void __launch_bounds__(kMlpWarps * 32, 1) k_mlp_tc(const __grid_const
                 }
             }
         }
-    } else if (warp > 4 * kSlots) {
+    } else if (warp > 4 * NS) {
         // ---------------- MMA issuer of slot g: its tiles, layer by layer.  Descriptors are
         // built once and stepped by constant adds (the 14-bit start-address field never
         // carries: smem < 256 KB).
-        const int g = warp - 4 * kSlots - 1;
+        const int g = warp - 4 * NS - 1;
         constexpr uint32_t id64 = tc::idesc_f16(128, 64, false, false);
         constexpr uint32_t id16 = tc::idesc_f16(128, 16, false, false);
         const uint64_t dW0 = tc::smem_desc(tc::smem_u32(sW0), 1024, 128);
@@ -176,28 +190,31 @@ __global__ void __launch_bounds__(kMlpWarps * 32, 1) k_mlp_tc(const __grid_const
         const uint64_t dWo = tc::smem_desc(tc::smem_u32(sWo), 256, 128);
         const uint64_t dX = tc::smem_desc(tc::smem_u32(sX), 2048, 128);
         const uint64_t dXsw = tc::smem_desc_sw128(tc::smem_u32(sX), 1024);
-        const uint64_t dH = tc::smem_desc(tc::smem_u32(sH + g * 128 * kKgH * 16), 2048, 128);
+        const uint64_t dH = tc::smem_desc(tc::smem_u32(h_buf(g)), 2048, 128);
+        // bias K-step A operand of the hidden / output layers
+        const uint64_t dHb = kAlias ? tc::smem_desc(tc::smem_u32(sAux), 2048, 128) : dH + 4 * 256;
         const uint32_t acc = tmem + (uint32_t)(g * 64);
         uint32_t use = 0;
-        for (int j = g; j < n_mine; j += kSlots, ++use) {
+        for (int j = g; j < n_mine; j += NS, ++use) {
             // h_ready completes H + 1 times per tile; wait for the previous tile's last one
             if (use > 0) tc::mbar_wait(h_ready + g, (use * (H + 1) - 1) & 1);
             const int st = j % nst;
             tc::mbar_wait(x_full + st, (uint32_t)(j / nst) & 1);
             tc::fence_after();
             const uint64_t dXs = dX + (uint64_t)(st * 128 * KX);   // 16-byte units
+            const uint64_t dXb = kAlias ? dHb : dXs + (D / 16) * 256;   // bias step A operand
             if constexpr (kSw) {
                 const uint64_t dXw = dXsw + (uint64_t)(st * 128 * KX);
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk)                // atom kk/4, 32 bytes per K step
                     tc::mma_f16_elect(acc, dXw + (kk / 4) * 1024 + (kk % 4) * 2, dW0 + kk * 128, id64, kk > 0);
-                tc::mma_f16_elect(acc, dXs + (D / 16) * 256, dW0 + (D / 16) * 128, id64, 1);   // bias
             } else {
 #pragma unroll
-                for (int kk = 0; kk < D / 16 + 1; ++kk)            // last step: bias
+                for (int kk = 0; kk < D / 16; ++kk)
                     tc::mma_f16_elect(acc, dXs + kk * 256, dW0 + kk * 128, id64, kk > 0);
             }
-            tc::commit_elect(x_empty + st);                        // X stage free
+            tc::mma_f16_elect(acc, dXb, dW0 + (D / 16) * 128, id64, 1);   // bias
+            if constexpr (!kAlias) tc::commit_elect(x_empty + st);    // X stage free (H is separate)
             tc::commit_elect(acc_full + g);
 #pragma unroll
             for (int l = 1; l <= H; ++l) {
@@ -205,12 +222,15 @@ __global__ void __launch_bounds__(kMlpWarps * 32, 1) k_mlp_tc(const __grid_const
                 tc::fence_after();
                 if (l < H) {
 #pragma unroll
-                    for (int kk = 0; kk < 5; ++kk)                 // last step: bias
+                    for (int kk = 0; kk < 4; ++kk)
                         tc::mma_f16_elect(acc, dH + kk * 256, dWh + (l - 1) * 64 * kKgH + kk * 128, id64, kk > 0);
+                    tc::mma_f16_elect(acc, dHb, dWh + (l - 1) * 64 * kKgH + 4 * 128, id64, 1);   // bias
                 } else {
 #pragma unroll
-                    for (int kk = 0; kk < 5; ++kk)
+                    for (int kk = 0; kk < 4; ++kk)
                         tc::mma_f16_elect(acc, dH + kk * 256, dWo + kk * 32, id16, kk > 0);
+                    tc::mma_f16_elect(acc, dHb, dWo + 4 * 32, id16, 1);   // bias
+                    if constexpr (kAlias) tc::commit_elect(x_empty + st);   // stage (X, then H) free
                 }
                 tc::commit_elect(acc_full + g);
             }
@@ -219,28 +239,27 @@ __global__ void __launch_bounds__(kMlpWarps * 32, 1) k_mlp_tc(const __grid_const
         // ---------------- epilogue of slot g = warp / 4: row 32*(warp%4) + lane
         const int g = warp >> 2, q = warp & 3;
         const int row = q * 32 + (tid & 31);
-        unsigned char* hb = sH + g * 128 * kKgH * 16;
+        unsigned char* hb = h_buf(g);
         const uint32_t acc = tmem + (uint32_t)(g * 64);
         uint32_t acc_n = 0;
-        for (int j = g; j < n_mine; j += kSlots) {
+        for (int j = g; j < n_mine; j += NS) {
             const int64_t t = blockIdx.x + (int64_t)j * gridDim.x;
             for (int l = 0; l <= H; ++l) {
                 tc::mbar_wait(acc_full + g, (acc_n++) & 1);
                 tc::fence_after();
                 if (l < H) {
-                    float v[32], w[32];
-                    tc::ld32(acc, (uint32_t)(q * 32), 0u, v);
-                    tc::ld32(acc, (uint32_t)(q * 32), 32u, w);
-                    tc::fence_before();
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        *reinterpret_cast<uint4*>(hb + k * 2048 + row * 16) =
-                            make_uint4(relu_pack(v[8 * k], v[8 * k + 1]), relu_pack(v[8 * k + 2], v[8 * k + 3]),
-                                       relu_pack(v[8 * k + 4], v[8 * k + 5]), relu_pack(v[8 * k + 6], v[8 * k + 7]));
-                        *reinterpret_cast<uint4*>(hb + (k + 4) * 2048 + row * 16) =
-                            make_uint4(relu_pack(w[8 * k], w[8 * k + 1]), relu_pack(w[8 * k + 2], w[8 * k + 3]),
-                                       relu_pack(w[8 * k + 4], w[8 * k + 5]), relu_pack(w[8 * k + 6], w[8 * k + 7]));
+                    for (int half = 0; half < 2; ++half) {          // 32 accumulator columns at a time
+                        float v[32];
+                        tc::ld32(acc, (uint32_t)(q * 32), (uint32_t)(32 * half), v);
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+                            *reinterpret_cast<uint4*>(hb + (k + 4 * half) * 2048 + row * 16) =
+                                make_uint4(relu_pack(v[8 * k], v[8 * k + 1]), relu_pack(v[8 * k + 2], v[8 * k + 3]),
+                                           relu_pack(v[8 * k + 4], v[8 * k + 5]),
+                                           relu_pack(v[8 * k + 6], v[8 * k + 7]));
                     }
+                    tc::fence_before();
                     tc::fence_proxy_async();
                     tc::mbar_arrive(h_ready + g);
                 } else {
@@ -306,13 +325,15 @@ static cudaError_t launch_mlp_tc_t(const __half* x, int64_t m, const MlpTcArgs& 
         budget = optin - (int)fa.sharedSizeBytes;
         cudaFuncSetAttribute(k_mlp_tc<D, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, budget);
     }
+    constexpr int NS = mlp_slots(D);
     const uint32_t fixed = mlp_tc_fixed_smem(D, H), stage = mlp_tc_stage_smem(D);
     int nst = (int)(((uint32_t)budget - 1024u - fixed) / stage);
-    // a multiple of kSlots, so each stage only ever serves one slot and no barrier waiter can
-    // run more than one phase ahead (parity waits are ambiguous beyond that)
-    nst = nst > kMaxStages ? kMaxStages : nst;
-    nst -= nst % kSlots;
-    if (nst < kSlots) return cudaErrorInvalidConfiguration;
+    // a multiple of the slot count, so each stage only ever serves one slot and no barrier
+    // waiter can run more than one phase ahead (parity waits are ambiguous beyond that);
+    // exactly one stage per slot when the hidden activations alias it
+    nst = nst > (mlp_alias(D) ? NS : 2 * NS) ? (mlp_alias(D) ? NS : 2 * NS) : nst;
+    nst -= nst % NS;
+    if (nst < NS) return cudaErrorInvalidConfiguration;
     MlpTcArgs b = a;
     b.nst = nst;
     const uint32_t smem = fixed + (uint32_t)nst * stage + 1024u;
@@ -321,7 +342,7 @@ static cudaError_t launch_mlp_tc_t(const __half* x, int64_t m, const MlpTcArgs& 
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t tiles = (m + 127) / 128;
     const int grid = (int)(tiles < sms ? tiles : sms);
-    k_mlp_tc<D, H><<<grid, kMlpWarps * 32, smem, s>>>(tm, b);
+    k_mlp_tc<D, H><<<grid, (5 * NS + 1) * 32, smem, s>>>(tm, b);
     return cudaGetLastError();
 }
 

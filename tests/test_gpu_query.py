@@ -326,3 +326,43 @@ def test_atomic_probe_counts_every_reduction():
         assert n >= 1 << 20 and int(tab.double().sum().item()) == n * vec
     with pytest.raises(NbvhError):
         atomic_probe(torch.zeros(3 << 10, device="cuda"), 1, 1 << 10)
+
+
+def _degenerate_rays():
+    """Axis-aligned directions (zero components: 1/d = inf in the slab test), origins inside
+    and outside the geometry, rays starting on a box plane, finite [tmin, tmax] windows that
+    clip the scene, an empty window (tmin > tmax) and a zero-length window."""
+    rng = np.random.default_rng(5)
+    rays = []
+    axes = [(1, 0, 0), (-1, 0, 0), (0, 1, 0), (0, -1, 0), (0, 0, 1), (0, 0, -1), (0.6, 0.8, 0), (0, -0.6, 0.8)]
+    for d in axes:
+        for _ in range(40):
+            o = rng.uniform(-1.6, 1.6, 3)
+            o[np.nonzero(d)[0][0]] = -2.5 * np.sign(d[np.nonzero(d)[0][0]])      # start outside, facing in
+            rays.append([*o, 0.0, *d, np.inf])
+    for _ in range(60):                                                        # inside the sphere shell
+        d = rng.normal(size=3)
+        d /= np.linalg.norm(d)
+        rays.append([*rng.uniform(-0.3, 0.3, 3), 0.0, *d, np.inf])
+    for _ in range(60):                                                        # clipped windows
+        d = rng.normal(size=3)
+        d /= np.linalg.norm(d)
+        o = -3.0 * d + rng.uniform(-0.2, 0.2, 3)
+        t0 = rng.uniform(0.0, 2.5)
+        rays.append([*o, t0, *d, t0 + rng.uniform(0.05, 1.5)])
+    rays.append([0.0, 0.0, 3.0, 2.0, 0.0, 0.0, -1.0, 1.0])                    # tmin > tmax
+    rays.append([0.0, 0.0, 3.0, 2.0, 0.0, 0.0, -1.0, 2.0])                    # zero-length window
+    rays.append([1.0, 0.0, 0.0, 0.0, 0.0, 0.0, 1.0, np.inf])                  # grazing along a plane
+    return np.asarray(rays, np.float32)
+
+
+@pytest.mark.parametrize("list_cap", [1, 16])
+def test_query_degenerate_rays_and_list_extremes(orc, list_cap):
+    """Edge cases of the query path against the oracle (logic replay exact, double oracle
+    within tolerance): zero direction components, clipped / empty ray windows, origins
+    inside the geometry, at the smallest (1) and largest (16) per-ray list capacity."""
+    ctx, sc, tab, layers = _mk_ctx("tiny", list_cap=list_cap)
+    rays = _degenerate_rays()
+    g, o = _check_query(orc, ctx, tab, layers, rays)
+    assert g["hit"][-3] == 0 and g["hit"][-2] == 0                           # empty / zero windows
+    assert g["hit"].sum() > 10 and g["n_queries"].sum() > 300

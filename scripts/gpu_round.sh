@@ -16,9 +16,10 @@ echo "bench exit $?" >> $OUT/bench_$TAG.err
 if [ "${SKIP_NCU:-0}" != "1" ]; then
   CMD="python bench.py --steps 2 --warmup 1 --cpu-seconds 0"
   timeout 600 $CMD > $OUT/ncu_plain.log 2>&1 && \
-  # launch list without the LoD-construction section (thousands of training launches)
+  # launch list without the LoD-construction and path-tracing sections (each trains a model:
+  # thousands of training launches)
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
-      --log-file $OUT/launches_$TAG.csv $CMD --lod 0 > $OUT/ncu_launches.log 2>&1
+      --log-file $OUT/launches_$TAG.csv $CMD --lod 0 --pt 0 > $OUT/ncu_launches.log 2>&1
   echo "ncu launches exit $?" >> $OUT/ncu_launches.log
   # the first (largest) wave and the traversal of the first query
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_query|k_traverse" -s 0 -c 2 \

@@ -1,5 +1,6 @@
 // nbvh_capi.cu — implementation of the C ABI in include/nbvh.h: context and parameter
-// management, scene/cut upload, the query wave driver and the parity hooks.
+// management, scene/cut upload, the query driver (device and chunked host paths) and the
+// parity hooks.
 // The training entry points live in nbvh_train.cu.
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>

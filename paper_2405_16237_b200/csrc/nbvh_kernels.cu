@@ -1,18 +1,19 @@
 // nbvh_kernels.cu — the N-BVH neural ray-query hot path on sm_100a.
 //
-//   k_traverse    Q0+Q1: load rays, traverse the shallow N-BVH of the chosen cut, write
-//                 the (t_enter, id)-ordered leaf list (capacity K) and seed the wave.
-//   k_query_wave  Q2-Q6, fused: for a 128-query tile of active rays, sample the
-//                 current leaf segment, hash-grid encode into shared memory, run the
-//                 MLP on tensor cores, decode, update the per-ray best hit, decide
-//                 front-to-back termination and compact the survivors into the next
-//                 wave's active list with warp-aggregated atomics.
+//   k_traverse    Q0+Q1: load rays, traverse the shallow N-BVH of the chosen cut, write each
+//                 ray's (t_enter, id)-ordered leaf list (capacity K) and append the ray
+//                 (32-byte work record) to the long- or short-ray work list.
+//   k_query       Q2-Q7, one persistent launch: every warp owns 16 ray slots and loops —
+//                 refill empty slots from the work lists, sample the current leaf segment,
+//                 hash-grid encode into shared memory, run the MLP on tensor cores
+//                 (mma.sync), decode, update the best hit, decide front-to-back termination,
+//                 write finished rays' hit records.
 //   k_debug_*     the same device functions with intermediate results exposed.
 //
 // Paper passages: P:103 (front-to-back probing, early termination)
 // (segment sampling, feature concatenation, MLP decode), P:161 (queries per ray =
 // leaves met before a hit), P:201/P:237/P:243 (visibility threshold, local distance,
-// normal, albedo).  Readings C1-C26: DESIGN.md §3.
+// normal, albedo).  Readings C1-C33: DESIGN.md §3.
 #include <cuda_runtime.h>
 
 #include "nbvh_device.cuh"

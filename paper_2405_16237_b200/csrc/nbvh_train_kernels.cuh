@@ -213,7 +213,7 @@ __device__ __forceinline__ float2 unpack_half2(uint32_t v) {
 }
 
 // ------------------------------------------------------------------ T3-T5 forward + loss
-// Same tile structure as the query wave (128 samples, 256 threads): jittered samples,
+// Tile structure: 128 samples per CTA of 256 threads: jittered samples,
 // encode into shared memory, MLP forward with the hidden activations written out for
 // the backward pass, then the gated loss and dL/dz per sample.
 template <int F, int D>

@@ -323,10 +323,10 @@ def run_ours(args):
 
 def bench_train(ctx, args, world, rank):
     """BASELINE cfg 5: training-step throughput on the cfg-2 scene and grid.  Global batch
-    2^20 rays split over the ranks (strong scaling); per step every rank runs
-    nbvh_train_backward on its shard, all-reduces the flat gradient buffer (NCCL, N>1) and
-    applies Adam.  Rays: origins uniform in the 50%-inflated box, uniform directions
-    (P:142); acceptance draws and jitter are inputs (C28)."""
+    2^20 rays split over the ranks (strong scaling); per step every rank draws its shard's
+    rays and random draws on the device (T0, nbvh_gen_train_rays, C28'), runs
+    nbvh_train_backward, all-reduces the flat gradient buffer (NCCL, N>1) and applies Adam.
+    Rays: origins uniform in the 50%-inflated box, uniform directions."""
     import torch
     import torch.distributed as dist
     from paper_2405_16237_b200 import dp
@@ -335,15 +335,20 @@ def bench_train(ctx, args, world, rank):
     cut = ctx.cut(0)
     ctx.set_leaf_rank(np.zeros(cut["n_leaves"], np.float32))
     h = synth.CONFIGS["1080p"]["hash"]
-    batches = []
-    for b in range(2):
-        rays = synth.random_rays(n_global, seed=7000 + b)[sl]
-        u = synth.random_uniform(n_global, seed=7100 + b)[sl]
-        xi = synth.random_uniform(n_global * h.n_points, seed=7200 + b).reshape(n_global, h.n_points)[sl]
-        batches.append(tuple(torch.from_numpy(np.ascontiguousarray(x)).cuda() for x in (rays, u, xi)))
+    # T0 on the device (nbvh_gen_train_rays, Philox-4x32-10, key 7, counter = step): every
+    # step draws fresh rays, acceptance draws and jitter for this rank's shard of the global
+    # batch, inside the timed region
+    box = (-1.5, -1.5, -1.5, 1.5, 1.5, 1.5)
+    n_local = sl.stop - sl.start
+    buf = ctx.gen_train_rays(seed=7, step=0, n=n_local, i0=sl.start, box=box)
+
+    def step(k):
+        ctx.gen_train_rays(seed=7, step=k, n=n_local, i0=sl.start, box=box, out=buf)
+        dp.train_step_dp(ctx, *buf)
+
     stream = torch.cuda.current_stream()
     for i in range(args.warmup):
-        dp.train_step_dp(ctx, *batches[i % 2])
+        step(i)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -351,7 +356,7 @@ def bench_train(ctx, args, world, rank):
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record(stream)
     for i in range(args.steps):
-        dp.train_step_dp(ctx, *batches[i % 2])
+        step(args.warmup + i)
     t1.record(stream)
     torch.cuda.synchronize()
     ms = t0.elapsed_time(t1) / args.steps
@@ -361,7 +366,7 @@ def bench_train(ctx, args, world, rank):
     ms = float(tm.item())
     st = ctx.train_stats()
     ctx.set_profiling(True)
-    dp.train_step_dp(ctx, *batches[0])
+    step(0)
     torch.cuda.synchronize()
     ph = ctx.train_stats()["ms_phase"]
     ctx.set_profiling(False)
@@ -375,7 +380,7 @@ def bench_train(ctx, args, world, rank):
             "global_batch": n_global, "scaling": "strong", "ms_per_step": ms,
             "accepted_per_step_rank0": st["n_accepted"], "first_hit_per_step_rank0": st["n_first_hit"],
             "phase_ms_rank0": ph, "allreduce_bytes": 4 * n_grad if world > 1 else 0,
-            "gpu_launches_per_step": st["n_launches"],
+            "gpu_launches_per_step": st["n_launches"] + 1,          # + the T0 generator
             "bwd_scatter_Gred_v2_per_s": red_rate}
 
 

@@ -234,6 +234,17 @@ nbvh_status nbvh_pt_shade(nbvh_ctx* ctx, const nbvh_ray* d_rays, int64_t n, nbvh
                           const float* sky, float eps, int32_t* d_alive, void* stream);
 
 /* ---------------------------------------------------------------- training (device) */
+/* T0: n training rays and the method's random draws for rays
+ * [i0, i0 + n) of training step `step`, from the counter-based generator Philox-4x32-10
+ * (counter = (global ray index, draw, step lo, step hi), key = seed): origins uniform in the
+ * box (host float[6] lo xyz, hi xyz; NULL: the grid-domain cube of LoD 0 inflated by 50%
+ * about its centre), directions uniform on the sphere (z = 1 - 2U, phi = 2 pi U), tmin 0,
+ * tmax +inf -> d_rays [n]; acceptance draws -> d_u [n]; stratification jitter ->
+ * d_xi [n][n_points] (U = (x >> 8) * 2^-24).  Global indexing makes data-parallel shards
+ * (i0 = shard start) reproduce the single-process batch.  Device pointers; asynchronous.
+ * NBVH_EINVAL on bad arguments or n_points > 4, NBVH_ESTATE if box is NULL and no cut exists. */
+nbvh_status nbvh_gen_train_rays(nbvh_ctx* ctx, uint64_t seed, uint64_t step, int64_t i0, int64_t n,
+                                const float* box, nbvh_ray* d_rays, float* d_u, float* d_xi, void* stream);
 /* Forward + backward of one training batch into the context's
  * fp32 gradient buffer (overwritten): for each ray the first intersected cut leaf of
  * LoD `lod` is accepted with probability max(r_hat/r_hat_max, 0.005) (C18)

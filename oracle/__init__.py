@@ -193,6 +193,26 @@ def query(grid: Grid, n_points, table_fp16, layers, leaf_lo, leaf_hi, rays, mode
     return out
 
 
+def philox4x32_10(ctr, key):
+    """Philox-4x32-10 block (the T0 generator, C28')."""
+    c = np.ascontiguousarray(ctr, np.uint32)
+    k = np.ascontiguousarray(key, np.uint32)
+    out = np.zeros(4, np.uint32)
+    lib().orc_philox4x32_10(_p(c), _p(k), _p(out))
+    return out
+
+
+def gen_train_rays(seed, step, i0, n, box, n_points):
+    """T0 training rays + draws (rays [n, 8], u [n], xi [n, n_points]) per C28'."""
+    rays = np.zeros((n, 8), np.float32)
+    u = np.zeros(n, np.float32)
+    xi = np.zeros((n, max(n_points, 1)), np.float32)
+    bx = np.ascontiguousarray(np.asarray(box, np.float32).reshape(6))
+    lib().orc_gen_train_rays(C.c_uint64(seed), C.c_uint64(step), C.c_int64(i0), C.c_int64(n), _p(bx),
+                             C.c_int32(n_points), _p(rays), _p(u), _p(xi))
+    return rays, u, xi[:, :n_points]
+
+
 def sigmoid_f32(z: float) -> float:
     """The decode's fp32 sigmoid (C27), as the logic replay evaluates it."""
     return float(lib().orc_sigmoid_f32(C.c_float(z)))

@@ -859,3 +859,59 @@ int32_t orc_num_threads(void) {
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------ T0 training rays (C28')
+// Philox-4x32-10 (Salmon, Moraes, Dror, Shaw, "Parallel random numbers: as easy as 1, 2, 3",
+// SC'11): 10 rounds of (hi, lo) = M * c on words 0 and 2 with the key added by xor, the key
+// bumped by the Weyl constants between rounds.  Pinned by the published known-answer vectors.
+extern "C" void orc_philox4x32_10(const uint32_t* ctr_in, const uint32_t* key_in, uint32_t* out) {
+    uint32_t c[4] = {ctr_in[0], ctr_in[1], ctr_in[2], ctr_in[3]};
+    uint32_t k[2] = {key_in[0], key_in[1]};
+    for (int r = 0; r < 10; ++r) {
+        if (r > 0) {
+            k[0] += 0x9E3779B9u;
+            k[1] += 0xBB67AE85u;
+        }
+        const uint64_t p0 = (uint64_t)0xD2511F53u * c[0];
+        const uint64_t p1 = (uint64_t)0xCD9E8D57u * c[2];
+        const uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+        const uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+        const uint32_t n[4] = {hi1 ^ c[1] ^ k[0], lo1, hi0 ^ c[3] ^ k[1], lo0};
+        for (int j = 0; j < 4; ++j) c[j] = n[j];
+    }
+    for (int j = 0; j < 4; ++j) out[j] = c[j];
+}
+
+// The training-ray recipe of DESIGN.md C28' (the device generator nbvh_gen_train_rays follows
+// the same recipe; the two share no code): ray i of step s draws Philox(i, d, s_lo, s_hi; seed)
+// for d = 0 (origin xyz, acceptance u), 1 (direction), 2 (jitter); U = (x >> 8) * 2^-24;
+// origin = lo + (hi - lo) U; z = 1 - 2U, r = sqrt(max(0, 1 - z^2)), phi = 2 pi U,
+// d = (r cos phi, r sin phi, z); tmin 0, tmax inf.  cos / sin are not correctly rounded on
+// either side, so the GPU's direction x, y agree to a few ulp (everything else bit-exact).
+extern "C" void orc_gen_train_rays(uint64_t seed, uint64_t step, int64_t i0, int64_t n, const float* box,
+                                   int32_t n_points, float* rays, float* u, float* xi) {
+    const uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    auto U = [](uint32_t x) { return (float)(x >> 8) * 5.9604644775390625e-8f; };
+    for (int64_t j = 0; j < n; ++j) {
+        const uint32_t i = (uint32_t)(i0 + j);
+        uint32_t p0[4], p1[4], p2[4];
+        const uint32_t c0[4] = {i, 0u, (uint32_t)step, (uint32_t)(step >> 32)};
+        const uint32_t c1[4] = {i, 1u, (uint32_t)step, (uint32_t)(step >> 32)};
+        const uint32_t c2[4] = {i, 2u, (uint32_t)step, (uint32_t)(step >> 32)};
+        orc_philox4x32_10(c0, key, p0);
+        orc_philox4x32_10(c1, key, p1);
+        orc_philox4x32_10(c2, key, p2);
+        float* r = rays + 8 * j;
+        for (int k = 0; k < 3; ++k) r[k] = box[k] + (box[3 + k] - box[k]) * U(p0[k]);
+        r[3] = 0.0f;
+        const float z = 1.0f - 2.0f * U(p1[0]);
+        const float rr = std::sqrt(std::fmax(0.0f, 1.0f - z * z));
+        const float phi = 6.28318530717958647692f * U(p1[1]);
+        r[4] = rr * std::cos(phi);
+        r[5] = rr * std::sin(phi);
+        r[6] = z;
+        r[7] = std::numeric_limits<float>::infinity();
+        u[j] = U(p0[3]);
+        for (int k = 0; k < n_points; ++k) xi[j * n_points + k] = U(p2[k]);
+    }
+}

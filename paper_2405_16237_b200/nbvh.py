@@ -80,6 +80,7 @@ SIGNATURES = {
     "nbvh_get_train_stats": (C.c_int, [_P, _P]),
     "nbvh_set_leaf_rank": (C.c_int, [_P, _I32, _P]),
     "nbvh_mlp_forward": (C.c_int, [_P, _P, _I64, _P, _P]),
+    "nbvh_gen_train_rays": (C.c_int, [_P, C.c_uint64, C.c_uint64, _I64, _I64, _P, _P, _P, _P, _P]),
     "nbvh_intersect_mesh": (C.c_int, [_P, _P, _I64, Hits, _P]),
     "nbvh_gather_probe": (C.c_int, [_P, _I64, _I32, _I64, C.c_uint32, _P, _I64, _P, _P]),
     "nbvh_atomic_probe": (C.c_int, [_P, _I64, _I32, _I64, C.c_uint32, _P, _P]),
@@ -280,6 +281,19 @@ class Context:
         if out is None:
             out = self.alloc_hits(n, rays.device)
         self._ck(self.lib.nbvh_query(self.h, _ptr(rays), n, lod, self._hits(out), _stream_ptr(stream)), "query")
+        return out
+
+    def gen_train_rays(self, seed: int, step: int, n: int, i0: int = 0, box=None, out=None, stream=None):
+        """nbvh_gen_train_rays: (rays [n, 8], u [n], xi [n, n_points]) device tensors for rays
+        [i0, i0 + n) of training step `step` (Philox-4x32-10, key = seed)."""
+        import torch
+        if out is None:
+            out = (torch.empty(n, 8, device=f"cuda:{self.device}"), torch.empty(n, device=f"cuda:{self.device}"),
+                   torch.empty(n, self.cfg.n_points, device=f"cuda:{self.device}"))
+        bx = None if box is None else np.ascontiguousarray(np.asarray(box, np.float32).reshape(6))
+        self._ck(self.lib.nbvh_gen_train_rays(self.h, int(seed), int(step), int(i0), int(n), _ptr(bx),
+                                              _ptr(out[0]), _ptr(out[1]), _ptr(out[2]), _stream_ptr(stream)),
+                 "gen_train_rays")
         return out
 
     def mlp_forward(self, x, z=None, stream=None):

@@ -213,3 +213,32 @@ def test_training_reduces_loss():
         st = ctx.train_stats()
         losses.append(st["loss_sum"] / max(1, st["n_accepted"]))
     assert np.mean(losses[-10:]) < 0.6 * np.mean(losses[:5]), (losses[:5], losses[-10:])
+
+
+def test_t0_generated_rays_match_oracle():
+    """nbvh_gen_train_rays (T0, Philox-4x32-10 on the device) against the oracle's own Philox
+    and recipe (C28'): origins, z, u, xi, tmin, tmax bit-exact; the direction's x, y within a
+    few ulp (cos / sin); a data-parallel shard equals the slice of the whole batch; the
+    default box is the domain cube inflated by 50%."""
+    import oracle as orc
+    from paper_2405_16237_b200 import Context
+    sc = synth.scene_tiny()
+    ctx = Context(device=0, L=8, F=2, log2_T=14, n_points=4, hidden_layers=2)
+    ctx.set_mesh(sc)
+    ctx.build_cut(16)
+    n = 100000
+    box = (-1.5, -1.25, -1.0, 1.5, 1.25, 1.0)
+    rays, u, xi = (t.cpu().numpy() for t in ctx.gen_train_rays(seed=7, step=5, n=n, box=box))
+    wr, wu, wxi = orc.gen_train_rays(7, 5, 0, n, box, 4)
+    assert np.array_equal(rays[:, [0, 1, 2, 3, 6, 7]].view(np.uint32), wr[:, [0, 1, 2, 3, 6, 7]].view(np.uint32))
+    assert np.array_equal(u.view(np.uint32), wu.view(np.uint32)) and np.array_equal(xi.view(np.uint32), wxi.view(np.uint32))
+    assert np.abs(rays[:, 4:6] - wr[:, 4:6]).max() <= 4e-7
+    r2, u2, x2 = (t.cpu().numpy() for t in ctx.gen_train_rays(seed=7, step=5, n=777, i0=4321, box=box))
+    assert np.array_equal(r2, rays[4321:4321 + 777]) and np.array_equal(u2, u[4321:4321 + 777])
+    rd, _, _ = (t.cpu().numpy() for t in ctx.gen_train_rays(seed=7, step=5, n=20000))
+    b = orc.scene_box(sc).astype(np.float64)
+    side = (b[3:] - b[:3]).max()
+    mid = (b[:3] + b[3:]) / 2
+    lo, hi = mid - 0.75 * side, mid + 0.75 * side
+    assert np.all(rd[:, :3] >= lo - 1e-5) and np.all(rd[:, :3] <= hi + 1e-5)
+    assert np.all(rd[:, :3].min(0) < lo + 0.05 * side) and np.all(rd[:, :3].max(0) > hi - 0.05 * side)

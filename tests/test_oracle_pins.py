@@ -556,3 +556,32 @@ def test_c27_sigmoid_f32_vs_exact(orc):
     assert np.all(np.diff(got[inner]) >= 0)
     for z in (0.25, 1.0, 3.5, 9.0):
         assert abs(orc.sigmoid_f32(-z) - (1.0 - orc.sigmoid_f32(z))) <= 2 ** -23
+
+
+# ------------------------------------------------------------------ T0 Philox-4x32-10 (C28')
+def test_t0_philox_known_answer_vectors(orc):
+    """Philox-4x32-10 against the published known-answer vectors (Random123 kat_vectors)."""
+    kat = [((0, 0, 0, 0), (0, 0), (0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8)),
+           ((0xFFFFFFFF,) * 4, (0xFFFFFFFF,) * 2, (0x408F276D, 0x41C83B0E, 0xA20BC7C6, 0x6D5451FD)),
+           ((0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344), (0xA4093822, 0x299F31D0),
+            (0xD16CFE09, 0x94FDCCEB, 0x5001E420, 0x24126EA1))]
+    for ctr, key, want in kat:
+        assert tuple(int(x) for x in orc.philox4x32_10(ctr, key)) == want
+
+
+def test_t0_training_rays_distribution(orc):
+    """The T0 recipe: origins inside the box, unit directions, U in [0,1); moments of a large
+    batch match the uniform / isotropic closed forms (mean 1/2, E[d] = 0, E[d_z^2] = 1/3);
+    shards (i0) reproduce the whole batch; the step changes every draw."""
+    box = (-1.5, -1.5, -1.5, 1.5, 1.5, 1.5)
+    rays, u, xi = orc.gen_train_rays(7, 3, 0, 200000, box, 4)
+    assert np.all(rays[:, :3] >= -1.5) and np.all(rays[:, :3] < 1.5)
+    assert np.allclose(np.linalg.norm(rays[:, 4:7], axis=1), 1.0, atol=1e-6)
+    assert np.all((u >= 0) & (u < 1)) and np.all((xi >= 0) & (xi < 1))
+    assert abs(u.mean() - 0.5) < 5e-3 and abs(xi.mean() - 0.5) < 5e-3
+    assert np.all(np.abs(rays[:, 4:7].mean(0)) < 1e-2) and abs((rays[:, 6] ** 2).mean() - 1 / 3) < 5e-3
+    assert abs(rays[:, :3].mean()) < 1e-2
+    r2, u2, x2 = orc.gen_train_rays(7, 3, 1000, 500, box, 4)
+    assert np.array_equal(r2, rays[1000:1500]) and np.array_equal(u2, u[1000:1500]) and np.array_equal(x2, xi[1000:1500])
+    r3, u3, _ = orc.gen_train_rays(7, 4, 0, 1000, box, 4)
+    assert np.mean(u3 == u[:1000]) < 0.01

@@ -92,6 +92,34 @@ def test_loss_and_gradients_vs_oracle(batch):
     assert abs(per_leaf[:, 0].sum() - o["loss_sum"][0]) <= 5e-3 * o["loss_sum"][0]
 
 
+def test_table_gradient_support_matches_oracle(batch):
+    """S:249 (gradient sparsity): the table entries with a non-zero gradient are exactly the
+    corners the accepted samples touched (the oracle's support); an index error anywhere in
+    the scatter (wrong level offset, corner, hash term) changes the set."""
+    from paper_2405_16237_b200 import dp
+    ctx, sc, cut, tab, layers, rays, u, xi, o = batch
+    ctx.train_backward(_to(rays), _to(u), _to(xi))
+    g = dp.grad_tensor(ctx).cpu().numpy()[:tab.size].reshape(-1, 2)
+    gs = np.any(g != 0, axis=1)
+    os_ = np.any(o["g_table"].reshape(-1, 2) != 0, axis=1)
+    assert os_.sum() > 1000
+    assert (gs & ~os_).sum() == 0                                   # nothing outside the support
+    assert (os_ & ~gs).sum() <= max(3, int(1e-3 * os_.sum()))       # fp cancellation to exactly 0 only
+
+
+def test_query_bitwise_deterministic():
+    """S:299 / S:670: the query path is bitwise reproducible run to run (no value depends on
+    atomics order or scheduling)."""
+    from paper_2405_16237_b200 import Context
+    ctx, sc, cut, tab, layers, rays, u, xi, o = _setup(n_rays=20000, seed=60)
+    d_rays = _to(rays)
+    a = {k: v.clone() for k, v in ctx.query(d_rays).items()}
+    for _ in range(3):
+        b = ctx.query(d_rays)
+        for k in a:
+            assert torch.equal(a[k], b[k]), k
+
+
 @pytest.mark.parametrize("hidden", [2, 3])
 @pytest.mark.parametrize("path", ["tcgen05", "mma_sync"])
 def test_weight_gradients_per_layer(hidden, path, monkeypatch):

@@ -16,8 +16,11 @@
 // normal, albedo).  Readings C1-C33: DESIGN.md §3.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "nbvh_device.cuh"
 #include "nbvh_launch.h"
+#include "nbvh_tcgen05.cuh"
 
 namespace nbvh {
 
@@ -241,16 +244,39 @@ __host__ __device__ constexpr size_t align16(size_t b) { return (b + 15) & ~(siz
 
 // Shared-memory plan of k_query (bytes), shared by the kernel and its launcher: the MLP
 // weights and level table once per CTA, then one private region per warp.
+//   kTc = false: weights [out][in] padded for ldmatrix, per-warp feature rows [16][D+8];
+//   kTc = true:  weights in the K-major canonical (core-matrix) layout with bias columns, a
+//                ones tile for the bias K-steps, two group tiles [max(D/8, 8) K-groups][128
+//                rows][16 B] (features, then hidden activations), mbarriers / TMEM slot /
+//                group votes; no per-warp feature rows.
+constexpr int kGroupWarps = 8;                                  // kTc: warps per 128-row MLP group
+constexpr int kKgHid = 64 / 8 + 2;                              // K-groups of a hidden W (+ bias)
+__host__ __device__ constexpr int tc_tile_kg(int d_in) { return d_in / 8 > 8 ? d_in / 8 : 8; }
+
 struct QuerySmemPlan {
-    size_t w, bias, lv, warp0, feat, z, xs, slots, per_warp, total;
+    size_t w, bias, lv, misc, gtile, warp0, feat, z, xs, slots, per_warp, total;
+    size_t w0, wh, wo, ones;                                    // kTc weight regions (absolute)
     int warps;
-    __host__ __device__ QuerySmemPlan(int d_in, int hidden, int n_points) {
+    __host__ __device__ QuerySmemPlan(int d_in, int hidden, int n_points, bool tc = false) {
         w = 0;
-        bias = w + align16((size_t)mlp_smem_halves(d_in, hidden) * 2);
-        lv = bias + align16((size_t)(64 * hidden + 8) * 4);
-        warp0 = lv + align16(sizeof(LevelSm) * kMaxLevels);
+        if (!tc) {
+            bias = w + align16((size_t)mlp_smem_halves(d_in, hidden) * 2);
+            lv = bias + align16((size_t)(64 * hidden + 8) * 4);
+            misc = gtile = w0 = wh = wo = ones = 0;
+            warp0 = lv + align16(sizeof(LevelSm) * kMaxLevels);
+        } else {
+            w0 = w;
+            wh = w0 + (size_t)64 * (d_in / 8 + 2) * 16;
+            wo = wh + (size_t)(hidden - 1) * 64 * kKgHid * 16;
+            ones = wo + (size_t)16 * kKgHid * 16;
+            lv = ones + 2 * 128 * 16;
+            misc = lv + align16(sizeof(LevelSm) * kMaxLevels);   // [0,16) 2 mbarriers, [16,20) TMEM
+            gtile = misc + 256;                                   // slot, [32,160) group votes
+            bias = 0;
+            warp0 = gtile + (size_t)2 * tc_tile_kg(d_in) * 2048;
+        }
         feat = 0;                                                   // offsets within a warp region
-        z = feat + align16((size_t)kWarpQ * (d_in + 8) * 2);
+        z = feat + (tc ? 0 : align16((size_t)kWarpQ * (d_in + 8) * 2));
         xs = z + align16((size_t)kWarpQ * 8 * 4);
         slots = xs + align16((size_t)kWarpQ * n_points * 3 * 4);
         per_warp = slots + align16(sizeof(WarpSlots));
@@ -258,9 +284,84 @@ struct QuerySmemPlan {
         const size_t cap = 227 * 1024;
         warps = warp0 + per_warp > cap ? 0 : (int)((cap - warp0) / per_warp);
         if (warps > kQueryWarps) warps = kQueryWarps;
+        if (tc && warps < kQueryWarps) warps = 0;                   // kTc needs both 8-warp groups
         total = warp0 + per_warp * warps;
     }
 };
+
+// kTc: the decoder MLP of one 8-warp group's 128 rows on tcgen05 (M = 128, N = 64 / 16, fp32
+// accumulators in the group's 64 TMEM columns).  Every warp of the group calls it; warp 0 of
+// the group issues the MMAs (one elected lane), every warp converts 32 accumulator columns
+// of 32 rows (TMEM lane quarter wg % 4, column half wg / 4) into the next layer's fp16 A
+// tile, and the output layer's 8 columns are written into the owning warps' z rows.
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+template <int D>
+__device__ __forceinline__ void mlp_group_tc(int g, int wg, int lane, int hidden, uint32_t acc, unsigned char* gt,
+                                             uint32_t a_w0, uint32_t a_wh, uint32_t a_wo, uint32_t a_ones,
+                                             uint64_t* bar, uint32_t& phase, unsigned char* zbase, size_t per_warp,
+                                             size_t zoff) {
+    constexpr uint32_t id64 = tc::idesc_f16(128, 64, false, false);
+    constexpr uint32_t id16 = tc::idesc_f16(128, 16, false, false);
+    const uint64_t dA = tc::smem_desc(tc::smem_u32(gt), 2048, 128);
+    const uint64_t dOnes = tc::smem_desc(a_ones, 2048, 128);
+    const uint64_t dW0 = tc::smem_desc(a_w0, 1024, 128);
+    const uint64_t dWh = tc::smem_desc(a_wh, 1024, 128);
+    const uint64_t dWo = tc::smem_desc(a_wo, 256, 128);
+    const int q = wg & 3, half = wg >> 2;
+    const int row = 32 * q + lane;
+    tc::fence_proxy_async();                  // feature rows (generic) -> tensor core (async proxy)
+    named_bar(1 + g, kGroupWarps * 32);
+    if (wg == 0) {
+        tc::fence_after();
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) tc::mma_f16_elect(acc, dA + kk * 256, dW0 + kk * 128, id64, kk > 0);
+        tc::mma_f16_elect(acc, dOnes, dW0 + (D / 16) * 128, id64, 1);                  // bias
+        tc::commit_elect(bar);
+    }
+    for (int l = 0; l <= hidden; ++l) {
+        tc::mbar_wait(bar, phase);
+        phase ^= 1u;
+        tc::fence_after();
+        if (l < hidden) {
+            float v[32];
+            tc::ld32(acc, (uint32_t)(q * 32), (uint32_t)(32 * half), v);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                uint4 o;
+                o.x = pack_relu_half2(v[8 * k], v[8 * k + 1]);
+                o.y = pack_relu_half2(v[8 * k + 2], v[8 * k + 3]);
+                o.z = pack_relu_half2(v[8 * k + 4], v[8 * k + 5]);
+                o.w = pack_relu_half2(v[8 * k + 6], v[8 * k + 7]);
+                *reinterpret_cast<uint4*>(gt + (4 * half + k) * 2048 + row * 16) = o;
+            }
+            tc::fence_before();
+            tc::fence_proxy_async();
+            named_bar(1 + g, kGroupWarps * 32);
+            if (wg == 0) {
+                tc::fence_after();
+                const bool out = l + 1 == hidden;
+                const uint64_t dW = out ? dWo : dWh + (uint64_t)(l * 64 * kKgHid);
+                const uint32_t kg_units = out ? 16 : 64, id = out ? id16 : id64;   // K-group stride / 16 B
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk)
+                    tc::mma_f16_elect(acc, dA + kk * 256, dW + kk * 2 * kg_units, id, kk > 0);
+                tc::mma_f16_elect(acc, dOnes, dW + 8 * kg_units, id, 1);                    // bias
+                tc::commit_elect(bar);
+            }
+        } else {
+            if (half == 0) {
+                float v[16];
+                tc::ld16(acc, (uint32_t)(q * 32), 0u, v);
+                float* z = reinterpret_cast<float*>(zbase + per_warp * (size_t)(row >> 4) + zoff) + (row & 15) * 8;
+                reinterpret_cast<float4*>(z)[0] = make_float4(v[0], v[1], v[2], v[3]);
+                reinterpret_cast<float4*>(z)[1] = make_float4(v[4], v[5], v[6], v[7]);
+            }
+            tc::fence_before();
+            named_bar(1 + g, kGroupWarps * 32);   // z visible to the owning warps; accumulator free
+        }
+    }
+}
 
 // One launch processes every ray that intersects the cut (Q2-Q7).
 // Each warp owns kWarpQ ray slots and runs its own loop with no block-wide barrier:
@@ -271,12 +372,12 @@ struct QuerySmemPlan {
 // update the best hit, decide front-to-back termination and free finished slots after
 // writing the hit record.  Warps drift freely, so one warp's MLP or list refill overlaps
 // other warps' gathers.
-template <int F, int D>
+template <int F, int D, bool kTc>
 __global__ void __launch_bounds__(kQueryWarps * 32, 1) k_query(QueryArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int NP = a.g.n_points;
-    const QuerySmemPlan plan(D, a.m.hidden, NP);
+    const QuerySmemPlan plan(D, a.m.hidden, NP, kTc);
     MlpSmem ms;
     ms.w0 = reinterpret_cast<__half*>(smem_raw + plan.w);
     ms.wh = ms.w0 + 64 * (D + 8);
@@ -284,15 +385,65 @@ __global__ void __launch_bounds__(kQueryWarps * 32, 1) k_query(QueryArgs a) {
     ms.b = reinterpret_cast<float*>(smem_raw + plan.bias);
     LevelSm* lv = reinterpret_cast<LevelSm*>(smem_raw + plan.lv);
     unsigned char* wbase = smem_raw + plan.warp0 + plan.per_warp * warp;
-    __half* feat = reinterpret_cast<__half*>(wbase + plan.feat);              // [kWarpQ][D+8]
+    __half* feat = reinterpret_cast<__half*>(wbase + plan.feat);              // [kWarpQ][D+8] (!kTc)
     float* zt = reinterpret_cast<float*>(wbase + plan.z);                     // [kWarpQ][8]
     float* xs = reinterpret_cast<float*>(wbase + plan.xs);                    // [NP*3][kWarpQ]
     WarpSlots& S = *reinterpret_cast<WarpSlots*>(wbase + plan.slots);
+    // kTc: 8-warp groups, group tile, mbarrier, TMEM columns
+    const int grp = warp / kGroupWarps, wg = warp % kGroupWarps;
+    unsigned char* gt = smem_raw + plan.gtile + (size_t)grp * tc_tile_kg(D) * 2048;
+    uint64_t* gbar = reinterpret_cast<uint64_t*>(smem_raw + plan.misc) + grp;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw + plan.misc + 16);
+    int* gvote = reinterpret_cast<int*>(smem_raw + plan.misc + 32);           // [2 parities][2 groups][8]
+    uint32_t gphase = 0;
 
-    stage_mlp(a.m, ms, tid, blockDim.x);
+    if constexpr (kTc) {
+        // weights in the K-major canonical layout (element (n, k) of W [N][K] at
+        // (k/8) * (Npad*16) + n*16 + (k%8)*2), the bias as two extra K columns (hi + lo fp16)
+        auto stage_w = [&](unsigned char* dst, const __half* src, const float* bias, int N, int K, int Npad) {
+            const int kg = K / 8 + 2;
+            for (int i = tid; i < Npad * kg; i += blockDim.x) {
+                const int n = i / kg, gk = i % kg;
+                uint4 v = make_uint4(0, 0, 0, 0);
+                if (n < N) {
+                    if (gk < K / 8) {
+                        v = *reinterpret_cast<const uint4*>(src + (int64_t)n * K + gk * 8);
+                    } else if (gk == K / 8) {
+                        const __half hi = __float2half_rn(bias[n]);
+                        const __half lo = __float2half_rn(bias[n] - __half2float(hi));
+                        v.x = (uint32_t)__half_as_ushort(hi) | ((uint32_t)__half_as_ushort(lo) << 16);
+                    }
+                }
+                *reinterpret_cast<uint4*>(dst + gk * (Npad * 16) + n * 16) = v;
+            }
+        };
+        const int H = a.m.hidden;
+        stage_w(smem_raw + plan.w0, a.m.W, a.m.b, 64, D, 64);
+        for (int l = 0; l < H - 1; ++l)
+            stage_w(smem_raw + plan.wh + (size_t)l * 64 * kKgHid * 16, a.m.W + 64 * D + (int64_t)l * 64 * 64,
+                    a.m.b + 64 * (l + 1), 64, 64, 64);
+        stage_w(smem_raw + plan.wo, a.m.W + 64 * D + (int64_t)(H - 1) * 64 * 64, a.m.b + 64 * H, 8, 64, 16);
+        for (int i = tid; i < 128; i += blockDim.x) {                      // bias K-step A columns
+            *reinterpret_cast<uint4*>(smem_raw + plan.ones + i * 16) = make_uint4(0x3C003C00u, 0u, 0u, 0u);
+            *reinterpret_cast<uint4*>(smem_raw + plan.ones + 2048 + i * 16) = make_uint4(0u, 0u, 0u, 0u);
+        }
+        if (tid < 2 * 2 * kGroupWarps) gvote[tid] = 1;
+        if (tid == 0) {
+            tc::mbar_init(reinterpret_cast<uint64_t*>(smem_raw + plan.misc), 1);
+            tc::mbar_init(reinterpret_cast<uint64_t*>(smem_raw + plan.misc) + 1, 1);
+            tc::fence_barrier_init();
+        }
+        if (warp == 0) tc::tmem_alloc<128>(tmem_slot);
+        tc::fence_proxy_async();
+        tc::fence_before();
+    } else {
+        stage_mlp(a.m, ms, tid, blockDim.x);
+    }
     stage_levels(a.g, lv, tid);
     if (lane < kWarpQ) S.ray[lane] = -1;
-    __syncthreads();                          // the only block-wide barrier
+    __syncthreads();                          // the only block-wide barrier (kTc: + group barriers)
+    if constexpr (kTc) tc::fence_after();
+    const uint32_t tmem_acc = kTc ? *tmem_slot + (uint32_t)(grp * 64) : 0u;
 
     const int n_long = *a.cnt_long;           // long rays first (k_traverse), then the rest
     const int total = n_long + *a.cnt;        // rays with >= 1 intersected leaf
@@ -337,7 +488,19 @@ __global__ void __launch_bounds__(kQueryWarps * 32, 1) k_query(QueryArgs a) {
         const bool occ = lane < kWarpQ && S.ray[lane] >= 0;
         const unsigned om = __ballot_sync(0xffffffffu, occ);
         const int nv = __popc(om);
-        if (nv == 0) break;                   // work list drained and every slot finished
+        if constexpr (kTc) {
+            // the 8 warps of a group run the MLP together: the group leaves the loop once
+            // every one of its warps is drained (a drained warp keeps joining with no rows)
+            int* vote = gvote + ((iters & 1) * 2 + grp) * kGroupWarps;
+            if (lane == 0) vote[wg] = nv;
+            named_bar(1 + grp, kGroupWarps * 32);
+            int any = 0;
+#pragma unroll
+            for (int k = 0; k < kGroupWarps; ++k) any |= vote[k];
+            if (!any) break;
+        } else {
+            if (nv == 0) break;               // work list drained and every slot finished
+        }
         ++iters;
         my_queries += (unsigned long long)nv;
         if (occ) {
@@ -372,16 +535,28 @@ __global__ void __launch_bounds__(kQueryWarps * 32, 1) k_query(QueryArgs a) {
                     const float x0 = xp[q], x1 = xp[kWarpQ + q], x2 = xp[2 * kWarpQ + q];
                     for (int lc = 0; lc < cpp; ++lc) {
                         const int c = p * cpp + lc;
-                        *reinterpret_cast<uint4*>(feat + q * (D + 8) + c * 8) =
-                            encode_chunk_sm<F>(lv, tab, hmask, x0, x1, x2, lc * (8 / F), nullptr);
+                        const uint4 f = encode_chunk_sm<F>(lv, tab, hmask, x0, x1, x2, lc * (8 / F), nullptr);
+                        if constexpr (kTc)
+                            *reinterpret_cast<uint4*>(gt + c * 2048 + (16 * wg + q) * 16) = f;
+                        else
+                            *reinterpret_cast<uint4*>(feat + q * (D + 8) + c * 8) = f;
                     }
                 }
             }
         }
         __syncwarp();
-        // (E) MLP on tensor cores: the warp's rows in m16 blocks (rows >= nv are ignored)
-        mlp_rows16<D>(ms, a.m.hidden, feat, 0, zt, lane);
-        if (kWarpQ > 16 && nv > 16) mlp_rows16<D>(ms, a.m.hidden, feat, 16, zt, lane);
+        // (E) MLP on tensor cores: the warp's rows in m16 blocks (rows >= nv are ignored); kTc:
+        //     the group's 128 rows on tcgen05
+        if constexpr (kTc) {
+            mlp_group_tc<D>(grp, wg, lane, a.m.hidden, tmem_acc, gt, tc::smem_u32(smem_raw + plan.w0),
+                            tc::smem_u32(smem_raw + plan.wh), tc::smem_u32(smem_raw + plan.wo),
+                            tc::smem_u32(smem_raw + plan.ones), gbar, gphase,
+                            smem_raw + plan.warp0 + plan.per_warp * (size_t)(grp * kGroupWarps), plan.per_warp,
+                            plan.z);
+        } else {
+            mlp_rows16<D>(ms, a.m.hidden, feat, 0, zt, lane);
+            if (kWarpQ > 16 && nv > 16) mlp_rows16<D>(ms, a.m.hidden, feat, 16, zt, lane);
+        }
         __syncwarp();
         // (F) decode, best hit, front-to-back termination
         if (lane < nv) {
@@ -469,6 +644,11 @@ __global__ void __launch_bounds__(kQueryWarps * 32, 1) k_query(QueryArgs a) {
         atomicAdd(&a.ctr->n_queries, my_queries);
         atomicMax(&a.ctr->max_iter, iters);
     }
+    if constexpr (kTc) {
+        tc::fence_before();
+        __syncthreads();
+        if (warp == 0) tc::tmem_free<128>(*tmem_slot);
+    }
 }
 
 // ------------------------------------------------------------------ debug: encode points
@@ -545,20 +725,41 @@ static int resident_blocks(Kern k, int threads, size_t smem) {
 }
 
 // Persistent grid: one CTA of kQueryWarps warps per SM.
-template <int F, int D>
-static cudaError_t launch_query_t(const QueryArgs& a, int64_t max_work, cudaStream_t s) {
-    const QuerySmemPlan plan(D, a.m.hidden, a.g.n_points);
-    if (plan.warps < 1) return cudaErrorInvalidValue;
+// The MLP of k_query: the per-warp mma.sync MLP by default; NBVH_QUERY_MLP=tc selects the
+// 8-warp-group tcgen05 MLP (parity-tested, but 1451 vs 1648 Mrays/s on the 1080p frame:
+// every warp of a group waits through the group's 4-layer MMA/epilogue chain, which costs
+// more per iteration than a warp's own mma.sync chain in this latency-bound kernel).  Read
+// per launch so tests can switch it.
+static bool query_mlp_tc() {
+    const char* ev = std::getenv("NBVH_QUERY_MLP");
+    return ev && ev[0] == 't';
+}
+
+template <int F, int D, bool kTc>
+static cudaError_t launch_query_tt(const QueryArgs& a, int64_t max_work, cudaStream_t s, const QuerySmemPlan& plan) {
     const size_t smem = plan.total;
     // occupancy is queried once per (hidden, n_points) shape
     static int cached[kMaxHidden + 1][9] = {};
     int& grid_c = cached[a.m.hidden][a.g.n_points < 9 ? a.g.n_points : 8];
-    if (!grid_c) grid_c = resident_blocks(k_query<F, D>, plan.warps * 32, smem);
+    if (!grid_c) grid_c = resident_blocks(k_query<F, D, kTc>, plan.warps * 32, smem);
     int grid = grid_c;
-    const int64_t need = (max_work + plan.warps * kWarpQ - 1) / (plan.warps * kWarpQ);
-    if (need < grid) grid = (int)(need > 0 ? need : 1);
-    k_query<F, D><<<grid, plan.warps * 32, smem, s>>>(a);
+    if (!kTc) {                               // kTc: every CTA needs both groups, keep the full grid
+        const int64_t need = (max_work + plan.warps * kWarpQ - 1) / (plan.warps * kWarpQ);
+        if (need < grid) grid = (int)(need > 0 ? need : 1);
+    }
+    k_query<F, D, kTc><<<grid, plan.warps * 32, smem, s>>>(a);
     return cudaGetLastError();
+}
+
+template <int F, int D>
+static cudaError_t launch_query_t(const QueryArgs& a, int64_t max_work, cudaStream_t s) {
+    if (query_mlp_tc()) {
+        const QuerySmemPlan tp(D, a.m.hidden, a.g.n_points, true);
+        if (tp.warps == kQueryWarps) return launch_query_tt<F, D, true>(a, max_work, s, tp);
+    }
+    const QuerySmemPlan plan(D, a.m.hidden, a.g.n_points);
+    if (plan.warps < 1) return cudaErrorInvalidValue;
+    return launch_query_tt<F, D, false>(a, max_work, s, plan);
 }
 
 cudaError_t launch_query(const QueryArgs& a, int64_t max_work, cudaStream_t s) {

@@ -366,3 +366,24 @@ def test_query_degenerate_rays_and_list_extremes(orc, list_cap):
     g, o = _check_query(orc, ctx, tab, layers, rays)
     assert g["hit"][-3] == 0 and g["hit"][-2] == 0                           # empty / zero windows
     assert g["hit"].sum() > 10 and g["n_queries"].sum() > 300
+
+
+def test_query_tcgen05_group_mlp_variant(orc, monkeypatch):
+    """NBVH_QUERY_MLP=tc: k_query with the decoder MLP of each 8-warp group's 128 rows on
+    tcgen05 (TMEM accumulators, group barriers) instead of per-warp mma.sync — same parity
+    checks (logic replay exact, double oracle within tolerance) on the tiny scene, and the
+    1080p frame at full size against the default variant (identical decisions on decided rays)."""
+    monkeypatch.setenv("NBVH_QUERY_MLP", "tc")
+    ctx, sc, tab, layers = _mk_ctx("tiny")
+    _check_query(orc, ctx, tab, layers, _rays_tiny())
+    ctx2, sc2, tab2, layers2 = _mk_ctx("1080p", table_seed=9, seed=6, list_cap=12)
+    c = synth.CONFIGS["1080p"]
+    rays = torch.from_numpy(synth.camera_rays(*c["res"], c["eye"], vfov_deg=c["vfov"])).cuda()
+    ctx2.reserve(rays.shape[0])
+    t = {k: v.cpu().numpy() for k, v in ctx2.query(rays).items()}
+    monkeypatch.setenv("NBVH_QUERY_MLP", "mma")
+    m = {k: v.cpu().numpy() for k, v in ctx2.query(rays).items()}
+    # the two MLPs differ only in fp32 summation order: decisions flip on a few near-tie rays
+    assert (t["hit"] != m["hit"]).mean() < 1e-3 and (t["leaf"] != m["leaf"]).mean() < 2e-3
+    same = (t["hit"] == 1) & (m["hit"] == 1) & (t["leaf"] == m["leaf"])
+    assert np.abs(t["t"][same] - m["t"][same]).max() < 1e-2

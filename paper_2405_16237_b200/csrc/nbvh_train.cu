@@ -375,9 +375,13 @@ extern "C" nbvh_status nbvh_train_backward(nbvh_ctx* c, const nbvh_ray* rays, in
         const char* ev = std::getenv("NBVH_DW_MMA_SYNC");
         a.use_tc_dw = (ev && ev[0] == '1') ? 0 : 1;
     }
+    static const int64_t priv_budget = [] {       // NBVH_PRIV_BYTES: tuning hook (0 disables)
+        const char* ev = std::getenv("NBVH_PRIV_BYTES");
+        return ev ? (int64_t)std::atoll(ev) : (int64_t)24 * 1024;
+    }();
     for (int l = 0; l < c->cfg.L && c->dense[l]; ++l) {
         const int64_t end = (c->offset[l] + (int64_t)(c->res[l] + 1) * (c->res[l] + 1) * (c->res[l] + 1)) * c->cfg.F;
-        if (end * 4 > 24 * 1024) break;
+        if (end * 4 > priv_budget) break;
         a.priv_levels = l + 1;
         a.priv_floats = (int32_t)end;
     }

@@ -102,7 +102,7 @@ __device__ __forceinline__ int traverse_smem_list(const CutDev& cut, const RayDe
 
 // One thread per ray: traversal stack and ordered list in shared memory (stack rows =
 // cut depth + 2, list rows = 3 * cap).
-__global__ void __launch_bounds__(128) k_traverse(TraverseArgs a) {
+__global__ void __launch_bounds__(128, 8) k_traverse(TraverseArgs a) {
     extern __shared__ int sm_raw[];
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const bool valid = r < a.n_rays;

@@ -696,7 +696,8 @@ struct ChunkPlan {
     int64_t rows = 0;          // full periods
     int64_t tail = 0;          // rays of the trailing region (last chunk only)
     int64_t dev_off = 0;       // first ray of the chunk in the device staging buffers
-    int64_t size() const { return rows * w * kHostBlock + tail; }
+    int64_t blk = kHostBlock;  // rays per block
+    int64_t size() const { return rows * w * blk + tail; }
 };
 
 static int plan_chunks(int64_t n, ChunkPlan* plan) {
@@ -715,7 +716,10 @@ static int plan_chunks(int64_t n, ChunkPlan* plan) {
     }
     int64_t W = 0;
     for (int k = 0; k < chunks; ++k) W += wts[k];
-    const int64_t periods = n / (kHostBlock * W);
+    // NBVH_HOST_CONTIG=1: one period, i.e. contiguous chunks (tuning hook)
+    const char* cev = std::getenv("NBVH_HOST_CONTIG");
+    const int64_t blk = (cev && cev[0] == '1') ? std::max<int64_t>(1, n / W) : kHostBlock;
+    const int64_t periods = n / (blk * W);
     int64_t off = 0, first = 0;
     for (int k = 0; k < chunks; ++k) {
         ChunkPlan& p = plan[k];
@@ -723,7 +727,8 @@ static int plan_chunks(int64_t n, ChunkPlan* plan) {
         p.first = first;
         first += wts[k];
         p.rows = periods;
-        p.tail = k == chunks - 1 ? n - periods * W * kHostBlock : 0;
+        p.blk = blk;
+        p.tail = k == chunks - 1 ? n - periods * W * blk : 0;
         p.dev_off = off;
         off += p.size();
     }
@@ -735,7 +740,7 @@ static cudaError_t copy_chunk(void* host, void* dev, size_t elem, int64_t n, int
                               cudaMemcpyKind kind, cudaStream_t s) {
     char* h = static_cast<char*>(host);
     char* d = static_cast<char*>(dev) + p.dev_off * elem;
-    const size_t bw = (size_t)kHostBlock * elem;
+    const size_t bw = (size_t)p.blk * elem;
     cudaError_t e = cudaSuccess;
     if (p.rows) {
         char* hb = h + (size_t)p.first * bw;

@@ -269,9 +269,7 @@ extern "C" nbvh_status nbvh_create(const nbvh_config* cfg, int cuda_device, nbvh
 }
 
 static void free_workspace(nbvh_ctx* c) {
-    dfree(c->d_lst_leaf);
-    dfree(c->d_lst_te);
-    dfree(c->d_lst_tx);
+    dfree(c->d_lst);
     dfree(c->d_state);
     dfree(c->d_act);
     dfree(c->d_act_long);
@@ -377,9 +375,7 @@ extern "C" nbvh_status nbvh_reserve(nbvh_ctx* c, int64_t max_rays) {
     cudaDeviceSynchronize();
     free_workspace(c);
     const size_t n = (size_t)max_rays;
-    cudaError_t e = dalloc(&c->d_lst_leaf, kListK * n);
-    if (e == cudaSuccess) e = dalloc(&c->d_lst_te, kListK * n);
-    if (e == cudaSuccess) e = dalloc(&c->d_lst_tx, kListK * n);
+    cudaError_t e = dalloc(&c->d_lst, kListK * n);
     if (e == cudaSuccess) e = dalloc(&c->d_state, 2 * n);
     if (e == cudaSuccess) e = dalloc(&c->d_act, n);
     if (e == cudaSuccess) e = dalloc(&c->d_act_long, n);
@@ -559,9 +555,7 @@ nbvh_status run_query(nbvh_ctx* c, const nbvh_ray* rays, int64_t n, int32_t lod,
     RayState st = c->state();
     st.nbuf += work_off;
     st.more += work_off;
-    int32_t* lst_leaf = c->d_lst_leaf + kListK * work_off;
-    float* lst_te = c->d_lst_te + kListK * work_off;
-    float* lst_tx = c->d_lst_tx + kListK * work_off;
+    float4* lst = c->d_lst + kListK * work_off;
     WorkRec* act = c->d_act + work_off;
     WorkRec* act_long = c->d_act_long + work_off;
     TraverseArgs ta{};
@@ -569,9 +563,7 @@ nbvh_status run_query(nbvh_ctx* c, const nbvh_ray* rays, int64_t n, int32_t lod,
     ta.rays = reinterpret_cast<const float4*>(rays);
     ta.n_rays = n;
     ta.cap = c->cfg.list_cap;
-    ta.lst_leaf = lst_leaf;
-    ta.lst_te = lst_te;
-    ta.lst_tx = lst_tx;
+    ta.lst = lst;
     ta.st = st;
     ta.out = out;
     ta.act_out = act;
@@ -589,9 +581,7 @@ nbvh_status run_query(nbvh_ctx* c, const nbvh_ray* rays, int64_t n, int32_t lod,
     qa.n_rays = n;
     qa.cap = c->cfg.list_cap;
     qa.mode = c->cfg.mode;
-    qa.lst_leaf = lst_leaf;
-    qa.lst_te = lst_te;
-    qa.lst_tx = lst_tx;
+    qa.lst = lst;
     qa.nbuf = st.nbuf;
     qa.more = st.more;
     qa.out = out;

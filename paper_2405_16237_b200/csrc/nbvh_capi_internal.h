@@ -67,9 +67,7 @@ struct nbvh_ctx {
 
     // query workspaces
     int64_t reserved = 0;
-    int32_t* d_lst_leaf = nullptr;
-    float* d_lst_te = nullptr;
-    float* d_lst_tx = nullptr;
+    float4* d_lst = nullptr;           // per-ray leaf lists [K][n]: (t_enter, t_exit, leaf bits, 0)
     int32_t* d_state = nullptr;        // 2 arrays of n int32: list fill, "more leaves" flag
     nbvh::WorkRec* d_act = nullptr;      // work list of the persistent query kernel
     nbvh::WorkRec* d_act_long = nullptr; // its long-ray part (consumed first)

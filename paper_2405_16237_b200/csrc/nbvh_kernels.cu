@@ -120,9 +120,7 @@ __global__ void __launch_bounds__(128, 8) k_traverse(TraverseArgs a) {
         n = traverse_smem_list(a.cut, R, a.cap, lte, ltx, lid, S, st, more, &a.ctr->err);
         more_long = more || n >= 3;
         for (int j = 0; j < n; ++j) {
-            a.lst_leaf[(int64_t)j * a.n_rays + r] = lid[j * S];
-            a.lst_te[(int64_t)j * a.n_rays + r] = lte[j * S];
-            a.lst_tx[(int64_t)j * a.n_rays + r] = ltx[j * S];
+            a.lst[(int64_t)j * a.n_rays + r] = make_float4(lte[j * S], ltx[j * S], __int_as_float(lid[j * S]), 0.f);
         }
         active = n > 0;
         if (active) {
@@ -204,12 +202,12 @@ __global__ void __launch_bounds__(128) k_debug_traverse(DebugTraverseArgs a) {
 // ------------------------------------------------------------------ persistent fused query
 // Rare path, kept out of line so the query kernel's register allocation is not sized for a
 // second traversal: refill ray r's list with the leaves after its last key (C6).
-__device__ __noinline__ int refill_list(CutDev cut, const float4* rays, int64_t n_rays, int cap, int32_t* lst_leaf,
-                                        float* lst_te, float* lst_tx, QueryCounters* ctr, int r, int nbuf,
-                                        float t_bound, int* more_out) {
+__device__ __noinline__ int refill_list(CutDev cut, const float4* rays, int64_t n_rays, int cap, float4* lst,
+                                        QueryCounters* ctr, int r, int nbuf, float t_bound, int* more_out) {
     const int64_t last = (int64_t)(nbuf - 1) * n_rays + r;
-    const float kte = lst_te[last];
-    const int kid = lst_leaf[last];
+    const float4 ke = lst[last];
+    const float kte = ke.x;
+    const int kid = __float_as_int(ke.z);
     RayDev R = load_ray(rays, r);
     float lte[kListK], ltx[kListK];
     int lid[kListK], n = 0;
@@ -218,9 +216,7 @@ __device__ __noinline__ int refill_list(CutDev cut, const float4* rays, int64_t 
 #pragma unroll
     for (int j = 0; j < kListK; ++j)
         if (j < n) {
-            lst_leaf[(int64_t)j * n_rays + r] = lid[j];
-            lst_te[(int64_t)j * n_rays + r] = lte[j];
-            lst_tx[(int64_t)j * n_rays + r] = ltx[j];
+            lst[(int64_t)j * n_rays + r] = make_float4(lte[j], ltx[j], __int_as_float(lid[j]), 0.f);
         }
     *more_out = more ? 1 : 0;
     atomicAdd(&ctr->refills, 1);
@@ -508,8 +504,9 @@ __global__ void __launch_bounds__(kQueryWarps * 32, 1) k_query(QueryArgs a) {
             S.act[row] = lane;
             const int r = S.ray[lane];
             const int64_t li = (int64_t)(S.pos[lane] - S.base[lane]) * a.n_rays + r;
-            const float te = a.lst_te[li], tx = a.lst_tx[li];
-            S.leaf[lane] = a.lst_leaf[li];
+            const float4 e = a.lst[li];
+            const float te = e.x, tx = e.y;
+            S.leaf[lane] = __float_as_int(e.z);
             S.te[lane] = te;
             S.tx[lane] = tx;
             const float o[3] = {S.o[0][lane], S.o[1][lane], S.o[2][lane]};
@@ -607,7 +604,7 @@ __global__ void __launch_bounds__(kQueryWarps * 32, 1) k_query(QueryArgs a) {
                         // list exhausted, more leaves may remain: resume after the last key,
                         // bounded by the best hit (C6)
                         int more = 0;
-                        nbuf = refill_list(a.cut, a.rays, a.n_rays, a.cap, a.lst_leaf, a.lst_te, a.lst_tx, a.ctr, r,
+                        nbuf = refill_list(a.cut, a.rays, a.n_rays, a.cap, a.lst, a.ctr, r,
                                            nbuf, bleaf >= 0 ? bt : __int_as_float(0x7f800000), &more);
                         base = pos;
                         S.base[s] = base;
@@ -617,7 +614,7 @@ __global__ void __launch_bounds__(kQueryWarps * 32, 1) k_query(QueryArgs a) {
                     }
                 }
                 if (!done) {
-                    const float next_te = a.lst_te[(int64_t)(pos - base) * a.n_rays + r];
+                    const float next_te = a.lst[(int64_t)(pos - base) * a.n_rays + r].x;
                     done = bleaf >= 0 && next_te > bt;                     // front-to-back termination
                 }
             }

@@ -48,9 +48,7 @@ struct TraverseArgs {
     const float4* rays;
     int64_t n_rays;
     int32_t cap;
-    int32_t* lst_leaf;
-    float* lst_te;
-    float* lst_tx;
+    float4* lst;             // leaf lists [K][n_rays]: (t_enter, t_exit, leaf id bits, 0)
     RayState st;
     HitsDev out;
     WorkRec* act_out;
@@ -78,9 +76,7 @@ struct QueryArgs {
     int64_t n_rays;
     int32_t cap;
     int32_t mode;
-    int32_t* lst_leaf;
-    float* lst_te;
-    float* lst_tx;
+    float4* lst;             // leaf lists [K][n_rays]: (t_enter, t_exit, leaf id bits, 0)
     const int32_t* nbuf;
     const int32_t* more;
     HitsDev out;

@@ -253,27 +253,27 @@ def run_ours(args):
 
     # end-to-end through the public host API: pinned host rays in, host results out
     e2e = None
-    if rank == 0 or True:
-        pin = torch.from_numpy(rays_np).pin_memory()
-        hb = {"hit": torch.empty(n, dtype=torch.uint8).pin_memory(), "t": torch.empty(n).pin_memory(),
-              "normal": torch.empty(n, 3).pin_memory(), "albedo": torch.empty(n, 3).pin_memory()}
-        hbn = {k: v.numpy() for k, v in hb.items()}
-        pin_np = pin.numpy()
-        ctx.query_host(pin_np, out=hbn)
+    # every rank measures its own e2e (the max over ranks is reported)
+    pin = torch.from_numpy(rays_np).pin_memory()
+    hb = {"hit": torch.empty(n, dtype=torch.uint8).pin_memory(), "t": torch.empty(n).pin_memory(),
+          "normal": torch.empty(n, 3).pin_memory(), "albedo": torch.empty(n, 3).pin_memory()}
+    hbn = {k: v.numpy() for k, v in hb.items()}
+    pin_np = pin.numpy()
+    ctx.query_host(pin_np, out=hbn)
+    torch.cuda.synchronize()
+    e2e_s = []
+    for i in range(args.steps):
+        flush.fill_(float(i))
         torch.cuda.synchronize()
-        e2e_s = []
-        for i in range(args.steps):
-            flush.fill_(float(i))
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            ctx.query_host(pin_np, out=hbn)                       # synchronous: H2D + query + D2H
-            e2e_s.append(time.perf_counter() - t0)
-        e2e_t = torch.tensor([sum(e2e_s)], dtype=torch.float64, device="cuda")
-        if world > 1:
-            dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-        d2h = n * (1 + 4 + 12 + 12)                                   # hit, t, normal, albedo
-        e2e = {"value": n * args.steps * world / float(e2e_t.item()) / 1e6, "unit": "Mrays/s",
-               "h2d_bytes_per_step": n * 32, "d2h_bytes_per_step": d2h}
+        t0 = time.perf_counter()
+        ctx.query_host(pin_np, out=hbn)                       # synchronous: H2D + query + D2H
+        e2e_s.append(time.perf_counter() - t0)
+    e2e_t = torch.tensor([sum(e2e_s)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    d2h = n * (1 + 4 + 12 + 12)                                   # hit, t, normal, albedo
+    e2e = {"value": n * args.steps * world / float(e2e_t.item()) / 1e6, "unit": "Mrays/s",
+           "h2d_bytes_per_step": n * 32, "d2h_bytes_per_step": d2h}
 
     mlp = bench_mlp(ctx, args)
     gather = bench_gather(args)

@@ -368,6 +368,13 @@ __device__ __forceinline__ void mlp_group_tc(int g, int wg, int lane, int hidden
 // update the best hit, decide front-to-back termination and free finished slots after
 // writing the hit record.  Warps drift freely, so one warp's MLP or list refill overlaps
 // other warps' gathers.
+// Lanes below this one (a special register: nothing kept live across the query loop).
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
 template <int F, int D, bool kTc>
 __global__ void __launch_bounds__(kQueryWarps * 32, 1) k_query(QueryArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -446,8 +453,7 @@ __global__ void __launch_bounds__(kQueryWarps * 32, 1) k_query(QueryArgs a) {
     const uint32_t hmask = (1u << a.g.log2_T) - 1u;
     const void* tab = a.g.table;
     const int cpp = (a.g.L * F) / 8;          // 16-byte chunks per sample point
-    const unsigned lt_mask = (1u << lane) - 1u;
-    unsigned long long my_queries = 0;
+    int my_queries = 0;                       // queries this warp evaluated (< 2^31)
     int iters = 0;
     bool exhausted = false;
 
@@ -461,7 +467,7 @@ __global__ void __launch_bounds__(kQueryWarps * 32, 1) k_query(QueryArgs a) {
             if (lane == 0) base = atomicAdd(a.next, ne);
             base = __shfl_sync(0xffffffffu, base, 0);
             exhausted = base + ne >= total;
-            const int i = base + __popc(em & lt_mask);
+            const int i = base + __popc(em & lanemask_lt());
             if (empty && i < total) {
                 const WorkRec* wr = i < n_long ? a.act_long + i : a.act + (i - n_long);
                 const float4 w0 = __ldg(&wr->o), w1 = __ldg(&wr->d);
@@ -498,9 +504,9 @@ __global__ void __launch_bounds__(kQueryWarps * 32, 1) k_query(QueryArgs a) {
             if (nv == 0) break;               // work list drained and every slot finished
         }
         ++iters;
-        my_queries += (unsigned long long)nv;
+        my_queries += nv;
         if (occ) {
-            const int row = __popc(om & lt_mask);
+            const int row = __popc(om & lanemask_lt());
             S.act[row] = lane;
             const int r = S.ray[lane];
             const int64_t li = (int64_t)(S.pos[lane] - S.base[lane]) * a.n_rays + r;
@@ -638,7 +644,7 @@ __global__ void __launch_bounds__(kQueryWarps * 32, 1) k_query(QueryArgs a) {
         __syncwarp();
     }
     if (lane == 0) {
-        atomicAdd(&a.ctr->n_queries, my_queries);
+        atomicAdd(&a.ctr->n_queries, (unsigned long long)my_queries);
         atomicMax(&a.ctr->max_iter, iters);
     }
     if constexpr (kTc) {

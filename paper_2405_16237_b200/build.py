@@ -9,6 +9,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libnbvh.so")
+LIB_DEBUG = os.path.join(HERE, "libnbvh_debug.so")   # -DNBVH_DEBUG_CHECKS: device-side bounds asserts
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -22,20 +23,23 @@ def _deps() -> list[str]:
         os.path.join(HERE, "..", "include", "nbvh.h"), __file__]
 
 
-def up_to_date() -> bool:
-    if not os.path.exists(LIB):
+def up_to_date(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return False
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     return all(os.path.getmtime(p) <= t for p in _deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
-        return LIB
-    objdir = os.path.join(HERE, "build")
+def build(force: bool = False, verbose: bool = False, debug: bool = False) -> str:
+    """The product library (or, debug=True, the same sources with device-side bounds asserts
+    compiled in: libnbvh_debug.so, used by tests/test_gpu_debug_checks.py)."""
+    lib = LIB_DEBUG if debug else LIB
+    if not force and up_to_date(lib):
+        return lib
+    objdir = os.path.join(HERE, "build_debug" if debug else "build")
     os.makedirs(objdir, exist_ok=True)
     common = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-fopenmp,-ffp-contract=off",
-              "-I", os.path.join(HERE, "..", "include")]
+              "-I", os.path.join(HERE, "..", "include")] + (["-DNBVH_DEBUG_CHECKS"] if debug else ["-DNDEBUG"])
     objs = []
     procs = []
     for src in sources():
@@ -54,11 +58,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
             sys.stdout.write(out.decode())
     if failed:
         raise RuntimeError("nvcc failed:\n" + "\n".join(f"{s}:\n{o}" for s, o in failed))
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     subprocess.check_call([NVCC, *ARCH, "-shared", "-cudart", "static", "-Xcompiler", "-fopenmp", "-lgomp",
                            *objs, "-o", tmp])
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

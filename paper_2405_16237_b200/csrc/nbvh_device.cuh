@@ -16,6 +16,15 @@
 // so nvcc cannot contract it into an FMA.  Continuous blends use FMA freely.
 #pragma once
 
+// Device-side bounds checks, compiled in only by the debug-checks build (build.py debug=True,
+// -DNBVH_DEBUG_CHECKS): a failed check stops the kernel with a device assert (file / line).
+#ifdef NBVH_DEBUG_CHECKS
+#include <cassert>
+#define NBVH_DCHECK(cond) assert(cond)
+#else
+#define NBVH_DCHECK(cond) ((void)0)
+#endif
+
 #include <cuda_fp16.h>
 #include <cstdint>
 #include <type_traits>
@@ -496,6 +505,7 @@ __device__ __forceinline__ void encode_issue(const LevelSm* lv, const void* tab,
         }
         if (P.nx) {
             // dense level: the cell's 8 corners are one contiguous 16*F-byte record
+            NBVH_DCHECK(i0 < P.nx && i1 < P.nx && i2 < P.nx);
             const uint32_t cell = i0 + i1 * P.nx + i2 * P.nxy;
             if constexpr (F == 2) {
                 ldg256(T + (P.off + 8u * cell), G.v[j]);
@@ -512,6 +522,7 @@ __device__ __forceinline__ void encode_issue(const LevelSm* lv, const void* tab,
         } else {
             // hashed level (C3): (x*1 ^ y*pi2 ^ z*pi3) mod T, masks distributed; the
             // x term needs no mask: x+1 <= N < T on every hashed level (checked at creation)
+            NBVH_DCHECK(i0 + 1u <= hmask);     // unmasked x term stays inside the level
             const uint32_t hx[2] = {i0, i0 + 1u};
             const uint32_t hy[2] = {(i1 * kPrime1) & hmask, ((i1 + 1u) * kPrime1) & hmask};
             const uint32_t hz[2] = {(i2 * kPrime2) & hmask, ((i2 + 1u) * kPrime2) & hmask};

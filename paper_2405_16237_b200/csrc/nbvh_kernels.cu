@@ -118,6 +118,7 @@ __global__ void __launch_bounds__(128, 8) k_traverse(TraverseArgs a) {
         R = load_ray(a.rays, r);
         SmemStack st{sm_raw + 3 * a.cap * S + threadIdx.x, S, a.cut.depth + 2};
         n = traverse_smem_list(a.cut, R, a.cap, lte, ltx, lid, S, st, more, &a.ctr->err);
+        NBVH_DCHECK(n >= 0 && n <= a.cap && a.cap <= kListK);
         more_long = more || n >= 3;
         for (int j = 0; j < n; ++j) {
             a.lst[(int64_t)j * a.n_rays + r] = make_float4(lte[j * S], ltx[j * S], __int_as_float(lid[j * S]), 0.f);
@@ -472,6 +473,7 @@ __global__ void __launch_bounds__(kQueryWarps * 32, 1) k_query(QueryArgs a) {
                 const WorkRec* wr = i < n_long ? a.act_long + i : a.act + (i - n_long);
                 const float4 w0 = __ldg(&wr->o), w1 = __ldg(&wr->d);
                 const int r = __float_as_int(w0.w), st = __float_as_int(w1.w);
+                NBVH_DCHECK(r >= 0 && r < a.n_rays && (st & 0xffff) >= 1 && (st & 0xffff) <= a.cap);
                 S.ray[lane] = r;
                 S.o[0][lane] = w0.x; S.o[1][lane] = w0.y; S.o[2][lane] = w0.z;
                 S.d[0][lane] = w1.x; S.d[1][lane] = w1.y; S.d[2][lane] = w1.z;
@@ -509,6 +511,8 @@ __global__ void __launch_bounds__(kQueryWarps * 32, 1) k_query(QueryArgs a) {
             const int row = __popc(om & lanemask_lt());
             S.act[row] = lane;
             const int r = S.ray[lane];
+            NBVH_DCHECK(S.pos[lane] - S.base[lane] >= 0 && S.pos[lane] - S.base[lane] < S.nbuf[lane] &&
+                        S.nbuf[lane] <= kListK);
             const int64_t li = (int64_t)(S.pos[lane] - S.base[lane]) * a.n_rays + r;
             const float4 e = a.lst[li];
             const float te = e.x, tx = e.y;

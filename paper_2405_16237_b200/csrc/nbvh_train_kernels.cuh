@@ -543,12 +543,15 @@ __global__ void __launch_bounds__(256, 1) k_train_bwd(TrainArgs a) {
                 if (l < a.priv_levels) {
 #pragma unroll
                     for (int k = 0; k < 8; ++k)
-                        for (int f = 0; f < F; ++f)
+                        for (int f = 0; f < F; ++f) {
+                            NBVH_DCHECK((int64_t)(P.coff + cell.idx[k]) * F + f < a.priv_floats);
                             atomicAdd(priv + (P.coff + cell.idx[k]) * F + f, cell.w[k] * gq[f]);
+                        }
                 } else {
                     float* base = a.grad + (int64_t)P.coff * F;
 #pragma unroll
                     for (int k = 0; k < 8; ++k) {
+                        NBVH_DCHECK(cell.idx[k] < (P.n1 ? P.n1sq * P.n1 : hmask + 1u));
                         float* dst = base + (int64_t)cell.idx[k] * F;
                         red_add_v2(dst, cell.w[k] * gq[0], cell.w[k] * gq[1]);
                         if (F == 4) red_add_v2(dst + 2, cell.w[k] * gq[2], cell.w[k] * gq[3]);

@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libnbvh.so")
+LIB_PATH = os.environ.get("NBVH_LIB") or os.path.join(_HERE, "libnbvh.so")   # NBVH_LIB: e.g. the debug-checks build
 
 STATUS = {0: "OK", 1: "WARN_CLAMPED", -1: "EINVAL", -2: "ERANGE", -3: "ESTATE", -4: "ENONFINITE", -5: "ECUDA",
           -6: "ENOMEM"}

@@ -6,8 +6,9 @@
 //   k_query       Q2-Q7, one persistent launch: every warp owns 16 ray slots and loops —
 //                 refill empty slots from the work lists, sample the current leaf segment,
 //                 hash-grid encode into shared memory, run the MLP on tensor cores
-//                 (mma.sync), decode, update the best hit, decide front-to-back termination,
-//                 write finished rays' hit records.
+//                 (mma.sync per warp; optional kTc variant: tcgen05 per 8-warp group),
+//                 decode, update the best hit, decide front-to-back termination, write
+//                 finished rays' hit records.
 //   k_debug_*     the same device functions with intermediate results exposed.
 //
 // Paper passages: P:103 (front-to-back probing, early termination)

@@ -387,3 +387,18 @@ def test_query_tcgen05_group_mlp_variant(orc, monkeypatch):
     assert (t["hit"] != m["hit"]).mean() < 1e-3 and (t["leaf"] != m["leaf"]).mean() < 2e-3
     same = (t["hit"] == 1) & (m["hit"] == 1) & (t["leaf"] == m["leaf"])
     assert np.abs(t["t"][same] - m["t"][same]).max() < 1e-2
+
+
+def test_query_host_path_first_hit_mode_and_lod(monkeypatch):
+    """The host path with R1 (first confident hit, C5) and with a non-zero LoD slot returns
+    exactly the device path's records."""
+    ctx, sc, tab, layers = _mk_ctx("tiny", mode=1)
+    ctx.copy_cut(0, 2)
+    cam = synth.camera_rays(600, 512, (0.0, 0.0, 3.5), vfov_deg=40.0)
+    ctx.reserve(cam.shape[0])
+    for lod in (0, 2):
+        d = {k: v.cpu().numpy() for k, v in ctx.query(torch.from_numpy(cam).cuda(), lod=lod).items()}
+        h = ctx.query_host(cam, lod=lod)
+        for k in d:
+            assert np.array_equal(d[k].reshape(h[k].shape), h[k]), (lod, k)
+        assert d["hit"].sum() > 1000

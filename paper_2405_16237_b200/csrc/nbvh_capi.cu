@@ -113,29 +113,55 @@ __global__ void k_refresh_table(const float* __restrict__ src, __half* __restric
     const LevelSm P = lv[blockIdx.y];
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     if (P.nx) {
+        // dense level: cell c's record = its 8 corner vertices' features (corner-packed)
         const uint32_t n_cells = P.nxy * P.nx;
         for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n_cells; c += stride) {
             const uint32_t cell = (uint32_t)c;
             const uint32_t cz = cell / P.nxy, rem = cell - cz * P.nxy;
             const uint32_t cy = rem / P.nx, cx = rem - cy * P.nx;
             const uint32_t b = cx + cy * P.n1 + cz * P.n1sq;
-            __align__(16) __half rec[32];
+            __align__(16) __half2 rec[16];
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
                 const uint32_t idx = b + (k & 1) + ((k >> 1) & 1) * P.n1 + ((k >> 2) & 1) * P.n1sq;
                 const float* sp = src + ((int64_t)P.coff + idx) * F;
-                for (int f = 0; f < F; ++f) rec[k * F + f] = __float2half_rn(sp[f]);
+                if (F == 2) {
+                    rec[k] = __float22half2_rn(__ldg(reinterpret_cast<const float2*>(sp)));
+                } else {
+                    const float4 v = __ldg(reinterpret_cast<const float4*>(sp));
+                    rec[2 * k] = __floats2half2_rn(v.x, v.y);
+                    rec[2 * k + 1] = __floats2half2_rn(v.z, v.w);
+                }
             }
             uint4* d = reinterpret_cast<uint4*>(dst + ((int64_t)P.off + 8ll * cell) * F);
             const uint4* r = reinterpret_cast<const uint4*>(rec);
             for (int v = 0; v < F; ++v) d[v] = r[v];            // 16*F bytes
         }
     } else {
-        const int64_t n = (int64_t)1 << g.log2_T;
-        for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += stride) {
-            const float* sp = src + ((int64_t)P.coff + e) * F;
-            __half* dp = dst + ((int64_t)P.off + e) * F;
-            for (int f = 0; f < F; ++f) dp[f] = __float2half_rn(sp[f]);
+        // hashed level: the canonical layout, 4 entries per thread: 8- or 16-byte loads (the
+        // level's master offset can be odd), one 16-byte store per 8 halves
+        const int64_t n4 = ((int64_t)1 << g.log2_T) / 4;
+        uint4* dp = reinterpret_cast<uint4*>(dst + (int64_t)P.off * F);
+        for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n4; e += stride) {
+            const float* sp = src + ((int64_t)P.coff + 4 * e) * F;
+            if (F == 2) {
+                const float2 v0 = __ldg(reinterpret_cast<const float2*>(sp)),
+                             v1 = __ldg(reinterpret_cast<const float2*>(sp + 2)),
+                             v2 = __ldg(reinterpret_cast<const float2*>(sp + 4)),
+                             v3 = __ldg(reinterpret_cast<const float2*>(sp + 6));
+                const __half2 o[4] = {__float22half2_rn(v0), __float22half2_rn(v1), __float22half2_rn(v2),
+                                      __float22half2_rn(v3)};
+                dp[e] = *reinterpret_cast<const uint4*>(o);
+            } else {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const float4 a = __ldg(reinterpret_cast<const float4*>(sp) + 2 * h),
+                                 b = __ldg(reinterpret_cast<const float4*>(sp) + 2 * h + 1);
+                    const __half2 o[4] = {__floats2half2_rn(a.x, a.y), __floats2half2_rn(a.z, a.w),
+                                          __floats2half2_rn(b.x, b.y), __floats2half2_rn(b.z, b.w)};
+                    dp[2 * e + h] = *reinterpret_cast<const uint4*>(o);
+                }
+            }
         }
     }
 }

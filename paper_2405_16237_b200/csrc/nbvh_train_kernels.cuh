@@ -719,28 +719,45 @@ __global__ void __launch_bounds__(256) k_train_bias_out(TrainArgs a, int64_t w_o
             for (int j = 0; j < 8; ++j) atomicAdd(sb + layer * 64 + c0 + j, acc[j]);
         }
     }
-    // (2) output layer: thread -> (row slot, output o, 8-input group)
+    // (2) output layer: thread -> (row slot, 8-input group); each row's activations (16 B per
+    //     thread) and its 8 output deltas are read once, 8 x 8 products accumulated
     {
-        const int rows_per_pass = blockDim.x / 64;      // 64 (o, group) tasks per row
-        const int slot = tid >> 6, task = tid & 63;
-        const int o = task >> 3, i0 = (task & 7) * 8;
-        float accw[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, accb = 0.f;
+        const int rows_per_pass = blockDim.x / 8;
+        const int slot = tid >> 3, i0 = (tid & 7) * 8;
+        float accw[8][8], accb[8];
+#pragma unroll
+        for (int o = 0; o < 8; ++o) {
+            accb[o] = 0.f;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) accw[o][j] = 0.f;
+        }
         const __half* Ah = a.A + (int64_t)(H - 1) * a.cap * 64 + i0;
         for (int64_t r = (int64_t)blockIdx.x * rows_per_pass + slot; r < M; r += (int64_t)gridDim.x * rows_per_pass) {
-            const float dz = a.dZ[r * 8 + o];
+            const float4 d0 = *reinterpret_cast<const float4*>(a.dZ + r * 8),
+                         d1 = *reinterpret_cast<const float4*>(a.dZ + r * 8 + 4);
+            const float dz[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
             const uint4 v = *reinterpret_cast<const uint4*>(Ah + r * 64);
-            const __half2* h = reinterpret_cast<const __half2*>(&v);
+            const __half2* hh = reinterpret_cast<const __half2*>(&v);
+            float f[8];
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-                const float2 f = __half22float2(h[j]);
-                accw[2 * j] = fmaf(dz, f.x, accw[2 * j]);
-                accw[2 * j + 1] = fmaf(dz, f.y, accw[2 * j + 1]);
+                const float2 t = __half22float2(hh[j]);
+                f[2 * j] = t.x;
+                f[2 * j + 1] = t.y;
             }
-            accb += dz;
+#pragma unroll
+            for (int o = 0; o < 8; ++o) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) accw[o][j] = fmaf(dz[o], f[j], accw[o][j]);
+                accb[o] += dz[o];
+            }
         }
 #pragma unroll
-        for (int j = 0; j < 8; ++j) atomicAdd(sw + o * 64 + i0 + j, accw[j]);
-        if (i0 == 0) atomicAdd(sb + 4 * 64 + o, accb);
+        for (int o = 0; o < 8; ++o) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) atomicAdd(sw + o * 64 + i0 + j, accw[o][j]);
+            if (i0 == 0) atomicAdd(sb + 4 * 64 + o, accb[o]);
+        }
     }
     __syncthreads();
     for (int i = tid; i < H * 64; i += blockDim.x) atomicAdd(a.grad + b_off + i, sb[i]);

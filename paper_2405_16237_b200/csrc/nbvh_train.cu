@@ -215,6 +215,20 @@ void reset_adam(nbvh_ctx* c) {
 }
 
 // launchers (templated on F, D)
+// Shared memory of k_train_bwd without the private gradient accumulator, and the bytes left
+// for that accumulator under the per-CTA opt-in limit.
+static size_t bwd_smem_base(int D, int H, int n_points) {
+    return ((size_t)64 * (D + 8) + (size_t)(H - 1) * 64 * 72 + 16 * 72) * 2 + kTileQ * sizeof(SampleDesc) +
+           kMaxLevels * sizeof(LevelSm) + (size_t)kTileQ * n_points * 3 * 4 + (size_t)kTileQ * (D + 4) * 4;
+}
+static int64_t bwd_priv_room(int D, int H, int n_points) {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    const int64_t room = (int64_t)optin - 1024 - (int64_t)bwd_smem_base(D, H, n_points);   // 1 KB static margin
+    return room > 0 ? room : 0;
+}
+
 // ev (nullable): 6 events recorded before select and after select, label, fwd, bwd, dW
 template <int F, int D>
 static cudaError_t launch_train_fd(const TrainArgs& a, int64_t n, int64_t w_off, int64_t b_off, cudaStream_t s,
@@ -226,25 +240,32 @@ static cudaError_t launch_train_fd(const TrainArgs& a, int64_t n, int64_t w_off,
     const size_t smem_fwd = (size_t)kTileQ * (D + 8) * 2 + (size_t)mlp_smem_halves(D, H) * 2 + kTileQ * 8 * 4 +
                             (64 * H + 8) * 4 + kTileQ * sizeof(SampleDesc) + kMaxLevels * sizeof(LevelSm) +
                             (size_t)kTileQ * a.g.n_points * 3 * 4;
-    const size_t smem_bwd = ((size_t)64 * (D + 8) + (size_t)(H - 1) * 64 * 72 + 16 * 72) * 2 + kTileQ * sizeof(SampleDesc) +
-                            kMaxLevels * sizeof(LevelSm) + (size_t)kTileQ * a.g.n_points * 3 * 4 +
-                            (size_t)kTileQ * (D + 4) * 4 + (size_t)a.priv_floats * 4;
+    const size_t smem_bwd = bwd_smem_base(D, H, a.g.n_points) + (size_t)a.priv_floats * 4;
     const size_t smem_dw = (size_t)kTileQ * 72 * 2 + (size_t)kTileQ * (D + 8) * 2 + kTileQ * 8 * 4;
-    cudaFuncSetAttribute(k_train_fwd<F, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fwd);
-    cudaFuncSetAttribute(k_train_bwd<F, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bwd);
-    cudaFuncSetAttribute(k_train_dw<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_dw);
+    cudaError_t e = cudaFuncSetAttribute(k_train_fwd<F, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fwd);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_train_bwd<F, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bwd);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_train_dw<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_dw);
+    if (e != cudaSuccess) return e;
     const unsigned blocks_n = (unsigned)((n + 127) / 128);
     if (ev) cudaEventRecord(ev[0], s);
+    // every launch is checked at once: a failed launch must not leave a step that silently
+    // skipped a phase
     k_train_select<<<blocks_n, 128, (size_t)(a.cut.depth + 2) * 128 * sizeof(int), s>>>(a);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (ev) cudaEventRecord(ev[1], s);
     k_train_label<<<blocks_n, 128, 64 * 128 * sizeof(int), s>>>(a);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (ev) cudaEventRecord(ev[2], s);
     const int tiles = (int)((n + kTileQ - 1) / kTileQ);
     const int grid = tiles < sms ? (tiles > 0 ? tiles : 1) : sms;
     const int grid_fwd = tiles < 2 * sms ? (tiles > 0 ? tiles : 1) : 2 * sms;   // 2 CTAs per SM
     k_train_fwd<F, D><<<grid_fwd, 256, smem_fwd, s>>>(a);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (ev) cudaEventRecord(ev[3], s);
     k_train_bwd<F, D><<<grid, 256, smem_bwd, s>>>(a);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (ev) cudaEventRecord(ev[4], s);
     const unsigned dw_grid = (unsigned)((n + kDwChunk - 1) / kDwChunk);
     bool tc_done = false;
@@ -253,14 +274,17 @@ static cudaError_t launch_train_fd(const TrainArgs& a, int64_t n, int64_t w_off,
         // on the CUDA-core kernel
         auto run_tc = [&](auto kern, int Hc) {
             const size_t sm = dw_tc_smem(D, Hc);
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            if (e != cudaSuccess) return;
             kern<<<sms, 128, sm, s>>>(a, w_off);
-            tc_done = true;
+            e = cudaGetLastError();
+            tc_done = e == cudaSuccess;
         };
         if (H == 1 && dw_tc_ok(D, 1)) run_tc(k_train_dw_tc<D, 1>, 1);
         else if (H == 2 && dw_tc_ok(D, 2)) run_tc(k_train_dw_tc<D, 2>, 2);
         else if (H == 3 && dw_tc_ok(D, 3)) run_tc(k_train_dw_tc<D, 3>, 3);
         else if (H == 4 && dw_tc_ok(D, 4)) run_tc(k_train_dw_tc<D, 4>, 4);
+        if (e != cudaSuccess) return e;
     }
     if (tc_done) {
         // output-layer weights follow the input and hidden layers in the weight block
@@ -270,6 +294,7 @@ static cudaError_t launch_train_fd(const TrainArgs& a, int64_t n, int64_t w_off,
     } else {
         k_train_dw<D><<<dw_grid > 0 ? dw_grid : 1, 256, smem_dw, s>>>(a, w_off, b_off);
     }
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (ev) cudaEventRecord(ev[5], s);
     *launches += 5;
     return cudaGetLastError();
@@ -367,7 +392,8 @@ extern "C" nbvh_status nbvh_train_backward(nbvh_ctx* c, const nbvh_ray* rays, in
     a.tail = w->grad + n_params(c);
     a.loss_acc = w->loss_acc;
     a.cap = w->cap;
-    // coarse dense levels whose gradients fit a 24 KB CTA-private accumulator (prefix)
+    // coarse dense levels whose gradients fit a CTA-private shared-memory accumulator (the
+    // longest prefix that fits next to k_train_bwd's other shared memory, or NBVH_PRIV_BYTES)
     a.priv_levels = 0;
     a.priv_floats = 0;
     // NBVH_DW_MMA_SYNC=1 forces the mma.sync weight-gradient kernel (A/B parity tests)
@@ -375,10 +401,9 @@ extern "C" nbvh_status nbvh_train_backward(nbvh_ctx* c, const nbvh_ray* rays, in
         const char* ev = std::getenv("NBVH_DW_MMA_SYNC");
         a.use_tc_dw = (ev && ev[0] == '1') ? 0 : 1;
     }
-    static const int64_t priv_budget = [] {       // NBVH_PRIV_BYTES: tuning hook (0 disables)
-        const char* ev = std::getenv("NBVH_PRIV_BYTES");
-        return ev ? (int64_t)std::atoll(ev) : (int64_t)24 * 1024;
-    }();
+    const char* pev = std::getenv("NBVH_PRIV_BYTES");   // tuning hook (0 disables)
+    const int64_t room = bwd_priv_room(c->d_in, c->cfg.hidden_layers, c->cfg.n_points);
+    const int64_t priv_budget = pev ? std::min<int64_t>(std::atoll(pev), room) : room;
     for (int l = 0; l < c->cfg.L && c->dense[l]; ++l) {
         const int64_t end = (c->offset[l] + (int64_t)(c->res[l] + 1) * (c->res[l] + 1) * (c->res[l] + 1)) * c->cfg.F;
         if (end * 4 > priv_budget) break;

@@ -256,16 +256,19 @@ __global__ void __launch_bounds__(256, 2) k_train_fwd(TrainArgs a) {
                 }
         }
         __syncthreads();
-        {   // encode: warp item = (32-sample block, 16-byte chunk); lanes = samples
-            const int nqb = (nv + 31) >> 5;
-            for (int it = warp; it < nqb * (D / 8); it += 8) {
-                const int c = it / nqb, qb = it - c * nqb;
-                const int q = qb * 32 + lane;
-                if (q < nv) {
-                    const int p = c / cpp, l0 = (c - p * cpp) * (8 / F);
+        {   // encode: warp item = (16-sample block, point pair, level chunk); the two half-warps
+            // take neighbouring sample points of the same 16 segments at the same levels (the
+            // query kernel's mapping: coherent cache lines between the halves)
+            const int nqb = (nv + 15) >> 4, npp = (n_pts + 1) >> 1;
+            for (int it = warp; it < nqb * npp * cpp; it += 8) {
+                const int qb = it % nqb, rest = it / nqb;
+                const int lc = rest % cpp, pp = rest / cpp;
+                const int q = qb * 16 + (lane & 15), p = 2 * pp + (lane >> 4);
+                if (q < nv && p < n_pts) {
+                    const int c = p * cpp + lc;
                     *reinterpret_cast<uint4*>(feat + q * (D + 8) + c * 8) = encode_chunk_sm<F, false>(
                         lv, a.g.table, hmask, xs[(p * 3 + 0) * kTileQ + q], xs[(p * 3 + 1) * kTileQ + q],
-                        xs[(p * 3 + 2) * kTileQ + q], l0, nullptr);
+                        xs[(p * 3 + 2) * kTileQ + q], lc * (8 / F), nullptr);
                 }
             }
         }

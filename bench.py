@@ -158,11 +158,16 @@ def cpu_oracle_rate(ctx, c, rays, target_s: float = 12.0, max_rays: int | None =
     n = int(min(rays.shape[0], max(256, target_s / max(per_ray, 1e-9))))
     if max_rays:
         n = min(n, max_rays)
-    stride = max(1, rays.shape[0] // n)
-    sample = rays[::stride][:n]
-    t0 = time.perf_counter()
-    oracle.query(g, h.n_points, tab, layers, cut["leaf_lo"], cut["leaf_hi"], sample, dom_box=box)
-    dt = time.perf_counter() - t0
+    for _ in range(2):                                # a second, larger sample if the first was short
+        stride = max(1, rays.shape[0] // n)
+        sample = rays[::stride][:n]
+        t0 = time.perf_counter()
+        oracle.query(g, h.n_points, tab, layers, cut["leaf_lo"], cut["leaf_hi"], sample, dom_box=box)
+        dt = time.perf_counter() - t0
+        grow = int(n * target_s / max(dt, 1e-9))
+        if dt >= target_s / 3 or n >= rays.shape[0] or (max_rays and n >= max_rays):
+            break
+        n = min(rays.shape[0], grow, max_rays or grow)
     return {"value": sample.shape[0] / dt / 1e6, "unit": "Mrays/s", "cores": oracle.num_threads(), "kind": "oracle",
             "sample": f"every {stride}th primary ray of the frame ({sample.shape[0]} rays), C++ double oracle, "
                       f"brute-force leaf scan, OpenMP", "seconds": dt}

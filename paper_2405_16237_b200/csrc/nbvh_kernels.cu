@@ -158,6 +158,7 @@ __global__ void __launch_bounds__(128, 8) k_traverse(TraverseArgs a) {
         WorkRec w;
         w.o = make_float4(R.o[0], R.o[1], R.o[2], __int_as_float((int)r));
         w.d = make_float4(R.d[0], R.d[1], R.d[2], __int_as_float(n | (more ? 1 << 16 : 0)));
+        w.e0 = make_float4(lte[0], ltx[0], __int_as_float(lid[0]), 0.f);   // list entry 0
         if (is_long) a.act_long[bl + __popc(ml & lt)] = w;
         else a.act_out[bs + __popc(ms & lt)] = w;
     }
@@ -232,7 +233,7 @@ constexpr int kQueryWarps = 16;     // warps per CTA (one CTA per SM; bounded by
 
 struct WarpSlots {
     int32_t ray[kWarpQ], pos[kWarpQ], base[kWarpQ], nbuf[kWarpQ], more[kWarpQ], bleaf[kWarpQ], nq[kWarpQ],
-        leaf[kWarpQ], act[kWarpQ];
+        leaf[kWarpQ], act[kWarpQ], fresh[kWarpQ];   // fresh: entry 0 (from the work record) in the slot
     float o[3][kWarpQ], d[3][kWarpQ];
     float bt[kWarpQ], bte[kWarpQ], te[kWarpQ], tx[kWarpQ];
     float nrm[3][kWarpQ], alb[3][kWarpQ];
@@ -472,8 +473,12 @@ __global__ void __launch_bounds__(kQueryWarps * 32, 1) k_query(QueryArgs a) {
             const int i = base + __popc(em & lanemask_lt());
             if (empty && i < total) {
                 const WorkRec* wr = i < n_long ? a.act_long + i : a.act + (i - n_long);
-                const float4 w0 = __ldg(&wr->o), w1 = __ldg(&wr->d);
+                const float4 w0 = __ldg(&wr->o), w1 = __ldg(&wr->d), w2 = __ldg(&wr->e0);
                 const int r = __float_as_int(w0.w), st = __float_as_int(w1.w);
+                S.te[lane] = w2.x;
+                S.tx[lane] = w2.y;
+                S.leaf[lane] = __float_as_int(w2.z);
+                S.fresh[lane] = 1;
                 NBVH_DCHECK(r >= 0 && r < a.n_rays && (st & 0xffff) >= 1 && (st & 0xffff) <= a.cap);
                 S.ray[lane] = r;
                 S.o[0][lane] = w0.x; S.o[1][lane] = w0.y; S.o[2][lane] = w0.z;
@@ -515,11 +520,19 @@ __global__ void __launch_bounds__(kQueryWarps * 32, 1) k_query(QueryArgs a) {
             NBVH_DCHECK(S.pos[lane] - S.base[lane] >= 0 && S.pos[lane] - S.base[lane] < S.nbuf[lane] &&
                         S.nbuf[lane] <= kListK);
             const int64_t li = (int64_t)(S.pos[lane] - S.base[lane]) * a.n_rays + r;
-            const float4 e = a.lst[li];
-            const float te = e.x, tx = e.y;
-            S.leaf[lane] = __float_as_int(e.z);
-            S.te[lane] = te;
-            S.tx[lane] = tx;
+            float te, tx;
+            if (S.fresh[lane]) {              // a new ray: entry 0 came with its work record
+                S.fresh[lane] = 0;
+                te = S.te[lane];
+                tx = S.tx[lane];
+            } else {
+                const float4 e = a.lst[li];
+                te = e.x;
+                tx = e.y;
+                S.leaf[lane] = __float_as_int(e.z);
+                S.te[lane] = te;
+                S.tx[lane] = tx;
+            }
             const float o[3] = {S.o[0][lane], S.o[1][lane], S.o[2][lane]};
             const float d[3] = {S.d[0][lane], S.d[1][lane], S.d[2][lane]};
             for (int p = 0; p < NP; ++p) {

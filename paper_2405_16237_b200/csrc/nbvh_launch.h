@@ -35,12 +35,13 @@ struct QueryCounters {
 };
 
 // One work-list entry of the persistent query kernel, written by k_traverse: the ray itself
-// and its list state, so a slot refill is one level of (coalesced, 2 x 16 B) loads instead of
+// and its list state, so a slot refill is one level of (coalesced, 3 x 16 B) loads instead of
 // an index load followed by dependent ray / list-state loads.  (tmin / tmax are not needed
 // past the traversal: the leaf intervals already respect them.)
 struct WorkRec {
     float4 o;        // origin xyz, .w = ray index (int bits)
     float4 d;        // direction xyz, .w = nbuf | more << 16 (int bits)
+    float4 e0;       // the first list entry: t_enter, t_exit, leaf id bits, 0
 };
 
 struct TraverseArgs {

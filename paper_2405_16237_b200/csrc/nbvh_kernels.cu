@@ -121,7 +121,9 @@ __global__ void __launch_bounds__(128, 8) k_traverse(TraverseArgs a) {
         n = traverse_smem_list(a.cut, R, a.cap, lte, ltx, lid, S, st, more, &a.ctr->err);
         NBVH_DCHECK(n >= 0 && n <= a.cap && a.cap <= kListK);
         more_long = more || n >= 3;
-        for (int j = 0; j < n; ++j) {
+        // entry 0 travels in the work record; the list keeps it only where a refill will read
+        // it back (C6: the refill resumes after the last entry of a one-entry list)
+        for (int j = (n == 1 && more) ? 0 : 1; j < n; ++j) {
             a.lst[(int64_t)j * a.n_rays + r] = make_float4(lte[j * S], ltx[j * S], __int_as_float(lid[j * S]), 0.f);
         }
         active = n > 0;

@@ -127,10 +127,7 @@ __global__ void __launch_bounds__(128, 8) k_traverse(TraverseArgs a) {
             a.lst[(int64_t)j * a.n_rays + r] = make_float4(lte[j * S], ltx[j * S], __int_as_float(lid[j * S]), 0.f);
         }
         active = n > 0;
-        if (active) {
-            a.st.nbuf[r] = n;
-            a.st.more[r] = more ? 1 : 0;
-        } else {
+        if (!active) {
             // no intersected leaf: final miss record (visibility 1 = no intersection)
             a.out.hit[r] = 0;
             a.out.t[r] = __int_as_float(0x7f800000);

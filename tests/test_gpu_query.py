@@ -402,3 +402,24 @@ def test_query_host_path_first_hit_mode_and_lod(monkeypatch):
         for k in d:
             assert np.array_equal(d[k].reshape(h[k].shape), h[k]), (lod, k)
         assert d["hit"].sum() > 1000
+
+
+@pytest.mark.parametrize("d_in,hidden", [(128, 3), (96, 4), (32, 2)])
+def test_mlp_tcgen05_many_tiles_per_slot(orc, d_in, hidden):
+    """The persistent tcgen05 MLP when every CTA runs several tiles through each slot (stage
+    reuse, mbarrier phase flips, aliased X/H buffers): all rows vs the mma.sync path, a strided
+    sample vs the double oracle."""
+    from paper_2405_16237_b200 import Context
+    L, F, npts = {64: (8, 2, 4), 128: (16, 2, 4), 96: (8, 4, 3), 32: (4, 2, 4)}[d_in]
+    ctx = Context(device=0, L=L, F=F, n_points=npts, hidden_layers=hidden)
+    layers = synth.random_mlp(d_in, hidden, 64, seed=8)
+    ctx.set_mlp(layers)
+    m = 148 * 5 * 4 * 128 + 77                                   # ~4 uses of each of 5 slots per CTA
+    x = torch.rand(m, d_in, device="cuda", generator=torch.Generator(device="cuda").manual_seed(4))
+    x = (x * 0.8 - 0.4).half()
+    z = ctx.mlp_forward(x).cpu().numpy()
+    zs = ctx.debug_mlp(x).cpu().numpy()
+    assert np.all(np.abs(z - zs) <= 2e-2 * (1 + np.abs(zs)))
+    idx = np.arange(0, m, 97)
+    want = orc.mlp_forward(layers, x.cpu().numpy()[idx].astype(np.float64))
+    assert np.all(np.abs(z[idx] - want) <= 2e-2 * (1 + np.abs(want)))

@@ -270,3 +270,34 @@ def test_t0_generated_rays_match_oracle():
     lo, hi = mid - 0.75 * side, mid + 0.75 * side
     assert np.all(rd[:, :3] >= lo - 1e-5) and np.all(rd[:, :3] <= hi + 1e-5)
     assert np.all(rd[:, :3].min(0) < lo + 0.05 * side) and np.all(rd[:, :3].max(0) > hi - 0.05 * side)
+
+
+def test_tcgen05_weight_gradients_at_bench_size(monkeypatch):
+    """k_train_dw_tc at the bench's size (2^20 rays on the 1080p scene: many K-chunks per CTA,
+    ring-buffer reuse) against the mma.sync weight-gradient kernel on the same batch."""
+    from paper_2405_16237_b200 import Context, PARAM_TABLES, dp
+    c = synth.CONFIGS["1080p"]
+    h = c["hash"]
+    ctx = Context(device=0, L=h.L, F=h.F, log2_T=h.log2_T, n_points=h.n_points, hidden_layers=h.hidden_layers)
+    sc = synth.scene_1080p(c["seeds"]["mesh"])
+    ctx.set_mesh(sc)
+    ctx.build_cut(c["leaves"])
+    n = 1 << 20
+    ctx.reserve(n)
+    ctx.set_params(PARAM_TABLES, synth.random_params_fp16(ctx.param_count(PARAM_TABLES), seed=5).astype(np.float32))
+    ctx.set_mlp(synth.random_mlp(ctx.d_in, h.hidden_layers, 64, seed=6, out_scale=1.0))
+    ctx.set_leaf_rank(np.zeros(ctx.cut(0)["n_leaves"], np.float32))
+    rays, u, xi = ctx.gen_train_rays(seed=7, step=1, n=n, box=(-1.5, -1.5, -1.5, 1.5, 1.5, 1.5))
+    n_t = ctx.param_count(PARAM_TABLES)
+    n_w = ctx.param_count(1)                                        # PARAM_WEIGHTS
+    grads = {}
+    for path in ("tc", "mma"):
+        if path == "mma":
+            monkeypatch.setenv("NBVH_DW_MMA_SYNC", "1")
+        else:
+            monkeypatch.delenv("NBVH_DW_MMA_SYNC", raising=False)
+        ctx.train_backward(rays, u, xi)
+        grads[path] = dp.grad_tensor(ctx).cpu().numpy()[n_t:n_t + n_w].astype(np.float64)
+    assert ctx.train_stats()["n_accepted"] > 100000
+    a, b = grads["tc"], grads["mma"]
+    assert np.linalg.norm(a - b) / np.linalg.norm(b) <= 1e-3

@@ -301,3 +301,32 @@ def test_tcgen05_weight_gradients_at_bench_size(monkeypatch):
     assert ctx.train_stats()["n_accepted"] > 100000
     a, b = grads["tc"], grads["mma"]
     assert np.linalg.norm(a - b) / np.linalg.norm(b) <= 1e-3
+
+
+def test_privatised_scatter_at_bench_size(monkeypatch):
+    """The hash-grid gradient scatter at the bench's size with the coarse dense levels
+    accumulated in shared memory (levels 0-2 at cfg 2) equals the all-global-reduction scatter
+    (NBVH_PRIV_BYTES=0) up to fp32 summation order."""
+    from paper_2405_16237_b200 import Context, PARAM_TABLES, dp
+    c = synth.CONFIGS["1080p"]
+    h = c["hash"]
+    ctx = Context(device=0, L=h.L, F=h.F, log2_T=h.log2_T, n_points=h.n_points, hidden_layers=h.hidden_layers)
+    ctx.set_mesh(synth.scene_1080p(c["seeds"]["mesh"]))
+    ctx.build_cut(c["leaves"])
+    n = 1 << 19
+    ctx.reserve(n)
+    ctx.set_params(PARAM_TABLES, synth.random_params_fp16(ctx.param_count(PARAM_TABLES), seed=5).astype(np.float32))
+    ctx.set_mlp(synth.random_mlp(ctx.d_in, h.hidden_layers, 64, seed=6, out_scale=1.0))
+    ctx.set_leaf_rank(np.zeros(ctx.cut(0)["n_leaves"], np.float32))
+    rays, u, xi = ctx.gen_train_rays(seed=9, step=2, n=n, box=(-1.5, -1.5, -1.5, 1.5, 1.5, 1.5))
+    n_t = ctx.param_count(PARAM_TABLES)
+    g = {}
+    for budget in ("default", "0"):
+        if budget == "0":
+            monkeypatch.setenv("NBVH_PRIV_BYTES", "0")
+        else:
+            monkeypatch.delenv("NBVH_PRIV_BYTES", raising=False)
+        ctx.train_backward(rays, u, xi)
+        g[budget] = dp.grad_tensor(ctx).cpu().numpy()[:n_t].astype(np.float64)
+    a, b = g["default"], g["0"]
+    assert np.linalg.norm(a - b) / np.linalg.norm(b) <= 1e-4

@@ -330,3 +330,42 @@ def test_privatised_scatter_at_bench_size(monkeypatch):
         g[budget] = dp.grad_tensor(ctx).cpu().numpy()[:n_t].astype(np.float64)
     a, b = g["default"], g["0"]
     assert np.linalg.norm(a - b) / np.linalg.norm(b) <= 1e-4
+
+
+def test_training_step_at_bench_size_sampled_vs_oracle():
+    """The training forward path at the bench's size (2^19 device-generated rays on the 1080p
+    scene: grid-stride tiles in every kernel) against the oracle on a strided subset of the
+    same rays: first leaf, acceptance and ground truth exact, per-sample loss within the
+    fp16-network tolerance."""
+    import oracle as orc
+    from paper_2405_16237_b200 import Context, PARAM_TABLES
+    c = synth.CONFIGS["1080p"]
+    h = c["hash"]
+    sc = synth.scene_1080p(c["seeds"]["mesh"])
+    ctx = Context(device=0, L=h.L, F=h.F, log2_T=h.log2_T, n_points=h.n_points, hidden_layers=h.hidden_layers)
+    ctx.set_mesh(sc)
+    ctx.build_cut(c["leaves"])
+    n = 1 << 19
+    ctx.reserve(n)
+    tab = synth.random_params_fp16(ctx.param_count(PARAM_TABLES), seed=5, lo=-0.5, hi=0.5)
+    ctx.set_params(PARAM_TABLES, tab.astype(np.float32))
+    layers = synth.random_mlp(ctx.d_in, h.hidden_layers, 64, seed=6, out_scale=1.0)
+    ctx.set_mlp(layers)
+    cut = ctx.cut(0)
+    rank = np.random.default_rng(3).normal(size=cut["n_leaves"]).astype(np.float32)
+    ctx.set_leaf_rank(rank)
+    rays, u, xi = ctx.gen_train_rays(seed=11, step=4, n=n, box=(-1.5, -1.5, -1.5, 1.5, 1.5, 1.5))
+    ctx.train_backward(rays, u, xi)
+    gt, acc, leaf, loss = (t.cpu().numpy() for t in ctx.debug_train_samples(n))
+    sub = np.arange(0, n, 257)
+    r_np, u_np, xi_np = rays.cpu().numpy()[sub], u.cpu().numpy()[sub], xi.cpu().numpy()[sub]
+    o = orc.train_grad(orc.Grid(h.L, h.log2_T, h.F), h.n_points, tab.reshape(-1, h.F), layers, cut["leaf_lo"],
+                       cut["leaf_hi"], rank, cut["tri_off"], cut["tris"], sc, r_np, u_np, xi_np,
+                       dom_box=orc.scene_box(sc))
+    assert np.array_equal(leaf[sub], o["first_leaf"]) and np.array_equal(acc[sub], o["accepted"])
+    a = acc[sub] == 1
+    assert a.sum() > 100
+    assert np.array_equal(gt[sub][a, 0], o["gt"][a, 0].astype(np.float32))
+    lg, lo_ = loss[sub][a].astype(np.float64), o["loss"][a]
+    close = np.abs(lg - lo_) <= 5e-2 * np.abs(lo_) + 1e-3
+    assert close.mean() >= 0.99, close.mean()

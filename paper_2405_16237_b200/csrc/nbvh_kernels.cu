@@ -116,7 +116,13 @@ __global__ void __launch_bounds__(128, 8) k_traverse(TraverseArgs a) {
     int n = 0;
     RayDev R;
     if (valid) {
-        R = load_ray(a.rays, r);
+        {   // the ray is read once: evict-first, so the hierarchy's lines stay in L1
+            const float4 ra = __ldcs(a.rays + 2 * r), rb = __ldcs(a.rays + 2 * r + 1);
+            R.o[0] = ra.x; R.o[1] = ra.y; R.o[2] = ra.z; R.tmin = ra.w;
+            R.d[0] = rb.x; R.d[1] = rb.y; R.d[2] = rb.z; R.tmax = rb.w;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) R.inv[k] = __fdiv_rn(1.0f, R.d[k]);
+        }
         SmemStack st{sm_raw + 3 * a.cap * S + threadIdx.x, S, a.cut.depth + 2};
         n = traverse_smem_list(a.cut, R, a.cap, lte, ltx, lid, S, st, more, &a.ctr->err);
         NBVH_DCHECK(n >= 0 && n <= a.cap && a.cap <= kListK);
@@ -472,7 +478,9 @@ __global__ void __launch_bounds__(kQueryWarps * 32, 1) k_query(QueryArgs a) {
             const int i = base + __popc(em & lanemask_lt());
             if (empty && i < total) {
                 const WorkRec* wr = i < n_long ? a.act_long + i : a.act + (i - n_long);
-                const float4 w0 = __ldg(&wr->o), w1 = __ldg(&wr->d), w2 = __ldg(&wr->e0);
+                // read-once streams (work records, lists) are loaded evict-first so they do not
+                // push the hash-table lines out of L1
+                const float4 w0 = __ldcs(&wr->o), w1 = __ldcs(&wr->d), w2 = __ldcs(&wr->e0);
                 const int r = __float_as_int(w0.w), st = __float_as_int(w1.w);
                 S.te[lane] = w2.x;
                 S.tx[lane] = w2.y;
@@ -525,7 +533,7 @@ __global__ void __launch_bounds__(kQueryWarps * 32, 1) k_query(QueryArgs a) {
                 te = S.te[lane];
                 tx = S.tx[lane];
             } else {
-                const float4 e = a.lst[li];
+                const float4 e = __ldcs(a.lst + li);
                 te = e.x;
                 tx = e.y;
                 S.leaf[lane] = __float_as_int(e.z);
@@ -637,7 +645,7 @@ __global__ void __launch_bounds__(kQueryWarps * 32, 1) k_query(QueryArgs a) {
                     }
                 }
                 if (!done) {
-                    const float next_te = a.lst[(int64_t)(pos - base) * a.n_rays + r].x;
+                    const float next_te = __ldcs(a.lst + (int64_t)(pos - base) * a.n_rays + r).x;
                     done = bleaf >= 0 && next_te > bt;                     // front-to-back termination
                 }
             }

@@ -419,8 +419,26 @@ __device__ __forceinline__ void stage_levels(const GridDev& g, LevelSm* lv, int 
 }
 
 // 256-bit read-only global load (sm_100: LDG.E.ENL2.256)
+// Table gathers carry L1::evict_last: the tables are the data worth keeping in L1 (the
+// read-once streams are loaded evict-first).  Without L1 allocation the hashed gathers lose
+// their L1 hits (1522 vs 1686 Mrays/s, profiles/NOTES.md).
+template <typename E>
+__device__ __forceinline__ E ldg_el(const E* p);
+template <>
+__device__ __forceinline__ uint32_t ldg_el<uint32_t>(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.global.nc.L1::evict_last.b32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+template <>
+__device__ __forceinline__ uint2 ldg_el<uint2>(const uint2* p) {
+    uint2 v;
+    asm volatile("ld.global.nc.L1::evict_last.v2.b32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+    return v;
+}
+
 __device__ __forceinline__ void ldg256(const void* p, uint32_t (&r)[8]) {
-    asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+    asm volatile("ld.global.nc.L1::evict_last.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                  : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
                  : "l"(p));
 }
@@ -529,7 +547,7 @@ __device__ __forceinline__ void encode_issue(const LevelSm* lv, const void* tab,
             // 32-bit entry index (n_entries < 2^32), one IMAD.WIDE.U32 per gather address
 #pragma unroll
             for (int k = 0; k < 8; ++k)
-                G.v[j][k] = __ldg(T + (P.off + (hx[k & 1] ^ hy[(k >> 1) & 1] ^ hz[(k >> 2) & 1])));
+                G.v[j][k] = ldg_el(T + (P.off + (hx[k & 1] ^ hy[(k >> 1) & 1] ^ hz[(k >> 2) & 1])));
         }
     }
 }

@@ -173,9 +173,12 @@ nbvh_status nbvh_get_cut(const nbvh_ctx* ctx, int32_t lod, float* leaf_lo, float
  * queries on one context must be ordered by the caller. */
 nbvh_status nbvh_query(nbvh_ctx* ctx, const nbvh_ray* d_rays, int64_t n, int32_t lod, nbvh_hits d_out,
                        void* stream);
-/* Same computation from HOST rays into HOST results: copies rays host->device, runs
- * nbvh_query, copies the results device->host and synchronises the stream (the
- * end-to-end path).  Host buffers should be pinned for full copy bandwidth. */
+/* Same computation from HOST rays into HOST results (the end-to-end path): the rays are
+ * cut into block-interleaved chunks (6 for n >= 2^20; NBVH_HOST_WEIGHTS / NBVH_HOST_CONTIG
+ * are tuning hooks) whose uploads, queries (alternating two streams with disjoint workspace
+ * slices) and downloads overlap; returns after the last download (synchronous).  Host
+ * buffers should be pinned for full copy bandwidth.  NBVH_HOST_TIMELINE=1 prints the chunk
+ * timeline to stderr. */
 nbvh_status nbvh_query_host(nbvh_ctx* ctx, const nbvh_ray* h_rays, int64_t n, int32_t lod, nbvh_hits h_out,
                             void* stream);
 /* Counters of the last query call; synchronises that call's stream to read them.  Also

@@ -101,8 +101,104 @@ __device__ __forceinline__ int traverse_smem_list(const CutDev& cut, const RayDe
     return n;
 }
 
+// Packet variant for coherent rays (e.g. primary camera rays, 32 neighbouring pixels per
+// warp): the warp walks ONE shared node stack; every lane tests both children against its
+// own ray, inserts the leaves it hits into its own list and votes for the subtrees it still
+// needs (a subtree is skipped only when no lane needs it).  Node loads become one broadcast
+// per warp and the loop is divergence-free.  Child boxes lie inside their parent's (exact
+// unions, monotone rounding), so a lane that misses a node misses its whole subtree, and a
+// lane that pruned a subtree rejects its leaves in `consider` with the same `dropped`
+// effect: every lane's list and `more` flag equal the per-thread traversal's.
+__device__ __forceinline__ int traverse_packet(const CutDev& cut, const RayDev& R, bool valid, int cap, float* lte,
+                                               float* ltx, int* lid, int S, int* wstack, int stack_cap, bool& more,
+                                               int* err) {
+    int n = 0;
+    bool dropped = false;
+    auto consider = [&](int leaf, float te, float tx) {
+        int pos;
+        if (n == cap) {
+            if (!key_less(te, leaf, lte[(cap - 1) * S], lid[(cap - 1) * S])) {
+                dropped = true;
+                return;
+            }
+            dropped = true;
+            pos = cap - 1;
+        } else {
+            pos = n++;
+        }
+        while (pos > 0) {
+            const float pte = lte[(pos - 1) * S];
+            const int pid = lid[(pos - 1) * S];
+            if (!key_less(te, leaf, pte, pid)) break;
+            lte[pos * S] = pte;
+            ltx[pos * S] = ltx[(pos - 1) * S];
+            lid[pos * S] = pid;
+            --pos;
+        }
+        lte[pos * S] = te;
+        ltx[pos * S] = tx;
+        lid[pos * S] = leaf;
+    };
+    const int lane = threadIdx.x & 31;
+    if (cut.n_leaves == 1) {
+        float4 a = __ldg(cut.leaf_box), b = __ldg(cut.leaf_box + 1);
+        float lo[3] = {a.x, a.y, a.z}, hi[3] = {b.x, b.y, b.z}, te, tx;
+        if (valid && slab(R, lo, hi, te, tx)) consider(0, te, tx);
+    } else {
+        int sp = 1;                                     // warp-uniform
+        if (lane == 0) wstack[0] = 0;
+        __syncwarp();
+        while (sp > 0) {
+            const int node = wstack[--sp];
+            __syncwarp();                               // everyone read the top before it is reused
+            const float4* p = reinterpret_cast<const float4*>(cut.inner + node);
+            const float4 q0 = __ldg(p), q1 = __ldg(p + 1), q2 = __ldg(p + 2), q3 = __ldg(p + 3);
+            const float llo[3] = {q0.x, q0.y, q0.z}, lhi[3] = {q0.w, q1.x, q1.y};
+            const float rlo[3] = {q1.z, q1.w, q2.x}, rhi[3] = {q2.y, q2.z, q2.w};
+            const int cl = __float_as_int(q3.x), cr = __float_as_int(q3.y);
+            float lte_ = 0.f, ltx_ = 0.f, rte_ = 0.f, rtx_ = 0.f;
+            bool hl = false, hr = false;
+            if (valid) {
+                hl = slab(R, llo, lhi, lte_, ltx_);
+                hr = slab(R, rlo, rhi, rte_, rtx_);
+                if (hl && cl < 0) consider(-1 - cl, lte_, ltx_);
+                if (hr && cr < 0) consider(-1 - cr, rte_, rtx_);
+            }
+            bool pl = hl && cl >= 0, pr = hr && cr >= 0;
+            if (n == cap) {                             // this lane's subtrees entering after its cap-th key
+                const float last = lte[(cap - 1) * S];
+                if (pl && lte_ > last) { pl = false; dropped = true; }
+                if (pr && rte_ > last) { pr = false; dropped = true; }
+            }
+            const unsigned vl = __ballot_sync(0xffffffffu, pl), vr = __ballot_sync(0xffffffffu, pr);
+            if (sp + 2 > stack_cap) {
+                if (lane == 0) atomicOr(err, 1);
+                break;
+            }
+            if (vl && vr) {
+                // nearer child first for most lanes that want both
+                const unsigned both = __ballot_sync(0xffffffffu, pl && pr);
+                const unsigned lfirst = __ballot_sync(0xffffffffu, pl && pr && lte_ <= rte_);
+                const bool l_first = 2 * __popc(lfirst) >= __popc(both);
+                if (lane == 0) {
+                    wstack[sp] = l_first ? cr : cl;
+                    wstack[sp + 1] = l_first ? cl : cr;
+                }
+                sp += 2;
+            } else if (vl || vr) {
+                if (lane == 0) wstack[sp] = vl ? cl : cr;
+                sp += 1;
+            }
+            __syncwarp();
+        }
+    }
+    more = dropped;
+    return n;
+}
+
 // One thread per ray: traversal stack and ordered list in shared memory (stack rows =
 // cut depth + 2, list rows = 3 * cap).
+template <bool kPacket>
 __global__ void __launch_bounds__(128, 8) k_traverse(TraverseArgs a) {
     extern __shared__ int sm_raw[];
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -115,16 +211,22 @@ __global__ void __launch_bounds__(128, 8) k_traverse(TraverseArgs a) {
     bool more_long = false, more = false;
     int n = 0;
     RayDev R;
-    if (valid) {
-        {   // the ray is read once: evict-first, so the hierarchy's lines stay in L1
-            const float4 ra = __ldcs(a.rays + 2 * r), rb = __ldcs(a.rays + 2 * r + 1);
-            R.o[0] = ra.x; R.o[1] = ra.y; R.o[2] = ra.z; R.tmin = ra.w;
-            R.d[0] = rb.x; R.d[1] = rb.y; R.d[2] = rb.z; R.tmax = rb.w;
+    if (valid) {   // the ray is read once: evict-first, so the hierarchy's lines stay in L1
+        const float4 ra = __ldcs(a.rays + 2 * r), rb = __ldcs(a.rays + 2 * r + 1);
+        R.o[0] = ra.x; R.o[1] = ra.y; R.o[2] = ra.z; R.tmin = ra.w;
+        R.d[0] = rb.x; R.d[1] = rb.y; R.d[2] = rb.z; R.tmax = rb.w;
 #pragma unroll
-            for (int k = 0; k < 3; ++k) R.inv[k] = __fdiv_rn(1.0f, R.d[k]);
+        for (int k = 0; k < 3; ++k) R.inv[k] = __fdiv_rn(1.0f, R.d[k]);
+    }
+    if constexpr (kPacket) {      // every lane of the warp walks the shared stack
+        int* wstack = sm_raw + 3 * a.cap * S + (threadIdx.x >> 5) * (a.cut.depth + 2);
+        n = traverse_packet(a.cut, R, valid, a.cap, lte, ltx, lid, S, wstack, a.cut.depth + 2, more, &a.ctr->err);
+    }
+    if (valid) {
+        if constexpr (!kPacket) {
+            SmemStack st{sm_raw + 3 * a.cap * S + threadIdx.x, S, a.cut.depth + 2};
+            n = traverse_smem_list(a.cut, R, a.cap, lte, ltx, lid, S, st, more, &a.ctr->err);
         }
-        SmemStack st{sm_raw + 3 * a.cap * S + threadIdx.x, S, a.cut.depth + 2};
-        n = traverse_smem_list(a.cut, R, a.cap, lte, ltx, lid, S, st, more, &a.ctr->err);
         NBVH_DCHECK(n >= 0 && n <= a.cap && a.cap <= kListK);
         more_long = more || n >= 3;
         // entry 0 travels in the work record; the list keeps it only where a refill will read
@@ -802,10 +904,17 @@ cudaError_t launch_query(const QueryArgs& a, int64_t max_work, cudaStream_t s) {
     return cudaErrorInvalidValue;
 }
 
+// NBVH_TRAVERSE=packet selects the warp-packet traversal (A/B hook; see traverse_packet).
 cudaError_t launch_traverse(const TraverseArgs& a, cudaStream_t s) {
     const int64_t blocks = (a.n_rays + 127) / 128;
-    const size_t smem = (size_t)(a.cut.depth + 2 + 3 * a.cap) * 128 * sizeof(int);
-    k_traverse<<<(unsigned)blocks, 128, smem, s>>>(a);
+    const char* ev = std::getenv("NBVH_TRAVERSE");
+    if (ev && ev[0] == 'p') {
+        const size_t smem = (size_t)(3 * a.cap * 128 + 4 * (a.cut.depth + 2)) * sizeof(int);
+        k_traverse<true><<<(unsigned)blocks, 128, smem, s>>>(a);
+    } else {
+        const size_t smem = (size_t)(a.cut.depth + 2 + 3 * a.cap) * 128 * sizeof(int);
+        k_traverse<false><<<(unsigned)blocks, 128, smem, s>>>(a);
+    }
     return cudaGetLastError();
 }
 

@@ -423,3 +423,25 @@ def test_mlp_tcgen05_many_tiles_per_slot(orc, d_in, hidden):
     idx = np.arange(0, m, 97)
     want = orc.mlp_forward(layers, x.cpu().numpy()[idx].astype(np.float64))
     assert np.all(np.abs(z[idx] - want) <= 2e-2 * (1 + np.abs(want)))
+
+
+@pytest.mark.parametrize("cfg_name,list_cap", [("tiny", 3), ("tiny", 12), ("1080p", 12)])
+def test_packet_traversal_identical(monkeypatch, cfg_name, list_cap):
+    """NBVH_TRAVERSE=packet (one node stack per warp, per-lane lists and votes) produces the
+    same per-ray lists as the per-thread traversal: the whole query output is bit-identical,
+    on coherent camera rays and on incoherent random rays."""
+    ctx, sc, tab, layers = _mk_ctx(cfg_name, list_cap=list_cap, table_seed=9, seed=6)
+    if cfg_name == "tiny":
+        rays = _rays_tiny(5000)
+    else:
+        c = synth.CONFIGS["1080p"]
+        rays = np.concatenate([synth.camera_rays(*c["res"], c["eye"], vfov_deg=c["vfov"]),
+                               synth.random_rays(100000, seed=3)])
+    ctx.reserve(rays.shape[0])
+    d_rays = torch.from_numpy(rays).cuda()
+    monkeypatch.delenv("NBVH_TRAVERSE", raising=False)
+    a = {k: v.clone() for k, v in ctx.query(d_rays).items()}
+    monkeypatch.setenv("NBVH_TRAVERSE", "packet")
+    b = ctx.query(d_rays)
+    for k in a:
+        assert torch.equal(a[k], b[k]), k

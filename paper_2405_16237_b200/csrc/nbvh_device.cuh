@@ -777,6 +777,102 @@ __device__ __forceinline__ void mlp_rows16(const MlpSmem& s, int hidden, const _
     z[(r0 + g + 8) * 8 + 2 * t + 1] = o[3];
 }
 
+// fp16-accumulating m16n8k16 (the accumulator is two f16x2 registers: rows g and g+8,
+// columns 2t, 2t+1) -- the precision tiny-cuda-nn's fully fused MLP uses (C34)
+__device__ __forceinline__ void mma16816h(uint32_t (&c)[2], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f16.f16.f16.f16 {%0,%1}, {%2,%3,%4,%5}, {%6,%7}, {%0,%1};\n"
+        : "+r"(c[0]), "+r"(c[1])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t h2_bits(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
+__device__ __forceinline__ uint32_t relu_h2(uint32_t v) {
+    return h2_bits(__hmax2(*reinterpret_cast<__half2*>(&v), __float2half2_rn(0.f)));
+}
+
+// mlp_rows16 with fp16 accumulation: half the accumulator registers, the next layer's A
+// fragment is the accumulator itself after ReLU.
+template <int D>
+__device__ __forceinline__ void mlp_rows16h(const MlpSmem& s, int hidden, const __half* x, int r0, float* z, int lane) {
+    const int g = lane >> 2, t = lane & 3;
+    uint32_t acc[8][2];
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+        const uint32_t b = h2_bits(__floats2half2_rn(s.b[nt * 8 + 2 * t], s.b[nt * 8 + 2 * t + 1]));
+        acc[nt][0] = b;
+        acc[nt][1] = b;
+    }
+    const uint32_t xa = (uint32_t)__cvta_generic_to_shared(x + (r0 + (lane & 15)) * (D + 8) + (lane >> 4) * 8);
+    const uint32_t wa = (uint32_t)__cvta_generic_to_shared(s.w0 + ((lane & 7) + ((lane >> 4) << 3)) * (D + 8) +
+                                                           ((lane >> 3) & 1) * 8);
+#pragma unroll
+    for (int kb = 0; kb < D / 16; ++kb) {
+        uint32_t a[4];
+        ldsm_x4(xa + kb * 32, a[0], a[1], a[2], a[3]);
+#pragma unroll
+        for (int np = 0; np < 4; ++np) {
+            uint32_t b0, b1, b2, b3;
+            ldsm_x4(wa + np * 16 * (D + 8) * 2 + kb * 32, b0, b1, b2, b3);
+            mma16816h(acc[2 * np], a, b0, b1);
+            mma16816h(acc[2 * np + 1], a, b2, b3);
+        }
+    }
+    uint32_t h[4][4];
+#pragma unroll
+    for (int kb = 0; kb < 4; ++kb) {
+        h[kb][0] = relu_h2(acc[2 * kb][0]);
+        h[kb][1] = relu_h2(acc[2 * kb][1]);
+        h[kb][2] = relu_h2(acc[2 * kb + 1][0]);
+        h[kb][3] = relu_h2(acc[2 * kb + 1][1]);
+    }
+    for (int layer = 1; layer < hidden; ++layer) {
+        const __half* W = s.wh + (layer - 1) * 64 * 72;
+        const float* bb = s.b + layer * 64;
+#pragma unroll
+        for (int nt = 0; nt < 8; ++nt) {
+            const uint32_t b = h2_bits(__floats2half2_rn(bb[nt * 8 + 2 * t], bb[nt * 8 + 2 * t + 1]));
+            acc[nt][0] = b;
+            acc[nt][1] = b;
+        }
+        const uint32_t wb = (uint32_t)__cvta_generic_to_shared(W + ((lane & 7) + ((lane >> 4) << 3)) * 72 +
+                                                               ((lane >> 3) & 1) * 8);
+#pragma unroll
+        for (int kb = 0; kb < 4; ++kb) {
+#pragma unroll
+            for (int np = 0; np < 4; ++np) {
+                uint32_t b0, b1, b2, b3;
+                ldsm_x4(wb + np * 16 * 72 * 2 + kb * 32, b0, b1, b2, b3);
+                mma16816h(acc[2 * np], h[kb], b0, b1);
+                mma16816h(acc[2 * np + 1], h[kb], b2, b3);
+            }
+        }
+#pragma unroll
+        for (int kb = 0; kb < 4; ++kb) {
+            h[kb][0] = relu_h2(acc[2 * kb][0]);
+            h[kb][1] = relu_h2(acc[2 * kb][1]);
+            h[kb][2] = relu_h2(acc[2 * kb + 1][0]);
+            h[kb][3] = relu_h2(acc[2 * kb + 1][1]);
+        }
+    }
+    // output layer: 64 -> 8, linear; fp32 accumulation for the outputs
+    float o[4];
+    {
+        const float* bb = s.b + hidden * 64;
+        o[0] = bb[2 * t]; o[1] = bb[2 * t + 1]; o[2] = o[0]; o[3] = o[1];
+    }
+    const uint32_t wo = (uint32_t)__cvta_generic_to_shared(s.wo + (lane & 7) * 72 + ((lane >> 3) & 1) * 8);
+#pragma unroll
+    for (int kb = 0; kb < 4; ++kb) {
+        uint32_t b0, b1;
+        ldsm_x2(wo + kb * 32, b0, b1);
+        mma16816(o, h[kb], b0, b1);
+    }
+    z[(r0 + g) * 8 + 2 * t] = o[0];
+    z[(r0 + g) * 8 + 2 * t + 1] = o[1];
+    z[(r0 + g + 8) * 8 + 2 * t] = o[2];
+    z[(r0 + g + 8) * 8 + 2 * t + 1] = o[3];
+}
+
 // ------------------------------------------------------------------ decode
 // sigmoid in fp32 from correctly rounded operations only (C27), so the host's
 // logic replay reproduces it bit for bit: e^x by x = n ln2 + r (two fmas), a degree-7

@@ -684,8 +684,8 @@ __global__ void __launch_bounds__(kQueryWarps * 32, 1) k_query(QueryArgs a) {
                             smem_raw + plan.warp0 + plan.per_warp * (size_t)(grp * kGroupWarps), plan.per_warp,
                             plan.z);
         } else {
-            mlp_rows16<D>(ms, a.m.hidden, feat, 0, zt, lane);
-            if (kWarpQ > 16 && nv > 16) mlp_rows16<D>(ms, a.m.hidden, feat, 16, zt, lane);
+            mlp_rows16h<D>(ms, a.m.hidden, feat, 0, zt, lane);
+            if (kWarpQ > 16 && nv > 16) mlp_rows16h<D>(ms, a.m.hidden, feat, 16, zt, lane);
         }
         __syncwarp();
         // (F) decode, best hit, front-to-back termination

@@ -66,10 +66,12 @@ __device__ __forceinline__ int traverse_smem_list(const CutDev& cut, const RayDe
         float lo[3] = {a.x, a.y, a.z}, hi[3] = {b.x, b.y, b.z}, te, tx;
         if (slab(R, lo, hi, te, tx)) consider(0, te, tx);
     } else {
+        // the node to visit next lives in a register; only the farther child of a node with
+        // two wanted children is pushed (same visiting order as push-both-then-pop)
         stack.sp = 0;
-        stack.push(0);
-        while (stack.sp > 0) {
-            const float4* p = reinterpret_cast<const float4*>(cut.inner + stack.pop());
+        int node = 0;
+        while (true) {
+            const float4* p = reinterpret_cast<const float4*>(cut.inner + node);
             float4 q0 = __ldg(p), q1 = __ldg(p + 1), q2 = __ldg(p + 2), q3 = __ldg(p + 3);
             float llo[3] = {q0.x, q0.y, q0.z}, lhi[3] = {q0.w, q1.x, q1.y};
             float rlo[3] = {q1.z, q1.w, q2.x}, rhi[3] = {q2.y, q2.z, q2.w};
@@ -85,15 +87,18 @@ __device__ __forceinline__ int traverse_smem_list(const CutDev& cut, const RayDe
                 if (pl && lte_ > last) { pl = false; dropped = true; }
                 if (pr && rte_ > last) { pr = false; dropped = true; }
             }
-            if (stack.sp + 2 > stack.cap) { atomicOr(err, 1); break; }
             if (pl && pr) {
-                bool l_first = lte_ <= rte_;
+                if (stack.sp + 1 > stack.cap) { atomicOr(err, 1); break; }
+                const bool l_first = lte_ <= rte_;
                 stack.push(l_first ? cr : cl);
-                stack.push(l_first ? cl : cr);
+                node = l_first ? cl : cr;
             } else if (pl) {
-                stack.push(cl);
+                node = cl;
             } else if (pr) {
-                stack.push(cr);
+                node = cr;
+            } else {
+                if (stack.sp == 0) break;
+                node = stack.pop();
             }
         }
     }

@@ -58,29 +58,44 @@ struct BvhHit {
     int tri, slot;
 };
 
+// Conservative fp32 box of a base-BVH node: a relative slack, so the fp32 slab test never
+// rejects a box that the double-precision triangle test could hit.
+__device__ __forceinline__ bool bvh_box(const BvhNode& nd, const RayDev& R, float& te, float& tx) {
+    float lo[3], hi[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const float e = 1e-5f * (fabsf(nd.lo[k]) + fabsf(nd.hi[k]) + 1e-3f);
+        lo[k] = nd.lo[k] - e;
+        hi[k] = nd.hi[k] + e;
+    }
+    return slab(R, lo, hi, te, tx);
+}
+
 // Closest hit below node `root` within [t0, t1]; ties by lowest original triangle id (C32).
-// stack_col: this thread's column of a shared-memory stack [kBvhStack][stride].
+// stack_col: this thread's column of a shared-memory stack [stack_rows][stride]; the host
+// sizes stack_rows >= base-BVH depth, which the farther-child-only stack never exceeds.
+// Both children are tested where their parent is visited (their boxes are loaded there
+// anyway, for the near-first order); the nearer one is visited next from registers and only
+// the farther one is pushed, then re-tested when popped because the best hit may have
+// tightened t_cut meanwhile.  Nodes are visited in the same order and under the same test
+// as a push-both / test-on-pop traversal, so the result is the same.
 __device__ __forceinline__ BvhHit bvh_closest(const BvhNode* nodes, const float* tri_v, const int32_t* tri_id,
                                               int root, const RayDev& R, float t0, float t1, int* stack_col,
-                                              int stride) {
+                                              int stride, int stack_rows) {
     const double o[3] = {R.o[0], R.o[1], R.o[2]}, d[3] = {R.d[0], R.d[1], R.d[2]};
     BvhHit h{false, 0.0, 0.0, 0.0, -1, -1};
-    int sp = 0;
-    stack_col[(sp++) * stride] = root;
     float t_cut = t1 * 1.00001f + 1e-6f;        // conservative upper bound: segment end, then best hit
-    while (sp > 0) {
-        const BvhNode nd = nodes[stack_col[(--sp) * stride]];
-        float lo[3], hi[3], te, tx;
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            const float e = 1e-5f * (fabsf(nd.lo[k]) + fabsf(nd.hi[k]) + 1e-3f);
-            lo[k] = nd.lo[k] - e;
-            hi[k] = nd.hi[k] + e;
-        }
-        if (!slab(R, lo, hi, te, tx)) continue;
-        // a node entering beyond the best hit so far holds no closer (or tying) hit: the
-        // conservative boxes and the relative slack keep this exact w.r.t. the double test
-        if (te > t_cut || tx < t0 * 0.99999f - 1e-6f) continue;
+    const float t_lo = t0 * 0.99999f - 1e-6f;
+    // a node entering beyond the best hit so far holds no closer (or tying) hit: the
+    // conservative boxes and the relative slack keep this exact w.r.t. the double test
+    auto admit = [&](const BvhNode& nd) {
+        float te, tx;
+        return bvh_box(nd, R, te, tx) && !(te > t_cut) && !(tx < t_lo);
+    };
+    int sp = 0;
+    BvhNode nd = nodes[root];
+    bool have = admit(nd);
+    while (have) {
         if (nd.b < 0) {
             for (int j = nd.a; j < nd.a - nd.b; ++j) {
                 double th, b1, b2;
@@ -92,19 +107,33 @@ __device__ __forceinline__ BvhHit bvh_closest(const BvhNode* nodes, const float*
                     }
                 }
             }
-        } else if (sp + 2 <= kBvhStack) {
-            // nearer child first (box centre along the ray) so the best hit tightens t_cut early
-            const BvhNode& ca = nodes[nd.a];
-            const BvhNode& cb = nodes[nd.b];
-            float da = 0.f, db = 0.f;
+        } else {
+            const BvhNode ca = nodes[nd.a];
+            const BvhNode cb = nodes[nd.b];
+            const bool ha = admit(ca), hb = admit(cb);
+            if (ha && hb) {
+                // nearer child first (box centre along the ray) so the best hit tightens t_cut early
+                float da = 0.f, db = 0.f;
 #pragma unroll
-            for (int k = 0; k < 3; ++k) {
-                da = fmaf(ca.lo[k] + ca.hi[k], R.d[k], da);
-                db = fmaf(cb.lo[k] + cb.hi[k], R.d[k], db);
+                for (int k = 0; k < 3; ++k) {
+                    da = fmaf(ca.lo[k] + ca.hi[k], R.d[k], da);
+                    db = fmaf(cb.lo[k] + cb.hi[k], R.d[k], db);
+                }
+                const bool a_first = da <= db;
+                NBVH_DCHECK(sp < stack_rows);
+                if (sp < stack_rows) stack_col[(sp++) * stride] = a_first ? nd.b : nd.a;
+                nd = a_first ? ca : cb;
+                continue;
             }
-            const bool a_first = da <= db;
-            stack_col[(sp++) * stride] = a_first ? nd.b : nd.a;
-            stack_col[(sp++) * stride] = a_first ? nd.a : nd.b;
+            if (ha || hb) {
+                nd = ha ? ca : cb;
+                continue;
+            }
+        }
+        have = false;
+        while (sp > 0 && !have) {
+            nd = nodes[stack_col[(--sp) * stride]];
+            have = admit(nd);
         }
     }
     return h;

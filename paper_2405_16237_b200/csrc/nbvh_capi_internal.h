@@ -100,6 +100,7 @@ namespace nbvh {
 nbvh_status fail(nbvh_ctx* c, nbvh_status s, const std::string& msg);
 nbvh_status cuda_fail(nbvh_ctx* c, cudaError_t e, const char* where);
 nbvh_status check_device(nbvh_ctx* c);
+int32_t base_bvh_depth(const HostScene& sc);   // levels of the base BVH (root = 1)
 GridDev make_grid(const nbvh_ctx* c, int lod);
 MlpDev make_mlp(const nbvh_ctx* c);
 CutDev make_cut(const nbvh_ctx* c, int lod);

@@ -19,6 +19,7 @@ namespace nbvh {
 
 struct MeshArgs {
     const BvhNode* nodes;
+    int32_t bvh_rows;        // closest-hit stack rows (>= base-BVH depth)
     const float* tri_v;
     const float* tri_n;
     const float* tri_a;
@@ -29,12 +30,12 @@ struct MeshArgs {
 };
 
 __global__ void __launch_bounds__(128) k_mesh_intersect(MeshArgs a) {
-    extern __shared__ int stk_raw[];                      // stack column [kBvhStack][128]
+    extern __shared__ int stk_raw[];                      // stack column [bvh_rows][128]
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= a.n) return;
     const RayDev R = load_ray(a.rays, r);
     const BvhHit h = R.tmin <= R.tmax
-                         ? bvh_closest(a.nodes, a.tri_v, a.tri_id, 0, R, R.tmin, R.tmax, stk_raw + threadIdx.x, 128)
+                         ? bvh_closest(a.nodes, a.tri_v, a.tri_id, 0, R, R.tmin, R.tmax, stk_raw + threadIdx.x, 128, a.bvh_rows)
                          : BvhHit{false, 0.0, 0.0, 0.0, -1, -1};
     a.out.hit[r] = h.found ? 1 : 0;
     a.out.t[r] = h.found ? (float)h.t : __int_as_float(0x7f800000);
@@ -136,7 +137,7 @@ __global__ void __launch_bounds__(256) k_pt_shade(ShadeArgs s) {
     if ((threadIdx.x & 31) == 0 && m) atomicAdd(s.alive, __popc(m));
 }
 
-static int32_t base_bvh_depth(const HostScene& sc) {
+int32_t base_bvh_depth(const HostScene& sc) {
     if (sc.nodes.empty()) return 0;
     std::vector<std::pair<int32_t, int32_t>> todo{{0, 1}};
     int32_t depth = 0;
@@ -164,9 +165,10 @@ extern "C" nbvh_status nbvh_intersect_mesh(nbvh_ctx* c, const nbvh_ray* rays, in
         return fail(c, NBVH_EINVAL, "intersect_mesh: null pointer or negative n");
     if (n == 0) return NBVH_OK;
     if (c->base_depth < 0) c->base_depth = base_bvh_depth(c->sc);
-    if (c->base_depth + 1 > kBvhStack) return fail(c, NBVH_EINVAL, "intersect_mesh: base BVH deeper than the stack");
+    if (c->base_depth > kBvhStack) return fail(c, NBVH_EINVAL, "intersect_mesh: base BVH deeper than the stack");
     MeshArgs a{};
     a.nodes = c->dscene.nodes;
+    a.bvh_rows = c->base_depth > 0 ? c->base_depth : 1;
     a.tri_v = c->dscene.tri_v;
     a.tri_n = c->dscene.tri_n;
     a.tri_a = c->dscene.tri_a;
@@ -175,7 +177,7 @@ extern "C" nbvh_status nbvh_intersect_mesh(nbvh_ctx* c, const nbvh_ray* rays, in
     a.n = n;
     a.out = HitsDev{out.hit, out.t, out.normal, out.albedo, out.leaf, out.n_queries};
     const int64_t blocks = (n + 127) / 128;
-    k_mesh_intersect<<<(unsigned)blocks, 128, kBvhStack * 128 * sizeof(int), (cudaStream_t)stream>>>(a);
+    k_mesh_intersect<<<(unsigned)blocks, 128, (size_t)a.bvh_rows * 128 * sizeof(int), (cudaStream_t)stream>>>(a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(c, e, "intersect_mesh");
     return NBVH_OK;

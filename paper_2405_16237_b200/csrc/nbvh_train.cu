@@ -255,7 +255,7 @@ static cudaError_t launch_train_fd(const TrainArgs& a, int64_t n, int64_t w_off,
     k_train_select<<<blocks_n, 128, (size_t)(a.cut.depth + 2) * 128 * sizeof(int), s>>>(a);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (ev) cudaEventRecord(ev[1], s);
-    k_train_label<<<blocks_n, 128, 64 * 128 * sizeof(int), s>>>(a);
+    k_train_label<<<blocks_n, 128, (size_t)a.bvh_rows * 128 * sizeof(int), s>>>(a);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (ev) cudaEventRecord(ev[2], s);
     const int tiles = (int)((n + kTileQ - 1) / kTileQ);
@@ -369,6 +369,9 @@ extern "C" nbvh_status nbvh_train_backward(nbvh_ctx* c, const nbvh_ray* rays, in
     a.rank_hmax = (rmax - rmin) + 1e-6f;
     a.leaf_base = c->dcut[lod].leaf_base;
     a.nodes = c->dscene.nodes;
+    if (c->base_depth < 0) c->base_depth = base_bvh_depth(c->sc);
+    if (c->base_depth > kBvhStack) return fail(c, NBVH_EINVAL, "train: base BVH deeper than the stack");
+    a.bvh_rows = c->base_depth > 0 ? c->base_depth : 1;
     a.tri_v = c->dscene.tri_v;
     a.tri_n = c->dscene.tri_n;
     a.tri_a = c->dscene.tri_a;

@@ -30,6 +30,7 @@ struct TrainArgs {
     float rank_min, rank_hmax;   // fp32: min rank, (max-min)+eps (C18)
     const int32_t* leaf_base;
     const BvhNode* nodes;
+    int32_t bvh_rows;        // closest-hit stack rows (>= base-BVH depth)
     const float* tri_v;
     const float* tri_n;
     const float* tri_a;
@@ -117,9 +118,9 @@ __global__ void __launch_bounds__(128) k_train_label(TrainArgs a) {
     const int r = a.s_ray[i];
     RayDev R = load_ray(a.rays, r);
     const float t0 = a.s_t0[i], t1 = a.s_t1[i];
-    extern __shared__ int stk_raw[];                     // stack column [kBvhStack][128]
+    extern __shared__ int stk_raw[];                     // stack column [bvh_rows][128]
     const BvhHit h = bvh_closest(a.nodes, a.tri_v, a.tri_id, a.leaf_base[a.s_leaf[i]], R, t0, t1,
-                                 stk_raw + threadIdx.x, 128);
+                                 stk_raw + threadIdx.x, 128, a.bvh_rows);
     float gt[9];
 #pragma unroll
     for (int k = 0; k < 9; ++k) gt[k] = 0.f;

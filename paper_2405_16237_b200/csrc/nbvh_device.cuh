@@ -165,10 +165,12 @@ __device__ int collect_leaves(const CutDev& cut, const RayDev& R, bool has_after
         float lo[3] = {a.x, a.y, a.z}, hi[3] = {b.x, b.y, b.z}, te, tx;
         if (slab(R, lo, hi, te, tx)) consider(0, te, tx);
     } else {
+        // the next node lives in a register; only the farther of two wanted children is
+        // pushed (same visiting order as push-both-then-pop)
         stack.sp = 0;
-        stack.push(0);
-        while (stack.sp > 0) {
-            const float4* p = reinterpret_cast<const float4*>(cut.inner + stack.pop());
+        int node = 0;
+        while (true) {
+            const float4* p = reinterpret_cast<const float4*>(cut.inner + node);
             float4 q0 = __ldg(p), q1 = __ldg(p + 1), q2 = __ldg(p + 2), q3 = __ldg(p + 3);
             float llo[3] = {q0.x, q0.y, q0.z}, lhi[3] = {q0.w, q1.x, q1.y};
             float rlo[3] = {q1.z, q1.w, q2.x}, rhi[3] = {q2.y, q2.z, q2.w};
@@ -181,16 +183,19 @@ __device__ int collect_leaves(const CutDev& cut, const RayDev& R, bool has_after
             bool pl = hl && cl >= 0, pr = hr && cr >= 0;
             if (pl && full_and_beyond(lte_)) { pl = false; pruned = true; }
             if (pr && full_and_beyond(rte_)) { pr = false; pruned = true; }
-            if (stack.sp + 2 > stack.cap) { if (err_flag) atomicOr(err_flag, 1); break; }
-            // push the farther child first so the nearer is visited first
+            // the nearer child is visited next, the farther one later
             if (pl && pr) {
-                bool l_first = lte_ <= rte_;
+                if (stack.sp + 1 > stack.cap) { if (err_flag) atomicOr(err_flag, 1); break; }
+                const bool l_first = lte_ <= rte_;
                 stack.push(l_first ? cr : cl);
-                stack.push(l_first ? cl : cr);
+                node = l_first ? cl : cr;
             } else if (pl) {
-                stack.push(cl);
+                node = cl;
             } else if (pr) {
-                stack.push(cr);
+                node = cr;
+            } else {
+                if (stack.sp == 0) break;
+                node = stack.pop();
             }
         }
     }

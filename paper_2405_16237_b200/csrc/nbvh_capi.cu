@@ -104,12 +104,13 @@ __global__ void k_refresh_fp16(const float* __restrict__ src, __half* __restrict
 
 // fp32 master tables -> fp16 inference table: hashed levels copied, dense levels
 // corner-packed (LevelSm in nbvh_device.cuh).  blockIdx.y = level; one thread per dense
-// cell (gathers its 8 corners, writes one 16*F-byte record) or per hashed entry.
+// cell (gathers its 8 corners, writes one 16*F-byte record) or per 4 hashed entries.
+// F is a template parameter so the record stays in registers (no local memory).
+template <int F>
 __global__ void k_refresh_table(const float* __restrict__ src, __half* __restrict__ dst, GridDev g) {
     __shared__ LevelSm lv[kMaxLevels];
     stage_levels(g, lv, threadIdx.x);
     __syncthreads();
-    const int F = g.F;
     const LevelSm P = lv[blockIdx.y];
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     if (P.nx) {
@@ -120,22 +121,25 @@ __global__ void k_refresh_table(const float* __restrict__ src, __half* __restric
             const uint32_t cz = cell / P.nxy, rem = cell - cz * P.nxy;
             const uint32_t cy = rem / P.nx, cx = rem - cy * P.nx;
             const uint32_t b = cx + cy * P.n1 + cz * P.n1sq;
-            __align__(16) __half2 rec[16];
+            uint32_t rec[4 * F];
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
                 const uint32_t idx = b + (k & 1) + ((k >> 1) & 1) * P.n1 + ((k >> 2) & 1) * P.n1sq;
                 const float* sp = src + ((int64_t)P.coff + idx) * F;
-                if (F == 2) {
-                    rec[k] = __float22half2_rn(__ldg(reinterpret_cast<const float2*>(sp)));
+                if constexpr (F == 2) {
+                    const __half2 h = __float22half2_rn(__ldg(reinterpret_cast<const float2*>(sp)));
+                    rec[k] = *reinterpret_cast<const uint32_t*>(&h);
                 } else {
                     const float4 v = __ldg(reinterpret_cast<const float4*>(sp));
-                    rec[2 * k] = __floats2half2_rn(v.x, v.y);
-                    rec[2 * k + 1] = __floats2half2_rn(v.z, v.w);
+                    const __half2 h0 = __floats2half2_rn(v.x, v.y), h1 = __floats2half2_rn(v.z, v.w);
+                    rec[2 * k] = *reinterpret_cast<const uint32_t*>(&h0);
+                    rec[2 * k + 1] = *reinterpret_cast<const uint32_t*>(&h1);
                 }
             }
             uint4* d = reinterpret_cast<uint4*>(dst + ((int64_t)P.off + 8ll * cell) * F);
-            const uint4* r = reinterpret_cast<const uint4*>(rec);
-            for (int v = 0; v < F; ++v) d[v] = r[v];            // 16*F bytes
+#pragma unroll
+            for (int v = 0; v < F; ++v)                          // 16*F bytes
+                d[v] = make_uint4(rec[4 * v], rec[4 * v + 1], rec[4 * v + 2], rec[4 * v + 3]);
         }
     } else {
         // hashed level: the canonical layout, 4 entries per thread: 8- or 16-byte loads (the
@@ -144,7 +148,7 @@ __global__ void k_refresh_table(const float* __restrict__ src, __half* __restric
         uint4* dp = reinterpret_cast<uint4*>(dst + (int64_t)P.off * F);
         for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n4; e += stride) {
             const float* sp = src + ((int64_t)P.coff + 4 * e) * F;
-            if (F == 2) {
+            if constexpr (F == 2) {
                 const float2 v0 = __ldg(reinterpret_cast<const float2*>(sp)),
                              v1 = __ldg(reinterpret_cast<const float2*>(sp + 2)),
                              v2 = __ldg(reinterpret_cast<const float2*>(sp + 4)),
@@ -166,9 +170,15 @@ __global__ void k_refresh_table(const float* __restrict__ src, __half* __restric
     }
 }
 
+static void launch_refresh_table(nbvh_ctx* c, cudaStream_t s) {
+    const GridDev g = make_grid(c, -1);
+    if (g.F == 2) k_refresh_table<2><<<dim3(148, c->cfg.L), 256, 0, s>>>(c->d_params, c->d_table16, g);
+    else k_refresh_table<4><<<dim3(148, c->cfg.L), 256, 0, s>>>(c->d_params, c->d_table16, g);
+}
+
 nbvh_status refresh_fp16(nbvh_ctx* c, cudaStream_t s) {
     const int64_t nt = c->n_table, nw = c->n_W;
-    k_refresh_table<<<dim3(148, c->cfg.L), 256, 0, s>>>(c->d_params, c->d_table16, make_grid(c, -1));
+    launch_refresh_table(c, s);
     k_refresh_fp16<<<148, 256, 0, s>>>(c->d_params + nt, c->d_W16, nw);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(c, e, "refresh_fp16");
@@ -176,7 +186,7 @@ nbvh_status refresh_fp16(nbvh_ctx* c, cudaStream_t s) {
 }
 
 nbvh_status refresh_table(nbvh_ctx* c, cudaStream_t s) {
-    k_refresh_table<<<dim3(148, c->cfg.L), 256, 0, s>>>(c->d_params, c->d_table16, make_grid(c, -1));
+    launch_refresh_table(c, s);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(c, e, "refresh_table");
     return NBVH_OK;

@@ -691,36 +691,47 @@ __global__ void __launch_bounds__(256, 1) k_train_dw(TrainArgs a, int64_t w_off,
 // fp32 on CUDA cores.  Memory-bound streaming pass over the samples: each thread owns a
 // 16-byte column group (8 deltas of one row) or an (output, 8-input) pair; per-CTA partial
 // sums meet in shared memory and are flushed with one atomic per parameter per CTA.
-__global__ void __launch_bounds__(256) k_train_bias_out(TrainArgs a, int64_t w_out_off, int64_t b_off) {
-    __shared__ float sb[4 * 64 + 8];             // hidden biases (H <= 4) + output biases
-    __shared__ float sw[8 * 64];                 // output-layer weights [o][i]
+constexpr int kBatch = 4;                        // rows in flight per thread (k_train_bias_out)
+__global__ void __launch_bounds__(256, 2) k_train_bias_out(TrainArgs a, int64_t w_out_off, int64_t b_off) {
+    // per-thread / per-warp partial sums, reduced over the row slots after one barrier (no
+    // shared-memory atomics: they are CAS loops on sm_100)
+    __shared__ float p1[256 * 8];                // (1): [slot * groups + g][8]
+    __shared__ float p2[8 * 576];                // (2): [warp][8 x 64 weights, 8 biases, pad]
     const int tid = threadIdx.x;
     const int H = a.m.hidden;
-    for (int i = tid; i < 4 * 64 + 8; i += blockDim.x) sb[i] = 0.f;
-    for (int i = tid; i < 8 * 64; i += blockDim.x) sw[i] = 0.f;
-    __syncthreads();
+    const int groups = H * 8;                    // 8 groups of 8 columns per hidden layer
+    const int rows1 = blockDim.x / groups;
     const int M = *a.n_samples;
     // (1) hidden-layer biases: thread -> (row slot, layer, 8-column group)
     {
-        const int groups = H * 8;                       // 8 groups of 8 columns per layer
-        const int rows_per_pass = blockDim.x / groups;
+        const int rows_per_pass = rows1;
         const int slot = tid / groups, g = tid - slot * groups;
         const int layer = g >> 3, c0 = (g & 7) * 8;
         float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         if (slot < rows_per_pass) {
             const __half* Dk = a.Dl + (int64_t)layer * a.cap * 64 + c0;
-            for (int64_t r = (int64_t)blockIdx.x * rows_per_pass + slot; r < M; r += (int64_t)gridDim.x * rows_per_pass) {
-                const uint4 v = *reinterpret_cast<const uint4*>(Dk + r * 64);
-                const __half2* h = reinterpret_cast<const __half2*>(&v);
+            const int64_t step = (int64_t)gridDim.x * rows_per_pass;
+            // kBatch independent row loads in flight per thread (a streaming pass needs
+            // ~40 KB in flight per SM to cover HBM latency)
+            for (int64_t r = (int64_t)blockIdx.x * rows_per_pass + slot; r < M; r += kBatch * step) {
+                uint4 v[kBatch];
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const float2 f = __half22float2(h[j]);
-                    acc[2 * j] += f.x;
-                    acc[2 * j + 1] += f.y;
+                for (int u = 0; u < kBatch; ++u)
+                    v[u] = r + u * step < M ? __ldcs(reinterpret_cast<const uint4*>(Dk + (r + u * step) * 64))
+                                            : make_uint4(0, 0, 0, 0);
+#pragma unroll
+                for (int u = 0; u < kBatch; ++u) {
+                    const __half2* h = reinterpret_cast<const __half2*>(&v[u]);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const float2 f = __half22float2(h[j]);
+                        acc[2 * j] += f.x;
+                        acc[2 * j + 1] += f.y;
+                    }
                 }
             }
 #pragma unroll
-            for (int j = 0; j < 8; ++j) atomicAdd(sb + layer * 64 + c0 + j, acc[j]);
+            for (int j = 0; j < 8; ++j) p1[tid * 8 + j] = acc[j];
         }
     }
     // (2) output layer: thread -> (row slot, 8-input group); each row's activations (16 B per
@@ -736,37 +747,73 @@ __global__ void __launch_bounds__(256) k_train_bias_out(TrainArgs a, int64_t w_o
             for (int j = 0; j < 8; ++j) accw[o][j] = 0.f;
         }
         const __half* Ah = a.A + (int64_t)(H - 1) * a.cap * 64 + i0;
-        for (int64_t r = (int64_t)blockIdx.x * rows_per_pass + slot; r < M; r += (int64_t)gridDim.x * rows_per_pass) {
-            const float4 d0 = *reinterpret_cast<const float4*>(a.dZ + r * 8),
-                         d1 = *reinterpret_cast<const float4*>(a.dZ + r * 8 + 4);
-            const float dz[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
-            const uint4 v = *reinterpret_cast<const uint4*>(Ah + r * 64);
-            const __half2* hh = reinterpret_cast<const __half2*>(&v);
-            float f[8];
+        const int64_t step = (int64_t)gridDim.x * rows_per_pass;
+        for (int64_t r = (int64_t)blockIdx.x * rows_per_pass + slot; r < M; r += kBatch * step) {
+            float4 d0[kBatch], d1[kBatch];
+            uint4 v[kBatch];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const float2 t = __half22float2(hh[j]);
-                f[2 * j] = t.x;
-                f[2 * j + 1] = t.y;
+            for (int u = 0; u < kBatch; ++u) {
+                const int64_t ru = r + u * step;
+                const bool ok = ru < M;   // rows past M add zeros
+                d0[u] = ok ? *reinterpret_cast<const float4*>(a.dZ + ru * 8) : make_float4(0.f, 0.f, 0.f, 0.f);
+                d1[u] = ok ? *reinterpret_cast<const float4*>(a.dZ + ru * 8 + 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+                v[u] = ok ? __ldcs(reinterpret_cast<const uint4*>(Ah + ru * 64)) : make_uint4(0, 0, 0, 0);
             }
 #pragma unroll
-            for (int o = 0; o < 8; ++o) {
+            for (int u = 0; u < kBatch; ++u) {
+                const float dz[8] = {d0[u].x, d0[u].y, d0[u].z, d0[u].w, d1[u].x, d1[u].y, d1[u].z, d1[u].w};
+                const __half2* hh = reinterpret_cast<const __half2*>(&v[u]);
+                float f[8];
 #pragma unroll
-                for (int j = 0; j < 8; ++j) accw[o][j] = fmaf(dz[o], f[j], accw[o][j]);
-                accb[o] += dz[o];
+                for (int j = 0; j < 4; ++j) {
+                    const float2 t = __half22float2(hh[j]);
+                    f[2 * j] = t.x;
+                    f[2 * j + 1] = t.y;
+                }
+#pragma unroll
+                for (int o = 0; o < 8; ++o) {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) accw[o][j] = fmaf(dz[o], f[j], accw[o][j]);
+                    accb[o] += dz[o];
+                }
             }
         }
+        // the 4 row slots of a warp that share i0 (lane bits 3-4) are summed with shuffles
 #pragma unroll
         for (int o = 0; o < 8; ++o) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j) atomicAdd(sw + o * 64 + i0 + j, accw[o][j]);
-            if (i0 == 0) atomicAdd(sb + 4 * 64 + o, accb[o]);
+            for (int j = 0; j < 8; ++j) {
+                accw[o][j] += __shfl_xor_sync(0xffffffffu, accw[o][j], 8);
+                accw[o][j] += __shfl_xor_sync(0xffffffffu, accw[o][j], 16);
+            }
+            accb[o] += __shfl_xor_sync(0xffffffffu, accb[o], 8);
+            accb[o] += __shfl_xor_sync(0xffffffffu, accb[o], 16);
+        }
+        if ((tid & 31) < 8) {
+            float* pw = p2 + (tid >> 5) * 576;
+#pragma unroll
+            for (int o = 0; o < 8; ++o) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) pw[o * 64 + i0 + j] = accw[o][j];
+                if (i0 == 0) pw[512 + o] = accb[o];
+            }
         }
     }
     __syncthreads();
-    for (int i = tid; i < H * 64; i += blockDim.x) atomicAdd(a.grad + b_off + i, sb[i]);
-    for (int i = tid; i < 8; i += blockDim.x) atomicAdd(a.grad + b_off + H * 64 + i, sb[4 * 64 + i]);
-    for (int i = tid; i < 8 * 64; i += blockDim.x) atomicAdd(a.grad + w_out_off + i, sw[i]);
+    // one global atomic per parameter per CTA
+    for (int i = tid; i < H * 64; i += blockDim.x) {
+        const int g = (i >> 6) * 8 + ((i & 63) >> 3), j = i & 7;
+        float v = 0.f;
+        for (int sl = 0; sl < rows1; ++sl) v += p1[(sl * groups + g) * 8 + j];
+        atomicAdd(a.grad + b_off + i, v);
+    }
+    const int nw = blockDim.x >> 5;
+    for (int i = tid; i < 520; i += blockDim.x) {             // 512 weights + 8 biases
+        float v = 0.f;
+        for (int w = 0; w < nw; ++w) v += p2[w * 576 + i];
+        if (i < 512) atomicAdd(a.grad + w_out_off + i, v);
+        else atomicAdd(a.grad + b_off + H * 64 + (i - 512), v);
+    }
 }
 
 // ------------------------------------------------------------------ T6 weight gradients on tcgen05

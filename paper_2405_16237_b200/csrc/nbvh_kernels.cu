@@ -36,10 +36,12 @@ __device__ __forceinline__ int traverse_smem_list(const CutDev& cut, const RayDe
                                                   int* lid, int S, SmemStack& stack, bool& more, int* err) {
     int n = 0;
     bool dropped = false;
+    float last_te = 0.f;                         // key of entry cap-1 once the list is full
+    int last_id = 0;
     auto consider = [&](int leaf, float te, float tx) {
         int pos;
         if (n == cap) {
-            if (!key_less(te, leaf, lte[(cap - 1) * S], lid[(cap - 1) * S])) {
+            if (!key_less(te, leaf, last_te, last_id)) {
                 dropped = true;
                 return;
             }
@@ -60,6 +62,10 @@ __device__ __forceinline__ int traverse_smem_list(const CutDev& cut, const RayDe
         lte[pos * S] = te;
         ltx[pos * S] = tx;
         lid[pos * S] = leaf;
+        if (n == cap) {
+            last_te = lte[(cap - 1) * S];
+            last_id = lid[(cap - 1) * S];
+        }
     };
     if (cut.n_leaves == 1) {
         float4 a = __ldg(cut.leaf_box), b = __ldg(cut.leaf_box + 1);
@@ -83,9 +89,8 @@ __device__ __forceinline__ int traverse_smem_list(const CutDev& cut, const RayDe
             if (hr && cr < 0) consider(-1 - cr, rte_, rtx_);
             bool pl = hl && cl >= 0, pr = hr && cr >= 0;
             if (n == cap) {                       // subtrees entering after the cap-th key
-                const float last = lte[(cap - 1) * S];
-                if (pl && lte_ > last) { pl = false; dropped = true; }
-                if (pr && rte_ > last) { pr = false; dropped = true; }
+                if (pl && lte_ > last_te) { pl = false; dropped = true; }
+                if (pr && rte_ > last_te) { pr = false; dropped = true; }
             }
             if (pl && pr) {
                 if (stack.sp + 1 > stack.cap) { atomicOr(err, 1); break; }

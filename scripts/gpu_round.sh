@@ -25,7 +25,7 @@ if [ "${SKIP_NCU:-0}" != "1" ]; then
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_query|k_traverse" -s 0 -c 2 \
       -o $OUT/prof_query_$TAG -f $CMD > $OUT/ncu_full.log 2>&1
   echo "ncu full exit $?" >> $OUT/ncu_full.log
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_train_(fwd|bwd|label|dw)" -s 0 -c 4 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_train_(select|fwd|bwd|label|dw|bias)" -s 0 -c 6 \
       -o $OUT/prof_train_$TAG -f $CMD > $OUT/ncu_full_train.log 2>&1
   echo "ncu full train exit $?" >> $OUT/ncu_full_train.log
 fi

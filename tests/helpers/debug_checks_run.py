@@ -29,8 +29,11 @@ ctx.set_leaf_rank(np.zeros(ctx.cut(0)["n_leaves"], np.float32))
 for step in range(3):
     r, u, xi = ctx.gen_train_rays(seed=5, step=step, n=8192, box=(-1.5, -1.5, -1.5, 1.5, 1.5, 1.5))
     ctx.train_step(r, u, xi)
+# classical closest-hit traversal (bvh_closest: farther-child stack sized by the BVH depth)
+mh = ctx.intersect_mesh(torch.from_numpy(rays).cuda())
 x = (torch.rand(1000, ctx.d_in, device="cuda") - 0.5).half()
 ctx.mlp_forward(x)
 torch.cuda.synchronize()
 st = ctx.query_stats()
-print("debug checks ok", int(d["hit"].sum().item()), st["n_refills"], ctx.train_stats()["n_accepted"])
+print("debug checks ok", int(d["hit"].sum().item()), st["n_refills"], ctx.train_stats()["n_accepted"],
+      int(mh["hit"].sum().item()))

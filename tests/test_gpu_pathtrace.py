@@ -130,3 +130,41 @@ def test_hybrid_render_bounded(orc):
     assert np.all(np.isfinite(rad)) and rad.min() >= 0 and rad.max() <= SKY.max() + 1e-6
     assert alive[0] > 0 and np.all(np.diff(alive) <= 0)
     assert (rad.sum(1) > 0).mean() > 0.5
+
+
+def test_intersect_mesh_deep_bvh_vs_oracle(orc):
+    """A chain-shaped base BVH (plates at exponentially growing spacing, so SAH peels one
+    off per level): the closest-hit stack is sized by the measured depth, not a fixed 64."""
+    from paper_2405_16237_b200 import Context
+    from synth.scenes import Scene
+    n_plates = 40
+    xs = np.cumsum(1.25 ** np.arange(n_plates)).astype(np.float32)
+    V, T = [], []
+    for i, x in enumerate(xs):
+        V += [(x, -1.0, -1.0), (x, 1.0, -1.0), (x, 0.0, 1.5)]
+        T.append((3 * i, 3 * i + 1, 3 * i + 2))
+    V = np.array(V, np.float32)
+    nrm = np.tile(np.array([[-1.0, 0.0, 0.0]], np.float32), (V.shape[0], 1))
+    sc = Scene(verts=V, tris=np.array(T, np.uint32), vnormals=nrm,
+               albedo=np.full((n_plates, 3), 0.5, np.float32))
+    ctx = Context(device=0, L=8, F=2, log2_T=14, n_points=4, hidden_layers=2)
+    ctx.set_mesh(sc)
+    rng = np.random.default_rng(5)
+    n = 4000
+    rays = np.zeros((n, 8), np.float32)
+    start = rng.integers(0, n_plates, n)
+    rays[:, 0] = xs[start] - rng.uniform(0.01, 0.5, n).astype(np.float32)
+    rays[:, 1:3] = rng.uniform(-0.6, 0.6, (n, 2))
+    d = np.stack([np.ones(n), rng.uniform(-0.02, 0.02, n), rng.uniform(-0.02, 0.02, n)], 1)
+    rays[:, 4:7] = d / np.linalg.norm(d, axis=1, keepdims=True)
+    rays[:, 3] = 0.0
+    rays[:, 7] = 1e30
+    out = ctx.intersect_mesh(torch.from_numpy(rays).cuda())
+    torch.cuda.synchronize()
+    g = {k: v.cpu().numpy() for k, v in out.items()}
+    gt = orc.label(sc, np.array([0, n_plates], np.int64), np.arange(n_plates, dtype=np.int32), rays,
+                   np.zeros(n, np.int32), rays[:, 3].copy(), rays[:, 7].copy())
+    hit = (gt[:, 0] == 0).astype(np.uint8)
+    assert np.array_equal(g["hit"], hit) and hit.sum() > n // 2
+    h = hit == 1
+    assert np.array_equal(g["t"][h], gt[h, 8].astype(np.float32))

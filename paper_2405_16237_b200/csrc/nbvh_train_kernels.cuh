@@ -248,8 +248,10 @@ __global__ void __launch_bounds__(256, 2) k_train_fwd(TrainArgs a) {
             load_sample_desc(a, tile * kTileQ + tid, M, q);
             qd[tid] = q;
             if (q.valid)
-                for (int p = 0; p < n_pts; ++p) {   // jittered stratified points (C8)
-                    float x[3];
+#pragma unroll
+                for (int p = 0; p < 4; ++p) {       // jittered stratified points (C8)
+                    if (p >= n_pts) break;          // n_points <= 4 (checked by the host); static
+                    float x[3];                     // indices keep the descriptor in registers
                     segment_point(a.g, q.o, q.d, q.t0, q.t1, p, n_pts, q.xi, x);
                     xs[(p * 3 + 0) * kTileQ + tid] = x[0];
                     xs[(p * 3 + 1) * kTileQ + tid] = x[1];
@@ -442,7 +444,9 @@ __global__ void __launch_bounds__(256, 1) k_train_bwd(TrainArgs a) {
             load_sample_desc(a, tile * kTileQ + tid, M, q);
             qd[tid] = q;
             if (q.valid)
-                for (int p = 0; p < a.g.n_points; ++p) {
+#pragma unroll
+                for (int p = 0; p < 4; ++p) {
+                    if (p >= a.g.n_points) break;
                     float x[3];
                     segment_point(a.g, q.o, q.d, q.t0, q.t1, p, a.g.n_points, q.xi, x);
                     xs[(p * 3 + 0) * kTileQ + tid] = x[0];

@@ -568,13 +568,21 @@ __global__ void __launch_bounds__(kQueryWarps * 32, 1) k_query(QueryArgs a) {
     if constexpr (kTc) tc::fence_after();
     const uint32_t tmem_acc = kTc ? *tmem_slot + (uint32_t)(grp * 64) : 0u;
 
-    const int n_long = *a.cnt_long;           // long rays first (k_traverse), then the rest
-    const int total = n_long + *a.cnt;        // rays with >= 1 intersected leaf
+    // work-list sizes and per-warp statistics live in shared memory (read on refills / written
+    // by one lane): kept out of the loop's 128 registers, which had spilled them to local memory
+    __shared__ int s_work[2];                 // n_long, total
+    __shared__ int s_stat[2 * 32];            // per warp: queries evaluated, loop iterations
+    if (lane == 0) {
+        s_work[0] = *a.cnt_long;              // long rays first (k_traverse), then the rest
+        s_work[1] = s_work[0] + *a.cnt;       // rays with >= 1 intersected leaf (same values in every warp)
+        s_stat[2 * warp] = 0;
+        s_stat[2 * warp + 1] = 0;
+    }
+    __syncwarp();
     const uint32_t hmask = (1u << a.g.log2_T) - 1u;
     const void* tab = a.g.table;
     const int cpp = (a.g.L * F) / 8;          // 16-byte chunks per sample point
-    int my_queries = 0;                       // queries this warp evaluated (< 2^31)
-    int iters = 0;
+    int iters = 0;                            // kTc: group vote parity
     bool exhausted = false;
 
     while (true) {
@@ -586,6 +594,7 @@ __global__ void __launch_bounds__(kQueryWarps * 32, 1) k_query(QueryArgs a) {
             int base = 0;
             if (lane == 0) base = atomicAdd(a.next, ne);
             base = __shfl_sync(0xffffffffu, base, 0);
+            const int total = s_work[1], n_long = s_work[0];
             exhausted = base + ne >= total;
             const int i = base + __popc(em & lanemask_lt());
             if (empty && i < total) {
@@ -630,8 +639,11 @@ __global__ void __launch_bounds__(kQueryWarps * 32, 1) k_query(QueryArgs a) {
         } else {
             if (nv == 0) break;               // work list drained and every slot finished
         }
-        ++iters;
-        my_queries += nv;
+        if constexpr (kTc) ++iters;
+        if (lane == 0) {
+            s_stat[2 * warp] += nv;
+            s_stat[2 * warp + 1] += 1;
+        }
         if (occ) {
             const int row = __popc(om & lanemask_lt());
             S.act[row] = lane;
@@ -781,8 +793,8 @@ __global__ void __launch_bounds__(kQueryWarps * 32, 1) k_query(QueryArgs a) {
         __syncwarp();
     }
     if (lane == 0) {
-        atomicAdd(&a.ctr->n_queries, (unsigned long long)my_queries);
-        atomicMax(&a.ctr->max_iter, iters);
+        atomicAdd(&a.ctr->n_queries, (unsigned long long)s_stat[2 * warp]);
+        atomicMax(&a.ctr->max_iter, s_stat[2 * warp + 1]);
     }
     if constexpr (kTc) {
         tc::fence_before();

@@ -571,31 +571,31 @@ __global__ void __launch_bounds__(kQueryWarps * 32, 1) k_query(QueryArgs a) {
     // work-list sizes and per-warp statistics live in shared memory (read on refills / written
     // by one lane): kept out of the loop's 128 registers, which had spilled them to local memory
     __shared__ int s_work[2];                 // n_long, total
-    __shared__ int s_stat[2 * 32];            // per warp: queries evaluated, loop iterations
+    // per warp: [0] queries evaluated, [1] loop iterations, [2] live rows this iteration,
+    // [3] work list exhausted (lane 0 writes; read back after the next __syncwarp)
+    __shared__ int s_stat[4 * 32];
+    int* ws = s_stat + 4 * warp;
     if (lane == 0) {
         s_work[0] = *a.cnt_long;              // long rays first (k_traverse), then the rest
         s_work[1] = s_work[0] + *a.cnt;       // rays with >= 1 intersected leaf (same values in every warp)
-        s_stat[2 * warp] = 0;
-        s_stat[2 * warp + 1] = 0;
+        ws[0] = ws[1] = ws[2] = ws[3] = 0;
     }
     __syncwarp();
     const uint32_t hmask = (1u << a.g.log2_T) - 1u;
     const void* tab = a.g.table;
-    const int cpp = (a.g.L * F) / 8;          // 16-byte chunks per sample point
     int iters = 0;                            // kTc: group vote parity
-    bool exhausted = false;
 
     while (true) {
         // (A) refill empty slots from the global work list (consecutive rays per warp)
         const bool empty = lane < kWarpQ && S.ray[lane] < 0;
         const unsigned em = __ballot_sync(0xffffffffu, empty);
-        if (em && !exhausted) {
+        if (em && !ws[3]) {
             const int ne = __popc(em);
             int base = 0;
             if (lane == 0) base = atomicAdd(a.next, ne);
             base = __shfl_sync(0xffffffffu, base, 0);
             const int total = s_work[1], n_long = s_work[0];
-            exhausted = base + ne >= total;
+            if (lane == 0) ws[3] = base + ne >= total;
             const int i = base + __popc(em & lanemask_lt());
             if (empty && i < total) {
                 const WorkRec* wr = i < n_long ? a.act_long + i : a.act + (i - n_long);
@@ -641,8 +641,9 @@ __global__ void __launch_bounds__(kQueryWarps * 32, 1) k_query(QueryArgs a) {
         }
         if constexpr (kTc) ++iters;
         if (lane == 0) {
-            s_stat[2 * warp] += nv;
-            s_stat[2 * warp + 1] += 1;
+            ws[0] += nv;
+            ws[1] += 1;
+            ws[2] = nv;
         }
         if (occ) {
             const int row = __popc(om & lanemask_lt());
@@ -681,7 +682,8 @@ __global__ void __launch_bounds__(kQueryWarps * 32, 1) k_query(QueryArgs a) {
         {
             constexpr int kHalves = 32 / kWarpQ;
             const int q = lane & (kWarpQ - 1), h = lane / kWarpQ;
-            if (q < nv) {
+            const int cpp = (a.g.L * F) / 8;  // 16-byte chunks per sample point
+            if (q < ws[2]) {
                 for (int p = h; p < NP; p += kHalves) {
                     const float* xp = xs + p * 3 * kWarpQ;
                     const float x0 = xp[q], x1 = xp[kWarpQ + q], x2 = xp[2 * kWarpQ + q];
@@ -707,11 +709,11 @@ __global__ void __launch_bounds__(kQueryWarps * 32, 1) k_query(QueryArgs a) {
                             plan.z);
         } else {
             mlp_rows16h<D>(ms, a.m.hidden, feat, 0, zt, lane);
-            if (kWarpQ > 16 && nv > 16) mlp_rows16h<D>(ms, a.m.hidden, feat, 16, zt, lane);
+            if (kWarpQ > 16 && ws[2] > 16) mlp_rows16h<D>(ms, a.m.hidden, feat, 16, zt, lane);
         }
         __syncwarp();
         // (F) decode, best hit, front-to-back termination
-        if (lane < nv) {
+        if (lane < ws[2]) {
             const int s = S.act[lane];
             const int r = S.ray[s];
             const float* z = zt + lane * 8;
@@ -793,8 +795,8 @@ __global__ void __launch_bounds__(kQueryWarps * 32, 1) k_query(QueryArgs a) {
         __syncwarp();
     }
     if (lane == 0) {
-        atomicAdd(&a.ctr->n_queries, (unsigned long long)s_stat[2 * warp]);
-        atomicMax(&a.ctr->max_iter, s_stat[2 * warp + 1]);
+        atomicAdd(&a.ctr->n_queries, (unsigned long long)ws[0]);
+        atomicMax(&a.ctr->max_iter, ws[1]);
     }
     if constexpr (kTc) {
         tc::fence_before();

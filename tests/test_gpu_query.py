@@ -6,7 +6,8 @@ plain CPU implementation in oracle/.  Tolerances:
   * encode features (fp16 out, U[-1,1] tables): 2e-3 absolute
   * MLP: decoded outputs (sigmoid channels, unit normal) 1e-2 absolute; raw z 2e-2*(1+|z|)
   * end-to-end hit mask vs the double oracle: identical on rays whose decisive
-    visibilities satisfy |sigmoid(z_vis)-0.5| >= 1e-2; band rays counted (< 1%)
+    visibilities satisfy |sigmoid(z_vis)-0.5| >= 1e-2 and whose t comparisons are >= 5e-3
+    apart (C30); band rays counted (< 1%; 2.5% for the paper-default variant, C35)
 """
 import math
 
@@ -137,7 +138,8 @@ def test_traversal_lists_bit_exact(orc, tiny, cap):
     assert np.array_equal(leaf.cpu().numpy(), wl)
     m = wl >= 0
     assert np.array_equal(te.cpu().numpy()[m], wte[m]) and np.array_equal(tx.cpu().numpy()[m], wtx[m])
-    assert wcnt.max() > 4
+    assert wcnt.max() >= 8                # depth of the tiny 64-leaf cut on these rays (oracle: 8);
+                                          # resumption past K: test_traversal_small_capacity
 
 
 def test_traversal_small_capacity(orc):
@@ -153,7 +155,7 @@ def test_traversal_small_capacity(orc):
 
 
 # ------------------------------------------------------------------ end-to-end query
-def _check_query(orc, ctx, tab, layers, rays, mode=0, cap=64, lod=0):
+def _check_query(orc, ctx, tab, layers, rays, mode=0, cap=64, lod=0, band_max=0.01):
     cut = ctx.cut(lod)
     out, zt = ctx.debug_query_trace(torch.from_numpy(rays).cuda(), cap, lod=lod)
     torch.cuda.synchronize()
@@ -175,7 +177,7 @@ def _check_query(orc, ctx, tab, layers, rays, mode=0, cap=64, lod=0):
     assert np.array_equal(g["hit"][clear], o["hit"][clear])
     assert np.array_equal(g["leaf"][clear], o["leaf"][clear])
     assert np.array_equal(g["n_queries"][clear], o["nq"][clear])
-    assert (~clear).mean() < 0.02, (~clear).mean()
+    assert (~clear).mean() < band_max, (~clear).mean()             # C30 band (< 1%)
     h = clear & (o["hit"] == 1)
     assert np.abs(g["t"][h] - o["t"][h]).max() <= 2e-3 * 3.5     # C23: t / scene diagonal
     assert np.abs(g["albedo"][h] - o["albedo"][h]).max() <= 1e-2
@@ -230,7 +232,9 @@ def test_query_paper_default_variant(orc):
     """NEXT-4: the paper's own model shape (L=8, F=4, T=2^18, n=3, 4x64 MLP; D_in = 96)."""
     ctx, sc, tab, layers = _mk_ctx("paper")
     assert ctx.d_in == 96
-    g, o = _check_query(orc, ctx, tab, layers, _rays_tiny(1500))
+    # C35: this 4-hidden-layer model's logits spread less under the same He x10 recipe
+    # (std 2.7 vs 3.8): 2.2% of its rays are in the band, computed by the oracle alone.
+    g, o = _check_query(orc, ctx, tab, layers, _rays_tiny(1500), band_max=0.025)
     assert g["hit"].sum() > 200
 
 

@@ -289,19 +289,27 @@ def test_p8_order_independence_R2_vs_R1(orc):
     r1 = orc.query(g, 3, tab, layers, lo, hi, rays, mode=1)
     # Brute force: evaluate EVERY intersected leaf from the primitives (sample, encode,
     # MLP) and take argmin (t, t_enter, id); R2 must return it although it skips leaves.
-    leaf, te, tx, cnt = orc.leaf_lists(rays, lo, hi, 12)
+    # The walk order for R1 comes from brute-force slabs + numpy's lexsort on (t_enter, id),
+    # not from the oracle's own leaf_list.
     dmin, dinv = orc.domain(lo, hi)
     n_first_hit_differs = 0
+    cnt = np.zeros(len(rays), np.int32)
     for r in range(len(rays)):
+        slabs = [orc.slab(rays[r], lo[i], hi[i]) for i in range(lo.shape[0])]
+        ids = [i for i in range(lo.shape[0]) if slabs[i][0]]
+        te = np.asarray([slabs[i][3] for i in ids], np.float32)
+        tx = np.asarray([slabs[i][4] for i in ids], np.float32)
+        order = np.lexsort((np.asarray(ids), te)) if ids else []
+        cnt[r] = len(ids)
         cands = []
         first = None
-        for k in range(cnt[r]):
-            pts = orc.segment_points(rays[r], te[r, k], tx[r, k], 3, dmin, dinv)
+        for k in order:
+            pts = orc.segment_points(rays[r], te[k], tx[k], 3, dmin, dinv)
             feat, _ = orc.encode_points(g, tab, pts)
             z = orc.mlp_forward(layers, feat.reshape(1, -1))[0]
             if z[0] < 0:
-                t = float(te[r, k]) + 1 / (1 + math.exp(-z[1])) * (float(tx[r, k]) - float(te[r, k]))
-                cands.append((t, float(te[r, k]), int(leaf[r, k])))
+                t = float(te[k]) + 1 / (1 + math.exp(-z[1])) * (float(tx[k]) - float(te[k]))
+                cands.append((t, float(te[k]), int(ids[k])))
                 if first is None:
                     first = cands[-1]
         if cands:

@@ -7,9 +7,10 @@ Default workload = BASELINE configs[1] ("1080p"): 988,928-triangle procedural sc
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1080p|tiny] [--impl ours|reference]
 
-Multi-GPU (torchrun): every rank renders its own 1080p frame (camera jittered by rank)
-with a replicated model; no collective on the data path; value = all ranks' rays / max
-rank time ("scaling": "weak").  `--impl reference` times the CPU oracle (oracle/) on a
+Multi-GPU (torchrun): the model is built on rank 0 and broadcast at init; every step's ONE
+1080p frame is split over the ranks by interleaved 16x16 pixel tiles; no collective on the
+data path; value = the frame's rays / max rank time ("scaling": "strong").  A weak-scaling
+line (every rank queries the whole frame) is reported beside it for N > 1.  `--impl reference` times the CPU oracle (oracle/) on a
 bounded sample of the same workload (there is no reference implementation to install:
 the paper ships no code).  Prints ONE JSON line on rank 0.
 """
@@ -132,11 +133,20 @@ def _profiled_traffic(kernel: str = "k_query"):
     return tot, os.path.basename(files[-1])
 
 
-def cpu_oracle_rate(ctx, c, rays, target_s: float = 12.0, max_rays: int | None = None):
-    """Time the oracle (as it stands) on a deterministic strided sample of the frame."""
-    import oracle
+def _cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.lower().startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def _oracle_model(ctx, c):
+    """The context's model as the oracle takes it (fp16 tables, (W, b) layers)."""
     h = c["hash"]
-    g = oracle.Grid(h.L, h.log2_T, h.F)
     from paper_2405_16237_b200 import PARAM_TABLES, PARAM_WEIGHTS, PARAM_BIASES
     tab = ctx.get_params(PARAM_TABLES).astype(np.float16).reshape(-1, h.F)
     W = ctx.get_params(PARAM_WEIGHTS)
@@ -148,45 +158,105 @@ def cpu_oracle_rate(ctx, c, rays, target_s: float = 12.0, max_rays: int | None =
                        b[bo:bo + dims[k + 1]]))
         wo += dims[k] * dims[k + 1]
         bo += dims[k + 1]
+    return tab, layers
+
+
+def cpu_oracle_rate(ctx, c, rays, target_s: float = 12.0, one_thread_s: float = 4.0):
+    """Time the oracle (as it stands) on an evenly spaced sample of the frame's rays
+    (np.linspace over the whole frame, so sky and geometry are represented in proportion),
+    on all host cores and on one thread."""
+    import oracle
+    h = c["hash"]
+    g = oracle.Grid(h.L, h.log2_T, h.F)
+    tab, layers = _oracle_model(ctx, c)
     cut = ctx.cut(0)
-    # calibrate on a small sample, then size the timed sample to ~target_s
-    probe = rays[:: max(1, rays.shape[0] // 512)]
-    t0 = time.perf_counter()
     box = oracle.scene_box(ctx.scene)
-    oracle.query(g, h.n_points, tab, layers, cut["leaf_lo"], cut["leaf_hi"], probe, dom_box=box)
-    per_ray = (time.perf_counter() - t0) / probe.shape[0]
-    n = int(min(rays.shape[0], max(256, target_s / max(per_ray, 1e-9))))
-    if max_rays:
-        n = min(n, max_rays)
-    for _ in range(2):                                # a second, larger sample if the first was short
-        stride = max(1, rays.shape[0] // n)
-        sample = rays[::stride][:n]
+    N = rays.shape[0]
+
+    def timed(n):
+        idx = np.unique(np.linspace(0, N - 1, max(1, min(n, N))).astype(np.int64))
         t0 = time.perf_counter()
-        oracle.query(g, h.n_points, tab, layers, cut["leaf_lo"], cut["leaf_hi"], sample, dom_box=box)
-        dt = time.perf_counter() - t0
-        grow = int(n * target_s / max(dt, 1e-9))
-        if dt >= target_s / 3 or n >= rays.shape[0] or (max_rays and n >= max_rays):
-            break
-        n = min(rays.shape[0], grow, max_rays or grow)
-    return {"value": sample.shape[0] / dt / 1e6, "unit": "Mrays/s", "cores": oracle.num_threads(), "kind": "oracle",
-            "sample": f"every {stride}th primary ray of the frame ({sample.shape[0]} rays), C++ double oracle, "
-                      f"brute-force leaf scan, OpenMP", "seconds": dt}
+        oracle.query(g, h.n_points, tab, layers, cut["leaf_lo"], cut["leaf_hi"], rays[idx], dom_box=box)
+        return idx.size, time.perf_counter() - t0
+
+    def rate(budget):
+        n, dt = timed(512)                                 # calibrate, then size the sample to the budget
+        for _ in range(3):
+            if dt >= budget / 3 or n >= N:
+                break
+            n, dt = timed(int(n * budget / max(dt, 1e-9)))
+        return n, dt
+
+    cores = oracle.num_threads()
+    n, dt = rate(target_s)
+    oracle.set_num_threads(1)
+    try:
+        n1, dt1 = rate(one_thread_s)
+    finally:
+        oracle.set_num_threads(cores)
+    return {"value": n / dt / 1e6, "unit": "Mrays/s", "cores": cores, "kind": "oracle",
+            "sample": f"{n} rays evenly spaced over the {N}-ray frame (np.linspace), C++ double oracle, "
+                      f"brute-force leaf scan, OpenMP on {cores} threads", "seconds": dt,
+            "one_thread": {"value": n1 / dt1 / 1e6, "unit": "Mrays/s", "rays": n1, "seconds": dt1},
+            "cpu_model": _cpu_model(), "host_cpus": os.cpu_count()}
+
+
+def _workload(cfg: str) -> str:
+    return f"{cfg}: " + ("988,928-tri procedural terrain+spheres, 2048-leaf cut, L=16 T=2^19 F=2 n=4, MLP 3x64, "
+                         "1920x1080 primary rays" if cfg == "1080p" else
+                         "9,680-tri displaced icosphere, 64-leaf cut, L=8 T=2^14 F=2 n=4, MLP 2x64, 64x64 primary rays")
+
+
+def _time_frames(ctx, rays, out, steps, flush, stream):
+    """CUDA-event time (ms) of each of `steps` nbvh_query calls; L2 flushed between calls
+    (outside the events)."""
+    import torch
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    for i in range(steps):
+        flush.fill_(float(i))                                  # evict L2 between timed steps
+        starts[i].record(stream)
+        ctx.query(rays, out=out)                               # async: counter reset + 2 kernels
+        ends[i].record(stream)
+    torch.cuda.synchronize()
+    return [s.elapsed_time(e) for s, e in zip(starts, ends)]
+
+
+def _max_over_ranks(x: float, world: int) -> float:
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
 
 
 def run_ours(args):
     import torch
     import torch.distributed as dist
+    from paper_2405_16237_b200 import dp
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
-    ctx, sc, rays_np, c = build_model(args.config, local, rank, args.list_cap)
+    ctx, sc, frame_np, c = build_model(args.config, local, 0, args.list_cap)
+    # the model is built on rank 0 and replicated by one broadcast at init (SURVEY §8(e))
+    t0 = time.perf_counter()
+    dp.broadcast_model(ctx, src=0, device="cuda")
+    bcast_s = time.perf_counter() - t0
+    identical = dp.params_identical_across_ranks(ctx)
+    assert identical, "model broadcast left ranks with different parameters"
+    # strong scaling: ONE 1080p frame per step, its 16x16 tiles dealt round-robin to the ranks
+    idx = dp.tile_partition(*c["res"], rank, world) if args.order == "tiles" else \
+        np.arange(frame_np.shape[0])[dp.shard(frame_np.shape[0], rank, world)]
+    rays_np = np.ascontiguousarray(frame_np[idx])
     n = rays_np.shape[0]
-    ctx.reserve(n)
+    n_frame = frame_np.shape[0]
+    ctx.reserve(max(n, n_frame))
     rays = torch.from_numpy(rays_np).cuda()
-    out = ctx.alloc_hits(n)
+    out = ctx.alloc_hits(max(n, n_frame))
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")   # > 126 MB L2
 
@@ -195,20 +265,13 @@ def run_ours(args):
         ctx.query(rays, out=out)
     torch.cuda.synchronize()
 
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     clocks = ClockSampler(local)
     clocks.start()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     wall0 = time.perf_counter()
-    for i in range(args.steps):
-        flush.fill_(float(i))                                  # evict L2 between timed steps
-        starts[i].record(stream)
-        ctx.query(rays, out=out)                               # async: counter reset + 2 kernels
-        ends[i].record(stream)
-    torch.cuda.synchronize()
+    step_ms = _time_frames(ctx, rays, out, args.steps, flush, stream)
     wall = time.perf_counter() - wall0
     if world > 1:
         dist.barrier()
@@ -222,43 +285,51 @@ def run_ours(args):
     torch.cuda.synchronize()
     st = ctx.query_stats()                                     # counters of the last step
     launches = st["n_launches"] * args.steps
-    queries = st["n_queries"] * args.steps
     iters = st["n_iters"]
-    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    t_ms = sum(step_ms)
-    tmax = torch.tensor([t_ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-    t_ms = float(tmax.item())
-    total_rays = n * args.steps * world
+    t_ms = _max_over_ranks(sum(step_ms), world)
+    total_rays = n_frame * args.steps                          # every rank's tiles of the frame
     value = total_rays / (t_ms / 1e3) / 1e6
+    q_all = torch.tensor([st["n_queries"]], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(q_all)
+    queries_per_ray = float(q_all.item()) / n_frame
+
+    # weak-scaling line (N > 1 only): every rank queries the whole frame
+    weak = None
+    if world > 1:
+        full = torch.from_numpy(frame_np).cuda()
+        for _ in range(args.warmup):
+            ctx.query(full, out=out)
+        dist.barrier()
+        torch.cuda.synchronize()
+        wms = _max_over_ranks(sum(_time_frames(ctx, full, out, args.steps, flush, stream)), world)
+        dist.barrier()
+        weak = {"scaling": "weak", "value": n_frame * args.steps * world / (wms / 1e3) / 1e6, "unit": "Mrays/s",
+                "ms_per_step": wms / args.steps, "rays_per_step_per_gpu": n_frame}
+        del full
 
     # live per-kernel timing of the dominant kernel (persistent fused query), one profiled
-    # pass per timed step (separate from the timed region; events on the launching stream)
+    # pass per step (separate from the timed region; events on the launching stream)
     ctx.set_profiling(True)
     wave_ms, trav_ms, prof_q = [], [], []
     for i in range(max(3, args.steps)):
         flush.fill_(float(i))
         ctx.query(rays, out=out)
-        st = ctx.query_stats()
-        wave_ms.append(st["ms_query"])
-        trav_ms.append(st["ms_traverse"])
-        prof_q.append(st["n_queries"])
+        st2 = ctx.query_stats()
+        wave_ms.append(st2["ms_query"])
+        trav_ms.append(st2["ms_traverse"])
+        prof_q.append(st2["n_queries"])
     ctx.set_profiling(False)
     h = c["hash"]
-    useful_gather = h.n_points * h.L * 8 * h.F * 2                # fp16 corner bytes per query
-    per_query_io = 32 + 12 + 8 + 37                                 # ray, list entry, list bookkeeping, hit record
-    bytes_per_query = useful_gather + per_query_io
+    useful_gather = h.n_points * h.L * 8 * h.F * 2                # fp16 corner bytes per query (§8(d))
     mean_q = statistics.mean(prof_q)
     wave_s = statistics.mean(wave_ms) / 1e3
-    achieved = mean_q * bytes_per_query / wave_s / 1e9
+    achieved = mean_q * useful_gather / wave_s / 1e9
     hbm, tflops, peak_src = _peaks()
     traffic, traffic_src = _profiled_traffic("k_query")
     mlp_flops = 2 * (ctx.d_in * 64 + (h.hidden_layers - 1) * 64 * 64 + 64 * 8)
 
     # end-to-end through the public host API: pinned host rays in, host results out
-    e2e = None
-    # every rank measures its own e2e (the max over ranks is reported)
     pin = torch.from_numpy(rays_np).pin_memory()
     hb = {"hit": torch.empty(n, dtype=torch.uint8).pin_memory(), "t": torch.empty(n).pin_memory(),
           "normal": torch.empty(n, 3).pin_memory(), "albedo": torch.empty(n, 3).pin_memory()}
@@ -267,58 +338,72 @@ def run_ours(args):
     ctx.query_host(pin_np, out=hbn)
     torch.cuda.synchronize()
     e2e_s = []
+    if world > 1:
+        dist.barrier()
     for i in range(args.steps):
         flush.fill_(float(i))
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         ctx.query_host(pin_np, out=hbn)                       # synchronous: H2D + query + D2H
         e2e_s.append(time.perf_counter() - t0)
-    e2e_t = torch.tensor([sum(e2e_s)], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_t = _max_over_ranks(sum(e2e_s), world)
     d2h = n * (1 + 4 + 12 + 12)                                   # hit, t, normal, albedo
-    e2e = {"value": n * args.steps * world / float(e2e_t.item()) / 1e6, "unit": "Mrays/s",
-           "h2d_bytes_per_step": n * 32, "d2h_bytes_per_step": d2h}
+    e2e = {"value": n_frame * args.steps / e2e_t / 1e6, "unit": "Mrays/s",
+           "h2d_bytes_per_step": n * 32, "d2h_bytes_per_step": d2h,
+           "note": "per rank; value = the frame's rays / max-over-ranks time"}
 
-    mlp = bench_mlp(ctx, args)
     gather = bench_gather(args)
+    l2_peak = gather.get("l2_random_4B_GBps")
+    mlp = bench_mlp(ctx, args)
     train = bench_train(ctx, args, world, rank) if args.train else None
     if train and train.get("bwd_scatter_Gred_v2_per_s") and gather.get("l2_red_v2_f32_Gops"):
         train["bwd_scatter_frac_of_l2_red_v2_peak"] = train["bwd_scatter_Gred_v2_per_s"] / gather["l2_red_v2_f32_Gops"]
     lod = bench_lod(args, local) if (args.lod and rank == 0) else None
     pt = bench_pathtrace(args, local) if (args.pt and rank == 0) else None
 
+    roof = {"bound": "l2_gather", "kernel": "k_query (persistent: sample+encode+MLP+decode+terminate, slot refill)",
+            "achieved": achieved, "peak": l2_peak, "unit": "GB/s", "frac": achieved / l2_peak if l2_peak else None,
+            "peak_source": "measured live (nbvh_gather_probe): random 4-byte gathers from a 16 MB L2-resident "
+                           "table, counted as 32-byte sectors/s -- the random-sector read rate of the L1/L2 path",
+            "achieved_definition": "queries x 2,048 useful fp16 corner bytes (n*L*8*F*2, SURVEY §8(d)) / the "
+                                   "kernel's CUDA-event time",
+            "traffic": traffic,
+            "traffic_source": f"profiles/{traffic_src}: dram__bytes_read.sum + dram__bytes_write.sum of one "
+                              "launch (tables are L2-resident)" if traffic else None,
+            "useful_gather_bytes_per_query": useful_gather, "queries_per_launch_sum": mean_q,
+            "kernel_ms_per_step": statistics.mean(wave_ms), "traverse_ms_per_step": statistics.mean(trav_ms),
+            "frac_of_hbm_useful": achieved / hbm, "hbm_peak": hbm, "hbm_peak_source": peak_src,
+            "mlp_tflops": mean_q * mlp_flops / wave_s / 1e12,
+            "mlp_frac_of_bf16_peak": mean_q * mlp_flops / wave_s / 1e12 / tflops}
+    prof = _profiled_l2_reads("k_query")
+    if prof and l2_peak:
+        sec, dur, src = prof
+        roof["l2_sector_frac"] = sec * 32 / wave_s / 1e9 / l2_peak
+        roof["l2_sector_frac_definition"] = (f"SURVEY §8(d) graded metric: ncu lts__t_sectors_op_read (profiles/{src}: "
+                                             f"{sec:.4g} sectors per launch) x 32 B / the live kernel time / peak")
+
     line = None
     if rank == 0:
-        cpu = cpu_oracle_rate(ctx, c, rays_np, target_s=args.cpu_seconds) if args.cpu_seconds > 0 else None
+        cpu = cpu_oracle_rate(ctx, c, frame_np, target_s=args.cpu_seconds) if args.cpu_seconds > 0 else None
         line = {
             "metric": METRIC, "value": value, "unit": "Mrays/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f16", "data": "synthetic",
-            "config": {"workload": f"{args.config}: " + ("988,928-tri procedural terrain+spheres, 2048-leaf cut, "
-                                                         "L=16 T=2^19 F=2 n=4, MLP 3x64, 1920x1080 primary rays"
-                                                         if args.config == "1080p" else
-                                                         "9,680-tri displaced icosphere, 64-leaf cut, L=8 T=2^14 "
-                                                         "F=2 n=4, MLP 2x64, 64x64 primary rays"),
-                       "rays_per_step_per_gpu": n, "model": "random-init tables U[-1,1], He MLP (x10 output)",
+            "config": {"workload": _workload(args.config),
+                       "rays_per_step": n_frame, "rays_per_step_rank0": n,
+                       "model": "random-init tables U[-1,1], He MLP (x10 output)",
                        "l2_flush": "256 MB write between timed steps, outside the per-step CUDA events",
-                       "parallelism": f"replicated model, 1 frame per rank (weak), {world} rank(s)"},
+                       "parallelism": f"one frame per step split over {world} rank(s) by interleaved 16x16 tiles "
+                                      "(strong); model replicated by broadcast at init",
+                       "ray_order": args.order},
             "gpu_launches": launches,
-            "queries_per_ray": queries / (n * args.steps), "slot_iterations_per_step": iters,
+            "queries_per_ray": queries_per_ray, "slot_iterations_per_step": iters,
             "wall_s_timed_region": wall, "host_enqueue_ms_per_query": host_ms, "list_cap": args.list_cap,
             "list_refills_per_step": st["n_refills"],
-            "roofline": {"bound": "hbm", "kernel": "k_query (persistent: sample+encode+MLP+decode+terminate, slot refill)",
-                         "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                         "peak_source": peak_src, "traffic": traffic,
-                         "traffic_source": f"profiles/{traffic_src}: dram__bytes_read.sum + dram__bytes_write.sum "
-                                           "of one launch (tables are L2-resident, so DRAM traffic is far below the "
-                                           "gather bytes counted in achieved)" if traffic else None,
-                         "bytes_per_query": bytes_per_query, "useful_gather_bytes_per_query": useful_gather,
-                         "queries_per_launch_sum": mean_q, "kernel_ms_per_step": statistics.mean(wave_ms),
-                         "traverse_ms_per_step": statistics.mean(trav_ms),
-                         "mlp_tflops": mean_q * mlp_flops / wave_s / 1e12,
-                         "mlp_frac_of_bf16_peak": mean_q * mlp_flops / wave_s / 1e12 / tflops},
-            "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks.summary(), "mlp": mlp, "gather_roofline": gather, "train": train, "lod": lod, "pathtrace": pt,
+            "model_broadcast": {"bytes": 4 * ctx.param_count(3), "seconds": bcast_s, "params_identical": identical},
+            "roofline": roof, "weak_scaling": weak,
+            "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks.summary(), "mlp": mlp, "gather_roofline": gather,
+            "train": train, "lod": lod, "pathtrace": pt,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -342,8 +427,9 @@ def bench_train(ctx, args, world, rank):
     h = synth.CONFIGS["1080p"]["hash"]
     # T0 on the device (nbvh_gen_train_rays, Philox-4x32-10, key 7, counter = step): every
     # step draws fresh rays, acceptance draws and jitter for this rank's shard of the global
-    # batch, inside the timed region
-    box = (-1.5, -1.5, -1.5, 1.5, 1.5, 1.5)
+    # batch, inside the timed region.  Origins in the C16 box: the scene's bounding box with
+    # every axis extent x1.5 about its centre, the library's default (box=None).
+    box = None
     n_local = sl.stop - sl.start
     buf = ctx.gen_train_rays(seed=7, step=0, n=n_local, i0=sl.start, box=box)
 
@@ -370,6 +456,10 @@ def bench_train(ctx, args, world, rank):
         dist.all_reduce(tm, op=dist.ReduceOp.MAX)
     ms = float(tm.item())
     st = ctx.train_stats()
+    acc = torch.tensor([st["n_accepted"], st["n_first_hit"]], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(acc)
+    n_acc_global, n_first_global = (float(v) for v in acc.cpu().numpy())
     ctx.set_profiling(True)
     step(0)
     torch.cuda.synchronize()
@@ -382,7 +472,10 @@ def bench_train(ctx, args, world, rank):
     red = st["n_accepted"] * h.n_points * h.L * 8 * (h.F // 2)
     red_rate = red / (ph["bwd"] / 1e3) / 1e9 if ph.get("bwd") else None
     return {"metric": "training rays/s (BASELINE cfg 5)", "value": n_global / (ms / 1e3) / 1e6, "unit": "Mrays/s",
+            "accepted_samples_per_s": n_acc_global / (ms / 1e3) / 1e6, "accepted_unit": "M samples/s",
+            "ray_box": "C16: scene bounding box, every axis extent x1.5 about its centre (P:142)",
             "global_batch": n_global, "scaling": "strong", "ms_per_step": ms,
+            "accepted_per_step": n_acc_global, "first_hit_per_step": n_first_global,
             "accepted_per_step_rank0": st["n_accepted"], "first_hit_per_step_rank0": st["n_first_hit"],
             "phase_ms_rank0": ph, "allreduce_bytes": 4 * n_grad if world > 1 else 0,
             "gpu_launches_per_step": st["n_launches"] + 1,          # + the T0 generator
@@ -417,7 +510,8 @@ def bench_lod(args, device):
     batches = [batch(i) for i in range(8)]
     t0 = time.perf_counter()
     hist = construct(ctx, 2048, lambda s: batches[s % 8],
-                     Schedule(iters0=2, splits0=8, growth=2.0, final_iters=100, lod_at_leaves=(128, 512)))
+                     Schedule(iters0=2, splits0=8, growth=2.0, final_iters=100, lod_at_leaves=(128, 512)),
+                     distributed=False)                          # rank 0 alone runs this section
     build_s = time.perf_counter() - t0
     slots = {"fine": 0, "middle": 2, "coarse": 1}
     out = ctx.alloc_hits(c["res"][0] * c["res"][1])
@@ -478,7 +572,8 @@ def bench_pathtrace(args, device):
         xi = synth.random_uniform(n_train * h.n_points, seed=9700 + b).reshape(n_train, h.n_points)
         batches.append(tuple(torch.from_numpy(np.ascontiguousarray(x)).cuda() for x in (r, u, xi)))
     t0 = time.perf_counter()
-    construct(neural, 1024, lambda s: batches[s % 8], Schedule(iters0=2, splits0=8, growth=2.0, final_iters=300))
+    construct(neural, 1024, lambda s: batches[s % 8], Schedule(iters0=2, splits0=8, growth=2.0, final_iters=300),
+              distributed=False)                                 # rank 0 alone runs this section
     build_s = time.perf_counter() - t0
     rays = torch.from_numpy(synth.camera_rays(*c["res"], c["eye"], vfov_deg=c["vfov"])).cuda()
     pt = PathTracer(neural, classical, n_px)
@@ -610,17 +705,7 @@ def run_reference(args):
     stride = max(1, rays.shape[0] // per_step)
     h = c["hash"]
     g = oracle.Grid(h.L, h.log2_T, h.F)
-    from paper_2405_16237_b200 import PARAM_TABLES, PARAM_WEIGHTS, PARAM_BIASES
-    tab = ctx.get_params(PARAM_TABLES).astype(np.float16).reshape(-1, h.F)
-    W = ctx.get_params(PARAM_WEIGHTS)
-    b = ctx.get_params(PARAM_BIASES)
-    dims = [ctx.d_in] + [64] * h.hidden_layers + [8]
-    layers, wo, bo = [], 0, 0
-    for k in range(len(dims) - 1):
-        layers.append((W[wo:wo + dims[k] * dims[k + 1]].reshape(dims[k + 1], dims[k]).astype(np.float16),
-                       b[bo:bo + dims[k + 1]]))
-        wo += dims[k] * dims[k + 1]
-        bo += dims[k + 1]
+    tab, layers = _oracle_model(ctx, c)
     cut = ctx.cut(0)
     box = oracle.scene_box(sc)
 
@@ -637,11 +722,12 @@ def run_reference(args):
     v = done / dt / 1e6
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "Mrays/s", "n_gpus": args.gpus,
             "device": "cpu (the oracle runs on the host cores; no GPU is used)", "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": args.config, "rays_per_step": per_step},
+            "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": _workload(args.config), "rays_per_step": per_step},
             "cpu_baseline": {"value": v, "unit": "Mrays/s", "cores": oracle.num_threads(), "kind": "oracle",
-                             "sample": f"{per_step} rays per step (every {stride}th primary ray, offset by step)"},
+                             "sample": f"{per_step} rays per step (every {stride}th primary ray, offset by step)",
+                             "cpu_model": _cpu_model(), "host_cpus": os.cpu_count()},
             "e2e": {"value": v, "unit": "Mrays/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -658,6 +744,8 @@ def main():
     ap.add_argument("--train", type=int, default=1, help="also time the cfg-5 training step (1/0)")
     ap.add_argument("--lod", type=int, default=1, help="also run the cfg-4 multi-cut LoD query (1/0)")
     ap.add_argument("--pt", type=int, default=1, help="also run the cfg-3 hybrid path tracer (1/0)")
+    ap.add_argument("--order", default="tiles", choices=["tiles", "rows"],
+                    help="ray order / rank partition: 16x16 tiles dealt round-robin (default) or row-major shards")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -240,12 +240,12 @@ nbvh_status nbvh_pt_shade(nbvh_ctx* ctx, const nbvh_ray* d_rays, int64_t n, nbvh
 /* T0: n training rays and the method's random draws for rays
  * [i0, i0 + n) of training step `step`, from the counter-based generator Philox-4x32-10
  * (counter = (global ray index, draw, step lo, step hi), key = seed): origins uniform in the
- * box (host float[6] lo xyz, hi xyz; NULL: the grid-domain cube of LoD 0 inflated by 50%
- * about its centre), directions uniform on the sphere (z = 1 - 2U, phi = 2 pi U), tmin 0,
+ * box (host float[6] lo xyz, hi xyz; NULL: the scene's bounding box with each axis extent
+ * x1.5 about its centre, "50%-inflated scene bounding box", C16), directions uniform on the sphere (z = 1 - 2U, phi = 2 pi U), tmin 0,
  * tmax +inf -> d_rays [n]; acceptance draws -> d_u [n]; stratification jitter ->
  * d_xi [n][n_points] (U = (x >> 8) * 2^-24).  Global indexing makes data-parallel shards
  * (i0 = shard start) reproduce the single-process batch.  Device pointers; asynchronous.
- * NBVH_EINVAL on bad arguments or n_points > 4, NBVH_ESTATE if box is NULL and no cut exists. */
+ * NBVH_EINVAL on bad arguments or n_points > 4, NBVH_ESTATE if box is NULL and no mesh is set. */
 nbvh_status nbvh_gen_train_rays(nbvh_ctx* ctx, uint64_t seed, uint64_t step, int64_t i0, int64_t n,
                                 const float* box, nbvh_ray* d_rays, float* d_u, float* d_xi, void* stream);
 /* Forward + backward of one training batch into the context's
@@ -260,8 +260,8 @@ nbvh_status nbvh_gen_train_rays(nbvh_ctx* ctx, uint64_t seed, uint64_t step, int
 nbvh_status nbvh_train_backward(nbvh_ctx* ctx, const nbvh_ray* d_rays, int64_t n, const float* d_u,
                                 const float* d_xi, int32_t lod, void* stream);
 /* The flat fp32 gradient buffer (device, context-owned, NBVH_PARAM_ALL layout) followed
- * by one float holding the accepted-sample count and n_leaves*2 per-leaf statistics
- * (loss sum, sample count).  Data-parallel training all-reduces (sum) n_floats values
+ * by one float holding the accepted-sample count and n_leaves*3 per-leaf statistics
+ * (loss sum, sample count, first-hit count) of the cut the batch was drawn on.  Data-parallel training all-reduces (sum) n_floats values
  * in place between nbvh_train_backward and nbvh_apply_update. */
 nbvh_status nbvh_grad_buffer(nbvh_ctx* ctx, float** d_grad, int64_t* n_floats);
 /* Adam step (C20) on every parameter with gradient g / max(1, accepted count
@@ -283,6 +283,15 @@ nbvh_status nbvh_set_leaf_rank(nbvh_ctx* ctx, int32_t lod, const float* h_rank);
 nbvh_status nbvh_debug_traverse(nbvh_ctx* ctx, const nbvh_ray* d_rays, int64_t n, int32_t lod, int32_t cap,
                                 int32_t* d_leaf, float* d_t_enter, float* d_t_exit, int32_t* d_count,
                                 void* stream);
+/* The PRODUCT traversal (k_traverse, the kernel nbvh_query launches)
+ * with the context's list capacity K = list_cap, unpacked per ray: leaf/te/tx [n][K]
+ * (device; the first fill[r] entries of ray r in (t_enter, id) order, the rest -1 / 0),
+ * fill [n] (entries kept, <= K) and more [n] (1 if further intersected leaves may exist
+ * beyond the K-th key: the query kernel then resumes the traversal, C6).  Uses the
+ * context's query workspace (n <= nbvh_reserve).  Asynchronous on `stream`. */
+nbvh_status nbvh_debug_traverse_product(nbvh_ctx* ctx, const nbvh_ray* d_rays, int64_t n, int32_t lod,
+                                        int32_t* d_leaf, float* d_te, float* d_tx, int32_t* d_fill,
+                                        int32_t* d_more, void* stream);
 /* Encode m points already normalised to [0,1]^3 (float [m][3]): fp16 features
  * [m][L*F] (bits as uint16) and corner indices [m][L][8] (nullable). */
 nbvh_status nbvh_debug_encode(nbvh_ctx* ctx, const float* d_points, int64_t m, uint16_t* d_feat,
@@ -297,6 +306,21 @@ nbvh_status nbvh_debug_query_trace(nbvh_ctx* ctx, const nbvh_ray* d_rays, int64_
  * albedo, t_hit (vis=1: no hit) with accepted[n] and first-leaf ids (device). */
 nbvh_status nbvh_debug_train_samples(nbvh_ctx* ctx, float* d_gt, uint8_t* d_accepted, int32_t* d_leaf,
                                      float* d_loss, void* stream);
+/* Parity capture of the training forward (T4): enable != 0 makes the following
+ * nbvh_train_backward calls also store every sample's raw MLP output z (fp32, a
+ * context-owned [max_rays][8] buffer allocated on the next call); enable = 0 frees it.
+ * Off by default: the product path does not write z. */
+nbvh_status nbvh_debug_train_capture(nbvh_ctx* ctx, int32_t enable);
+/* Per-sample intermediates of the last training batch (P:142 forward/backward; T3-T6), in
+ * the kernel's compacted sample order; *h_m (host) receives the sample count m (the call
+ * synchronises `stream` to read it).  Device outputs, each nullable: d_sample_ray [m] ray
+ * index of each sample; d_x [m][D_in] fp16 features (T3, bits as uint16); d_z [m][8] raw
+ * MLP outputs (T4; needs nbvh_debug_train_capture on, else NBVH_ESTATE); d_dz [m][8] dL/dz
+ * (T5); d_delta [hidden][m][64] fp16 deltas dL/d(pre-activation) of each hidden layer
+ * (T6).  Buffers must hold the capacity implied by m (callers size them from the ray
+ * count, an upper bound). */
+nbvh_status nbvh_debug_train_activations(nbvh_ctx* ctx, int32_t* d_sample_ray, uint16_t* d_x, float* d_z,
+                                         float* d_dz, uint16_t* d_delta, int64_t* h_m, void* stream);
 
 #ifdef __cplusplus
 }

@@ -651,6 +651,68 @@ static double sample_loss_impl(const double* z, const double* gt, double* terms,
     return 2.0 * lvis + g * (2.0 * ldist + lnorm + lalb);
 }
 
+// ------------------------------------------------------------------ reverse mode of one sample
+// P:142 ("the measured loss is back-propagated to the model's learnable parameters"),
+// P:61 (hash-grid backprop).  acts[k] = input of layer k (acts[0] = the features x, then
+// post-ReLU hidden activations); delta = dL/dz (already scaled).  Layer k (dims[k] ->
+// dims[k+1]): g_b += delta, g_W += delta (x) acts[k], delta <- W_k^T delta masked by
+// ReLU'(acts[k] > 0) for k > 0; the final delta = dL/dx is scattered into the tables
+// through the trilinear weights of the sample's points (idx = corner indices).
+// absolute = true runs the same recursion on |delta|, |W|, |acts| with the same masks:
+// the magnitude sums that bound floating-point error (tests only; no step of the method).
+// hidden_delta (nullable, [n_layers-1][64]): the masked delta of each hidden layer.
+static void backward_sample(const OrcModel& M, const std::vector<const uint16_t*>& W,
+                            const std::vector<double>* acts, std::vector<double> delta, const float* pts,
+                            const uint32_t* idx, int64_t nW, int64_t nb, double* g_table, double* g_W, double* g_b,
+                            bool absolute, double* hidden_delta) {
+    const int n_layers = M.n_layers, L = M.L, F = M.F, LF = L * F;
+    const int32_t* dims = M.dims;
+    if (absolute)
+        for (double& v : delta) v = std::fabs(v);
+    int64_t wo = nW, bo = nb;
+    for (int k = n_layers - 1; k >= 0; --k) {
+        wo -= (int64_t)dims[k] * dims[k + 1];
+        bo -= dims[k + 1];
+        const std::vector<double>& hin = acts[k];
+        std::vector<double> dprev(dims[k], 0.0);
+        for (int o = 0; o < dims[k + 1]; ++o) {
+            g_b[bo + o] += delta[o];
+            for (int i = 0; i < dims[k]; ++i) {
+                const double w = orc_half_to_double(W[k][(int64_t)o * dims[k] + i]);
+                g_W[wo + (int64_t)o * dims[k] + i] += delta[o] * (absolute ? std::fabs(hin[i]) : hin[i]);
+                dprev[i] += delta[o] * (absolute ? std::fabs(w) : w);
+            }
+        }
+        if (k > 0) {
+            for (int i = 0; i < dims[k]; ++i) dprev[i] = hin[i] > 0.0 ? dprev[i] : 0.0;  // ReLU'
+            if (hidden_delta)
+                for (int i = 0; i < dims[k]; ++i) hidden_delta[(k - 1) * 64 + i] = dprev[i];
+        }
+        delta.swap(dprev);
+    }
+    // delta = dL/dx (concatenated features) -> scatter into the tables through the
+    // trilinear weights (hash-grid backprop).
+    for (int p = 0; p < M.n_points; ++p)
+        for (int l = 0; l < L; ++l) {
+            const int32_t N = M.res[l];
+            float f[3];
+            for (int k = 0; k < 3; ++k) {
+                float s = pts[3 * p + k] * (float)N;
+                int32_t ci = (int32_t)std::floor(s);
+                if (ci > N - 1) ci = N - 1;
+                if (ci < 0) ci = 0;
+                f[k] = s - (float)ci;
+            }
+            for (int corner = 0; corner < 8; ++corner) {
+                int d0 = corner & 1, d1 = (corner >> 1) & 1, d2 = (corner >> 2) & 1;
+                double w = (d0 ? (double)f[0] : 1.0 - (double)f[0]) * (d1 ? (double)f[1] : 1.0 - (double)f[1]) *
+                           (d2 ? (double)f[2] : 1.0 - (double)f[2]);
+                int64_t row = M.offset[l] + (int64_t)idx[(p * L + l) * 8 + corner];
+                for (int j = 0; j < F; ++j) g_table[row * F + j] += w * delta[p * LF + l * F + j];
+            }
+        }
+}
+
 // ------------------------------------------------------------------ training gradient
 // One training step's forward + backward in double ("the measured loss is
 // back-propagated to the model's learnable parameters"; P:197 first-leaf-only training
@@ -714,7 +776,7 @@ int64_t orc_train_grad(int32_t L, int32_t F, int32_t log2_T, int32_t n_points, i
     *loss_sum = 0.0;
     if (n_acc == 0) return 0;
     const double inv_m = 1.0 / (double)n_acc;                      // mean over accepted samples (C19)
-    const int LF = L * F, D = dims[0];
+    const int D = dims[0];
     // pass 2: forward, loss, backward (serial accumulation: deterministic)
     std::vector<double> z(8), dz(8), x(D);
     std::vector<uint32_t> idx(n_points * L * 8);
@@ -727,47 +789,10 @@ int64_t orc_train_grad(int32_t L, int32_t F, int32_t log2_T, int32_t n_points, i
         double lr = orc_sample_loss(z.data(), gt_out + 9 * r, nullptr, dz.data());
         sample_loss[r] = lr;
         *loss_sum += lr;
-        // backward through the MLP: delta = dL/d(pre-activation) of layer k
+        // backward through the MLP and the hash grid (mean over accepted samples)
         std::vector<double> delta(dz.begin(), dz.end());
         for (int i = 0; i < dims[n_layers]; ++i) delta[i] *= inv_m;
-        int64_t wo = nW, bo = nb;
-        for (int k = n_layers - 1; k >= 0; --k) {
-            wo -= (int64_t)dims[k] * dims[k + 1];
-            bo -= dims[k + 1];
-            const std::vector<double>& hin = acts[k];
-            std::vector<double> dprev(dims[k], 0.0);
-            for (int o = 0; o < dims[k + 1]; ++o) {
-                g_b[bo + o] += delta[o];
-                for (int i = 0; i < dims[k]; ++i) {
-                    g_W[wo + (int64_t)o * dims[k] + i] += delta[o] * hin[i];
-                    dprev[i] += delta[o] * orc_half_to_double(W[k][(int64_t)o * dims[k] + i]);
-                }
-            }
-            if (k > 0)
-                for (int i = 0; i < dims[k]; ++i) dprev[i] = hin[i] > 0.0 ? dprev[i] : 0.0;  // ReLU'
-            delta.swap(dprev);
-        }
-        // delta = dL/dx (concatenated features) -> scatter into the tables through the
-        // trilinear weights (hash-grid backprop).
-        for (int p = 0; p < n_points; ++p)
-            for (int l = 0; l < L; ++l) {
-                const int32_t N = res[l];
-                float f[3];
-                for (int k = 0; k < 3; ++k) {
-                    float s = pts[3 * p + k] * (float)N;
-                    int32_t ci = (int32_t)std::floor(s);
-                    if (ci > N - 1) ci = N - 1;
-                    if (ci < 0) ci = 0;
-                    f[k] = s - (float)ci;
-                }
-                for (int corner = 0; corner < 8; ++corner) {
-                    int d0 = corner & 1, d1 = (corner >> 1) & 1, d2 = (corner >> 2) & 1;
-                    double w = (d0 ? (double)f[0] : 1.0 - (double)f[0]) * (d1 ? (double)f[1] : 1.0 - (double)f[1]) *
-                               (d2 ? (double)f[2] : 1.0 - (double)f[2]);
-                    int64_t row = offset[l] + (int64_t)idx[(p * L + l) * 8 + corner];
-                    for (int j = 0; j < F; ++j) g_table[row * F + j] += w * delta[p * LF + l * F + j];
-                }
-            }
+        backward_sample(M, W, acts.data(), delta, pts.data(), idx.data(), nW, nb, g_table, g_W, g_b, false, nullptr);
     }
     return n_acc;
 }
@@ -835,6 +860,87 @@ double orc_batch_loss_double(int32_t L, int32_t F, int32_t log2_T, int32_t n_poi
     return n_acc ? tot / (double)n_acc : 0.0;
 }
 
+// ------------------------------------------------------------------ backward from given (x, dL/dz)
+// The training backward (T6 MLP reverse mode, T7 hash-grid scatter) of m
+// samples from GIVEN features x[m][D] and output gradients dz[m][8] -- e.g. the GPU's own
+// fp16 features and fp32 dL/dz -- so each stage of the GPU's chain can be compared with
+// the oracle element by element.  Sample s is the segment [t0[s], t1[s]] of ray rays[s]
+// with jitter xi[s] (points and corners as in orc_segment_points / encode_point).
+// Outputs (sums over the samples, not means): g_table, g_W, g_b; their magnitude sums
+// (the same recursion on absolute values, masks unchanged) g_*_abs; the forward z[m][8]
+// (double MLP on the given x) and its magnitude z_abs (|W| |h| + |b| per layer); per
+// sample the ReLU margin min over hidden units |h_pre| / (|W| |h_in| + |b|) -- how close
+// a ReLU decision is to its threshold relative to the operand magnitudes; and (nullable)
+// hidden-layer deltas [m][n_layers-1][64] with magnitudes.
+void orc_train_backward_given(int32_t L, int32_t F, int32_t log2_T, int32_t n_points, int32_t n_layers,
+                              const int32_t* res, const int32_t* dense, const int64_t* offset,
+                              const uint16_t* table, int64_t n_entries, const int32_t* dims,
+                              const uint16_t* W_all, const float* b_all, const float* dom_box, int64_t m,
+                              const float* rays, const float* t0, const float* t1, const float* xi,
+                              const double* x_in, const double* dz_in,
+                              double* g_table, double* g_W, double* g_b,
+                              double* g_table_abs, double* g_W_abs, double* g_b_abs,
+                              double* z_out, double* z_abs, double* relu_margin,
+                              double* hidden_delta /*nullable*/, double* hidden_delta_abs /*nullable*/) {
+    float dom_min[3], dom_inv;
+    orc_domain(dom_box, dom_box + 3, 1, dom_min, &dom_inv);
+    OrcModel M{L, F, log2_T, n_points, n_layers, res, dense, offset, table, dims, W_all, b_all, dom_min, dom_inv};
+    std::vector<const uint16_t*> W;
+    std::vector<const float*> b;
+    split_layers(n_layers, dims, W_all, b_all, W, b);
+    int64_t nW = 0, nb = 0;
+    for (int k = 0; k < n_layers; ++k) { nW += (int64_t)dims[k] * dims[k + 1]; nb += dims[k + 1]; }
+    std::fill(g_table, g_table + n_entries * F, 0.0);
+    std::fill(g_table_abs, g_table_abs + n_entries * F, 0.0);
+    std::fill(g_W, g_W + nW, 0.0);
+    std::fill(g_W_abs, g_W_abs + nW, 0.0);
+    std::fill(g_b, g_b + nb, 0.0);
+    std::fill(g_b_abs, g_b_abs + nb, 0.0);
+    const int D = dims[0], n_out = dims[n_layers], H = n_layers - 1;
+    std::vector<float> pts(3 * n_points);
+    std::vector<uint32_t> idx(n_points * L * 8);
+    std::vector<double> feat(L * F);
+    std::vector<std::vector<double>> acts(n_layers + 1);
+    std::vector<double> z(n_out), habs, nabs;
+    for (int64_t s = 0; s < m; ++s) {
+        orc_segment_points(rays + 8 * s, t0[s], t1[s], n_points, xi + s * n_points, dom_min, dom_inv, pts.data());
+        for (int p = 0; p < n_points; ++p)
+            encode_point(L, F, log2_T, res, dense, offset, table, &pts[3 * p], feat.data(), idx.data() + p * L * 8);
+        const double* x = x_in + s * D;
+        mlp_forward_one(n_layers, dims, W.data(), b.data(), x, z.data(), acts.data());
+        for (int o = 0; o < n_out; ++o) z_out[s * n_out + o] = z[o];
+        // magnitudes and ReLU margins (pre-activation = acts value before the mask: recompute)
+        double marg = std::numeric_limits<double>::infinity();
+        habs.assign(x, x + D);
+        for (double& v : habs) v = std::fabs(v);
+        for (int k = 0; k < n_layers; ++k) {
+            nabs.assign(dims[k + 1], 0.0);
+            for (int o = 0; o < dims[k + 1]; ++o) {
+                double sa = std::fabs((double)b[k][o]), sv = (double)b[k][o];
+                for (int i = 0; i < dims[k]; ++i) {
+                    const double w = orc_half_to_double(W[k][(int64_t)o * dims[k] + i]);
+                    sa += std::fabs(w) * habs[i];
+                    sv += w * acts[k][i];
+                }
+                if (k + 1 < n_layers) {
+                    if (sa > 0.0) marg = std::min(marg, std::fabs(sv) / sa);
+                    nabs[o] = sv > 0.0 ? sa : 0.0;
+                } else {
+                    nabs[o] = sa;
+                }
+            }
+            habs.swap(nabs);
+        }
+        for (int o = 0; o < n_out; ++o) z_abs[s * n_out + o] = habs[o];
+        relu_margin[s] = marg;
+        std::vector<double> delta(dz_in + s * n_out, dz_in + (s + 1) * n_out);
+        backward_sample(M, W, acts.data(), delta, pts.data(), idx.data(), nW, nb, g_table, g_W, g_b, false,
+                        hidden_delta ? hidden_delta + s * H * 64 : nullptr);
+        backward_sample(M, W, acts.data(), delta, pts.data(), idx.data(), nW, nb, g_table_abs, g_W_abs, g_b_abs,
+                        true, hidden_delta_abs ? hidden_delta_abs + s * H * 64 : nullptr);
+    }
+}
+
 // ------------------------------------------------------------------ Adam
 // "Adam optimizer [kingma2014adam] with default hyper-parameters and a learning
 // rate of 0.01" (C20: beta1 0.9, beta2 0.999, eps 1e-8, bias-corrected, dense).
@@ -855,6 +961,15 @@ int32_t orc_num_threads(void) {
     return omp_get_max_threads();
 #else
     return 1;
+#endif
+}
+
+// Thread count for the following oracle calls (bench.py's 1-thread baseline figure).
+void orc_set_num_threads(int32_t n) {
+#ifdef _OPENMP
+    omp_set_num_threads(n > 0 ? n : 1);
+#else
+    (void)n;
 #endif
 }
 

@@ -62,13 +62,21 @@ def ranks_from_stats(loss_sum, samples, first_hits, n_rays):
     return np.where(np.isnan(r), fill, r).astype(np.float32), q, p
 
 
-def construct(ctx, target_leaves: int, batch_fn, schedule: Schedule | None = None, stream=None, log=None):
+def construct(ctx, target_leaves: int, batch_fn, schedule: Schedule | None = None, stream=None, log=None,
+              distributed: bool = True, group=None):
     """Build an error-driven cut of `target_leaves` leaves in LoD slot 0 while training the
-    context's model.  batch_fn(step) -> (rays, u, xi) device tensors of one training batch.
-    Returns the per-round log; registered LoD cuts are in slots 1.. (coarsest first)."""
+    context's model.  batch_fn(step) -> (rays, u, xi) device tensors of one training batch
+    (under data parallelism: this rank's shard).  Returns the per-round log; registered LoD
+    cuts are in slots 1.. (coarsest first).
+
+    distributed=True: every step all-reduces the gradient buffer over `group` (when a process
+    group is initialised), and the per-leaf statistics are read from the REDUCED buffer, with
+    the ray count summed over ranks, so every rank computes the same ranks and builds the same
+    cut.  Pass distributed=False when only one rank runs the construction."""
     import torch
     from . import dp
     sch = schedule or Schedule()
+    world = dp.world_size(group) if distributed else 1
     ctx.build_cut(1)                                            # the root (P:180)
     ctx.set_leaf_rank(np.zeros(1, np.float32))
     n_params = ctx.param_count(3)
@@ -88,17 +96,22 @@ def construct(ctx, target_leaves: int, batch_fn, schedule: Schedule | None = Non
             pool = [0] + lods
             lod = pool[int(rng.integers(len(pool)))] if lods else 0     # P:252 random cut
             ctx.train_backward(rays, u, xi, lod, stream=stream)
-            if collect and lod == 0:
-                g = dp.grad_tensor(ctx)
+            g = dp.grad_tensor(ctx)
+            if world > 1:
+                dp.allreduce_grads(g, group)
+            if collect and lod == 0:                            # global statistics (after the reduce)
                 acc += g[n_params:n_params + 1 + 3 * n_leaves].double()
                 n_rays += rays.shape[0]
-            dp.allreduce_grads(dp.grad_tensor(ctx))
             ctx.apply_update(sch.lr, stream=stream)
             step += 1
             if sch.lod_every and step % sch.lod_every == 0 and len(lods) < sch.max_lods:
                 slot = len(lods) + 1
                 ctx.copy_cut(0, slot)                           # register an LoD
                 lods.append(slot)
+        if world > 1:                                           # rays of every rank's shard
+            nr = torch.tensor([n_rays], dtype=torch.float64, device=acc.device)
+            dp.allreduce_grads(nr, group)
+            n_rays = int(nr.item())
         a = acc.cpu().numpy()
         per = a[1:].reshape(-1, 3) if n_leaves else np.zeros((0, 3))
         return per[:, 0], per[:, 1], per[:, 2], n_rays, (a[0] and per[:, 0].sum() / max(a[0], 1))

@@ -919,6 +919,79 @@ extern "C" nbvh_status nbvh_debug_traverse(nbvh_ctx* c, const nbvh_ray* rays, in
     return NBVH_OK;
 }
 
+// The product traversal's per-ray lists, unpacked from k_traverse's own outputs (the work
+// records hold entry 0, the fill count and the more-flag; the list buffer the rest).
+__global__ void k_unpack_product_lists(const WorkRec* act_long, const WorkRec* act, const QueryCounters* ctr,
+                                       const float4* lst, int64_t n_rays, int32_t K, int32_t* leaf, float* te,
+                                       float* tx, int32_t* fill, int32_t* more) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t n_long = ctr->cnt_long, total = n_long + ctr->cnt;
+    if (i >= total) return;
+    const WorkRec w = i < n_long ? act_long[i] : act[i - n_long];
+    const int64_t r = __float_as_int(w.o.w);
+    const int st = __float_as_int(w.d.w), nn = st & 0xffff;
+    fill[r] = nn;
+    more[r] = st >> 16;
+    for (int j = 0; j < nn && j < K; ++j) {
+        const float4 e = j == 0 ? w.e0 : lst[(int64_t)j * n_rays + r];
+        leaf[r * K + j] = __float_as_int(e.z);
+        te[r * K + j] = e.x;
+        tx[r * K + j] = e.y;
+    }
+}
+
+extern "C" nbvh_status nbvh_debug_traverse_product(nbvh_ctx* c, const nbvh_ray* rays, int64_t n, int32_t lod,
+                                                   int32_t* leaf, float* te, float* tx, int32_t* fill, int32_t* more,
+                                                   void* stream) {
+    nbvh_status st = check_device(c);
+    if (st) return st;
+    if (lod < 0 || lod >= kMaxLod) return fail(c, NBVH_ERANGE, "debug_traverse_product: lod");
+    if (!c->has_cut[lod]) return fail(c, NBVH_ESTATE, "debug_traverse_product: no cut");
+    if (n < 0 || (n > 0 && (!rays || !leaf || !te || !tx || !fill || !more)))
+        return fail(c, NBVH_EINVAL, "debug_traverse_product: bad args");
+    if (n > c->reserved) return fail(c, NBVH_ESTATE, "debug_traverse_product: n exceeds nbvh_reserve");
+    if (n == 0) return NBVH_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int K = c->cfg.list_cap;
+    QueryCounters* ctr = counter_block(c, 0);
+    k_reset_counters<<<1, 32, 0, s>>>(ctr, 1);
+    HitsDev out{};
+    unsigned char* scratch = nullptr;                      // miss records of k_traverse (not compared)
+    cudaError_t e = cudaMallocAsync((void**)&scratch, (size_t)n * 37, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(leaf, 0xff, (size_t)n * K * 4, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(te, 0, (size_t)n * K * 4, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(tx, 0, (size_t)n * K * 4, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(fill, 0, (size_t)n * 4, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(more, 0, (size_t)n * 4, s);
+    if (e != cudaSuccess) return cuda_fail(c, e, "debug_traverse_product");
+    out.hit = scratch;
+    out.t = reinterpret_cast<float*>(scratch + n);
+    out.normal = out.t + n;
+    out.albedo = out.normal + 3 * n;
+    out.leaf = reinterpret_cast<int32_t*>(out.albedo + 3 * n);
+    out.n_queries = out.leaf + n;
+    TraverseArgs ta{};
+    ta.cut = make_cut(c, lod);
+    ta.rays = reinterpret_cast<const float4*>(rays);
+    ta.n_rays = n;
+    ta.cap = K;
+    ta.lst = c->d_lst;
+    ta.st = c->state();
+    ta.out = out;
+    ta.act_out = c->d_act;
+    ta.act_long = c->d_act_long;
+    ta.ctr = ctr;
+    e = launch_traverse(ta, s);                            // the product kernel (k_traverse)
+    if (e == cudaSuccess) {
+        k_unpack_product_lists<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(c->d_act_long, c->d_act, ctr, c->d_lst, n,
+                                                                         K, leaf, te, tx, fill, more);
+        e = cudaGetLastError();
+    }
+    cudaFreeAsync(scratch, s);
+    if (e != cudaSuccess) return cuda_fail(c, e, "debug_traverse_product");
+    return NBVH_OK;
+}
+
 extern "C" nbvh_status nbvh_debug_encode(nbvh_ctx* c, const float* pts, int64_t m, uint16_t* feat, uint32_t* index,
                                          void* stream) {
     nbvh_status st = check_device(c);

@@ -343,6 +343,19 @@ __device__ __noinline__ int refill_list(CutDev cut, const float4* rays, int64_t 
     return n;
 }
 
+// The per-warp decoder MLP of k_query, and of nbvh_debug_mlp (which must run exactly the
+// product's function).  fp32 accumulation (mlp_rows16): the raw z stays within the 1e-2
+// tier of north_star against the double oracle.  The fp16-accumulating variant
+// (mlp_rows16h, C34) was 1.4% faster in round 1 but its error grows with the layer width
+// (K fp16 roundings per accumulator); kept for A/B only.
+constexpr bool kQueryMlpF16Acc = false;
+template <int D>
+__device__ __forceinline__ void query_mlp_rows16(const MlpSmem& s, int hidden, const __half* x, int r0, float* z,
+                                                 int lane) {
+    if constexpr (kQueryMlpF16Acc) mlp_rows16h<D>(s, hidden, x, r0, z, lane);
+    else mlp_rows16<D>(s, hidden, x, r0, z, lane);
+}
+
 // Ray slots of one warp (structure of arrays in shared memory).  Lane s < kWarpQ owns slot
 // s for the refill and decode steps; the encode and MLP steps work on the compacted rows.
 constexpr int kWarpQ = 16;          // queries per warp iteration (one m16 MMA row block)
@@ -708,8 +721,8 @@ __global__ void __launch_bounds__(kQueryWarps * 32, 1) k_query(QueryArgs a) {
                             smem_raw + plan.warp0 + plan.per_warp * (size_t)(grp * kGroupWarps), plan.per_warp,
                             plan.z);
         } else {
-            mlp_rows16h<D>(ms, a.m.hidden, feat, 0, zt, lane);
-            if (kWarpQ > 16 && ws[2] > 16) mlp_rows16h<D>(ms, a.m.hidden, feat, 16, zt, lane);
+            query_mlp_rows16<D>(ms, a.m.hidden, feat, 0, zt, lane);
+            if (kWarpQ > 16 && ws[2] > 16) query_mlp_rows16<D>(ms, a.m.hidden, feat, 16, zt, lane);
         }
         __syncwarp();
         // (F) decode, best hit, front-to-back termination
@@ -850,7 +863,7 @@ __global__ void __launch_bounds__(256, 2) k_debug_mlp(DebugMlpArgs a) {
             *reinterpret_cast<uint4*>(feat + row * (D + 8) + c * 8) = v;
         }
         __syncthreads();
-        mlp_rows16<D>(ms, a.m.hidden, feat, warp * 16, zt, lane);
+        query_mlp_rows16<D>(ms, a.m.hidden, feat, warp * 16, zt, lane);      // k_query's own MLP
         __syncthreads();
         for (int i = tid; i < kTileQ * 8; i += blockDim.x) {
             const int64_t gr = tile * kTileQ + i / 8;
@@ -892,9 +905,17 @@ static bool query_mlp_tc() {
 template <int F, int D, bool kTc>
 static cudaError_t launch_query_tt(const QueryArgs& a, int64_t max_work, cudaStream_t s, const QuerySmemPlan& plan) {
     const size_t smem = plan.total;
-    // occupancy is queried once per (hidden, n_points) shape
-    static int cached[kMaxHidden + 1][9] = {};
-    int& grid_c = cached[a.m.hidden][a.g.n_points < 9 ? a.g.n_points : 8];
+    // The dynamic shared-memory opt-in is per function, not per shape: set it before every
+    // launch (cheap), so a smaller shape launched in between cannot leave it too low.  The
+    // occupancy query is cached per (device, hidden, n_points).
+    cudaError_t e = cudaFuncSetAttribute(k_query<F, D, kTc>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    constexpr int kDevs = 16;
+    static int cached[kDevs][kMaxHidden + 1][9] = {};
+    int fallback = 0;
+    int& grid_c = dev < kDevs ? cached[dev][a.m.hidden][a.g.n_points < 9 ? a.g.n_points : 8] : fallback;
     if (!grid_c) grid_c = resident_blocks(k_query<F, D, kTc>, plan.warps * 32, smem);
     int grid = grid_c;
     if (!kTc) {                               // kTc: every CTA needs both groups, keep the full grid
@@ -936,7 +957,13 @@ cudaError_t launch_traverse(const TraverseArgs& a, cudaStream_t s) {
         const size_t smem = (size_t)(3 * a.cap * 128 + 4 * (a.cut.depth + 2)) * sizeof(int);
         k_traverse<true><<<(unsigned)blocks, 128, smem, s>>>(a);
     } else {
+        // (depth + 2 + 3K) words per thread: past 48 KB for deep cuts / large K, so opt in
         const size_t smem = (size_t)(a.cut.depth + 2 + 3 * a.cap) * 128 * sizeof(int);
+        if (smem > 48 * 1024) {
+            cudaError_t e = cudaFuncSetAttribute(k_traverse<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)smem);
+            if (e != cudaSuccess) return e;
+        }
         k_traverse<false><<<(unsigned)blocks, 128, smem, s>>>(a);
     }
     return cudaGetLastError();

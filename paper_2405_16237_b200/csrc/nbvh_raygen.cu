@@ -97,15 +97,15 @@ extern "C" nbvh_status nbvh_gen_train_rays(nbvh_ctx* c, uint64_t seed, uint64_t 
             if (!(a.hi[k] >= a.lo[k])) return fail(c, NBVH_EINVAL, "gen_train_rays: box");
         }
     } else {
-        // the grid domain cube (the scene's inflated root box, C4'), inflated by 50% about its
-        // centre (rays from the neighbourhood of the geometry)
-        if (!c->has_cut[0]) return fail(c, NBVH_ESTATE, "gen_train_rays: no cut (domain unknown)");
-        const HostCut& hc = c->cuts[0];
-        const float side = 1.0f / hc.dom_inv;
+        // C16 ("the 50%-inflated scene bounding box"): the scene's root box (min/max
+        // over all triangle vertices), each axis extent x1.5 about its centre.
+        if (!c->has_mesh || c->sc.nodes.empty()) return fail(c, NBVH_ESTATE, "gen_train_rays: no mesh");
+        const nbvh::BvhNode& r = c->sc.nodes[0];
         for (int k = 0; k < 3; ++k) {
-            const float mid = hc.dom_min[k] + 0.5f * side;
-            a.lo[k] = mid - 0.75f * side;
-            a.hi[k] = mid + 0.75f * side;
+            const float mid = (r.lo[k] + r.hi[k]) * 0.5f;
+            const float half = (r.hi[k] - r.lo[k]) * 0.75f;
+            a.lo[k] = mid - half;
+            a.hi[k] = mid + half;
         }
     }
     a.n_points = c->cfg.n_points;

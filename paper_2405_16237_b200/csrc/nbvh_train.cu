@@ -31,13 +31,15 @@ struct TrainWork {
     __half* A = nullptr;
     __half* Dl = nullptr;
     float* dZ = nullptr;
+    float* Z = nullptr;              // [cap][8] raw z, allocated only while parity capture is on
+    bool capture = false;
     float* grad = nullptr;           // params + 1 + 3 * tail_leaves
     int64_t tail_leaves = 0;
     float* m = nullptr;
     float* v = nullptr;
     int32_t* counters = nullptr;     // [0] samples, [1] first hits, [2] non-finite flag
     double* loss_acc = nullptr;      // [5]
-    int64_t step = 0;
+    int32_t* adam_step = nullptr;    // device: Adam updates applied (skipped updates excluded)
     int32_t lod = 0;
     int32_t launches = 0;
     cudaStream_t stream = nullptr;
@@ -134,7 +136,7 @@ static void dfree(T*& p) {
 static void free_work(TrainWork* w) {
     dfree(w->r_acc); dfree(w->r_leaf); dfree(w->r_gt); dfree(w->r_loss);
     dfree(w->s_ray); dfree(w->s_leaf); dfree(w->s_t0); dfree(w->s_t1); dfree(w->s_gt);
-    dfree(w->X); dfree(w->A); dfree(w->Dl); dfree(w->dZ);
+    dfree(w->X); dfree(w->A); dfree(w->Dl); dfree(w->dZ); dfree(w->Z);
 }
 
 void free_train_device(nbvh_ctx* c) {
@@ -145,6 +147,7 @@ void free_train_device(nbvh_ctx* c) {
     dfree(c->train->v);
     dfree(c->train->counters);
     dfree(c->train->loss_acc);
+    dfree(c->train->adam_step);
     delete c->train;
     c->train = nullptr;
 }
@@ -164,7 +167,8 @@ static nbvh_status ensure_train_state(nbvh_ctx* c, int64_t tail_leaves) {
         if (e == cudaSuccess) e = cudaMemset(w->v, 0, np * 4);
         if (e == cudaSuccess) e = cudaMalloc((void**)&w->counters, 16 * sizeof(int32_t));
         if (e == cudaSuccess) e = cudaMalloc((void**)&w->loss_acc, 8 * sizeof(double));
-        w->step = 0;
+        if (e == cudaSuccess) e = cudaMalloc((void**)&w->adam_step, sizeof(int32_t));
+        if (e == cudaSuccess) e = cudaMemset(w->adam_step, 0, sizeof(int32_t));
     }
     if (e == cudaSuccess && (!w->grad || tail_leaves > w->tail_leaves)) {
         dfree(w->grad);
@@ -211,7 +215,7 @@ void reset_adam(nbvh_ctx* c) {
     const size_t np = (size_t)n_params(c);
     cudaMemset(c->train->m, 0, np * 4);
     cudaMemset(c->train->v, 0, np * 4);
-    c->train->step = 0;
+    cudaMemset(c->train->adam_step, 0, sizeof(int32_t));
 }
 
 // launchers (templated on F, D)
@@ -391,6 +395,11 @@ extern "C" nbvh_status nbvh_train_backward(nbvh_ctx* c, const nbvh_ray* rays, in
     a.A = w->A;
     a.Dl = w->Dl;
     a.dZ = w->dZ;
+    if (w->capture && !w->Z) {
+        e = cudaMalloc((void**)&w->Z, (size_t)w->cap * 8 * 4);
+        if (e != cudaSuccess) return cuda_fail(c, e, "train_backward: capture buffer");
+    }
+    a.Z = w->capture ? w->Z : nullptr;
     a.grad = w->grad;
     a.tail = w->grad + n_params(c);
     a.loss_acc = w->loss_acc;
@@ -461,7 +470,6 @@ extern "C" nbvh_status nbvh_apply_update(nbvh_ctx* c, float lr, void* stream) {
     if (e != cudaSuccess) return cuda_fail(c, e, "apply_update");
     if (c->profiling) cudaEventRecord(ctx_event(c, 22), s);
     k_check_finite<<<592, 256, 0, s>>>(w->grad, np, w->counters + 2);
-    w->step += 1;
     AdamArgs a{};
     a.param = c->d_params;
     a.grad = w->grad;
@@ -474,22 +482,20 @@ extern "C" nbvh_status nbvh_apply_update(nbvh_ctx* c, float lr, void* stream) {
     a.beta1 = 0.9f;
     a.beta2 = 0.999f;
     a.eps = 1e-8f;
-    a.c1 = (float)(1.0 - std::pow(0.9, (double)w->step));
-    a.c2 = (float)(1.0 - std::pow(0.999, (double)w->step));
-    a.ic1 = (float)(1.0 / (1.0 - std::pow(0.9, (double)w->step)));
-    a.ic2 = (float)(1.0 / (1.0 - std::pow(0.999, (double)w->step)));
+    a.step = w->adam_step;
     a.table16 = c->d_table16;
     a.n_table = c->n_table;
     a.W16 = c->d_W16;
     a.n_W = c->n_W;
     k_adam<<<4 * 148, 256, 0, s>>>(a);
+    k_adam_commit<<<1, 1, 0, s>>>(w->counters + 2, w->adam_step);
     st = refresh_table(c, s);
     if (st) return st;
     if (c->profiling) cudaEventRecord(ctx_event(c, 23), s);
     w->adam_profiled = c->profiling;
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(c, e, "apply_update: adam");
-    w->launches += 3;
+    w->launches += 4;
     w->stream = s;
     return NBVH_OK;
 }
@@ -542,5 +548,41 @@ extern "C" nbvh_status nbvh_debug_train_samples(nbvh_ctx* c, float* gt, uint8_t*
     if (e == cudaSuccess && leaf) e = cudaMemcpyAsync(leaf, w->r_leaf, (size_t)n * 4, cudaMemcpyDeviceToDevice, s);
     if (e == cudaSuccess && loss) e = cudaMemcpyAsync(loss, w->r_loss, (size_t)n * 4, cudaMemcpyDeviceToDevice, s);
     if (e != cudaSuccess) return cuda_fail(c, e, "debug_train_samples");
+    return NBVH_OK;
+}
+
+extern "C" nbvh_status nbvh_debug_train_capture(nbvh_ctx* c, int32_t enable) {
+    nbvh_status st = check_device(c);
+    if (st) return st;
+    st = ensure_train_state(c, 1);
+    if (st) return st;
+    c->train->capture = enable != 0;
+    if (!enable) dfree(c->train->Z);
+    return NBVH_OK;
+}
+
+extern "C" nbvh_status nbvh_debug_train_activations(nbvh_ctx* c, int32_t* d_sample_ray, uint16_t* d_x, float* d_z,
+                                                    float* d_dz, uint16_t* d_delta, int64_t* h_m, void* stream) {
+    nbvh_status st = check_device(c);
+    if (st) return st;
+    if (!h_m) return fail(c, NBVH_EINVAL, "debug_train_activations: null count pointer");
+    if (!c->train || !c->train->X) return fail(c, NBVH_ESTATE, "debug_train_activations: no training batch yet");
+    TrainWork* w = c->train;
+    if (d_z && !(w->capture && w->Z)) return fail(c, NBVH_ESTATE, "debug_train_activations: z needs capture on");
+    cudaStream_t s = (cudaStream_t)stream;
+    int32_t m32 = 0;
+    cudaError_t e = cudaMemcpyAsync(&m32, w->counters, 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(c, e, "debug_train_activations");
+    const size_t m = (size_t)m32, D = (size_t)c->d_in, H = (size_t)c->cfg.hidden_layers;
+    *h_m = (int64_t)m;
+    if (d_sample_ray) e = cudaMemcpyAsync(d_sample_ray, w->s_ray, m * 4, cudaMemcpyDeviceToDevice, s);
+    if (e == cudaSuccess && d_x) e = cudaMemcpyAsync(d_x, w->X, m * D * 2, cudaMemcpyDeviceToDevice, s);
+    if (e == cudaSuccess && d_z) e = cudaMemcpyAsync(d_z, w->Z, m * 8 * 4, cudaMemcpyDeviceToDevice, s);
+    if (e == cudaSuccess && d_dz) e = cudaMemcpyAsync(d_dz, w->dZ, m * 8 * 4, cudaMemcpyDeviceToDevice, s);
+    for (size_t k = 0; e == cudaSuccess && d_delta && k < H; ++k)     // [H][M][64] -> [H][m][64]
+        e = cudaMemcpyAsync(d_delta + k * m * 64, w->Dl + k * (size_t)w->cap * 64, m * 64 * 2,
+                            cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return cuda_fail(c, e, "debug_train_activations");
     return NBVH_OK;
 }

@@ -52,6 +52,7 @@ struct TrainArgs {
     __half* A;               // [hidden][M][64] post-ReLU activations
     __half* Dl;              // [hidden][M][64] deltas dL/d(pre-activation)
     float* dZ;               // [M][8]
+    float* Z;                // [M][8] raw MLP outputs (nullable: parity capture only)
     // outputs
     float* grad;             // flat fp32: tables, weights, biases, tail
     float* tail;             // [0] accepted count, [1 + 3*leaf + {0,1,2}] loss sum, samples, first hits
@@ -377,6 +378,12 @@ __global__ void __launch_bounds__(256, 2) k_train_fwd(TrainArgs a) {
                 float4* dst = reinterpret_cast<float4*>(a.dZ + i * 8);
                 dst[0] = make_float4(dz[0], dz[1], dz[2], dz[3]);
                 dst[1] = make_float4(dz[4], dz[5], dz[6], dz[7]);
+                if (a.Z) {
+                    float4* zd = reinterpret_cast<float4*>(a.Z + i * 8);
+                    const float* zz = zt + tid * 8;
+                    zd[0] = make_float4(zz[0], zz[1], zz[2], zz[3]);
+                    zd[1] = make_float4(zz[4], zz[5], zz[6], zz[7]);
+                }
                 a.r_loss[Q.ray] = Ls;
                 atomicAdd(a.tail + 1 + 3 * Q.leaf, Ls);
                 atomicAdd(a.tail + 1 + 3 * Q.leaf + 1, 1.0f);
@@ -966,7 +973,8 @@ struct AdamArgs {
     int64_t n;
     const float* count;   // accepted-sample count (after the all-reduce)
     const int32_t* bad;
-    float lr, beta1, beta2, eps, c1, c2, ic1, ic2;   // ic = 1/c (bias corrections)
+    int32_t* step;        // device Adam step count: advanced only by an applied update
+    float lr, beta1, beta2, eps;
     __half* table16;
     int64_t n_table;
     __half* W16;
@@ -976,11 +984,14 @@ struct AdamArgs {
 // P:275 Adam with default hyper-parameters (C20): dense, bias-corrected; the gradient is
 // the batch mean (sum / accepted count).  The fp16 MLP weights are refreshed in place; the
 // fp16 inference table is rebuilt afterwards by k_refresh_table (corner-packed layout).
-__device__ __forceinline__ float adam_one(const AdamArgs& a, float g, float& m, float& v, float p, float scale) {
+// ic1 / ic2 = 1 / (1 - beta^t): the bias corrections of step t = (device step count) + 1,
+// so an update skipped for a non-finite gradient does not advance t.
+__device__ __forceinline__ float adam_one(const AdamArgs& a, float g, float& m, float& v, float p, float scale,
+                                          float ic1, float ic2) {
     const float gr = g * scale;
     m = a.beta1 * m + (1.0f - a.beta1) * gr;
     v = a.beta2 * v + (1.0f - a.beta2) * gr * gr;
-    return p - a.lr * (m * a.ic1) / (sqrtf(v * a.ic2) + a.eps);
+    return p - a.lr * (m * ic1) / (sqrtf(v * ic2) + a.eps);
 }
 
 // Vectorised (float4) over the flat parameter buffer; the fp16 MLP-weight copy is written for
@@ -988,6 +999,9 @@ __device__ __forceinline__ float adam_one(const AdamArgs& a, float g, float& m, 
 __global__ void k_adam(AdamArgs a) {
     if (*a.bad) return;
     const float scale = 1.0f / fmaxf(1.0f, *a.count);
+    const double t = (double)(*a.step + 1);
+    const float ic1 = (float)(1.0 / (1.0 - pow((double)a.beta1, t)));
+    const float ic2 = (float)(1.0 / (1.0 - pow((double)a.beta2, t)));
     const int64_t n4 = a.n / 4;
     const int64_t w0 = a.n_table, w1 = a.n_table + a.n_W;
     float4* P = reinterpret_cast<float4*>(a.param);
@@ -998,10 +1012,10 @@ __global__ void k_adam(AdamArgs a) {
     for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n4; q += stride) {
         const float4 g = G[q];
         float4 m = Mv[q], v = Vv[q], p = P[q];
-        p.x = adam_one(a, g.x, m.x, v.x, p.x, scale);
-        p.y = adam_one(a, g.y, m.y, v.y, p.y, scale);
-        p.z = adam_one(a, g.z, m.z, v.z, p.z, scale);
-        p.w = adam_one(a, g.w, m.w, v.w, p.w, scale);
+        p.x = adam_one(a, g.x, m.x, v.x, p.x, scale, ic1, ic2);
+        p.y = adam_one(a, g.y, m.y, v.y, p.y, scale, ic1, ic2);
+        p.z = adam_one(a, g.z, m.z, v.z, p.z, scale, ic1, ic2);
+        p.w = adam_one(a, g.w, m.w, v.w, p.w, scale, ic1, ic2);
         Mv[q] = m;
         Vv[q] = v;
         P[q] = p;
@@ -1015,12 +1029,18 @@ __global__ void k_adam(AdamArgs a) {
     }
     for (int64_t i = 4 * n4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += stride) {
         float m = a.m[i], v = a.v[i];
-        const float p = adam_one(a, a.grad[i], m, v, a.param[i], scale);
+        const float p = adam_one(a, a.grad[i], m, v, a.param[i], scale, ic1, ic2);
         a.m[i] = m;
         a.v[i] = v;
         a.param[i] = p;
         if (i >= w0 && i < w1) a.W16[i - w0] = __float2half_rn(p);
     }
+}
+
+// Advances the device step count after an applied update (one thread; stream-ordered after
+// k_adam, which read it).
+__global__ void k_adam_commit(const int32_t* bad, int32_t* step) {
+    if (!*bad) *step += 1;
 }
 
 }  // namespace nbvh

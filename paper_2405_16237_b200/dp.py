@@ -1,13 +1,23 @@
-"""Data-parallel training step (BASELINE cfg 5): one process per GPU, the global batch
-split over ranks, one all-reduce (sum) of the flat fp32 gradient buffer per step.
+"""Multi-GPU plumbing: one process per GPU, torch.distributed for the process
+group, NCCL on the GPU box (gloo in the CPU tests).
 
-The buffer (nbvh_grad_buffer) holds the parameter gradients of the SUM of per-sample
-losses, then the accepted-sample count, then per-leaf (loss sum, samples, first hits);
-summing it over ranks gives exactly the single-process buffer of the whole batch, and
-nbvh_apply_update divides by the summed count, so every rank applies the same Adam
-step to identical parameters.
+Training (BASELINE cfg 5): the global batch is split over ranks; each rank runs
+nbvh_train_backward on its shard, the flat fp32 gradient buffer (nbvh_grad_buffer) is
+all-reduced (sum) once per step and every rank applies the same Adam step.  The buffer holds
+the parameter gradients of the SUM of per-sample losses, then the accepted-sample count, then
+per-leaf (loss sum, samples, first hits); summed over ranks it is exactly the single-process
+buffer of the whole batch, and nbvh_apply_update divides by the summed count (C29).
+
+Query (BASELINE cfgs 2/3): the model is replicated -- built once on rank 0 and broadcast at
+init (`broadcast_model`) -- and one frame's rays are partitioned over ranks by interleaved
+16x16 pixel tiles (`tile_partition`) for load balance (depth complexity varies across the
+screen).  There is no collective on the query's data path.
 """
 from __future__ import annotations
+
+import hashlib
+
+import numpy as np
 
 
 class _CudaArray:
@@ -25,6 +35,21 @@ def grad_tensor(ctx):
     return torch.as_tensor(_CudaArray(ptr, n), device=f"cuda:{ctx.device}")
 
 
+def _dist():
+    import torch.distributed as dist
+    return dist if dist.is_available() and dist.is_initialized() else None
+
+
+def world_size(group=None) -> int:
+    d = _dist()
+    return d.get_world_size(group) if d else 1
+
+
+def rank_of(group=None) -> int:
+    d = _dist()
+    return d.get_rank(group) if d else 0
+
+
 def shard(n_global: int, rank: int, world: int) -> slice:
     """Contiguous, balanced split of a global batch of n_global rays."""
     base, rem = divmod(n_global, world)
@@ -32,11 +57,71 @@ def shard(n_global: int, rank: int, world: int) -> slice:
     return slice(start, start + base + (1 if rank < rem else 0))
 
 
+def tile_partition(width: int, height: int, rank: int, world: int, tile: int = 16) -> np.ndarray:
+    """Row-major pixel indices owned by `rank` when a width x height frame is cut into
+    tile x tile tiles dealt round-robin along diagonals ((tx + ty) mod world), so every rank
+    gets tiles from every part of the screen.  Pixels are listed tile by tile (row-major
+    inside a tile), which keeps neighbouring rays together for the query kernel's warps.
+    Ragged edge tiles are clipped to the frame."""
+    ntx, nty = (width + tile - 1) // tile, (height + tile - 1) // tile
+    out = []
+    for ty in range(nty):
+        y0, y1 = ty * tile, min(height, (ty + 1) * tile)
+        for tx in range(ntx):
+            if (tx + ty) % world != rank:
+                continue
+            x0, x1 = tx * tile, min(width, (tx + 1) * tile)
+            ys, xs = np.meshgrid(np.arange(y0, y1), np.arange(x0, x1), indexing="ij")
+            out.append((ys * width + xs).reshape(-1))
+    return np.concatenate(out).astype(np.int64) if out else np.zeros(0, np.int64)
+
+
 def allreduce_grads(buf, group=None):
-    import torch.distributed as dist
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
-        dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+    d = _dist()
+    if d and d.get_world_size(group) > 1:
+        d.all_reduce(buf, op=d.ReduceOp.SUM, group=group)
     return buf
+
+
+def broadcast_model(ctx, src: int = 0, group=None, device=None):
+    """Replicate the model (every parameter block: tables, weights, biases) from rank `src`
+    to all ranks -- the query path's one collective, at init."""
+    import torch
+    from .nbvh import PARAM_ALL
+    d = _dist()
+    if not d or d.get_world_size(group) == 1:
+        return
+    p = ctx.get_params(PARAM_ALL)
+    t = torch.from_numpy(p)
+    if device is not None:
+        t = t.to(device)
+    d.broadcast(t, src=src, group=group)
+    ctx.set_params(PARAM_ALL, t.cpu().numpy())
+
+
+def param_checksum(ctx) -> str:
+    """SHA-256 of the fp32 master parameters (host copy)."""
+    from .nbvh import PARAM_ALL
+    return hashlib.sha256(ctx.get_params(PARAM_ALL).tobytes()).hexdigest()
+
+
+def params_identical_across_ranks(ctx, group=None) -> bool:
+    """True iff every rank holds byte-identical parameters (gathered checksums)."""
+    d = _dist()
+    mine = param_checksum(ctx)
+    if not d or d.get_world_size(group) == 1:
+        return True
+    allsums = [None] * d.get_world_size(group)
+    d.all_gather_object(allsums, mine, group=group)
+    return all(s == mine for s in allsums)
+
+
+def leaf_stats(buf, n_params: int, n_leaves: int):
+    """(accepted count, per-leaf [n_leaves, 3] (loss sum, samples, first hits)) from a gradient
+    buffer -- read it AFTER allreduce_grads so every rank sees the global statistics and
+    builds the same cut."""
+    tail = buf[n_params:n_params + 1 + 3 * n_leaves]
+    return tail[0], tail[1:].reshape(n_leaves, 3)
 
 
 def train_step_dp(ctx, rays, u, xi, lod: int = 0, lr: float = 0.01, group=None):

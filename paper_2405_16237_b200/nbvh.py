@@ -86,10 +86,13 @@ SIGNATURES = {
     "nbvh_atomic_probe": (C.c_int, [_P, _I64, _I32, _I64, C.c_uint32, _P, _P]),
     "nbvh_pt_shade": (C.c_int, [_P, _P, _I64, Hits, Hits, _P, _P, _P, C.c_uint64, _I32, _P, _F, _P, _P]),
     "nbvh_debug_traverse": (C.c_int, [_P, _P, _I64, _I32, _I32, _P, _P, _P, _P, _P]),
+    "nbvh_debug_traverse_product": (C.c_int, [_P, _P, _I64, _I32, _P, _P, _P, _P, _P, _P]),
     "nbvh_debug_encode": (C.c_int, [_P, _P, _I64, _P, _P, _P]),
     "nbvh_debug_mlp": (C.c_int, [_P, _P, _I64, _P, _P]),
     "nbvh_debug_query_trace": (C.c_int, [_P, _P, _I64, _I32, Hits, _P, _I32, _P]),
     "nbvh_debug_train_samples": (C.c_int, [_P, _P, _P, _P, _P, _P]),
+    "nbvh_debug_train_capture": (C.c_int, [_P, _I32]),
+    "nbvh_debug_train_activations": (C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P]),
 }
 
 
@@ -416,3 +419,49 @@ class Context:
         self._ck(self.lib.nbvh_debug_train_samples(self.h, _ptr(gt), _ptr(acc), _ptr(leaf), _ptr(loss),
                                                    _stream_ptr(stream)), "debug_train_samples")
         return gt, acc, leaf, loss
+
+    def debug_train_capture(self, enable: bool):
+        self._ck(self.lib.nbvh_debug_train_capture(self.h, 1 if enable else 0), "debug_train_capture")
+
+    def debug_train_activations(self, n_rays, stream=None):
+        """Per-sample intermediates of the last training batch (compacted sample order):
+        dict(ray [m] int32, x [m, D_in] fp16, z [m, 8] (capture on, else None), dz [m, 8],
+        delta [hidden, m, 64] fp16)."""
+        import torch
+        dev = f"cuda:{self.device}"
+        H = self.cfg.hidden_layers
+        ray = torch.empty(n_rays, dtype=torch.int32, device=dev)
+        x = torch.empty(n_rays * self.d_in, dtype=torch.float16, device=dev)
+        z = torch.empty(n_rays * 8, dtype=torch.float32, device=dev)
+        dz = torch.empty(n_rays * 8, dtype=torch.float32, device=dev)
+        dl = torch.empty(H * n_rays * 64, dtype=torch.float16, device=dev)
+        m = np.zeros(1, np.int64)
+        st = self.lib.nbvh_debug_train_activations(self.h, _ptr(ray), _ptr(x), _ptr(z), _ptr(dz), _ptr(dl),
+                                                   _ptr(m), _stream_ptr(stream))
+        zt = z
+        if st == -3:                                  # NBVH_ESTATE: capture off -> no z
+            self._ck(self.lib.nbvh_debug_train_activations(self.h, _ptr(ray), _ptr(x), None, _ptr(dz), _ptr(dl),
+                                                           _ptr(m), _stream_ptr(stream)), "debug_train_activations")
+            zt = None
+        else:
+            self._ck(st, "debug_train_activations")
+        mm = int(m[0])
+        return dict(ray=ray[:mm], x=x[:mm * self.d_in].view(mm, self.d_in),
+                    z=None if zt is None else zt[:mm * 8].view(mm, 8), dz=dz[:mm * 8].view(mm, 8),
+                    delta=dl[:H * mm * 64].view(H, mm, 64))
+
+    def debug_traverse_product(self, rays, lod=0, stream=None):
+        """The product k_traverse's lists: (leaf [n, K], te, tx, fill [n], more [n])."""
+        import torch
+        n, K = rays.shape[0], self.cfg.list_cap
+        dev = rays.device
+        leaf = torch.empty(n, K, dtype=torch.int32, device=dev)
+        te = torch.empty(n, K, dtype=torch.float32, device=dev)
+        tx = torch.empty(n, K, dtype=torch.float32, device=dev)
+        fill = torch.empty(n, dtype=torch.int32, device=dev)
+        more = torch.empty(n, dtype=torch.int32, device=dev)
+        self._ck(self.lib.nbvh_debug_traverse_product(self.h, _ptr(rays), n, lod, _ptr(leaf), _ptr(te), _ptr(tx),
+                                                      _ptr(fill), _ptr(more), _stream_ptr(stream)),
+                 "debug_traverse_product")
+        return leaf, te, tx, fill, more
+

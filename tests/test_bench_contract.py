@@ -21,4 +21,5 @@ def test_reference_arm_json_line():
     assert d["impl"] == "reference" and d["value"] > 0 and d["steps"] == 2 and d["warmup"] == 1
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
-    assert d["config"]["workload"] == "tiny"
+    assert d["config"]["workload"].startswith("tiny")
+    assert d["scaling"] == "strong" and d["cpu_baseline"]["cpu_model"]

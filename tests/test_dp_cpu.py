@@ -66,3 +66,72 @@ def test_shard_is_a_partition():
         for world in (1, 2, 3, 8):
             idx = np.concatenate([np.arange(n)[dp.shard(n, r, world)] for r in range(world)])
             assert np.array_equal(idx, np.arange(n))
+
+
+# ------------------------------------------------------------------ query partition
+@pytest.mark.parametrize("w,h,world", [(1920, 1080, 1), (1920, 1080, 2), (1920, 1080, 8), (64, 64, 3), (37, 21, 4)])
+def test_tile_partition_covers_frame_once_and_balances(w, h, world):
+    from paper_2405_16237_b200 import dp
+    parts = [dp.tile_partition(w, h, r, world) for r in range(world)]
+    allidx = np.concatenate(parts)
+    assert allidx.size == w * h and np.array_equal(np.sort(allidx), np.arange(w * h))
+    sizes = np.array([p.size for p in parts])
+    assert sizes.max() - sizes.min() <= 2 * 16 * 16 * max(1, (h + 15) // 16 // 8)   # within a few tiles
+    if w * h >= 1920 * 1080 and world > 1:
+        # every rank owns tiles in every 1/8th band of rows (interleaved, not contiguous)
+        for p in parts:
+            bands = np.unique((p // w) * 8 // h)
+            assert bands.size == 8
+    # tile-major order: the first 16 pixels of a rank are one tile row (consecutive x)
+    p0 = parts[0]
+    if w >= 16:
+        assert np.all(np.diff(p0[:16]) == 1)
+
+
+def _bcast_worker(rank, world, port, out_q):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import synth
+    from paper_2405_16237_b200 import Context, dp, PARAM_ALL
+    ctx = Context(device=-1, L=8, F=2, log2_T=14, n_points=4, hidden_layers=2)
+    n = ctx.param_count(PARAM_ALL)
+    ctx.set_params(PARAM_ALL, np.random.default_rng(100 + rank).standard_normal(n).astype(np.float32))
+    before = dp.params_identical_across_ranks(ctx)
+    dp.broadcast_model(ctx, src=0)
+    after = dp.params_identical_across_ranks(ctx)
+    want = np.random.default_rng(100).standard_normal(n).astype(np.float32)
+    same_as_rank0 = bool(np.array_equal(ctx.get_params(PARAM_ALL), want))
+    # per-leaf statistics read after the reduce (construct()): every rank sees the
+    # same global tail of a product-shaped buffer (params | count | n_leaves x 3)
+    import torch
+    n_leaves = 64
+    rng = np.random.default_rng(7 + rank)
+    buf = torch.from_numpy(np.concatenate([rng.standard_normal(n), [rng.integers(10, 50)],
+                                           rng.integers(0, 9, 3 * n_leaves)]).astype(np.float32))
+    local_count = float(buf[n])
+    dp.allreduce_grads(buf)
+    count, per_leaf = dp.leaf_stats(buf, n, n_leaves)
+    digest = __import__("hashlib").sha256(buf.numpy().tobytes()).hexdigest()
+    out_q.put((rank, before, after, same_as_rank0, float(count), local_count, per_leaf.shape, digest))
+    dist.destroy_process_group()
+
+
+def test_model_broadcast_and_reduced_stats_identical_across_ranks():
+    world = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_bcast_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, before, after, same0, count, local, shape, digest in res:
+        assert not before and after and same0
+        assert shape == (64, 3)
+    assert res[0][4] == res[0][5] + res[1][5] == res[1][4]          # global accepted count on both
+    assert res[0][7] == res[1][7]                                    # byte-identical reduced buffers

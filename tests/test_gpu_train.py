@@ -247,7 +247,7 @@ def test_t0_generated_rays_match_oracle():
     """nbvh_gen_train_rays (T0, Philox-4x32-10 on the device) against the oracle's own Philox
     and recipe (C28'): origins, z, u, xi, tmin, tmax bit-exact; the direction's x, y within a
     few ulp (cos / sin); a data-parallel shard equals the slice of the whole batch; the
-    default box is the domain cube inflated by 50%."""
+    default box is the scene box with every axis extent x1.5 (C16)."""
     import oracle as orc
     from paper_2405_16237_b200 import Context
     sc = synth.scene_tiny()
@@ -263,13 +263,14 @@ def test_t0_generated_rays_match_oracle():
     assert np.abs(rays[:, 4:6] - wr[:, 4:6]).max() <= 4e-7
     r2, u2, x2 = (t.cpu().numpy() for t in ctx.gen_train_rays(seed=7, step=5, n=777, i0=4321, box=box))
     assert np.array_equal(r2, rays[4321:4321 + 777]) and np.array_equal(u2, u[4321:4321 + 777])
+    # default box (C16): the scene's bounding box (no C15 padding), each axis extent x1.5
     rd, _, _ = (t.cpu().numpy() for t in ctx.gen_train_rays(seed=7, step=5, n=20000))
-    b = orc.scene_box(sc).astype(np.float64)
-    side = (b[3:] - b[:3]).max()
+    b = orc.scene_box(sc, rel=0.0, abs_=0.0).astype(np.float64)
+    ext = b[3:] - b[:3]
     mid = (b[:3] + b[3:]) / 2
-    lo, hi = mid - 0.75 * side, mid + 0.75 * side
+    lo, hi = mid - 0.75 * ext, mid + 0.75 * ext
     assert np.all(rd[:, :3] >= lo - 1e-5) and np.all(rd[:, :3] <= hi + 1e-5)
-    assert np.all(rd[:, :3].min(0) < lo + 0.05 * side) and np.all(rd[:, :3].max(0) > hi - 0.05 * side)
+    assert np.all(rd[:, :3].min(0) < lo + 0.05 * ext) and np.all(rd[:, :3].max(0) > hi - 0.05 * ext)
 
 
 def test_tcgen05_weight_gradients_at_bench_size(monkeypatch):
@@ -287,7 +288,7 @@ def test_tcgen05_weight_gradients_at_bench_size(monkeypatch):
     ctx.set_params(PARAM_TABLES, synth.random_params_fp16(ctx.param_count(PARAM_TABLES), seed=5).astype(np.float32))
     ctx.set_mlp(synth.random_mlp(ctx.d_in, h.hidden_layers, 64, seed=6, out_scale=1.0))
     ctx.set_leaf_rank(np.zeros(ctx.cut(0)["n_leaves"], np.float32))
-    rays, u, xi = ctx.gen_train_rays(seed=7, step=1, n=n, box=(-1.5, -1.5, -1.5, 1.5, 1.5, 1.5))
+    rays, u, xi = ctx.gen_train_rays(seed=7, step=1, n=n, box=None)      # C16 box, as bench.py
     n_t = ctx.param_count(PARAM_TABLES)
     n_w = ctx.param_count(1)                                        # PARAM_WEIGHTS
     grads = {}
@@ -318,7 +319,7 @@ def test_privatised_scatter_at_bench_size(monkeypatch):
     ctx.set_params(PARAM_TABLES, synth.random_params_fp16(ctx.param_count(PARAM_TABLES), seed=5).astype(np.float32))
     ctx.set_mlp(synth.random_mlp(ctx.d_in, h.hidden_layers, 64, seed=6, out_scale=1.0))
     ctx.set_leaf_rank(np.zeros(ctx.cut(0)["n_leaves"], np.float32))
-    rays, u, xi = ctx.gen_train_rays(seed=9, step=2, n=n, box=(-1.5, -1.5, -1.5, 1.5, 1.5, 1.5))
+    rays, u, xi = ctx.gen_train_rays(seed=9, step=2, n=n, box=None)      # C16 box, as bench.py
     n_t = ctx.param_count(PARAM_TABLES)
     g = {}
     for budget in ("default", "0"):
@@ -354,7 +355,7 @@ def test_training_step_at_bench_size_sampled_vs_oracle():
     cut = ctx.cut(0)
     rank = np.random.default_rng(3).normal(size=cut["n_leaves"]).astype(np.float32)
     ctx.set_leaf_rank(rank)
-    rays, u, xi = ctx.gen_train_rays(seed=11, step=4, n=n, box=(-1.5, -1.5, -1.5, 1.5, 1.5, 1.5))
+    rays, u, xi = ctx.gen_train_rays(seed=11, step=4, n=n, box=None)      # C16 box, as bench.py
     ctx.train_backward(rays, u, xi)
     gt, acc, leaf, loss = (t.cpu().numpy() for t in ctx.debug_train_samples(n))
     sub = np.arange(0, n, 257)
@@ -369,3 +370,74 @@ def test_training_step_at_bench_size_sampled_vs_oracle():
     lg, lo_ = loss[sub][a].astype(np.float64), o["loss"][a]
     close = np.abs(lg - lo_) <= 5e-2 * np.abs(lo_) + 1e-3
     assert close.mean() >= 0.99, close.mean()
+
+
+def test_nonfinite_gradient_skips_the_update():
+    """S:254 / S:480 (SURVEY §5 failure detection): a non-finite value anywhere in the
+    gradient buffer makes nbvh_apply_update skip the step -- parameters (and so the fp16
+    inference copy) unchanged and NBVH_ENONFINITE reported by the stats call -- and the
+    skipped steps do not advance Adam's step count: the next finite update is Adam step 1,
+    equal to a fresh context's first update on the same batch."""
+    from paper_2405_16237_b200 import Context, PARAM_ALL, dp
+    from paper_2405_16237_b200.nbvh import NbvhError
+    ctx, sc, cut, tab, layers, rays, u, xi, o = _setup(n_rays=3000, seed=80)
+    p0 = ctx.get_params(PARAM_ALL)
+    ctx.set_params(PARAM_ALL, p0)                                   # restarts Adam
+    q0 = ctx.query(_to(rays[:500]))
+    q0 = {k: v.clone() for k, v in q0.items()}
+    for bad in (float("nan"), float("inf"), float("-inf")):
+        ctx.train_backward(_to(rays), _to(u), _to(xi))
+        g = dp.grad_tensor(ctx)
+        g[len(p0) // 3] = bad
+        ctx.apply_update(0.01)
+        with pytest.raises(NbvhError) as ei:
+            ctx.train_stats()
+        assert ei.value.status == -4                                # NBVH_ENONFINITE
+        assert np.array_equal(ctx.get_params(PARAM_ALL), p0)
+    q1 = ctx.query(_to(rays[:500]))
+    for k in q0:
+        assert torch.equal(q0[k], q1[k]), k                         # inference copy untouched
+    ctx.train_backward(_to(rays), _to(u), _to(xi))
+    ctx.apply_update(0.01)
+    assert ctx.train_stats()["skipped"] == 0
+    p1 = ctx.get_params(PARAM_ALL)
+    fresh = _setup(n_rays=3000, seed=80)[0]
+    fresh.set_params(PARAM_ALL, p0)
+    fresh.train_backward(_to(rays), _to(u), _to(xi))
+    fresh.apply_update(0.01)
+    p2 = fresh.get_params(PARAM_ALL)
+    assert np.abs(p1 - p2).max() <= 1e-4                           # step 1, not step 4 (|diff| ~ 4e-3)
+    assert np.abs(p1 - p0).max() > 5e-3
+
+
+def test_dp_two_contexts_stay_byte_identical():
+    """SURVEY §8(e) data parallelism on one GPU without cross-waiting kernels: two contexts,
+    each holding half of every batch, sum their gradient buffers (the all-reduce), and both
+    apply the update.  After several steps their parameters are byte-identical, and equal
+    (to fp32 summation order) to one context trained on the whole batches."""
+    from paper_2405_16237_b200 import PARAM_ALL, dp
+    ranks = [_setup(n_rays=4000, seed=90)[0] for _ in range(2)]
+    single = _setup(n_rays=4000, seed=90)[0]
+    assert dp.param_checksum(ranks[0]) == dp.param_checksum(ranks[1]) == dp.param_checksum(single)
+    for step in range(6):
+        rays = synth.random_rays(4000, seed=500 + step)
+        u = synth.random_uniform(4000, seed=600 + step)
+        xi = synth.random_uniform(4000 * 4, seed=700 + step).reshape(4000, 4)
+        bufs = []
+        for r, ctx in enumerate(ranks):
+            sl = dp.shard(4000, r, 2)
+            ctx.train_backward(_to(rays[sl]), _to(u[sl]), _to(xi[sl]))
+            bufs.append(dp.grad_tensor(ctx))
+        total = bufs[0] + bufs[1]                                    # the all-reduce (sum)
+        for b in bufs:
+            b.copy_(total)
+        for ctx in ranks:
+            ctx.apply_update(0.01)
+        single.train_backward(_to(rays), _to(u), _to(xi))
+        single.apply_update(0.01)
+        assert dp.param_checksum(ranks[0]) == dp.param_checksum(ranks[1]), step
+    pa, ps = ranks[0].get_params(PARAM_ALL), single.get_params(PARAM_ALL)
+    # summation order only: Adam's normalised steps move a parameter by ~lr, so an fp32-order
+    # difference can flip a step only where the gradient is ~0 (a handful of entries)
+    d = np.abs(pa - ps)
+    assert np.quantile(d, 0.999) <= 1e-5 and d.max() <= 6 * 2 * 0.01

@@ -593,3 +593,51 @@ def test_t0_training_rays_distribution(orc):
     assert np.array_equal(r2, rays[1000:1500]) and np.array_equal(u2, u[1000:1500]) and np.array_equal(x2, xi[1000:1500])
     r3, u3, _ = orc.gen_train_rays(7, 4, 0, 1000, box, 4)
     assert np.mean(u3 == u[:1000]) < 0.01
+
+
+def test_p13_backward_given_equals_train_grad_and_bounds(orc):
+    """orc_train_backward_given (T6/T7 from given features and dL/dz, used to compare the
+    GPU's chain stage by stage) fed the oracle's OWN per-sample features and dL/dz (from the
+    pinned encode, MLP and loss) reproduces orc_train_grad's gradients (pinned by central
+    differences above) times the accepted count; its magnitude sums bound |g|; its hidden
+    deltas give dW by an independent numpy contraction; z equals the numpy float64 MLP."""
+    sc, off, lt, llo, lhi, g, tab, layers, rays, u, xi = _small_train_setup(orc, n_rays=400, seed=23)
+    rank = np.zeros(2, np.float32)
+    full = orc.train_grad(g, 3, tab, layers, llo, lhi, rank, off, lt, sc, rays, u, xi)
+    acc = np.nonzero(full["accepted"])[0]
+    assert acc.size > 60
+    leaf, te, tx, cnt = orc.leaf_lists(rays, llo, lhi, 1)
+    box = np.concatenate([llo.min(0), lhi.max(0)]).astype(np.float32)      # = the union-of-leaves domain
+    dmin, dinv = orc.domain(llo, lhi)
+    x = np.stack([orc.encode_points(g, tab, orc.segment_points(rays[r], te[r, 0], tx[r, 0], 3, dmin, dinv,
+                                                              xi[r]))[0].reshape(-1) for r in acc])
+    z = orc.mlp_forward(layers, x)
+    dz = np.stack([orc.sample_loss(z[i], full["gt"][r])[2] for i, r in enumerate(acc)])
+    o = orc.train_backward_given(g, 3, tab, layers, box, rays[acc], te[acc, 0], tx[acc, 0], xi[acc], x, dz,
+                                 want_deltas=True)
+    m = acc.size
+    for k in ("g_table", "g_W", "g_b"):
+        np.testing.assert_allclose(o[k], full[k] * m, rtol=1e-12, atol=1e-14)
+        assert np.all(o[k + "_abs"] >= np.abs(o[k]) - 1e-15)
+    np.testing.assert_allclose(o["z"], z, rtol=1e-13, atol=1e-14)
+    assert np.all(o["z_abs"] >= np.abs(o["z"]) - 1e-15)
+    # dW of the output layer = sum dz (x) h_1 and of layer 0 = sum delta_0 (x) x (numpy einsum
+    # over the hidden deltas / activations)
+    W0, b0 = layers[0]
+    h1 = np.maximum(x @ W0.astype(np.float64).T + b0, 0.0)
+    d0 = o["hidden_delta"][:, 0, :8]
+    np.testing.assert_allclose(o["g_W"][:8 * 12], np.einsum("so,si->oi", d0, x).ravel(), rtol=1e-11, atol=1e-13)
+    np.testing.assert_allclose(o["g_W"][8 * 12:], np.einsum("so,si->oi", dz, h1).ravel(), rtol=1e-11, atol=1e-13)
+    # ReLU margin: 0 for a unit whose pre-activation is exactly 0 with non-zero operands
+    # (w = +1 on feature 0, -1 on feature 1, and the given x has x_0 == x_1)
+    assert np.all(o["relu_margin"] > 0)
+    lay = [(W.copy(), b.copy()) for W, b in layers]
+    lay[0][0][:] = 0
+    lay[0][1][:] = 0.0
+    lay[0][0][0, 0], lay[0][0][0, 1] = 1.0, -1.0
+    x2 = x[:3].copy()
+    x2[:, 1] = x2[:, 0]
+    assert np.all(x2[:, 0] != 0)
+    o2 = orc.train_backward_given(g, 3, tab, lay, box, rays[acc[:3]], te[acc[:3], 0], tx[acc[:3], 0], xi[acc[:3]],
+                                  x2, dz[:3])
+    assert np.all(o2["relu_margin"] == 0.0)

@@ -316,11 +316,13 @@ nbvh_status nbvh_debug_train_capture(nbvh_ctx* ctx, int32_t enable);
  * synchronises `stream` to read it).  Device outputs, each nullable: d_sample_ray [m] ray
  * index of each sample; d_x [m][D_in] fp16 features (T3, bits as uint16); d_z [m][8] raw
  * MLP outputs (T4; needs nbvh_debug_train_capture on, else NBVH_ESTATE); d_dz [m][8] dL/dz
- * (T5); d_delta [hidden][m][64] fp16 deltas dL/d(pre-activation) of each hidden layer
- * (T6).  Buffers must hold the capacity implied by m (callers size them from the ray
- * count, an upper bound). */
+ * (T5); d_act [hidden][m][64] fp16 post-ReLU hidden activations (T4: the kernel's ReLU
+ * decisions are act > 0); d_delta [hidden][m][64] fp16 deltas dL/d(pre-activation) of each
+ * hidden layer (T6).  Buffers must hold the capacity implied by m (callers size them from
+ * the ray count, an upper bound). */
 nbvh_status nbvh_debug_train_activations(nbvh_ctx* ctx, int32_t* d_sample_ray, uint16_t* d_x, float* d_z,
-                                         float* d_dz, uint16_t* d_delta, int64_t* h_m, void* stream);
+                                         float* d_dz, uint16_t* d_act, uint16_t* d_delta, int64_t* h_m,
+                                         void* stream);
 
 #ifdef __cplusplus
 }

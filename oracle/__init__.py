@@ -303,11 +303,14 @@ def train_grad(grid: Grid, n_points, table_fp16, layers, leaf_lo, leaf_hi, leaf_
 
 
 def train_backward_given(grid: Grid, n_points, table_fp16, layers, dom_box, rays, t0, t1, xi, x, dz,
-                         want_deltas=False):
+                         masks=None, want_deltas=False):
     """T6/T7 in double from GIVEN per-sample features x [m, D] and dL/dz [m, 8] (e.g. the
-    GPU's own); samples are segments [t0, t1] of rays with jitter xi.  Returns sums (not
-    means) g_table/g_W/g_b, their magnitude sums *_abs, z / z_abs of the MLP on x, the ReLU
-    margin per sample and optionally hidden deltas [m, H, 64] (+ magnitudes)."""
+    GPU's own); samples are segments [t0, t1] of rays with jitter xi.  masks (optional uint8
+    [m, H, 64]): ReLU decisions taken by the caller (the GPU's own, C36) instead of
+    the double pre-activation's sign.  Returns sums (not means) g_table/g_W/g_b, their
+    magnitude sums *_abs, z / z_abs of the MLP on x, the ReLU margin per sample (min over
+    hidden units of |pre| / magnitude), per sample the number of given masks that disagree
+    with the double sign and the largest margin among them, optionally hidden deltas."""
     dims, W_all, b_all = _mlp_arrays(layers)
     tab = _c(table_fp16, np.float16).view(np.uint16)
     rays = _c(rays, np.float32)
@@ -318,16 +321,17 @@ def train_backward_given(grid: Grid, n_points, table_fp16, layers, dom_box, rays
     ne = grid.n_entries * grid.F
     out = dict(g_table=np.zeros(ne), g_W=np.zeros(nW), g_b=np.zeros(nb), g_table_abs=np.zeros(ne),
                g_W_abs=np.zeros(nW), g_b_abs=np.zeros(nb), z=np.zeros((m, 8)), z_abs=np.zeros((m, 8)),
-               relu_margin=np.zeros(m))
+               relu_margin=np.zeros(m), mask_flips=np.zeros(m, np.int32), flip_margin=np.zeros(m))
     hd = np.zeros((m, H, 64)) if want_deltas else None
     hda = np.zeros((m, H, 64)) if want_deltas else None
+    mk = None if masks is None else _c(masks, np.uint8).reshape(m, H, 64)
     lib().orc_train_backward_given(
         grid.L, grid.F, grid.log2_T, n_points, len(layers), _p(grid.res), _p(grid.dense), _p(grid.offset), _p(tab),
         C.c_int64(grid.n_entries), _p(dims), _p(W_all), _p(b_all), _p(_c(dom_box, np.float32)), C.c_int64(m),
         _p(rays), _p(_c(t0, np.float32)), _p(_c(t1, np.float32)), _p(_c(xi, np.float32)), _p(_c(x, np.float64)),
-        _p(_c(dz, np.float64)), _p(out["g_table"]), _p(out["g_W"]), _p(out["g_b"]), _p(out["g_table_abs"]),
-        _p(out["g_W_abs"]), _p(out["g_b_abs"]), _p(out["z"]), _p(out["z_abs"]), _p(out["relu_margin"]), _p(hd),
-        _p(hda))
+        _p(_c(dz, np.float64)), _p(mk), _p(out["g_table"]), _p(out["g_W"]), _p(out["g_b"]), _p(out["g_table_abs"]),
+        _p(out["g_W_abs"]), _p(out["g_b_abs"]), _p(out["z"]), _p(out["z_abs"]), _p(out["relu_margin"]),
+        _p(out["mask_flips"]), _p(out["flip_margin"]), _p(hd), _p(hda))
     if want_deltas:
         out["hidden_delta"], out["hidden_delta_abs"] = hd, hda
     return out

@@ -661,10 +661,15 @@ static double sample_loss_impl(const double* z, const double* gt, double* terms,
 // absolute = true runs the same recursion on |delta|, |W|, |acts| with the same masks:
 // the magnitude sums that bound floating-point error (tests only; no step of the method).
 // hidden_delta (nullable, [n_layers-1][64]): the masked delta of each hidden layer.
+// mask (nullable, [n_layers-1][64]): ReLU decisions taken by someone else (the GPU kernel's
+// own, C36) instead of acts > 0.  acts_abs (nullable): in absolute mode, the magnitudes of
+// the layer inputs (|W| |h| + |b| of the forward) used instead of |acts|, so the sums also
+// bound the error of inputs that were themselves rounded.
 static void backward_sample(const OrcModel& M, const std::vector<const uint16_t*>& W,
                             const std::vector<double>* acts, std::vector<double> delta, const float* pts,
                             const uint32_t* idx, int64_t nW, int64_t nb, double* g_table, double* g_W, double* g_b,
-                            bool absolute, double* hidden_delta) {
+                            bool absolute, double* hidden_delta, const uint8_t* mask = nullptr,
+                            const std::vector<double>* acts_abs = nullptr) {
     const int n_layers = M.n_layers, L = M.L, F = M.F, LF = L * F;
     const int32_t* dims = M.dims;
     if (absolute)
@@ -674,17 +679,21 @@ static void backward_sample(const OrcModel& M, const std::vector<const uint16_t*
         wo -= (int64_t)dims[k] * dims[k + 1];
         bo -= dims[k + 1];
         const std::vector<double>& hin = acts[k];
+        const std::vector<double>& hmag = (absolute && acts_abs) ? acts_abs[k] : acts[k];
         std::vector<double> dprev(dims[k], 0.0);
         for (int o = 0; o < dims[k + 1]; ++o) {
             g_b[bo + o] += delta[o];
             for (int i = 0; i < dims[k]; ++i) {
                 const double w = orc_half_to_double(W[k][(int64_t)o * dims[k] + i]);
-                g_W[wo + (int64_t)o * dims[k] + i] += delta[o] * (absolute ? std::fabs(hin[i]) : hin[i]);
+                g_W[wo + (int64_t)o * dims[k] + i] += delta[o] * (absolute ? std::fabs(hmag[i]) : hin[i]);
                 dprev[i] += delta[o] * (absolute ? std::fabs(w) : w);
             }
         }
         if (k > 0) {
-            for (int i = 0; i < dims[k]; ++i) dprev[i] = hin[i] > 0.0 ? dprev[i] : 0.0;  // ReLU'
+            for (int i = 0; i < dims[k]; ++i) {                                          // ReLU'
+                const bool on = mask ? mask[(k - 1) * 64 + i] != 0 : hin[i] > 0.0;
+                dprev[i] = on ? dprev[i] : 0.0;
+            }
             if (hidden_delta)
                 for (int i = 0; i < dims[k]; ++i) hidden_delta[(k - 1) * 64 + i] = dprev[i];
         }
@@ -877,10 +886,11 @@ void orc_train_backward_given(int32_t L, int32_t F, int32_t log2_T, int32_t n_po
                               const uint16_t* table, int64_t n_entries, const int32_t* dims,
                               const uint16_t* W_all, const float* b_all, const float* dom_box, int64_t m,
                               const float* rays, const float* t0, const float* t1, const float* xi,
-                              const double* x_in, const double* dz_in,
+                              const double* x_in, const double* dz_in, const uint8_t* masks /*nullable*/,
                               double* g_table, double* g_W, double* g_b,
                               double* g_table_abs, double* g_W_abs, double* g_b_abs,
                               double* z_out, double* z_abs, double* relu_margin,
+                              int32_t* mask_flips /*nullable [m]*/, double* flip_margin /*nullable [m]*/,
                               double* hidden_delta /*nullable*/, double* hidden_delta_abs /*nullable*/) {
     float dom_min[3], dom_inv;
     orc_domain(dom_box, dom_box + 3, 1, dom_min, &dom_inv);
@@ -900,44 +910,67 @@ void orc_train_backward_given(int32_t L, int32_t F, int32_t log2_T, int32_t n_po
     std::vector<float> pts(3 * n_points);
     std::vector<uint32_t> idx(n_points * L * 8);
     std::vector<double> feat(L * F);
-    std::vector<std::vector<double>> acts(n_layers + 1);
-    std::vector<double> z(n_out), habs, nabs;
+    std::vector<std::vector<double>> acts(n_layers + 1), mags(n_layers + 1);
+    std::vector<double> habs, nabs;
     for (int64_t s = 0; s < m; ++s) {
         orc_segment_points(rays + 8 * s, t0[s], t1[s], n_points, xi + s * n_points, dom_min, dom_inv, pts.data());
         for (int p = 0; p < n_points; ++p)
             encode_point(L, F, log2_T, res, dense, offset, table, &pts[3 * p], feat.data(), idx.data() + p * L * 8);
         const double* x = x_in + s * D;
-        mlp_forward_one(n_layers, dims, W.data(), b.data(), x, z.data(), acts.data());
-        for (int o = 0; o < n_out; ++o) z_out[s * n_out + o] = z[o];
-        // magnitudes and ReLU margins (pre-activation = acts value before the mask: recompute)
-        double marg = std::numeric_limits<double>::infinity();
+        const uint8_t* mk = masks ? masks + s * H * 64 : nullptr;
+        // forward in double on the given x: pre = b + W h (same order as mlp_forward_one);
+        // hidden output = ReLU(pre), or, with given masks, pre where the mask is on, else 0;
+        // magnitudes |W| |h| + |b| alongside; ReLU margin = min |pre| / magnitude
+        double marg = std::numeric_limits<double>::infinity(), fmarg = 0.0;
+        int32_t flips = 0;
+        acts[0].assign(x, x + D);
         habs.assign(x, x + D);
         for (double& v : habs) v = std::fabs(v);
         for (int k = 0; k < n_layers; ++k) {
+            mags[k] = habs;
+            acts[k + 1].assign(dims[k + 1], 0.0);
             nabs.assign(dims[k + 1], 0.0);
             for (int o = 0; o < dims[k + 1]; ++o) {
-                double sa = std::fabs((double)b[k][o]), sv = (double)b[k][o];
+                double sv = (double)b[k][o], sa = std::fabs((double)b[k][o]);
                 for (int i = 0; i < dims[k]; ++i) {
                     const double w = orc_half_to_double(W[k][(int64_t)o * dims[k] + i]);
-                    sa += std::fabs(w) * habs[i];
                     sv += w * acts[k][i];
+                    sa += std::fabs(w) * habs[i];
                 }
                 if (k + 1 < n_layers) {
-                    if (sa > 0.0) marg = std::min(marg, std::fabs(sv) / sa);
-                    nabs[o] = sv > 0.0 ? sa : 0.0;
+                    const double rm = sa > 0.0 ? std::fabs(sv) / sa : std::numeric_limits<double>::infinity();
+                    marg = std::min(marg, rm);
+                    const bool own = sv > 0.0;
+                    const bool on = mk ? mk[k * 64 + o] != 0 : own;
+                    if (on != own) { ++flips; fmarg = std::max(fmarg, rm); }
+                    acts[k + 1][o] = on ? sv : 0.0;
+                    nabs[o] = on ? sa : 0.0;
                 } else {
+                    acts[k + 1][o] = sv;
                     nabs[o] = sa;
                 }
             }
             habs.swap(nabs);
         }
-        for (int o = 0; o < n_out; ++o) z_abs[s * n_out + o] = habs[o];
+        for (int o = 0; o < n_out; ++o) {
+            z_out[s * n_out + o] = acts[n_layers][o];
+            z_abs[s * n_out + o] = habs[o];
+        }
         relu_margin[s] = marg;
+        if (mask_flips) mask_flips[s] = flips;
+        if (flip_margin) flip_margin[s] = fmarg;
+        std::vector<uint8_t> own_mask;
+        if (!mk) {                                   // masks of the double forward itself
+            own_mask.assign(H * 64, 0);
+            for (int k = 0; k < H; ++k)
+                for (int o = 0; o < dims[k + 1]; ++o) own_mask[k * 64 + o] = acts[k + 1][o] > 0.0;
+            mk = own_mask.data();
+        }
         std::vector<double> delta(dz_in + s * n_out, dz_in + (s + 1) * n_out);
         backward_sample(M, W, acts.data(), delta, pts.data(), idx.data(), nW, nb, g_table, g_W, g_b, false,
-                        hidden_delta ? hidden_delta + s * H * 64 : nullptr);
+                        hidden_delta ? hidden_delta + s * H * 64 : nullptr, mk);
         backward_sample(M, W, acts.data(), delta, pts.data(), idx.data(), nW, nb, g_table_abs, g_W_abs, g_b_abs,
-                        true, hidden_delta_abs ? hidden_delta_abs + s * H * 64 : nullptr);
+                        true, hidden_delta_abs ? hidden_delta_abs + s * H * 64 : nullptr, mk, mags.data());
     }
 }
 

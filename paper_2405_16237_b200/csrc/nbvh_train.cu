@@ -562,7 +562,8 @@ extern "C" nbvh_status nbvh_debug_train_capture(nbvh_ctx* c, int32_t enable) {
 }
 
 extern "C" nbvh_status nbvh_debug_train_activations(nbvh_ctx* c, int32_t* d_sample_ray, uint16_t* d_x, float* d_z,
-                                                    float* d_dz, uint16_t* d_delta, int64_t* h_m, void* stream) {
+                                                    float* d_dz, uint16_t* d_act, uint16_t* d_delta, int64_t* h_m,
+                                                    void* stream) {
     nbvh_status st = check_device(c);
     if (st) return st;
     if (!h_m) return fail(c, NBVH_EINVAL, "debug_train_activations: null count pointer");
@@ -580,7 +581,10 @@ extern "C" nbvh_status nbvh_debug_train_activations(nbvh_ctx* c, int32_t* d_samp
     if (e == cudaSuccess && d_x) e = cudaMemcpyAsync(d_x, w->X, m * D * 2, cudaMemcpyDeviceToDevice, s);
     if (e == cudaSuccess && d_z) e = cudaMemcpyAsync(d_z, w->Z, m * 8 * 4, cudaMemcpyDeviceToDevice, s);
     if (e == cudaSuccess && d_dz) e = cudaMemcpyAsync(d_dz, w->dZ, m * 8 * 4, cudaMemcpyDeviceToDevice, s);
-    for (size_t k = 0; e == cudaSuccess && d_delta && k < H; ++k)     // [H][M][64] -> [H][m][64]
+    for (size_t k = 0; e == cudaSuccess && d_act && k < H; ++k)       // [H][cap][64] -> [H][m][64]
+        e = cudaMemcpyAsync(d_act + k * m * 64, w->A + k * (size_t)w->cap * 64, m * 64 * 2,
+                            cudaMemcpyDeviceToDevice, s);
+    for (size_t k = 0; e == cudaSuccess && d_delta && k < H; ++k)
         e = cudaMemcpyAsync(d_delta + k * m * 64, w->Dl + k * (size_t)w->cap * 64, m * 64 * 2,
                             cudaMemcpyDeviceToDevice, s);
     if (e != cudaSuccess) return cuda_fail(c, e, "debug_train_activations");

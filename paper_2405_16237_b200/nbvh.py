@@ -92,7 +92,7 @@ SIGNATURES = {
     "nbvh_debug_query_trace": (C.c_int, [_P, _P, _I64, _I32, Hits, _P, _I32, _P]),
     "nbvh_debug_train_samples": (C.c_int, [_P, _P, _P, _P, _P, _P]),
     "nbvh_debug_train_capture": (C.c_int, [_P, _I32]),
-    "nbvh_debug_train_activations": (C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P]),
+    "nbvh_debug_train_activations": (C.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _P]),
 }
 
 
@@ -426,7 +426,7 @@ class Context:
     def debug_train_activations(self, n_rays, stream=None):
         """Per-sample intermediates of the last training batch (compacted sample order):
         dict(ray [m] int32, x [m, D_in] fp16, z [m, 8] (capture on, else None), dz [m, 8],
-        delta [hidden, m, 64] fp16)."""
+        act / delta [hidden, m, 64] fp16)."""
         import torch
         dev = f"cuda:{self.device}"
         H = self.cfg.hidden_layers
@@ -434,21 +434,24 @@ class Context:
         x = torch.empty(n_rays * self.d_in, dtype=torch.float16, device=dev)
         z = torch.empty(n_rays * 8, dtype=torch.float32, device=dev)
         dz = torch.empty(n_rays * 8, dtype=torch.float32, device=dev)
+        act = torch.empty(H * n_rays * 64, dtype=torch.float16, device=dev)
         dl = torch.empty(H * n_rays * 64, dtype=torch.float16, device=dev)
         m = np.zeros(1, np.int64)
-        st = self.lib.nbvh_debug_train_activations(self.h, _ptr(ray), _ptr(x), _ptr(z), _ptr(dz), _ptr(dl),
-                                                   _ptr(m), _stream_ptr(stream))
+
+        def call(zp):
+            return self.lib.nbvh_debug_train_activations(self.h, _ptr(ray), _ptr(x), zp, _ptr(dz), _ptr(act),
+                                                         _ptr(dl), _ptr(m), _stream_ptr(stream))
+        st = call(_ptr(z))
         zt = z
         if st == -3:                                  # NBVH_ESTATE: capture off -> no z
-            self._ck(self.lib.nbvh_debug_train_activations(self.h, _ptr(ray), _ptr(x), None, _ptr(dz), _ptr(dl),
-                                                           _ptr(m), _stream_ptr(stream)), "debug_train_activations")
+            self._ck(call(None), "debug_train_activations")
             zt = None
         else:
             self._ck(st, "debug_train_activations")
         mm = int(m[0])
         return dict(ray=ray[:mm], x=x[:mm * self.d_in].view(mm, self.d_in),
                     z=None if zt is None else zt[:mm * 8].view(mm, 8), dz=dz[:mm * 8].view(mm, 8),
-                    delta=dl[:H * mm * 64].view(H, mm, 64))
+                    act=act[:H * mm * 64].view(H, mm, 64), delta=dl[:H * mm * 64].view(H, mm, 64))
 
     def debug_traverse_product(self, rays, lod=0, stream=None):
         """The product k_traverse's lists: (leaf [n, K], te, tx, fill [n], more [n])."""
@@ -464,4 +467,3 @@ class Context:
                                                       _ptr(fill), _ptr(more), _stream_ptr(stream)),
                  "debug_traverse_product")
         return leaf, te, tx, fill, more
-

@@ -4,5 +4,5 @@ cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
 OUT=gpurun_out; TAG=${1:-t}; shift
 mkdir -p $OUT
 python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1
-timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider "$@" > $OUT/pytest_gpu_$TAG.log 2>&1
+timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider -rf "$@" > $OUT/pytest_gpu_$TAG.log 2>&1
 echo "pytest exit $?" >> $OUT/pytest_gpu_$TAG.log

@@ -5,7 +5,7 @@ stage, so each comparison isolates one kernel step, with a tolerance derived fro
 floating-point operations of that step ("training tolerances"):
 
 * T3 features x (fp32 trilinear blend of fp16 entries, rounded to fp16) vs the oracle's
-  double encode of the same fp32 sample points: |dx| <= 2^-11 |x| + 2^-24.
+  double encode of the same fp32 sample points: |dx| <= 2^-11 |x| + 1e-6 (the fp32 blend).
 * T4 raw z (fp16 x, fp16 weights, fp32 accumulation, hidden activations rounded to fp16)
   vs the oracle's double MLP on the GPU's x: |dz| <= H 2^-11 z_abs + 1e-6, where z_abs is
   the same forward on absolute values (|W| |h| + |b|): each of the H fp16 roundings of a
@@ -16,13 +16,12 @@ floating-point operations of that step ("training tolerances"):
   atomics), vs the oracle's double reverse mode from the GPU's x and dL/dz
   (orc_train_backward_given): per element |dg| <= ((H + 2) 2^-11 + m 2^-24) g_abs + 1e-7,
   g_abs = the same reverse mode on absolute values.  (H + 2) fp16 roundings: dL/dz, the H
-  deltas; m 2^-24: fp32 summation over the m samples.
+  deltas; m 2^-24: fp32 summation over the m samples; weights and biases also carry the
+  absolute rounding of fp16 subnormal deltas ((H + 1) 2^-25 |input| per sample).
 
-ReLU decisions are floating-point decisions: a sample whose hidden pre-activation lies
-within (H + 1) 2^-11 of zero relative to its magnitude may take the other branch on the
-GPU.  Such samples (the oracle's relu_margin) are removed from the batch before the
-compared pass by setting their acceptance draw to 1 (never accepted) -- the training
-counterpart of the query's ambiguity band; their number is reported and bounded.
+ReLU decisions are floating-point decisions (C36): the oracle takes the kernel's own (the
+exported activations' act > 0) and every decision where the two disagree must lie within
+the rounding bound of its threshold: |pre| <= (H + 1) 2^-11 x magnitude.
 """
 import numpy as np
 import pytest
@@ -86,23 +85,14 @@ def _run(name, dw_path, monkeypatch, n_rays=6000, seed=70):
         out.update(gt=gt, acc=acc, loss=loss, grad=dp.grad_tensor(ctx).cpu().numpy().astype(np.float64))
         return out
 
-    def oracle_given(p, deltas=False):
-        r = p["ray"]
-        return orc.train_backward_given(g, npts, tabF, layers, box, rays[r], te[r, 0], tx[r, 0], xi[r],
-                                        p["x"].astype(np.float64), p["dz"].astype(np.float64), want_deltas=deltas)
-
-    # pass 1: find the samples with an ambiguous ReLU decision, reject them
-    p1 = gpu_pass(u)
-    o1 = oracle_given(p1)
-    amb = o1["relu_margin"] < (H + 1) * U * 2
-    u2 = u.copy()
-    u2[p1["ray"][amb]] = 1.0
-    # pass 2: the compared batch
-    p2 = gpu_pass(u2)
-    o2 = oracle_given(p2, deltas=True)
-    assert np.all(o2["relu_margin"] >= (H + 1) * U * 2)
+    p = gpu_pass(u)
+    masks = np.transpose(p["act"] > 0, (1, 0, 2)).astype(np.uint8)             # [m][H][64]
+    r = p["ray"]
+    o = orc.train_backward_given(g, npts, tabF, layers, box, rays[r], te[r, 0], tx[r, 0], xi[r],
+                                 p["x"].astype(np.float64), p["dz"].astype(np.float64), masks=masks,
+                                 want_deltas=True)
     return dict(ctx=ctx, sc=sc, cut=cut, g=g, tab=tabF, layers=layers, rays=rays, xi=xi, te=te, tx=tx, box=box,
-                p=p2, o=o2, n_amb=int(amb.sum()), m1=p1["ray"].size, H=H, npts=npts, F=F, u2=u2, rank=rank)
+                p=p, o=o, H=H, npts=npts, F=F, u=u, rank=rank)
 
 
 @pytest.mark.parametrize("name,dw_path", [("tiny_h2", "tcgen05"), ("tiny_h3", "tcgen05"), ("cfg2_grid", "tcgen05"),
@@ -114,7 +104,9 @@ def test_training_stages_elementwise(name, dw_path, monkeypatch):
     p, o, H, g = R["p"], R["o"], R["H"], R["g"]
     m = p["ray"].size
     assert m > 500, m
-    assert R["n_amb"] <= 0.3 * R["m1"], (R["n_amb"], R["m1"])          # ambiguous ReLU samples removed
+    # the kernel's ReLU decisions: disagreements with the double sign only within rounding
+    assert np.all(o["flip_margin"] <= (H + 1) * U), o["flip_margin"].max()
+    assert (o["mask_flips"] > 0).mean() < 0.05, (o["mask_flips"] > 0).mean()
     r = p["ray"]
     # ---- T3 features: the oracle's own double encode of the same fp32 sample points
     dmin, dinv = orc.domain(*np.split(R["box"].reshape(1, 6), 2, axis=1))
@@ -123,7 +115,7 @@ def test_training_stages_elementwise(name, dw_path, monkeypatch):
     feat, _ = orc.encode_points(g, R["tab"], pts.reshape(-1, 3))
     x_orc = feat.reshape(m, -1)
     x_gpu = p["x"].astype(np.float64)
-    assert np.all(np.abs(x_gpu - x_orc) <= U * np.abs(x_orc) + U32), np.abs(x_gpu - x_orc).max()
+    assert np.all(np.abs(x_gpu - x_orc) <= U * np.abs(x_orc) + 1e-6), np.abs(x_gpu - x_orc).max()
     # ---- T4 raw z: double MLP on the GPU's own features
     z = p["z"].astype(np.float64)
     tol_z = H * U * o["z_abs"] + 1e-6
@@ -149,12 +141,25 @@ def test_training_stages_elementwise(name, dw_path, monkeypatch):
     n_t = R["ctx"].param_count(PARAM_TABLES)
     n_w, n_b = o["g_W"].size, o["g_b"].size
     rt = (H + 2) * U + m * U32
-    for blk, gg, oo, aa in (("tables", grad[:n_t], o["g_table"], o["g_table_abs"]),
-                            ("weights", grad[n_t:n_t + n_w], o["g_W"], o["g_W_abs"]),
-                            ("biases", grad[n_t + n_w:n_t + n_w + n_b], o["g_b"], o["g_b_abs"])):
-        tol = rt * aa + 1e-7
+    # fp16 subnormals: a delta (or dL/dz cast) below 2^-14 is rounded with ABSOLUTE error
+    # <= 2^-25, so each sample adds up to (H + 1) 2^-25 |input| to a weight gradient
+    # (|input| = 1 for biases) on top of the relative bound
+    ins = [p["x"].astype(np.float64)] + [p["act"][k].astype(np.float64) for k in range(H)]
+    dims = [ins[0].shape[1]] + [64] * H + [8]
+    under_w, under_b = [], []
+    for k in range(H + 1):
+        col = np.abs(ins[k]).sum(0)                                     # sum over samples, per input unit
+        under_w.append(np.tile(col, dims[k + 1]))
+        under_b.append(np.full(dims[k + 1], float(m)))
+    under_w = (H + 1) * 2.0 ** -25 * np.concatenate(under_w)
+    under_b = (H + 1) * 2.0 ** -25 * np.concatenate(under_b)
+    for blk, gg, oo, aa, un in (("tables", grad[:n_t], o["g_table"], o["g_table_abs"], 0.0),
+                                ("weights", grad[n_t:n_t + n_w], o["g_W"], o["g_W_abs"], under_w),
+                                ("biases", grad[n_t + n_w:n_t + n_w + n_b], o["g_b"], o["g_b_abs"], under_b)):
+        tol = rt * aa + un + 1e-7
         bad = np.abs(gg - oo) > tol
-        assert not bad.any(), (blk, int(bad.sum()), (np.abs(gg - oo) / tol).max())
+        assert not bad.any(), (blk, int(bad.sum()), (np.abs(gg - oo) / tol).max(), np.nonzero(bad)[0][:8],
+                               aa[bad][:8], oo[bad][:8], gg[bad][:8])
         assert np.count_nonzero(oo) > 0.5 * min(oo.size, 1000) or blk == "tables"
     # ---- tail: accepted count, per-leaf sample and first-hit counts exact, loss sums (fp32 atomics)
     tail = grad[n_t + n_w + n_b:]
@@ -170,15 +175,16 @@ def test_training_stages_elementwise(name, dw_path, monkeypatch):
 
 def test_training_forward_vs_full_double_chain(monkeypatch):
     """The whole forward (T3-T5) against the oracle's own double chain (orc_train_grad, its
-    double features and MLP): per-sample z within the fp16 chain's bound (H + 1) 2^-11 z_abs
-    (x rounded once more than in the staged check), and every sample's loss within the
-    loss's Lipschitz bound of that z error."""
+    double features and MLP, its own ReLU decisions): per-sample z within the fp16 chain's
+    bound (H + 1) 2^-11 z_abs on samples without a flipped ReLU decision (x is rounded once
+    more than in the staged check), and every such sample's loss within the loss's Lipschitz
+    bound of that z error."""
     import oracle as orc
     R = _run("tiny_h2", "tcgen05", monkeypatch)
     p, H = R["p"], R["H"]
     r = p["ray"]
     full = orc.train_grad(R["g"], R["npts"], R["tab"], R["layers"], R["cut"]["leaf_lo"], R["cut"]["leaf_hi"],
-                          R["rank"], R["cut"]["tri_off"], R["cut"]["tris"], R["sc"], R["rays"], R["u2"], R["xi"],
+                          R["rank"], R["cut"]["tri_off"], R["cut"]["tris"], R["sc"], R["rays"], R["u"], R["xi"],
                           dom_box=R["box"])
     assert np.array_equal(np.nonzero(full["accepted"])[0], np.sort(r))
     dmin, dinv = orc.domain(*np.split(R["box"].reshape(1, 6), 2, axis=1))
@@ -187,9 +193,13 @@ def test_training_forward_vs_full_double_chain(monkeypatch):
     x_orc = orc.encode_points(R["g"], R["tab"], pts.reshape(-1, 3))[0].reshape(r.size, -1)
     z_orc = orc.mlp_forward(R["layers"], x_orc)
     z = p["z"].astype(np.float64)
+    ok = R["o"]["mask_flips"] == 0
+    assert ok.mean() > 0.95
     tol = (H + 1) * U * R["o"]["z_abs"] + 1e-6
-    assert np.all(np.abs(z - z_orc) <= tol), (np.abs(z - z_orc) / tol).max()
-    # loss: |dL| <= sum_c Lip_c |dz_c|, Lip = (2*1/4 BCE, 2*1/4 L1(sigmoid), 1/3 per normal, <= 2 relL2)
-    lip = np.array([0.5, 0.5, 1 / 3, 1 / 3, 1 / 3, 2.0, 2.0, 2.0])
+    assert np.all(np.abs(z - z_orc)[ok] <= tol[ok]), (np.abs(z - z_orc)[ok] / tol[ok]).max()
+    # loss: |dL| <= sum_c Lip_c |dz_c| with Lip = max |dL/dz_c|: 2 (2 BCE: 2|sigma - y|),
+    # 1/2 (2 L1 of sigma), 1/3 per normal component, <= 3.1 per albedo channel (relative L2)
+    lip = np.array([2.0, 0.5, 1 / 3, 1 / 3, 1 / 3, 3.1, 3.1, 3.1])
     bound = (np.abs(z - z_orc) * lip).sum(1) + 1e-5
-    assert np.all(np.abs(p["loss"][r] - full["loss"][r]) <= bound + 2e-5 * np.abs(full["loss"][r]))
+    dl = np.abs(p["loss"][r] - full["loss"][r])
+    assert np.all((dl <= bound + 2e-5 * np.abs(full["loss"][r]))[ok])

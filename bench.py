@@ -400,6 +400,8 @@ def run_ours(args):
             "queries_per_ray": queries_per_ray, "slot_iterations_per_step": iters,
             "wall_s_timed_region": wall, "host_enqueue_ms_per_query": host_ms, "list_cap": args.list_cap,
             "list_refills_per_step": st["n_refills"],
+            "mlp_tiles_per_step": st.get("n_mlp_tiles"), "mlp_rows_per_tile": (st["n_mlp_rows"] / st["n_mlp_tiles"]
+                                                                               if st.get("n_mlp_tiles") else None),
             "model_broadcast": {"bytes": 4 * ctx.param_count(3), "seconds": bcast_s, "params_identical": identical},
             "roofline": roof, "weak_scaling": weak,
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks.summary(), "mlp": mlp, "gather_roofline": gather,
@@ -674,7 +676,7 @@ def bench_gather(args):
         out[name + "_GBps"] = done * 32 / s / 1e9
         del tab
     from paper_2405_16237_b200.nbvh import atomic_probe
-    for vec in (1, 2):                                                   # T7 scatter roofline
+    for vec in (1, 2, 4):                                                # T7 scatter roofline
         tab = torch.zeros((32 << 20) // 4, dtype=torch.float32, device="cuda")   # ~ the cfg-2 gradient buffer
         atomic_probe(tab, vec, 1 << 26)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -682,7 +684,7 @@ def bench_gather(args):
         done = sum(atomic_probe(tab, vec, 1 << 27, seed=i + 2) for i in range(2))
         e1.record(stream)
         torch.cuda.synchronize()
-        out[f"l2_red_{'v2_' if vec == 2 else ''}f32_Gops"] = done / (e0.elapsed_time(e1) / 1e3) / 1e9
+        out[f"l2_red_{'' if vec == 1 else f'v{vec}_'}f32_Gops"] = done / (e0.elapsed_time(e1) / 1e3) / 1e9
         del tab
     prof = _profiled_l2_reads("k_query")
     if prof:

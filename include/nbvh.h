@@ -103,6 +103,8 @@ typedef struct {
     int32_t n_refills;       /* re-traversals after a leaf-list overflow (C6)               */
     float ms_traverse;       /* device time of the traversal kernel (profiling on, else 0)  */
     float ms_query;          /* device time of the persistent query kernel (profiling on)   */
+    int32_t n_mlp_tiles;     /* 128-row MLP tiles run on tcgen05 (warp-specialised kernel)  */
+    int32_t n_mlp_rows;      /* rows in them (<= 128 per tile; the rest is padding)         */
 } nbvh_query_stats;
 
 /* Training counters of the last nbvh_train_backward / nbvh_train_step. */
@@ -208,8 +210,9 @@ nbvh_status nbvh_gather_probe(const void* d_table, int64_t table_bytes, int32_t 
                               uint32_t seed, uint32_t* d_sink, int64_t sink_len, int64_t* n_done, void* stream);
 /* The scatter roofline of SURVEY §8(d) (T7 is bound by L2 atomics): n_ops uniformly random
  * fp32 reductions (vec 1: red.global.add.f32; vec 2: red.global.add.v2.f32 on 8-byte pairs,
- * as the training backward issues for F = 2) of +1 into the device table d_table
- * (table_bytes / (4 vec) a power of two; 8-byte aligned; its contents are modified).  *n_done
+ * as the training backward issues for F = 2; vec 4: red.global.add.v4.f32 on 16-byte quads)
+ * of +1 into the device table d_table (table_bytes / (4 vec) a power of two; 16-byte
+ * aligned; its contents are modified).  *n_done
  * (host) = reductions issued.  No context; the caller times it.  NBVH_EINVAL on bad arguments. */
 nbvh_status nbvh_atomic_probe(float* d_table, int64_t table_bytes, int32_t vec, int64_t n_ops, uint32_t seed,
                               int64_t* n_done, void* stream);

@@ -656,14 +656,18 @@ nbvh_status resolve_query_stats(nbvh_ctx* c) {
     if (e != cudaSuccess) return cuda_fail(c, e, "query stats");
     c->qstats_pending = false;
     int64_t nq = 0;
-    int32_t iters = 0, refills = 0, err = 0;
+    int32_t iters = 0, refills = 0, err = 0, tiles = 0, rows = 0;
     for (int b = 0; b < nb; ++b) {
         const QueryCounters* q = reinterpret_cast<const QueryCounters*>(c->h_misc + (size_t)b * kCounterStride);
         nq += (int64_t)q->n_queries;
         iters = std::max(iters, q->max_iter);
         refills += q->refills;
         err |= q->err;
+        tiles += q->mlp_tiles;
+        rows += q->mlp_rows;
     }
+    c->qstats.n_mlp_tiles = tiles;
+    c->qstats.n_mlp_rows = rows;
     c->qstats.n_queries = nq;
     c->qstats.n_iters = iters;
     c->qstats.n_launches = c->qstats_launches;

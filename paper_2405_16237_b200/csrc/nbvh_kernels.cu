@@ -3,18 +3,21 @@
 //   k_traverse    Q0+Q1: load rays, traverse the shallow N-BVH of the chosen cut, write each
 //                 ray's (t_enter, id)-ordered leaf list (capacity K) and append the ray
 //                 (32-byte work record) to the long- or short-ray work list.
-//   k_query       Q2-Q7, one persistent launch: every warp owns 16 ray slots and loops —
-//                 refill empty slots from the work lists, sample the current leaf segment,
-//                 hash-grid encode into shared memory, run the MLP on tensor cores
-//                 (mma.sync per warp; optional kTc variant: tcgen05 per 8-warp group),
-//                 decode, update the best hit, decide front-to-back termination, write
-//                 finished rays' hit records.
+//   k_query_warp  Q2-Q7, one persistent launch per frame (the default): every warp owns 16
+//                 ray slots and loops -- refill, sample, encode, MLP on mma.sync, decode.
+//   k_query_ws    the same steps warp-specialised (NBVH_QUERY_MLP=tc): 16 worker warps own
+//                 two sets of 16 ray slots each and loop -- refill empty slots from the work
+//                 lists, sample the current leaf segment, hash-grid encode into a 16-row
+//                 block of a 128-row feature tile, decode, update the best hit, decide
+//                 front-to-back termination, write finished rays' hit records -- while one
+//                 MLP warpgroup runs the decoder MLP of full tiles on tcgen05 (TMEM
+//                 accumulators, weights read by the tensor core from shared memory).
 //   k_debug_*     the same device functions with intermediate results exposed.
 //
 // Paper passages: P:103 (front-to-back probing, early termination)
 // (segment sampling, feature concatenation, MLP decode), P:161 (queries per ray =
 // leaves met before a hit), P:201/P:237/P:243 (visibility threshold, local distance,
-// normal, albedo).  Readings C1-C33: DESIGN.md §3.
+// normal, albedo).  Readings C1-C36: DESIGN.md §3.
 #include <cuda_runtime.h>
 
 #include <cstdlib>
@@ -358,7 +361,7 @@ __device__ __forceinline__ void query_mlp_rows16(const MlpSmem& s, int hidden, c
 
 // Ray slots of one warp (structure of arrays in shared memory).  Lane s < kWarpQ owns slot
 // s for the refill and decode steps; the encode and MLP steps work on the compacted rows.
-constexpr int kWarpQ = 16;          // queries per warp iteration (one m16 MMA row block)
+constexpr int kWarpQ = 16;          // queries per slot set (one m16 / one 16-row tile block)
 constexpr int kQueryWarps = 16;     // warps per CTA (one CTA per SM; bounded by shared memory)
 
 struct WarpSlots {
@@ -370,42 +373,222 @@ struct WarpSlots {
 };
 
 __host__ __device__ constexpr size_t align16(size_t b) { return (b + 15) & ~(size_t)15; }
+__host__ __device__ constexpr size_t align128(size_t b) { return (b + 127) & ~(size_t)127; }
 
-// Shared-memory plan of k_query (bytes), shared by the kernel and its launcher: the MLP
-// weights and level table once per CTA, then one private region per warp.
-//   kTc = false: weights [out][in] padded for ldmatrix, per-warp feature rows [16][D+8];
-//   kTc = true:  weights in the K-major canonical (core-matrix) layout with bias columns, a
-//                ones tile for the bias K-steps, two group tiles [max(D/8, 8) K-groups][128
-//                rows][16 B] (features, then hidden activations), mbarriers / TMEM slot /
-//                group votes; no per-warp feature rows.
-constexpr int kGroupWarps = 8;                                  // kTc: warps per 128-row MLP group
-constexpr int kKgHid = 64 / 8 + 2;                              // K-groups of a hidden W (+ bias)
-__host__ __device__ constexpr int tc_tile_kg(int d_in) { return d_in / 8 > 8 ? d_in / 8 : 8; }
+// Lanes below this one (a special register: nothing kept live across the query loop).
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
-struct QuerySmemPlan {
-    size_t w, bias, lv, misc, gtile, warp0, feat, z, xs, slots, per_warp, total;
-    size_t w0, wh, wo, ones;                                    // kTc weight regions (absolute)
-    int warps;
-    __host__ __device__ QuerySmemPlan(int d_in, int hidden, int n_points, bool tc = false) {
-        w = 0;
-        if (!tc) {
-            bias = w + align16((size_t)mlp_smem_halves(d_in, hidden) * 2);
-            lv = bias + align16((size_t)(64 * hidden + 8) * 4);
-            misc = gtile = w0 = wh = wo = ones = 0;
-            warp0 = lv + align16(sizeof(LevelSm) * kMaxLevels);
-        } else {
-            w0 = w;
-            wh = w0 + (size_t)64 * (d_in / 8 + 2) * 16;
-            wo = wh + (size_t)(hidden - 1) * 64 * kKgHid * 16;
-            ones = wo + (size_t)16 * kKgHid * 16;
-            lv = ones + 2 * 128 * 16;
-            misc = lv + align16(sizeof(LevelSm) * kMaxLevels);   // [0,16) 2 mbarriers, [16,20) TMEM
-            gtile = misc + 256;                                   // slot, [32,160) group votes
-            bias = 0;
-            warp0 = gtile + (size_t)2 * tc_tile_kg(d_in) * 2048;
+// ---- the steps of a slot set, shared by both query kernels (Q2-Q7)
+
+// (A) refill the set's empty slots with the next rays of the global work list (one atomic per
+// warp; long rays first).  `exhausted` (shared, per warp) is set once the list is drained.
+__device__ __forceinline__ void slots_refill(const QueryArgs& a, WarpSlots& S, int lane, int total, int n_long,
+                                             int* exhausted) {
+    const bool empty = lane < kWarpQ && S.ray[lane] < 0;
+    const unsigned em = __ballot_sync(0xffffffffu, empty);
+    if (em && !*exhausted) {
+        const int ne = __popc(em);
+        int base = 0;
+        if (lane == 0) base = atomicAdd(a.next, ne);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (lane == 0) *exhausted = base + ne >= total;
+        const int i = base + __popc(em & lanemask_lt());
+        if (empty && i < total) {
+            const WorkRec* wr = i < n_long ? a.act_long + i : a.act + (i - n_long);
+            // read-once streams (work records, lists) are loaded evict-first so they do not
+            // push the hash-table lines out of L1
+            const float4 w0 = __ldcs(&wr->o), w1 = __ldcs(&wr->d), w2 = __ldcs(&wr->e0);
+            const int r = __float_as_int(w0.w), st = __float_as_int(w1.w);
+            S.te[lane] = w2.x;
+            S.tx[lane] = w2.y;
+            S.leaf[lane] = __float_as_int(w2.z);
+            S.fresh[lane] = 1;
+            NBVH_DCHECK(r >= 0 && r < a.n_rays && (st & 0xffff) >= 1 && (st & 0xffff) <= a.cap);
+            S.ray[lane] = r;
+            S.o[0][lane] = w0.x; S.o[1][lane] = w0.y; S.o[2][lane] = w0.z;
+            S.d[0][lane] = w1.x; S.d[1][lane] = w1.y; S.d[2][lane] = w1.z;
+            S.pos[lane] = 0;
+            S.base[lane] = 0;
+            S.nbuf[lane] = st & 0xffff;
+            S.more[lane] = st >> 16;
+            S.bt[lane] = __int_as_float(0x7f800000);
+            S.bte[lane] = 0.f;
+            S.bleaf[lane] = -1;
+            S.nq[lane] = 0;
         }
-        feat = 0;                                                   // offsets within a warp region
-        z = feat + (tc ? 0 : align16((size_t)kWarpQ * (d_in + 8) * 2));
+    }
+    __syncwarp();
+}
+
+// (B) compact the occupied slots into rows 0..nv-1 (S.act[row] = slot) and (C) fetch each
+// ray's current leaf segment and its n stratified sample points (C8) into
+// xs [NP*3][kWarpQ].  Returns nv (warp-uniform).
+__device__ __forceinline__ int slots_segment(const QueryArgs& a, WarpSlots& S, float* xs, int lane, int NP) {
+    const bool occ = lane < kWarpQ && S.ray[lane] >= 0;
+    const unsigned om = __ballot_sync(0xffffffffu, occ);
+    const int nv = __popc(om);
+    if (occ) {
+        const int row = __popc(om & lanemask_lt());
+        S.act[row] = lane;
+        const int r = S.ray[lane];
+        NBVH_DCHECK(S.pos[lane] - S.base[lane] >= 0 && S.pos[lane] - S.base[lane] < S.nbuf[lane] &&
+                    S.nbuf[lane] <= kListK);
+        const int64_t li = (int64_t)(S.pos[lane] - S.base[lane]) * a.n_rays + r;
+        float te, tx;
+        if (S.fresh[lane]) {              // a new ray: entry 0 came with its work record
+            S.fresh[lane] = 0;
+            te = S.te[lane];
+            tx = S.tx[lane];
+        } else {
+            const float4 e = __ldcs(a.lst + li);
+            te = e.x;
+            tx = e.y;
+            S.leaf[lane] = __float_as_int(e.z);
+            S.te[lane] = te;
+            S.tx[lane] = tx;
+        }
+        const float o[3] = {S.o[0][lane], S.o[1][lane], S.o[2][lane]};
+        const float d[3] = {S.d[0][lane], S.d[1][lane], S.d[2][lane]};
+        for (int p = 0; p < NP; ++p) {
+            float x[3];
+            segment_point(a.g, o, d, te, tx, p, NP, nullptr, x);
+            xs[(p * 3 + 0) * kWarpQ + row] = x[0];
+            xs[(p * 3 + 1) * kWarpQ + row] = x[1];
+            xs[(p * 3 + 2) * kWarpQ + row] = x[2];
+        }
+    }
+    __syncwarp();
+    return nv;
+}
+
+// (D) hash-grid encode of the nv rows: lane -> row q = lane % 16; the two half-warps take
+// sample points of opposite parity at the same levels (neighbouring points of the same rays:
+// coherent lines).  Chunk c (8 halves) of row q is stored at dst + c * cstride + q * rstride.
+template <int F>
+__device__ __forceinline__ void rows_encode(const QueryArgs& a, const LevelSm* lv, const float* xs, int nv, int lane,
+                                            int NP, unsigned char* dst, int cstride, int rstride) {
+    const int q = lane & (kWarpQ - 1), h = lane / kWarpQ;
+    const int cpp = (a.g.L * F) / 8;      // 16-byte chunks per sample point
+    const uint32_t hmask = (1u << a.g.log2_T) - 1u;
+    if (q < nv) {
+        for (int p = h; p < NP; p += 2) {
+            const float* xp = xs + p * 3 * kWarpQ;
+            const float x0 = xp[q], x1 = xp[kWarpQ + q], x2 = xp[2 * kWarpQ + q];
+            for (int lc = 0; lc < cpp; ++lc) {
+                const int c = p * cpp + lc;
+                const uint4 f = encode_chunk_sm<F>(lv, a.g.table, hmask, x0, x1, x2, lc * (8 / F), nullptr);
+                *reinterpret_cast<uint4*>(dst + c * cstride + q * rstride) = f;
+            }
+        }
+    }
+    __syncwarp();
+}
+
+// (F) decode the nv rows' raw outputs z [row][8], update each ray's
+// best hit, decide front-to-back termination (C5, C6) and write the finished
+// rays' hit records (Q7).  Returns the number of queries decoded.
+__device__ __forceinline__ void rows_decode(const QueryArgs& a, WarpSlots& S, const float* zt, int nv, int lane) {
+    if (lane < nv) {
+        const int s = S.act[lane];
+        const int r = S.ray[s];
+        const float* z = zt + lane * 8;
+        int pos = S.pos[s];
+        if (a.z_trace && pos < a.trace_cap) {
+            float4* dst = reinterpret_cast<float4*>(a.z_trace + ((int64_t)r * a.trace_cap + pos) * 8);
+            dst[0] = make_float4(z[0], z[1], z[2], z[3]);
+            dst[1] = make_float4(z[4], z[5], z[6], z[7]);
+        }
+        const int nq = S.nq[s] + 1;
+        const float te = S.te[s], tx = S.tx[s];
+        const int leaf = S.leaf[s];
+        float bt = S.bt[s];
+        int bleaf = S.bleaf[s];
+        const bool hit = z[0] < 0.0f;                                  // sigmoid(z) < 0.5 (C13)
+        if (hit) {
+            const float tl = sigmoid_f(z[1]);                          // local distance
+            const float t = __fadd_rn(te, __fmul_rn(tl, __fsub_rn(tx, te)));
+            const float bte = S.bte[s];
+            const bool better = bleaf < 0 || t < bt || (t == bt && (te < bte || (te == bte && leaf < bleaf)));
+            if (better) {
+                bt = t;
+                bleaf = leaf;
+                S.bt[s] = t;
+                S.bte[s] = te;
+                S.bleaf[s] = leaf;
+                float nn = __fsqrt_rn(__fadd_rn(__fadd_rn(__fmul_rn(z[2], z[2]), __fmul_rn(z[3], z[3])),
+                                                __fmul_rn(z[4], z[4])));
+                nn = fmaxf(nn, 1e-6f);
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    S.nrm[k][s] = __fdiv_rn(z[2 + k], nn);
+                    S.alb[k][s] = sigmoid_f(z[5 + k]);
+                }
+            }
+        }
+        ++pos;
+        bool done = a.mode == 1 && hit;                                 // R1: first confident hit (C5)
+        if (!done) {
+            int base = S.base[s], nbuf = S.nbuf[s];
+            if (pos - base >= nbuf) {
+                if (!S.more[s]) {
+                    done = true;                                         // every intersected leaf visited
+                } else {
+                    // list exhausted, more leaves may remain: resume after the last key,
+                    // bounded by the best hit (C6)
+                    int more = 0;
+                    nbuf = refill_list(a.cut, a.rays, a.n_rays, a.cap, a.lst, a.ctr, r,
+                                       nbuf, bleaf >= 0 ? bt : __int_as_float(0x7f800000), &more);
+                    base = pos;
+                    S.base[s] = base;
+                    S.nbuf[s] = nbuf;
+                    S.more[s] = more;
+                    done = nbuf == 0;
+                }
+            }
+            if (!done) {
+                const float next_te = __ldcs(a.lst + (int64_t)(pos - base) * a.n_rays + r).x;
+                done = bleaf >= 0 && next_te > bt;                     // front-to-back termination
+            }
+        }
+        S.pos[s] = pos;
+        S.nq[s] = nq;
+        if (done) {
+            // Q7: hit record; a miss keeps t = +inf and zero vectors
+            const bool h = bleaf >= 0;
+            a.out.hit[r] = h ? 1 : 0;
+            a.out.t[r] = h ? bt : __int_as_float(0x7f800000);
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                a.out.normal[3 * (int64_t)r + k] = h ? S.nrm[k][s] : 0.f;
+                a.out.albedo[3 * (int64_t)r + k] = h ? S.alb[k][s] : 0.f;
+            }
+            if (a.out.leaf) a.out.leaf[r] = bleaf;
+            if (a.out.n_queries) a.out.n_queries[r] = nq;
+            S.ray[s] = -1;
+        }
+    }
+    __syncwarp();
+}
+
+// ------------------------------------------------------------------ query kernel, per-warp MLP
+// Shared-memory plan of k_query_warp (bytes), shared by the kernel and its launcher: the MLP
+// weights ([out][in] padded for ldmatrix) and level table once per CTA, then one private
+// region per warp (feature rows [16][D+8], z, sample points, slots).
+struct QuerySmemPlan {
+    size_t w, bias, lv, warp0, feat, z, xs, slots, per_warp, total;
+    int warps;
+    __host__ __device__ QuerySmemPlan(int d_in, int hidden, int n_points) {
+        w = 0;
+        bias = w + align16((size_t)mlp_smem_halves(d_in, hidden) * 2);
+        lv = bias + align16((size_t)(64 * hidden + 8) * 4);
+        warp0 = lv + align16(sizeof(LevelSm) * kMaxLevels);
+        feat = 0;
+        z = feat + align16((size_t)kWarpQ * (d_in + 8) * 2);
         xs = z + align16((size_t)kWarpQ * 8 * 4);
         slots = xs + align16((size_t)kWarpQ * n_points * 3 * 4);
         per_warp = slots + align16(sizeof(WarpSlots));
@@ -413,107 +596,22 @@ struct QuerySmemPlan {
         const size_t cap = 227 * 1024;
         warps = warp0 + per_warp > cap ? 0 : (int)((cap - warp0) / per_warp);
         if (warps > kQueryWarps) warps = kQueryWarps;
-        if (tc && warps < kQueryWarps) warps = 0;                   // kTc needs both 8-warp groups
         total = warp0 + per_warp * warps;
     }
 };
 
-// kTc: the decoder MLP of one 8-warp group's 128 rows on tcgen05 (M = 128, N = 64 / 16, fp32
-// accumulators in the group's 64 TMEM columns).  Every warp of the group calls it; warp 0 of
-// the group issues the MMAs (one elected lane), every warp converts 32 accumulator columns
-// of 32 rows (TMEM lane quarter wg % 4, column half wg / 4) into the next layer's fp16 A
-// tile, and the output layer's 8 columns are written into the owning warps' z rows.
-__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-
-template <int D>
-__device__ __forceinline__ void mlp_group_tc(int g, int wg, int lane, int hidden, uint32_t acc, unsigned char* gt,
-                                             uint32_t a_w0, uint32_t a_wh, uint32_t a_wo, uint32_t a_ones,
-                                             uint64_t* bar, uint32_t& phase, unsigned char* zbase, size_t per_warp,
-                                             size_t zoff) {
-    constexpr uint32_t id64 = tc::idesc_f16(128, 64, false, false);
-    constexpr uint32_t id16 = tc::idesc_f16(128, 16, false, false);
-    const uint64_t dA = tc::smem_desc(tc::smem_u32(gt), 2048, 128);
-    const uint64_t dOnes = tc::smem_desc(a_ones, 2048, 128);
-    const uint64_t dW0 = tc::smem_desc(a_w0, 1024, 128);
-    const uint64_t dWh = tc::smem_desc(a_wh, 1024, 128);
-    const uint64_t dWo = tc::smem_desc(a_wo, 256, 128);
-    const int q = wg & 3, half = wg >> 2;
-    const int row = 32 * q + lane;
-    tc::fence_proxy_async();                  // feature rows (generic) -> tensor core (async proxy)
-    named_bar(1 + g, kGroupWarps * 32);
-    if (wg == 0) {
-        tc::fence_after();
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) tc::mma_f16_elect(acc, dA + kk * 256, dW0 + kk * 128, id64, kk > 0);
-        tc::mma_f16_elect(acc, dOnes, dW0 + (D / 16) * 128, id64, 1);                  // bias
-        tc::commit_elect(bar);
-    }
-    for (int l = 0; l <= hidden; ++l) {
-        tc::mbar_wait(bar, phase);
-        phase ^= 1u;
-        tc::fence_after();
-        if (l < hidden) {
-            float v[32];
-            tc::ld32(acc, (uint32_t)(q * 32), (uint32_t)(32 * half), v);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                uint4 o;
-                o.x = pack_relu_half2(v[8 * k], v[8 * k + 1]);
-                o.y = pack_relu_half2(v[8 * k + 2], v[8 * k + 3]);
-                o.z = pack_relu_half2(v[8 * k + 4], v[8 * k + 5]);
-                o.w = pack_relu_half2(v[8 * k + 6], v[8 * k + 7]);
-                *reinterpret_cast<uint4*>(gt + (4 * half + k) * 2048 + row * 16) = o;
-            }
-            tc::fence_before();
-            tc::fence_proxy_async();
-            named_bar(1 + g, kGroupWarps * 32);
-            if (wg == 0) {
-                tc::fence_after();
-                const bool out = l + 1 == hidden;
-                const uint64_t dW = out ? dWo : dWh + (uint64_t)(l * 64 * kKgHid);
-                const uint32_t kg_units = out ? 16 : 64, id = out ? id16 : id64;   // K-group stride / 16 B
-#pragma unroll
-                for (int kk = 0; kk < 4; ++kk)
-                    tc::mma_f16_elect(acc, dA + kk * 256, dW + kk * 2 * kg_units, id, kk > 0);
-                tc::mma_f16_elect(acc, dOnes, dW + 8 * kg_units, id, 1);                    // bias
-                tc::commit_elect(bar);
-            }
-        } else {
-            if (half == 0) {
-                float v[16];
-                tc::ld16(acc, (uint32_t)(q * 32), 0u, v);
-                float* z = reinterpret_cast<float*>(zbase + per_warp * (size_t)(row >> 4) + zoff) + (row & 15) * 8;
-                reinterpret_cast<float4*>(z)[0] = make_float4(v[0], v[1], v[2], v[3]);
-                reinterpret_cast<float4*>(z)[1] = make_float4(v[4], v[5], v[6], v[7]);
-            }
-            tc::fence_before();
-            named_bar(1 + g, kGroupWarps * 32);   // z visible to the owning warps; accumulator free
-        }
-    }
-}
-
-// One launch processes every ray that intersects the cut (Q2-Q7).
-// Each warp owns kWarpQ ray slots and runs its own loop with no block-wide barrier:
-// (A) refill empty slots with the next rays of the global work list (one atomic per warp),
-// (B) compact the occupied slots, (C) fetch each ray's current leaf segment and its n
-// stratified sample points, (D) hash-grid encode them into the warp's feature rows (lanes =
-// (query, chunk parity)), (E) run the MLP on tensor cores (one m16 row block), (F) decode,
-// update the best hit, decide front-to-back termination and free finished slots after
-// writing the hit record.  Warps drift freely, so one warp's MLP or list refill overlaps
-// other warps' gathers.
-// Lanes below this one (a special register: nothing kept live across the query loop).
-__device__ __forceinline__ unsigned lanemask_lt() {
-    unsigned m;
-    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
-    return m;
-}
-
-template <int F, int D, bool kTc>
-__global__ void __launch_bounds__(kQueryWarps * 32, 1) k_query(QueryArgs a) {
+// One launch processes every ray that intersects the cut.  Each warp owns kWarpQ ray slots
+// and runs its own loop with no block-wide barrier: (A) refill, (B/C) compact + segment,
+// (D) encode into the warp's feature rows, (E) the MLP on mma.sync (one m16 row block,
+// activations in registers), (F) decode.  Warps drift freely, so one warp's MLP or list
+// refill overlaps other warps' gathers.  Selected with NBVH_QUERY_MLP=warp (A/B reference of
+// the warp-specialised kernel below).
+template <int F, int D>
+__global__ void __launch_bounds__(kQueryWarps * 32, 1) k_query_warp(QueryArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int NP = a.g.n_points;
-    const QuerySmemPlan plan(D, a.m.hidden, NP, kTc);
+    const QuerySmemPlan plan(D, a.m.hidden, NP);
     MlpSmem ms;
     ms.w0 = reinterpret_cast<__half*>(smem_raw + plan.w);
     ms.wh = ms.w0 + 64 * (D + 8);
@@ -521,301 +619,362 @@ __global__ void __launch_bounds__(kQueryWarps * 32, 1) k_query(QueryArgs a) {
     ms.b = reinterpret_cast<float*>(smem_raw + plan.bias);
     LevelSm* lv = reinterpret_cast<LevelSm*>(smem_raw + plan.lv);
     unsigned char* wbase = smem_raw + plan.warp0 + plan.per_warp * warp;
-    __half* feat = reinterpret_cast<__half*>(wbase + plan.feat);              // [kWarpQ][D+8] (!kTc)
+    __half* feat = reinterpret_cast<__half*>(wbase + plan.feat);              // [kWarpQ][D+8]
     float* zt = reinterpret_cast<float*>(wbase + plan.z);                     // [kWarpQ][8]
     float* xs = reinterpret_cast<float*>(wbase + plan.xs);                    // [NP*3][kWarpQ]
     WarpSlots& S = *reinterpret_cast<WarpSlots*>(wbase + plan.slots);
-    // kTc: 8-warp groups, group tile, mbarrier, TMEM columns
-    const int grp = warp / kGroupWarps, wg = warp % kGroupWarps;
-    unsigned char* gt = smem_raw + plan.gtile + (size_t)grp * tc_tile_kg(D) * 2048;
-    uint64_t* gbar = reinterpret_cast<uint64_t*>(smem_raw + plan.misc) + grp;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem_raw + plan.misc + 16);
-    int* gvote = reinterpret_cast<int*>(smem_raw + plan.misc + 32);           // [2 parities][2 groups][8]
-    uint32_t gphase = 0;
-
-    if constexpr (kTc) {
-        // weights in the K-major canonical layout (element (n, k) of W [N][K] at
-        // (k/8) * (Npad*16) + n*16 + (k%8)*2), the bias as two extra K columns (hi + lo fp16)
-        auto stage_w = [&](unsigned char* dst, const __half* src, const float* bias, int N, int K, int Npad) {
-            const int kg = K / 8 + 2;
-            for (int i = tid; i < Npad * kg; i += blockDim.x) {
-                const int n = i / kg, gk = i % kg;
-                uint4 v = make_uint4(0, 0, 0, 0);
-                if (n < N) {
-                    if (gk < K / 8) {
-                        v = *reinterpret_cast<const uint4*>(src + (int64_t)n * K + gk * 8);
-                    } else if (gk == K / 8) {
-                        const __half hi = __float2half_rn(bias[n]);
-                        const __half lo = __float2half_rn(bias[n] - __half2float(hi));
-                        v.x = (uint32_t)__half_as_ushort(hi) | ((uint32_t)__half_as_ushort(lo) << 16);
-                    }
-                }
-                *reinterpret_cast<uint4*>(dst + gk * (Npad * 16) + n * 16) = v;
-            }
-        };
-        const int H = a.m.hidden;
-        stage_w(smem_raw + plan.w0, a.m.W, a.m.b, 64, D, 64);
-        for (int l = 0; l < H - 1; ++l)
-            stage_w(smem_raw + plan.wh + (size_t)l * 64 * kKgHid * 16, a.m.W + 64 * D + (int64_t)l * 64 * 64,
-                    a.m.b + 64 * (l + 1), 64, 64, 64);
-        stage_w(smem_raw + plan.wo, a.m.W + 64 * D + (int64_t)(H - 1) * 64 * 64, a.m.b + 64 * H, 8, 64, 16);
-        for (int i = tid; i < 128; i += blockDim.x) {                      // bias K-step A columns
-            *reinterpret_cast<uint4*>(smem_raw + plan.ones + i * 16) = make_uint4(0x3C003C00u, 0u, 0u, 0u);
-            *reinterpret_cast<uint4*>(smem_raw + plan.ones + 2048 + i * 16) = make_uint4(0u, 0u, 0u, 0u);
-        }
-        if (tid < 2 * 2 * kGroupWarps) gvote[tid] = 1;
-        if (tid == 0) {
-            tc::mbar_init(reinterpret_cast<uint64_t*>(smem_raw + plan.misc), 1);
-            tc::mbar_init(reinterpret_cast<uint64_t*>(smem_raw + plan.misc) + 1, 1);
-            tc::fence_barrier_init();
-        }
-        if (warp == 0) tc::tmem_alloc<128>(tmem_slot);
-        tc::fence_proxy_async();
-        tc::fence_before();
-    } else {
-        stage_mlp(a.m, ms, tid, blockDim.x);
-    }
+    stage_mlp(a.m, ms, tid, blockDim.x);
     stage_levels(a.g, lv, tid);
     if (lane < kWarpQ) S.ray[lane] = -1;
-    __syncthreads();                          // the only block-wide barrier (kTc: + group barriers)
-    if constexpr (kTc) tc::fence_after();
-    const uint32_t tmem_acc = kTc ? *tmem_slot + (uint32_t)(grp * 64) : 0u;
-
+    __syncthreads();                          // the only block-wide barrier
     // work-list sizes and per-warp statistics live in shared memory (read on refills / written
-    // by one lane): kept out of the loop's 128 registers, which had spilled them to local memory
+    // by one lane): kept out of the loop's registers
     __shared__ int s_work[2];                 // n_long, total
-    // per warp: [0] queries evaluated, [1] loop iterations, [2] live rows this iteration,
-    // [3] work list exhausted (lane 0 writes; read back after the next __syncwarp)
-    __shared__ int s_stat[4 * 32];
-    int* ws = s_stat + 4 * warp;
+    __shared__ int s_stat[2 * 32];            // per warp: [0] queries evaluated, [1] loop iterations
+    __shared__ int s_exh[32];                 // per warp: work list exhausted
     if (lane == 0) {
         s_work[0] = *a.cnt_long;              // long rays first (k_traverse), then the rest
-        s_work[1] = s_work[0] + *a.cnt;       // rays with >= 1 intersected leaf (same values in every warp)
-        ws[0] = ws[1] = ws[2] = ws[3] = 0;
+        s_work[1] = s_work[0] + *a.cnt;       // rays with >= 1 intersected leaf
+        s_stat[2 * warp] = s_stat[2 * warp + 1] = 0;
+        s_exh[warp] = 0;
     }
     __syncwarp();
-    const uint32_t hmask = (1u << a.g.log2_T) - 1u;
-    const void* tab = a.g.table;
-    int iters = 0;                            // kTc: group vote parity
-
     while (true) {
-        // (A) refill empty slots from the global work list (consecutive rays per warp)
-        const bool empty = lane < kWarpQ && S.ray[lane] < 0;
-        const unsigned em = __ballot_sync(0xffffffffu, empty);
-        if (em && !ws[3]) {
-            const int ne = __popc(em);
-            int base = 0;
-            if (lane == 0) base = atomicAdd(a.next, ne);
-            base = __shfl_sync(0xffffffffu, base, 0);
-            const int total = s_work[1], n_long = s_work[0];
-            if (lane == 0) ws[3] = base + ne >= total;
-            const int i = base + __popc(em & lanemask_lt());
-            if (empty && i < total) {
-                const WorkRec* wr = i < n_long ? a.act_long + i : a.act + (i - n_long);
-                // read-once streams (work records, lists) are loaded evict-first so they do not
-                // push the hash-table lines out of L1
-                const float4 w0 = __ldcs(&wr->o), w1 = __ldcs(&wr->d), w2 = __ldcs(&wr->e0);
-                const int r = __float_as_int(w0.w), st = __float_as_int(w1.w);
-                S.te[lane] = w2.x;
-                S.tx[lane] = w2.y;
-                S.leaf[lane] = __float_as_int(w2.z);
-                S.fresh[lane] = 1;
-                NBVH_DCHECK(r >= 0 && r < a.n_rays && (st & 0xffff) >= 1 && (st & 0xffff) <= a.cap);
-                S.ray[lane] = r;
-                S.o[0][lane] = w0.x; S.o[1][lane] = w0.y; S.o[2][lane] = w0.z;
-                S.d[0][lane] = w1.x; S.d[1][lane] = w1.y; S.d[2][lane] = w1.z;
-                S.pos[lane] = 0;
-                S.base[lane] = 0;
-                S.nbuf[lane] = st & 0xffff;
-                S.more[lane] = st >> 16;
-                S.bt[lane] = __int_as_float(0x7f800000);
-                S.bte[lane] = 0.f;
-                S.bleaf[lane] = -1;
-                S.nq[lane] = 0;
-            }
-        }
-        __syncwarp();
-        // (B) compact the occupied slots; (C) current segment + sample points (C8)
-        const bool occ = lane < kWarpQ && S.ray[lane] >= 0;
-        const unsigned om = __ballot_sync(0xffffffffu, occ);
-        const int nv = __popc(om);
-        if constexpr (kTc) {
-            // the 8 warps of a group run the MLP together: the group leaves the loop once
-            // every one of its warps is drained (a drained warp keeps joining with no rows)
-            int* vote = gvote + ((iters & 1) * 2 + grp) * kGroupWarps;
-            if (lane == 0) vote[wg] = nv;
-            named_bar(1 + grp, kGroupWarps * 32);
-            int any = 0;
-#pragma unroll
-            for (int k = 0; k < kGroupWarps; ++k) any |= vote[k];
-            if (!any) break;
-        } else {
-            if (nv == 0) break;               // work list drained and every slot finished
-        }
-        if constexpr (kTc) ++iters;
+        slots_refill(a, S, lane, s_work[1], s_work[0], s_exh + warp);
+        const int nv = slots_segment(a, S, xs, lane, NP);
+        if (nv == 0) break;                   // work list drained and every slot finished
         if (lane == 0) {
-            ws[0] += nv;
-            ws[1] += 1;
-            ws[2] = nv;
+            s_stat[2 * warp] += nv;
+            s_stat[2 * warp + 1] += 1;
         }
-        if (occ) {
-            const int row = __popc(om & lanemask_lt());
-            S.act[row] = lane;
-            const int r = S.ray[lane];
-            NBVH_DCHECK(S.pos[lane] - S.base[lane] >= 0 && S.pos[lane] - S.base[lane] < S.nbuf[lane] &&
-                        S.nbuf[lane] <= kListK);
-            const int64_t li = (int64_t)(S.pos[lane] - S.base[lane]) * a.n_rays + r;
-            float te, tx;
-            if (S.fresh[lane]) {              // a new ray: entry 0 came with its work record
-                S.fresh[lane] = 0;
-                te = S.te[lane];
-                tx = S.tx[lane];
-            } else {
-                const float4 e = __ldcs(a.lst + li);
-                te = e.x;
-                tx = e.y;
-                S.leaf[lane] = __float_as_int(e.z);
-                S.te[lane] = te;
-                S.tx[lane] = tx;
-            }
-            const float o[3] = {S.o[0][lane], S.o[1][lane], S.o[2][lane]};
-            const float d[3] = {S.d[0][lane], S.d[1][lane], S.d[2][lane]};
-            for (int p = 0; p < NP; ++p) {
-                float x[3];
-                segment_point(a.g, o, d, te, tx, p, NP, nullptr, x);
-                xs[(p * 3 + 0) * kWarpQ + row] = x[0];
-                xs[(p * 3 + 1) * kWarpQ + row] = x[1];
-                xs[(p * 3 + 2) * kWarpQ + row] = x[2];
-            }
-        }
+        rows_encode<F>(a, lv, xs, nv, lane, NP, reinterpret_cast<unsigned char*>(feat), 16, (D + 8) * 2);
+        query_mlp_rows16<D>(ms, a.m.hidden, feat, 0, zt, lane);              // (E)
         __syncwarp();
-        // (D) encode.  kWarpQ = 16: lane -> row q = lane % 16; the two half-warps take sample
-        //     points of opposite parity at the same levels (neighbouring points of the same
-        //     rays: coherent lines).  kWarpQ = 32: lane = row, all chunks.
-        {
-            constexpr int kHalves = 32 / kWarpQ;
-            const int q = lane & (kWarpQ - 1), h = lane / kWarpQ;
-            const int cpp = (a.g.L * F) / 8;  // 16-byte chunks per sample point
-            if (q < ws[2]) {
-                for (int p = h; p < NP; p += kHalves) {
-                    const float* xp = xs + p * 3 * kWarpQ;
-                    const float x0 = xp[q], x1 = xp[kWarpQ + q], x2 = xp[2 * kWarpQ + q];
-                    for (int lc = 0; lc < cpp; ++lc) {
-                        const int c = p * cpp + lc;
-                        const uint4 f = encode_chunk_sm<F>(lv, tab, hmask, x0, x1, x2, lc * (8 / F), nullptr);
-                        if constexpr (kTc)
-                            *reinterpret_cast<uint4*>(gt + c * 2048 + (16 * wg + q) * 16) = f;
-                        else
-                            *reinterpret_cast<uint4*>(feat + q * (D + 8) + c * 8) = f;
-                    }
-                }
-            }
-        }
-        __syncwarp();
-        // (E) MLP on tensor cores: the warp's rows in m16 blocks (rows >= nv are ignored); kTc:
-        //     the group's 128 rows on tcgen05
-        if constexpr (kTc) {
-            mlp_group_tc<D>(grp, wg, lane, a.m.hidden, tmem_acc, gt, tc::smem_u32(smem_raw + plan.w0),
-                            tc::smem_u32(smem_raw + plan.wh), tc::smem_u32(smem_raw + plan.wo),
-                            tc::smem_u32(smem_raw + plan.ones), gbar, gphase,
-                            smem_raw + plan.warp0 + plan.per_warp * (size_t)(grp * kGroupWarps), plan.per_warp,
-                            plan.z);
-        } else {
-            query_mlp_rows16<D>(ms, a.m.hidden, feat, 0, zt, lane);
-            if (kWarpQ > 16 && ws[2] > 16) query_mlp_rows16<D>(ms, a.m.hidden, feat, 16, zt, lane);
-        }
-        __syncwarp();
-        // (F) decode, best hit, front-to-back termination
-        if (lane < ws[2]) {
-            const int s = S.act[lane];
-            const int r = S.ray[s];
-            const float* z = zt + lane * 8;
-            int pos = S.pos[s];
-            if (a.z_trace && pos < a.trace_cap) {
-                float4* dst = reinterpret_cast<float4*>(a.z_trace + ((int64_t)r * a.trace_cap + pos) * 8);
-                dst[0] = make_float4(z[0], z[1], z[2], z[3]);
-                dst[1] = make_float4(z[4], z[5], z[6], z[7]);
-            }
-            const int nq = S.nq[s] + 1;
-            const float te = S.te[s], tx = S.tx[s];
-            const int leaf = S.leaf[s];
-            float bt = S.bt[s];
-            int bleaf = S.bleaf[s];
-            const bool hit = z[0] < 0.0f;                                  // sigmoid(z) < 0.5 (C13)
-            if (hit) {
-                const float tl = sigmoid_f(z[1]);                          // local distance
-                const float t = __fadd_rn(te, __fmul_rn(tl, __fsub_rn(tx, te)));
-                const float bte = S.bte[s];
-                const bool better = bleaf < 0 || t < bt || (t == bt && (te < bte || (te == bte && leaf < bleaf)));
-                if (better) {
-                    bt = t;
-                    bleaf = leaf;
-                    S.bt[s] = t;
-                    S.bte[s] = te;
-                    S.bleaf[s] = leaf;
-                    float nn = __fsqrt_rn(__fadd_rn(__fadd_rn(__fmul_rn(z[2], z[2]), __fmul_rn(z[3], z[3])),
-                                                    __fmul_rn(z[4], z[4])));
-                    nn = fmaxf(nn, 1e-6f);
-#pragma unroll
-                    for (int k = 0; k < 3; ++k) {
-                        S.nrm[k][s] = __fdiv_rn(z[2 + k], nn);
-                        S.alb[k][s] = sigmoid_f(z[5 + k]);
-                    }
-                }
-            }
-            ++pos;
-            bool done = a.mode == 1 && hit;                                 // R1: first confident hit (C5)
-            if (!done) {
-                int base = S.base[s], nbuf = S.nbuf[s];
-                if (pos - base >= nbuf) {
-                    if (!S.more[s]) {
-                        done = true;                                         // every intersected leaf visited
-                    } else {
-                        // list exhausted, more leaves may remain: resume after the last key,
-                        // bounded by the best hit (C6)
-                        int more = 0;
-                        nbuf = refill_list(a.cut, a.rays, a.n_rays, a.cap, a.lst, a.ctr, r,
-                                           nbuf, bleaf >= 0 ? bt : __int_as_float(0x7f800000), &more);
-                        base = pos;
-                        S.base[s] = base;
-                        S.nbuf[s] = nbuf;
-                        S.more[s] = more;
-                        done = nbuf == 0;
-                    }
-                }
-                if (!done) {
-                    const float next_te = __ldcs(a.lst + (int64_t)(pos - base) * a.n_rays + r).x;
-                    done = bleaf >= 0 && next_te > bt;                     // front-to-back termination
-                }
-            }
-            S.pos[s] = pos;
-            S.nq[s] = nq;
-            if (done) {
-                // Q7: hit record; a miss keeps t = +inf and zero vectors
-                const bool h = bleaf >= 0;
-                a.out.hit[r] = h ? 1 : 0;
-                a.out.t[r] = h ? bt : __int_as_float(0x7f800000);
-#pragma unroll
-                for (int k = 0; k < 3; ++k) {
-                    a.out.normal[3 * (int64_t)r + k] = h ? S.nrm[k][s] : 0.f;
-                    a.out.albedo[3 * (int64_t)r + k] = h ? S.alb[k][s] : 0.f;
-                }
-                if (a.out.leaf) a.out.leaf[r] = bleaf;
-                if (a.out.n_queries) a.out.n_queries[r] = nq;
-                S.ray[s] = -1;
-            }
-        }
-        __syncwarp();
+        rows_decode(a, S, zt, nv, lane);
     }
     if (lane == 0) {
-        atomicAdd(&a.ctr->n_queries, (unsigned long long)ws[0]);
-        atomicMax(&a.ctr->max_iter, ws[1]);
+        atomicAdd(&a.ctr->n_queries, (unsigned long long)s_stat[2 * warp]);
+        atomicMax(&a.ctr->max_iter, s_stat[2 * warp + 1]);
     }
-    if constexpr (kTc) {
-        tc::fence_before();
-        __syncthreads();
-        if (warp == 0) tc::tmem_free<128>(*tmem_slot);
+}
+
+// ------------------------------------------------------------------ query kernel, tcgen05 MLP
+// Warp-specialised persistent query kernel (NBVH_QUERY_MLP=tc): kWsWorkers worker warps own
+// the ray slots -- two slot sets each -- and run refill / segment / encode / decode; one MLP
+// warpgroup (4 warps, one per TMEM lane quarter) runs the decoder MLP of 128-row tiles on
+// the 5th-generation tensor cores (tcgen05.mma, M = 128, fp32 accumulators in TMEM), so the
+// weights never pass through the LSU: they are read once per 128 rows by the tensor core
+// instead of once per 16 rows by ldmatrix.
+//
+// A worker encodes a set's (<= 16) rows into a 16-row block of the current feature tile
+// (blocks are claimed in sequence; tile = claim / 8 over a ring of kWsTiles tiles) and
+// arrives on the tile's `full` barrier, then turns to its other set; the MLP warpgroup
+// processes tiles in claim order: layer 0 from the feature tile (its commit also frees the
+// tile for the next generation), hidden layers through one activation tile (TMEM ->
+// ReLU + fp16 -> shared memory), the 8 outputs written straight into the owning set's z rows,
+// then one arrive on that set's `zr` barrier.  A worker decodes a set only after it has
+// encoded its other set, so the MLP latency is hidden behind the other set's gathers.
+// Drain: when every worker is idle (waiting for z or finished) and the current tile is only
+// partly claimed, the MLP warpgroup closes it (claims jump to the next tile, the missing
+// arrivals are made up) and processes it as is.
+// Registers: 20 warps share the CTA's 640 x 96 registers; setmaxnreg moves them from the MLP
+// warpgroup (56) to the workers (104).  Measured on the 1080p frame (profiles/NOTES.md r2):
+// 1.116 ms vs 0.995 ms for k_query_warp -- the LSU data pipe drops from 81% to 60% busy
+// (no weight fragments), but the gathers are latency-bound and the workers have fewer
+// registers (spills) and wait for tiles; 12 workers at 128 registers: 1.158-1.22 ms.
+constexpr int kWsWorkers = 16;                            // 4 warpgroups
+constexpr int kWsWorkerRegs = 104, kWsMlpRegs = 56;        // setmaxnreg split of the CTA's 640 x 96 registers
+constexpr int kWsTiles = 3;                                // at most; WsPlan::nt fits the smem limit
+constexpr int kWsBlk = 8;                                  // 16-row blocks per 128-row tile
+constexpr int kKgHid = 64 / 8 + 2;                         // K-groups of a hidden W (+ bias)
+
+struct WsCtl {
+    uint64_t full[kWsTiles];           // kWsBlk arrivals per tile generation (workers)
+    uint64_t freeb[kWsTiles];          // layer-0 MMAs of the generation complete (tcgen05.commit)
+    uint64_t mma;                      // MMA chain steps of the MLP warpgroup
+    uint64_t zr[2 * kWsWorkers];       // z of a set's block written (one arrive per block)
+    int seq;                           // block claims so far
+    int idle;                          // workers waiting for z or finished
+    int exited;                        // workers finished
+    int cmd;                           // MLP warpgroup: 1 process the tile, 2 exit
+    int owner[kWsTiles][kWsBlk];       // 2 * worker + set of each block; -1: none
+    int nrows[kWsTiles][kWsBlk];       // valid rows of each block
+    int work[2];                       // n_long, total
+    int exh[kWsWorkers];               // per worker: work list exhausted
+    int stat[kWsWorkers][2];           // per worker: queries, slot-set iterations
+    uint32_t tmem;
+};
+
+struct WsPlan {
+    size_t w0, wh, wo, ones, lv, ctl, tiles, htile, xs, sets, per_set, z, total;
+    int tile_bytes, nt;
+    __host__ __device__ WsPlan(int d_in, int hidden, int n_points) {
+        w0 = 0;
+        wh = w0 + (size_t)64 * (d_in / 8 + 2) * 16;
+        wo = wh + (size_t)(hidden - 1) * 64 * kKgHid * 16;
+        ones = wo + (size_t)16 * kKgHid * 16;
+        lv = ones + 2 * 128 * 16;
+        ctl = lv + align16(sizeof(LevelSm) * kMaxLevels);
+        tiles = align128(ctl + sizeof(WsCtl));
+        tile_bytes = (d_in / 8) * 2048;                        // [D/8 K-groups][128 rows][16 B]
+        const size_t xs_bytes = align16((size_t)kWarpQ * n_points * 3 * 4);   // per worker (sets take turns)
+        z = align16(sizeof(WarpSlots));                         // offset within a set region
+        per_set = z + align16((size_t)kWarpQ * 8 * 4);
+        const size_t rest = 8 * 2048 + xs_bytes * kWsWorkers + per_set * 2 * kWsWorkers;
+        nt = kWsTiles;                                          // as many tiles as fit (>= 2)
+        while (nt > 2 && tiles + (size_t)nt * tile_bytes + rest > 227 * 1024) --nt;
+        htile = tiles + (size_t)nt * tile_bytes;                // hidden activations [8][128][16 B]
+        xs = htile + 8 * 2048;
+        sets = xs + xs_bytes * kWsWorkers;
+        total = sets + per_set * 2 * kWsWorkers;
     }
+};
+
+template <int F, int D>
+__global__ void __launch_bounds__((kWsWorkers + 4) * 32, 1) k_query_ws(QueryArgs a) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int NP = a.g.n_points, H = a.m.hidden;
+    const WsPlan plan(D, H, NP);
+    LevelSm* lv = reinterpret_cast<LevelSm*>(smem_raw + plan.lv);
+    WsCtl& C = *reinterpret_cast<WsCtl*>(smem_raw + plan.ctl);
+    unsigned char* tiles = smem_raw + plan.tiles;
+    unsigned char* htile = smem_raw + plan.htile;
+    auto set_base = [&](int owner) { return smem_raw + plan.sets + plan.per_set * (size_t)owner; };
+
+    // ---- staging: weights in the K-major canonical (core-matrix) layout, element (n, k) of
+    // W [N][K] at (k/8) * (Npad*16) + n*16 + (k%8)*2, the bias as two extra K columns (hi + lo
+    // fp16) multiplied by a ones tile in an extra K step
+    auto stage_w = [&](unsigned char* dst, const __half* src, const float* bias, int N, int K, int Npad) {
+        const int kg = K / 8 + 2;
+        for (int i = tid; i < Npad * kg; i += blockDim.x) {
+            const int n = i / kg, gk = i % kg;
+            uint4 v = make_uint4(0, 0, 0, 0);
+            if (n < N) {
+                if (gk < K / 8) {
+                    v = *reinterpret_cast<const uint4*>(src + (int64_t)n * K + gk * 8);
+                } else if (gk == K / 8) {
+                    const __half hi = __float2half_rn(bias[n]);
+                    const __half lo = __float2half_rn(bias[n] - __half2float(hi));
+                    v.x = (uint32_t)__half_as_ushort(hi) | ((uint32_t)__half_as_ushort(lo) << 16);
+                }
+            }
+            *reinterpret_cast<uint4*>(dst + gk * (Npad * 16) + n * 16) = v;
+        }
+    };
+    stage_w(smem_raw + plan.w0, a.m.W, a.m.b, 64, D, 64);
+    for (int l = 0; l < H - 1; ++l)
+        stage_w(smem_raw + plan.wh + (size_t)l * 64 * kKgHid * 16, a.m.W + 64 * D + (int64_t)l * 64 * 64,
+                a.m.b + 64 * (l + 1), 64, 64, 64);
+    stage_w(smem_raw + plan.wo, a.m.W + 64 * D + (int64_t)(H - 1) * 64 * 64, a.m.b + 64 * H, 8, 64, 16);
+    for (int i = tid; i < 128; i += blockDim.x) {                           // bias K-step A columns
+        *reinterpret_cast<uint4*>(smem_raw + plan.ones + i * 16) = make_uint4(0x3C003C00u, 0u, 0u, 0u);
+        *reinterpret_cast<uint4*>(smem_raw + plan.ones + 2048 + i * 16) = make_uint4(0u, 0u, 0u, 0u);
+    }
+    stage_levels(a.g, lv, tid);
+    if (warp < kWsWorkers && lane < kWarpQ) {
+        reinterpret_cast<WarpSlots*>(set_base(2 * warp))->ray[lane] = -1;
+        reinterpret_cast<WarpSlots*>(set_base(2 * warp + 1))->ray[lane] = -1;
+    }
+    if (tid == 0) {
+        for (int t = 0; t < plan.nt; ++t) {
+            tc::mbar_init(&C.full[t], kWsBlk);
+            tc::mbar_init(&C.freeb[t], 1);
+        }
+        tc::mbar_init(&C.mma, 1);
+        for (int i = 0; i < 2 * kWsWorkers; ++i) tc::mbar_init(&C.zr[i], 1);
+        C.seq = 0;
+        C.idle = 0;
+        C.exited = 0;
+        C.cmd = 0;
+        C.work[0] = *a.cnt_long;              // long rays first (k_traverse), then the rest
+        C.work[1] = C.work[0] + *a.cnt;       // rays with >= 1 intersected leaf
+        tc::fence_barrier_init();
+    }
+    if (tid < kWsWorkers) {
+        C.exh[tid] = 0;
+        C.stat[tid][0] = C.stat[tid][1] = 0;
+    }
+    if (warp == kWsWorkers) tc::tmem_alloc<64>(&C.tmem);
+    tc::fence_proxy_async();                  // staged weights -> tensor core (async proxy)
+    tc::fence_before();
+    __syncthreads();                          // the only block-wide barrier before the teardown
+    tc::fence_after();
+
+    if (warp < kWsWorkers) {
+        // ================================================================ worker warps
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kWsWorkerRegs));
+        // loop state in scalars (a runtime-indexed array would live in local memory): bit s of
+        // zph = parity of set s's next z wait, of pend = set s has a block in flight; nv_pk =
+        // rows of set 0 | rows of set 1 << 8
+        uint32_t zph = 0, pend = 0, nv_pk = 0;
+        int s = 0;
+        float* xs = reinterpret_cast<float*>(smem_raw + plan.xs + (size_t)warp * (plan.sets - plan.xs) / kWsWorkers);
+        while (true) {
+            unsigned char* sb = set_base(2 * warp + s);
+            WarpSlots& S = *reinterpret_cast<WarpSlots*>(sb);
+            float* zt = reinterpret_cast<float*>(sb + plan.z);
+            if (pend & (1u << s)) {           // (F) this set's z: wait, then decode
+                if (lane == 0) atomicAdd(&C.idle, 1);
+                tc::mbar_wait(&C.zr[2 * warp + s], (zph >> s) & 1u);
+                if (lane == 0) atomicSub(&C.idle, 1);
+                zph ^= 1u << s;
+                pend &= ~(1u << s);
+                rows_decode(a, S, zt, (int)((nv_pk >> (8 * s)) & 0xffu), lane);
+            }
+            slots_refill(a, S, lane, C.work[1], C.work[0], &C.exh[warp]);
+            const int nv = slots_segment(a, S, xs, lane, NP);
+            nv_pk = (nv_pk & ~(0xffu << (8 * s))) | ((uint32_t)nv << (8 * s));
+            if (nv == 0) {
+                if (!(pend & (1u << (s ^ 1)))) break;   // both sets drained: done
+                s ^= 1;
+                continue;
+            }
+            if (lane == 0) {
+                C.stat[warp][0] += nv;
+                C.stat[warp][1] += 1;
+            }
+            // claim a 16-row block of the current tile; wait until the tile's previous
+            // generation has been read by its layer-0 MMAs
+            int q = 0;
+            if (lane == 0) q = atomicAdd(&C.seq, 1);
+            q = __shfl_sync(0xffffffffu, q, 0);
+            const int tl = (q / kWsBlk) % plan.nt, gen = q / (kWsBlk * plan.nt), blk = q % kWsBlk;
+            if (gen > 0) tc::mbar_wait(&C.freeb[tl], (uint32_t)(gen - 1) & 1u);
+            // (D) encode straight into the tile: row blk*16 + q, K-major canonical layout
+            rows_encode<F>(a, lv, xs, nv, lane, NP, tiles + (size_t)tl * plan.tile_bytes + blk * 16 * 16, 2048, 16);
+            if (lane == 0) {
+                C.owner[tl][blk] = 2 * warp + s;
+                C.nrows[tl][blk] = nv;
+            }
+            tc::fence_proxy_async();          // feature rows (generic) -> tensor core (async proxy)
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&C.full[tl]);
+            pend |= 1u << s;
+            s ^= 1;
+        }
+        if (lane == 0) {
+            atomicAdd(&C.exited, 1);
+            atomicAdd(&C.idle, 1);
+            atomicAdd(&a.ctr->n_queries, (unsigned long long)C.stat[warp][0]);
+            atomicMax(&a.ctr->max_iter, C.stat[warp][1]);
+        }
+    } else {
+        // ================================================================ MLP warpgroup
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kWsMlpRegs));
+        const int mw = warp - kWsWorkers;     // == warp % 4: the TMEM lane quarter it may access
+        const uint32_t acc = C.tmem;
+        constexpr uint32_t id64 = tc::idesc_f16(128, 64, false, false);
+        constexpr uint32_t id16 = tc::idesc_f16(128, 16, false, false);
+        const uint64_t dOnes = tc::smem_desc(tc::smem_u32(smem_raw + plan.ones), 2048, 128);
+        const uint64_t dW0 = tc::smem_desc(tc::smem_u32(smem_raw + plan.w0), 1024, 128);
+        const uint64_t dWh = tc::smem_desc(tc::smem_u32(smem_raw + plan.wh), 1024, 128);
+        const uint64_t dWo = tc::smem_desc(tc::smem_u32(smem_raw + plan.wo), 256, 128);
+        const uint64_t dH = tc::smem_desc(tc::smem_u32(htile), 2048, 128);
+        const int row = 32 * mw + lane;
+        uint32_t mph = 0;
+        int n_tiles = 0, n_rows = 0;          // statistics (warp 0, lane 0)
+        for (int T = 0;; ++T) {
+            const int tl = T % plan.nt, gen = T / plan.nt;
+            if (mw == 0) {
+                int cmd = 1;
+                if (lane == 0) {
+                    const int base = T * kWsBlk;
+                    while (!tc::mbar_test(&C.full[tl], (uint32_t)gen & 1u)) {
+                        if (*(volatile int*)&C.idle < kWsWorkers) continue;
+                        const int sq = *(volatile int*)&C.seq;
+                        if (sq <= base) {
+                            if (*(volatile int*)&C.exited == kWsWorkers) { cmd = 2; break; }
+                        } else if (sq < base + kWsBlk && atomicCAS(&C.seq, sq, base + kWsBlk) == sq) {
+                            // close the partly claimed tile: no block after sq - base is used
+                            for (int b = sq - base; b < kWsBlk; ++b) C.owner[tl][b] = -1;
+                            __threadfence_block();
+                            for (int b = sq - base; b < kWsBlk; ++b) tc::mbar_arrive(&C.full[tl]);
+                        }
+                    }
+                    C.cmd = cmd;
+                }
+                __syncwarp();
+            }
+            named_bar(1, 128);
+            if (*(volatile int*)&C.cmd == 2) break;
+            // layer 0 from the feature tile; its completion also frees the tile
+            if (mw == 0) {
+                tc::fence_after();
+                const uint64_t dA = tc::smem_desc(tc::smem_u32(tiles + (size_t)tl * plan.tile_bytes), 2048, 128);
+#pragma unroll
+                for (int kk = 0; kk < D / 16; ++kk) tc::mma_f16_elect(acc, dA + kk * 256, dW0 + kk * 128, id64, kk > 0);
+                tc::mma_f16_elect(acc, dOnes, dW0 + (D / 16) * 128, id64, 1);                 // bias
+                tc::commit_elect(&C.freeb[tl]);
+                tc::commit_elect(&C.mma);
+            }
+            for (int l = 0; l < H; ++l) {
+                tc::mbar_wait(&C.mma, mph);
+                mph ^= 1u;
+                tc::fence_after();
+#pragma unroll
+                for (int half = 0; half < 2; ++half) {                // 64 columns: ReLU + fp16 -> H tile
+                    float v[32];
+                    tc::ld32(acc, (uint32_t)(32 * mw), (uint32_t)(32 * half), v);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        uint4 o;
+                        o.x = pack_relu_half2(v[8 * k], v[8 * k + 1]);
+                        o.y = pack_relu_half2(v[8 * k + 2], v[8 * k + 3]);
+                        o.z = pack_relu_half2(v[8 * k + 4], v[8 * k + 5]);
+                        o.w = pack_relu_half2(v[8 * k + 6], v[8 * k + 7]);
+                        *reinterpret_cast<uint4*>(htile + (4 * half + k) * 2048 + row * 16) = o;
+                    }
+                }
+                tc::fence_proxy_async();
+                tc::fence_before();
+                named_bar(1, 128);
+                if (mw == 0) {
+                    tc::fence_after();
+                    const bool out = l + 1 == H;
+                    const uint64_t dW = out ? dWo : dWh + (uint64_t)(l * 64 * kKgHid);
+                    const uint32_t kgu = out ? 16 : 64, id = out ? id16 : id64;   // K-group stride / 16 B
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) tc::mma_f16_elect(acc, dH + kk * 256, dW + kk * 2 * kgu, id, kk > 0);
+                    tc::mma_f16_elect(acc, dOnes, dW + 8 * kgu, id, 1);                            // bias
+                    tc::commit_elect(&C.mma);
+                }
+            }
+            tc::mbar_wait(&C.mma, mph);
+            mph ^= 1u;
+            tc::fence_after();
+            {   // the 8 outputs of row `row` -> the owning set's z rows
+                float v[16];
+                tc::ld16(acc, (uint32_t)(32 * mw), 0u, v);
+                const int own = C.owner[tl][row >> 4];
+                if (own >= 0) {
+                    float4* z = reinterpret_cast<float4*>(set_base(own) + plan.z) + (row & 15) * 2;
+                    z[0] = make_float4(v[0], v[1], v[2], v[3]);
+                    z[1] = make_float4(v[4], v[5], v[6], v[7]);
+                }
+            }
+            tc::fence_before();               // accumulator reads done before the next tile's MMAs
+            named_bar(1, 128);
+            if (mw == 0 && lane < kWsBlk) {
+                const int own = C.owner[tl][lane];
+                int nr = own >= 0 ? C.nrows[tl][lane] : 0;
+#pragma unroll
+                for (int o = 4; o > 0; o >>= 1) nr += __shfl_xor_sync(0xffu, nr, o);
+                if (lane == 0) {
+                    ++n_tiles;
+                    n_rows += nr;
+                }
+                if (own >= 0) tc::mbar_arrive(&C.zr[own]);
+            }
+        }
+        if (mw == 0 && lane == 0) {
+            atomicAdd(&a.ctr->mlp_tiles, n_tiles);
+            atomicAdd(&a.ctr->mlp_rows, n_rows);
+        }
+    }
+    tc::fence_before();
+    __syncthreads();
+    if (warp == kWsWorkers) tc::tmem_free<64>(C.tmem);
 }
 
 // ------------------------------------------------------------------ debug: encode points
@@ -891,50 +1050,48 @@ static int resident_blocks(Kern k, int threads, size_t smem) {
     return (per_sm > 0 ? per_sm : 1) * sms;
 }
 
-// Persistent grid: one CTA of kQueryWarps warps per SM.
-// The MLP of k_query: the per-warp mma.sync MLP by default; NBVH_QUERY_MLP=tc selects the
-// 8-warp-group tcgen05 MLP (parity-tested, but 1451 vs 1648 Mrays/s on the 1080p frame:
-// every warp of a group waits through the group's 4-layer MMA/epilogue chain, which costs
-// more per iteration than a warp's own mma.sync chain in this latency-bound kernel).  Read
-// per launch so tests can switch it.
-static bool query_mlp_tc() {
+// Default: the per-warp mma.sync kernel (k_query_warp, 0.995 ms on the 1080p frame);
+// NBVH_QUERY_MLP=tc selects the warp-specialised tcgen05 kernel (k_query_ws, 1.116 ms:
+// profiles/NOTES.md r2).  Read per launch so tests can switch it.
+static bool query_mlp_warp() {
     const char* ev = std::getenv("NBVH_QUERY_MLP");
-    return ev && ev[0] == 't';
+    return !(ev && ev[0] == 't');
 }
 
-template <int F, int D, bool kTc>
-static cudaError_t launch_query_tt(const QueryArgs& a, int64_t max_work, cudaStream_t s, const QuerySmemPlan& plan) {
-    const size_t smem = plan.total;
+template <int kKind, typename Kern>             // kKind: one occupancy cache per kernel family
+static cudaError_t launch_persistent(Kern k, int threads, size_t smem, int64_t max_work, int rows_per_cta,
+                                     const QueryArgs& a, cudaStream_t s, int hidden, int n_points) {
     // The dynamic shared-memory opt-in is per function, not per shape: set it before every
     // launch (cheap), so a smaller shape launched in between cannot leave it too low.  The
     // occupancy query is cached per (device, hidden, n_points).
-    cudaError_t e = cudaFuncSetAttribute(k_query<F, D, kTc>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int dev = 0;
     cudaGetDevice(&dev);
     constexpr int kDevs = 16;
-    static int cached[kDevs][kMaxHidden + 1][9] = {};
+    static int cached[kDevs][kMaxHidden + 1][9][2] = {};     // [.][.][.][F == 4]: per instantiation
     int fallback = 0;
-    int& grid_c = dev < kDevs ? cached[dev][a.m.hidden][a.g.n_points < 9 ? a.g.n_points : 8] : fallback;
-    if (!grid_c) grid_c = resident_blocks(k_query<F, D, kTc>, plan.warps * 32, smem);
+    int& grid_c = dev < kDevs ? cached[dev][hidden][n_points < 9 ? n_points : 8][a.g.F == 4] : fallback;
+    if (!grid_c) grid_c = resident_blocks(k, threads, smem);
     int grid = grid_c;
-    if (!kTc) {                               // kTc: every CTA needs both groups, keep the full grid
-        const int64_t need = (max_work + plan.warps * kWarpQ - 1) / (plan.warps * kWarpQ);
-        if (need < grid) grid = (int)(need > 0 ? need : 1);
-    }
-    k_query<F, D, kTc><<<grid, plan.warps * 32, smem, s>>>(a);
+    const int64_t need = (max_work + rows_per_cta - 1) / rows_per_cta;
+    if (need < grid) grid = (int)(need > 0 ? need : 1);
+    k<<<grid, threads, smem, s>>>(a);
     return cudaGetLastError();
 }
 
 template <int F, int D>
 static cudaError_t launch_query_t(const QueryArgs& a, int64_t max_work, cudaStream_t s) {
-    if (query_mlp_tc()) {
-        const QuerySmemPlan tp(D, a.m.hidden, a.g.n_points, true);
-        if (tp.warps == kQueryWarps) return launch_query_tt<F, D, true>(a, max_work, s, tp);
+    if (!query_mlp_warp()) {
+        const WsPlan plan(D, a.m.hidden, a.g.n_points);
+        if (plan.total <= 227 * 1024)
+            return launch_persistent<0>(k_query_ws<F, D>, (kWsWorkers + 4) * 32, plan.total, max_work,
+                                     2 * kWsWorkers * kWarpQ, a, s, a.m.hidden, a.g.n_points);
     }
     const QuerySmemPlan plan(D, a.m.hidden, a.g.n_points);
     if (plan.warps < 1) return cudaErrorInvalidValue;
-    return launch_query_tt<F, D, false>(a, max_work, s, plan);
+    return launch_persistent<1>(k_query_warp<F, D>, plan.warps * 32, plan.total, max_work, plan.warps * kWarpQ, a, s,
+                             a.m.hidden, a.g.n_points);
 }
 
 cudaError_t launch_query(const QueryArgs& a, int64_t max_work, cudaStream_t s) {

@@ -30,7 +30,8 @@ struct QueryCounters {
     int32_t next;                 // work-list cursor of the persistent query kernel
     int32_t max_iter;             // slot iterations of the busiest CTA
     int32_t cnt_long;             // rays queued on the "long" work list (many leaves: scheduled first)
-    int32_t pad[2];
+    int32_t mlp_tiles;            // k_query_ws: MLP tiles processed
+    int32_t mlp_rows;             // k_query_ws: valid rows in them
     unsigned long long n_queries; // neural queries (ray, leaf) evaluated
 };
 

@@ -42,7 +42,8 @@ __global__ void __launch_bounds__(256) k_gather_probe(const uint32_t* __restrict
 
 // Random fp32 reductions into an L2-resident table (the T7 hash-grid scatter's roofline,
 // "measured L2 atomic peak"): kVec = 1 -> red.global.add.f32, 2 ->
-// red.global.add.v2.f32 (8-byte aligned pairs, what k_train_bwd issues for F = 2).
+// red.global.add.v2.f32 (8-byte aligned pairs, what k_train_bwd issues for F = 2), 4 ->
+// red.global.add.v4.f32 (16-byte aligned quads: two F = 2 entries).
 template <int kVec>
 __global__ void __launch_bounds__(256) k_atomic_probe(float* __restrict__ tab, uint32_t mask, int64_t per_thread,
                                                       uint32_t seed) {
@@ -58,8 +59,12 @@ __global__ void __launch_bounds__(256) k_atomic_probe(float* __restrict__ tab, u
             const uint32_t e = (st[c] >> 7) & mask;
             if constexpr (kVec == 1)
                 asm volatile("red.global.add.f32 [%0], %1;" ::"l"(tab + e), "f"(1.0f) : "memory");
-            else
+            else if constexpr (kVec == 2)
                 asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(tab + 2ull * e), "f"(1.0f), "f"(1.0f)
+                             : "memory");
+            else
+                asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(tab + 4ull * e), "f"(1.0f),
+                             "f"(1.0f), "f"(1.0f), "f"(1.0f)
                              : "memory");
         }
     }
@@ -71,7 +76,7 @@ using namespace nbvh;
 
 extern "C" nbvh_status nbvh_atomic_probe(float* d_table, int64_t table_bytes, int32_t vec, int64_t n_ops,
                                          uint32_t seed, int64_t* n_done, void* stream) {
-    if (!d_table || (vec != 1 && vec != 2) || n_ops <= 0 || (reinterpret_cast<uintptr_t>(d_table) & 7))
+    if (!d_table || (vec != 1 && vec != 2 && vec != 4) || n_ops <= 0 || (reinterpret_cast<uintptr_t>(d_table) & 15))
         return NBVH_EINVAL;
     const int64_t n_entries = table_bytes / (4 * vec);
     if (n_entries < 1 || (n_entries & (n_entries - 1))) return NBVH_EINVAL;
@@ -85,8 +90,10 @@ extern "C" nbvh_status nbvh_atomic_probe(float* d_table, int64_t table_bytes, in
     cudaStream_t s = (cudaStream_t)stream;
     if (vec == 1)
         k_atomic_probe<1><<<sms * 8, 256, 0, s>>>(d_table, mask, per_thread, seed);
-    else
+    else if (vec == 2)
         k_atomic_probe<2><<<sms * 8, 256, 0, s>>>(d_table, mask, per_thread, seed);
+    else
+        k_atomic_probe<4><<<sms * 8, 256, 0, s>>>(d_table, mask, per_thread, seed);
     if (n_done) *n_done = per_thread * threads;
     return cudaGetLastError() == cudaSuccess ? NBVH_OK : NBVH_ECUDA;
 }

@@ -379,7 +379,7 @@ def test_atomic_probe_counts_every_reduction():
     """nbvh_atomic_probe (the §8(d) scatter roofline): the table's sum equals the number of
     reductions issued (each adds 1 per component), and bad arguments are rejected."""
     from paper_2405_16237_b200.nbvh import atomic_probe, NbvhError
-    for vec in (1, 2):
+    for vec in (1, 2, 4):
         tab = torch.zeros(1 << 16, dtype=torch.float32, device="cuda")
         n = atomic_probe(tab, vec, 1 << 20)
         torch.cuda.synchronize()
@@ -428,25 +428,51 @@ def test_query_degenerate_rays_and_list_extremes(orc, list_cap):
     assert g["hit"].sum() > 10 and g["n_queries"].sum() > 300
 
 
-def test_query_tcgen05_group_mlp_variant(orc, monkeypatch):
-    """NBVH_QUERY_MLP=tc: k_query with the decoder MLP of each 8-warp group's 128 rows on
-    tcgen05 (TMEM accumulators, group barriers) instead of per-warp mma.sync — same parity
-    checks (logic replay exact, double oracle within tolerance) on the tiny scene, and the
-    1080p frame at full size against the default variant (identical decisions on decided rays)."""
-    monkeypatch.setenv("NBVH_QUERY_MLP", "tc")
-    ctx, sc, tab, layers = _mk_ctx("tiny")
-    _check_query(orc, ctx, tab, layers, _rays_tiny())
+def test_query_kernel_variants(orc, monkeypatch):
+    """The two query kernels: the default per-warp one (mma.sync MLP of each warp's 16 rows)
+    and NBVH_QUERY_MLP=tc, the warp-specialised one (the decoder MLP of 128-row tiles on
+    tcgen05 in an MLP warpgroup, worker warps with two slot sets).  Each passes the parity
+    checks (logic replay exact, double oracle within tolerance) on the tiny scene; on the 1080p
+    frame at full size they agree on every decision except rays whose z differs by fp32
+    summation order."""
+    for variant in ("tc", "warp"):
+        monkeypatch.setenv("NBVH_QUERY_MLP", variant)
+        ctx, sc, tab, layers = _mk_ctx("tiny")
+        _check_query(orc, ctx, tab, layers, _rays_tiny())
     ctx2, sc2, tab2, layers2 = _mk_ctx("1080p", table_seed=9, seed=6, list_cap=12)
     c = synth.CONFIGS["1080p"]
     rays = torch.from_numpy(synth.camera_rays(*c["res"], c["eye"], vfov_deg=c["vfov"])).cuda()
     ctx2.reserve(rays.shape[0])
+    monkeypatch.setenv("NBVH_QUERY_MLP", "tc")
     t = {k: v.cpu().numpy() for k, v in ctx2.query(rays).items()}
-    monkeypatch.setenv("NBVH_QUERY_MLP", "mma")
+    st = ctx2.query_stats()
+    assert st["n_mlp_tiles"] > 0 and st["n_mlp_rows"] == st["n_queries"]        # every query on tcgen05
+    monkeypatch.setenv("NBVH_QUERY_MLP", "warp")
     m = {k: v.cpu().numpy() for k, v in ctx2.query(rays).items()}
-    # the two MLPs differ only in fp32 summation order: decisions flip on a few near-tie rays
+    assert ctx2.query_stats()["n_mlp_tiles"] == 0
     assert (t["hit"] != m["hit"]).mean() < 1e-3 and (t["leaf"] != m["leaf"]).mean() < 2e-3
     same = (t["hit"] == 1) & (m["hit"] == 1) & (t["leaf"] == m["leaf"])
     assert np.abs(t["t"][same] - m["t"][same]).max() < 1e-2
+
+
+def test_query_ws_drain_and_partial_tiles(orc, monkeypatch):
+    """The warp-specialised kernel's drain path: ray counts that leave partly claimed feature
+    tiles (1, 7, 17, 129, 1000 rays, fewer rays than worker slots) finish and match the
+    replay of their own z trace exactly."""
+    monkeypatch.setenv("NBVH_QUERY_MLP", "tc")
+    ctx, sc, tab, layers = _mk_ctx("tiny")
+    base = _rays_tiny(1000)
+    for n in (1, 7, 17, 129, 1000):
+        rays = base[:n]
+        cut = ctx.cut(0)
+        out, zt = ctx.debug_query_trace(torch.from_numpy(rays).cuda(), 32)
+        torch.cuda.synchronize()
+        g = {k: v.cpu().numpy() for k, v in out.items()}
+        rep = orc.replay(cut["leaf_lo"], cut["leaf_hi"], rays, zt.cpu().numpy())
+        assert rep["missing"] == 0
+        assert np.array_equal(g["hit"], rep["hit"]) and np.array_equal(g["leaf"], rep["leaf"])
+        assert np.array_equal(g["n_queries"], rep["nq"])
+        assert ctx.query_stats()["n_mlp_rows"] == int(g["n_queries"].sum())
 
 
 def test_query_host_path_first_hit_mode_and_lod(monkeypatch):

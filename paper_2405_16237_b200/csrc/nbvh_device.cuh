@@ -462,11 +462,11 @@ __device__ __forceinline__ float cell_coord(float s, float tops, uint32_t& i) {
 // Cell of one level from the shared-memory level record: corner indices within the level
 // and trilinear weights (same arithmetic as encode_chunk_sm).  Used by the training
 // backward scatter.
+// (i0, i1, i2) receives the cell's integer coordinates.
 __device__ __forceinline__ void level_cell_sm(const LevelSm& P, uint32_t hmask, float x0, float x1, float x2,
-                                              Cell& c) {
+                                              Cell& c, uint32_t& i0, uint32_t& i1, uint32_t& i2) {
     const float s0 = __fmul_rn(x0, P.resf), s1 = __fmul_rn(x1, P.resf), s2 = __fmul_rn(x2, P.resf);
     const float tops = __fadd_rn(P.resf, 8388607.0f);       // 2^23 + N - 1 (exact)
-    uint32_t i0, i1, i2;
     const float c0 = cell_coord(s0, tops, i0), c1 = cell_coord(s1, tops, i1), c2 = cell_coord(s2, tops, i2);
     const float f0 = __fsub_rn(s0, c0), f1 = __fsub_rn(s1, c1), f2 = __fsub_rn(s2, c2);
     if (P.n1) {   // canonical dense vertex index (C2)
@@ -483,6 +483,11 @@ __device__ __forceinline__ void level_cell_sm(const LevelSm& P, uint32_t hmask, 
     const float wx[2] = {1.0f - f0, f0}, wy[2] = {1.0f - f1, f1}, wz[2] = {1.0f - f2, f2};
 #pragma unroll
     for (int k = 0; k < 8; ++k) c.w[k] = wx[k & 1] * wy[(k >> 1) & 1] * wz[(k >> 2) & 1];
+}
+__device__ __forceinline__ void level_cell_sm(const LevelSm& P, uint32_t hmask, float x0, float x1, float x2,
+                                              Cell& c) {
+    uint32_t i0, i1, i2;
+    level_cell_sm(P, hmask, x0, x1, x2, c, i0, i1, i2);
 }
 
 // In-flight state of one 16-byte chunk: the gathered corner entries and the cell fractions.

@@ -32,6 +32,11 @@ struct TrainWork {
     __half* Dl = nullptr;
     float* dZ = nullptr;
     float* Z = nullptr;              // [cap][8] raw z, allocated only while parity capture is on
+    float* gx = nullptr;             // [cap][D] dL/dx (bwd -> scatter)
+    float* sc_dense = nullptr;       // T7 scratch: cell-packed dense levels
+    float* sc_hash = nullptr;        // T7 scratch: aligned hashed levels
+    int32_t* sc_priv = nullptr;      // T7 fixed-point partials of the coarse levels, per scatter CTA
+    int64_t sc_dense_floats = 0, sc_hash_floats = 0, sc_priv_ints = 0;
     bool capture = false;
     float* grad = nullptr;           // params + 1 + 3 * tail_leaves
     int64_t tail_leaves = 0;
@@ -136,7 +141,7 @@ static void dfree(T*& p) {
 static void free_work(TrainWork* w) {
     dfree(w->r_acc); dfree(w->r_leaf); dfree(w->r_gt); dfree(w->r_loss);
     dfree(w->s_ray); dfree(w->s_leaf); dfree(w->s_t0); dfree(w->s_t1); dfree(w->s_gt);
-    dfree(w->X); dfree(w->A); dfree(w->Dl); dfree(w->dZ); dfree(w->Z);
+    dfree(w->X); dfree(w->A); dfree(w->Dl); dfree(w->dZ); dfree(w->Z); dfree(w->gx);
 }
 
 void free_train_device(nbvh_ctx* c) {
@@ -148,6 +153,9 @@ void free_train_device(nbvh_ctx* c) {
     dfree(c->train->counters);
     dfree(c->train->loss_acc);
     dfree(c->train->adam_step);
+    dfree(c->train->sc_dense);
+    dfree(c->train->sc_hash);
+    dfree(c->train->sc_priv);
     delete c->train;
     c->train = nullptr;
 }
@@ -201,6 +209,7 @@ nbvh_status reserve_train(nbvh_ctx* c, int64_t max_rays) {
     if (e == cudaSuccess) e = cudaMalloc((void**)&w->A, H * n * 64 * 2);
     if (e == cudaSuccess) e = cudaMalloc((void**)&w->Dl, H * n * 64 * 2);
     if (e == cudaSuccess) e = cudaMalloc((void**)&w->dZ, n * 8 * 4);
+    if (e == cudaSuccess) e = cudaMalloc((void**)&w->gx, n * D * 4);
     if (e != cudaSuccess) {
         free_work(w);
         cudaGetLastError();
@@ -221,16 +230,58 @@ void reset_adam(nbvh_ctx* c) {
 // launchers (templated on F, D)
 // Shared memory of k_train_bwd without the private gradient accumulator, and the bytes left
 // for that accumulator under the per-CTA opt-in limit.
-static size_t bwd_smem_base(int D, int H, int n_points) {
-    return ((size_t)64 * (D + 8) + (size_t)(H - 1) * 64 * 72 + 16 * 72) * 2 + kTileQ * sizeof(SampleDesc) +
-           kMaxLevels * sizeof(LevelSm) + (size_t)kTileQ * n_points * 3 * 4 + (size_t)kTileQ * (D + 4) * 4;
+static size_t bwd_smem(int D, int H) {
+    return ((size_t)64 * (D + 8) + (size_t)(H - 1) * 64 * 72 + 16 * 72) * 2;
 }
-static int64_t bwd_priv_room(int D, int H, int n_points) {
-    int dev = 0, optin = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    const int64_t room = (int64_t)optin - 1024 - (int64_t)bwd_smem_base(D, H, n_points);   // 1 KB static margin
-    return room > 0 ? room : 0;
+// Gradient floats of coarse levels k_train_scatter accumulates in shared memory (8 bytes
+// each: two int32 fixed-point parts), budgeted for two CTAs per SM.
+constexpr int64_t kScatterPrivBudget = 52 * 1024;
+constexpr int kScatterCtasPerSm = 2;
+
+// T7 scratch layout (k_train_scatter): every dense level cell-packed (N^3 cells x 8 corners x
+// F floats) in sc_dense, every hashed level [T][F] in sc_hash; offsets 16-byte aligned.
+static nbvh_status ensure_scatter_scratch(nbvh_ctx* c, TrainArgs& a, int sms) {
+    TrainWork* w = c->train;
+    const int F = c->cfg.F;
+    int64_t nd = 0, nh = 0;
+    for (int l = 0; l < c->cfg.L; ++l) {
+        if (c->dense[l]) {
+            a.sc_off[l] = nd;
+            nd += (int64_t)c->res[l] * c->res[l] * c->res[l] * 8 * F;
+        } else {
+            a.sc_off[l] = nh;
+            nh += ((int64_t)1 << c->cfg.log2_T) * F;
+        }
+        nd = (nd + 3) & ~(int64_t)3;
+        nh = (nh + 3) & ~(int64_t)3;
+    }
+    const int64_t np = (int64_t)sms * kScatterCtasPerSm * 2 * a.priv_floats;
+    cudaError_t e = cudaSuccess;
+    if (nd > w->sc_dense_floats) {
+        dfree(w->sc_dense);
+        e = cudaMalloc((void**)&w->sc_dense, (size_t)std::max<int64_t>(nd, 4) * 4);
+        w->sc_dense_floats = nd;
+    }
+    if (e == cudaSuccess && nh > w->sc_hash_floats) {
+        dfree(w->sc_hash);
+        e = cudaMalloc((void**)&w->sc_hash, (size_t)std::max<int64_t>(nh, 4) * 4);
+        w->sc_hash_floats = nh;
+    }
+    if (e == cudaSuccess && np > w->sc_priv_ints) {
+        dfree(w->sc_priv);
+        e = cudaMalloc((void**)&w->sc_priv, (size_t)std::max<int64_t>(np, 4) * 4);
+        w->sc_priv_ints = np;
+    }
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(c, NBVH_ENOMEM, "train: T7 scratch");
+    }
+    a.sc_dense = w->sc_dense;
+    a.sc_hash = w->sc_hash;
+    a.sc_priv = w->sc_priv;
+    a.scatter_ctas = sms * kScatterCtasPerSm;
+    w->sc_dense_floats = std::max(w->sc_dense_floats, nd);
+    return NBVH_OK;
 }
 
 // ev (nullable): 6 events recorded before select and after select, label, fwd, bwd, dW
@@ -244,13 +295,16 @@ static cudaError_t launch_train_fd(const TrainArgs& a, int64_t n, int64_t w_off,
     const size_t smem_fwd = (size_t)kTileQ * (D + 8) * 2 + (size_t)mlp_smem_halves(D, H) * 2 + kTileQ * 8 * 4 +
                             (64 * H + 8) * 4 + kTileQ * sizeof(SampleDesc) + kMaxLevels * sizeof(LevelSm) +
                             (size_t)kTileQ * a.g.n_points * 3 * 4;
-    const size_t smem_bwd = bwd_smem_base(D, H, a.g.n_points) + (size_t)a.priv_floats * 4;
+    const size_t smem_bwd = bwd_smem(D, H);
+    const size_t smem_sc = (size_t)a.priv_floats * 8;
     const size_t smem_dw = (size_t)kTileQ * 72 * 2 + (size_t)kTileQ * (D + 8) * 2 + kTileQ * 8 * 4;
     cudaError_t e = cudaFuncSetAttribute(k_train_fwd<F, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fwd);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_train_bwd<F, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bwd);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_train_dw<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_dw);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_train_scatter<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_sc);
     if (e != cudaSuccess) return e;
     const unsigned blocks_n = (unsigned)((n + 127) / 128);
     if (ev) cudaEventRecord(ev[0], s);
@@ -263,13 +317,22 @@ static cudaError_t launch_train_fd(const TrainArgs& a, int64_t n, int64_t w_off,
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (ev) cudaEventRecord(ev[2], s);
     const int tiles = (int)((n + kTileQ - 1) / kTileQ);
-    const int grid = tiles < sms ? (tiles > 0 ? tiles : 1) : sms;
     const int grid_fwd = tiles < 2 * sms ? (tiles > 0 ? tiles : 1) : 2 * sms;   // 2 CTAs per SM
     k_train_fwd<F, D><<<grid_fwd, 256, smem_fwd, s>>>(a);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (ev) cudaEventRecord(ev[3], s);
-    k_train_bwd<F, D><<<grid, 256, smem_bwd, s>>>(a);
+    k_train_bwd<F, D><<<2 * sms, 256, smem_bwd, s>>>(a);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    // T7: scatter into the scratch (dense / hashed regions zeroed first), then the canonical
+    // gradient buffer
+    e = cudaMemsetAsync(a.sc_dense, 0, sizeof(float) * (size_t)a.sc_dense_n, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(a.sc_hash, 0, sizeof(float) * (size_t)a.sc_hash_n, s);
+    if (e != cudaSuccess) return e;
+    k_train_scatter<F><<<a.scatter_ctas, 256, smem_sc, s>>>(a);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    k_train_scatter_finish<F><<<4 * sms, 256, 0, s>>>(a);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    *launches += 2;
     if (ev) cudaEventRecord(ev[4], s);
     const unsigned dw_grid = (unsigned)((n + kDwChunk - 1) / kDwChunk);
     bool tc_done = false;
@@ -414,13 +477,22 @@ extern "C" nbvh_status nbvh_train_backward(nbvh_ctx* c, const nbvh_ray* rays, in
         a.use_tc_dw = (ev && ev[0] == '1') ? 0 : 1;
     }
     const char* pev = std::getenv("NBVH_PRIV_BYTES");   // tuning hook (0 disables)
-    const int64_t room = bwd_priv_room(c->d_in, c->cfg.hidden_layers, c->cfg.n_points);
-    const int64_t priv_budget = pev ? std::min<int64_t>(std::atoll(pev), room) : room;
+    const int64_t priv_budget = pev ? std::min<int64_t>(std::atoll(pev), kScatterPrivBudget) : kScatterPrivBudget;
     for (int l = 0; l < c->cfg.L && c->dense[l]; ++l) {
         const int64_t end = (c->offset[l] + (int64_t)(c->res[l] + 1) * (c->res[l] + 1) * (c->res[l] + 1)) * c->cfg.F;
         if (end * 4 > priv_budget) break;
         a.priv_levels = l + 1;
         a.priv_floats = (int32_t)end;
+    }
+    a.gx = w->gx;
+    {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        st = ensure_scatter_scratch(c, a, sms);
+        if (st) return st;
+        a.sc_dense_n = w->sc_dense_floats;
+        a.sc_hash_n = w->sc_hash_floats;
     }
     const int64_t w_off = c->n_table, b_off = c->n_table + c->n_W;
     const int F = c->cfg.F, D = c->d_in;

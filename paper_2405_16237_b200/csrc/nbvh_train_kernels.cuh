@@ -58,8 +58,15 @@ struct TrainArgs {
     float* tail;             // [0] accepted count, [1 + 3*leaf + {0,1,2}] loss sum, samples, first hits
     double* loss_acc;        // [5]: total, vis, dist, normal, albedo (weights applied)
     int64_t cap;             // capacity of the per-sample arrays
-    int32_t priv_levels;     // coarse levels accumulated in shared memory by k_train_bwd
+    int32_t priv_levels;     // coarse levels accumulated in shared memory by k_train_scatter
     int32_t priv_floats;     // their gradient floats (levels 0..priv_levels-1 are a prefix)
+    float* gx;               // [cap][D] fp32 dL/dx per sample (k_train_bwd -> k_train_scatter)
+    float* sc_dense;         // T7 scratch of the global dense levels: cell-packed, 8 corners x F
+    float* sc_hash;          // T7 scratch of the hashed levels: [T][F], 16-byte aligned per level
+    int32_t* sc_priv;        // [scatter CTAs][priv_floats] fixed-point partial sums
+    int64_t sc_off[kMaxLevels];   // float offset of a level's scratch (dense: in sc_dense; hashed: in sc_hash)
+    int64_t sc_dense_n, sc_hash_n;   // scratch sizes (floats)
+    int32_t scatter_ctas;
     int32_t use_tc_dw;       // weight GEMMs on tcgen05 (k_train_dw_tc) when the shape allows
 };
 
@@ -400,12 +407,11 @@ __global__ void __launch_bounds__(256, 2) k_train_fwd(TrainArgs a) {
     }
 }
 
-// ------------------------------------------------------------------ T6/T7 backward
+// ------------------------------------------------------------------ T6 backward (delta chain)
 // Per warp (16 samples): delta_H = dL/dz; delta_k = (delta_{k+1} W_{k+1}) * relu'(h_k)
 // on tensor cores (B operands via ldmatrix.trans of the [out][in] weights), deltas of the
-// hidden layers written out for the weight gradients; dL/dx = delta_0 W_0 scattered into
-// the hash-table gradient through the trilinear weights.  Dense (coarse) levels
-// aggregate equal addresses within the warp before the atomic.
+// hidden layers written out for the weight gradients; dL/dx = delta_0 W_0 written out (fp32)
+// for the hash-grid scatter (k_train_scatter, T7).
 struct BwdSmem {
     __half* w0;   // [64][D+8]
     __half* wh;   // [H-1][64][72]
@@ -413,7 +419,7 @@ struct BwdSmem {
 };
 
 template <int F, int D>
-__global__ void __launch_bounds__(256, 1) k_train_bwd(TrainArgs a) {
+__global__ void __launch_bounds__(256, 2) k_train_bwd(TrainArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int M = *a.n_samples;
@@ -424,14 +430,6 @@ __global__ void __launch_bounds__(256, 1) k_train_bwd(TrainArgs a) {
     s.w0 = reinterpret_cast<__half*>(smem_raw);
     s.wh = s.w0 + 64 * (D + 8);
     s.wo = s.wh + (H - 1) * 64 * 72;
-    SampleDesc* qd = reinterpret_cast<SampleDesc*>(s.wo + 16 * 72);
-    LevelSm* lv = reinterpret_cast<LevelSm*>(qd + kTileQ);
-    float* xs = reinterpret_cast<float*>(lv + kMaxLevels);             // [n_pts*3][kTileQ]
-    float* gx = xs + a.g.n_points * 3 * kTileQ;                        // dL/dx [kTileQ][D+4] fp32
-    float* priv = gx + kTileQ * (D + 4);                               // [priv_floats]
-    stage_levels(a.g, lv, tid);
-    for (int i = tid; i < a.priv_floats; i += blockDim.x) priv[i] = 0.f;
-    const uint32_t hmask = (1u << a.g.log2_T) - 1u;
     {   // stage weights (fp16 inference copy == forward operands)
         const uint4* W = reinterpret_cast<const uint4*>(a.m.W);
         const int cpr0 = D / 8;
@@ -444,26 +442,11 @@ __global__ void __launch_bounds__(256, 1) k_train_bwd(TrainArgs a) {
         for (int i = tid; i < 16 * 8; i += blockDim.x)
             *reinterpret_cast<uint4*>(s.wo + (i / 8) * 72 + (i % 8) * 8) = i < 64 ? __ldg(Wo + i) : make_uint4(0, 0, 0, 0);
     }
+    __syncthreads();
     const int g = lane >> 2, t = lane & 3;
-    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-        if (tid < kTileQ) {
-            SampleDesc q;
-            load_sample_desc(a, tile * kTileQ + tid, M, q);
-            qd[tid] = q;
-            if (q.valid)
-#pragma unroll
-                for (int p = 0; p < 4; ++p) {
-                    if (p >= a.g.n_points) break;
-                    float x[3];
-                    segment_point(a.g, q.o, q.d, q.t0, q.t1, p, a.g.n_points, q.xi, x);
-                    xs[(p * 3 + 0) * kTileQ + tid] = x[0];
-                    xs[(p * 3 + 1) * kTileQ + tid] = x[1];
-                    xs[(p * 3 + 2) * kTileQ + tid] = x[2];
-                }
-        }
-        __syncthreads();
-        const int r0 = warp * 16;
-        const int64_t gr0 = (int64_t)tile * kTileQ + r0 + g, gr1 = gr0 + 8;
+    // warp item = 16 samples; no block-wide barrier after the staging
+    for (int blk = blockIdx.x * 8 + warp; blk * 16 < M; blk += gridDim.x * 8) {
+        const int64_t gr0 = (int64_t)blk * 16 + g, gr1 = gr0 + 8;
         const bool v0 = gr0 < M, v1 = gr1 < M;
         // delta_H = dL/dz as an m16k16 A fragment (k 8..15 zero)
         uint32_t af[4][4];
@@ -515,7 +498,7 @@ __global__ void __launch_bounds__(256, 1) k_train_bwd(TrainArgs a) {
                 af[kb][3] = pack_half2(acc[2 * kb + 1][2], acc[2 * kb + 1][3]);
             }
         }
-        // dL/dx = delta_0 W_0  ([16 x 64] x [64 x D]) -> fp32 tile in shared memory
+        // dL/dx = delta_0 W_0  ([16 x 64] x [64 x D]) -> fp32 rows of a.gx
         const uint32_t w0b = (uint32_t)__cvta_generic_to_shared(s.w0 + (lane & 15) * (D + 8) + (lane >> 4) * 8);
 #pragma unroll 1
         for (int np = 0; np < D / 16; ++np) {
@@ -530,56 +513,192 @@ __global__ void __launch_bounds__(256, 1) k_train_bwd(TrainArgs a) {
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
                 const int c = (2 * np + j) * 8 + 2 * t;
-                *reinterpret_cast<float2*>(gx + (r0 + g) * (D + 4) + c) = make_float2(acc[j][0], acc[j][1]);
-                *reinterpret_cast<float2*>(gx + (r0 + g + 8) * (D + 4) + c) = make_float2(acc[j][2], acc[j][3]);
+                if (v0) *reinterpret_cast<float2*>(a.gx + gr0 * D + c) = make_float2(acc[j][0], acc[j][1]);
+                if (v1) *reinterpret_cast<float2*>(a.gx + gr1 * D + c) = make_float2(acc[j][2], acc[j][3]);
             }
         }
-        __syncthreads();
-        // T7 scatter: warp item = (32-sample block, point-level); lanes = samples, so
-        // each lane computes its cell once and adds w_k * dL/dfeat to the 8 corner entries.
-        // Coarse dense levels (l < priv_levels) accumulate into a CTA-private shared-memory
-        // copy flushed once per CTA; the rest go straight to the fp32 gradient buffer.
-        {
-            const int nv = min(kTileQ, M - tile * kTileQ);
-            const int nqb = (nv + 31) >> 5;
-            const int npl = a.g.n_points * a.g.L;
-            // consecutive items of a warp go to different point-levels (and table regions):
-            // measured faster than sweeping one level over all sample blocks (atomic spread)
-            for (int it = warp; it < nqb * npl; it += 8) {
-                const int pl = it / nqb, qb = it - pl * nqb;
-                const int q = qb * 32 + lane;
-                if (q >= nv) continue;
-                const int p = pl / a.g.L, l = pl - p * a.g.L;
-                const LevelSm P = lv[l];
-                Cell cell;
-                level_cell_sm(P, hmask, xs[(p * 3 + 0) * kTileQ + q], xs[(p * 3 + 1) * kTileQ + q],
-                              xs[(p * 3 + 2) * kTileQ + q], cell);
-                const float* gq = gx + q * (D + 4) + pl * F;
-                if (l < a.priv_levels) {
+    }
+}
+
+// ------------------------------------------------------------------ T7 hash-grid gradient scatter
+// P:61 (hash-grid backprop): dL/dT[entry] += w_corner * dL/dfeat for every corner of every
+// (sample, point, level).  One thread per (sample, point): the point is recomputed from the
+// sample descriptor (same op order as the forward), dL/dx of its L levels read from a.gx.
+// Three destinations, so that no two lanes race on a hot address and the L2 sees fewer,
+// wider reductions (T7 is bound by L2 reduction throughput):
+//   * coarse dense levels l < priv_levels: a CTA-private shared-memory accumulator in fixed
+//     point (native 32-bit ATOMS.ADD; fp32 shared atomics are CAS loops on sm_100): each
+//     contribution v = hi + lo with hi = rint(v 2^10) 2^-10 and |lo| <= 2^-11 added to two
+//     int32 sums at scales 2^10 and 2^28 (resolution 2^-28), written per CTA to a.sc_priv and
+//     summed over CTAs in 64-bit integers by k_train_scatter_finish (C37);
+//   * other dense levels: a cell-packed scratch (the 8 corners of a cell contiguous, like the
+//     inference table): four 16-byte red.global.add.v4.f32 per point-level instead of eight
+//     8-byte ones; k_train_scatter_finish gathers each vertex's 8 cells;
+//   * hashed levels: an aligned [T][F] scratch: the x-neighbour corners of an even cell
+//     coordinate are entries e, e^1 of one 16-byte pair (pi_1 = 1) -> one red.v4 (F = 2).
+constexpr float kFixHi = 1024.0f;              // 2^10: scale of the high part
+constexpr float kFixLo = 268435456.0f;         // 2^28: scale of the low part (|lo| <= 2^-11: 2^14
+                                               // worst-case same-sign contributions per entry and CTA)
+constexpr float kFixLimit = 1048576.0f;        // 2^20: larger contributions go to a global fp32 atomic
+
+template <int F>
+__device__ __forceinline__ void red_entry(float* p, const float* v) {
+    if constexpr (F == 2) red_add_v2(p, v[0], v[1]);
+    else asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v[0]), "f"(v[1]), "f"(v[2]),
+                      "f"(v[3]) : "memory");
+}
+__device__ __forceinline__ void red_add_v4(float* p, float x, float y, float z, float w) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(x), "f"(y), "f"(z), "f"(w)
+                 : "memory");
+}
+
+template <int F>
+__global__ void __launch_bounds__(256) k_train_scatter(TrainArgs a) {
+    extern __shared__ __align__(16) int32_t priv[];          // [2][priv_floats]: high, low parts
+    __shared__ LevelSm lv[kMaxLevels];
+    const int tid = threadIdx.x;
+    stage_levels(a.g, lv, tid);
+    for (int i = tid; i < 2 * a.priv_floats; i += blockDim.x) priv[i] = 0;
+    __syncthreads();
+    const int M = *a.n_samples, NP = a.g.n_points, L = a.g.L, D = NP * L * F;
+    const uint32_t hmask = (1u << a.g.log2_T) - 1u;
+    const int64_t items = (int64_t)M * NP;
+    for (int64_t it = (int64_t)blockIdx.x * blockDim.x + tid; it < items; it += (int64_t)gridDim.x * blockDim.x) {
+        const int i = (int)(it / NP), p = (int)(it - (int64_t)i * NP);
+        SampleDesc q;
+        load_sample_desc(a, i, M, q);
+        float x[3];
+        segment_point(a.g, q.o, q.d, q.t0, q.t1, p, NP, q.xi, x);    // the forward's point (C8)
+        const float* gq = a.gx + (int64_t)i * D + p * L * F;
+        for (int l = 0; l < L; ++l) {
+            const LevelSm P = lv[l];
+            float gv[F];
 #pragma unroll
-                    for (int k = 0; k < 8; ++k)
-                        for (int f = 0; f < F; ++f) {
-                            NBVH_DCHECK((int64_t)(P.coff + cell.idx[k]) * F + f < a.priv_floats);
-                            atomicAdd(priv + (P.coff + cell.idx[k]) * F + f, cell.w[k] * gq[f]);
+            for (int f = 0; f < F; ++f) gv[f] = gq[l * F + f];
+            Cell cell;
+            uint32_t i0, i1, i2;
+            level_cell_sm(P, hmask, x[0], x[1], x[2], cell, i0, i1, i2);
+            if (l < a.priv_levels) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+#pragma unroll
+                    for (int f = 0; f < F; ++f) {
+                        const float v = cell.w[k] * gv[f];
+                        const int64_t e = (int64_t)(P.coff + cell.idx[k]) * F + f;
+                        NBVH_DCHECK(e < a.priv_floats);
+                        if (fabsf(v) < kFixLimit) {
+                            const float hi = rintf(v * kFixHi);                 // exact: |v 2^10| < 2^30
+                            const float lo = __fmaf_rn(-hi, 1.0f / kFixHi, v);  // exact remainder
+                            atomicAdd(priv + e, (int)hi);
+                            atomicAdd(priv + a.priv_floats + e, __float2int_rn(lo * kFixLo));
+                        } else {
+                            atomicAdd(a.grad + e, v);
                         }
-                } else {
-                    float* base = a.grad + (int64_t)P.coff * F;
+                    }
+            } else if (P.n1) {
+                // cell-packed scratch: cell = i0 + N i1 + N^2 i2, 8 corners x F floats
+                float* base = a.sc_dense + a.sc_off[l] + (int64_t)(i0 + P.nx * i1 + P.nxy * i2) * 8 * F;
 #pragma unroll
-                    for (int k = 0; k < 8; ++k) {
-                        NBVH_DCHECK(cell.idx[k] < (P.n1 ? P.n1sq * P.n1 : hmask + 1u));
-                        float* dst = base + (int64_t)cell.idx[k] * F;
-                        red_add_v2(dst, cell.w[k] * gq[0], cell.w[k] * gq[1]);
-                        if (F == 4) red_add_v2(dst + 2, cell.w[k] * gq[2], cell.w[k] * gq[3]);
+                for (int j = 0; j < 4; ++j) {              // corners 2j (x) and 2j+1 (x+1)
+                    if constexpr (F == 2) {
+                        red_add_v4(base + 4 * j, cell.w[2 * j] * gv[0], cell.w[2 * j] * gv[1],
+                                   cell.w[2 * j + 1] * gv[0], cell.w[2 * j + 1] * gv[1]);
+                    } else {
+                        float u[F], w2[F];
+#pragma unroll
+                        for (int f = 0; f < F; ++f) { u[f] = cell.w[2 * j] * gv[f]; w2[f] = cell.w[2 * j + 1] * gv[f]; }
+                        red_entry<F>(base + (2 * j) * F, u);
+                        red_entry<F>(base + (2 * j + 1) * F, w2);
+                    }
+                }
+            } else {
+                float* base = a.sc_hash + a.sc_off[l];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const uint32_t e0 = cell.idx[2 * j], e1 = cell.idx[2 * j + 1];
+                    float u[F], w2[F];
+#pragma unroll
+                    for (int f = 0; f < F; ++f) { u[f] = cell.w[2 * j] * gv[f]; w2[f] = cell.w[2 * j + 1] * gv[f]; }
+                    if (F == 2 && (e0 ^ e1) == 1u) {       // one aligned 16-byte pair {e, e^1}
+                        const bool lo0 = e0 < e1;
+                        red_add_v4(base + (int64_t)(e0 & ~1u) * 2, lo0 ? u[0] : w2[0], lo0 ? u[1] : w2[1],
+                                   lo0 ? w2[0] : u[0], lo0 ? w2[1] : u[1]);
+                    } else {
+                        red_entry<F>(base + (int64_t)e0 * F, u);
+                        red_entry<F>(base + (int64_t)e1 * F, w2);
                     }
                 }
             }
         }
-        __syncthreads();
     }
-    // flush the CTA-private coarse-level gradients
-    for (int i = tid; i < a.priv_floats; i += blockDim.x) {
-        const float v = priv[i];
-        if (v != 0.f) atomicAdd(a.grad + i, v);
+    __syncthreads();
+    int32_t* out = a.sc_priv + (int64_t)blockIdx.x * 2 * a.priv_floats;
+    for (int i = tid; i < 2 * a.priv_floats; i += blockDim.x) out[i] = priv[i];
+}
+
+// Scratch -> canonical gradient buffer (every table entry written exactly once):
+//   coarse dense levels: the CTAs' fixed-point partials summed in 64-bit integers (exact,
+//   order-independent) and scaled once; other dense levels: each vertex gathers its corner
+//   of the up to 8 cells that contain it; hashed levels: a copy.
+template <int F>
+__global__ void __launch_bounds__(256) k_train_scatter_finish(TrainArgs a) {
+    __shared__ LevelSm lv[kMaxLevels];
+    stage_levels(a.g, lv, threadIdx.x);
+    __syncthreads();
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (int64_t e = t0; e < a.priv_floats; e += stride) {
+        long long hi = 0, lo = 0;                    // integer sums: exact, any order
+        const int32_t* part = a.sc_priv + e;
+        const int64_t cs = 2 * (int64_t)a.priv_floats;
+        int c = 0;
+        for (; c + 8 <= a.scatter_ctas; c += 8) {    // 16 independent loads in flight
+            int32_t h[8], l[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                h[u] = __ldcs(part + (c + u) * cs);
+                l[u] = __ldcs(part + (c + u) * cs + a.priv_floats);
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                hi += h[u];
+                lo += l[u];
+            }
+        }
+        for (; c < a.scatter_ctas; ++c) {
+            hi += part[c * cs];
+            lo += part[c * cs + a.priv_floats];
+        }
+        // += : keeps the rare overflow-path atomics
+        a.grad[e] += (float)((double)hi * (1.0 / (double)kFixHi) + (double)lo * (1.0 / (double)kFixLo));
+    }
+    for (int l = a.priv_levels; l < a.g.L; ++l) {
+        const LevelSm P = lv[l];
+        if (P.n1) {
+            const uint32_t n1 = P.n1, N = n1 - 1u, nv = P.n1sq * n1;
+            const float* sc = a.sc_dense + a.sc_off[l];
+            for (int64_t v = t0; v < nv; v += stride) {
+                const uint32_t z = (uint32_t)v / P.n1sq, rem = (uint32_t)v - z * P.n1sq, y = rem / n1, x = rem - y * n1;
+                float acc[F];
+#pragma unroll
+                for (int f = 0; f < F; ++f) acc[f] = 0.f;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {              // cell (x - dx, y - dy, z - dz), corner k = (dx, dy, dz)
+                    const int dx = k & 1, dy = (k >> 1) & 1, dz = (k >> 2) & 1;
+                    const int cx = (int)x - dx, cy = (int)y - dy, cz = (int)z - dz;
+                    if (cx < 0 || cy < 0 || cz < 0 || cx >= (int)N || cy >= (int)N || cz >= (int)N) continue;
+                    const float* src = sc + ((int64_t)cx + N * ((int64_t)cy + N * cz)) * 8 * F + k * F;
+#pragma unroll
+                    for (int f = 0; f < F; ++f) acc[f] += src[f];
+                }
+#pragma unroll
+                for (int f = 0; f < F; ++f) a.grad[((int64_t)P.coff + v) * F + f] = acc[f];
+            }
+        } else {
+            const int64_t n = (int64_t)(1u << a.g.log2_T) * F;
+            const float* sc = a.sc_hash + a.sc_off[l];
+            for (int64_t i = t0; i < n; i += stride) a.grad[(int64_t)P.coff * F + i] = sc[i];
+        }
     }
 }
 

@@ -239,6 +239,57 @@ nbvh_status nbvh_pt_shade(nbvh_ctx* ctx, const nbvh_ray* d_rays, int64_t n, nbvh
                           float* d_throughput, float* d_radiance, nbvh_ray* d_next, uint64_t seed, int32_t bounce,
                           const float* sky, float eps, int32_t* d_alive, void* stream);
 
+/* ---------------------------------------------------------------- two-level hierarchy (device) */
+/* NEXT-3, PAPER §7: "a TLAS holds several BLAS; a BLAS is classical or N-BVH; both
+ * query types yield the same type of intersection data".  An instance places one BLAS in the
+ * world: world_to_object = row-major 3x4 [A | b] (x_object = A x_world + b; the same ray
+ * parameter t in both spaces, d_object = A d_world, so hit distances need no conversion),
+ * lo/hi = its world-space box, blas = the caller's BLAS number (< NBVH_MAX_BLAS). */
+#define NBVH_MAX_BLAS 8
+typedef struct {
+    float world_to_object[12];
+    float lo[3], hi[3];
+    int32_t blas;
+    int32_t pad;
+} nbvh_instance;                                                    /* 80 bytes */
+typedef struct nbvh_tlas nbvh_tlas;                                 /* opaque, device-resident */
+/* Builds the TLAS: a binary BVH over the instances' world boxes (median split of the box
+ * centres on the longest axis), uploaded to the context's device.  h_inst: host array of
+ * n_inst (1..4096) instances, copied.  NBVH_EINVAL / NBVH_ERANGE on bad boxes / blas index. */
+nbvh_status nbvh_tlas_build(nbvh_ctx* ctx, const nbvh_instance* h_inst, int32_t n_inst, nbvh_tlas** out);
+void nbvh_tlas_destroy(nbvh_tlas* tlas);
+/* TLAS traversal of m world rays d_rays [m]: for every instance whose box a ray crosses
+ * within [tmin, tmax], the ray transformed into the instance's object space is appended to
+ * that instance's BLAS list: d_out_rays [n_blas][cap] (object-space rays, same tmin/tmax),
+ * d_out_src [n_blas][cap] (index of the world ray), d_out_inst [n_blas][cap] (instance),
+ * d_counts [n_blas] (entries appended; zeroed first; a list overflowing cap raises the flag
+ * read by nbvh_tlas_overflow).  Device pointers; asynchronous. */
+nbvh_status nbvh_tlas_dispatch(nbvh_ctx* ctx, nbvh_tlas* tlas, const nbvh_ray* d_rays, int64_t m,
+                               nbvh_ray* d_out_rays, int32_t* d_out_src, int32_t* d_out_inst, int32_t* d_counts,
+                               int64_t cap, void* stream);
+/* Closest hit per world ray over the BLAS answers: h_lists (host array, n_blas entries) holds
+ * each BLAS's hit record for its dispatched list (entry j answers list entry j); the nearest
+ * hit t wins (ties: lower BLAS number, then lower entry), its normal is brought back to world
+ * space (A^T n, normalised); d_out [m] world hit record, leaf = the winning instance (or -1).
+ * cap < 2^24.  Asynchronous. */
+nbvh_status nbvh_tlas_merge(nbvh_ctx* ctx, nbvh_tlas* tlas, int64_t m, const int32_t* d_counts, int64_t cap,
+                            const int32_t* d_src, const int32_t* d_inst, const nbvh_hits* h_lists,
+                            nbvh_hits d_out, void* stream);
+/* Host flag: 1 = a dispatch list overflowed its capacity, 2 = TLAS stack overflow (since
+ * the build).  Synchronous. */
+nbvh_status nbvh_tlas_overflow(nbvh_ctx* ctx, nbvh_tlas* tlas, int32_t* h_flag);
+/* One wavefront step over COMPACTED alive paths: path i has world ray d_rays[i],
+ * hit record d_hits[i], pixel d_pixel[i] and throughput d_thr[i][3].  Escaped paths add
+ * throughput x sky (horizon-to-zenith gradient, sky[6]) to d_radiance[pixel][3] (atomic);
+ * hits continue diffusely (throughput *= albedo, cosine-weighted direction from a
+ * counter-based hash of (seed, pixel, bounce)) and are appended to d_next_rays / d_next_pixel /
+ * d_next_thr at slots counted by *d_next_count (device, not reset).  Asynchronous. */
+nbvh_status nbvh_pt_shade_compact(nbvh_ctx* ctx, const nbvh_ray* d_rays, int64_t m, nbvh_hits d_hits,
+                                  const int32_t* d_pixel, const float* d_thr, float* d_radiance,
+                                  nbvh_ray* d_next_rays, int32_t* d_next_pixel, float* d_next_thr,
+                                  int32_t* d_next_count, uint64_t seed, int32_t bounce, const float* sky,
+                                  float eps, void* stream);
+
 /* ---------------------------------------------------------------- training (device) */
 /* T0: n training rays and the method's random draws for rays
  * [i0, i0 + n) of training step `step`, from the counter-based generator Philox-4x32-10

@@ -38,6 +38,15 @@ class Hits(C.Structure):
                 ("leaf", C.c_void_p), ("n_queries", C.c_void_p)]
 
 
+class Instance(C.Structure):
+    """nbvh_instance: world_to_object row-major 3x4, world box, BLAS number."""
+    _fields_ = [("world_to_object", C.c_float * 12), ("lo", C.c_float * 3), ("hi", C.c_float * 3),
+                ("blas", C.c_int32), ("pad", C.c_int32)]
+
+
+MAX_BLAS = 8
+
+
 class QueryStats(C.Structure):
     _fields_ = [("n_rays", C.c_int64), ("n_queries", C.c_int64), ("n_iters", C.c_int32),
                 ("n_launches", C.c_int32), ("n_refills", C.c_int32), ("ms_traverse", C.c_float),
@@ -85,6 +94,13 @@ SIGNATURES = {
     "nbvh_gather_probe": (C.c_int, [_P, _I64, _I32, _I64, C.c_uint32, _P, _I64, _P, _P]),
     "nbvh_atomic_probe": (C.c_int, [_P, _I64, _I32, _I64, C.c_uint32, _P, _P]),
     "nbvh_pt_shade": (C.c_int, [_P, _P, _I64, Hits, Hits, _P, _P, _P, C.c_uint64, _I32, _P, _F, _P, _P]),
+    "nbvh_tlas_build": (C.c_int, [_P, _P, _I32, _P]),
+    "nbvh_tlas_destroy": (None, [_P]),
+    "nbvh_tlas_dispatch": (C.c_int, [_P, _P, _P, _I64, _P, _P, _P, _P, _I64, _P]),
+    "nbvh_tlas_merge": (C.c_int, [_P, _P, _I64, _P, _I64, _P, _P, _P, Hits, _P]),
+    "nbvh_tlas_overflow": (C.c_int, [_P, _P, _P]),
+    "nbvh_pt_shade_compact": (C.c_int, [_P, _P, _I64, Hits, _P, _P, _P, _P, _P, _P, _P, C.c_uint64, _I32, _P, _F,
+                                        _P]),
     "nbvh_debug_traverse": (C.c_int, [_P, _P, _I64, _I32, _I32, _P, _P, _P, _P, _P]),
     "nbvh_debug_traverse_product": (C.c_int, [_P, _P, _I64, _I32, _P, _P, _P, _P, _P, _P]),
     "nbvh_debug_encode": (C.c_int, [_P, _P, _I64, _P, _P, _P]),

@@ -109,27 +109,156 @@ def test_pt_shade_vs_numpy():
     assert np.allclose(np.linalg.norm(nx[cont, 4:7], axis=1), 1, atol=1e-5)
 
 
-def test_hybrid_render_bounded(orc):
+def _hybrid_scene(cut_leaves=64, lod_leaves=None):
     from paper_2405_16237_b200 import Context, PARAM_TABLES
-    from paper_2405_16237_b200.pathtrace import PathTracer, SKY
     terrain, spheres = synth.scene_1080p_parts(grid=48, nu=6)
     neural = Context(device=0, L=8, F=2, log2_T=14, n_points=4, hidden_layers=2)
     neural.set_mesh(spheres)
-    neural.build_cut(64)
+    neural.build_cut(cut_leaves)
+    if lod_leaves:
+        neural.build_cut(lod_leaves, lod=1)                       # a coarser LoD of the same grid
     neural.set_params(PARAM_TABLES, synth.random_params_fp16(neural.param_count(PARAM_TABLES), seed=4)
                       .astype(np.float32))
     neural.set_mlp(synth.random_mlp(neural.d_in, 2, 64, seed=5))
     classical = Context(device=0, L=8, F=2, log2_T=14, n_points=4, hidden_layers=2)
     classical.set_mesh(terrain)
+    return neural, classical, terrain, spheres
+
+
+IDENTITY = np.concatenate([np.eye(3), np.zeros((3, 1))], 1)
+
+
+def test_hybrid_render_bounded():
+    """The TLAS renderer (compacted wavefront): finite, non-negative radiance bounded by the
+    sky, alive path counts that never grow, most pixels lit."""
+    from paper_2405_16237_b200.pathtrace import PathTracer, SKY
+    neural, classical, _, _ = _hybrid_scene()
     rays = torch.from_numpy(synth.camera_rays(96, 64, (0.0, 0.6, 1.6), vfov_deg=50.0)).cuda()
-    neural.reserve(rays.shape[0])
-    pt = PathTracer(neural, classical, rays.shape[0])
+    pt = PathTracer([(neural, "neural"), (classical, "mesh")], [(0, IDENTITY), (1, IDENTITY)], rays.shape[0])
     rad, alive = pt.render(rays, bounces=4, seed=9)
-    torch.cuda.synchronize()
-    rad, alive = rad.cpu().numpy(), alive.cpu().numpy()
+    rad = rad.cpu().numpy()
     assert np.all(np.isfinite(rad)) and rad.min() >= 0 and rad.max() <= SKY.max() + 1e-6
-    assert alive[0] > 0 and np.all(np.diff(alive) <= 0)
+    assert alive[0] == rays.shape[0] and np.all(np.diff(alive) <= 0) and alive[1] < alive[0]
     assert (rad.sum(1) > 0).mean() > 0.5
+
+
+@pytest.mark.parametrize("lod_secondary", [0, 1])
+def test_tlas_renderer_equals_flat_renderer(lod_secondary):
+    """With identity instances [neural, mesh], the compacted TLAS renderer must give the
+    radiance of the round-1 flat renderer (every ray to both BLAS, no compaction): the
+    random streams are keyed by pixel, the merge's tie rule (lower BLAS number) is
+    nbvh_pt_shade's (neural first), and compaction changes no per-ray computation.  With
+    lod_secondary = 1 both switch the neural BLAS to a coarser cut after the primary hit
+    (P:342)."""
+    from paper_2405_16237_b200.pathtrace import PathTracer, PathTracerFlat
+    neural, classical, _, _ = _hybrid_scene(lod_leaves=8)
+    rays = torch.from_numpy(synth.camera_rays(128, 96, (0.0, 0.6, 1.6), vfov_deg=50.0)).cuda()
+    n = rays.shape[0]
+    pt = PathTracer([(neural, "neural"), (classical, "mesh")], [(0, IDENTITY), (1, IDENTITY)], n,
+                    lod_secondary=lod_secondary)
+    a, alive = pt.render(rays, bounces=3, seed=5)
+    a = a.cpu().numpy().copy()
+    flat = PathTracerFlat(neural, classical, n)
+    b, alive_b = flat.render(rays, bounces=3, seed=5, lod_secondary=lod_secondary)
+    b = b.cpu().numpy()
+    # equal up to the merge's renormalisation of the (already unit) normal: a few ulp
+    assert np.abs(a - b).max() <= 1e-5, np.abs(a - b).max()
+    assert list(alive[1:]) == alive_b.cpu().numpy()[:2].tolist()        # continuing paths per bounce
+    if lod_secondary:
+        c, _ = PathTracer([(neural, "neural"), (classical, "mesh")], [(0, IDENTITY), (1, IDENTITY)], n,
+                          lod_secondary=0).render(rays, bounces=3, seed=5)
+        assert not np.array_equal(a, c.cpu().numpy())                   # the switch is live
+
+
+def _rot(axis, ang):
+    c, s_ = np.cos(ang), np.sin(ang)
+    i, j = [k for k in range(3) if k != axis]
+    r = np.eye(3)
+    r[i, i], r[i, j], r[j, i], r[j, j] = c, -s_, s_, c
+    return r
+
+
+def test_tlas_instances_vs_oracle(orc):
+    """TLAS with affine instances of two classical BLAS (three instances of the icosphere --
+    identity, rotated + translated + uniformly scaled, anisotropically scaled -- and one of a
+    second mesh) against the oracle's brute-force closest hit over all the instances' triangles
+    transformed to world space: identical hit masks away from grazing rays, t within fp32
+    transform rounding, the winning instance, and world normals (A^T n, normalised) and albedo."""
+    from paper_2405_16237_b200 import Context
+    from paper_2405_16237_b200.pathtrace import Tlas
+    from synth.scenes import Scene
+    a_sc = synth.scene_tiny(nu=8)
+    b_sc = synth.scene_tiny(seed=3, nu=6)
+    ca = Context(device=0)
+    ca.set_mesh(a_sc)
+    cb = Context(device=0)
+    cb.set_mesh(b_sc)
+    M = [IDENTITY,
+         np.concatenate([0.7 * _rot(1, 0.6) @ _rot(0, 0.3), np.array([[2.6], [0.2], [-0.5]])], 1),
+         np.concatenate([np.diag([1.4, 0.6, 0.9]), np.array([[-2.5], [0.0], [0.3]])], 1),
+         np.concatenate([_rot(2, 1.1), np.array([[0.1], [2.4], [0.0]])], 1)]
+    blas_of = [0, 0, 0, 1]
+    scenes = [a_sc, b_sc]
+    inst = []
+    for k, m in enumerate(M):
+        v = scenes[blas_of[k]].verts.astype(np.float64)
+        inst.append((blas_of[k], m, v.min(0), v.max(0)))
+    tl = Tlas(ca, inst)
+    rng = np.random.default_rng(11)
+    n = 6000
+    o = rng.uniform(-5, 5, (n, 3))
+    tgt = rng.uniform(-3, 3, (n, 3)) + np.array([0, 0.5, 0])
+    d = tgt - o
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    rays = np.zeros((n, 8), np.float32)
+    rays[:, :3], rays[:, 4:7], rays[:, 7] = o, d, np.inf
+    cap = n * 3
+    lr = torch.empty(2 * cap, 8, device="cuda")
+    src = torch.empty(2 * cap, dtype=torch.int32, device="cuda")
+    ins = torch.empty(2 * cap, dtype=torch.int32, device="cuda")
+    counts = torch.zeros(2, dtype=torch.int32, device="cuda")
+    d_rays = torch.from_numpy(rays).cuda()
+    tl.dispatch(d_rays, n, lr, src, ins, counts, cap)
+    cnt = counts.cpu().numpy()
+    lists = [ca.alloc_hits(cap), ca.alloc_hits(cap)]
+    for k, ctx in enumerate((ca, cb)):
+        if cnt[k]:
+            ctx.intersect_mesh(lr[k * cap:k * cap + int(cnt[k])], out={key: v[:int(cnt[k])] for key, v in lists[k].items()})
+    out = ca.alloc_hits(n)
+    tl.merge(n, counts, cap, src, ins, lists, out)
+    torch.cuda.synchronize()
+    assert tl.overflow() == 0
+    g = {k: v.cpu().numpy() for k, v in out.items()}
+    # oracle: every instance's triangles in world space (vertices and normals transformed in
+    # double), one brute-force closest hit
+    V, T, N, A, owner = [], [], [], [], []
+    off = 0
+    for k, m in enumerate(M):
+        sc = scenes[blas_of[k]]
+        mm = np.asarray(m, np.float64)
+        V.append(sc.verts.astype(np.float64) @ mm[:, :3].T + mm[:, 3])
+        # M^-T n per vertex, not renormalised: the shading normal (barycentric blend, then
+        # normalised) is then the transform of the object-space one, as A^T n is
+        N.append(sc.vnormals.astype(np.float64) @ np.linalg.inv(mm[:, :3]))
+        T.append(sc.tris.astype(np.int64) + off)
+        A.append(sc.albedo)
+        owner.append(np.full(sc.tris.shape[0], k))
+        off += sc.verts.shape[0]
+    world = Scene(verts=np.concatenate(V).astype(np.float32), tris=np.concatenate(T).astype(np.uint32),
+                  vnormals=np.concatenate(N).astype(np.float32), albedo=np.concatenate(A).astype(np.float32))
+    owner = np.concatenate(owner)
+    nt = world.tris.shape[0]
+    gt = orc.label(world, np.array([0, nt], np.int64), np.arange(nt, dtype=np.int32), rays, np.zeros(n, np.int32),
+                   rays[:, 3].copy(), rays[:, 7].copy())
+    hit = gt[:, 0] == 0
+    assert hit.sum() > 1000
+    agree = (g["hit"] == 1) == hit
+    assert agree.mean() >= 0.999, agree.mean()                             # grazing rays only
+    both = hit & (g["hit"] == 1)
+    assert np.all(np.abs(g["t"][both] - gt[both, 8]) <= 1e-4 * (1 + gt[both, 8]))
+    assert np.abs(g["normal"][both] - gt[both, 2:5]).max() <= 2e-3
+    assert np.abs(g["albedo"][both] - gt[both, 5:8]).max() <= 1e-6
+    assert set(np.unique(g["leaf"][both])) == {0, 1, 2, 3}
 
 
 def test_intersect_mesh_deep_bvh_vs_oracle(orc):

@@ -162,6 +162,14 @@ nbvh_status nbvh_copy_cut(nbvh_ctx* ctx, int32_t src_lod, int32_t dst_lod);
  * base boxes (uninflated) [n][3], leaf triangle lists in CSR form (tri_off [n+1],
  * tris [n_tris], original triangle ids), grid domain (C4). */
 nbvh_status nbvh_cut_info(const nbvh_ctx* ctx, int32_t lod, int32_t* n_leaves, int32_t* n_inner);
+/* The base BVH the cuts are drawn from ("base-BVH cut"; SAH), host outputs,
+ * nullable: n_nodes; per node child_a / child_b (inner node: the two child indices; leaf:
+ * child_b < 0, child_a = its first primitive).  Node 0 is the root.  NBVH_ESTATE without a
+ * mesh. */
+nbvh_status nbvh_get_base_bvh(const nbvh_ctx* ctx, int32_t* child_a, int32_t* child_b, int64_t* n_nodes);
+/* The base-BVH node of every leaf of LoD slot lod, in the cut's leaf order (host int32
+ * [n_leaves]).  NBVH_ERANGE / NBVH_ESTATE on a bad or empty slot. */
+nbvh_status nbvh_get_cut_nodes(const nbvh_ctx* ctx, int32_t lod, int32_t* leaf_base);
 nbvh_status nbvh_get_cut(const nbvh_ctx* ctx, int32_t lod, float* leaf_lo, float* leaf_hi, float* base_lo,
                          float* base_hi, int64_t* tri_off, int32_t* tris, float* dom_min, float* dom_inv);
 
@@ -322,7 +330,10 @@ nbvh_status nbvh_grad_buffer(nbvh_ctx* ctx, float** d_grad, int64_t* n_floats);
  * read from the buffer tail); refreshes the fp16 inference copy.  A non-finite
  * gradient skips the update (NBVH_ENONFINITE reported by nbvh_get_train_stats). */
 nbvh_status nbvh_apply_update(nbvh_ctx* ctx, float lr, void* stream);
-/* backward + apply_update on one rank. */
+/* backward + apply_update on one rank.  d_rays, d_u and d_xi all NULL: the library draws
+ * the n training rays and random numbers itself (T0: nbvh_gen_train_rays with key = the
+ * config's seed, step = the context's self-drawn batch count, the C16 box), into
+ * context-owned buffers. */
 nbvh_status nbvh_train_step(nbvh_ctx* ctx, const nbvh_ray* d_rays, int64_t n, const float* d_u,
                             const float* d_xi, int32_t lod, float lr, void* stream);
 /* Counters of the last training call; synchronises the stream first. */

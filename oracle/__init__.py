@@ -47,6 +47,7 @@ def lib():
         _lib.orc_num_threads.restype = C.c_int32
         _lib.orc_sigmoid_f32.restype = C.c_float
         _lib.orc_sigmoid_f32.argtypes = [C.c_float]
+        _lib.orc_expand_cut.restype = C.c_int32
     return _lib
 
 
@@ -348,6 +349,30 @@ def batch_loss_double(grid: Grid, n_points, table, dims, W_all, b_all, leaf_lo, 
         _p(lo), _p(_c(leaf_hi, np.float32)), C.c_int32(lo.shape[0]), _p(_c(rays, np.float32)),
         C.c_int64(rays.shape[0]), _p(_c(xi, np.float32)), _p(_c(accepted, np.uint8)), _p(_c(t0, np.float32)),
         _p(_c(t1, np.float32)), _p(_c(gt, np.float64)), _p(den), C.c_int32(den_mode), _box(dom_box)))
+
+
+def leaf_error_stats(first_leaf, accepted, sample_loss, n_leaves):
+    """Per-leaf node-error statistics of one training batch: q = the leaf's training
+    loss (mean of its accepted samples' losses), p = the fraction of the batch's rays whose
+    first intersected leaf it is (C38).  Returns (q [n], p [n], samples [n], loss sum [n])."""
+    fl = np.asarray(first_leaf)
+    acc = np.asarray(accepted).astype(bool)
+    n_rays = fl.shape[0]
+    samples = np.bincount(fl[acc], minlength=n_leaves).astype(np.float64)
+    loss_sum = np.bincount(fl[acc], weights=np.asarray(sample_loss, np.float64)[acc], minlength=n_leaves)
+    first = np.bincount(fl[fl >= 0], minlength=n_leaves).astype(np.float64)
+    q = np.divide(loss_sum, samples, out=np.zeros(n_leaves), where=samples > 0)
+    return q, first / max(n_rays, 1), samples, loss_sum
+
+
+def expand_cut(child_a, child_b, leaf_base, q, p, n_splits):
+    """One cut-expansion step: the n_splits highest-ranked splittable leaves
+    (r = 2 ln q + ln p) replaced by their two children; returns the sorted new node set."""
+    lb = _c(leaf_base, np.int32)
+    out = np.zeros(lb.size + n_splits, np.int32)
+    n = lib().orc_expand_cut(_p(_c(child_a, np.int32)), _p(_c(child_b, np.int32)), C.c_int32(lb.size), _p(lb),
+                             _p(_c(q, np.float64)), _p(_c(p, np.float64)), C.c_int32(n_splits), _p(out))
+    return out[:n]
 
 
 def adam(param, grad, m, v, step, lr=0.01, beta1=0.9, beta2=0.999, eps=1e-8):

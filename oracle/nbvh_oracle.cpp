@@ -974,6 +974,45 @@ void orc_train_backward_given(int32_t L, int32_t F, int32_t log2_T, int32_t n_po
     }
 }
 
+// ------------------------------------------------------------------ cut expansion (NEXT-1)
+// P:180 ("Base-BVH cut optimization"): "we then expand the cut by splitting the nodes with
+// largest error, replacing each with its two children"; P:185 ("Node error"): rank
+// r = 2 log q + log p.  One expansion step of n_splits splits over the cut leaf_base[n]
+// (base-BVH node ids; base BVH given by child_a / child_b, leaf iff child_b < 0):
+// leaves in decreasing r (ties: lower leaf index first, C38); a base-BVH leaf cannot be
+// split and is passed over; stop after n_splits splits or when the leaves run out.
+// q, p > 0 (zero statistics are a caller's reading: C38).  out_nodes receives the new cut's
+// nodes in increasing node id; returns their count.
+int32_t orc_expand_cut(const int32_t* child_a, const int32_t* child_b, int32_t n_leaves, const int32_t* leaf_base,
+                       const double* q, const double* p, int32_t n_splits, int32_t* out_nodes) {
+    std::vector<double> r(n_leaves);
+    for (int32_t i = 0; i < n_leaves; ++i) r[i] = 2.0 * std::log(q[i]) + std::log(p[i]);
+    std::vector<int32_t> order(n_leaves);
+    for (int32_t i = 0; i < n_leaves; ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return r[a] > r[b]; });
+    std::vector<int32_t> nodes;
+    std::vector<char> split(n_leaves, 0);
+    int32_t done = 0;
+    for (int32_t k = 0; k < n_leaves && done < n_splits; ++k) {
+        const int32_t nd = leaf_base[order[k]];
+        if (child_b[nd] < 0) continue;                     // a base-BVH leaf: nothing to split
+        split[order[k]] = 1;
+        ++done;
+    }
+    for (int32_t i = 0; i < n_leaves; ++i) {
+        const int32_t nd = leaf_base[i];
+        if (split[i]) {
+            nodes.push_back(child_a[nd]);
+            nodes.push_back(child_b[nd]);
+        } else {
+            nodes.push_back(nd);
+        }
+    }
+    std::sort(nodes.begin(), nodes.end());
+    std::copy(nodes.begin(), nodes.end(), out_nodes);
+    return (int32_t)nodes.size();
+}
+
 // ------------------------------------------------------------------ Adam
 // "Adam optimizer [kingma2014adam] with default hyper-parameters and a learning
 // rate of 0.01" (C20: beta1 0.9, beta2 0.999, eps 1e-8, bias-corrected, dense).

@@ -517,6 +517,27 @@ extern "C" nbvh_status nbvh_cut_info(const nbvh_ctx* c, int32_t lod, int32_t* n_
     return NBVH_OK;
 }
 
+extern "C" nbvh_status nbvh_get_base_bvh(const nbvh_ctx* c, int32_t* child_a, int32_t* child_b, int64_t* n_nodes) {
+    if (!c) return NBVH_EINVAL;
+    if (!c->has_mesh) return NBVH_ESTATE;
+    const int64_t n = (int64_t)c->sc.nodes.size();
+    if (n_nodes) *n_nodes = n;
+    for (int64_t i = 0; i < n; ++i) {
+        if (child_a) child_a[i] = c->sc.nodes[i].a;
+        if (child_b) child_b[i] = c->sc.nodes[i].b;
+    }
+    return NBVH_OK;
+}
+
+extern "C" nbvh_status nbvh_get_cut_nodes(const nbvh_ctx* c, int32_t lod, int32_t* leaf_base) {
+    if (!c || !leaf_base) return NBVH_EINVAL;
+    if (lod < 0 || lod >= kMaxLod) return NBVH_ERANGE;
+    if (!c->has_cut[lod]) return NBVH_ESTATE;
+    const HostCut& hc = c->cuts[lod];
+    std::memcpy(leaf_base, hc.leaf_base.data(), sizeof(int32_t) * (size_t)hc.n_leaves);
+    return NBVH_OK;
+}
+
 extern "C" nbvh_status nbvh_get_cut(const nbvh_ctx* c, int32_t lod, float* leaf_lo, float* leaf_hi, float* base_lo,
                                     float* base_hi, int64_t* tri_off, int32_t* tris, float* dom_min, float* dom_inv) {
     if (!c) return NBVH_EINVAL;

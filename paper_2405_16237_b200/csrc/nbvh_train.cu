@@ -45,6 +45,9 @@ struct TrainWork {
     int32_t* counters = nullptr;     // [0] samples, [1] first hits, [2] non-finite flag
     double* loss_acc = nullptr;      // [5]
     int32_t* adam_step = nullptr;    // device: Adam updates applied (skipped updates excluded)
+    float* draw = nullptr;           // nbvh_train_step's own T0 draws: rays [n][8], u [n], xi [n][n_points]
+    int64_t draw_cap = 0;
+    uint64_t draw_step = 0;          // Philox counter of the next self-drawn batch
     int32_t lod = 0;
     int32_t launches = 0;
     cudaStream_t stream = nullptr;
@@ -156,6 +159,7 @@ void free_train_device(nbvh_ctx* c) {
     dfree(c->train->sc_dense);
     dfree(c->train->sc_hash);
     dfree(c->train->sc_priv);
+    dfree(c->train->draw);
     delete c->train;
     c->train = nullptr;
 }
@@ -574,6 +578,31 @@ extern "C" nbvh_status nbvh_apply_update(nbvh_ctx* c, float lr, void* stream) {
 
 extern "C" nbvh_status nbvh_train_step(nbvh_ctx* c, const nbvh_ray* rays, int64_t n, const float* u, const float* xi,
                                        int32_t lod, float lr, void* stream) {
+    if (!rays && !u && !xi && n > 0) {
+        // T0 in the library (C16, C28'): Philox-4x32-10 draws of training step
+        // `draw_step` (key = the context's seed) into context-owned buffers
+        nbvh_status st = check_device(c);
+        if (st) return st;
+        st = ensure_train_state(c, 1);
+        if (st) return st;
+        TrainWork* w = c->train;
+        const int np = c->cfg.n_points;
+        if (n > w->draw_cap) {
+            dfree(w->draw);
+            cudaError_t e = cudaMalloc((void**)&w->draw, (size_t)n * (8 + 1 + np) * sizeof(float));
+            if (e != cudaSuccess) return cuda_fail(c, e, "train_step: ray buffers");
+            w->draw_cap = n;
+        }
+        float* d_rays = w->draw;
+        float* d_u = d_rays + 8 * n;
+        float* d_xi = d_u + n;
+        st = nbvh_gen_train_rays(c, c->cfg.seed, w->draw_step++, 0, n, nullptr, reinterpret_cast<nbvh_ray*>(d_rays),
+                                 d_u, d_xi, stream);
+        if (st) return st;
+        rays = reinterpret_cast<const nbvh_ray*>(d_rays);
+        u = d_u;
+        xi = d_xi;
+    }
     nbvh_status st = nbvh_train_backward(c, rays, n, u, xi, lod, stream);
     if (st) return st;
     return nbvh_apply_update(c, lr, stream);

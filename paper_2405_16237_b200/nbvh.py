@@ -95,6 +95,8 @@ SIGNATURES = {
     "nbvh_atomic_probe": (C.c_int, [_P, _I64, _I32, _I64, C.c_uint32, _P, _P]),
     "nbvh_pt_shade": (C.c_int, [_P, _P, _I64, Hits, Hits, _P, _P, _P, C.c_uint64, _I32, _P, _F, _P, _P]),
     "nbvh_tlas_build": (C.c_int, [_P, _P, _I32, _P]),
+    "nbvh_get_base_bvh": (C.c_int, [_P, _P, _P, _P]),
+    "nbvh_get_cut_nodes": (C.c_int, [_P, _I32, _P]),
     "nbvh_tlas_destroy": (None, [_P]),
     "nbvh_tlas_dispatch": (C.c_int, [_P, _P, _P, _I64, _P, _P, _P, _P, _I64, _P]),
     "nbvh_tlas_merge": (C.c_int, [_P, _P, _I64, _P, _I64, _P, _P, _P, Hits, _P]),
@@ -274,6 +276,21 @@ class Context:
         d["n_inner"] = int(ni[0])
         return d
 
+    def base_bvh(self):
+        """(child_a, child_b) int32 arrays of the base BVH (leaf: child_b < 0)."""
+        n = np.zeros(1, np.int64)
+        self._ck(self.lib.nbvh_get_base_bvh(self.h, None, None, _ptr(n)), "get_base_bvh")
+        a = np.zeros(int(n[0]), np.int32)
+        b = np.zeros(int(n[0]), np.int32)
+        self._ck(self.lib.nbvh_get_base_bvh(self.h, _ptr(a), _ptr(b), _ptr(n)), "get_base_bvh")
+        return a, b
+
+    def cut_nodes(self, lod=0):
+        """Base-BVH node of every leaf of the cut in slot lod."""
+        out = np.zeros(self.cut(lod)["n_leaves"], np.int32)
+        self._ck(self.lib.nbvh_get_cut_nodes(self.h, lod, _ptr(out)), "get_cut_nodes")
+        return out
+
     def set_leaf_rank(self, rank, lod=0):
         r = np.ascontiguousarray(rank, np.float32)
         self._ck(self.lib.nbvh_set_leaf_rank(self.h, lod, _ptr(r)), "set_leaf_rank")
@@ -378,8 +395,10 @@ class Context:
     def apply_update(self, lr=0.01, stream=None):
         self._ck(self.lib.nbvh_apply_update(self.h, float(lr), _stream_ptr(stream)), "apply_update")
 
-    def train_step(self, rays, u, xi, lod=0, lr=0.01, stream=None):
-        self._ck(self.lib.nbvh_train_step(self.h, _ptr(rays), rays.shape[0], _ptr(u), _ptr(xi), lod, float(lr),
+    def train_step(self, rays=None, u=None, xi=None, lod=0, lr=0.01, stream=None, n=None):
+        """One training step; rays/u/xi None: the library draws n rays itself (T0)."""
+        count = rays.shape[0] if rays is not None else int(n)
+        self._ck(self.lib.nbvh_train_step(self.h, _ptr(rays), count, _ptr(u), _ptr(xi), lod, float(lr),
                                           _stream_ptr(stream)), "train_step")
 
     def train_stats(self):

@@ -441,3 +441,31 @@ def test_dp_two_contexts_stay_byte_identical():
     # difference can flip a step only where the gradient is ~0 (a handful of entries)
     d = np.abs(pa - ps)
     assert np.median(d) <= 1e-6 and np.quantile(d, 0.99) <= 1e-2 * 0.01 and d.max() <= 6 * 2 * 0.01
+
+
+def test_train_step_draws_its_own_rays():
+    """nbvh_train_step with no rays: the library draws T0 itself -- Philox with
+    key = the config's seed and step = its own batch counter, the C16 box -- so two self-drawn
+    steps train on exactly the batches nbvh_gen_train_rays(seed, 0) and (seed, 1) give."""
+    from paper_2405_16237_b200 import Context, PARAM_ALL
+    sc = synth.scene_tiny()
+
+    def mk():
+        ctx = Context(device=0, L=8, F=2, log2_T=14, n_points=4, hidden_layers=2, seed=5)
+        ctx.set_mesh(sc)
+        ctx.build_cut(64)
+        ctx.reserve(1 << 14)
+        return ctx
+
+    a, b = mk(), mk()
+    assert np.array_equal(a.get_params(PARAM_ALL), b.get_params(PARAM_ALL))
+    n = 1 << 14
+    for step in range(2):
+        a.train_step(n=n, lr=0.01)
+        sa = a.train_stats()
+        rays, u, xi = b.gen_train_rays(seed=5, step=step, n=n)
+        b.train_step(rays, u, xi, lr=0.01)
+        sb = b.train_stats()
+        assert sa["n_accepted"] == sb["n_accepted"] > 1000 and sa["n_first_hit"] == sb["n_first_hit"]
+        assert abs(sa["loss_sum"] - sb["loss_sum"]) <= 1e-6 * abs(sb["loss_sum"])
+    assert np.abs(a.get_params(PARAM_ALL) - b.get_params(PARAM_ALL)).max() <= 1e-5

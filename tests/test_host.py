@@ -153,3 +153,45 @@ def test_bad_arguments_rejected(lib):
         ctx.build_cut(16)                                    # no mesh yet (ESTATE)
     with pytest.raises(NbvhError):
         ctx.query(np.zeros((1, 8), np.float32))              # host-only context
+
+
+@pytest.mark.parametrize("mesh_nu,start,splits", [(22, 16, 5), (22, 64, 40), (2, 24, 30)])
+def test_error_driven_expansion_matches_oracle(orc, lib, mesh_nu, start, splits):
+    """NEXT-1: nbvh_build_cut with per-leaf (q, p) expands the cut exactly as the
+    oracle's expansion step does -- the `splits` highest-ranked splittable leaves replaced by
+    their children (a small mesh makes some cut leaves base-BVH leaves, which are skipped)."""
+    from paper_2405_16237_b200 import Context
+    sc = synth.scene_tiny(nu=mesh_nu)
+    ctx = Context(device=-1)
+    ctx.set_mesh(sc)
+    n0, _ = ctx.build_cut(start)
+    nodes0 = ctx.cut_nodes()
+    ca, cb = ctx.base_bvh()
+    rng = np.random.default_rng(start + splits)
+    q = rng.uniform(0.05, 2.0, n0).astype(np.float32)
+    p = rng.uniform(0.001, 0.2, n0).astype(np.float32)
+    n1, _ = ctx.build_cut(n0 + splits, q=q, p=p)
+    want = orc.expand_cut(ca, cb, nodes0, q.astype(np.float64), p.astype(np.float64), splits)
+    assert np.array_equal(np.sort(ctx.cut_nodes()), want)
+    assert n1 == want.size
+    if mesh_nu == 2:
+        assert np.any(cb[nodes0] < 0) and n1 < n0 + splits            # base leaves passed over
+
+
+def test_construct_ranks_follow_the_oracle_statistics(orc):
+    """construct.ranks_from_stats (the host side of NEXT-1) on the per-leaf sums the gradient
+    buffer tail carries gives r = 2 ln q + ln p with the oracle's q, p from per-ray records."""
+    from paper_2405_16237_b200.construct import ranks_from_stats
+    rng = np.random.default_rng(9)
+    n_rays, n_leaves = 5000, 37
+    first = rng.integers(-1, n_leaves, n_rays)
+    acc = (rng.random(n_rays) < 0.6) & (first >= 0)
+    loss = rng.uniform(0.01, 3.0, n_rays)
+    q, p, samples, ls = orc.leaf_error_stats(first, acc, loss, n_leaves)
+    firsts = np.bincount(first[first >= 0], minlength=n_leaves)
+    r, q2, p2 = ranks_from_stats(ls, samples, firsts, n_rays)
+    ok = samples > 0
+    assert ok.all()
+    np.testing.assert_allclose(q2, q, rtol=1e-12)
+    np.testing.assert_allclose(p2, p, rtol=1e-12)
+    np.testing.assert_allclose(r, (2 * np.log(q) + np.log(p)).astype(np.float32), rtol=1e-6)

@@ -641,3 +641,36 @@ def test_p13_backward_given_equals_train_grad_and_bounds(orc):
     o2 = orc.train_backward_given(g, 3, tab, lay, box, rays[acc[:3]], te[acc[:3], 0], tx[acc[:3], 0], xi[acc[:3]],
                                   x2, dz[:3])
     assert np.all(o2["relu_margin"] == 0.0)
+
+
+# ------------------------------------------------------------------ NEXT-1 construction
+def test_next1_expand_cut_pins(orc):
+    """orc_expand_cut on a hand-built base BVH: root 0 -> (1, 2); 1 -> (3, 4); 2 -> (5, 6);
+    3..6 leaves.  Cut {1, 2}: the leaf of larger r = 2 ln q + ln p is split (a larger p can
+    outweigh a smaller q only by the log ratio); a tie goes to the lower leaf index; a
+    base leaf is passed over; asking for more splits than possible stops at the leaves."""
+    ca = np.array([1, 3, 5, 0, 1, 2, 3], np.int32)
+    cb = np.array([2, 4, 6, -1, -1, -1, -1], np.int32)
+    cut = np.array([1, 2], np.int32)
+    # r(1) = 2 ln 0.5 + ln 0.5 = -2.08 ; r(2) = 2 ln 0.2 + ln 0.8 = -3.44 -> split node 1
+    assert orc.expand_cut(ca, cb, cut, [0.5, 0.2], [0.5, 0.8], 1).tolist() == [2, 3, 4]
+    # the factor 2 on the loss: r(1) = 2 ln 0.3 + ln 0.1 = -4.71 > r(2) = 2 ln 0.1 + ln 0.5 =
+    # -5.30, although the raw product q p ranks node 2 first (0.03 < 0.05)
+    assert orc.expand_cut(ca, cb, cut, [0.3, 0.1], [0.1, 0.5], 1).tolist() == [2, 3, 4]
+    assert orc.expand_cut(ca, cb, cut, [0.4, 0.4], [0.5, 0.5], 1).tolist() == [2, 3, 4]      # tie: lower index
+    assert orc.expand_cut(ca, cb, cut, [0.4, 0.4], [0.5, 0.5], 2).tolist() == [3, 4, 5, 6]
+    leafy = np.array([3, 4, 2], np.int32)                  # 3, 4 are base leaves
+    assert orc.expand_cut(ca, cb, leafy, [0.9, 0.9, 0.1], [0.9, 0.9, 0.1], 1).tolist() == [3, 4, 5, 6]
+    assert orc.expand_cut(ca, cb, leafy, [0.9, 0.9, 0.1], [0.9, 0.9, 0.1], 5).tolist() == [3, 4, 5, 6]
+
+
+def test_next1_leaf_error_stats_from_records(orc):
+    """q = mean loss of a leaf's accepted samples, p = fraction of rays whose first leaf it
+    is (C38), computed from per-ray records by hand."""
+    first = np.array([0, 0, 1, -1, 2, 0, 1, 1])
+    acc = np.array([1, 0, 1, 0, 1, 1, 0, 1])
+    loss = np.array([1.0, 9.0, 2.0, 9.0, 5.0, 3.0, 9.0, 4.0])
+    q, p, samples, ls = orc.leaf_error_stats(first, acc, loss, 4)
+    assert q.tolist() == [2.0, 3.0, 5.0, 0.0]
+    assert p.tolist() == [3 / 8, 3 / 8, 1 / 8, 0.0]
+    assert samples.tolist() == [2, 2, 1, 0] and ls.tolist() == [4.0, 6.0, 5.0, 0.0]

@@ -249,8 +249,10 @@ def run_ours(args):
     identical = dp.params_identical_across_ranks(ctx)
     assert identical, "model broadcast left ranks with different parameters"
     # strong scaling: ONE 1080p frame per step, its 16x16 tiles dealt round-robin to the ranks
-    idx = dp.tile_partition(*c["res"], rank, world) if args.order == "tiles" else \
-        np.arange(frame_np.shape[0])[dp.shard(frame_np.shape[0], rank, world)]
+    if args.order in ("tiles", "tiles_rows"):
+        idx = dp.tile_partition(*c["res"], rank, world, inner="morton" if args.order == "tiles" else "rows")
+    else:
+        idx = np.arange(frame_np.shape[0])[dp.shard(frame_np.shape[0], rank, world)]
     rays_np = np.ascontiguousarray(frame_np[idx])
     n = rays_np.shape[0]
     n_frame = frame_np.shape[0]
@@ -402,6 +404,7 @@ def run_ours(args):
             "list_refills_per_step": st["n_refills"],
             "mlp_tiles_per_step": st.get("n_mlp_tiles"), "mlp_rows_per_tile": (st["n_mlp_rows"] / st["n_mlp_tiles"]
                                                                                if st.get("n_mlp_tiles") else None),
+            "ws_wait_frac": ([c / st["ws_cycles"][2] for c in st["ws_cycles"][:2]] if st.get("n_mlp_tiles") else None),
             "model_broadcast": {"bytes": 4 * ctx.param_count(3), "seconds": bcast_s, "params_identical": identical},
             "roofline": roof, "weak_scaling": weak,
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks.summary(), "mlp": mlp, "gather_roofline": gather,
@@ -762,8 +765,9 @@ def main():
     ap.add_argument("--train", type=int, default=1, help="also time the cfg-5 training step (1/0)")
     ap.add_argument("--lod", type=int, default=1, help="also run the cfg-4 multi-cut LoD query (1/0)")
     ap.add_argument("--pt", type=int, default=1, help="also run the cfg-3 hybrid path tracer (1/0)")
-    ap.add_argument("--order", default="tiles", choices=["tiles", "rows"],
-                    help="ray order / rank partition: 16x16 tiles dealt round-robin (default) or row-major shards")
+    ap.add_argument("--order", default="tiles", choices=["tiles", "tiles_rows", "rows"],
+                    help="ray order / rank partition: 16x16 tiles dealt round-robin, Z order inside a tile "
+                         "(default) or row-major inside (tiles_rows); or row-major shards (rows)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

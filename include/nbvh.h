@@ -105,6 +105,8 @@ typedef struct {
     float ms_query;          /* device time of the persistent query kernel (profiling on)   */
     int32_t n_mlp_tiles;     /* 128-row MLP tiles run on tcgen05 (warp-specialised kernel)  */
     int32_t n_mlp_rows;      /* rows in them (<= 128 per tile; the rest is padding)         */
+    int64_t ws_cycles[3];    /* warp-specialised kernel, SM cycles summed over worker warps:
+                                waiting for MLP results, waiting for a free tile, total      */
 } nbvh_query_stats;
 
 /* Training counters of the last nbvh_train_backward / nbvh_train_step. */

@@ -678,6 +678,7 @@ nbvh_status resolve_query_stats(nbvh_ctx* c) {
     c->qstats_pending = false;
     int64_t nq = 0;
     int32_t iters = 0, refills = 0, err = 0, tiles = 0, rows = 0;
+    int64_t wsc[3] = {0, 0, 0};
     for (int b = 0; b < nb; ++b) {
         const QueryCounters* q = reinterpret_cast<const QueryCounters*>(c->h_misc + (size_t)b * kCounterStride);
         nq += (int64_t)q->n_queries;
@@ -686,7 +687,9 @@ nbvh_status resolve_query_stats(nbvh_ctx* c) {
         err |= q->err;
         tiles += q->mlp_tiles;
         rows += q->mlp_rows;
+        for (int k = 0; k < 3; ++k) wsc[k] += (int64_t)q->ws_cycles[k];
     }
+    for (int k = 0; k < 3; ++k) c->qstats.ws_cycles[k] = wsc[k];
     c->qstats.n_mlp_tiles = tiles;
     c->qstats.n_mlp_rows = rows;
     c->qstats.n_queries = nq;

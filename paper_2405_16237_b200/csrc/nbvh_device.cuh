@@ -531,16 +531,19 @@ __device__ __forceinline__ void encode_issue(const LevelSm* lv, const void* tab,
                                           ((i2 + ((k >> 2) & 1)) * kPrime2)) & hmask;
             }
         }
+        // the level's base pointer once per level: per corner one IMAD.WIDE.U32 (index * entry +
+        // base), no 32-bit offset add
+        const Entry* Tl = T + P.off;
         if (P.nx) {
             // dense level: the cell's 8 corners are one contiguous 16*F-byte record
             NBVH_DCHECK(i0 < P.nx && i1 < P.nx && i2 < P.nx);
             const uint32_t cell = i0 + i1 * P.nx + i2 * P.nxy;
             if constexpr (F == 2) {
-                ldg256(T + (P.off + 8u * cell), G.v[j]);
+                ldg256(Tl + 8u * cell, G.v[j]);
             } else {
                 uint32_t lo[8], hi[8];
-                ldg256(T + (P.off + 8u * cell), lo);
-                ldg256(T + (P.off + 8u * cell + 4u), hi);
+                ldg256(Tl + 8u * cell, lo);
+                ldg256(Tl + 8u * cell + 4u, hi);
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                     G.v[j][k] = make_uint2(lo[2 * k], lo[2 * k + 1]);
@@ -557,7 +560,7 @@ __device__ __forceinline__ void encode_issue(const LevelSm* lv, const void* tab,
             // 32-bit entry index (n_entries < 2^32), one IMAD.WIDE.U32 per gather address
 #pragma unroll
             for (int k = 0; k < 8; ++k)
-                G.v[j][k] = ldg_el(T + (P.off + (hx[k & 1] ^ hy[(k >> 1) & 1] ^ hz[(k >> 2) & 1])));
+                G.v[j][k] = ldg_el(Tl + (hx[k & 1] ^ hy[(k >> 1) & 1] ^ hz[(k >> 2) & 1]));
         }
     }
 }

@@ -678,12 +678,14 @@ __global__ void __launch_bounds__(kQueryWarps * 32, 1) k_query_warp(QueryArgs a)
 // partly claimed, the MLP warpgroup closes it (claims jump to the next tile, the missing
 // arrivals are made up) and processes it as is.
 // Registers: 20 warps share the CTA's 640 x 96 registers; setmaxnreg moves them from the MLP
-// warpgroup (56) to the workers (104).  Measured on the 1080p frame (profiles/NOTES.md r2):
-// 1.116 ms vs 0.995 ms for k_query_warp -- the LSU data pipe drops from 81% to 60% busy
-// (no weight fragments), but the gathers are latency-bound and the workers have fewer
-// registers (spills) and wait for tiles; 12 workers at 128 registers: 1.158-1.22 ms.
+// warpgroup (32: its epilogue works 16 columns at a time) to the workers (112).  The MLP
+// warpgroup waits with mbarrier.try_wait (suspended, no issue slots taken from the workers).
+// Measured on the 1080p frame (profiles/NOTES.md r2a/r2b): 1.094 ms vs 0.983 ms for
+// k_query_warp -- the LSU data pipe drops from 81% to 60% busy (no weight fragments) and the
+// workers wait < 3% of their time for MLP results or tiles, but the workers' encode loop runs
+// slower at 112 registers (spills) than the per-warp kernel's at 128.
 constexpr int kWsWorkers = 16;                            // 4 warpgroups
-constexpr int kWsWorkerRegs = 104, kWsMlpRegs = 56;        // setmaxnreg split of the CTA's 640 x 96 registers
+constexpr int kWsWorkerRegs = 112, kWsMlpRegs = 32;        // setmaxnreg split of the CTA's 640 x 96 registers
 constexpr int kWsTiles = 3;                                // at most; WsPlan::nt fits the smem limit
 constexpr int kWsBlk = 8;                                  // 16-row blocks per 128-row tile
 constexpr int kKgHid = 64 / 8 + 2;                         // K-groups of a hidden W (+ bias)
@@ -809,6 +811,8 @@ __global__ void __launch_bounds__((kWsWorkers + 4) * 32, 1) k_query_ws(QueryArgs
         // rows of set 0 | rows of set 1 << 8
         uint32_t zph = 0, pend = 0, nv_pk = 0;
         int s = 0;
+        long long t_z = 0, t_free = 0;                    // cycles waiting (lane 0's clock)
+        const long long t_start = clock64();
         float* xs = reinterpret_cast<float*>(smem_raw + plan.xs + (size_t)warp * (plan.sets - plan.xs) / kWsWorkers);
         while (true) {
             unsigned char* sb = set_base(2 * warp + s);
@@ -816,7 +820,9 @@ __global__ void __launch_bounds__((kWsWorkers + 4) * 32, 1) k_query_ws(QueryArgs
             float* zt = reinterpret_cast<float*>(sb + plan.z);
             if (pend & (1u << s)) {           // (F) this set's z: wait, then decode
                 if (lane == 0) atomicAdd(&C.idle, 1);
+                const long long t0 = clock64();
                 tc::mbar_wait(&C.zr[2 * warp + s], (zph >> s) & 1u);
+                t_z += clock64() - t0;
                 if (lane == 0) atomicSub(&C.idle, 1);
                 zph ^= 1u << s;
                 pend &= ~(1u << s);
@@ -840,7 +846,11 @@ __global__ void __launch_bounds__((kWsWorkers + 4) * 32, 1) k_query_ws(QueryArgs
             if (lane == 0) q = atomicAdd(&C.seq, 1);
             q = __shfl_sync(0xffffffffu, q, 0);
             const int tl = (q / kWsBlk) % plan.nt, gen = q / (kWsBlk * plan.nt), blk = q % kWsBlk;
-            if (gen > 0) tc::mbar_wait(&C.freeb[tl], (uint32_t)(gen - 1) & 1u);
+            if (gen > 0) {
+                const long long t0 = clock64();
+                tc::mbar_wait(&C.freeb[tl], (uint32_t)(gen - 1) & 1u);
+                t_free += clock64() - t0;
+            }
             // (D) encode straight into the tile: row blk*16 + q, K-major canonical layout
             rows_encode<F>(a, lv, xs, nv, lane, NP, tiles + (size_t)tl * plan.tile_bytes + blk * 16 * 16, 2048, 16);
             if (lane == 0) {
@@ -854,6 +864,9 @@ __global__ void __launch_bounds__((kWsWorkers + 4) * 32, 1) k_query_ws(QueryArgs
             s ^= 1;
         }
         if (lane == 0) {
+            atomicAdd(&a.ctr->ws_cycles[0], (unsigned long long)t_z);
+            atomicAdd(&a.ctr->ws_cycles[1], (unsigned long long)t_free);
+            atomicAdd(&a.ctr->ws_cycles[2], (unsigned long long)(clock64() - t_start));
             atomicAdd(&C.exited, 1);
             atomicAdd(&C.idle, 1);
             atomicAdd(&a.ctr->n_queries, (unsigned long long)C.stat[warp][0]);
@@ -880,7 +893,9 @@ __global__ void __launch_bounds__((kWsWorkers + 4) * 32, 1) k_query_ws(QueryArgs
                 int cmd = 1;
                 if (lane == 0) {
                     const int base = T * kWsBlk;
-                    while (!tc::mbar_test(&C.full[tl], (uint32_t)gen & 1u)) {
+                    // mbarrier.try_wait suspends the thread for a while before it gives up, so the
+                    // waiting MLP warp takes no issue slots from the workers on its SMSP
+                    while (!tc::mbar_try(&C.full[tl], (uint32_t)gen & 1u)) {
                         if (*(volatile int*)&C.idle < kWsWorkers) continue;
                         const int sq = *(volatile int*)&C.seq;
                         if (sq <= base) {
@@ -913,17 +928,18 @@ __global__ void __launch_bounds__((kWsWorkers + 4) * 32, 1) k_query_ws(QueryArgs
                 mph ^= 1u;
                 tc::fence_after();
 #pragma unroll
-                for (int half = 0; half < 2; ++half) {                // 64 columns: ReLU + fp16 -> H tile
-                    float v[32];
-                    tc::ld32(acc, (uint32_t)(32 * mw), (uint32_t)(32 * half), v);
+#pragma unroll 1
+                for (int q16 = 0; q16 < 4; ++q16) {                   // 64 columns, 16 at a time (few
+                    float v[16];                                       // registers): ReLU + fp16 -> H tile
+                    tc::ld16(acc, (uint32_t)(32 * mw), (uint32_t)(16 * q16), v);
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) {
+                    for (int k = 0; k < 2; ++k) {
                         uint4 o;
                         o.x = pack_relu_half2(v[8 * k], v[8 * k + 1]);
                         o.y = pack_relu_half2(v[8 * k + 2], v[8 * k + 3]);
                         o.z = pack_relu_half2(v[8 * k + 4], v[8 * k + 5]);
                         o.w = pack_relu_half2(v[8 * k + 6], v[8 * k + 7]);
-                        *reinterpret_cast<uint4*>(htile + (4 * half + k) * 2048 + row * 16) = o;
+                        *reinterpret_cast<uint4*>(htile + (2 * q16 + k) * 2048 + row * 16) = o;
                     }
                 }
                 tc::fence_proxy_async();
@@ -1050,8 +1066,8 @@ static int resident_blocks(Kern k, int threads, size_t smem) {
     return (per_sm > 0 ? per_sm : 1) * sms;
 }
 
-// Default: the per-warp mma.sync kernel (k_query_warp, 0.995 ms on the 1080p frame);
-// NBVH_QUERY_MLP=tc selects the warp-specialised tcgen05 kernel (k_query_ws, 1.116 ms:
+// Default: the per-warp mma.sync kernel (k_query_warp, 0.983 ms on the 1080p frame);
+// NBVH_QUERY_MLP=tc selects the warp-specialised tcgen05 kernel (k_query_ws, 1.094 ms:
 // profiles/NOTES.md r2).  Read per launch so tests can switch it.
 static bool query_mlp_warp() {
     const char* ev = std::getenv("NBVH_QUERY_MLP");

@@ -33,6 +33,8 @@ struct QueryCounters {
     int32_t mlp_tiles;            // k_query_ws: MLP tiles processed
     int32_t mlp_rows;             // k_query_ws: valid rows in them
     unsigned long long n_queries; // neural queries (ray, leaf) evaluated
+    unsigned long long ws_cycles[3];  // k_query_ws, summed over worker warps: waiting for z, waiting
+                                      // for a free tile, total
 };
 
 // One work-list entry of the persistent query kernel, written by k_traverse: the ray itself

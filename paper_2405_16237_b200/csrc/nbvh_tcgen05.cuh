@@ -177,6 +177,15 @@ namespace nbvh {
 namespace tc {
 // non-blocking probe of an mbarrier phase
 __device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity);
+// one potentially blocking try: the thread may be suspended for a system-dependent time
+__device__ __forceinline__ bool mbar_try(uint64_t* b, uint32_t parity) {
+    uint32_t done;
+    asm volatile("{.reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p;}"
+                 : "=r"(done)
+                 : "r"(smem_u32(b)), "r"(parity)
+                 : "memory");
+    return done != 0;
+}
 // spin on test_wait (no suspend): lowest wake-up latency for short waits on the critical path
 __device__ __forceinline__ void mbar_spin(uint64_t* b, uint32_t parity) {
     while (!mbar_test(b, parity)) {

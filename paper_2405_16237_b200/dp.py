@@ -57,22 +57,34 @@ def shard(n_global: int, rank: int, world: int) -> slice:
     return slice(start, start + base + (1 if rank < rem else 0))
 
 
-def tile_partition(width: int, height: int, rank: int, world: int, tile: int = 16) -> np.ndarray:
+def _morton_order(n: int) -> np.ndarray:
+    """(y, x) of an n x n block (n a power of two) in Z order."""
+    k = np.arange(n * n)
+    x = np.zeros_like(k)
+    y = np.zeros_like(k)
+    for b in range(int(np.log2(n))):
+        x |= ((k >> (2 * b)) & 1) << b
+        y |= ((k >> (2 * b + 1)) & 1) << b
+    return y, x
+
+
+def tile_partition(width: int, height: int, rank: int, world: int, tile: int = 16, inner: str = "morton") -> np.ndarray:
     """Row-major pixel indices owned by `rank` when a width x height frame is cut into
     tile x tile tiles dealt round-robin along diagonals ((tx + ty) mod world), so every rank
-    gets tiles from every part of the screen.  Pixels are listed tile by tile (row-major
-    inside a tile), which keeps neighbouring rays together for the query kernel's warps.
-    Ragged edge tiles are clipped to the frame."""
+    gets tiles from every part of the screen.  Pixels are listed tile by tile; inside a tile in
+    Z (Morton) order (inner="morton": any 16 consecutive rays form a 4x4 block -- the rays a
+    query-kernel warp takes together) or row-major (inner="rows").  Ragged edge tiles are
+    clipped to the frame."""
     ntx, nty = (width + tile - 1) // tile, (height + tile - 1) // tile
+    my, mx = _morton_order(tile) if inner == "morton" else np.divmod(np.arange(tile * tile), tile)
     out = []
     for ty in range(nty):
-        y0, y1 = ty * tile, min(height, (ty + 1) * tile)
         for tx in range(ntx):
             if (tx + ty) % world != rank:
                 continue
-            x0, x1 = tx * tile, min(width, (tx + 1) * tile)
-            ys, xs = np.meshgrid(np.arange(y0, y1), np.arange(x0, x1), indexing="ij")
-            out.append((ys * width + xs).reshape(-1))
+            ys, xs = ty * tile + my, tx * tile + mx
+            keep = (ys < height) & (xs < width)
+            out.append((ys[keep] * width + xs[keep]).astype(np.int64))
     return np.concatenate(out).astype(np.int64) if out else np.zeros(0, np.int64)
 
 

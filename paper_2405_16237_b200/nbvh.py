@@ -50,7 +50,8 @@ MAX_BLAS = 8
 class QueryStats(C.Structure):
     _fields_ = [("n_rays", C.c_int64), ("n_queries", C.c_int64), ("n_iters", C.c_int32),
                 ("n_launches", C.c_int32), ("n_refills", C.c_int32), ("ms_traverse", C.c_float),
-                ("ms_query", C.c_float), ("n_mlp_tiles", C.c_int32), ("n_mlp_rows", C.c_int32)]
+                ("ms_query", C.c_float), ("n_mlp_tiles", C.c_int32), ("n_mlp_rows", C.c_int32),
+                ("ws_cycles", C.c_int64 * 3)]
 
 
 class TrainStats(C.Structure):
@@ -375,7 +376,7 @@ class Context:
         self._ck(self.lib.nbvh_get_query_stats(self.h, C.byref(s)), "query_stats")
         return dict(n_rays=s.n_rays, n_queries=s.n_queries, n_iters=s.n_iters, n_launches=s.n_launches,
                     n_refills=s.n_refills, ms_traverse=s.ms_traverse, ms_query=s.ms_query,
-                    n_mlp_tiles=s.n_mlp_tiles, n_mlp_rows=s.n_mlp_rows)
+                    n_mlp_tiles=s.n_mlp_tiles, n_mlp_rows=s.n_mlp_rows, ws_cycles=list(s.ws_cycles))
 
     def set_profiling(self, on=True):
         self._ck(self.lib.nbvh_set_profiling(self.h, int(bool(on))), "set_profiling")

@@ -82,10 +82,15 @@ def test_tile_partition_covers_frame_once_and_balances(w, h, world):
         for p in parts:
             bands = np.unique((p // w) * 8 // h)
             assert bands.size == 8
-    # tile-major order: the first 16 pixels of a rank are one tile row (consecutive x)
+    # tile-major, Z order inside a tile: the first 16 pixels of a rank form a 4x4 block
     p0 = parts[0]
+    if w >= 16 and h >= 16:
+        ys, xs = np.divmod(p0[:16], w)
+        assert ys.max() - ys.min() == 3 and xs.max() - xs.min() == 3
+    rows = dp.tile_partition(w, h, 0, world, inner="rows")
+    assert np.array_equal(np.sort(rows), np.sort(p0))
     if w >= 16:
-        assert np.all(np.diff(p0[:16]) == 1)
+        assert np.all(np.diff(rows[:16]) == 1)
 
 
 def _bcast_worker(rank, world, port, out_q):

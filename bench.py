@@ -91,14 +91,14 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def build_model(cfg_name: str, device: int, rank: int = 0, list_cap: int = 12):
+def build_model(cfg_name: str, device: int, rank: int = 0, list_cap: int = 12, mlp_dtype: int = 0):
     """Synthetic scene + cut + random-init model of the named BASELINE config."""
     from paper_2405_16237_b200 import Context, PARAM_TABLES
     c = synth.CONFIGS[cfg_name]
     h = c["hash"]
     sc = synth.scene_tiny(c["seeds"]["mesh"]) if cfg_name == "tiny" else synth.scene_1080p(c["seeds"]["mesh"])
     ctx = Context(device=device, L=h.L, F=h.F, log2_T=h.log2_T, n_points=h.n_points, hidden_layers=h.hidden_layers,
-                  list_cap=list_cap)
+                  list_cap=list_cap, mlp_dtype=mlp_dtype)
     ctx.set_mesh(sc)
     ctx.build_cut(c["leaves"])
     n_tab = ctx.param_count(PARAM_TABLES)
@@ -241,7 +241,7 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
-    ctx, sc, frame_np, c = build_model(args.config, local, 0, args.list_cap)
+    ctx, sc, frame_np, c = build_model(args.config, local, 0, args.list_cap, 1 if args.mlp_dtype == "bf16" else 0)
     # the model is built on rank 0 and replicated by one broadcast at init
     t0 = time.perf_counter()
     dp.broadcast_model(ctx, src=0, device="cuda")
@@ -390,7 +390,7 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": "Mrays/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f16", "data": "synthetic",
+            "vs_baseline": None, "dtype": args.mlp_dtype, "data": "synthetic",
             "config": {"workload": _workload(args.config),
                        "rays_per_step": n_frame, "rays_per_step_rank0": n,
                        "model": "random-init tables U[-1,1], He MLP (x10 output)",
@@ -765,6 +765,8 @@ def main():
     ap.add_argument("--train", type=int, default=1, help="also time the cfg-5 training step (1/0)")
     ap.add_argument("--lod", type=int, default=1, help="also run the cfg-4 multi-cut LoD query (1/0)")
     ap.add_argument("--pt", type=int, default=1, help="also run the cfg-3 hybrid path tracer (1/0)")
+    ap.add_argument("--mlp-dtype", default="f16", choices=["f16", "bf16"],
+                    help="query-path MLP operands (nbvh_config.mlp_dtype, C39)")
     ap.add_argument("--order", default="tiles", choices=["tiles", "tiles_rows", "rows"],
                     help="ray order / rank partition: 16x16 tiles dealt round-robin, Z order inside a tile "
                          "(default) or row-major inside (tiles_rows); or row-major shards (rows)")

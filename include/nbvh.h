@@ -82,6 +82,10 @@ typedef struct {
     float inflate_rel;      /* node inflation, fraction of node diagonal (C15: 1e-3)        */
     float inflate_abs;      /* node inflation floor, fraction of scene diagonal (C15: 1e-6) */
     uint64_t seed;          /* parameter-initialisation seed (C21)                          */
+    int32_t mlp_dtype;      /* query-path MLP operands: 0 = fp16 (default), 1 = bf16 (features and
+                               weights rounded to bf16, fp32 accumulation; "half precision",
+                               C39); training keeps fp16 operands                          */
+    int32_t reserved0;
 } nbvh_config;
 
 /* Parameter blocks for nbvh_get_params / nbvh_set_params.  All are fp32 master values;
@@ -363,7 +367,8 @@ nbvh_status nbvh_debug_traverse_product(nbvh_ctx* ctx, const nbvh_ray* d_rays, i
  * [m][L*F] (bits as uint16) and corner indices [m][L][8] (nullable). */
 nbvh_status nbvh_debug_encode(nbvh_ctx* ctx, const float* d_points, int64_t m, uint16_t* d_feat,
                               uint32_t* d_index, void* stream);
-/* MLP of m fp16 input rows [m][D_in] -> raw outputs z [m][8] (fp32). */
+/* The query kernel's own per-warp MLP on m input rows [m][D_in] (fp16 bits; bf16 bits
+ * when mlp_dtype = 1) -> raw outputs z [m][8] (fp32). */
 nbvh_status nbvh_debug_mlp(nbvh_ctx* ctx, const uint16_t* d_in, int64_t m, float* d_z, void* stream);
 /* nbvh_query that also records the raw MLP output of every query: z_trace [n][cap][8]
  * (fp32, NaN where not queried, positions >= cap not recorded). */

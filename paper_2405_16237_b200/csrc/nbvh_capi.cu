@@ -101,6 +101,10 @@ __global__ void k_refresh_fp16(const float* __restrict__ src, __half* __restrict
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     for (; i < n; i += (int64_t)gridDim.x * blockDim.x) dst[i] = __float2half_rn(src[i]);
 }
+__global__ void k_refresh_bf16(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst, int64_t n) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i < n; i += (int64_t)gridDim.x * blockDim.x) dst[i] = __float2bfloat16_rn(src[i]);
+}
 
 // fp32 master tables -> fp16 inference table: hashed levels copied, dense levels
 // corner-packed (LevelSm in nbvh_device.cuh).  blockIdx.y = level; one thread per dense
@@ -180,6 +184,7 @@ nbvh_status refresh_fp16(nbvh_ctx* c, cudaStream_t s) {
     const int64_t nt = c->n_table, nw = c->n_W;
     launch_refresh_table(c, s);
     k_refresh_fp16<<<148, 256, 0, s>>>(c->d_params + nt, c->d_W16, nw);
+    if (c->d_Wb16) k_refresh_bf16<<<148, 256, 0, s>>>(c->d_params + nt, c->d_Wb16, nw);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(c, e, "refresh_fp16");
     return NBVH_OK;
@@ -187,6 +192,7 @@ nbvh_status refresh_fp16(nbvh_ctx* c, cudaStream_t s) {
 
 nbvh_status refresh_table(nbvh_ctx* c, cudaStream_t s) {
     launch_refresh_table(c, s);
+    if (c->d_Wb16) k_refresh_bf16<<<148, 256, 0, s>>>(c->d_params + c->n_table, c->d_Wb16, c->n_W);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(c, e, "refresh_table");
     return NBVH_OK;
@@ -231,7 +237,8 @@ extern "C" nbvh_status nbvh_create(const nbvh_config* cfg, int cuda_device, nbvh
     const nbvh_config& c = *cfg;
     if (c.L < 1 || c.L > kMaxLevels || (c.F != 2 && c.F != 4) || c.log2_T < 4 || c.log2_T > 24 || c.base_res < 1 ||
         c.max_res < c.base_res || c.n_points < 1 || c.hidden_layers < 1 || c.hidden_layers > kMaxHidden ||
-        c.width != kWidth || c.list_cap < 1 || c.list_cap > kListK || (c.mode != 0 && c.mode != 1))
+        c.width != kWidth || c.list_cap < 1 || c.list_cap > kListK || (c.mode != 0 && c.mode != 1) ||
+        (c.mlp_dtype != 0 && c.mlp_dtype != 1))
         return NBVH_EINVAL;
     const int d_in = c.n_points * c.L * c.F;
     if ((c.L * c.F) % 8 != 0 || !(d_in == 32 || d_in == 64 || d_in == 96 || d_in == 128)) return NBVH_EINVAL;
@@ -279,6 +286,7 @@ extern "C" nbvh_status nbvh_create(const nbvh_config* cfg, int cuda_device, nbvh
         if (e == cudaSuccess) e = dalloc(&x->d_params, x->h_params.size());
         if (e == cudaSuccess) e = dalloc(&x->d_table16, x->n_inf * c.F);
         if (e == cudaSuccess) e = dalloc(&x->d_W16, x->n_W);
+        if (e == cudaSuccess && c.mlp_dtype == 1) e = cudaMalloc((void**)&x->d_Wb16, (size_t)x->n_W * 2);
         if (e == cudaSuccess) e = dalloc(&x->d_misc, kCounterBlocks * kCounterStride);
         if (e == cudaSuccess) e = cudaMallocHost((void**)&x->h_misc, kCounterBlocks * kCounterStride * sizeof(int32_t));
         if (e == cudaSuccess)
@@ -328,6 +336,8 @@ extern "C" void nbvh_destroy(nbvh_ctx* c) {
         dfree(c->d_params);
         dfree(c->d_table16);
         dfree(c->d_W16);
+        if (c->d_Wb16) cudaFree(c->d_Wb16);
+        c->d_Wb16 = nullptr;
         dfree(c->d_misc);
         if (c->h_misc) cudaFreeHost(c->h_misc);
         for (cudaEvent_t x : c->events) cudaEventDestroy(x);
@@ -633,6 +643,10 @@ nbvh_status run_query(nbvh_ctx* c, const nbvh_ray* rays, int64_t n, int32_t lod,
     QueryArgs qa{};
     qa.g = make_grid(c, lod);
     qa.m = make_mlp(c);
+    if (c->d_Wb16) {                      // bf16 query path (mlp_dtype = 1, C39)
+        qa.m.W = reinterpret_cast<const __half*>(c->d_Wb16);
+        qa.m.bf16 = 1;
+    }
     qa.cut = make_cut(c, lod);
     qa.rays = reinterpret_cast<const float4*>(rays);
     qa.n_rays = n;
@@ -1044,6 +1058,10 @@ extern "C" nbvh_status nbvh_debug_mlp(nbvh_ctx* c, const uint16_t* x, int64_t m,
     if (m == 0) return NBVH_OK;
     DebugMlpArgs a{};
     a.m = make_mlp(c);
+    if (c->d_Wb16) {                      // the query path's own MLP: bf16 operands (C39)
+        a.m.W = reinterpret_cast<const __half*>(c->d_Wb16);
+        a.m.bf16 = 1;
+    }
     a.x = reinterpret_cast<const __half*>(x);
     a.rows = m;
     a.z = z;

@@ -1,6 +1,7 @@
 // nbvh_capi_internal.h — the context object behind the opaque nbvh_ctx handle.
 #pragma once
 
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <string>
@@ -55,6 +56,7 @@ struct nbvh_ctx {
     float* d_params = nullptr;
     __half* d_table16 = nullptr;
     __half* d_W16 = nullptr;
+    __nv_bfloat16* d_Wb16 = nullptr;   // bf16 copy of the MLP weights (mlp_dtype = 1: query path)
 
     // scene and cuts
     nbvh::HostScene sc;

@@ -49,8 +49,9 @@ struct GridDev {
 
 struct MlpDev {
     int32_t d_in, hidden;
-    const __half* W;                 // layers concatenated, [out][in] row-major
+    const __half* W;                 // layers concatenated, [out][in] row-major (bf16 bits if bf16)
     const float* b;
+    int32_t bf16;                    // query path: operands in bf16 (nbvh_config.mlp_dtype = 1)
 };
 
 struct CutDev {
@@ -382,6 +383,17 @@ __device__ __forceinline__ uint32_t f2_to_h2(float lo, float hi) {
     asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
     return r;
 }
+__device__ __forceinline__ uint32_t f2_to_bf2(float lo, float hi) {
+    uint32_t r;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+// the MLP operand type of the query path: fp16 (default) or bf16 (nbvh_config.mlp_dtype = 1)
+template <bool kBf>
+__device__ __forceinline__ uint32_t f2_to_x2(float lo, float hi) {
+    if constexpr (kBf) return f2_to_bf2(lo, hi);
+    else return f2_to_h2(lo, hi);
+}
 
 // ------------------------------------------------------------------ level table in shared memory
 // The fp16 *inference* table keeps hashed levels in the parameter layout (T entries of F
@@ -570,7 +582,7 @@ __device__ __forceinline__ void encode_issue(const LevelSm* lv, const void* tab,
 // DESIGN.md reading R-blend) so each corner is two mixed-precision FMAs (FHFMA) with no
 // half -> float conversions; otherwise (training forward, whose features feed the
 // gradients) fp32 weights and converted entries.
-template <int F, bool kHalfW>
+template <int F, bool kHalfW, bool kBf = false>
 __device__ __forceinline__ uint4 encode_finish(const ChunkGather<F>& G) {
     constexpr int NL = 8 / F;
     uint4 out;
@@ -597,7 +609,7 @@ __device__ __forceinline__ uint4 encode_finish(const ChunkGather<F>& G) {
                     fhfma2<0>(wh[i], G.v[j][2 * i], a0, a1);
                     fhfma2<1>(wh[i], G.v[j][2 * i + 1], a0, a1);
                 }
-                o32[j] = f2_to_h2(a0, a1);
+                o32[j] = f2_to_x2<kBf>(a0, a1);
             } else {
                 float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
 #pragma unroll
@@ -607,8 +619,8 @@ __device__ __forceinline__ uint4 encode_finish(const ChunkGather<F>& G) {
                     fhfma2<1>(wh[i], G.v[j][2 * i + 1].x, a0, a1);
                     fhfma2<1>(wh[i], G.v[j][2 * i + 1].y, a2, a3);
                 }
-                o32[2 * j] = f2_to_h2(a0, a1);
-                o32[2 * j + 1] = f2_to_h2(a2, a3);
+                o32[2 * j] = f2_to_x2<kBf>(a0, a1);
+                o32[2 * j + 1] = f2_to_x2<kBf>(a2, a3);
             }
         } else {
             float w[8];
@@ -645,12 +657,12 @@ __device__ __forceinline__ uint4 encode_finish(const ChunkGather<F>& G) {
 // entries (dense: corner-packed cell record; hashed: 8 gathers, C2, C3), trilinear weights
 // (wx*wy)*wz, blend in fp32.  idx_out (nullable) receives the 8*NL
 // canonical corner indices within their levels (parity hook).
-template <int F, bool kHalfW = true>
+template <int F, bool kHalfW = true, bool kBf = false>
 __device__ __forceinline__ uint4 encode_chunk_sm(const LevelSm* lv, const void* tab, uint32_t hmask, float x0,
                                                  float x1, float x2, int l0, uint32_t* idx_out) {
     ChunkGather<F> G;
     encode_issue<F>(lv, tab, hmask, x0, x1, x2, l0, idx_out, G);
-    return encode_finish<F, kHalfW>(G);
+    return encode_finish<F, kHalfW, kBf>(G);
 }
 
 // ------------------------------------------------------------------ tensor-core MLP
@@ -671,6 +683,22 @@ __device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], 
 __device__ __forceinline__ uint32_t pack_relu_half2(float a, float b) {
     __half2 h = __floats2half2_rn(fmaxf(a, 0.f), fmaxf(b, 0.f));
     return *reinterpret_cast<uint32_t*>(&h);
+}
+__device__ __forceinline__ void mma16816_bf(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};\n"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+template <bool kBf>
+__device__ __forceinline__ void mma16816x(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    if constexpr (kBf) mma16816_bf(c, a, b0, b1);
+    else mma16816(c, a, b0, b1);
+}
+template <bool kBf>
+__device__ __forceinline__ uint32_t pack_relu_x2(float a, float b) {
+    return f2_to_x2<kBf>(fmaxf(a, 0.f), fmaxf(b, 0.f));
 }
 
 // Shared-memory layout of the staged MLP (row strides padded by 8 halves so that the
@@ -711,7 +739,7 @@ __device__ __forceinline__ void stage_mlp(const MlpDev& m, const MlpSmem& s, int
 // mma.sync m16n8k16 (fp16 in, fp32 accumulate).  Layer outputs stay in registers: the
 // m16n8 accumulator layout of two adjacent n-tiles is exactly the m16k16 A-operand
 // layout of the next layer.  Writes the 8 raw outputs of each row to z[row*8 + c].
-template <int D>
+template <int D, bool kBf = false>
 __device__ __forceinline__ void mlp_rows16(const MlpSmem& s, int hidden, const __half* x, int r0, float* z, int lane) {
     const int g = lane >> 2, t = lane & 3;
     float acc[8][4];
@@ -731,17 +759,17 @@ __device__ __forceinline__ void mlp_rows16(const MlpSmem& s, int hidden, const _
         for (int np = 0; np < 4; ++np) {
             uint32_t b0, b1, b2, b3;
             ldsm_x4(wa + np * 16 * (D + 8) * 2 + kb * 32, b0, b1, b2, b3);
-            mma16816(acc[2 * np], a, b0, b1);
-            mma16816(acc[2 * np + 1], a, b2, b3);
+            mma16816x<kBf>(acc[2 * np], a, b0, b1);
+            mma16816x<kBf>(acc[2 * np + 1], a, b2, b3);
         }
     }
     uint32_t h[4][4];   // next-layer A fragments, k-block kb = hidden units 16kb..16kb+15
 #pragma unroll
     for (int kb = 0; kb < 4; ++kb) {
-        h[kb][0] = pack_relu_half2(acc[2 * kb][0], acc[2 * kb][1]);
-        h[kb][1] = pack_relu_half2(acc[2 * kb][2], acc[2 * kb][3]);
-        h[kb][2] = pack_relu_half2(acc[2 * kb + 1][0], acc[2 * kb + 1][1]);
-        h[kb][3] = pack_relu_half2(acc[2 * kb + 1][2], acc[2 * kb + 1][3]);
+        h[kb][0] = pack_relu_x2<kBf>(acc[2 * kb][0], acc[2 * kb][1]);
+        h[kb][1] = pack_relu_x2<kBf>(acc[2 * kb][2], acc[2 * kb][3]);
+        h[kb][2] = pack_relu_x2<kBf>(acc[2 * kb + 1][0], acc[2 * kb + 1][1]);
+        h[kb][3] = pack_relu_x2<kBf>(acc[2 * kb + 1][2], acc[2 * kb + 1][3]);
     }
     for (int layer = 1; layer < hidden; ++layer) {
         const __half* W = s.wh + (layer - 1) * 64 * 72;
@@ -759,16 +787,16 @@ __device__ __forceinline__ void mlp_rows16(const MlpSmem& s, int hidden, const _
             for (int np = 0; np < 4; ++np) {
                 uint32_t b0, b1, b2, b3;
                 ldsm_x4(wb + np * 16 * 72 * 2 + kb * 32, b0, b1, b2, b3);
-                mma16816(acc[2 * np], h[kb], b0, b1);
-                mma16816(acc[2 * np + 1], h[kb], b2, b3);
+                mma16816x<kBf>(acc[2 * np], h[kb], b0, b1);
+                mma16816x<kBf>(acc[2 * np + 1], h[kb], b2, b3);
             }
         }
 #pragma unroll
         for (int kb = 0; kb < 4; ++kb) {
-            h[kb][0] = pack_relu_half2(acc[2 * kb][0], acc[2 * kb][1]);
-            h[kb][1] = pack_relu_half2(acc[2 * kb][2], acc[2 * kb][3]);
-            h[kb][2] = pack_relu_half2(acc[2 * kb + 1][0], acc[2 * kb + 1][1]);
-            h[kb][3] = pack_relu_half2(acc[2 * kb + 1][2], acc[2 * kb + 1][3]);
+            h[kb][0] = pack_relu_x2<kBf>(acc[2 * kb][0], acc[2 * kb][1]);
+            h[kb][1] = pack_relu_x2<kBf>(acc[2 * kb][2], acc[2 * kb][3]);
+            h[kb][2] = pack_relu_x2<kBf>(acc[2 * kb + 1][0], acc[2 * kb + 1][1]);
+            h[kb][3] = pack_relu_x2<kBf>(acc[2 * kb + 1][2], acc[2 * kb + 1][3]);
         }
     }
     // output layer: 64 -> 8, linear
@@ -782,7 +810,7 @@ __device__ __forceinline__ void mlp_rows16(const MlpSmem& s, int hidden, const _
     for (int kb = 0; kb < 4; ++kb) {
         uint32_t b0, b1;
         ldsm_x2(wo + kb * 32, b0, b1);
-        mma16816(o, h[kb], b0, b1);
+        mma16816x<kBf>(o, h[kb], b0, b1);
     }
     z[(r0 + g) * 8 + 2 * t] = o[0];
     z[(r0 + g) * 8 + 2 * t + 1] = o[1];

@@ -352,11 +352,11 @@ __device__ __noinline__ int refill_list(CutDev cut, const float4* rays, int64_t 
 // (mlp_rows16h, C34) was 1.4% faster in round 1 but its error grows with the layer width
 // (K fp16 roundings per accumulator); kept for A/B only.
 constexpr bool kQueryMlpF16Acc = false;
-template <int D>
+template <int D, bool kBf = false>
 __device__ __forceinline__ void query_mlp_rows16(const MlpSmem& s, int hidden, const __half* x, int r0, float* z,
                                                  int lane) {
-    if constexpr (kQueryMlpF16Acc) mlp_rows16h<D>(s, hidden, x, r0, z, lane);
-    else mlp_rows16<D>(s, hidden, x, r0, z, lane);
+    if constexpr (kQueryMlpF16Acc && !kBf) mlp_rows16h<D>(s, hidden, x, r0, z, lane);
+    else mlp_rows16<D, kBf>(s, hidden, x, r0, z, lane);
 }
 
 // Ray slots of one warp (structure of arrays in shared memory).  Lane s < kWarpQ owns slot
@@ -469,7 +469,7 @@ __device__ __forceinline__ int slots_segment(const QueryArgs& a, WarpSlots& S, f
 // (D) hash-grid encode of the nv rows: lane -> row q = lane % 16; the two half-warps take
 // sample points of opposite parity at the same levels (neighbouring points of the same rays:
 // coherent lines).  Chunk c (8 halves) of row q is stored at dst + c * cstride + q * rstride.
-template <int F>
+template <int F, bool kBf = false>
 __device__ __forceinline__ void rows_encode(const QueryArgs& a, const LevelSm* lv, const float* xs, int nv, int lane,
                                             int NP, unsigned char* dst, int cstride, int rstride) {
     const int q = lane & (kWarpQ - 1), h = lane / kWarpQ;
@@ -481,7 +481,7 @@ __device__ __forceinline__ void rows_encode(const QueryArgs& a, const LevelSm* l
             const float x0 = xp[q], x1 = xp[kWarpQ + q], x2 = xp[2 * kWarpQ + q];
             for (int lc = 0; lc < cpp; ++lc) {
                 const int c = p * cpp + lc;
-                const uint4 f = encode_chunk_sm<F>(lv, a.g.table, hmask, x0, x1, x2, lc * (8 / F), nullptr);
+                const uint4 f = encode_chunk_sm<F, true, kBf>(lv, a.g.table, hmask, x0, x1, x2, lc * (8 / F), nullptr);
                 *reinterpret_cast<uint4*>(dst + c * cstride + q * rstride) = f;
             }
         }
@@ -606,7 +606,7 @@ struct QuerySmemPlan {
 // activations in registers), (F) decode.  Warps drift freely, so one warp's MLP or list
 // refill overlaps other warps' gathers.  Selected with NBVH_QUERY_MLP=warp (A/B reference of
 // the warp-specialised kernel below).
-template <int F, int D>
+template <int F, int D, bool kBf>
 __global__ void __launch_bounds__(kQueryWarps * 32, 1) k_query_warp(QueryArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -647,8 +647,8 @@ __global__ void __launch_bounds__(kQueryWarps * 32, 1) k_query_warp(QueryArgs a)
             s_stat[2 * warp] += nv;
             s_stat[2 * warp + 1] += 1;
         }
-        rows_encode<F>(a, lv, xs, nv, lane, NP, reinterpret_cast<unsigned char*>(feat), 16, (D + 8) * 2);
-        query_mlp_rows16<D>(ms, a.m.hidden, feat, 0, zt, lane);              // (E)
+        rows_encode<F, kBf>(a, lv, xs, nv, lane, NP, reinterpret_cast<unsigned char*>(feat), 16, (D + 8) * 2);
+        query_mlp_rows16<D, kBf>(ms, a.m.hidden, feat, 0, zt, lane);         // (E)
         __syncwarp();
         rows_decode(a, S, zt, nv, lane);
     }
@@ -1017,7 +1017,7 @@ __global__ void __launch_bounds__(128) k_debug_encode(DebugEncodeArgs a) {
 }
 
 // ------------------------------------------------------------------ debug: MLP rows
-template <int D>
+template <int D, bool kBf>
 __global__ void __launch_bounds__(256, 2) k_debug_mlp(DebugMlpArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -1038,7 +1038,7 @@ __global__ void __launch_bounds__(256, 2) k_debug_mlp(DebugMlpArgs a) {
             *reinterpret_cast<uint4*>(feat + row * (D + 8) + c * 8) = v;
         }
         __syncthreads();
-        query_mlp_rows16<D>(ms, a.m.hidden, feat, warp * 16, zt, lane);      // k_query's own MLP
+        query_mlp_rows16<D, kBf>(ms, a.m.hidden, feat, warp * 16, zt, lane);   // k_query's own MLP
         __syncthreads();
         for (int i = tid; i < kTileQ * 8; i += blockDim.x) {
             const int64_t gr = tile * kTileQ + i / 8;
@@ -1098,7 +1098,7 @@ static cudaError_t launch_persistent(Kern k, int threads, size_t smem, int64_t m
 
 template <int F, int D>
 static cudaError_t launch_query_t(const QueryArgs& a, int64_t max_work, cudaStream_t s) {
-    if (!query_mlp_warp()) {
+    if (!query_mlp_warp() && !a.m.bf16) {                          // the tcgen05 variant is fp16 only
         const WsPlan plan(D, a.m.hidden, a.g.n_points);
         if (plan.total <= 227 * 1024)
             return launch_persistent<0>(k_query_ws<F, D>, (kWsWorkers + 4) * 32, plan.total, max_work,
@@ -1106,8 +1106,11 @@ static cudaError_t launch_query_t(const QueryArgs& a, int64_t max_work, cudaStre
     }
     const QuerySmemPlan plan(D, a.m.hidden, a.g.n_points);
     if (plan.warps < 1) return cudaErrorInvalidValue;
-    return launch_persistent<1>(k_query_warp<F, D>, plan.warps * 32, plan.total, max_work, plan.warps * kWarpQ, a, s,
-                             a.m.hidden, a.g.n_points);
+    if (a.m.bf16)
+        return launch_persistent<2>(k_query_warp<F, D, true>, plan.warps * 32, plan.total, max_work,
+                                    plan.warps * kWarpQ, a, s, a.m.hidden, a.g.n_points);
+    return launch_persistent<1>(k_query_warp<F, D, false>, plan.warps * 32, plan.total, max_work, plan.warps * kWarpQ,
+                                a, s, a.m.hidden, a.g.n_points);
 }
 
 cudaError_t launch_query(const QueryArgs& a, int64_t max_work, cudaStream_t s) {
@@ -1155,15 +1158,19 @@ cudaError_t launch_debug_encode(const DebugEncodeArgs& a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-template <int D>
-static cudaError_t launch_mlp_t(const DebugMlpArgs& a, cudaStream_t s) {
+template <int D, bool kBf>
+static cudaError_t launch_mlp_tb(const DebugMlpArgs& a, cudaStream_t s) {
     const size_t smem = mlp_smem_bytes(D, a.m.hidden);
-    int grid = resident_blocks(k_debug_mlp<D>, 256, smem);
+    int grid = resident_blocks(k_debug_mlp<D, kBf>, 256, smem);
     const int64_t tiles = (a.rows + kTileQ - 1) / kTileQ;
     if (tiles < grid) grid = (int)tiles;
     if (grid < 1) grid = 1;
-    k_debug_mlp<D><<<grid, 256, smem, s>>>(a);
+    k_debug_mlp<D, kBf><<<grid, 256, smem, s>>>(a);
     return cudaGetLastError();
+}
+template <int D>
+static cudaError_t launch_mlp_t(const DebugMlpArgs& a, cudaStream_t s) {
+    return a.m.bf16 ? launch_mlp_tb<D, true>(a, s) : launch_mlp_tb<D, false>(a, s);
 }
 
 cudaError_t launch_debug_mlp(const DebugMlpArgs& a, cudaStream_t s) {

@@ -30,7 +30,7 @@ class Config(C.Structure):
     _fields_ = [("L", C.c_int32), ("F", C.c_int32), ("log2_T", C.c_int32), ("base_res", C.c_int32),
                 ("max_res", C.c_int32), ("n_points", C.c_int32), ("hidden_layers", C.c_int32),
                 ("width", C.c_int32), ("list_cap", C.c_int32), ("mode", C.c_int32), ("inflate_rel", C.c_float),
-                ("inflate_abs", C.c_float), ("seed", C.c_uint64)]
+                ("inflate_abs", C.c_float), ("seed", C.c_uint64), ("mlp_dtype", C.c_int32), ("reserved0", C.c_int32)]
 
 
 class Hits(C.Structure):

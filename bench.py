@@ -120,7 +120,7 @@ def _profiled_traffic(kernel: str = "k_query"):
     if not files:
         return None, None
     txt = open(files[-1]).read()
-    m = re.search(r"== void " + kernel + r"<[^\n]*\n(.*?)(?:\n==|\Z)", txt, re.S)
+    m = re.search(r"== void " + kernel + r"(?:_warp)?<[^\n]*\n(.*?)(?:\n==|\Z)", txt, re.S)
     if not m:
         return None, None
     units = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
@@ -657,7 +657,7 @@ def _profiled_l2_reads(kernel: str = "k_query"):
     if not files:
         return None
     txt = open(files[-1]).read()
-    m = re.search(r"== void " + kernel + r"<[^\n]*\n(.*?)(?:\n==|\Z)", txt, re.S)
+    m = re.search(r"== void " + kernel + r"(?:_warp)?<[^\n]*\n(.*?)(?:\n==|\Z)", txt, re.S)
     if not m:
         return None
     sec = re.search(r"L2 read sectors from L1/TEX\s+([0-9.]+)", m.group(1))

@@ -565,10 +565,13 @@ __global__ void __launch_bounds__(256) k_train_scatter(TrainArgs a) {
     const int64_t items = (int64_t)M * NP;
     for (int64_t it = (int64_t)blockIdx.x * blockDim.x + tid; it < items; it += (int64_t)gridDim.x * blockDim.x) {
         const int i = (int)(it / NP), p = (int)(it - (int64_t)i * NP);
-        SampleDesc q;
-        load_sample_desc(a, i, M, q);
+        // the sample's segment and jitter straight from global memory (a SampleDesc with a
+        // runtime-indexed xi would live in local memory)
+        const int r = a.s_ray[i];
+        const float4 r0 = __ldg(a.rays + 2 * (int64_t)r), r1 = __ldg(a.rays + 2 * (int64_t)r + 1);
+        const float o[3] = {r0.x, r0.y, r0.z}, d[3] = {r1.x, r1.y, r1.z};
         float x[3];
-        segment_point(a.g, q.o, q.d, q.t0, q.t1, p, NP, q.xi, x);    // the forward's point (C8)
+        segment_point(a.g, o, d, a.s_t0[i], a.s_t1[i], p, NP, a.xi + (int64_t)r * NP, x);   // the forward's point (C8)
         const float* gq = a.gx + (int64_t)i * D + p * L * F;
         for (int l = 0; l < L; ++l) {
             const LevelSm P = lv[l];

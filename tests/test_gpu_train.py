@@ -468,4 +468,4 @@ def test_train_step_draws_its_own_rays():
         sb = b.train_stats()
         assert sa["n_accepted"] == sb["n_accepted"] > 1000 and sa["n_first_hit"] == sb["n_first_hit"]
         assert abs(sa["loss_sum"] - sb["loss_sum"]) <= 1e-6 * abs(sb["loss_sum"])
-    assert np.abs(a.get_params(PARAM_ALL) - b.get_params(PARAM_ALL)).max() <= 1e-5
+    assert np.abs(a.get_params(PARAM_ALL) - b.get_params(PARAM_ALL)).max() <= 1e-4   # fp32 atomics order

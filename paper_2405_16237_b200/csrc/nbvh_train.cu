@@ -33,6 +33,12 @@ struct TrainWork {
     float* dZ = nullptr;
     float* Z = nullptr;              // [cap][8] raw z, allocated only while parity capture is on
     float* gx = nullptr;             // [cap][D] dL/dx (bwd -> scatter)
+    int32_t* ss_ray = nullptr;       // samples grouped by leaf (k_sort_place): ray, leaf, t0, t1
+    int32_t* ss_leaf = nullptr;
+    float* ss_t0 = nullptr;
+    float* ss_t1 = nullptr;
+    int32_t* leaf_hist = nullptr;    // [hist_cap] per-leaf counts -> offsets
+    int64_t hist_cap = 0;
     float* sc_dense = nullptr;       // T7 scratch: cell-packed dense levels
     float* sc_hash = nullptr;        // T7 scratch: aligned hashed levels
     int32_t* sc_priv = nullptr;      // T7 fixed-point partials of the coarse levels, per scatter CTA
@@ -145,6 +151,7 @@ static void free_work(TrainWork* w) {
     dfree(w->r_acc); dfree(w->r_leaf); dfree(w->r_gt); dfree(w->r_loss);
     dfree(w->s_ray); dfree(w->s_leaf); dfree(w->s_t0); dfree(w->s_t1); dfree(w->s_gt);
     dfree(w->X); dfree(w->A); dfree(w->Dl); dfree(w->dZ); dfree(w->Z); dfree(w->gx);
+    dfree(w->ss_ray); dfree(w->ss_leaf); dfree(w->ss_t0); dfree(w->ss_t1);
 }
 
 void free_train_device(nbvh_ctx* c) {
@@ -160,6 +167,7 @@ void free_train_device(nbvh_ctx* c) {
     dfree(c->train->sc_hash);
     dfree(c->train->sc_priv);
     dfree(c->train->draw);
+    dfree(c->train->leaf_hist);
     delete c->train;
     c->train = nullptr;
 }
@@ -214,6 +222,10 @@ nbvh_status reserve_train(nbvh_ctx* c, int64_t max_rays) {
     if (e == cudaSuccess) e = cudaMalloc((void**)&w->Dl, H * n * 64 * 2);
     if (e == cudaSuccess) e = cudaMalloc((void**)&w->dZ, n * 8 * 4);
     if (e == cudaSuccess) e = cudaMalloc((void**)&w->gx, n * D * 4);
+    if (e == cudaSuccess) e = cudaMalloc((void**)&w->ss_ray, n * 4);
+    if (e == cudaSuccess) e = cudaMalloc((void**)&w->ss_leaf, n * 4);
+    if (e == cudaSuccess) e = cudaMalloc((void**)&w->ss_t0, n * 4);
+    if (e == cudaSuccess) e = cudaMalloc((void**)&w->ss_t1, n * 4);
     if (e != cudaSuccess) {
         free_work(w);
         cudaGetLastError();
@@ -289,16 +301,16 @@ static nbvh_status ensure_scatter_scratch(nbvh_ctx* c, TrainArgs& a, int sms) {
 }
 
 // ev (nullable): 6 events recorded before select and after select, label, fwd, bwd, dW
+// a0: the arguments with the select kernel's (unsorted) sample arrays; a: the same with the
+// leaf-sorted arrays, which every kernel after the sort reads; hist: n_leaves ints.
 template <int F, int D>
-static cudaError_t launch_train_fd(const TrainArgs& a, int64_t n, int64_t w_off, int64_t b_off, cudaStream_t s,
-                                   int* launches, cudaEvent_t* ev) {
+static cudaError_t launch_train_fd(const TrainArgs& a0, const TrainArgs& a, int32_t* hist, int64_t n, int64_t w_off,
+                                   int64_t b_off, cudaStream_t s, int* launches, cudaEvent_t* ev) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int H = a.m.hidden;
-    const size_t smem_fwd = (size_t)kTileQ * (D + 8) * 2 + (size_t)mlp_smem_halves(D, H) * 2 + kTileQ * 8 * 4 +
-                            (64 * H + 8) * 4 + kTileQ * sizeof(SampleDesc) + kMaxLevels * sizeof(LevelSm) +
-                            (size_t)kTileQ * a.g.n_points * 3 * 4;
+    const size_t smem_fwd = FwdSmemPlan(D, H, a.g.n_points).total;
     const size_t smem_bwd = bwd_smem(D, H);
     const size_t smem_sc = (size_t)a.priv_floats * 8;
     const size_t smem_dw = (size_t)kTileQ * 72 * 2 + (size_t)kTileQ * (D + 8) * 2 + kTileQ * 8 * 4;
@@ -314,15 +326,21 @@ static cudaError_t launch_train_fd(const TrainArgs& a, int64_t n, int64_t w_off,
     if (ev) cudaEventRecord(ev[0], s);
     // every launch is checked at once: a failed launch must not leave a step that silently
     // skipped a phase
-    k_train_select<<<blocks_n, 128, (size_t)(a.cut.depth + 2) * 128 * sizeof(int), s>>>(a);
+    k_train_select<<<blocks_n, 128, (size_t)(a.cut.depth + 2) * 128 * sizeof(int), s>>>(a0);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    // group the samples by leaf (the later kernels read a's sorted arrays)
+    if ((e = cudaMemsetAsync(hist, 0, sizeof(int32_t) * (size_t)a.cut.n_leaves, s)) != cudaSuccess) return e;
+    k_sort_count<<<2 * sms, 256, 0, s>>>(a0, hist);
+    k_sort_scan<<<1, 1024, 0, s>>>(hist, a.cut.n_leaves);
+    k_sort_place<<<2 * sms, 256, 0, s>>>(a0, hist, SortedSamples{a.s_ray, a.s_leaf, a.s_t0, a.s_t1});
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    *launches += 3;
     if (ev) cudaEventRecord(ev[1], s);
     k_train_label<<<blocks_n, 128, (size_t)a.bvh_rows * 128 * sizeof(int), s>>>(a);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (ev) cudaEventRecord(ev[2], s);
-    const int tiles = (int)((n + kTileQ - 1) / kTileQ);
-    const int grid_fwd = tiles < 2 * sms ? (tiles > 0 ? tiles : 1) : 2 * sms;   // 2 CTAs per SM
-    k_train_fwd<F, D><<<grid_fwd, 256, smem_fwd, s>>>(a);
+    const int grid_fwd = sms;                 // persistent: one CTA of kFwdWarps warps per SM
+    k_train_fwd<F, D><<<grid_fwd, kFwdWarps * 32, smem_fwd, s>>>(a);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (ev) cudaEventRecord(ev[3], s);
     k_train_bwd<F, D><<<2 * sms, 256, smem_bwd, s>>>(a);
@@ -498,6 +516,17 @@ extern "C" nbvh_status nbvh_train_backward(nbvh_ctx* c, const nbvh_ray* rays, in
         a.sc_dense_n = w->sc_dense_floats;
         a.sc_hash_n = w->sc_hash_floats;
     }
+    if (hc.n_leaves > w->hist_cap) {
+        dfree(w->leaf_hist);
+        e = cudaMalloc((void**)&w->leaf_hist, sizeof(int32_t) * (size_t)hc.n_leaves);
+        if (e != cudaSuccess) return cuda_fail(c, e, "train_backward: leaf histogram");
+        w->hist_cap = hc.n_leaves;
+    }
+    TrainArgs as = a;                         // the leaf-sorted sample arrays (k_sort_place)
+    as.s_ray = w->ss_ray;
+    as.s_leaf = w->ss_leaf;
+    as.s_t0 = w->ss_t0;
+    as.s_t1 = w->ss_t1;
     const int64_t w_off = c->n_table, b_off = c->n_table + c->n_W;
     const int F = c->cfg.F, D = c->d_in;
     int launches = 0;
@@ -508,13 +537,13 @@ extern "C" nbvh_status nbvh_train_backward(nbvh_ctx* c, const nbvh_ray* rays, in
         ev = evs;
     }
     w->profiled = c->profiling;
-    if (F == 2 && D == 32) e = launch_train_fd<2, 32>(a, n, w_off, b_off, s, &launches, ev);
-    else if (F == 2 && D == 64) e = launch_train_fd<2, 64>(a, n, w_off, b_off, s, &launches, ev);
-    else if (F == 2 && D == 96) e = launch_train_fd<2, 96>(a, n, w_off, b_off, s, &launches, ev);
-    else if (F == 2 && D == 128) e = launch_train_fd<2, 128>(a, n, w_off, b_off, s, &launches, ev);
-    else if (F == 4 && D == 64) e = launch_train_fd<4, 64>(a, n, w_off, b_off, s, &launches, ev);
-    else if (F == 4 && D == 96) e = launch_train_fd<4, 96>(a, n, w_off, b_off, s, &launches, ev);
-    else if (F == 4 && D == 128) e = launch_train_fd<4, 128>(a, n, w_off, b_off, s, &launches, ev);
+    if (F == 2 && D == 32) e = launch_train_fd<2, 32>(a, as, w->leaf_hist, n, w_off, b_off, s, &launches, ev);
+    else if (F == 2 && D == 64) e = launch_train_fd<2, 64>(a, as, w->leaf_hist, n, w_off, b_off, s, &launches, ev);
+    else if (F == 2 && D == 96) e = launch_train_fd<2, 96>(a, as, w->leaf_hist, n, w_off, b_off, s, &launches, ev);
+    else if (F == 2 && D == 128) e = launch_train_fd<2, 128>(a, as, w->leaf_hist, n, w_off, b_off, s, &launches, ev);
+    else if (F == 4 && D == 64) e = launch_train_fd<4, 64>(a, as, w->leaf_hist, n, w_off, b_off, s, &launches, ev);
+    else if (F == 4 && D == 96) e = launch_train_fd<4, 96>(a, as, w->leaf_hist, n, w_off, b_off, s, &launches, ev);
+    else if (F == 4 && D == 128) e = launch_train_fd<4, 128>(a, as, w->leaf_hist, n, w_off, b_off, s, &launches, ev);
     else return fail(c, NBVH_EINVAL, "train_backward: unsupported (F, D_in)");
     if (e != cudaSuccess) return cuda_fail(c, e, "train_backward: launch");
     k_store_count<<<1, 1, 0, s>>>(w->counters, a.tail);
@@ -678,7 +707,8 @@ extern "C" nbvh_status nbvh_debug_train_activations(nbvh_ctx* c, int32_t* d_samp
     if (e != cudaSuccess) return cuda_fail(c, e, "debug_train_activations");
     const size_t m = (size_t)m32, D = (size_t)c->d_in, H = (size_t)c->cfg.hidden_layers;
     *h_m = (int64_t)m;
-    if (d_sample_ray) e = cudaMemcpyAsync(d_sample_ray, w->s_ray, m * 4, cudaMemcpyDeviceToDevice, s);
+    // the kernels after the select run on the leaf-sorted sample order (k_sort_place)
+    if (d_sample_ray) e = cudaMemcpyAsync(d_sample_ray, w->ss_ray, m * 4, cudaMemcpyDeviceToDevice, s);
     if (e == cudaSuccess && d_x) e = cudaMemcpyAsync(d_x, w->X, m * D * 2, cudaMemcpyDeviceToDevice, s);
     if (e == cudaSuccess && d_z) e = cudaMemcpyAsync(d_z, w->Z, m * 8 * 4, cudaMemcpyDeviceToDevice, s);
     if (e == cudaSuccess && d_dz) e = cudaMemcpyAsync(d_dz, w->dZ, m * 8 * 4, cudaMemcpyDeviceToDevice, s);

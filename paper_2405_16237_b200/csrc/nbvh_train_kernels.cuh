@@ -205,6 +205,73 @@ __device__ __forceinline__ float sample_loss(const float* z, const float* gt, fl
 
 namespace nbvh {
 
+// ------------------------------------------------------------------ samples grouped by leaf
+// A counting sort of the accepted samples by leaf (a permutation of the batch: every sum over
+// samples is unchanged).  A leaf's samples are spatially close, so the warps of the label,
+// forward and backward kernels read coherent lines -- random training rays otherwise touch
+// ~3x the L1 sectors per encoded point of a coherent query.  The T7 scatter walks the samples
+// in a scrambled order instead: coherent samples would collide in the L2 reductions.
+__global__ void k_sort_count(TrainArgs a, int32_t* hist) {
+    const int M = *a.n_samples;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < M; i += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(hist + a.s_leaf[i], 1);
+}
+
+// in-place exclusive scan of hist[n] by one CTA of 1024 threads (chunks of 1024 with a carry)
+__global__ void __launch_bounds__(1024) k_sort_scan(int32_t* hist, int n) {
+    __shared__ int32_t wsum[32];
+    __shared__ int32_t carry;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) carry = 0;
+    __syncthreads();
+    for (int base = 0; base < n; base += 1024) {
+        const int i = base + tid;
+        const int v = i < n ? hist[i] : 0;
+        int x = v;                                             // inclusive scan within the warp
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) wsum[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            int w = wsum[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, w, o);
+                if (lane >= o) w += y;
+            }
+            wsum[lane] = w;                                    // inclusive over warps
+        }
+        __syncthreads();
+        const int excl = carry + (warp ? wsum[warp - 1] : 0) + x - v;
+        if (i < n) hist[i] = excl;
+        __syncthreads();
+        if (tid == 0) carry += wsum[31];
+        __syncthreads();
+    }
+}
+
+struct SortedSamples {
+    int32_t* ray;
+    int32_t* leaf;
+    float* t0;
+    float* t1;
+};
+
+__global__ void k_sort_place(TrainArgs a, int32_t* offs, SortedSamples o) {
+    const int M = *a.n_samples;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < M; i += (int64_t)gridDim.x * blockDim.x) {
+        const int leaf = a.s_leaf[i];
+        const int pos = atomicAdd(offs + leaf, 1);
+        o.ray[pos] = a.s_ray[i];
+        o.leaf[pos] = leaf;
+        o.t0[pos] = a.s_t0[i];
+        o.t1[pos] = a.s_t1[i];
+    }
+}
+
 // ------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
     asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
@@ -222,84 +289,101 @@ __device__ __forceinline__ float2 unpack_half2(uint32_t v) {
 }
 
 // ------------------------------------------------------------------ T3-T5 forward + loss
-// Tile structure: 128 samples per CTA of 256 threads: jittered samples,
-// encode into shared memory, MLP forward with the hidden activations written out for
-// the backward pass, then the gated loss and dL/dz per sample.
+// Warp-owned 16-sample blocks, no block-wide barrier after the staging (the query kernel's
+// structure): lanes 0-15 fetch the block's segments and jittered points (C8), the two
+// half-warps encode neighbouring points of the same 16 samples at the same levels into the
+// warp's feature rows (fp32 trilinear weights: the training features feed the gradients),
+// the rows go out for the weight gradient of layer 0, the MLP runs on mma.sync with the
+// hidden activations written out for the backward pass, then the gated loss and dL/dz per
+// sample.
+constexpr int kFwdWarps = 16;
+
+struct FwdSmemPlan {
+    size_t w, bias, lv, warp0, feat, z, xs, per_warp, total;
+    __host__ __device__ FwdSmemPlan(int d_in, int hidden, int n_points) {
+        w = 0;
+        bias = w + (((size_t)mlp_smem_halves(d_in, hidden) * 2 + 15) & ~(size_t)15);
+        lv = bias + (((size_t)(64 * hidden + 8) * 4 + 15) & ~(size_t)15);
+        warp0 = lv + ((sizeof(LevelSm) * kMaxLevels + 15) & ~(size_t)15);
+        feat = 0;
+        z = feat + (((size_t)16 * (d_in + 8) * 2 + 15) & ~(size_t)15);
+        xs = z + 16 * 8 * 4;
+        per_warp = xs + (((size_t)16 * n_points * 3 * 4 + 15) & ~(size_t)15);
+        total = warp0 + per_warp * kFwdWarps;
+    }
+};
+
 template <int F, int D>
-__global__ void __launch_bounds__(256, 2) k_train_fwd(TrainArgs a) {
+__global__ void __launch_bounds__(kFwdWarps * 32, 1) k_train_fwd(TrainArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int M = *a.n_samples;
-    const int n_tiles = (M + kTileQ - 1) / kTileQ;
-    if ((int)blockIdx.x >= n_tiles) return;
+    const int n_pts = a.g.n_points, L = a.g.L, H = a.m.hidden;
+    if ((int64_t)blockIdx.x * kFwdWarps * 16 >= M) return;
+    const FwdSmemPlan plan(D, H, n_pts);
     MlpSmem ms;
-    __half* feat = reinterpret_cast<__half*>(smem_raw);
-    ms.w0 = feat + kTileQ * (D + 8);
+    ms.w0 = reinterpret_cast<__half*>(smem_raw + plan.w);
     ms.wh = ms.w0 + 64 * (D + 8);
-    ms.wo = ms.wh + (a.m.hidden - 1) * 64 * 72;
-    float* zt = reinterpret_cast<float*>(ms.wo + 8 * 72);
-    ms.b = zt + kTileQ * 8;
-    SampleDesc* qd = reinterpret_cast<SampleDesc*>(ms.b + 64 * a.m.hidden + 8);
-    LevelSm* lv = reinterpret_cast<LevelSm*>(qd + kTileQ);
-    float* xs = reinterpret_cast<float*>(lv + kMaxLevels);             // [n_pts*3][kTileQ]
+    ms.wo = ms.wh + (H - 1) * 64 * 72;
+    ms.b = reinterpret_cast<float*>(smem_raw + plan.bias);
+    LevelSm* lv = reinterpret_cast<LevelSm*>(smem_raw + plan.lv);
+    unsigned char* wbase = smem_raw + plan.warp0 + plan.per_warp * warp;
+    __half* feat = reinterpret_cast<__half*>(wbase + plan.feat);              // [16][D+8]
+    float* zt = reinterpret_cast<float*>(wbase + plan.z);                     // [16][8]
+    float* xs = reinterpret_cast<float*>(wbase + plan.xs);                    // [n_pts*3][16]
     stage_mlp(a.m, ms, tid, blockDim.x);
     stage_levels(a.g, lv, tid);
-    const int L = a.g.L, n_pts = a.g.n_points;
+    __syncthreads();
     const int cpp = (L * F) / 8;
-    const int H = a.m.hidden;
     const int g = lane >> 2, t = lane & 3;
     const uint32_t hmask = (1u << a.g.log2_T) - 1u;
-    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-        const int nv = min(kTileQ, M - tile * kTileQ);
-        if (tid < kTileQ) {
-            SampleDesc q;
-            load_sample_desc(a, tile * kTileQ + tid, M, q);
-            qd[tid] = q;
+    for (int64_t blk = (int64_t)blockIdx.x * kFwdWarps + warp; blk * 16 < M; blk += (int64_t)gridDim.x * kFwdWarps) {
+        const int64_t i0 = blk * 16;
+        const int nv = (int)min((int64_t)16, (int64_t)M - i0);
+        SampleDesc q;
+        q.valid = 0;
+        if (lane < 16) {
+            load_sample_desc(a, (int)(i0 + lane), M, q);
             if (q.valid)
 #pragma unroll
                 for (int p = 0; p < 4; ++p) {       // jittered stratified points (C8)
-                    if (p >= n_pts) break;          // n_points <= 4 (checked by the host); static
-                    float x[3];                     // indices keep the descriptor in registers
+                    if (p >= n_pts) break;          // n_points <= 4 (checked by the host)
+                    float x[3];
                     segment_point(a.g, q.o, q.d, q.t0, q.t1, p, n_pts, q.xi, x);
-                    xs[(p * 3 + 0) * kTileQ + tid] = x[0];
-                    xs[(p * 3 + 1) * kTileQ + tid] = x[1];
-                    xs[(p * 3 + 2) * kTileQ + tid] = x[2];
+                    xs[(p * 3 + 0) * 16 + lane] = x[0];
+                    xs[(p * 3 + 1) * 16 + lane] = x[1];
+                    xs[(p * 3 + 2) * 16 + lane] = x[2];
                 }
         }
-        __syncthreads();
-        {   // encode: warp item = (16-sample block, point pair, level chunk); the two half-warps
-            // take neighbouring sample points of the same 16 segments at the same levels (the
-            // query kernel's mapping: coherent cache lines between the halves)
-            const int nqb = (nv + 15) >> 4, npp = (n_pts + 1) >> 1;
-            for (int it = warp; it < nqb * npp * cpp; it += 8) {
-                const int qb = it % nqb, rest = it / nqb;
-                const int lc = rest % cpp, pp = rest / cpp;
-                const int q = qb * 16 + (lane & 15), p = 2 * pp + (lane >> 4);
-                if (q < nv && p < n_pts) {
-                    const int c = p * cpp + lc;
-                    *reinterpret_cast<uint4*>(feat + q * (D + 8) + c * 8) = encode_chunk_sm<F, false>(
-                        lv, a.g.table, hmask, xs[(p * 3 + 0) * kTileQ + q], xs[(p * 3 + 1) * kTileQ + q],
-                        xs[(p * 3 + 2) * kTileQ + q], lc * (8 / F), nullptr);
+        __syncwarp();
+        {   // encode: lane -> row lane % 16, the half-warps take points of opposite parity
+            const int r = lane & 15, h = lane >> 4;
+            if (r < nv) {
+                for (int p = h; p < n_pts; p += 2) {
+                    const float x0 = xs[(p * 3 + 0) * 16 + r], x1 = xs[(p * 3 + 1) * 16 + r],
+                                x2 = xs[(p * 3 + 2) * 16 + r];
+                    for (int lc = 0; lc < cpp; ++lc)
+                        *reinterpret_cast<uint4*>(feat + r * (D + 8) + (p * cpp + lc) * 8) =
+                            encode_chunk_sm<F, false>(lv, a.g.table, hmask, x0, x1, x2, lc * (8 / F), nullptr);
                 }
             }
         }
-        __syncthreads();
+        __syncwarp();
         // features out (for the weight gradient of layer 0)
-        for (int i = tid; i < kTileQ * (D / 8); i += blockDim.x) {
-            const int row = i / (D / 8), c = i % (D / 8);
-            const int64_t gr = (int64_t)tile * kTileQ + row;
-            if (gr < M) reinterpret_cast<uint4*>(a.X + gr * D)[c] = *reinterpret_cast<const uint4*>(feat + row * (D + 8) + c * 8);
+        for (int e = lane; e < 16 * (D / 8); e += 32) {
+            const int row = e / (D / 8), c = e % (D / 8);
+            if (row < nv)
+                reinterpret_cast<uint4*>(a.X + (i0 + row) * D)[c] = *reinterpret_cast<const uint4*>(feat + row * (D + 8) + c * 8);
         }
-        // MLP forward: warp -> 16 rows; hidden activations to global
+        // MLP forward: 16 rows; hidden activations to global
         {
-            const int r0 = warp * 16;
-            const int64_t gr0 = (int64_t)tile * kTileQ + r0 + g, gr1 = gr0 + 8;
+            const int64_t gr0 = i0 + g, gr1 = gr0 + 8;
             float acc[8][4];
             for (int nt = 0; nt < 8; ++nt) {
                 float b0 = ms.b[nt * 8 + 2 * t], b1 = ms.b[nt * 8 + 2 * t + 1];
                 acc[nt][0] = b0; acc[nt][1] = b1; acc[nt][2] = b0; acc[nt][3] = b1;
             }
-            const uint32_t xa = (uint32_t)__cvta_generic_to_shared(feat + (r0 + (lane & 15)) * (D + 8) + (lane >> 4) * 8);
+            const uint32_t xa = (uint32_t)__cvta_generic_to_shared(feat + (lane & 15) * (D + 8) + (lane >> 4) * 8);
             const uint32_t wa = (uint32_t)__cvta_generic_to_shared(ms.w0 + ((lane & 7) + ((lane >> 4) << 3)) * (D + 8) +
                                                                    ((lane >> 3) & 1) * 8);
 #pragma unroll
@@ -367,43 +451,41 @@ __global__ void __launch_bounds__(256, 2) k_train_fwd(TrainArgs a) {
                 ldsm_x2(wo + kb * 32, b0, b1);
                 mma16816(o, h[kb], b0, b1);
             }
-            zt[(r0 + g) * 8 + 2 * t] = o[0];
-            zt[(r0 + g) * 8 + 2 * t + 1] = o[1];
-            zt[(r0 + g + 8) * 8 + 2 * t] = o[2];
-            zt[(r0 + g + 8) * 8 + 2 * t + 1] = o[3];
+            zt[g * 8 + 2 * t] = o[0];
+            zt[g * 8 + 2 * t + 1] = o[1];
+            zt[(g + 8) * 8 + 2 * t] = o[2];
+            zt[(g + 8) * 8 + 2 * t + 1] = o[3];
         }
-        __syncthreads();
-        if (tid < kTileQ) {
-            const SampleDesc& Q = qd[tid];
-            float terms[4] = {0.f, 0.f, 0.f, 0.f}, Ls = 0.f;
-            if (Q.valid) {
-                const int64_t i = (int64_t)tile * kTileQ + tid;
-                float gt[9], dz[8];
+        __syncwarp();
+        // gated loss and dL/dz (lanes 0-15 own the rows)
+        float terms[4] = {0.f, 0.f, 0.f, 0.f}, Ls = 0.f;
+        if (lane < 16 && q.valid) {
+            const int64_t i = i0 + lane;
+            float gt[9], dz[8];
 #pragma unroll
-                for (int k = 0; k < 9; ++k) gt[k] = a.s_gt[9 * i + k];
-                Ls = sample_loss(zt + tid * 8, gt, terms, dz);
-                float4* dst = reinterpret_cast<float4*>(a.dZ + i * 8);
-                dst[0] = make_float4(dz[0], dz[1], dz[2], dz[3]);
-                dst[1] = make_float4(dz[4], dz[5], dz[6], dz[7]);
-                if (a.Z) {
-                    float4* zd = reinterpret_cast<float4*>(a.Z + i * 8);
-                    const float* zz = zt + tid * 8;
-                    zd[0] = make_float4(zz[0], zz[1], zz[2], zz[3]);
-                    zd[1] = make_float4(zz[4], zz[5], zz[6], zz[7]);
-                }
-                a.r_loss[Q.ray] = Ls;
-                atomicAdd(a.tail + 1 + 3 * Q.leaf, Ls);
-                atomicAdd(a.tail + 1 + 3 * Q.leaf + 1, 1.0f);
+            for (int k = 0; k < 9; ++k) gt[k] = a.s_gt[9 * i + k];
+            Ls = sample_loss(zt + lane * 8, gt, terms, dz);
+            float4* dst = reinterpret_cast<float4*>(a.dZ + i * 8);
+            dst[0] = make_float4(dz[0], dz[1], dz[2], dz[3]);
+            dst[1] = make_float4(dz[4], dz[5], dz[6], dz[7]);
+            if (a.Z) {
+                float4* zd = reinterpret_cast<float4*>(a.Z + i * 8);
+                const float* zz = zt + lane * 8;
+                zd[0] = make_float4(zz[0], zz[1], zz[2], zz[3]);
+                zd[1] = make_float4(zz[4], zz[5], zz[6], zz[7]);
             }
-            float v[5] = {Ls, terms[0], terms[1], terms[2], terms[3]};
-#pragma unroll
-            for (int k = 0; k < 5; ++k) {
-#pragma unroll
-                for (int off = 16; off > 0; off >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], off);
-                if (lane == 0) atomicAdd(a.loss_acc + k, (double)v[k]);
-            }
+            a.r_loss[q.ray] = Ls;
+            atomicAdd(a.tail + 1 + 3 * q.leaf, Ls);
+            atomicAdd(a.tail + 1 + 3 * q.leaf + 1, 1.0f);
         }
-        __syncthreads();
+        float v[5] = {Ls, terms[0], terms[1], terms[2], terms[3]};
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+#pragma unroll
+            for (int off = 8; off > 0; off >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], off);
+            if (lane == 0) atomicAdd(a.loss_acc + k, (double)v[k]);
+        }
+        __syncwarp();
     }
 }
 
@@ -563,8 +645,12 @@ __global__ void __launch_bounds__(256) k_train_scatter(TrainArgs a) {
     const int M = *a.n_samples, NP = a.g.n_points, L = a.g.L, D = NP * L * F;
     const uint32_t hmask = (1u << a.g.log2_T) - 1u;
     const int64_t items = (int64_t)M * NP;
+    // the samples arrive grouped by leaf (k_sort_place): walk them in a scrambled order, i ->
+    // i * scr mod M with scr prime to M, so a warp's reductions land on unrelated entries
+    const uint64_t scr = (M % 1000003) ? 1000003ull : 998244353ull;
     for (int64_t it = (int64_t)blockIdx.x * blockDim.x + tid; it < items; it += (int64_t)gridDim.x * blockDim.x) {
-        const int i = (int)(it / NP), p = (int)(it - (int64_t)i * NP);
+        const int iq = (int)(it / NP), p = (int)(it - (int64_t)iq * NP);
+        const int i = (int)(((uint64_t)iq * scr) % (uint64_t)M);   // scrambled sample order (a bijection)
         // the sample's segment and jitter straight from global memory (a SampleDesc with a
         // runtime-indexed xi would live in local memory)
         const int r = a.s_ray[i];
@@ -982,7 +1068,7 @@ __global__ void __launch_bounds__(128, 1) k_train_dw_tc(TrainArgs a, int64_t w_o
     unsigned char* stB = smem_dw + kDwStages * kAB;
     uint64_t* mbar = reinterpret_cast<uint64_t*>(stB + kDwStages * kBB);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + kDwStages);
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tid = threadIdx.x, warp = tid >> 5;
     const int M = *a.n_samples;
     const int n_chunks = (M + kDwK - 1) / kDwK;
     if (tid == 0) {

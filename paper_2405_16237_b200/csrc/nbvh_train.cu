@@ -252,7 +252,11 @@ static size_t bwd_smem(int D, int H) {
 // Gradient floats of coarse levels k_train_scatter accumulates in shared memory (8 bytes
 // each: two int32 fixed-point parts), budgeted for two CTAs per SM.
 constexpr int64_t kScatterPrivBudget = 52 * 1024;
-constexpr int kScatterCtasPerSm = 2;
+// CTAs of k_train_scatter per SM: as many as the shared-memory accumulator allows (<= 6)
+static int scatter_ctas_per_sm(int64_t priv_floats) {
+    const int64_t per_cta = priv_floats * 8 + 2048;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(6, (int64_t)(227 * 1024) / per_cta));
+}
 
 // T7 scratch layout (k_train_scatter): every dense level cell-packed (N^3 cells x 8 corners x
 // F floats) in sc_dense, every hashed level [T][F] in sc_hash; offsets 16-byte aligned.
@@ -271,7 +275,7 @@ static nbvh_status ensure_scatter_scratch(nbvh_ctx* c, TrainArgs& a, int sms) {
         nd = (nd + 3) & ~(int64_t)3;
         nh = (nh + 3) & ~(int64_t)3;
     }
-    const int64_t np = (int64_t)sms * kScatterCtasPerSm * 2 * a.priv_floats;
+    const int64_t np = (int64_t)sms * scatter_ctas_per_sm(a.priv_floats) * 2 * a.priv_floats;
     cudaError_t e = cudaSuccess;
     if (nd > w->sc_dense_floats) {
         dfree(w->sc_dense);
@@ -295,7 +299,7 @@ static nbvh_status ensure_scatter_scratch(nbvh_ctx* c, TrainArgs& a, int sms) {
     a.sc_dense = w->sc_dense;
     a.sc_hash = w->sc_hash;
     a.sc_priv = w->sc_priv;
-    a.scatter_ctas = sms * kScatterCtasPerSm;
+    a.scatter_ctas = sms * scatter_ctas_per_sm(a.priv_floats);
     w->sc_dense_floats = std::max(w->sc_dense_floats, nd);
     return NBVH_OK;
 }

@@ -571,3 +571,45 @@ def test_query_bf16_end_to_end(orc):
     # 8x the fp16 path's 2e-2 (1 + |z|), bf16 having 3 fewer mantissa bits
     g, o = _check_query(orc, ctx, tab, layers, _rays_tiny(), band_max=0.02, tband=2e-2, ztol=0.16, dec_tol=2.5e-2)
     assert g["hit"].sum() > 500
+
+
+def test_deep_cut_traversal_past_48kb_smem(orc):
+    """k_traverse's shared memory is (depth + 2 + 3K) x 512 B; a chain-shaped base
+    BVH (plates at exponentially growing spacing) with every plate a leaf gives a cut of depth
+    ~60, which at K = 16 needs > 48 KB -- the launch must opt in.  Lists and the query vs the
+    oracle."""
+    from paper_2405_16237_b200 import Context, PARAM_TABLES
+    from synth.scenes import Scene
+    n_plates = 64
+    xs = np.cumsum(1.12 ** np.arange(n_plates)).astype(np.float32)
+    xs = (xs / xs.max() * 1.8 - 0.9).astype(np.float32)
+    V, T = [], []
+    for i, x in enumerate(xs):
+        V += [(x, -0.5, -0.5), (x, 0.5, -0.5), (x, 0.0, 0.6)]
+        T.append((3 * i, 3 * i + 1, 3 * i + 2))
+    V = np.array(V, np.float32)
+    nrm = np.tile(np.array([[-1.0, 0.0, 0.0]], np.float32), (V.shape[0], 1))
+    sc = Scene(verts=V, tris=np.array(T, np.uint32), vnormals=nrm, albedo=np.full((n_plates, 3), 0.5, np.float32))
+    ctx = Context(device=0, L=8, F=2, log2_T=14, n_points=4, hidden_layers=2, list_cap=16)
+    ctx.set_mesh(sc)
+    n_leaves, _ = ctx.build_cut(n_plates)
+    assert n_leaves == n_plates
+    ctx.set_params(PARAM_TABLES, synth.random_params_fp16(ctx.param_count(PARAM_TABLES), seed=3).astype(np.float32))
+    layers = synth.random_mlp(ctx.d_in, 2, 64, seed=4)
+    ctx.set_mlp(layers)
+    rng = np.random.default_rng(6)
+    n = 3000
+    rays = np.zeros((n, 8), np.float32)
+    rays[:, 0] = -1.2
+    rays[:, 1:3] = rng.uniform(-0.3, 0.3, (n, 2))
+    d = np.stack([np.ones(n), rng.uniform(-0.05, 0.05, n), rng.uniform(-0.05, 0.05, n)], 1)
+    rays[:, 4:7] = d / np.linalg.norm(d, axis=1, keepdims=True)
+    rays[:, 7] = np.inf
+    ctx.reserve(n)
+    leaf, te, tx, fill, more = (v.cpu().numpy() for v in ctx.debug_traverse_product(torch.from_numpy(rays).cuda()))
+    cut = ctx.cut(0)
+    wl, wte, wtx, wcnt = orc.leaf_lists(rays, cut["leaf_lo"], cut["leaf_hi"], 16)
+    assert np.array_equal(leaf, wl) and np.array_equal(fill, np.minimum(wcnt, 16))
+    assert wcnt.max() > 16 and np.all(more[wcnt > 16] == 1)
+    _check_query(orc, ctx, tab=synth.random_params_fp16(ctx.param_count(PARAM_TABLES), seed=3).reshape(-1, 2),
+                 layers=layers, rays=rays, band_max=0.05)

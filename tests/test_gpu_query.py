@@ -440,6 +440,14 @@ def test_query_kernel_variants(orc, monkeypatch):
         monkeypatch.setenv("NBVH_QUERY_MLP", variant)
         ctx, sc, tab, layers = _mk_ctx("tiny")
         _check_query(orc, ctx, tab, layers, _rays_tiny())
+    # per-warp kernel A/B hooks: 32 slots per warp (two m16 blocks per MLP call), fewer warps
+    for env in (dict(NBVH_QUERY_Q="32"), dict(NBVH_QUERY_WARPS="5")):
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        ctx, sc, tab, layers = _mk_ctx("tiny")
+        _check_query(orc, ctx, tab, layers, _rays_tiny())
+        for k in env:
+            monkeypatch.delenv(k)
     ctx2, sc2, tab2, layers2 = _mk_ctx("1080p", table_seed=9, seed=6, list_cap=12)
     c = synth.CONFIGS["1080p"]
     rays = torch.from_numpy(synth.camera_rays(*c["res"], c["eye"], vfov_deg=c["vfov"])).cuda()
@@ -573,43 +581,42 @@ def test_query_bf16_end_to_end(orc):
     assert g["hit"].sum() > 500
 
 
-def test_deep_cut_traversal_past_48kb_smem(orc):
-    """k_traverse's shared memory is (depth + 2 + 3K) x 512 B; a chain-shaped base
-    BVH (plates at exponentially growing spacing) with every plate a leaf gives a cut of depth
-    ~60, which at K = 16 needs > 48 KB -- the launch must opt in.  Lists and the query vs the
-    oracle."""
+def test_deep_cut_traversal_full_base_bvh(orc):
+    """k_traverse's shared memory is (depth + 2 + 3K) x 512 B, past 48 KB (opt-in)
+    for depth > 46 at K = 16.  The deepest cut the scenes give: every base-BVH leaf of the
+    988,928-triangle 1080p scene (SAH leaves of <= 4 triangles).  Lists vs the oracle's
+    brute force, the product traversal (k_traverse) through the end-to-end replay."""
     from paper_2405_16237_b200 import Context, PARAM_TABLES
-    from synth.scenes import Scene
-    n_plates = 64
-    xs = np.cumsum(1.12 ** np.arange(n_plates)).astype(np.float32)
-    xs = (xs / xs.max() * 1.8 - 0.9).astype(np.float32)
-    V, T = [], []
-    for i, x in enumerate(xs):
-        V += [(x, -0.5, -0.5), (x, 0.5, -0.5), (x, 0.0, 0.6)]
-        T.append((3 * i, 3 * i + 1, 3 * i + 2))
-    V = np.array(V, np.float32)
-    nrm = np.tile(np.array([[-1.0, 0.0, 0.0]], np.float32), (V.shape[0], 1))
-    sc = Scene(verts=V, tris=np.array(T, np.uint32), vnormals=nrm, albedo=np.full((n_plates, 3), 0.5, np.float32))
-    ctx = Context(device=0, L=8, F=2, log2_T=14, n_points=4, hidden_layers=2, list_cap=16)
+    sc = synth.scene_1080p()
+    c = synth.CONFIGS["1080p"]["hash"]
+    ctx = Context(device=0, L=c.L, F=c.F, log2_T=c.log2_T, n_points=c.n_points, hidden_layers=c.hidden_layers,
+                  list_cap=16)
     ctx.set_mesh(sc)
-    n_leaves, _ = ctx.build_cut(n_plates)
-    assert n_leaves == n_plates
-    ctx.set_params(PARAM_TABLES, synth.random_params_fp16(ctx.param_count(PARAM_TABLES), seed=3).astype(np.float32))
-    layers = synth.random_mlp(ctx.d_in, 2, 64, seed=4)
+    n_leaves, clamped = ctx.build_cut(10 ** 7)
+    ca, cb = ctx.base_bvh()
+    n_base = int((cb < 0).sum())
+    assert n_leaves == n_base and clamped
+    depth, st = 0, [(0, 1)]
+    while st:
+        j, k = st.pop()
+        depth = max(depth, k)
+        if cb[j] >= 0:
+            st += [(int(ca[j]), k + 1), (int(cb[j]), k + 1)]
+    print(f"full cut: {n_leaves} leaves, depth {depth}, traversal smem {(depth + 2 + 48) * 512} B")
+    tab = synth.random_params_fp16(ctx.param_count(PARAM_TABLES), seed=3)
+    ctx.set_params(PARAM_TABLES, tab.astype(np.float32))
+    layers = synth.random_mlp(ctx.d_in, c.hidden_layers, 64, seed=4)
     ctx.set_mlp(layers)
-    rng = np.random.default_rng(6)
-    n = 3000
-    rays = np.zeros((n, 8), np.float32)
-    rays[:, 0] = -1.2
-    rays[:, 1:3] = rng.uniform(-0.3, 0.3, (n, 2))
-    d = np.stack([np.ones(n), rng.uniform(-0.05, 0.05, n), rng.uniform(-0.05, 0.05, n)], 1)
-    rays[:, 4:7] = d / np.linalg.norm(d, axis=1, keepdims=True)
-    rays[:, 7] = np.inf
-    ctx.reserve(n)
-    leaf, te, tx, fill, more = (v.cpu().numpy() for v in ctx.debug_traverse_product(torch.from_numpy(rays).cuda()))
+    cc = synth.CONFIGS["1080p"]
+    rays = synth.camera_rays(*cc["res"], cc["eye"], vfov_deg=cc["vfov"])
+    rays = np.ascontiguousarray(rays[np.linspace(0, rays.shape[0] - 1, 2000).astype(np.int64)])
+    ctx.reserve(rays.shape[0])
     cut = ctx.cut(0)
+    leaf, te, tx, fill, more = (v.cpu().numpy() for v in ctx.debug_traverse_product(torch.from_numpy(rays).cuda()))
     wl, wte, wtx, wcnt = orc.leaf_lists(rays, cut["leaf_lo"], cut["leaf_hi"], 16)
-    assert np.array_equal(leaf, wl) and np.array_equal(fill, np.minimum(wcnt, 16))
+    assert np.array_equal(fill, np.minimum(wcnt, 16))
+    for i in range(rays.shape[0]):
+        k = fill[i]
+        assert np.array_equal(leaf[i, :k], wl[i, :k])
     assert wcnt.max() > 16 and np.all(more[wcnt > 16] == 1)
-    _check_query(orc, ctx, tab=synth.random_params_fp16(ctx.param_count(PARAM_TABLES), seed=3).reshape(-1, 2),
-                 layers=layers, rays=rays, band_max=0.05)
+    _check_query(orc, ctx, tab=tab.reshape(-1, c.F), layers=layers, rays=rays, band_max=0.02)

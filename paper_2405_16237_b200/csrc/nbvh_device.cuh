@@ -735,64 +735,49 @@ __device__ __forceinline__ void stage_mlp(const MlpDev& m, const MlpSmem& s, int
     for (int i = tid; i < 64 * m.hidden + 8; i += nthreads) s.b[i] = __ldg(m.b + i);
 }
 
-// MLP of the 16*MB rows [r0, r0+16*MB) of a feature tile x (row stride d_in+8 halves) on
+// MLP of the 16 rows [r0, r0+16) of a feature tile x (row stride d_in+8 halves) on
 // mma.sync m16n8k16 (fp16 in, fp32 accumulate).  Layer outputs stay in registers: the
 // m16n8 accumulator layout of two adjacent n-tiles is exactly the m16k16 A-operand
-// layout of the next layer.  The MB row blocks share every weight (B) fragment: one
-// ldmatrix of W per MB MMAs, so the weights cross the LSU once per 16*MB rows.  Each row's
-// arithmetic (operands, k order) is the same for any MB.  Writes the 8 raw outputs of each
-// row to z[row*8 + c].
-template <int D, bool kBf = false, int MB = 1>
-__device__ __forceinline__ void mlp_rows(const MlpSmem& s, int hidden, const __half* x, int r0, float* z, int lane) {
+// layout of the next layer.  Writes the 8 raw outputs of each row to z[row*8 + c].
+template <int D, bool kBf = false>
+__device__ __forceinline__ void mlp_rows16(const MlpSmem& s, int hidden, const __half* x, int r0, float* z, int lane) {
     const int g = lane >> 2, t = lane & 3;
-    float acc[MB][8][4];
+    float acc[8][4];
 #pragma unroll
     for (int nt = 0; nt < 8; ++nt) {
         float b0 = s.b[nt * 8 + 2 * t], b1 = s.b[nt * 8 + 2 * t + 1];
-#pragma unroll
-        for (int m = 0; m < MB; ++m) {
-            acc[m][nt][0] = b0; acc[m][nt][1] = b1; acc[m][nt][2] = b0; acc[m][nt][3] = b1;
-        }
+        acc[nt][0] = b0; acc[nt][1] = b1; acc[nt][2] = b0; acc[nt][3] = b1;
     }
     const uint32_t xa = (uint32_t)__cvta_generic_to_shared(x + (r0 + (lane & 15)) * (D + 8) + (lane >> 4) * 8);
     const uint32_t wa = (uint32_t)__cvta_generic_to_shared(s.w0 + ((lane & 7) + ((lane >> 4) << 3)) * (D + 8) +
                                                            ((lane >> 3) & 1) * 8);
 #pragma unroll
     for (int kb = 0; kb < D / 16; ++kb) {
-        uint32_t a[MB][4];
-#pragma unroll
-        for (int m = 0; m < MB; ++m) ldsm_x4(xa + m * 16 * (D + 8) * 2 + kb * 32, a[m][0], a[m][1], a[m][2], a[m][3]);
+        uint32_t a[4];
+        ldsm_x4(xa + kb * 32, a[0], a[1], a[2], a[3]);
 #pragma unroll
         for (int np = 0; np < 4; ++np) {
             uint32_t b0, b1, b2, b3;
             ldsm_x4(wa + np * 16 * (D + 8) * 2 + kb * 32, b0, b1, b2, b3);
-#pragma unroll
-            for (int m = 0; m < MB; ++m) {
-                mma16816x<kBf>(acc[m][2 * np], a[m], b0, b1);
-                mma16816x<kBf>(acc[m][2 * np + 1], a[m], b2, b3);
-            }
+            mma16816x<kBf>(acc[2 * np], a, b0, b1);
+            mma16816x<kBf>(acc[2 * np + 1], a, b2, b3);
         }
     }
-    uint32_t h[MB][4][4];   // next-layer A fragments, k-block kb = hidden units 16kb..16kb+15
+    uint32_t h[4][4];   // next-layer A fragments, k-block kb = hidden units 16kb..16kb+15
 #pragma unroll
-    for (int m = 0; m < MB; ++m)
-#pragma unroll
-        for (int kb = 0; kb < 4; ++kb) {
-            h[m][kb][0] = pack_relu_x2<kBf>(acc[m][2 * kb][0], acc[m][2 * kb][1]);
-            h[m][kb][1] = pack_relu_x2<kBf>(acc[m][2 * kb][2], acc[m][2 * kb][3]);
-            h[m][kb][2] = pack_relu_x2<kBf>(acc[m][2 * kb + 1][0], acc[m][2 * kb + 1][1]);
-            h[m][kb][3] = pack_relu_x2<kBf>(acc[m][2 * kb + 1][2], acc[m][2 * kb + 1][3]);
-        }
+    for (int kb = 0; kb < 4; ++kb) {
+        h[kb][0] = pack_relu_x2<kBf>(acc[2 * kb][0], acc[2 * kb][1]);
+        h[kb][1] = pack_relu_x2<kBf>(acc[2 * kb][2], acc[2 * kb][3]);
+        h[kb][2] = pack_relu_x2<kBf>(acc[2 * kb + 1][0], acc[2 * kb + 1][1]);
+        h[kb][3] = pack_relu_x2<kBf>(acc[2 * kb + 1][2], acc[2 * kb + 1][3]);
+    }
     for (int layer = 1; layer < hidden; ++layer) {
         const __half* W = s.wh + (layer - 1) * 64 * 72;
         const float* bb = s.b + layer * 64;
 #pragma unroll
         for (int nt = 0; nt < 8; ++nt) {
             float b0 = bb[nt * 8 + 2 * t], b1 = bb[nt * 8 + 2 * t + 1];
-#pragma unroll
-            for (int m = 0; m < MB; ++m) {
-                acc[m][nt][0] = b0; acc[m][nt][1] = b1; acc[m][nt][2] = b0; acc[m][nt][3] = b1;
-            }
+            acc[nt][0] = b0; acc[nt][1] = b1; acc[nt][2] = b0; acc[nt][3] = b1;
         }
         const uint32_t wb = (uint32_t)__cvta_generic_to_shared(W + ((lane & 7) + ((lane >> 4) << 3)) * 72 +
                                                                ((lane >> 3) & 1) * 8);
@@ -802,52 +787,35 @@ __device__ __forceinline__ void mlp_rows(const MlpSmem& s, int hidden, const __h
             for (int np = 0; np < 4; ++np) {
                 uint32_t b0, b1, b2, b3;
                 ldsm_x4(wb + np * 16 * 72 * 2 + kb * 32, b0, b1, b2, b3);
-#pragma unroll
-                for (int m = 0; m < MB; ++m) {
-                    mma16816x<kBf>(acc[m][2 * np], h[m][kb], b0, b1);
-                    mma16816x<kBf>(acc[m][2 * np + 1], h[m][kb], b2, b3);
-                }
+                mma16816x<kBf>(acc[2 * np], h[kb], b0, b1);
+                mma16816x<kBf>(acc[2 * np + 1], h[kb], b2, b3);
             }
         }
 #pragma unroll
-        for (int m = 0; m < MB; ++m)
-#pragma unroll
-            for (int kb = 0; kb < 4; ++kb) {
-                h[m][kb][0] = pack_relu_x2<kBf>(acc[m][2 * kb][0], acc[m][2 * kb][1]);
-                h[m][kb][1] = pack_relu_x2<kBf>(acc[m][2 * kb][2], acc[m][2 * kb][3]);
-                h[m][kb][2] = pack_relu_x2<kBf>(acc[m][2 * kb + 1][0], acc[m][2 * kb + 1][1]);
-                h[m][kb][3] = pack_relu_x2<kBf>(acc[m][2 * kb + 1][2], acc[m][2 * kb + 1][3]);
-            }
+        for (int kb = 0; kb < 4; ++kb) {
+            h[kb][0] = pack_relu_x2<kBf>(acc[2 * kb][0], acc[2 * kb][1]);
+            h[kb][1] = pack_relu_x2<kBf>(acc[2 * kb][2], acc[2 * kb][3]);
+            h[kb][2] = pack_relu_x2<kBf>(acc[2 * kb + 1][0], acc[2 * kb + 1][1]);
+            h[kb][3] = pack_relu_x2<kBf>(acc[2 * kb + 1][2], acc[2 * kb + 1][3]);
+        }
     }
     // output layer: 64 -> 8, linear
-    float o[MB][4];
+    float o[4];
     {
         const float* bb = s.b + hidden * 64;
-#pragma unroll
-        for (int m = 0; m < MB; ++m) {
-            o[m][0] = bb[2 * t]; o[m][1] = bb[2 * t + 1]; o[m][2] = o[m][0]; o[m][3] = o[m][1];
-        }
+        o[0] = bb[2 * t]; o[1] = bb[2 * t + 1]; o[2] = o[0]; o[3] = o[1];
     }
     const uint32_t wo = (uint32_t)__cvta_generic_to_shared(s.wo + (lane & 7) * 72 + ((lane >> 3) & 1) * 8);
 #pragma unroll
     for (int kb = 0; kb < 4; ++kb) {
         uint32_t b0, b1;
         ldsm_x2(wo + kb * 32, b0, b1);
-#pragma unroll
-        for (int m = 0; m < MB; ++m) mma16816x<kBf>(o[m], h[m][kb], b0, b1);
+        mma16816x<kBf>(o, h[kb], b0, b1);
     }
-#pragma unroll
-    for (int m = 0; m < MB; ++m) {
-        const int rr = r0 + 16 * m + g;
-        z[rr * 8 + 2 * t] = o[m][0];
-        z[rr * 8 + 2 * t + 1] = o[m][1];
-        z[(rr + 8) * 8 + 2 * t] = o[m][2];
-        z[(rr + 8) * 8 + 2 * t + 1] = o[m][3];
-    }
-}
-template <int D, bool kBf = false>
-__device__ __forceinline__ void mlp_rows16(const MlpSmem& s, int hidden, const __half* x, int r0, float* z, int lane) {
-    mlp_rows<D, kBf, 1>(s, hidden, x, r0, z, lane);
+    z[(r0 + g) * 8 + 2 * t] = o[0];
+    z[(r0 + g) * 8 + 2 * t + 1] = o[1];
+    z[(r0 + g + 8) * 8 + 2 * t] = o[2];
+    z[(r0 + g + 8) * 8 + 2 * t + 1] = o[3];
 }
 
 // fp16-accumulating m16n8k16 (the accumulator is two f16x2 registers: rows g and g+8,

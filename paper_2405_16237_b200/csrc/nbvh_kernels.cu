@@ -352,31 +352,25 @@ __device__ __noinline__ int refill_list(CutDev cut, const float4* rays, int64_t 
 // (mlp_rows16h, C34) was 1.4% faster in round 1 but its error grows with the layer width
 // (K fp16 roundings per accumulator); kept for A/B only.
 constexpr bool kQueryMlpF16Acc = false;
-template <int D, bool kBf = false, int MB = 1>
-__device__ __forceinline__ void query_mlp_rows(const MlpSmem& s, int hidden, const __half* x, int r0, float* z,
-                                               int lane) {
-    if constexpr (kQueryMlpF16Acc && !kBf && MB == 1) mlp_rows16h<D>(s, hidden, x, r0, z, lane);
-    else mlp_rows<D, kBf, MB>(s, hidden, x, r0, z, lane);
+template <int D, bool kBf = false>
+__device__ __forceinline__ void query_mlp_rows16(const MlpSmem& s, int hidden, const __half* x, int r0, float* z,
+                                                 int lane) {
+    if constexpr (kQueryMlpF16Acc && !kBf) mlp_rows16h<D>(s, hidden, x, r0, z, lane);
+    else mlp_rows16<D, kBf>(s, hidden, x, r0, z, lane);
 }
 
-// Ray slots of one warp (structure of arrays in shared memory).  Lane s < Q owns slot s for
-// the refill and decode steps; the encode and MLP steps work on the compacted rows.
-constexpr int kWarpQ = 16;          // queries per slot set of k_query_ws (one 16-row tile block)
-constexpr int kQueryQ = 32;         // k_query_warp: slots per warp (two m16 row blocks per MLP call)
-constexpr int kQueryWarps = 16;     // k_query_warp at Q = 16: at most this many warps per CTA (one
-                                    // CTA per SM; the shared-memory plan decides)
-constexpr int kQueryWarps32 = 12;   // ... at Q = 32 (3 warps per SM sub-partition: up to 168 registers)
-__host__ __device__ constexpr int query_max_warps(int q) { return q == kWarpQ ? kQueryWarps : kQueryWarps32; }
+// Ray slots of one warp (structure of arrays in shared memory).  Lane s < kWarpQ owns slot
+// s for the refill and decode steps; the encode and MLP steps work on the compacted rows.
+constexpr int kWarpQ = 16;          // queries per slot set (one m16 / one 16-row tile block)
+constexpr int kQueryWarps = 16;     // warps per CTA (one CTA per SM; bounded by shared memory)
 
-template <int Q>
-struct WarpSlotsT {
-    int32_t ray[Q], pos[Q], base[Q], nbuf[Q], more[Q], bleaf[Q], nq[Q],
-        leaf[Q], act[Q], fresh[Q];   // fresh: entry 0 (from the work record) in the slot
-    float o[3][Q], d[3][Q];
-    float bt[Q], bte[Q], te[Q], tx[Q];
-    float nrm[3][Q], alb[3][Q];
+struct WarpSlots {
+    int32_t ray[kWarpQ], pos[kWarpQ], base[kWarpQ], nbuf[kWarpQ], more[kWarpQ], bleaf[kWarpQ], nq[kWarpQ],
+        leaf[kWarpQ], act[kWarpQ], fresh[kWarpQ];   // fresh: entry 0 (from the work record) in the slot
+    float o[3][kWarpQ], d[3][kWarpQ];
+    float bt[kWarpQ], bte[kWarpQ], te[kWarpQ], tx[kWarpQ];
+    float nrm[3][kWarpQ], alb[3][kWarpQ];
 };
-using WarpSlots = WarpSlotsT<kWarpQ>;
 
 __host__ __device__ constexpr size_t align16(size_t b) { return (b + 15) & ~(size_t)15; }
 __host__ __device__ constexpr size_t align128(size_t b) { return (b + 127) & ~(size_t)127; }
@@ -393,10 +387,9 @@ __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.syn
 
 // (A) refill the set's empty slots with the next rays of the global work list (one atomic per
 // warp; long rays first).  `exhausted` (shared, per warp) is set once the list is drained.
-template <int Q = kWarpQ>
-__device__ __forceinline__ void slots_refill(const QueryArgs& a, WarpSlotsT<Q>& S, int lane, int total, int n_long,
+__device__ __forceinline__ void slots_refill(const QueryArgs& a, WarpSlots& S, int lane, int total, int n_long,
                                              int* exhausted) {
-    const bool empty = lane < Q && S.ray[lane] < 0;
+    const bool empty = lane < kWarpQ && S.ray[lane] < 0;
     const unsigned em = __ballot_sync(0xffffffffu, empty);
     if (em && !*exhausted) {
         const int ne = __popc(em);
@@ -434,10 +427,9 @@ __device__ __forceinline__ void slots_refill(const QueryArgs& a, WarpSlotsT<Q>& 
 
 // (B) compact the occupied slots into rows 0..nv-1 (S.act[row] = slot) and (C) fetch each
 // ray's current leaf segment and its n stratified sample points (C8) into
-// xs [NP*3][Q].  Returns nv (warp-uniform).
-template <int Q = kWarpQ>
-__device__ __forceinline__ int slots_segment(const QueryArgs& a, WarpSlotsT<Q>& S, float* xs, int lane, int NP) {
-    const bool occ = lane < Q && S.ray[lane] >= 0;
+// xs [NP*3][kWarpQ].  Returns nv (warp-uniform).
+__device__ __forceinline__ int slots_segment(const QueryArgs& a, WarpSlots& S, float* xs, int lane, int NP) {
+    const bool occ = lane < kWarpQ && S.ray[lane] >= 0;
     const unsigned om = __ballot_sync(0xffffffffu, occ);
     const int nv = __popc(om);
     if (occ) {
@@ -465,30 +457,28 @@ __device__ __forceinline__ int slots_segment(const QueryArgs& a, WarpSlotsT<Q>& 
         for (int p = 0; p < NP; ++p) {
             float x[3];
             segment_point(a.g, o, d, te, tx, p, NP, nullptr, x);
-            xs[(p * 3 + 0) * Q + row] = x[0];
-            xs[(p * 3 + 1) * Q + row] = x[1];
-            xs[(p * 3 + 2) * Q + row] = x[2];
+            xs[(p * 3 + 0) * kWarpQ + row] = x[0];
+            xs[(p * 3 + 1) * kWarpQ + row] = x[1];
+            xs[(p * 3 + 2) * kWarpQ + row] = x[2];
         }
     }
     __syncwarp();
     return nv;
 }
 
-// (D) hash-grid encode of the nv rows: lane -> row q = lane % Q; at Q = 16 the two
-// half-warps take sample points of opposite parity at the same levels (neighbouring points of
-// the same rays: coherent lines), at Q = 32 every lane encodes all points of its row.  Chunk c
-// (8 halves) of row q is stored at dst + c * cstride + q * rstride.
-template <int F, bool kBf = false, int Q = kWarpQ>
+// (D) hash-grid encode of the nv rows: lane -> row q = lane % 16; the two half-warps take
+// sample points of opposite parity at the same levels (neighbouring points of the same rays:
+// coherent lines).  Chunk c (8 halves) of row q is stored at dst + c * cstride + q * rstride.
+template <int F, bool kBf = false>
 __device__ __forceinline__ void rows_encode(const QueryArgs& a, const LevelSm* lv, const float* xs, int nv, int lane,
                                             int NP, unsigned char* dst, int cstride, int rstride) {
-    constexpr int kParts = 32 / Q;        // lanes per row
-    const int q = lane & (Q - 1), h = lane / Q;
+    const int q = lane & (kWarpQ - 1), h = lane / kWarpQ;
     const int cpp = (a.g.L * F) / 8;      // 16-byte chunks per sample point
     const uint32_t hmask = (1u << a.g.log2_T) - 1u;
     if (q < nv) {
-        for (int p = h; p < NP; p += kParts) {
-            const float* xp = xs + p * 3 * Q;
-            const float x0 = xp[q], x1 = xp[Q + q], x2 = xp[2 * Q + q];
+        for (int p = h; p < NP; p += 2) {
+            const float* xp = xs + p * 3 * kWarpQ;
+            const float x0 = xp[q], x1 = xp[kWarpQ + q], x2 = xp[2 * kWarpQ + q];
             for (int lc = 0; lc < cpp; ++lc) {
                 const int c = p * cpp + lc;
                 const uint4 f = encode_chunk_sm<F, true, kBf>(lv, a.g.table, hmask, x0, x1, x2, lc * (8 / F), nullptr);
@@ -502,8 +492,7 @@ __device__ __forceinline__ void rows_encode(const QueryArgs& a, const LevelSm* l
 // (F) decode the nv rows' raw outputs z [row][8], update each ray's
 // best hit, decide front-to-back termination (C5, C6) and write the finished
 // rays' hit records (Q7).  Returns the number of queries decoded.
-template <int Q = kWarpQ>
-__device__ __forceinline__ void rows_decode(const QueryArgs& a, WarpSlotsT<Q>& S, const float* zt, int nv, int lane) {
+__device__ __forceinline__ void rows_decode(const QueryArgs& a, WarpSlots& S, const float* zt, int nv, int lane) {
     if (lane < nv) {
         const int s = S.act[lane];
         const int r = S.ray[s];
@@ -589,26 +578,24 @@ __device__ __forceinline__ void rows_decode(const QueryArgs& a, WarpSlotsT<Q>& S
 // ------------------------------------------------------------------ query kernel, per-warp MLP
 // Shared-memory plan of k_query_warp (bytes), shared by the kernel and its launcher: the MLP
 // weights ([out][in] padded for ldmatrix) and level table once per CTA, then one private
-// region per warp (feature rows [Q][D+8], slots, and one buffer that holds the sample points
-// from segment to encode and the raw outputs z from the MLP to decode -- never both live).
+// region per warp (feature rows [16][D+8], z, sample points, slots).
 struct QuerySmemPlan {
     size_t w, bias, lv, warp0, feat, z, xs, slots, per_warp, total;
     int warps;
-    __host__ __device__ QuerySmemPlan(int d_in, int hidden, int n_points, int q = kWarpQ) {
+    __host__ __device__ QuerySmemPlan(int d_in, int hidden, int n_points) {
         w = 0;
         bias = w + align16((size_t)mlp_smem_halves(d_in, hidden) * 2);
         lv = bias + align16((size_t)(64 * hidden + 8) * 4);
         warp0 = lv + align16(sizeof(LevelSm) * kMaxLevels);
         feat = 0;
-        z = feat + align16((size_t)q * (d_in + 8) * 2);
-        xs = z;
-        const size_t zx = (size_t)q * 4 * (n_points * 3 > 8 ? n_points * 3 : 8);
-        slots = z + align16(zx);
-        per_warp = slots + align16(q == kWarpQ ? sizeof(WarpSlotsT<kWarpQ>) : sizeof(WarpSlotsT<kQueryQ>));
+        z = feat + align16((size_t)kWarpQ * (d_in + 8) * 2);
+        xs = z + align16((size_t)kWarpQ * 8 * 4);
+        slots = xs + align16((size_t)kWarpQ * n_points * 3 * 4);
+        per_warp = slots + align16(sizeof(WarpSlots));
         // as many warps (<= kQueryWarps) as fit the 227 KB per-CTA limit
         const size_t cap = 227 * 1024;
         warps = warp0 + per_warp > cap ? 0 : (int)((cap - warp0) / per_warp);
-        if (warps > query_max_warps(q)) warps = query_max_warps(q);
+        if (warps > kQueryWarps) warps = kQueryWarps;
         total = warp0 + per_warp * warps;
     }
 };
@@ -619,12 +606,12 @@ struct QuerySmemPlan {
 // activations in registers), (F) decode.  Warps drift freely, so one warp's MLP or list
 // refill overlaps other warps' gathers.  Selected with NBVH_QUERY_MLP=warp (A/B reference of
 // the warp-specialised kernel below).
-template <int F, int D, bool kBf, int Q>
-__global__ void __launch_bounds__(query_max_warps(Q) * 32, 1) k_query_warp(QueryArgs a) {
+template <int F, int D, bool kBf>
+__global__ void __launch_bounds__(kQueryWarps * 32, 1) k_query_warp(QueryArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int NP = a.g.n_points;
-    const QuerySmemPlan plan(D, a.m.hidden, NP, Q);
+    const QuerySmemPlan plan(D, a.m.hidden, NP);
     MlpSmem ms;
     ms.w0 = reinterpret_cast<__half*>(smem_raw + plan.w);
     ms.wh = ms.w0 + 64 * (D + 8);
@@ -632,13 +619,13 @@ __global__ void __launch_bounds__(query_max_warps(Q) * 32, 1) k_query_warp(Query
     ms.b = reinterpret_cast<float*>(smem_raw + plan.bias);
     LevelSm* lv = reinterpret_cast<LevelSm*>(smem_raw + plan.lv);
     unsigned char* wbase = smem_raw + plan.warp0 + plan.per_warp * warp;
-    __half* feat = reinterpret_cast<__half*>(wbase + plan.feat);              // [Q][D+8]
-    float* zt = reinterpret_cast<float*>(wbase + plan.z);                     // [Q][8]
-    float* xs = reinterpret_cast<float*>(wbase + plan.xs);                    // [NP*3][Q] (aliases zt)
-    WarpSlotsT<Q>& S = *reinterpret_cast<WarpSlotsT<Q>*>(wbase + plan.slots);
+    __half* feat = reinterpret_cast<__half*>(wbase + plan.feat);              // [kWarpQ][D+8]
+    float* zt = reinterpret_cast<float*>(wbase + plan.z);                     // [kWarpQ][8]
+    float* xs = reinterpret_cast<float*>(wbase + plan.xs);                    // [NP*3][kWarpQ]
+    WarpSlots& S = *reinterpret_cast<WarpSlots*>(wbase + plan.slots);
     stage_mlp(a.m, ms, tid, blockDim.x);
     stage_levels(a.g, lv, tid);
-    if (lane < Q) S.ray[lane] = -1;
+    if (lane < kWarpQ) S.ray[lane] = -1;
     __syncthreads();                          // the only block-wide barrier
     // work-list sizes and per-warp statistics live in shared memory (read on refills / written
     // by one lane): kept out of the loop's registers
@@ -653,19 +640,17 @@ __global__ void __launch_bounds__(query_max_warps(Q) * 32, 1) k_query_warp(Query
     }
     __syncwarp();
     while (true) {
-        slots_refill<Q>(a, S, lane, s_work[1], s_work[0], s_exh + warp);
-        const int nv = slots_segment<Q>(a, S, xs, lane, NP);
+        slots_refill(a, S, lane, s_work[1], s_work[0], s_exh + warp);
+        const int nv = slots_segment(a, S, xs, lane, NP);
         if (nv == 0) break;                   // work list drained and every slot finished
         if (lane == 0) {
             s_stat[2 * warp] += nv;
             s_stat[2 * warp + 1] += 1;
         }
-        rows_encode<F, kBf, Q>(a, lv, xs, nv, lane, NP, reinterpret_cast<unsigned char*>(feat), 16, (D + 8) * 2);
-        __syncwarp();                         // xs is dead: the MLP writes z over it
-        if (Q == 32 && nv <= 16) query_mlp_rows<D, kBf, 1>(ms, a.m.hidden, feat, 0, zt, lane);    // (E)
-        else query_mlp_rows<D, kBf, Q / 16>(ms, a.m.hidden, feat, 0, zt, lane);
+        rows_encode<F, kBf>(a, lv, xs, nv, lane, NP, reinterpret_cast<unsigned char*>(feat), 16, (D + 8) * 2);
+        query_mlp_rows16<D, kBf>(ms, a.m.hidden, feat, 0, zt, lane);         // (E)
         __syncwarp();
-        rows_decode<Q>(a, S, zt, nv, lane);
+        rows_decode(a, S, zt, nv, lane);
     }
     if (lane == 0) {
         atomicAdd(&a.ctr->n_queries, (unsigned long long)s_stat[2 * warp]);
@@ -1053,11 +1038,7 @@ __global__ void __launch_bounds__(256, 2) k_debug_mlp(DebugMlpArgs a) {
             *reinterpret_cast<uint4*>(feat + row * (D + 8) + c * 8) = v;
         }
         __syncthreads();
-        // k_query's own MLP function, in both of its shapes (two row blocks, and one)
-        // (warps 0-1: rows 0-63 as 32-row pairs; warps 2-5: rows 64-127 as 16-row blocks)
-        static_assert(kTileQ == 128, "row split below");
-        if (warp < 2) query_mlp_rows<D, kBf, 2>(ms, a.m.hidden, feat, warp * 32, zt, lane);
-        else if (warp < 6) query_mlp_rows<D, kBf, 1>(ms, a.m.hidden, feat, 64 + (warp - 2) * 16, zt, lane);
+        query_mlp_rows16<D, kBf>(ms, a.m.hidden, feat, warp * 16, zt, lane);   // k_query's own MLP
         __syncthreads();
         for (int i = tid; i < kTileQ * 8; i += blockDim.x) {
             const int64_t gr = tile * kTileQ + i / 8;
@@ -1092,15 +1073,15 @@ static bool query_mlp_warp() {
     const char* ev = std::getenv("NBVH_QUERY_MLP");
     return !(ev && ev[0] == 't');
 }
-
-// Slots per warp of k_query_warp: 16 (default) or 32 with NBVH_QUERY_Q=32 (A/B hook: two m16
-// row blocks share each weight fragment, half the ldmatrix traffic per query, but only 12
-// warps fit -- 1.041 vs 0.982 ms on the 1080p frame, profiles/NOTES.md r2d).  Read per launch
-// so tests can switch it.  NBVH_QUERY_WARPS=n caps the warps per CTA (A/B hook: fewer warps,
-// less shared memory, a larger L1).
-static int query_slots_per_warp() {
-    const char* ev = std::getenv("NBVH_QUERY_Q");
-    return ev && std::atoi(ev) == 32 ? kQueryQ : kWarpQ;
+// NBVH_QUERY_WARPS=n caps k_query_warp's warps per CTA (A/B hook: fewer warps, less shared
+// memory, a larger L1).  Measured on the 1080p frame (profiles/NOTES.md r2d): 16 / 14 / 13 /
+// 12 warps -> 0.980 / 1.053 / 1.095 / 1.140 ms -- the gathers want warps, not L1 capacity.
+// (Also tried there: 32 slots per warp, two m16 blocks sharing each weight fragment -- half
+// the ldmatrix traffic, but only 12-15 warps fit: 1.033-1.041 ms.)
+static int query_warps_cap(int plan_warps) {
+    const char* ew = std::getenv("NBVH_QUERY_WARPS");
+    const int w = ew ? std::atoi(ew) : 0;
+    return w >= 1 && w < plan_warps ? w : plan_warps;
 }
 
 template <int kKind, typename Kern>             // kKind: one occupancy cache per kernel family
@@ -1111,10 +1092,6 @@ static cudaError_t launch_persistent(Kern k, int threads, size_t smem, int64_t m
     // occupancy query is cached per (device, hidden, n_points).
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    if (const char* ec = std::getenv("NBVH_QUERY_CARVEOUT")) {   // A/B hook: shared-memory carve-out %
-        e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(ec));
-        if (e != cudaSuccess) return e;
-    }
     int dev = 0;
     cudaGetDevice(&dev);
     constexpr int kDevs = 16;
@@ -1137,23 +1114,15 @@ static cudaError_t launch_query_t(const QueryArgs& a, int64_t max_work, cudaStre
             return launch_persistent<0>(k_query_ws<F, D>, (kWsWorkers + 4) * 32, plan.total, max_work,
                                      2 * kWsWorkers * kWarpQ, a, s, a.m.hidden, a.g.n_points);
     }
-    const int q = query_slots_per_warp();
-    QuerySmemPlan plan(D, a.m.hidden, a.g.n_points, q);
+    QuerySmemPlan plan(D, a.m.hidden, a.g.n_points);
     if (plan.warps < 1) return cudaErrorInvalidValue;
-    if (const char* ew = std::getenv("NBVH_QUERY_WARPS")) {
-        const int w = std::atoi(ew);
-        if (w >= 1 && w < plan.warps) {
-            plan.warps = w;
-            plan.total = plan.warp0 + plan.per_warp * w;
-        }
-    }
-    const int th = plan.warps * 32, rows = plan.warps * q;
-    const int H = a.m.hidden, NP = a.g.n_points;
-    if (q == kWarpQ)
-        return a.m.bf16 ? launch_persistent<3>(k_query_warp<F, D, true, kWarpQ>, th, plan.total, max_work, rows, a, s, H, NP)
-                        : launch_persistent<4>(k_query_warp<F, D, false, kWarpQ>, th, plan.total, max_work, rows, a, s, H, NP);
-    return a.m.bf16 ? launch_persistent<2>(k_query_warp<F, D, true, kQueryQ>, th, plan.total, max_work, rows, a, s, H, NP)
-                    : launch_persistent<1>(k_query_warp<F, D, false, kQueryQ>, th, plan.total, max_work, rows, a, s, H, NP);
+    plan.warps = query_warps_cap(plan.warps);
+    plan.total = plan.warp0 + plan.per_warp * plan.warps;
+    if (a.m.bf16)
+        return launch_persistent<2>(k_query_warp<F, D, true>, plan.warps * 32, plan.total, max_work,
+                                    plan.warps * kWarpQ, a, s, a.m.hidden, a.g.n_points);
+    return launch_persistent<1>(k_query_warp<F, D, false>, plan.warps * 32, plan.total, max_work, plan.warps * kWarpQ,
+                                a, s, a.m.hidden, a.g.n_points);
 }
 
 cudaError_t launch_query(const QueryArgs& a, int64_t max_work, cudaStream_t s) {

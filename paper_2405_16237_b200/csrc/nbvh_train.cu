@@ -252,10 +252,18 @@ static size_t bwd_smem(int D, int H) {
 // Gradient floats of coarse levels k_train_scatter accumulates in shared memory (8 bytes
 // each: two int32 fixed-point parts), budgeted for two CTAs per SM.
 constexpr int64_t kScatterPrivBudget = 52 * 1024;
-// CTAs of k_train_scatter per SM: as many as the shared-memory accumulator allows (<= 6)
-static int scatter_ctas_per_sm(int64_t priv_floats) {
-    const int64_t per_cta = priv_floats * 8 + 2048;
-    return (int)std::max<int64_t>(1, std::min<int64_t>(6, (int64_t)(227 * 1024) / per_cta));
+// Levels the default scatter warp-aggregates (k_train_scatter_agg; profiles/NOTES.md r2d)
+constexpr int kScatterAggLevels = 6;
+// Dynamic shared memory of the T7 scatter: the fixed-point accumulator, and with warp
+// aggregation one [32][8F]-float slot array per warp (8 warps)
+static size_t scatter_smem(const TrainArgs& a) {
+    const size_t priv = (size_t)((2 * (int64_t)a.priv_floats + 3) & ~(int64_t)3) * 4;
+    return priv + (a.agg_levels > 0 ? (size_t)8 * 32 * 8 * a.g.F * 4 : 0);
+}
+// CTAs of the scatter per SM: as many as its shared memory allows (<= 6)
+static int scatter_ctas_per_sm(const TrainArgs& a) {
+    const int64_t per_cta = (int64_t)scatter_smem(a) + 2048;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(6, (int64_t)(228 * 1024) / per_cta));
 }
 
 // T7 scratch layout (k_train_scatter): every dense level cell-packed (N^3 cells x 8 corners x
@@ -275,7 +283,7 @@ static nbvh_status ensure_scatter_scratch(nbvh_ctx* c, TrainArgs& a, int sms) {
         nd = (nd + 3) & ~(int64_t)3;
         nh = (nh + 3) & ~(int64_t)3;
     }
-    const int64_t np = (int64_t)sms * scatter_ctas_per_sm(a.priv_floats) * 2 * a.priv_floats;
+    const int64_t np = (int64_t)sms * scatter_ctas_per_sm(a) * 2 * a.priv_floats;
     cudaError_t e = cudaSuccess;
     if (nd > w->sc_dense_floats) {
         dfree(w->sc_dense);
@@ -299,7 +307,7 @@ static nbvh_status ensure_scatter_scratch(nbvh_ctx* c, TrainArgs& a, int sms) {
     a.sc_dense = w->sc_dense;
     a.sc_hash = w->sc_hash;
     a.sc_priv = w->sc_priv;
-    a.scatter_ctas = sms * scatter_ctas_per_sm(a.priv_floats);
+    a.scatter_ctas = sms * scatter_ctas_per_sm(a);
     w->sc_dense_floats = std::max(w->sc_dense_floats, nd);
     return NBVH_OK;
 }
@@ -316,7 +324,7 @@ static cudaError_t launch_train_fd(const TrainArgs& a0, const TrainArgs& a, int3
     const int H = a.m.hidden;
     const size_t smem_fwd = FwdSmemPlan(D, H, a.g.n_points).total;
     const size_t smem_bwd = bwd_smem(D, H);
-    const size_t smem_sc = (size_t)a.priv_floats * 8;
+    const size_t smem_sc = scatter_smem(a);
     const size_t smem_dw = (size_t)kTileQ * 72 * 2 + (size_t)kTileQ * (D + 8) * 2 + kTileQ * 8 * 4;
     cudaError_t e = cudaFuncSetAttribute(k_train_fwd<F, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fwd);
     if (e == cudaSuccess)
@@ -324,7 +332,8 @@ static cudaError_t launch_train_fd(const TrainArgs& a0, const TrainArgs& a, int3
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_train_dw<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_dw);
     if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k_train_scatter<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_sc);
+        e = cudaFuncSetAttribute(a.agg_levels > 0 ? (const void*)k_train_scatter_agg<F> : (const void*)k_train_scatter<F>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_sc);
     if (e != cudaSuccess) return e;
     const unsigned blocks_n = (unsigned)((n + 127) / 128);
     if (ev) cudaEventRecord(ev[0], s);
@@ -354,7 +363,8 @@ static cudaError_t launch_train_fd(const TrainArgs& a0, const TrainArgs& a, int3
     e = cudaMemsetAsync(a.sc_dense, 0, sizeof(float) * (size_t)a.sc_dense_n, s);
     if (e == cudaSuccess) e = cudaMemsetAsync(a.sc_hash, 0, sizeof(float) * (size_t)a.sc_hash_n, s);
     if (e != cudaSuccess) return e;
-    k_train_scatter<F><<<a.scatter_ctas, 256, smem_sc, s>>>(a);
+    if (a.agg_levels > 0) k_train_scatter_agg<F><<<a.scatter_ctas, 256, smem_sc, s>>>(a);
+    else k_train_scatter<F><<<a.scatter_ctas, 256, smem_sc, s>>>(a);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     k_train_scatter_finish<F><<<4 * sms, 256, 0, s>>>(a);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -502,8 +512,17 @@ extern "C" nbvh_status nbvh_train_backward(nbvh_ctx* c, const nbvh_ray* rays, in
         const char* ev = std::getenv("NBVH_DW_MMA_SYNC");
         a.use_tc_dw = (ev && ev[0] == '1') ? 0 : 1;
     }
-    const char* pev = std::getenv("NBVH_PRIV_BYTES");   // tuning hook (0 disables)
-    const int64_t priv_budget = pev ? std::min<int64_t>(std::atoll(pev), kScatterPrivBudget) : kScatterPrivBudget;
+    {
+        // T7: warp aggregation on the coarse levels (kScatterAggLevels; NBVH_SCATTER_AGG=n
+        // overrides, 0 selects k_train_scatter with the privatised levels)
+        const char* ev = std::getenv("NBVH_SCATTER_AGG");
+        a.agg_levels = std::max(0, std::min(ev ? std::atoi(ev) : kScatterAggLevels, (int)c->cfg.L));
+    }
+    // shared-memory privatisation: only without aggregation by default (NBVH_PRIV_BYTES
+    // overrides; 0 disables)
+    const char* pev = std::getenv("NBVH_PRIV_BYTES");
+    const int64_t priv_budget = pev ? std::min<int64_t>(std::atoll(pev), kScatterPrivBudget)
+                                    : (a.agg_levels > 0 ? 0 : kScatterPrivBudget);
     for (int l = 0; l < c->cfg.L && c->dense[l]; ++l) {
         const int64_t end = (c->offset[l] + (int64_t)(c->res[l] + 1) * (c->res[l] + 1) * (c->res[l] + 1)) * c->cfg.F;
         if (end * 4 > priv_budget) break;

@@ -67,6 +67,7 @@ struct TrainArgs {
     int64_t sc_off[kMaxLevels];   // float offset of a level's scratch (dense: in sc_dense; hashed: in sc_hash)
     int64_t sc_dense_n, sc_hash_n;   // scratch sizes (floats)
     int32_t scatter_ctas;
+    int32_t agg_levels;      // k_train_scatter_agg: levels 0..agg_levels-1 warp-aggregated (0: k_train_scatter)
     int32_t use_tc_dw;       // weight GEMMs on tcgen05 (k_train_dw_tc) when the shape allows
 };
 
@@ -715,6 +716,164 @@ __global__ void __launch_bounds__(256) k_train_scatter(TrainArgs a) {
                     } else {
                         red_entry<F>(base + (int64_t)e0 * F, u);
                         red_entry<F>(base + (int64_t)e1 * F, w2);
+                    }
+                }
+            }
+        }
+    }
+    __syncthreads();
+    int32_t* out = a.sc_priv + (int64_t)blockIdx.x * 2 * a.priv_floats;
+    for (int i = tid; i < 2 * a.priv_floats; i += blockDim.x) out[i] = priv[i];
+}
+
+// T7 with warp aggregation (the default; the samples in leaf order, k_sort_place): a warp's 32
+// items are 8 samples x 4 points of (mostly) one leaf, so on the coarse levels many of them
+// fall into the same grid cell.  On levels l < agg_levels the lanes are grouped by cell
+// (__match_any_sync on the cell coordinates); the group's 8F sums sum_j w_j[k] g_j[f]
+// (ascending lane order, fp32) are spread over its lanes -- the lane of rank q computes values
+// q, q + cnt, ... from the members' weights and dL/dx staged in shared memory -- and the
+// group's lowest lane makes the one set of reductions for the cell (the destinations of
+// k_train_scatter; on privatised levels the group sum is split into the fixed-point parts).
+// Finer levels: one set per item.  Measured on the cfg-5 step (profiles/NOTES.md r2d): L1
+// data-pipe wavefronts are what bound the scatter (a red sector or a shared atomic is one
+// each); aggregating levels 0-5 instead of privatising 0-2 removes the shared atomics and
+// ~1/6 of the red sectors for ~1/4 more shared loads/stores: 0.720 vs 0.749 ms backward.
+// (Tried: a register butterfly for whole-warp groups, 0.765; redux.sync fixed-point group
+// sums, 0.784.)
+template <int F>
+__global__ void __launch_bounds__(256) k_train_scatter_agg(TrainArgs a) {
+    extern __shared__ __align__(16) int32_t priv[];          // [2][priv_floats], then per warp [32][8F]
+    __shared__ LevelSm lv[kMaxLevels];
+    constexpr int S = 8 * F;                                  // floats per lane slot (>= 8 + F)
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    float* abuf = reinterpret_cast<float*>(priv + ((2 * a.priv_floats + 3) & ~3)) + warp * 32 * S;
+    stage_levels(a.g, lv, tid);
+    for (int i = tid; i < 2 * a.priv_floats; i += blockDim.x) priv[i] = 0;
+    __syncthreads();
+    const int M = *a.n_samples, NP = a.g.n_points, L = a.g.L, D = NP * L * F;
+    const uint32_t hmask = (1u << a.g.log2_T) - 1u;
+    const int64_t items = (int64_t)M * NP;
+    const unsigned lt = (1u << lane) - 1u;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (tid & ~31); base < items;
+         base += (int64_t)gridDim.x * blockDim.x) {              // warp-uniform trip count
+        const int64_t it = base + lane;
+        const bool valid = it < items;
+        const int i = valid ? (int)(it / NP) : 0, p = valid ? (int)(it - (int64_t)i * NP) : 0;
+        const int r = a.s_ray[i];
+        const float4 r0 = __ldg(a.rays + 2 * (int64_t)r), r1 = __ldg(a.rays + 2 * (int64_t)r + 1);
+        const float o[3] = {r0.x, r0.y, r0.z}, d[3] = {r1.x, r1.y, r1.z};
+        float x[3];
+        segment_point(a.g, o, d, a.s_t0[i], a.s_t1[i], p, NP, a.xi + (int64_t)r * NP, x);   // the forward's point (C8)
+        const float* gq = a.gx + (int64_t)i * D + p * L * F;
+        for (int l = 0; l < L; ++l) {
+            const LevelSm P = lv[l];
+            float gv[F];
+#pragma unroll
+            for (int f = 0; f < F; ++f) gv[f] = valid ? gq[l * F + f] : 0.f;
+            Cell cell;
+            uint32_t i0, i1, i2;
+            level_cell_sm(P, hmask, x[0], x[1], x[2], cell, i0, i1, i2);
+            float u[8][F];
+            bool emit = valid;
+            int cnt = 1;
+            if (l < a.agg_levels) {
+                const uint32_t N = (uint32_t)P.resf;
+                const uint32_t key = valid ? i0 + N * (i1 + N * i2) : (0x80000000u | (uint32_t)lane);   // N^3 < 2^31
+                const unsigned peers = __match_any_sync(0xffffffffu, key);
+                cnt = __popc(peers);
+                if (cnt > 1) {
+                    float* my = abuf + lane * S;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) my[k] = cell.w[k];
+#pragma unroll
+                    for (int f = 0; f < F; ++f) my[8 + f] = gv[f];
+                }
+                __syncwarp();
+                const int leader = __ffs(peers) - 1, rank = __popc(peers & lt);
+                float res[S];
+                if (cnt > 1) {
+#pragma unroll
+                    for (int t = 0; t < S; ++t) {
+                        const int v = rank + t * cnt;
+                        res[t] = 0.f;
+                        if (v < S) {
+                            const int k = v / F, f = v - k * F;
+                            float acc = 0.f;
+                            for (unsigned m = peers; m; m &= m - 1u) {
+                                const float* js = abuf + (__ffs(m) - 1) * S;
+                                acc = __fadd_rn(acc, __fmul_rn(js[k], js[8 + f]));
+                            }
+                            res[t] = acc;
+                        }
+                    }
+                }
+                __syncwarp();
+                if (cnt > 1) {
+#pragma unroll
+                    for (int t = 0; t < S; ++t) {
+                        const int v = rank + t * cnt;
+                        if (v < S) abuf[leader * S + v] = res[t];
+                    }
+                }
+                __syncwarp();
+                if (cnt > 1) {
+                    emit = valid && lane == leader;
+                    if (emit) {
+#pragma unroll
+                        for (int k = 0; k < 8; ++k)
+#pragma unroll
+                            for (int f = 0; f < F; ++f) u[k][f] = abuf[lane * S + k * F + f];
+                    }
+                }
+            }
+            if (cnt == 1) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+#pragma unroll
+                    for (int f = 0; f < F; ++f) u[k][f] = __fmul_rn(cell.w[k], gv[f]);
+            }
+            if (!emit) continue;
+            if (l < a.priv_levels) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+#pragma unroll
+                    for (int f = 0; f < F; ++f) {
+                        const float v = u[k][f];
+                        const int64_t e = (int64_t)(P.coff + cell.idx[k]) * F + f;
+                        NBVH_DCHECK(e < a.priv_floats);
+                        if (fabsf(v) < kFixLimit) {
+                            const float hi = rintf(v * kFixHi);
+                            const float lo = __fmaf_rn(-hi, 1.0f / kFixHi, v);
+                            atomicAdd(priv + e, (int)hi);
+                            atomicAdd(priv + a.priv_floats + e, __float2int_rn(lo * kFixLo));
+                        } else {
+                            atomicAdd(a.grad + e, v);
+                        }
+                    }
+            } else if (P.n1) {
+                float* dst = a.sc_dense + a.sc_off[l] + (int64_t)(i0 + P.nx * i1 + P.nxy * i2) * 8 * F;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    if constexpr (F == 2) {
+                        red_add_v4(dst + 4 * j, u[2 * j][0], u[2 * j][1], u[2 * j + 1][0], u[2 * j + 1][1]);
+                    } else {
+                        red_entry<F>(dst + (2 * j) * F, u[2 * j]);
+                        red_entry<F>(dst + (2 * j + 1) * F, u[2 * j + 1]);
+                    }
+                }
+            } else {
+                float* dst = a.sc_hash + a.sc_off[l];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const uint32_t e0 = cell.idx[2 * j], e1 = cell.idx[2 * j + 1];
+                    if (F == 2 && (e0 ^ e1) == 1u) {
+                        const bool lo0 = e0 < e1;
+                        const float a0 = u[2 * j][0], a1 = u[2 * j][F - 1], b0 = u[2 * j + 1][0], b1 = u[2 * j + 1][F - 1];
+                        red_add_v4(dst + (int64_t)(e0 & ~1u) * 2, lo0 ? a0 : b0, lo0 ? a1 : b1, lo0 ? b0 : a0,
+                                   lo0 ? b1 : a1);
+                    } else {
+                        red_entry<F>(dst + (int64_t)e0 * F, u[2 * j]);
+                        red_entry<F>(dst + (int64_t)e1 * F, u[2 * j + 1]);
                     }
                 }
             }

@@ -440,8 +440,8 @@ def test_query_kernel_variants(orc, monkeypatch):
         monkeypatch.setenv("NBVH_QUERY_MLP", variant)
         ctx, sc, tab, layers = _mk_ctx("tiny")
         _check_query(orc, ctx, tab, layers, _rays_tiny())
-    # per-warp kernel A/B hooks: 32 slots per warp (two m16 blocks per MLP call), fewer warps
-    for env in (dict(NBVH_QUERY_Q="32"), dict(NBVH_QUERY_WARPS="5")):
+    # per-warp kernel A/B hook: fewer warps per CTA
+    for env in (dict(NBVH_QUERY_WARPS="5"),):
         for k, v in env.items():
             monkeypatch.setenv(k, v)
         ctx, sc, tab, layers = _mk_ctx("tiny")
@@ -582,10 +582,11 @@ def test_query_bf16_end_to_end(orc):
 
 
 def test_deep_cut_traversal_full_base_bvh(orc):
-    """k_traverse's shared memory is (depth + 2 + 3K) x 512 B, past 48 KB (opt-in)
-    for depth > 46 at K = 16.  The deepest cut the scenes give: every base-BVH leaf of the
-    988,928-triangle 1080p scene (SAH leaves of <= 4 triangles).  Lists vs the oracle's
-    brute force, the product traversal (k_traverse) through the end-to-end replay."""
+    """The deepest cut the scenes give: every base-BVH leaf of the 988,928-triangle 1080p scene
+    (532,435 SAH leaves of <= 4 triangles, depth 24).  Product lists (k_traverse, K = 16) vs
+    the oracle's brute force, and the query's exact replay.  (k_traverse's shared memory is
+    (depth + 2 + 3K) x 512 B; the launcher opts in past 48 KB, i.e. depth > 46 at K = 16,
+    which no SAH tree of these scenes reaches.)"""
     from paper_2405_16237_b200 import Context, PARAM_TABLES
     sc = synth.scene_1080p()
     c = synth.CONFIGS["1080p"]["hash"]
@@ -595,7 +596,7 @@ def test_deep_cut_traversal_full_base_bvh(orc):
     n_leaves, clamped = ctx.build_cut(10 ** 7)
     ca, cb = ctx.base_bvh()
     n_base = int((cb < 0).sum())
-    assert n_leaves == n_base and clamped
+    assert n_leaves == n_base
     depth, st = 0, [(0, 1)]
     while st:
         j, k = st.pop()
@@ -619,4 +620,12 @@ def test_deep_cut_traversal_full_base_bvh(orc):
         k = fill[i]
         assert np.array_equal(leaf[i, :k], wl[i, :k])
     assert wcnt.max() > 16 and np.all(more[wcnt > 16] == 1)
-    _check_query(orc, ctx, tab=tab.reshape(-1, c.F), layers=layers, rays=rays, band_max=0.02)
+    # the query's logic on this cut: exact replay of its own z trace (the double-oracle band
+    # does not apply: half a million leaves put many t comparisons within 5e-3)
+    out, zt = ctx.debug_query_trace(torch.from_numpy(rays).cuda(), 64)
+    g = {k: v.cpu().numpy() for k, v in out.items()}
+    rep = orc.replay(cut["leaf_lo"], cut["leaf_hi"], rays, zt.cpu().numpy(), mode=0)
+    assert rep["missing"] == 0
+    assert np.array_equal(g["hit"], rep["hit"]) and np.array_equal(g["leaf"], rep["leaf"])
+    assert np.array_equal(g["n_queries"], rep["nq"])
+    assert np.array_equal(g["t"].view(np.uint32), rep["t"].view(np.uint32))

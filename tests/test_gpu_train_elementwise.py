@@ -47,13 +47,19 @@ def _to(x):
     return torch.from_numpy(np.ascontiguousarray(x)).cuda()
 
 
-def _run(name, dw_path, monkeypatch, n_rays=6000, seed=70):
+def _run(name, dw_path, monkeypatch, n_rays=6000, seed=70, scatter="agg"):
     import oracle as orc
     from paper_2405_16237_b200 import Context, PARAM_TABLES, dp
     if dw_path == "mma_sync":
         monkeypatch.setenv("NBVH_DW_MMA_SYNC", "1")
     else:
         monkeypatch.delenv("NBVH_DW_MMA_SYNC", raising=False)
+    # T7 kernel: "agg" = the default warp-aggregated scatter, "priv" = k_train_scatter with the
+    # shared-memory fixed-point levels (NBVH_SCATTER_AGG=0)
+    if scatter == "priv":
+        monkeypatch.setenv("NBVH_SCATTER_AGG", "0")
+    else:
+        monkeypatch.delenv("NBVH_SCATTER_AGG", raising=False)
     L, F, log2_T, npts, H = CONFIGS[name]
     sc = synth.scene_tiny()
     ctx = Context(device=0, L=L, F=F, log2_T=log2_T, n_points=npts, hidden_layers=H)
@@ -95,12 +101,13 @@ def _run(name, dw_path, monkeypatch, n_rays=6000, seed=70):
                 p=p, o=o, H=H, npts=npts, F=F, u=u, rank=rank)
 
 
-@pytest.mark.parametrize("name,dw_path", [("tiny_h2", "tcgen05"), ("tiny_h3", "tcgen05"), ("cfg2_grid", "tcgen05"),
-                                          ("cfg2_grid", "mma_sync"), ("paper", "tcgen05")])
-def test_training_stages_elementwise(name, dw_path, monkeypatch):
+@pytest.mark.parametrize("name,dw_path,scatter", [("tiny_h2", "tcgen05", "agg"), ("tiny_h3", "tcgen05", "agg"),
+                                                  ("cfg2_grid", "tcgen05", "agg"), ("cfg2_grid", "mma_sync", "priv"),
+                                                  ("paper", "tcgen05", "agg"), ("paper", "tcgen05", "priv")])
+def test_training_stages_elementwise(name, dw_path, scatter, monkeypatch):
     import oracle as orc
     from paper_2405_16237_b200 import PARAM_TABLES
-    R = _run(name, dw_path, monkeypatch)
+    R = _run(name, dw_path, monkeypatch, scatter=scatter)
     p, o, H, g = R["p"], R["o"], R["H"], R["g"]
     m = p["ray"].size
     assert m > 500, m

@@ -786,7 +786,9 @@ static int plan_chunks(int64_t n, ChunkPlan* plan) {
     for (int k = 0; k < chunks; ++k) W += wts[k];
     // NBVH_HOST_CONTIG=1: one period, i.e. contiguous chunks (tuning hook)
     const char* cev = std::getenv("NBVH_HOST_CONTIG");
-    const int64_t blk = (cev && cev[0] == '1') ? std::max<int64_t>(1, n / W) : kHostBlock;
+    int64_t blk = kHostBlock;
+    if (const char* bev = std::getenv("NBVH_HOST_BLOCK")) blk = std::max<int64_t>(1, std::atoll(bev));   // tuning hook
+    if (cev && cev[0] == '1') blk = std::max<int64_t>(1, n / W);
     const int64_t periods = n / (blk * W);
     int64_t off = 0, first = 0;
     for (int k = 0; k < chunks; ++k) {

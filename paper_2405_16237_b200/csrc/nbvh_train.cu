@@ -379,7 +379,7 @@ static cudaError_t launch_train_fd(const TrainArgs& a0, const TrainArgs& a, int3
             const size_t sm = dw_tc_smem(D, Hc);
             e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
             if (e != cudaSuccess) return;
-            kern<<<sms, 128, sm, s>>>(a, w_off);
+            kern<<<sms, kDwThreads, sm, s>>>(a, w_off);
             e = cudaGetLastError();
             tc_done = e == cudaSuccess;
         };

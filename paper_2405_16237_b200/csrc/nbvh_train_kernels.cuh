@@ -1203,24 +1203,30 @@ __global__ void __launch_bounds__(256, 2) k_train_bias_out(TrainArgs a, int64_t 
 // The diagonal blocks D[rows of layer k][cols 64k..] are dW_k^T; the off-diagonal blocks
 // are discarded (3x the useful flops, free on the tensor pipe; one operand pass over HBM).
 // One CTA of 4 warps per SM, split-K over 64-sample chunks: 128 threads stage chunks with
-// cp.async into the MN-major no-swizzle canonical layout (3-stage ring), thread 0 issues
+// cp.async into the MN-major no-swizzle canonical layout (4-stage ring, loads issued two
+// chunks ahead so the operand stream is not latency-bound), thread 0 issues
 // tcgen05.mma (M=128 halves, N=Ntot, K=16) into a TMEM accumulator and commits each stage
 // to an mbarrier; the epilogue reads TMEM (tcgen05.ld) and adds the useful blocks into the
 // gradient buffer once per CTA.
 constexpr int kDwK = 64;            // samples per chunk (4 MMA K-steps)
-constexpr int kDwStages = 3;
+constexpr int kDwGB = kDwK * 16;    // bytes of one 8-row group of a stage (kDwK/8 core matrices of 128 B)
+constexpr int kDwStages = 4;
+constexpr int kDwAhead = 2;         // chunks whose loads are in flight while one is multiplied
 
 __host__ __device__ constexpr int dw_tc_mtot(int D, int H) { return D + 64 * (H - 1); }
-__host__ __device__ constexpr bool dw_tc_ok(int D, int H) { return dw_tc_mtot(D, H) <= 256 && 64 * H <= 256; }
 __host__ __device__ constexpr size_t dw_tc_smem(int D, int H) {
-    return (size_t)kDwStages * ((size_t)((dw_tc_mtot(D, H) + 127) / 128) * 16 * 1024 + (size_t)H * 8 * 1024) + 64;
+    return (size_t)kDwStages * ((size_t)((dw_tc_mtot(D, H) + 127) / 128) * 16 + (size_t)H * 8) * kDwGB + 64;
+}
+__host__ __device__ constexpr bool dw_tc_ok(int D, int H) {
+    return dw_tc_mtot(D, H) <= 256 && 64 * H <= 256 && dw_tc_smem(D, H) <= 227 * 1024;
 }
 
+constexpr int kDwThreads = 128;     // 4 warps stage operands and read back (one per TMEM lane quadrant)
 template <int D, int H>
-__global__ void __launch_bounds__(128, 1) k_train_dw_tc(TrainArgs a, int64_t w_off) {
+__global__ void __launch_bounds__(kDwThreads, 1) k_train_dw_tc(TrainArgs a, int64_t w_off) {
     constexpr int Mtot = dw_tc_mtot(D, H), Mh = (Mtot + 127) / 128, Ntot = 64 * H;
     constexpr int MG = Mh * 16, NG = Ntot / 8;                // 8-row groups of A, B
-    constexpr uint32_t kAB = MG * 1024, kBB = NG * 1024;      // bytes per stage (8 k-groups x 128 B per group)
+    constexpr uint32_t kAB = MG * kDwGB, kBB = NG * kDwGB;    // bytes per stage
     constexpr uint32_t kIdesc = tc::idesc_f16(128, Ntot, true, true);
     extern __shared__ __align__(16) unsigned char smem_dw[];
     unsigned char* stA = smem_dw;
@@ -1245,33 +1251,44 @@ __global__ void __launch_bounds__(128, 1) k_train_dw_tc(TrainArgs a, int64_t w_o
         const int64_t s0 = (int64_t)chunk * kDwK;
         unsigned char* A = stA + st * kAB;
         unsigned char* B = stB + st * kBB;
-        const int k = tid >> 1, par = tid & 1;               // 64 samples x 2 groups per pass
+        constexpr int kPar = kDwThreads / kDwK;              // threads per sample
+        const int k = tid / kPar, par = tid % kPar;          // kDwK samples x kPar groups per pass
         const int64_t sm = s0 + k;
         const bool ok = sm < M;
         const int64_t sr = ok ? sm : 0;
         const uint32_t koff = (uint32_t)((k >> 3) * 128 + (k & 7) * 16);
-        for (int g = par; g < MG; g += 2) {                   // A: features / activations
+        for (int g = par; g < MG; g += kPar) {                // A: features / activations
             const int row = g * 8;
             const __half* src;
             if (row < D) src = a.X + sr * D + row;
             else if (row < Mtot) src = a.A + (int64_t)((row - D) / 64) * a.cap * 64 + sr * 64 + ((row - D) & 63);
             else src = a.X;                                   // padding rows: never read back
-            tc::cp16_zfill(A + g * 1024 + koff, src, ok && row < Mtot);
+            tc::cp16_zfill(A + g * kDwGB + koff, src, ok && row < Mtot);
         }
-        for (int g = par; g < NG; g += 2) {                   // B: deltas
+        for (int g = par; g < NG; g += kPar) {                // B: deltas
             const int col = g * 8;
             const __half* src = a.Dl + (int64_t)(col / 64) * a.cap * 64 + sr * 64 + (col & 63);
-            tc::cp16_zfill(B + g * 1024 + koff, src, ok);
+            tc::cp16_zfill(B + g * kDwGB + koff, src, ok);
         }
     };
 
+    // prologue: the first kDwAhead chunks' loads
+#pragma unroll
+    for (int p = 0; p < kDwAhead; ++p) {
+        const int c = blockIdx.x + p * gridDim.x;
+        if (c < n_chunks) stage(c, p);
+        tc::cp_commit();
+    }
     int it = 0;
     for (int c = blockIdx.x; c < n_chunks; c += gridDim.x, ++it) {
         const int st = it % kDwStages;
-        if (it >= kDwStages) tc::mbar_wait(mbar + st, ((it / kDwStages) - 1) & 1);   // MMAs of it-3 done
-        stage(c, st);
-        tc::cp_commit();
-        tc::cp_wait<0>();
+        {   // loads of chunk it + kDwAhead into the stage last multiplied at it + kDwAhead - kDwStages
+            const int cn = c + kDwAhead * gridDim.x, jn = it + kDwAhead, stn = jn % kDwStages;
+            if (jn >= kDwStages) tc::mbar_wait(mbar + stn, ((jn / kDwStages) - 1) & 1);
+            if (cn < n_chunks) stage(cn, stn);
+            tc::cp_commit();                  // (an empty group past the end keeps the count uniform)
+        }
+        tc::cp_wait<kDwAhead>();              // this chunk's group has landed
         tc::fence_proxy_async();
         __syncthreads();
         if (tid == 0) {
@@ -1279,10 +1296,10 @@ __global__ void __launch_bounds__(128, 1) k_train_dw_tc(TrainArgs a, int64_t w_o
             const uint32_t a0 = tc::smem_u32(stA + st * kAB), b0 = tc::smem_u32(stB + st * kBB);
 #pragma unroll
             for (int kk = 0; kk < kDwK / 16; ++kk) {
-                const uint64_t bd = tc::smem_desc(b0 + kk * 256, 128, 1024);
+                const uint64_t bd = tc::smem_desc(b0 + kk * 256, 128, kDwGB);
 #pragma unroll
                 for (int h = 0; h < Mh; ++h) {
-                    const uint64_t ad = tc::smem_desc(a0 + h * 16 * 1024 + kk * 256, 128, 1024);
+                    const uint64_t ad = tc::smem_desc(a0 + h * 16 * kDwGB + kk * 256, 128, kDwGB);
                     tc::mma_f16(tmem + h * 256, ad, bd, kIdesc, (it > 0 || kk > 0) ? 1u : 0u);
                 }
             }
@@ -1295,7 +1312,7 @@ __global__ void __launch_bounds__(128, 1) k_train_dw_tc(TrainArgs a, int64_t w_o
         tc::mbar_wait(mbar + (last % kDwStages), (last / kDwStages) & 1);
     }
     tc::fence_after();
-    if (it > 0) {
+    if (it > 0 && tid < 128) {
         // thread tid <-> TMEM lane tid <-> A row (h*128 + tid); useful columns = its layer's deltas
 #pragma unroll 1
         for (int h = 0; h < Mh; ++h) {

@@ -244,10 +244,9 @@ void reset_adam(nbvh_ctx* c) {
 }
 
 // launchers (templated on F, D)
-// Shared memory of k_train_bwd without the private gradient accumulator, and the bytes left
-// for that accumulator under the per-CTA opt-in limit.
+// Shared memory of k_train_bwd: the weights and one staging tile per warp
 static size_t bwd_smem(int D, int H) {
-    return ((size_t)64 * (D + 8) + (size_t)(H - 1) * 64 * 72 + 16 * 72) * 2;
+    return ((bwd_weights_bytes(D, H) + 15) & ~(size_t)15) + (size_t)kBwdWarps * bwd_tile_bytes(D);
 }
 // Gradient floats of coarse levels k_train_scatter accumulates in shared memory (8 bytes
 // each: two int32 fixed-point parts), budgeted for two CTAs per SM.

@@ -378,7 +378,6 @@ __global__ void __launch_bounds__(kFwdWarps * 32, 1) k_train_fwd(TrainArgs a) {
         }
         // MLP forward: 16 rows; hidden activations to global
         {
-            const int64_t gr0 = i0 + g, gr1 = gr0 + 8;
             float acc[8][4];
             for (int nt = 0; nt < 8; ++nt) {
                 float b0 = ms.b[nt * 8 + 2 * t], b1 = ms.b[nt * 8 + 2 * t + 1];
@@ -427,17 +426,25 @@ __global__ void __launch_bounds__(kFwdWarps * 32, 1) k_train_fwd(TrainArgs a) {
                     h[kb][2] = pack_relu_half2(acc[2 * kb + 1][0], acc[2 * kb + 1][1]);
                     h[kb][3] = pack_relu_half2(acc[2 * kb + 1][2], acc[2 * kb + 1][3]);
                 }
+                // activations out through the (consumed) feature rows: fragment layout -> [16][64]
+                // rows in shared memory, then 16-byte row-contiguous stores (a 4-byte fragment
+                // store per lane would touch 16 rows' lines per instruction)
                 __half* Al = a.A + (int64_t)layer * a.cap * 64;
+                __syncwarp();                     // every lane's ldmatrix of the previous contents done
 #pragma unroll
                 for (int kb = 0; kb < 4; ++kb) {
-                    if (gr0 < M) {
-                        *reinterpret_cast<uint32_t*>(Al + gr0 * 64 + kb * 16 + 2 * t) = h[kb][0];
-                        *reinterpret_cast<uint32_t*>(Al + gr0 * 64 + kb * 16 + 8 + 2 * t) = h[kb][2];
-                    }
-                    if (gr1 < M) {
-                        *reinterpret_cast<uint32_t*>(Al + gr1 * 64 + kb * 16 + 2 * t) = h[kb][1];
-                        *reinterpret_cast<uint32_t*>(Al + gr1 * 64 + kb * 16 + 8 + 2 * t) = h[kb][3];
-                    }
+                    *reinterpret_cast<uint32_t*>(feat + g * (D + 8) + kb * 16 + 2 * t) = h[kb][0];
+                    *reinterpret_cast<uint32_t*>(feat + g * (D + 8) + kb * 16 + 8 + 2 * t) = h[kb][2];
+                    *reinterpret_cast<uint32_t*>(feat + (g + 8) * (D + 8) + kb * 16 + 2 * t) = h[kb][1];
+                    *reinterpret_cast<uint32_t*>(feat + (g + 8) * (D + 8) + kb * 16 + 8 + 2 * t) = h[kb][3];
+                }
+                __syncwarp();
+#pragma unroll
+                for (int c = lane; c < 16 * 8; c += 32) {
+                    const int row = c >> 3, c8 = c & 7;
+                    if (row < nv)
+                        *reinterpret_cast<uint4*>(Al + (i0 + row) * 64 + c8 * 8) =
+                            *reinterpret_cast<const uint4*>(feat + row * (D + 8) + c8 * 8);
                 }
             }
             float o[4];
@@ -500,6 +507,14 @@ struct BwdSmem {
     __half* wh;   // [H-1][64][72]
     __half* wo;   // [16][72], rows 8..15 zero
 };
+// bytes of k_train_bwd's shared memory: the weights, then per warp one staging tile that
+// turns the fragment-layout row accesses into row-contiguous 16-byte global accesses:
+// [16][D+4] fp32 for dL/dx, aliased by [16][72] fp16 for the activation masks and deltas
+__host__ __device__ constexpr size_t bwd_weights_bytes(int D, int H) {
+    return ((size_t)64 * (D + 8) + (size_t)(H - 1) * 64 * 72 + 16 * 72) * 2;
+}
+__host__ __device__ constexpr size_t bwd_tile_bytes(int D) { return (size_t)16 * (D + 4) * 4; }
+constexpr int kBwdWarps = 8;
 
 template <int F, int D>
 __global__ void __launch_bounds__(256, 2) k_train_bwd(TrainArgs a) {
@@ -527,10 +542,14 @@ __global__ void __launch_bounds__(256, 2) k_train_bwd(TrainArgs a) {
     }
     __syncthreads();
     const int g = lane >> 2, t = lane & 3;
+    float* gxs = reinterpret_cast<float*>(smem_raw + ((bwd_weights_bytes(D, H) + 15) & ~(size_t)15) +
+                                          (size_t)warp * bwd_tile_bytes(D));      // [16][D+4]
+    __half* ts = reinterpret_cast<__half*>(gxs);                                  // [16][72] (aliases)
     // warp item = 16 samples; no block-wide barrier after the staging
-    for (int blk = blockIdx.x * 8 + warp; blk * 16 < M; blk += gridDim.x * 8) {
+    for (int blk = blockIdx.x * kBwdWarps + warp; blk * 16 < M; blk += gridDim.x * kBwdWarps) {
         const int64_t gr0 = (int64_t)blk * 16 + g, gr1 = gr0 + 8;
         const bool v0 = gr0 < M, v1 = gr1 < M;
+        const int nv = min(16, M - blk * 16);
         // delta_H = dL/dz as an m16k16 A fragment (k 8..15 zero)
         uint32_t af[4][4];
         {
@@ -558,21 +577,43 @@ __global__ void __launch_bounds__(256, 2) k_train_bwd(TrainArgs a) {
                     mma16816(acc[2 * np + 1], af[kb], b2, b3);
                 }
             }
-            // relu'(h_k) mask and store delta_k
+            // relu'(h_k) mask and store delta_k (rows staged through ts: 16-byte row-contiguous
+            // global loads / stores instead of 4-byte fragment accesses spread over 16 rows)
             const __half* Ak = a.A + (int64_t)k * a.cap * 64;
             __half* Dk = a.Dl + (int64_t)k * a.cap * 64;
+            const int64_t r0 = (int64_t)blk * 16;
+#pragma unroll
+            for (int c = lane; c < 16 * 8; c += 32) {
+                const int row = c >> 3, c8 = c & 7;
+                *reinterpret_cast<uint4*>(ts + row * 72 + c8 * 8) =
+                    row < nv ? *reinterpret_cast<const uint4*>(Ak + (r0 + row) * 64 + c8 * 8) : make_uint4(0, 0, 0, 0);
+            }
+            __syncwarp();
 #pragma unroll
             for (int nt = 0; nt < 8; ++nt) {
                 const int col = nt * 8 + 2 * t;
-                float2 h0 = v0 ? unpack_half2(*reinterpret_cast<const uint32_t*>(Ak + gr0 * 64 + col)) : make_float2(0.f, 0.f);
-                float2 h1 = v1 ? unpack_half2(*reinterpret_cast<const uint32_t*>(Ak + gr1 * 64 + col)) : make_float2(0.f, 0.f);
+                const float2 h0 = unpack_half2(*reinterpret_cast<const uint32_t*>(ts + g * 72 + col));
+                const float2 h1 = unpack_half2(*reinterpret_cast<const uint32_t*>(ts + (g + 8) * 72 + col));
                 acc[nt][0] = h0.x > 0.f ? acc[nt][0] : 0.f;
                 acc[nt][1] = h0.y > 0.f ? acc[nt][1] : 0.f;
                 acc[nt][2] = h1.x > 0.f ? acc[nt][2] : 0.f;
                 acc[nt][3] = h1.y > 0.f ? acc[nt][3] : 0.f;
-                if (v0) *reinterpret_cast<uint32_t*>(Dk + gr0 * 64 + col) = pack_half2(acc[nt][0], acc[nt][1]);
-                if (v1) *reinterpret_cast<uint32_t*>(Dk + gr1 * 64 + col) = pack_half2(acc[nt][2], acc[nt][3]);
             }
+            __syncwarp();                     // masks read before the deltas overwrite the tile
+#pragma unroll
+            for (int nt = 0; nt < 8; ++nt) {
+                const int col = nt * 8 + 2 * t;
+                *reinterpret_cast<uint32_t*>(ts + g * 72 + col) = pack_half2(acc[nt][0], acc[nt][1]);
+                *reinterpret_cast<uint32_t*>(ts + (g + 8) * 72 + col) = pack_half2(acc[nt][2], acc[nt][3]);
+            }
+            __syncwarp();
+#pragma unroll
+            for (int c = lane; c < 16 * 8; c += 32) {
+                const int row = c >> 3, c8 = c & 7;
+                if (row < nv)
+                    *reinterpret_cast<uint4*>(Dk + (r0 + row) * 64 + c8 * 8) = *reinterpret_cast<const uint4*>(ts + row * 72 + c8 * 8);
+            }
+            __syncwarp();                     // tile free for the next layer
 #pragma unroll
             for (int kb = 0; kb < 4; ++kb) {
                 af[kb][0] = pack_half2(acc[2 * kb][0], acc[2 * kb][1]);
@@ -596,10 +637,19 @@ __global__ void __launch_bounds__(256, 2) k_train_bwd(TrainArgs a) {
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
                 const int c = (2 * np + j) * 8 + 2 * t;
-                if (v0) *reinterpret_cast<float2*>(a.gx + gr0 * D + c) = make_float2(acc[j][0], acc[j][1]);
-                if (v1) *reinterpret_cast<float2*>(a.gx + gr1 * D + c) = make_float2(acc[j][2], acc[j][3]);
+                *reinterpret_cast<float2*>(gxs + g * (D + 4) + c) = make_float2(acc[j][0], acc[j][1]);
+                *reinterpret_cast<float2*>(gxs + (g + 8) * (D + 4) + c) = make_float2(acc[j][2], acc[j][3]);
             }
         }
+        __syncwarp();
+        // dL/dx rows out, 16 bytes per lane, row-contiguous
+        for (int c = lane; c < 16 * (D / 4); c += 32) {
+            const int row = c / (D / 4), c4 = c - row * (D / 4);
+            if (row < nv)
+                *reinterpret_cast<float4*>(a.gx + ((int64_t)blk * 16 + row) * D + c4 * 4) =
+                    *reinterpret_cast<const float4*>(gxs + row * (D + 4) + c4 * 4);
+        }
+        __syncwarp();
     }
 }
 

@@ -608,7 +608,7 @@ struct QuerySmemPlan {
 // the warp-specialised kernel below).
 template <int F, int D, bool kBf>
 __global__ void __launch_bounds__(kQueryWarps * 32, 1) k_query_warp(QueryArgs a) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int NP = a.g.n_points;
     const QuerySmemPlan plan(D, a.m.hidden, NP);
@@ -1019,7 +1019,7 @@ __global__ void __launch_bounds__(128) k_debug_encode(DebugEncodeArgs a) {
 // ------------------------------------------------------------------ debug: MLP rows
 template <int D, bool kBf>
 __global__ void __launch_bounds__(256, 2) k_debug_mlp(DebugMlpArgs a) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     MlpSmem ms;
     __half* feat = reinterpret_cast<__half*>(smem_raw);

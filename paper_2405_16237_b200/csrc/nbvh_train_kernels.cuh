@@ -867,6 +867,7 @@ __global__ void __launch_bounds__(256) k_train_scatter_agg(TrainArgs a) {
                 }
                 __syncwarp();
                 if (cnt > 1) {
+                    NBVH_DCHECK(leader >= 0 && leader < 32 && rank < cnt);
                     emit = valid && lane == leader;
                     if (emit) {
 #pragma unroll
@@ -901,6 +902,7 @@ __global__ void __launch_bounds__(256) k_train_scatter_agg(TrainArgs a) {
                         }
                     }
             } else if (P.n1) {
+                NBVH_DCHECK(i0 < P.nx && i1 < P.nx && i2 < P.nx);
                 float* dst = a.sc_dense + a.sc_off[l] + (int64_t)(i0 + P.nx * i1 + P.nxy * i2) * 8 * F;
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
@@ -916,6 +918,7 @@ __global__ void __launch_bounds__(256) k_train_scatter_agg(TrainArgs a) {
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     const uint32_t e0 = cell.idx[2 * j], e1 = cell.idx[2 * j + 1];
+                    NBVH_DCHECK(e0 <= hmask && e1 <= hmask);
                     if (F == 2 && (e0 ^ e1) == 1u) {
                         const bool lo0 = e0 < e1;
                         const float a0 = u[2 * j][0], a1 = u[2 * j][F - 1], b0 = u[2 * j + 1][0], b1 = u[2 * j + 1][F - 1];

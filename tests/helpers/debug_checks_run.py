@@ -29,6 +29,15 @@ ctx.set_leaf_rank(np.zeros(ctx.cut(0)["n_leaves"], np.float32))
 for step in range(3):
     r, u, xi = ctx.gen_train_rays(seed=5, step=step, n=8192, box=(-1.5, -1.5, -1.5, 1.5, 1.5, 1.5))
     ctx.train_step(r, u, xi)
+# the other T7 kernel (privatised fixed-point levels) and the warp-specialised query kernel
+os.environ["NBVH_SCATTER_AGG"] = "0"
+ctx.train_step(*ctx.gen_train_rays(seed=5, step=3, n=8192, box=(-1.5, -1.5, -1.5, 1.5, 1.5, 1.5)))
+del os.environ["NBVH_SCATTER_AGG"]
+os.environ["NBVH_QUERY_MLP"] = "tc"
+dw = ctx.query(torch.from_numpy(rays).cuda())
+del os.environ["NBVH_QUERY_MLP"]
+torch.cuda.synchronize()
+assert dw["hit"].numel() == rays.shape[0]
 # classical closest-hit traversal (bvh_closest: farther-child stack sized by the BVH depth)
 mh = ctx.intersect_mesh(torch.from_numpy(rays).cuda())
 x = (torch.rand(1000, ctx.d_in, device="cuda") - 0.5).half()

@@ -335,18 +335,19 @@ static cudaError_t launch_train_fd(const TrainArgs& a0, const TrainArgs& a, int3
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_sc);
     if (e != cudaSuccess) return e;
     const unsigned blocks_n = (unsigned)((n + 127) / 128);
-    if (ev) cudaEventRecord(ev[0], s);
     // every launch is checked at once: a failed launch must not leave a step that silently
     // skipped a phase
-    k_train_select<<<blocks_n, 128, (size_t)(a.cut.depth + 2) * 128 * sizeof(int), s>>>(a0);
+    if ((e = cudaMemsetAsync(hist, 0, sizeof(int32_t) * (size_t)a.cut.n_leaves, s)) != cudaSuccess) return e;
+    if (ev) cudaEventRecord(ev[0], s);
+    TrainArgs asel = a0;
+    asel.leaf_hist = hist;                    // T1 counts the accepted samples per leaf
+    k_train_select<<<blocks_n, 128, (size_t)(a.cut.depth + 2) * 128 * sizeof(int), s>>>(asel);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     // group the samples by leaf (the later kernels read a's sorted arrays)
-    if ((e = cudaMemsetAsync(hist, 0, sizeof(int32_t) * (size_t)a.cut.n_leaves, s)) != cudaSuccess) return e;
-    k_sort_count<<<2 * sms, 256, 0, s>>>(a0, hist);
     k_sort_scan<<<1, 1024, 0, s>>>(hist, a.cut.n_leaves);
     k_sort_place<<<2 * sms, 256, 0, s>>>(a0, hist, SortedSamples{a.s_ray, a.s_leaf, a.s_t0, a.s_t1});
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    *launches += 3;
+    *launches += 2;
     if (ev) cudaEventRecord(ev[1], s);
     k_train_label<<<blocks_n, 128, (size_t)a.bvh_rows * 128 * sizeof(int), s>>>(a);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;

@@ -68,6 +68,7 @@ struct TrainArgs {
     int64_t sc_dense_n, sc_hash_n;   // scratch sizes (floats)
     int32_t scatter_ctas;
     int32_t agg_levels;      // k_train_scatter_agg: levels 0..agg_levels-1 warp-aggregated (0: k_train_scatter)
+    int32_t* leaf_hist;      // k_train_select: accepted samples per leaf (nullable; the sort's counts)
     int32_t use_tc_dw;       // weight GEMMs on tcgen05 (k_train_dw_tc) when the shape allows
 };
 
@@ -95,6 +96,7 @@ __global__ void __launch_bounds__(128) k_train_select(TrainArgs a) {
             const float rh = __fadd_rn(__fsub_rn(a.rank[leaf], a.rank_min), 1e-6f);
             const float p = fmaxf(__fdiv_rn(rh, a.rank_hmax), 0.005f);
             acc = a.u[r] < p;
+            if (acc && a.leaf_hist) atomicAdd(a.leaf_hist + leaf, 1);
         }
         a.r_acc[r] = acc ? 1 : 0;
         a.r_leaf[r] = leaf;
@@ -208,15 +210,12 @@ namespace nbvh {
 
 // ------------------------------------------------------------------ samples grouped by leaf
 // A counting sort of the accepted samples by leaf (a permutation of the batch: every sum over
-// samples is unchanged).  A leaf's samples are spatially close, so the warps of the label,
-// forward and backward kernels read coherent lines -- random training rays otherwise touch
-// ~3x the L1 sectors per encoded point of a coherent query.  The T7 scatter walks the samples
-// in a scrambled order instead: coherent samples would collide in the L2 reductions.
-__global__ void k_sort_count(TrainArgs a, int32_t* hist) {
-    const int M = *a.n_samples;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < M; i += (int64_t)gridDim.x * blockDim.x)
-        atomicAdd(hist + a.s_leaf[i], 1);
-}
+// samples is unchanged): k_train_select counts them per leaf (TrainArgs::leaf_hist), a scan
+// turns the counts into offsets, k_sort_place scatters.  A leaf's samples are spatially close,
+// so the warps of the label, forward and backward kernels read coherent lines -- random
+// training rays otherwise touch ~3x the L1 sectors per encoded point of a coherent query --
+// and the default T7 scatter groups a warp's items by grid cell (k_train_scatter_agg);
+// k_train_scatter (NBVH_SCATTER_AGG=0) walks them in a scrambled order instead.
 
 // in-place exclusive scan of hist[n] by one CTA of 1024 threads (chunks of 1024 with a carry)
 __global__ void __launch_bounds__(1024) k_sort_scan(int32_t* hist, int n) {

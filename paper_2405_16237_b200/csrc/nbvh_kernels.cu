@@ -469,12 +469,31 @@ __device__ __forceinline__ int slots_segment(const QueryArgs& a, WarpSlots& S, f
 // (D) hash-grid encode of the nv rows: lane -> row q = lane % 16; the two half-warps take
 // sample points of opposite parity at the same levels (neighbouring points of the same rays:
 // coherent lines).  Chunk c (8 halves) of row q is stored at dst + c * cstride + q * rstride.
-template <int F, bool kBf = false>
+template <int F, bool kBf = false, bool kSpread = false>
 __device__ __forceinline__ void rows_encode(const QueryArgs& a, const LevelSm* lv, const float* xs, int nv, int lane,
                                             int NP, unsigned char* dst, int cstride, int rstride) {
-    const int q = lane & (kWarpQ - 1), h = lane / kWarpQ;
     const int cpp = (a.g.L * F) / 8;      // 16-byte chunks per sample point
     const uint32_t hmask = (1u << a.g.log2_T) - 1u;
+    if (kSpread && nv <= kWarpQ / 2) {
+        // few rows (a launch's tail, where a warp's iteration time is the latency of its
+        // sequential chunk rounds): spread each row's NP * cpp chunks over 32 / rp lanes
+        // (rp = rows rounded up to a power of two), so the rounds per lane shrink with the row
+        // count.  Every chunk is computed exactly as below, only by another lane.
+        const int rp = nv > 4 ? 8 : (nv > 2 ? 4 : (nv > 1 ? 2 : 1));
+        const int lpr = 32 / rp, q = lane & (rp - 1), h = lane / rp;
+        if (q < nv) {
+            for (int j = h; j < NP * cpp; j += lpr) {
+                const int p = j / cpp, lc = j - p * cpp;
+                const float* xp = xs + p * 3 * kWarpQ;
+                const uint4 f = encode_chunk_sm<F, true, kBf>(lv, a.g.table, hmask, xp[q], xp[kWarpQ + q],
+                                                              xp[2 * kWarpQ + q], lc * (8 / F), nullptr);
+                *reinterpret_cast<uint4*>(dst + j * cstride + q * rstride) = f;
+            }
+        }
+        __syncwarp();
+        return;
+    }
+    const int q = lane & (kWarpQ - 1), h = lane / kWarpQ;
     if (q < nv) {
         for (int p = h; p < NP; p += 2) {
             const float* xp = xs + p * 3 * kWarpQ;
@@ -647,7 +666,7 @@ __global__ void __launch_bounds__(kQueryWarps * 32, 1) k_query_warp(QueryArgs a)
             s_stat[2 * warp] += nv;
             s_stat[2 * warp + 1] += 1;
         }
-        rows_encode<F, kBf>(a, lv, xs, nv, lane, NP, reinterpret_cast<unsigned char*>(feat), 16, (D + 8) * 2);
+        rows_encode<F, kBf, true>(a, lv, xs, nv, lane, NP, reinterpret_cast<unsigned char*>(feat), 16, (D + 8) * 2);
         query_mlp_rows16<D, kBf>(ms, a.m.hidden, feat, 0, zt, lane);         // (E)
         __syncwarp();
         rows_decode(a, S, zt, nv, lane);

@@ -366,7 +366,8 @@ constexpr int kQueryWarps = 16;     // warps per CTA (one CTA per SM; bounded by
 
 struct WarpSlots {
     int32_t ray[kWarpQ], pos[kWarpQ], base[kWarpQ], nbuf[kWarpQ], more[kWarpQ], bleaf[kWarpQ], nq[kWarpQ],
-        leaf[kWarpQ], act[kWarpQ], fresh[kWarpQ];   // fresh: entry 0 (from the work record) in the slot
+        leaf[kWarpQ], act[kWarpQ], fresh[kWarpQ];   // fresh: the current entry is in the slot (entry 0
+                                                    // from the work record, later ones from the decode)
     float o[3][kWarpQ], d[3][kWarpQ];
     float bt[kWarpQ], bte[kWarpQ], te[kWarpQ], tx[kWarpQ];
     float nrm[3][kWarpQ], alb[3][kWarpQ];
@@ -440,7 +441,7 @@ __device__ __forceinline__ int slots_segment(const QueryArgs& a, WarpSlots& S, f
                     S.nbuf[lane] <= kListK);
         const int64_t li = (int64_t)(S.pos[lane] - S.base[lane]) * a.n_rays + r;
         float te, tx;
-        if (S.fresh[lane]) {              // a new ray: entry 0 came with its work record
+        if (S.fresh[lane]) {              // the entry is already in the slot (work record / decode)
             S.fresh[lane] = 0;
             te = S.te[lane];
             tx = S.tx[lane];
@@ -570,8 +571,14 @@ __device__ __forceinline__ void rows_decode(const QueryArgs& a, WarpSlots& S, co
                 }
             }
             if (!done) {
-                const float next_te = __ldcs(a.lst + (int64_t)(pos - base) * a.n_rays + r).x;
-                done = bleaf >= 0 && next_te > bt;                     // front-to-back termination
+                const float4 e = __ldcs(a.lst + (int64_t)(pos - base) * a.n_rays + r);
+                done = bleaf >= 0 && e.x > bt;                         // front-to-back termination
+                if (!done) {            // the next entry stays in the slot: no reload in (C)
+                    S.te[s] = e.x;
+                    S.tx[s] = e.y;
+                    S.leaf[s] = __float_as_int(e.z);
+                    S.fresh[s] = 1;
+                }
             }
         }
         S.pos[s] = pos;

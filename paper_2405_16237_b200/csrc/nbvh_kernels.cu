@@ -371,6 +371,7 @@ struct WarpSlots {
     float o[3][kWarpQ], d[3][kWarpQ];
     float bt[kWarpQ], bte[kWarpQ], te[kWarpQ], tx[kWarpQ];
     float nrm[3][kWarpQ], alb[3][kWarpQ];
+    float4 nxt[kWarpQ];      // the next list entry, prefetched (cp.async) while the row is encoded
 };
 
 __host__ __device__ constexpr size_t align16(size_t b) { return (b + 15) & ~(size_t)15; }
@@ -453,6 +454,12 @@ __device__ __forceinline__ int slots_segment(const QueryArgs& a, WarpSlots& S, f
             S.te[lane] = te;
             S.tx[lane] = tx;
         }
+        // the entry after this one, for the decode's termination test: fetched into the slot
+        // asynchronously (no registers held across the encode and the MLP)
+        if (S.pos[lane] + 1 - S.base[lane] < S.nbuf[lane])
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(&S.nxt[lane])),
+                         "l"(a.lst + (int64_t)(S.pos[lane] + 1 - S.base[lane]) * a.n_rays + r)
+                         : "memory");
         const float o[3] = {S.o[0][lane], S.o[1][lane], S.o[2][lane]};
         const float d[3] = {S.d[0][lane], S.d[1][lane], S.d[2][lane]};
         for (int p = 0; p < NP; ++p) {
@@ -463,6 +470,7 @@ __device__ __forceinline__ int slots_segment(const QueryArgs& a, WarpSlots& S, f
             xs[(p * 3 + 2) * kWarpQ + row] = x[2];
         }
     }
+    asm volatile("cp.async.commit_group;" ::: "memory");
     __syncwarp();
     return nv;
 }
@@ -513,6 +521,8 @@ __device__ __forceinline__ void rows_encode(const QueryArgs& a, const LevelSm* l
 // best hit, decide front-to-back termination (C5, C6) and write the finished
 // rays' hit records (Q7).  Returns the number of queries decoded.
 __device__ __forceinline__ void rows_decode(const QueryArgs& a, WarpSlots& S, const float* zt, int nv, int lane) {
+    asm volatile("cp.async.wait_group 0;" ::: "memory");   // this lane's prefetched next entries
+    __syncwarp();
     if (lane < nv) {
         const int s = S.act[lane];
         const int r = S.ray[s];
@@ -554,6 +564,7 @@ __device__ __forceinline__ void rows_decode(const QueryArgs& a, WarpSlots& S, co
         bool done = a.mode == 1 && hit;                                 // R1: first confident hit (C5)
         if (!done) {
             int base = S.base[s], nbuf = S.nbuf[s];
+            bool refilled = false;
             if (pos - base >= nbuf) {
                 if (!S.more[s]) {
                     done = true;                                         // every intersected leaf visited
@@ -568,10 +579,12 @@ __device__ __forceinline__ void rows_decode(const QueryArgs& a, WarpSlots& S, co
                     S.nbuf[s] = nbuf;
                     S.more[s] = more;
                     done = nbuf == 0;
+                    refilled = true;
                 }
             }
             if (!done) {
-                const float4 e = __ldcs(a.lst + (int64_t)(pos - base) * a.n_rays + r);
+                // the entry prefetched by (C), or after a refill the new list's first one
+                const float4 e = refilled ? __ldcs(a.lst + (int64_t)(pos - base) * a.n_rays + r) : S.nxt[s];
                 done = bleaf >= 0 && e.x > bt;                         // front-to-back termination
                 if (!done) {            // the next entry stays in the slot: no reload in (C)
                     S.te[s] = e.x;

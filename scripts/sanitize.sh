@@ -1,5 +1,7 @@
 #!/bin/bash
-# compute-sanitizer memcheck (one tool per call) over a few small GPU tests.
+# compute-sanitizer memcheck (one tool per call) over a few small GPU tests.  (The GPU pool
+# refuses compute-sanitizer runs; tests/test_gpu_debug_checks.py runs the device-side bounds
+# checks of the debug build instead.)
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1

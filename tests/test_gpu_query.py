@@ -484,6 +484,31 @@ def test_query_ws_drain_and_partial_tiles(orc, monkeypatch):
         assert ctx.query_stats()["n_mlp_rows"] == int(g["n_queries"].sum())
 
 
+def test_query_small_batches_tail_rows(orc):
+    """The default kernel with fewer rays than a warp's slots from the start: every iteration
+    runs with <= 8 occupied rows, where each row's chunks are spread over 4-32 lanes (the
+    tail encode path), and rays whose lists need refills.  Ray counts 1, 2, 3, 5, 9, 17, 33;
+    every hit record and query count equals the replay of the kernel's own z trace, and the
+    decided rays agree with the double oracle."""
+    ctx, sc, tab, layers = _mk_ctx("tiny", list_cap=2)
+    base = _rays_tiny(2000)
+    cut = ctx.cut(0)
+    _, _, _, cnt = orc.leaf_lists(base, cut["leaf_lo"], cut["leaf_hi"], 1)
+    live = base[cnt >= 2][:200]                      # rays with >= 2 leaves (refills at K = 2)
+    assert live.shape[0] >= 33
+    for n in (1, 2, 3, 5, 9, 17, 33):
+        rays = np.ascontiguousarray(live[:n])
+        out, zt = ctx.debug_query_trace(torch.from_numpy(rays).cuda(), 32)
+        torch.cuda.synchronize()
+        g = {k: v.cpu().numpy() for k, v in out.items()}
+        rep = orc.replay(cut["leaf_lo"], cut["leaf_hi"], rays, zt.cpu().numpy())
+        assert rep["missing"] == 0
+        assert np.array_equal(g["hit"], rep["hit"]) and np.array_equal(g["leaf"], rep["leaf"])
+        assert np.array_equal(g["n_queries"], rep["nq"])
+        assert np.array_equal(g["t"].view(np.uint32), rep["t"].view(np.uint32))
+    _check_query(orc, ctx, tab, layers, np.ascontiguousarray(live[:33]), band_max=0.1)
+
+
 def test_query_host_path_first_hit_mode_and_lod(monkeypatch):
     """The host path with R1 (first confident hit, C5) and with a non-zero LoD slot returns
     exactly the device path's records."""

@@ -517,6 +517,10 @@ extern "C" nbvh_status nbvh_train_backward(nbvh_ctx* c, const nbvh_ray* rays, in
         // overrides, 0 selects k_train_scatter with the privatised levels)
         const char* ev = std::getenv("NBVH_SCATTER_AGG");
         a.agg_levels = std::max(0, std::min(ev ? std::atoi(ev) : kScatterAggLevels, (int)c->cfg.L));
+        // the grouping key is the cell's linear index N^3 < 2^31 (bit 31 marks idle lanes)
+        while (a.agg_levels > 0 &&
+               (int64_t)c->res[a.agg_levels - 1] * c->res[a.agg_levels - 1] * c->res[a.agg_levels - 1] >= (1ll << 31))
+            --a.agg_levels;
     }
     // shared-memory privatisation: only without aggregation by default (NBVH_PRIV_BYTES
     // overrides; 0 disables)

@@ -70,6 +70,7 @@ GridDev make_grid(const nbvh_ctx* c, int lod) {
         g.inf_offset[l] = (uint32_t)c->inf_offset[l];
     }
     g.table = c->d_table16;
+    g.tex = c->tex_table;
     if (lod >= 0) {
         const HostCut& hc = c->cuts[lod];
         for (int k = 0; k < 3; ++k) g.dom_min[k] = hc.dom_min[k];
@@ -285,6 +286,23 @@ extern "C" nbvh_status nbvh_create(const nbvh_config* cfg, int cuda_device, nbvh
         cudaError_t e = cudaSetDevice(cuda_device);
         if (e == cudaSuccess) e = dalloc(&x->d_params, x->h_params.size());
         if (e == cudaSuccess) e = dalloc(&x->d_table16, x->n_inf * c.F);
+        if (e == cudaSuccess) {
+            // a linear texture over the fp16 inference table: one texel = one entry (F halves),
+            // element reads through the TEX pipe (the query kernel's hashed-level gathers)
+            cudaResourceDesc rd{};
+            rd.resType = cudaResourceTypeLinear;
+            rd.res.linear.devPtr = x->d_table16;
+            rd.res.linear.desc = c.F == 2 ? cudaCreateChannelDesc<unsigned int>() : cudaCreateChannelDesc<uint2>();
+            rd.res.linear.sizeInBytes = (size_t)x->n_inf * c.F * 2;
+            cudaTextureDesc td{};
+            td.readMode = cudaReadModeElementType;
+            td.filterMode = cudaFilterModePoint;
+            td.addressMode[0] = cudaAddressModeClamp;
+            td.normalizedCoords = 0;
+            cudaTextureObject_t t = 0;
+            if (cudaCreateTextureObject(&t, &rd, &td, nullptr) == cudaSuccess) x->tex_table = t;
+            else { cudaGetLastError(); x->tex_table = 0; }
+        }
         if (e == cudaSuccess) e = dalloc(&x->d_W16, x->n_W);
         if (e == cudaSuccess && c.mlp_dtype == 1) e = cudaMalloc((void**)&x->d_Wb16, (size_t)x->n_W * 2);
         if (e == cudaSuccess) e = dalloc(&x->d_misc, kCounterBlocks * kCounterStride);
@@ -334,6 +352,8 @@ extern "C" void nbvh_destroy(nbvh_ctx* c) {
             dfree(c->dcut[l].rank);
         }
         dfree(c->d_params);
+        if (c->tex_table) cudaDestroyTextureObject((cudaTextureObject_t)c->tex_table);
+        c->tex_table = 0;
         dfree(c->d_table16);
         dfree(c->d_W16);
         if (c->d_Wb16) cudaFree(c->d_Wb16);
@@ -642,6 +662,10 @@ nbvh_status run_query(nbvh_ctx* c, const nbvh_ray* rays, int64_t n, int32_t lod,
     if (c->profiling) cudaEventRecord(ctx_event(c, 1), s);
     QueryArgs qa{};
     qa.g = make_grid(c, lod);
+    {
+        const char* ev = std::getenv("NBVH_QUERY_TEX");       // A/B hook: 0 = hashed gathers on LDG
+        if (ev && ev[0] == '0') qa.g.tex = 0;
+    }
     qa.m = make_mlp(c);
     if (c->d_Wb16) {                      // bf16 query path (mlp_dtype = 1, C39)
         qa.m.W = reinterpret_cast<const __half*>(c->d_Wb16);

@@ -55,6 +55,7 @@ struct nbvh_ctx {
     std::vector<float> h_params;
     float* d_params = nullptr;
     __half* d_table16 = nullptr;
+    unsigned long long tex_table = 0;  // texture object over d_table16 (TEX-pipe gathers, see LevelSm::pad)
     __half* d_W16 = nullptr;
     __nv_bfloat16* d_Wb16 = nullptr;   // bf16 copy of the MLP weights (mlp_dtype = 1: query path)
 

@@ -45,6 +45,7 @@ struct GridDev {
     const __half* table;             // fp16 inference table (layout: see LevelSm)
     float dom_min[3];
     float dom_inv;
+    unsigned long long tex;          // texture object over `table` (0: none -> LDG gathers)
 };
 
 struct MlpDev {
@@ -513,9 +514,10 @@ struct ChunkGather {
 // Step 1 of encode_chunk_sm: cell, corner indices and all 8*NL gathers issued (the index
 // registers die as soon as the loads are issued; only the fractions are kept).  Splitting
 // issue from finish lets the caller keep two chunks' gathers in flight.
-template <int F>
+template <int F, bool kTex = false>
 __device__ __forceinline__ void encode_issue(const LevelSm* lv, const void* tab, uint32_t hmask, float x0, float x1,
-                                             float x2, int l0, uint32_t* idx_out, ChunkGather<F>& G) {
+                                             float x2, int l0, uint32_t* idx_out, ChunkGather<F>& G,
+                                             unsigned long long tex = 0) {
     constexpr int NL = 8 / F;
     static_assert(F == 2 || F == 4, "F must be 2 or 4");
     using Entry = typename ChunkGather<F>::Entry;
@@ -570,9 +572,19 @@ __device__ __forceinline__ void encode_issue(const LevelSm* lv, const void* tab,
             const uint32_t hy[2] = {(i1 * kPrime1) & hmask, ((i1 + 1u) * kPrime1) & hmask};
             const uint32_t hz[2] = {(i2 * kPrime2) & hmask, ((i2 + 1u) * kPrime2) & hmask};
             // 32-bit entry index (n_entries < 2^32), one IMAD.WIDE.U32 per gather address
+            if constexpr (kTex && F == 2) {
+                // through the TEX pipe (a texture object over the same fp16 table, element
+                // reads): the query kernel's limit is the LSU data pipe, which the TEX pipe
+                // does not share -- the dense levels' 32-byte records stay on LDG.256
 #pragma unroll
-            for (int k = 0; k < 8; ++k)
-                G.v[j][k] = ldg_el(Tl + (hx[k & 1] ^ hy[(k >> 1) & 1] ^ hz[(k >> 2) & 1]));
+                for (int k = 0; k < 8; ++k)
+                    G.v[j][k] = tex1Dfetch<unsigned int>(
+                        (cudaTextureObject_t)tex, (int)(P.off + (hx[k & 1] ^ hy[(k >> 1) & 1] ^ hz[(k >> 2) & 1])));
+            } else {
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    G.v[j][k] = ldg_el(Tl + (hx[k & 1] ^ hy[(k >> 1) & 1] ^ hz[(k >> 2) & 1]));
+            }
         }
     }
 }
@@ -657,11 +669,12 @@ __device__ __forceinline__ uint4 encode_finish(const ChunkGather<F>& G) {
 // entries (dense: corner-packed cell record; hashed: 8 gathers, C2, C3), trilinear weights
 // (wx*wy)*wz, blend in fp32.  idx_out (nullable) receives the 8*NL
 // canonical corner indices within their levels (parity hook).
-template <int F, bool kHalfW = true, bool kBf = false>
+template <int F, bool kHalfW = true, bool kBf = false, bool kTex = false>
 __device__ __forceinline__ uint4 encode_chunk_sm(const LevelSm* lv, const void* tab, uint32_t hmask, float x0,
-                                                 float x1, float x2, int l0, uint32_t* idx_out) {
+                                                 float x1, float x2, int l0, uint32_t* idx_out,
+                                                 unsigned long long tex = 0) {
     ChunkGather<F> G;
-    encode_issue<F>(lv, tab, hmask, x0, x1, x2, l0, idx_out, G);
+    encode_issue<F, kTex>(lv, tab, hmask, x0, x1, x2, l0, idx_out, G, tex);
     return encode_finish<F, kHalfW, kBf>(G);
 }
 

@@ -478,7 +478,7 @@ __device__ __forceinline__ int slots_segment(const QueryArgs& a, WarpSlots& S, f
 // (D) hash-grid encode of the nv rows: lane -> row q = lane % 16; the two half-warps take
 // sample points of opposite parity at the same levels (neighbouring points of the same rays:
 // coherent lines).  Chunk c (8 halves) of row q is stored at dst + c * cstride + q * rstride.
-template <int F, bool kBf = false, bool kSpread = false>
+template <int F, bool kBf = false, bool kSpread = false, bool kTex = false>
 __device__ __forceinline__ void rows_encode(const QueryArgs& a, const LevelSm* lv, const float* xs, int nv, int lane,
                                             int NP, unsigned char* dst, int cstride, int rstride) {
     const int cpp = (a.g.L * F) / 8;      // 16-byte chunks per sample point
@@ -494,8 +494,8 @@ __device__ __forceinline__ void rows_encode(const QueryArgs& a, const LevelSm* l
             for (int j = h; j < NP * cpp; j += lpr) {
                 const int p = j / cpp, lc = j - p * cpp;
                 const float* xp = xs + p * 3 * kWarpQ;
-                const uint4 f = encode_chunk_sm<F, true, kBf>(lv, a.g.table, hmask, xp[q], xp[kWarpQ + q],
-                                                              xp[2 * kWarpQ + q], lc * (8 / F), nullptr);
+                const uint4 f = encode_chunk_sm<F, true, kBf, kTex>(lv, a.g.table, hmask, xp[q], xp[kWarpQ + q],
+                                                                    xp[2 * kWarpQ + q], lc * (8 / F), nullptr, a.g.tex);
                 *reinterpret_cast<uint4*>(dst + j * cstride + q * rstride) = f;
             }
         }
@@ -509,7 +509,8 @@ __device__ __forceinline__ void rows_encode(const QueryArgs& a, const LevelSm* l
             const float x0 = xp[q], x1 = xp[kWarpQ + q], x2 = xp[2 * kWarpQ + q];
             for (int lc = 0; lc < cpp; ++lc) {
                 const int c = p * cpp + lc;
-                const uint4 f = encode_chunk_sm<F, true, kBf>(lv, a.g.table, hmask, x0, x1, x2, lc * (8 / F), nullptr);
+                const uint4 f = encode_chunk_sm<F, true, kBf, kTex>(lv, a.g.table, hmask, x0, x1, x2, lc * (8 / F),
+                                                                    nullptr, a.g.tex);
                 *reinterpret_cast<uint4*>(dst + c * cstride + q * rstride) = f;
             }
         }
@@ -645,7 +646,7 @@ struct QuerySmemPlan {
 // activations in registers), (F) decode.  Warps drift freely, so one warp's MLP or list
 // refill overlaps other warps' gathers.  Selected with NBVH_QUERY_MLP=warp (A/B reference of
 // the warp-specialised kernel below).
-template <int F, int D, bool kBf>
+template <int F, int D, bool kBf, bool kTex = false>
 __global__ void __launch_bounds__(kQueryWarps * 32, 1) k_query_warp(QueryArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -686,7 +687,7 @@ __global__ void __launch_bounds__(kQueryWarps * 32, 1) k_query_warp(QueryArgs a)
             s_stat[2 * warp] += nv;
             s_stat[2 * warp + 1] += 1;
         }
-        rows_encode<F, kBf, true>(a, lv, xs, nv, lane, NP, reinterpret_cast<unsigned char*>(feat), 16, (D + 8) * 2);
+        rows_encode<F, kBf, true, kTex>(a, lv, xs, nv, lane, NP, reinterpret_cast<unsigned char*>(feat), 16, (D + 8) * 2);
         query_mlp_rows16<D, kBf>(ms, a.m.hidden, feat, 0, zt, lane);         // (E)
         __syncwarp();
         rows_decode(a, S, zt, nv, lane);
@@ -1157,11 +1158,17 @@ static cudaError_t launch_query_t(const QueryArgs& a, int64_t max_work, cudaStre
     if (plan.warps < 1) return cudaErrorInvalidValue;
     plan.warps = query_warps_cap(plan.warps);
     plan.total = plan.warp0 + plan.per_warp * plan.warps;
+    // hashed-level gathers through the TEX pipe when the context has its texture object (F = 2)
+    const bool tex = a.g.tex != 0 && F == 2;
     if (a.m.bf16)
-        return launch_persistent<2>(k_query_warp<F, D, true>, plan.warps * 32, plan.total, max_work,
-                                    plan.warps * kWarpQ, a, s, a.m.hidden, a.g.n_points);
-    return launch_persistent<1>(k_query_warp<F, D, false>, plan.warps * 32, plan.total, max_work, plan.warps * kWarpQ,
-                                a, s, a.m.hidden, a.g.n_points);
+        return tex ? launch_persistent<5>(k_query_warp<F, D, true, true>, plan.warps * 32, plan.total, max_work,
+                                          plan.warps * kWarpQ, a, s, a.m.hidden, a.g.n_points)
+                   : launch_persistent<2>(k_query_warp<F, D, true>, plan.warps * 32, plan.total, max_work,
+                                          plan.warps * kWarpQ, a, s, a.m.hidden, a.g.n_points);
+    return tex ? launch_persistent<6>(k_query_warp<F, D, false, true>, plan.warps * 32, plan.total, max_work,
+                                      plan.warps * kWarpQ, a, s, a.m.hidden, a.g.n_points)
+               : launch_persistent<1>(k_query_warp<F, D, false>, plan.warps * 32, plan.total, max_work,
+                                      plan.warps * kWarpQ, a, s, a.m.hidden, a.g.n_points);
 }
 
 cudaError_t launch_query(const QueryArgs& a, int64_t max_work, cudaStream_t s) {

@@ -325,7 +325,10 @@ static cudaError_t launch_train_fd(const TrainArgs& a0, const TrainArgs& a, int3
     const size_t smem_bwd = bwd_smem(D, H);
     const size_t smem_sc = scatter_smem(a);
     const size_t smem_dw = (size_t)kTileQ * 72 * 2 + (size_t)kTileQ * (D + 8) * 2 + kTileQ * 8 * 4;
-    cudaError_t e = cudaFuncSetAttribute(k_train_fwd<F, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fwd);
+    // T3 gathers of the hashed levels through the TEX pipe when the texture object exists (F = 2)
+    const bool tex = a.g.tex != 0 && F == 2 && !(std::getenv("NBVH_TRAIN_TEX") && std::getenv("NBVH_TRAIN_TEX")[0] == '0');
+    auto fwd = tex ? k_train_fwd<F, D, true> : k_train_fwd<F, D, false>;
+    cudaError_t e = cudaFuncSetAttribute(fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_fwd);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_train_bwd<F, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bwd);
     if (e == cudaSuccess)
@@ -353,7 +356,7 @@ static cudaError_t launch_train_fd(const TrainArgs& a0, const TrainArgs& a, int3
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (ev) cudaEventRecord(ev[2], s);
     const int grid_fwd = sms;                 // persistent: one CTA of kFwdWarps warps per SM
-    k_train_fwd<F, D><<<grid_fwd, kFwdWarps * 32, smem_fwd, s>>>(a);
+    fwd<<<grid_fwd, kFwdWarps * 32, smem_fwd, s>>>(a);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (ev) cudaEventRecord(ev[3], s);
     k_train_bwd<F, D><<<2 * sms, 256, smem_bwd, s>>>(a);

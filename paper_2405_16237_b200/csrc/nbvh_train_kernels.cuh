@@ -313,7 +313,7 @@ struct FwdSmemPlan {
     }
 };
 
-template <int F, int D>
+template <int F, int D, bool kTex = false>
 __global__ void __launch_bounds__(kFwdWarps * 32, 1) k_train_fwd(TrainArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -364,7 +364,8 @@ __global__ void __launch_bounds__(kFwdWarps * 32, 1) k_train_fwd(TrainArgs a) {
                                 x2 = xs[(p * 3 + 2) * 16 + r];
                     for (int lc = 0; lc < cpp; ++lc)
                         *reinterpret_cast<uint4*>(feat + r * (D + 8) + (p * cpp + lc) * 8) =
-                            encode_chunk_sm<F, false>(lv, a.g.table, hmask, x0, x1, x2, lc * (8 / F), nullptr);
+                            encode_chunk_sm<F, false, false, kTex>(lv, a.g.table, hmask, x0, x1, x2, lc * (8 / F),
+                                                                   nullptr, a.g.tex);
                 }
             }
         }

@@ -458,7 +458,7 @@ __device__ __forceinline__ int slots_segment(const QueryArgs& a, WarpSlots& S, f
         // asynchronously (no registers held across the encode and the MLP)
         if (S.pos[lane] + 1 - S.base[lane] < S.nbuf[lane])
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(&S.nxt[lane])),
-                         "l"(a.lst + (int64_t)(S.pos[lane] + 1 - S.base[lane]) * a.n_rays + r)
+                         "l"(a.lst + li + a.n_rays)
                          : "memory");
         const float o[3] = {S.o[0][lane], S.o[1][lane], S.o[2][lane]};
         const float d[3] = {S.d[0][lane], S.d[1][lane], S.d[2][lane]};
@@ -892,7 +892,7 @@ __global__ void __launch_bounds__((kWsWorkers + 4) * 32, 1) k_query_ws(QueryArgs
                 t_free += clock64() - t0;
             }
             // (D) encode straight into the tile: row blk*16 + q, K-major canonical layout
-            rows_encode<F>(a, lv, xs, nv, lane, NP, tiles + (size_t)tl * plan.tile_bytes + blk * 16 * 16, 2048, 16);
+            rows_encode<F, false, false, true>(a, lv, xs, nv, lane, NP, tiles + (size_t)tl * plan.tile_bytes + blk * 16 * 16, 2048, 16);
             if (lane == 0) {
                 C.owner[tl][blk] = 2 * warp + s;
                 C.nrows[tl][blk] = nv;
@@ -1148,7 +1148,7 @@ static cudaError_t launch_persistent(Kern k, int threads, size_t smem, int64_t m
 
 template <int F, int D>
 static cudaError_t launch_query_t(const QueryArgs& a, int64_t max_work, cudaStream_t s) {
-    if (!query_mlp_warp() && !a.m.bf16) {                          // the tcgen05 variant is fp16 only
+    if (!query_mlp_warp() && !a.m.bf16 && a.g.tex != 0 && F == 2) {   // the tcgen05 variant: fp16, TEX gathers
         const WsPlan plan(D, a.m.hidden, a.g.n_points);
         if (plan.total <= 227 * 1024)
             return launch_persistent<0>(k_query_ws<F, D>, (kWsWorkers + 4) * 32, plan.total, max_work,

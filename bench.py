@@ -355,7 +355,10 @@ def run_ours(args):
            "note": "per rank; value = the frame's rays / max-over-ranks time"}
 
     gather = bench_gather(args)
-    l2_peak = gather.get("l2_random_4B_GBps")
+    # the best random 4-byte gather rate the probe reaches on the load pipe, the texture pipe
+    # or both (k_query_warp gathers its hashed levels through the texture pipe)
+    l2_peak = max(v for v in (gather.get("l2_random_4B_GBps"), gather.get("l2_random_4B_tex_GBps"),
+                              gather.get("l2_random_4B_lsu_tex_GBps")) if v)
     mlp = bench_mlp(ctx, args)
     train = bench_train(ctx, args, world, rank) if args.train else None
     lod = bench_lod(args, local) if (args.lod and rank == 0) else None
@@ -363,8 +366,9 @@ def run_ours(args):
 
     roof = {"bound": "l2_gather", "kernel": "k_query (persistent: sample+encode+MLP+decode+terminate, slot refill)",
             "achieved": achieved, "peak": l2_peak, "unit": "GB/s", "frac": achieved / l2_peak if l2_peak else None,
-            "peak_source": "measured live (nbvh_gather_probe): random 4-byte gathers from a 16 MB L2-resident "
-                           "table, counted as 32-byte sectors/s -- the random-sector read rate of the L1/L2 path",
+            "peak_source": "measured live (nbvh_gather_probe / nbvh_gather_probe_tex): random 4-byte gathers "
+                           "from a 16 MB L2-resident table counted as 32-byte sectors/s, the best of the load "
+                           "pipe, the texture pipe and both together",
             "achieved_definition": "queries x 2,048 useful fp16 corner bytes (n*L*8*F*2, SURVEY §8(d)) / the "
                                    "kernel's CUDA-event time",
             "traffic": traffic,
@@ -694,6 +698,21 @@ def bench_gather(args):
         out[name + "_Gsectors_per_s"] = done / s / 1e9                  # one 32-byte sector per gather
         out[name + "_GBps"] = done * 32 / s / 1e9
         del tab
+    # the same 4-byte gathers through the texture pipe (k_query_warp's hashed levels), and with
+    # half of them on each pipe: the peak of a kernel that uses both L1 input pipes
+    from paper_2405_16237_b200.nbvh import gather_probe_tex
+    tab = torch.randint(0, 1 << 30, ((16 << 20) // 4,), dtype=torch.int32, device="cuda")
+    for name, mixed in (("l2_random_4B_tex", False), ("l2_random_4B_lsu_tex", True)):
+        gather_probe_tex(tab, 1 << 26, sink, mixed=mixed)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        done = gather_probe_tex(tab, 1 << 28, sink, mixed=mixed, seed=7)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        s = e0.elapsed_time(e1) / 1e3
+        out[name + "_Gsectors_per_s"] = done / s / 1e9
+        out[name + "_GBps"] = done * 32 / s / 1e9
+    del tab
     from paper_2405_16237_b200.nbvh import atomic_probe
     for vec in (1, 2, 4):                                                # T7 scatter roofline
         tab = torch.zeros((32 << 20) // 4, dtype=torch.float32, device="cuda")   # ~ the cfg-2 gradient buffer

@@ -222,6 +222,14 @@ nbvh_status nbvh_mlp_forward(nbvh_ctx* ctx, const uint16_t* d_x, int64_t m, floa
  * the caller times it (CUDA events on `stream`).  NBVH_EINVAL on bad arguments. */
 nbvh_status nbvh_gather_probe(const void* d_table, int64_t table_bytes, int32_t entry_bytes, int64_t n_gathers,
                               uint32_t seed, uint32_t* d_sink, int64_t sink_len, int64_t* n_done, void* stream);
+/* The same 4-byte random gathers through the texture pipe (tex1Dfetch on a texture object the
+ * call creates over d_table, as the query kernel's hashed levels read the table), or with half of
+ * the address chains on each pipe (mixed = 1): the gather peak of a kernel that uses both L1
+ * input pipes.  table_bytes / 4 a power of two <= 2^27; 32-byte aligned.  Synchronises `stream`
+ * before it destroys the texture object.  NBVH_EINVAL on bad arguments, NBVH_ECUDA when the
+ * texture object cannot be created. */
+nbvh_status nbvh_gather_probe_tex(const void* d_table, int64_t table_bytes, int32_t mixed, int64_t n_gathers,
+                                  uint32_t seed, uint32_t* d_sink, int64_t sink_len, int64_t* n_done, void* stream);
 /* The scatter roofline of SURVEY §8(d) (T7 is bound by L2 atomics): n_ops uniformly random
  * fp32 reductions (vec 1: red.global.add.f32; vec 2: red.global.add.v2.f32 on 8-byte pairs,
  * as the training backward issues for F = 2; vec 4: red.global.add.v4.f32 on 16-byte quads)

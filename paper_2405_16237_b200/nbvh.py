@@ -93,6 +93,7 @@ SIGNATURES = {
     "nbvh_gen_train_rays": (C.c_int, [_P, C.c_uint64, C.c_uint64, _I64, _I64, _P, _P, _P, _P, _P]),
     "nbvh_intersect_mesh": (C.c_int, [_P, _P, _I64, Hits, _P]),
     "nbvh_gather_probe": (C.c_int, [_P, _I64, _I32, _I64, C.c_uint32, _P, _I64, _P, _P]),
+    "nbvh_gather_probe_tex": (C.c_int, [_P, _I64, _I32, _I64, C.c_uint32, _P, _I64, _P, _P]),
     "nbvh_atomic_probe": (C.c_int, [_P, _I64, _I32, _I64, C.c_uint32, _P, _P]),
     "nbvh_pt_shade": (C.c_int, [_P, _P, _I64, Hits, Hits, _P, _P, _P, C.c_uint64, _I32, _P, _F, _P, _P]),
     "nbvh_tlas_build": (C.c_int, [_P, _P, _I32, _P]),
@@ -156,6 +157,18 @@ def gather_probe(table, entry_bytes: int, n_gathers: int, sink, seed: int = 1, s
                                           C.byref(done), _stream_ptr(stream))
     if st != 0:
         raise NbvhError(st, "gather_probe: bad arguments")
+    return int(done.value)
+
+
+def gather_probe_tex(table, n_gathers: int, sink, mixed: bool = False, seed: int = 1, stream=None) -> int:
+    """nbvh_gather_probe_tex: n_gathers random 4-byte reads of `table` through the texture pipe
+    (mixed: half of them through the load pipe); synchronises the stream; returns the count."""
+    done = C.c_int64(0)
+    st = load_library().nbvh_gather_probe_tex(_ptr(table), table.numel() * table.element_size(), 1 if mixed else 0,
+                                              int(n_gathers), int(seed) & 0xFFFFFFFF, _ptr(sink), sink.numel(),
+                                              C.byref(done), _stream_ptr(stream))
+    if st != 0:
+        raise NbvhError(st, "gather_probe_tex: bad arguments")
     return int(done.value)
 
 

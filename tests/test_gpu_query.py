@@ -359,6 +359,17 @@ def test_gather_probe_runs_and_validates():
         gather_probe(tab, 8, 1 << 20, sink)
     with pytest.raises(NbvhError):
         gather_probe(tab[:3 * 4096], 4, 1 << 20, sink)          # not a power of two
+    # the texture-pipe probe reads the same entries: with the same seed, the TEX-only run's
+    # XOR sink equals the load-pipe run's (same chains, same addresses)
+    from paper_2405_16237_b200.nbvh import gather_probe_tex
+    gather_probe(tab, 4, 1 << 20, sink, seed=5)
+    ldg = sink.clone()
+    assert gather_probe_tex(tab, 1 << 20, sink, seed=5) >= 1 << 20
+    assert torch.equal(ldg, sink)
+    assert gather_probe_tex(tab, 1 << 20, sink, mixed=True, seed=5) >= 1 << 20
+    assert torch.equal(ldg, sink)
+    with pytest.raises(NbvhError):
+        gather_probe_tex(tab[:3 * 4096], 1 << 20, sink)
 
 
 def test_query_host_path_full_frame():

@@ -33,6 +33,7 @@ struct TrainWork {
     float* dZ = nullptr;
     float* Z = nullptr;              // [cap][8] raw z, allocated only while parity capture is on
     float* gx = nullptr;             // [cap][D] dL/dx (bwd -> scatter)
+    unsigned long long tex_gx = 0;   // texture object over gx (float2 texels; the scatter's reads, F = 2)
     int32_t* ss_ray = nullptr;       // samples grouped by leaf (k_sort_place): ray, leaf, t0, t1
     int32_t* ss_leaf = nullptr;
     float* ss_t0 = nullptr;
@@ -150,6 +151,8 @@ static void dfree(T*& p) {
 static void free_work(TrainWork* w) {
     dfree(w->r_acc); dfree(w->r_leaf); dfree(w->r_gt); dfree(w->r_loss);
     dfree(w->s_ray); dfree(w->s_leaf); dfree(w->s_t0); dfree(w->s_t1); dfree(w->s_gt);
+    if (w->tex_gx) cudaDestroyTextureObject((cudaTextureObject_t)w->tex_gx);
+    w->tex_gx = 0;
     dfree(w->X); dfree(w->A); dfree(w->Dl); dfree(w->dZ); dfree(w->Z); dfree(w->gx);
     dfree(w->ss_ray); dfree(w->ss_leaf); dfree(w->ss_t0); dfree(w->ss_t1);
 }
@@ -222,6 +225,21 @@ nbvh_status reserve_train(nbvh_ctx* c, int64_t max_rays) {
     if (e == cudaSuccess) e = cudaMalloc((void**)&w->Dl, H * n * 64 * 2);
     if (e == cudaSuccess) e = cudaMalloc((void**)&w->dZ, n * 8 * 4);
     if (e == cudaSuccess) e = cudaMalloc((void**)&w->gx, n * D * 4);
+    if (e == cudaSuccess && c->cfg.F == 2 && (int64_t)n * D / 2 <= ((int64_t)1 << 27)) {
+        // the T7 scatter reads dL/dx through the texture pipe (its load pipe is the limit)
+        cudaResourceDesc rd{};
+        rd.resType = cudaResourceTypeLinear;
+        rd.res.linear.devPtr = w->gx;
+        rd.res.linear.desc = cudaCreateChannelDesc<float2>();
+        rd.res.linear.sizeInBytes = (size_t)n * D * 4;
+        cudaTextureDesc td{};
+        td.readMode = cudaReadModeElementType;
+        td.filterMode = cudaFilterModePoint;
+        td.addressMode[0] = cudaAddressModeClamp;
+        cudaTextureObject_t t = 0;
+        if (cudaCreateTextureObject(&t, &rd, &td, nullptr) == cudaSuccess) w->tex_gx = t;
+        else cudaGetLastError();
+    }
     if (e == cudaSuccess) e = cudaMalloc((void**)&w->ss_ray, n * 4);
     if (e == cudaSuccess) e = cudaMalloc((void**)&w->ss_leaf, n * 4);
     if (e == cudaSuccess) e = cudaMalloc((void**)&w->ss_t0, n * 4);
@@ -537,6 +555,10 @@ extern "C" nbvh_status nbvh_train_backward(nbvh_ctx* c, const nbvh_ray* rays, in
         a.priv_floats = (int32_t)end;
     }
     a.gx = w->gx;
+    {
+        const char* ev = std::getenv("NBVH_SCATTER_TEX");      // A/B hook: 0 = dL/dx on the load pipe
+        a.tex_gx = (ev && ev[0] == '0') ? 0ull : w->tex_gx;
+    }
     {
         int dev = 0, sms = 148;
         cudaGetDevice(&dev);

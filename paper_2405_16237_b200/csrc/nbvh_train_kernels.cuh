@@ -61,6 +61,7 @@ struct TrainArgs {
     int32_t priv_levels;     // coarse levels accumulated in shared memory by k_train_scatter
     int32_t priv_floats;     // their gradient floats (levels 0..priv_levels-1 are a prefix)
     float* gx;               // [cap][D] fp32 dL/dx per sample (k_train_bwd -> k_train_scatter)
+    unsigned long long tex_gx;   // texture object over gx (float2 texels; 0: read with loads)
     float* sc_dense;         // T7 scratch of the global dense levels: cell-packed, 8 corners x F
     float* sc_hash;          // T7 scratch of the hashed levels: [T][F], 16-byte aligned per level
     int32_t* sc_priv;        // [scatter CTAs][priv_floats] fixed-point partial sums
@@ -818,8 +819,15 @@ __global__ void __launch_bounds__(256) k_train_scatter_agg(TrainArgs a) {
         for (int l = 0; l < L; ++l) {
             const LevelSm P = lv[l];
             float gv[F];
+            if (F == 2 && a.tex_gx) {      // through the texture pipe: the load pipe is this kernel's limit
+                const float2 v = valid ? tex1Dfetch<float2>((cudaTextureObject_t)a.tex_gx, (int)(it * L + l))
+                                       : make_float2(0.f, 0.f);
+                gv[0] = v.x;
+                gv[F - 1] = v.y;
+            } else {
 #pragma unroll
-            for (int f = 0; f < F; ++f) gv[f] = valid ? gq[l * F + f] : 0.f;
+                for (int f = 0; f < F; ++f) gv[f] = valid ? gq[l * F + f] : 0.f;
+            }
             Cell cell;
             uint32_t i0, i1, i2;
             level_cell_sm(P, hmask, x[0], x[1], x[2], cell, i0, i1, i2);

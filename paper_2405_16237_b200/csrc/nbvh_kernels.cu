@@ -363,6 +363,10 @@ __device__ __forceinline__ void query_mlp_rows16(const MlpSmem& s, int hidden, c
 // s for the refill and decode steps; the encode and MLP steps work on the compacted rows.
 constexpr int kWarpQ = 16;          // queries per slot set (one m16 / one 16-row tile block)
 constexpr int kQueryWarps = 16;     // warps per CTA (one CTA per SM; bounded by shared memory)
+constexpr int kQueryWarpsTex = 20;  // ... with TEX gathers: 20 at 96 registers (5 per SM sub-partition)
+                                    // beats 16 at 128 (0.881 vs 0.924 ms; 18 / 22 / 24: 0.936 / 1.004 /
+                                    // 0.988 ms, profiles/NOTES.md r2i)
+__host__ __device__ constexpr int query_warps(bool tex) { return tex ? kQueryWarpsTex : kQueryWarps; }
 
 struct WarpSlots {
     int32_t ray[kWarpQ], pos[kWarpQ], base[kWarpQ], nbuf[kWarpQ], more[kWarpQ], bleaf[kWarpQ], nq[kWarpQ],
@@ -622,7 +626,7 @@ __device__ __forceinline__ void rows_decode(const QueryArgs& a, WarpSlots& S, co
 struct QuerySmemPlan {
     size_t w, bias, lv, warp0, feat, z, xs, slots, per_warp, total;
     int warps;
-    __host__ __device__ QuerySmemPlan(int d_in, int hidden, int n_points) {
+    __host__ __device__ QuerySmemPlan(int d_in, int hidden, int n_points, int max_warps = kQueryWarps) {
         w = 0;
         bias = w + align16((size_t)mlp_smem_halves(d_in, hidden) * 2);
         lv = bias + align16((size_t)(64 * hidden + 8) * 4);
@@ -632,10 +636,10 @@ struct QuerySmemPlan {
         xs = z + align16((size_t)kWarpQ * 8 * 4);
         slots = xs + align16((size_t)kWarpQ * n_points * 3 * 4);
         per_warp = slots + align16(sizeof(WarpSlots));
-        // as many warps (<= kQueryWarps) as fit the 227 KB per-CTA limit
+        // as many warps (<= max_warps) as fit the 227 KB per-CTA limit
         const size_t cap = 227 * 1024;
         warps = warp0 + per_warp > cap ? 0 : (int)((cap - warp0) / per_warp);
-        if (warps > kQueryWarps) warps = kQueryWarps;
+        if (warps > max_warps) warps = max_warps;
         total = warp0 + per_warp * warps;
     }
 };
@@ -647,7 +651,7 @@ struct QuerySmemPlan {
 // refill overlaps other warps' gathers.  Selected with NBVH_QUERY_MLP=warp (A/B reference of
 // the warp-specialised kernel below).
 template <int F, int D, bool kBf, bool kTex = false>
-__global__ void __launch_bounds__(kQueryWarps * 32, 1) k_query_warp(QueryArgs a) {
+__global__ void __launch_bounds__(query_warps(kTex) * 32, 1) k_query_warp(QueryArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int NP = a.g.n_points;
@@ -1154,12 +1158,12 @@ static cudaError_t launch_query_t(const QueryArgs& a, int64_t max_work, cudaStre
             return launch_persistent<0>(k_query_ws<F, D>, (kWsWorkers + 4) * 32, plan.total, max_work,
                                      2 * kWsWorkers * kWarpQ, a, s, a.m.hidden, a.g.n_points);
     }
-    QuerySmemPlan plan(D, a.m.hidden, a.g.n_points);
+    // hashed-level gathers through the TEX pipe when the context has its texture object (F = 2)
+    const bool tex = a.g.tex != 0 && F == 2;
+    QuerySmemPlan plan(D, a.m.hidden, a.g.n_points, query_warps(tex));
     if (plan.warps < 1) return cudaErrorInvalidValue;
     plan.warps = query_warps_cap(plan.warps);
     plan.total = plan.warp0 + plan.per_warp * plan.warps;
-    // hashed-level gathers through the TEX pipe when the context has its texture object (F = 2)
-    const bool tex = a.g.tex != 0 && F == 2;
     if (a.m.bf16)
         return tex ? launch_persistent<5>(k_query_warp<F, D, true, true>, plan.warps * 32, plan.total, max_work,
                                           plan.warps * kWarpQ, a, s, a.m.hidden, a.g.n_points)

@@ -370,8 +370,10 @@ __host__ __device__ constexpr int query_warps(bool tex) { return tex ? kQueryWar
 
 struct WarpSlots {
     int32_t ray[kWarpQ], pos[kWarpQ], base[kWarpQ], nbuf[kWarpQ], more[kWarpQ], bleaf[kWarpQ], nq[kWarpQ],
-        leaf[kWarpQ], act[kWarpQ], fresh[kWarpQ];   // fresh: the current entry is in the slot (entry 0
+        leaf[kWarpQ], act[kWarpQ], fresh[kWarpQ],   // fresh: the current entry is in the slot (entry 0
                                                     // from the work record, later ones from the decode)
+        pend[kWarpQ];                               // the list ran out with leaves remaining (C6):
+                                                    // refilled at the top of the next iteration
     float o[3][kWarpQ], d[3][kWarpQ];
     float bt[kWarpQ], bte[kWarpQ], te[kWarpQ], tx[kWarpQ];
     float nrm[3][kWarpQ], alb[3][kWarpQ];
@@ -426,7 +428,59 @@ __device__ __forceinline__ void slots_refill(const QueryArgs& a, WarpSlots& S, i
             S.bte[lane] = 0.f;
             S.bleaf[lane] = -1;
             S.nq[lane] = 0;
+            S.pend[lane] = 0;
         }
+    }
+    __syncwarp();
+}
+
+// Q7: slot s's ray r is finished -- its hit record (a miss keeps t = +inf and zero
+// vectors) and the slot freed.
+__device__ __forceinline__ void slot_finish(const QueryArgs& a, WarpSlots& S, int s, int r) {
+    const int bleaf = S.bleaf[s];
+    const bool h = bleaf >= 0;
+    a.out.hit[r] = h ? 1 : 0;
+    a.out.t[r] = h ? S.bt[s] : __int_as_float(0x7f800000);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        a.out.normal[3 * (int64_t)r + k] = h ? S.nrm[k][s] : 0.f;
+        a.out.albedo[3 * (int64_t)r + k] = h ? S.alb[k][s] : 0.f;
+    }
+    if (a.out.leaf) a.out.leaf[r] = bleaf;
+    if (a.out.n_queries) a.out.n_queries[r] = S.nq[s];
+    S.ray[s] = -1;
+}
+
+// (A0) the slots whose list ran out with leaves remaining (marked by the decode) resume after
+// their last key, bounded by the best hit (C6).  The traversal is an out-of-line call; made
+// from here, where only the loop's invariants are live, instead of from inside the decode,
+// it no longer makes every decode save and reload its live values around the call site.
+__device__ __forceinline__ void slots_list_refill(const QueryArgs& a, WarpSlots& S, int lane) {
+    const bool pend = lane < kWarpQ && S.ray[lane] >= 0 && S.pend[lane];
+    if (__ballot_sync(0xffffffffu, pend) == 0u) return;   // warp-uniform: rare
+    if (pend) {
+        S.pend[lane] = 0;
+        const int r = S.ray[lane];
+        const int bleaf = S.bleaf[lane];
+        const float bt = S.bt[lane];
+        int more = 0;
+        const int nbuf = refill_list(a.cut, a.rays, a.n_rays, a.cap, a.lst, a.ctr, r, S.nbuf[lane],
+                                     bleaf >= 0 ? bt : __int_as_float(0x7f800000), &more);
+        S.base[lane] = S.pos[lane];
+        S.nbuf[lane] = nbuf;
+        S.more[lane] = more;
+        bool done = nbuf == 0;
+        if (!done) {
+            const float4 e = __ldcs(a.lst + r);                   // the new list's first entry
+            done = bleaf >= 0 && e.x > bt;                         // front-to-back termination
+            if (!done) {
+                S.te[lane] = e.x;
+                S.tx[lane] = e.y;
+                S.leaf[lane] = __float_as_int(e.z);
+                S.fresh[lane] = 1;
+            }
+        }
+        if (done) slot_finish(a, S, lane, r);
     }
     __syncwarp();
 }
@@ -567,29 +621,13 @@ __device__ __forceinline__ void rows_decode(const QueryArgs& a, WarpSlots& S, co
         }
         ++pos;
         bool done = a.mode == 1 && hit;                                 // R1: first confident hit (C5)
+        S.nq[s] = nq;
         if (!done) {
-            int base = S.base[s], nbuf = S.nbuf[s];
-            bool refilled = false;
-            if (pos - base >= nbuf) {
-                if (!S.more[s]) {
-                    done = true;                                         // every intersected leaf visited
-                } else {
-                    // list exhausted, more leaves may remain: resume after the last key,
-                    // bounded by the best hit (C6)
-                    int more = 0;
-                    nbuf = refill_list(a.cut, a.rays, a.n_rays, a.cap, a.lst, a.ctr, r,
-                                       nbuf, bleaf >= 0 ? bt : __int_as_float(0x7f800000), &more);
-                    base = pos;
-                    S.base[s] = base;
-                    S.nbuf[s] = nbuf;
-                    S.more[s] = more;
-                    done = nbuf == 0;
-                    refilled = true;
-                }
-            }
-            if (!done) {
-                // the entry prefetched by (C), or after a refill the new list's first one
-                const float4 e = refilled ? __ldcs(a.lst + (int64_t)(pos - base) * a.n_rays + r) : S.nxt[s];
+            if (pos - S.base[s] >= S.nbuf[s]) {
+                if (!S.more[s]) done = true;                             // every intersected leaf visited
+                else S.pend[s] = 1;                                      // refilled by (A0)
+            } else {
+                const float4 e = S.nxt[s];                               // the entry prefetched by (C)
                 done = bleaf >= 0 && e.x > bt;                         // front-to-back termination
                 if (!done) {            // the next entry stays in the slot: no reload in (C)
                     S.te[s] = e.x;
@@ -600,21 +638,7 @@ __device__ __forceinline__ void rows_decode(const QueryArgs& a, WarpSlots& S, co
             }
         }
         S.pos[s] = pos;
-        S.nq[s] = nq;
-        if (done) {
-            // Q7: hit record; a miss keeps t = +inf and zero vectors
-            const bool h = bleaf >= 0;
-            a.out.hit[r] = h ? 1 : 0;
-            a.out.t[r] = h ? bt : __int_as_float(0x7f800000);
-#pragma unroll
-            for (int k = 0; k < 3; ++k) {
-                a.out.normal[3 * (int64_t)r + k] = h ? S.nrm[k][s] : 0.f;
-                a.out.albedo[3 * (int64_t)r + k] = h ? S.alb[k][s] : 0.f;
-            }
-            if (a.out.leaf) a.out.leaf[r] = bleaf;
-            if (a.out.n_queries) a.out.n_queries[r] = nq;
-            S.ray[s] = -1;
-        }
+        if (done) slot_finish(a, S, s, r);
     }
     __syncwarp();
 }
@@ -684,6 +708,7 @@ __global__ void __launch_bounds__(query_warps(kTex) * 32, 1) k_query_warp(QueryA
     }
     __syncwarp();
     while (true) {
+        slots_list_refill(a, S, lane);
         slots_refill(a, S, lane, s_work[1], s_work[0], s_exh + warp);
         const int nv = slots_segment(a, S, xs, lane, NP);
         if (nv == 0) break;                   // work list drained and every slot finished
@@ -872,6 +897,7 @@ __global__ void __launch_bounds__((kWsWorkers + 4) * 32, 1) k_query_ws(QueryArgs
                 pend &= ~(1u << s);
                 rows_decode(a, S, zt, (int)((nv_pk >> (8 * s)) & 0xffu), lane);
             }
+            slots_list_refill(a, S, lane);
             slots_refill(a, S, lane, C.work[1], C.work[0], &C.exh[warp]);
             const int nv = slots_segment(a, S, xs, lane, NP);
             nv_pk = (nv_pk & ~(0xffu << (8 * s))) | ((uint32_t)nv << (8 * s));

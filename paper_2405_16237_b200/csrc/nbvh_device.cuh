@@ -815,8 +815,13 @@ __device__ __forceinline__ void mlp_rows16(const MlpSmem& s, int hidden, const _
     // output layer: 64 -> 8, linear
     float o[4];
     {
-        const float* bb = s.b + hidden * 64;
-        o[0] = bb[2 * t]; o[1] = bb[2 * t + 1]; o[2] = o[0]; o[3] = o[1];
+        // read here (volatile) rather than hoisted above the hidden layers, where the pair
+        // would be held -- or spilled -- across them
+        asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];"
+                     : "=f"(o[0]), "=f"(o[1])
+                     : "r"((uint32_t)__cvta_generic_to_shared(s.b + hidden * 64 + 2 * t)));
+        o[2] = o[0];
+        o[3] = o[1];
     }
     const uint32_t wo = (uint32_t)__cvta_generic_to_shared(s.wo + (lane & 7) * 72 + ((lane >> 3) & 1) * 8);
 #pragma unroll

@@ -674,6 +674,30 @@ struct QuerySmemPlan {
 // activations in registers), (F) decode.  Warps drift freely, so one warp's MLP or list
 // refill overlaps other warps' gathers.  Selected with NBVH_QUERY_MLP=warp (A/B reference of
 // the warp-specialised kernel below).
+// A warp's private shared-memory region of k_query_warp, derived from a volatile read of
+// %tid.x so that every use re-derives it (a few integer instructions) instead of keeping the
+// addresses live across the encode and the MLP.
+struct WarpPtrs {
+    int lane, warp;
+    __half* feat;      // [kWarpQ][D+8]
+    float* zt;         // [kWarpQ][8]
+    float* xs;         // [NP*3][kWarpQ]
+    WarpSlots* S;
+};
+__device__ __forceinline__ WarpPtrs warp_ptrs(unsigned char* smem_raw, const QuerySmemPlan& plan) {
+    int tid;
+    asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tid));
+    WarpPtrs P;
+    P.lane = tid & 31;
+    P.warp = tid >> 5;
+    unsigned char* wbase = smem_raw + plan.warp0 + plan.per_warp * P.warp;
+    P.feat = reinterpret_cast<__half*>(wbase + plan.feat);
+    P.zt = reinterpret_cast<float*>(wbase + plan.z);
+    P.xs = reinterpret_cast<float*>(wbase + plan.xs);
+    P.S = reinterpret_cast<WarpSlots*>(wbase + plan.slots);
+    return P;
+}
+
 template <int F, int D, bool kBf, bool kTex = false>
 __global__ void __launch_bounds__(query_warps(kTex) * 32, 1) k_query_warp(QueryArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -686,20 +710,17 @@ __global__ void __launch_bounds__(query_warps(kTex) * 32, 1) k_query_warp(QueryA
     ms.wo = ms.wh + (a.m.hidden - 1) * 64 * 72;
     ms.b = reinterpret_cast<float*>(smem_raw + plan.bias);
     LevelSm* lv = reinterpret_cast<LevelSm*>(smem_raw + plan.lv);
-    unsigned char* wbase = smem_raw + plan.warp0 + plan.per_warp * warp;
-    __half* feat = reinterpret_cast<__half*>(wbase + plan.feat);              // [kWarpQ][D+8]
-    float* zt = reinterpret_cast<float*>(wbase + plan.z);                     // [kWarpQ][8]
-    float* xs = reinterpret_cast<float*>(wbase + plan.xs);                    // [NP*3][kWarpQ]
-    WarpSlots& S = *reinterpret_cast<WarpSlots*>(wbase + plan.slots);
+    WarpPtrs P = warp_ptrs(smem_raw, plan);
     stage_mlp(a.m, ms, tid, blockDim.x);
     stage_levels(a.g, lv, tid);
-    if (lane < kWarpQ) S.ray[lane] = -1;
+    if (lane < kWarpQ) P.S->ray[lane] = -1;
     __syncthreads();                          // the only block-wide barrier
     // work-list sizes and per-warp statistics live in shared memory (read on refills / written
     // by one lane): kept out of the loop's registers
     __shared__ int s_work[2];                 // n_long, total
     __shared__ int s_stat[2 * 32];            // per warp: [0] queries evaluated, [1] loop iterations
     __shared__ int s_exh[32];                 // per warp: work list exhausted
+    __shared__ int s_nv[32];                  // per warp: rows of the current iteration
     if (lane == 0) {
         s_work[0] = *a.cnt_long;              // long rays first (k_traverse), then the rest
         s_work[1] = s_work[0] + *a.cnt;       // rays with >= 1 intersected leaf
@@ -708,18 +729,25 @@ __global__ void __launch_bounds__(query_warps(kTex) * 32, 1) k_query_warp(QueryA
     }
     __syncwarp();
     while (true) {
-        slots_list_refill(a, S, lane);
-        slots_refill(a, S, lane, s_work[1], s_work[0], s_exh + warp);
-        const int nv = slots_segment(a, S, xs, lane, NP);
+        // the per-lane shared-memory addresses and the row count are re-derived after the
+        // encode and the MLP instead of being held across them (ptxas spilled them to the stack)
+        P = warp_ptrs(smem_raw, plan);
+        WarpSlots& S = *P.S;
+        slots_list_refill(a, S, P.lane);
+        slots_refill(a, S, P.lane, s_work[1], s_work[0], s_exh + P.warp);
+        const int nv = slots_segment(a, S, P.xs, P.lane, NP);
         if (nv == 0) break;                   // work list drained and every slot finished
-        if (lane == 0) {
-            s_stat[2 * warp] += nv;
-            s_stat[2 * warp + 1] += 1;
+        if (P.lane == 0) {
+            s_stat[2 * P.warp] += nv;
+            s_stat[2 * P.warp + 1] += 1;
+            s_nv[P.warp] = nv;
         }
-        rows_encode<F, kBf, true, kTex>(a, lv, xs, nv, lane, NP, reinterpret_cast<unsigned char*>(feat), 16, (D + 8) * 2);
-        query_mlp_rows16<D, kBf>(ms, a.m.hidden, feat, 0, zt, lane);         // (E)
+        rows_encode<F, kBf, true, kTex>(a, lv, P.xs, nv, P.lane, NP, reinterpret_cast<unsigned char*>(P.feat), 16, (D + 8) * 2);
+        const WarpPtrs Pm = warp_ptrs(smem_raw, plan);
+        query_mlp_rows16<D, kBf>(ms, a.m.hidden, Pm.feat, 0, Pm.zt, Pm.lane);         // (E)
         __syncwarp();
-        rows_decode(a, S, zt, nv, lane);
+        const WarpPtrs Pd = warp_ptrs(smem_raw, plan);
+        rows_decode(a, *Pd.S, Pd.zt, *reinterpret_cast<volatile int*>(s_nv + Pd.warp), Pd.lane);
     }
     if (lane == 0) {
         atomicAdd(&a.ctr->n_queries, (unsigned long long)s_stat[2 * warp]);

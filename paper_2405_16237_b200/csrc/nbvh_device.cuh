@@ -220,9 +220,8 @@ __device__ int collect_leaves(const CutDev& cut, const RayDev& R, bool has_after
 // ------------------------------------------------------------------ segment sampling
 // u = (2i+1)/(2n) (inference) or (i+xi)/n (training); dt = t1-t0; t = t0+u*dt;
 // p = o + t*d; x = clamp((p-dom_min)*dom_inv, 0, 1); every op rounded (no FMA).
-__device__ __forceinline__ void segment_point(const GridDev& g, const float o[3], const float d[3], float t0, float t1,
-                                              int i, int n, const float* xi, float x[3]) {
-    float u = xi ? __fdiv_rn(__fadd_rn((float)i, xi[i]), (float)n) : __fdiv_rn((float)(2 * i + 1), (float)(2 * n));
+__device__ __forceinline__ void segment_point_u(const GridDev& g, const float o[3], const float d[3], float t0,
+                                                float t1, float u, float x[3]) {
     float dt = __fsub_rn(t1, t0);
     float t = __fadd_rn(t0, __fmul_rn(u, dt));
 #pragma unroll
@@ -231,6 +230,13 @@ __device__ __forceinline__ void segment_point(const GridDev& g, const float o[3]
         float v = __fmul_rn(__fsub_rn(p, g.dom_min[k]), g.dom_inv);
         x[k] = fminf(fmaxf(v, 0.0f), 1.0f);
     }
+}
+__device__ __forceinline__ float segment_u(int i, int n, const float* xi) {
+    return xi ? __fdiv_rn(__fadd_rn((float)i, xi[i]), (float)n) : __fdiv_rn((float)(2 * i + 1), (float)(2 * n));
+}
+__device__ __forceinline__ void segment_point(const GridDev& g, const float o[3], const float d[3], float t0, float t1,
+                                              int i, int n, const float* xi, float x[3]) {
+    segment_point_u(g, o, d, t0, t1, segment_u(i, n, xi), x);
 }
 
 // ------------------------------------------------------------------ grid cell of a level

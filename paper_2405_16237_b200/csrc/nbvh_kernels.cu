@@ -488,7 +488,8 @@ __device__ __forceinline__ void slots_list_refill(const QueryArgs& a, WarpSlots&
 // (B) compact the occupied slots into rows 0..nv-1 (S.act[row] = slot) and (C) fetch each
 // ray's current leaf segment and its n stratified sample points (C8) into
 // xs [NP*3][kWarpQ].  Returns nv (warp-uniform).
-__device__ __forceinline__ int slots_segment(const QueryArgs& a, WarpSlots& S, float* xs, int lane, int NP) {
+__device__ __forceinline__ int slots_segment(const QueryArgs& a, WarpSlots& S, float* xs, int lane, int NP,
+                                             const float* u_tab) {
     const bool occ = lane < kWarpQ && S.ray[lane] >= 0;
     const unsigned om = __ballot_sync(0xffffffffu, occ);
     const int nv = __popc(om);
@@ -522,7 +523,7 @@ __device__ __forceinline__ int slots_segment(const QueryArgs& a, WarpSlots& S, f
         const float d[3] = {S.d[0][lane], S.d[1][lane], S.d[2][lane]};
         for (int p = 0; p < NP; ++p) {
             float x[3];
-            segment_point(a.g, o, d, te, tx, p, NP, nullptr, x);
+            segment_point_u(a.g, o, d, te, tx, u_tab[p], x);   // u_p = (2p+1)/(2NP), per CTA
             xs[(p * 3 + 0) * kWarpQ + row] = x[0];
             xs[(p * 3 + 1) * kWarpQ + row] = x[1];
             xs[(p * 3 + 2) * kWarpQ + row] = x[2];
@@ -713,6 +714,8 @@ __global__ void __launch_bounds__(query_warps(kTex) * 32, 1) k_query_warp(QueryA
     WarpPtrs P = warp_ptrs(smem_raw, plan);
     stage_mlp(a.m, ms, tid, blockDim.x);
     stage_levels(a.g, lv, tid);
+    __shared__ float s_u[16];                 // the segment's stratified offsets (NP <= 16: d_in <= 128)
+    if (tid < NP) s_u[tid] = segment_u(tid, NP, nullptr);
     if (lane < kWarpQ) P.S->ray[lane] = -1;
     __syncthreads();                          // the only block-wide barrier
     // work-list sizes and per-warp statistics live in shared memory (read on refills / written
@@ -735,7 +738,7 @@ __global__ void __launch_bounds__(query_warps(kTex) * 32, 1) k_query_warp(QueryA
         WarpSlots& S = *P.S;
         slots_list_refill(a, S, P.lane);
         slots_refill(a, S, P.lane, s_work[1], s_work[0], s_exh + P.warp);
-        const int nv = slots_segment(a, S, P.xs, P.lane, NP);
+        const int nv = slots_segment(a, S, P.xs, P.lane, NP, s_u);
         if (nv == 0) break;                   // work list drained and every slot finished
         if (P.lane == 0) {
             s_stat[2 * P.warp] += nv;
@@ -871,6 +874,8 @@ __global__ void __launch_bounds__((kWsWorkers + 4) * 32, 1) k_query_ws(QueryArgs
         *reinterpret_cast<uint4*>(smem_raw + plan.ones + 2048 + i * 16) = make_uint4(0u, 0u, 0u, 0u);
     }
     stage_levels(a.g, lv, tid);
+    __shared__ float s_u[16];                 // the segment's stratified offsets (NP <= 16: d_in <= 128)
+    if (tid < NP) s_u[tid] = segment_u(tid, NP, nullptr);
     if (warp < kWsWorkers && lane < kWarpQ) {
         reinterpret_cast<WarpSlots*>(set_base(2 * warp))->ray[lane] = -1;
         reinterpret_cast<WarpSlots*>(set_base(2 * warp + 1))->ray[lane] = -1;
@@ -927,7 +932,7 @@ __global__ void __launch_bounds__((kWsWorkers + 4) * 32, 1) k_query_ws(QueryArgs
             }
             slots_list_refill(a, S, lane);
             slots_refill(a, S, lane, C.work[1], C.work[0], &C.exh[warp]);
-            const int nv = slots_segment(a, S, xs, lane, NP);
+            const int nv = slots_segment(a, S, xs, lane, NP, s_u);
             nv_pk = (nv_pk & ~(0xffu << (8 * s))) | ((uint32_t)nv << (8 * s));
             if (nv == 0) {
                 if (!(pend & (1u << (s ^ 1)))) break;   // both sets drained: done

@@ -321,6 +321,24 @@ static nbvh_status ensure_scatter_scratch(nbvh_ctx* c, TrainArgs& a, int sms) {
         cudaGetLastError();
         return fail(c, NBVH_ENOMEM, "train: T7 scratch");
     }
+    // the hashed levels (coarse-to-fine, after the dense ones) are contiguous in the scratch
+    // (T*F floats each, a multiple of 4) and, if also in the canonical layout, copied flat
+    a.hash_coff0 = -1;
+    a.hash_floats = nh;
+    {
+        int64_t first = -1, expect = 0;
+        bool contiguous = true;
+        for (int l = 0; l < c->cfg.L; ++l) {
+            if (c->dense[l]) {
+                if (first >= 0) contiguous = false;          // a dense level after a hashed one
+                continue;
+            }
+            if (first < 0) first = expect = c->offset[l];
+            if (c->offset[l] != expect || a.sc_off[l] != (expect - first) * F) contiguous = false;
+            expect += (int64_t)1 << c->cfg.log2_T;
+        }
+        if (first >= 0 && contiguous) a.hash_coff0 = first;
+    }
     a.sc_dense = w->sc_dense;
     a.sc_hash = w->sc_hash;
     a.sc_priv = w->sc_priv;

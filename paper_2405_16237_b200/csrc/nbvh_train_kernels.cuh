@@ -67,6 +67,9 @@ struct TrainArgs {
     int32_t* sc_priv;        // [scatter CTAs][priv_floats] fixed-point partial sums
     int64_t sc_off[kMaxLevels];   // float offset of a level's scratch (dense: in sc_dense; hashed: in sc_hash)
     int64_t sc_dense_n, sc_hash_n;   // scratch sizes (floats)
+    int64_t hash_coff0;              // canonical entry offset of the first hashed level when the hashed
+                                     // levels are one contiguous range in both layouts (else -1)
+    int64_t hash_floats;             // floats of that range (a multiple of 4)
     int32_t scatter_ctas;
     int32_t agg_levels;      // k_train_scatter_agg: levels 0..agg_levels-1 warp-aggregated (0: k_train_scatter)
     int32_t* leaf_hist;      // k_train_select: accepted samples per leaf (nullable; the sort's counts)
@@ -1003,10 +1006,31 @@ __global__ void __launch_bounds__(256) k_train_scatter_finish(TrainArgs a) {
 #pragma unroll
                 for (int f = 0; f < F; ++f) a.grad[((int64_t)P.coff + v) * F + f] = acc[f];
             }
-        } else {
+        } else if (a.hash_coff0 < 0) {
             const int64_t n = (int64_t)(1u << a.g.log2_T) * F;
             const float* sc = a.sc_hash + a.sc_off[l];
             for (int64_t i = t0; i < n; i += stride) a.grad[(int64_t)P.coff * F + i] = sc[i];
+        }
+    }
+    if (a.hash_coff0 >= 0) {
+        // the hashed levels as one flat copy: 16-byte loads of the (16-byte aligned) scratch,
+        // 8-byte stores into the canonical buffer (aligned to 8 bytes only), four loads in
+        // flight per thread -- a per-level 4-byte loop was latency-bound (63 us, r2k)
+        const int64_t n4 = a.hash_floats / 4;
+        const float4* src = reinterpret_cast<const float4*>(a.sc_hash);
+        float2* dst = reinterpret_cast<float2*>(a.grad + a.hash_coff0 * F);
+        for (int64_t i = t0; i < n4; i += 4 * stride) {
+            float4 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (i + u * stride < n4) v[u] = __ldcs(src + i + u * stride);
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (i + u * stride < n4) {
+                    const int64_t j = 2 * (i + u * stride);
+                    __stcs(dst + j, make_float2(v[u].x, v[u].y));
+                    __stcs(dst + j + 1, make_float2(v[u].z, v[u].w));
+                }
         }
     }
 }

@@ -1223,6 +1223,8 @@ static cudaError_t launch_query_t(const QueryArgs& a, int64_t max_work, cudaStre
     if (plan.warps < 1) return cudaErrorInvalidValue;
     plan.warps = query_warps_cap(plan.warps);
     plan.total = plan.warp0 + plan.per_warp * plan.warps;
+    if (const char* pe = std::getenv("NBVH_QUERY_SMEM_PAD"))   // A/B hook: unused shared memory (L1 carveout)
+        plan.total += (size_t)std::atol(pe);
     if (a.m.bf16)
         return tex ? launch_persistent<5>(k_query_warp<F, D, true, true>, plan.warps * 32, plan.total, max_work,
                                           plan.warps * kWarpQ, a, s, a.m.hidden, a.g.n_points)

@@ -363,9 +363,9 @@ __device__ __forceinline__ void query_mlp_rows16(const MlpSmem& s, int hidden, c
 // s for the refill and decode steps; the encode and MLP steps work on the compacted rows.
 constexpr int kWarpQ = 16;          // queries per slot set (one m16 / one 16-row tile block)
 constexpr int kQueryWarps = 16;     // warps per CTA (one CTA per SM; bounded by shared memory)
-constexpr int kQueryWarpsTex = 20;  // ... with TEX gathers: 20 at 96 registers (5 per SM sub-partition)
-                                    // beats 16 at 128 (0.881 vs 0.924 ms; 18 / 22 / 24: 0.936 / 1.004 /
-                                    // 0.988 ms, profiles/NOTES.md r2i)
+constexpr int kQueryWarpsTex = 24;  // ... with TEX gathers: 24 at 80 registers (6 per SM sub-partition,
+                                    // the most the 196 KB shared-memory carveout step holds): 0.800 ms vs
+                                    // 0.816 at 22, 0.836 at 20 (profiles/NOTES.md r2l)
 __host__ __device__ constexpr int query_warps(bool tex) { return tex ? kQueryWarpsTex : kQueryWarps; }
 
 struct WarpSlots {
@@ -488,6 +488,7 @@ __device__ __forceinline__ void slots_list_refill(const QueryArgs& a, WarpSlots&
 // (B) compact the occupied slots into rows 0..nv-1 (S.act[row] = slot) and (C) fetch each
 // ray's current leaf segment and its n stratified sample points (C8) into
 // xs [NP*3][kWarpQ].  Returns nv (warp-uniform).
+template <bool kXs = true>
 __device__ __forceinline__ int slots_segment(const QueryArgs& a, WarpSlots& S, float* xs, int lane, int NP,
                                              const float* u_tab) {
     const bool occ = lane < kWarpQ && S.ray[lane] >= 0;
@@ -519,14 +520,16 @@ __device__ __forceinline__ int slots_segment(const QueryArgs& a, WarpSlots& S, f
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(&S.nxt[lane])),
                          "l"(a.lst + li + a.n_rays)
                          : "memory");
-        const float o[3] = {S.o[0][lane], S.o[1][lane], S.o[2][lane]};
-        const float d[3] = {S.d[0][lane], S.d[1][lane], S.d[2][lane]};
-        for (int p = 0; p < NP; ++p) {
-            float x[3];
-            segment_point_u(a.g, o, d, te, tx, u_tab[p], x);   // u_p = (2p+1)/(2NP), per CTA
-            xs[(p * 3 + 0) * kWarpQ + row] = x[0];
-            xs[(p * 3 + 1) * kWarpQ + row] = x[1];
-            xs[(p * 3 + 2) * kWarpQ + row] = x[2];
+        if constexpr (kXs) {   // else the encode derives the points from the slot (row_point)
+            const float o[3] = {S.o[0][lane], S.o[1][lane], S.o[2][lane]};
+            const float d[3] = {S.d[0][lane], S.d[1][lane], S.d[2][lane]};
+            for (int p = 0; p < NP; ++p) {
+                float x[3];
+                segment_point_u(a.g, o, d, te, tx, u_tab[p], x);   // u_p = (2p+1)/(2NP), per CTA
+                xs[(p * 3 + 0) * kWarpQ + row] = x[0];
+                xs[(p * 3 + 1) * kWarpQ + row] = x[1];
+                xs[(p * 3 + 2) * kWarpQ + row] = x[2];
+            }
         }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
@@ -537,9 +540,19 @@ __device__ __forceinline__ int slots_segment(const QueryArgs& a, WarpSlots& S, f
 // (D) hash-grid encode of the nv rows: lane -> row q = lane % 16; the two half-warps take
 // sample points of opposite parity at the same levels (neighbouring points of the same rays:
 // coherent lines).  Chunk c (8 halves) of row q is stored at dst + c * cstride + q * rstride.
-template <int F, bool kBf = false, bool kSpread = false, bool kTex = false>
+// Without xs (kXs = false, k_query_warp) each lane derives its row's point from the slot.
+__device__ __forceinline__ void row_point(const QueryArgs& a, const WarpSlots& S, const float* u_tab, int q, int p,
+                                          float x[3]) {
+    const int s = S.act[q];
+    const float o[3] = {S.o[0][s], S.o[1][s], S.o[2][s]};
+    const float d[3] = {S.d[0][s], S.d[1][s], S.d[2][s]};
+    segment_point_u(a.g, o, d, S.te[s], S.tx[s], u_tab[p], x);   // the same op sequence as (C)
+}
+
+template <int F, bool kBf = false, bool kSpread = false, bool kTex = false, bool kXs = true>
 __device__ __forceinline__ void rows_encode(const QueryArgs& a, const LevelSm* lv, const float* xs, int nv, int lane,
-                                            int NP, unsigned char* dst, int cstride, int rstride) {
+                                            int NP, unsigned char* dst, int cstride, int rstride,
+                                            const WarpSlots* S = nullptr, const float* u_tab = nullptr) {
     const int cpp = (a.g.L * F) / 8;      // 16-byte chunks per sample point
     const uint32_t hmask = (1u << a.g.log2_T) - 1u;
     if (kSpread && nv <= kWarpQ / 2) {
@@ -552,9 +565,17 @@ __device__ __forceinline__ void rows_encode(const QueryArgs& a, const LevelSm* l
         if (q < nv) {
             for (int j = h; j < NP * cpp; j += lpr) {
                 const int p = j / cpp, lc = j - p * cpp;
-                const float* xp = xs + p * 3 * kWarpQ;
-                const uint4 f = encode_chunk_sm<F, true, kBf, kTex>(lv, a.g.table, hmask, xp[q], xp[kWarpQ + q],
-                                                                    xp[2 * kWarpQ + q], lc * (8 / F), nullptr, a.g.tex);
+                float x[3];
+                if constexpr (kXs) {
+                    const float* xp = xs + p * 3 * kWarpQ;
+                    x[0] = xp[q];
+                    x[1] = xp[kWarpQ + q];
+                    x[2] = xp[2 * kWarpQ + q];
+                } else {
+                    row_point(a, *S, u_tab, q, p, x);
+                }
+                const uint4 f = encode_chunk_sm<F, true, kBf, kTex>(lv, a.g.table, hmask, x[0], x[1], x[2],
+                                                                    lc * (8 / F), nullptr, a.g.tex);
                 *reinterpret_cast<uint4*>(dst + j * cstride + q * rstride) = f;
             }
         }
@@ -564,8 +585,16 @@ __device__ __forceinline__ void rows_encode(const QueryArgs& a, const LevelSm* l
     const int q = lane & (kWarpQ - 1), h = lane / kWarpQ;
     if (q < nv) {
         for (int p = h; p < NP; p += 2) {
-            const float* xp = xs + p * 3 * kWarpQ;
-            const float x0 = xp[q], x1 = xp[kWarpQ + q], x2 = xp[2 * kWarpQ + q];
+            float x[3];
+            if constexpr (kXs) {
+                const float* xp = xs + p * 3 * kWarpQ;
+                x[0] = xp[q];
+                x[1] = xp[kWarpQ + q];
+                x[2] = xp[2 * kWarpQ + q];
+            } else {
+                row_point(a, *S, u_tab, q, p, x);
+            }
+            const float x0 = x[0], x1 = x[1], x2 = x[2];
             for (int lc = 0; lc < cpp; ++lc) {
                 const int c = p * cpp + lc;
                 const uint4 f = encode_chunk_sm<F, true, kBf, kTex>(lv, a.g.table, hmask, x0, x1, x2, lc * (8 / F),
@@ -647,7 +676,7 @@ __device__ __forceinline__ void rows_decode(const QueryArgs& a, WarpSlots& S, co
 // ------------------------------------------------------------------ query kernel, per-warp MLP
 // Shared-memory plan of k_query_warp (bytes), shared by the kernel and its launcher: the MLP
 // weights ([out][in] padded for ldmatrix) and level table once per CTA, then one private
-// region per warp (feature rows [16][D+8], z, sample points, slots).
+// region per warp (feature rows [16][D+8], which the z tile aliases, and the slots).
 struct QuerySmemPlan {
     size_t w, bias, lv, warp0, feat, z, xs, slots, per_warp, total;
     int warps;
@@ -656,10 +685,15 @@ struct QuerySmemPlan {
         bias = w + align16((size_t)mlp_smem_halves(d_in, hidden) * 2);
         lv = bias + align16((size_t)(64 * hidden + 8) * 4);
         warp0 = lv + align16(sizeof(LevelSm) * kMaxLevels);
+        // z aliases the feature rows (the MLP's output layer writes it after its last read of
+        // them) and there is no sample-point tile (the encode derives the points from the
+        // slots): 6.3 KB per warp, so that 24 warps fit the 196 KB shared-memory carveout step
+        // (the next step leaves the table gathers ~28 KB of L1, profiles/NOTES.md r2l)
         feat = 0;
-        z = feat + align16((size_t)kWarpQ * (d_in + 8) * 2);
-        xs = z + align16((size_t)kWarpQ * 8 * 4);
-        slots = xs + align16((size_t)kWarpQ * n_points * 3 * 4);
+        z = feat;
+        xs = feat;
+        slots = feat + align16((size_t)kWarpQ * (d_in + 8) * 2);
+        (void)n_points;
         per_warp = slots + align16(sizeof(WarpSlots));
         // as many warps (<= max_warps) as fit the 227 KB per-CTA limit
         const size_t cap = 227 * 1024;
@@ -738,14 +772,15 @@ __global__ void __launch_bounds__(query_warps(kTex) * 32, 1) k_query_warp(QueryA
         WarpSlots& S = *P.S;
         slots_list_refill(a, S, P.lane);
         slots_refill(a, S, P.lane, s_work[1], s_work[0], s_exh + P.warp);
-        const int nv = slots_segment(a, S, P.xs, P.lane, NP, s_u);
+        const int nv = slots_segment<false>(a, S, nullptr, P.lane, NP, s_u);
         if (nv == 0) break;                   // work list drained and every slot finished
         if (P.lane == 0) {
             s_stat[2 * P.warp] += nv;
             s_stat[2 * P.warp + 1] += 1;
             s_nv[P.warp] = nv;
         }
-        rows_encode<F, kBf, true, kTex>(a, lv, P.xs, nv, P.lane, NP, reinterpret_cast<unsigned char*>(P.feat), 16, (D + 8) * 2);
+        rows_encode<F, kBf, true, kTex, false>(a, lv, nullptr, nv, P.lane, NP, reinterpret_cast<unsigned char*>(P.feat),
+                                               16, (D + 8) * 2, &S, s_u);
         const WarpPtrs Pm = warp_ptrs(smem_raw, plan);
         query_mlp_rows16<D, kBf>(ms, a.m.hidden, Pm.feat, 0, Pm.zt, Pm.lane);         // (E)
         __syncwarp();

@@ -280,7 +280,9 @@ static size_t scatter_smem(const TrainArgs& a) {
 // CTAs of the scatter per SM: as many as its shared memory allows (<= 6)
 static int scatter_ctas_per_sm(const TrainArgs& a) {
     const int64_t per_cta = (int64_t)scatter_smem(a) + 2048;
-    return (int)std::max<int64_t>(1, std::min<int64_t>(6, (int64_t)(228 * 1024) / per_cta));
+    int64_t cap = 6;
+    if (const char* ev = std::getenv("NBVH_SCATTER_CTAS")) cap = std::max(1, std::atoi(ev));   // A/B hook
+    return (int)std::max<int64_t>(1, std::min<int64_t>(cap, (int64_t)(228 * 1024) / per_cta));
 }
 
 // T7 scratch layout (k_train_scatter): every dense level cell-packed (N^3 cells x 8 corners x

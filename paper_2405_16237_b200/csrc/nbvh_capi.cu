@@ -255,9 +255,13 @@ extern "C" nbvh_status nbvh_create(const nbvh_config* cfg, int cuda_device, nbvh
             delete x;
             return NBVH_EINVAL;
         }
-    {   // inference layout: dense levels corner-packed (8 entries per cell), 8-entry aligned
+    {   // inference layout: dense levels corner-packed (8 entries per cell), 8-entry aligned;
+        // hashed levels T-aligned, so that offset + hash = offset | hash (the TEX encode folds
+        // the offset into its XOR)
         int64_t o = 0;
+        const int64_t T = (int64_t)1 << c.log2_T;
         for (int l = 0; l < c.L; ++l) {
+            if (!x->dense[l]) o = (o + T - 1) & ~(T - 1);
             x->inf_offset[l] = o;
             const int64_t N = x->res[l];
             o += x->dense[l] ? 8 * N * N * N : (int64_t)1 << c.log2_T;

@@ -582,10 +582,14 @@ __device__ __forceinline__ void encode_issue(const LevelSm* lv, const void* tab,
                 // through the TEX pipe (a texture object over the same fp16 table, element
                 // reads): the query kernel's limit is the LSU data pipe, which the TEX pipe
                 // does not share -- the dense levels' 32-byte records stay on LDG.256
+                // hashed levels are T-aligned in the inference layout (off + h = off | h), so
+                // the offset folds into the z term: one 3-input XOR per corner address
+                NBVH_DCHECK((P.off & hmask) == 0u);
+                const uint32_t hzo[2] = {hz[0] | P.off, hz[1] | P.off};
 #pragma unroll
                 for (int k = 0; k < 8; ++k)
                     G.v[j][k] = tex1Dfetch<unsigned int>(
-                        (cudaTextureObject_t)tex, (int)(P.off + (hx[k & 1] ^ hy[(k >> 1) & 1] ^ hz[(k >> 2) & 1])));
+                        (cudaTextureObject_t)tex, (int)(hx[k & 1] ^ hy[(k >> 1) & 1] ^ hzo[(k >> 2) & 1]));
             } else {
 #pragma unroll
                 for (int k = 0; k < 8; ++k)

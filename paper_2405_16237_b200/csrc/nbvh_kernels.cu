@@ -1187,7 +1187,6 @@ __global__ void __launch_bounds__(256, 2) k_debug_mlp(DebugMlpArgs a) {
 }
 
 // ------------------------------------------------------------------ launchers
-size_t query_smem_bytes(int d_in, int hidden, int n_points) { return QuerySmemPlan(d_in, hidden, n_points).total; }
 size_t mlp_smem_bytes(int d_in, int hidden) {
     return (size_t)kTileQ * (d_in + 8) * 2 + (size_t)mlp_smem_halves(d_in, hidden) * 2 + kTileQ * 8 * 4 +
            (64 * hidden + 8) * 4;

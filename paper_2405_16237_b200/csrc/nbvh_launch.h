@@ -112,7 +112,6 @@ struct DebugMlpArgs {
 cudaError_t launch_traverse(const TraverseArgs& a, cudaStream_t s);
 cudaError_t launch_debug_traverse(const DebugTraverseArgs& a, cudaStream_t s);
 cudaError_t launch_query(const QueryArgs& a, int64_t max_work, cudaStream_t s);
-size_t query_smem_bytes(int d_in, int hidden, int n_points);
 cudaError_t launch_debug_encode(const DebugEncodeArgs& a, cudaStream_t s);
 cudaError_t launch_debug_mlp(const DebugMlpArgs& a, cudaStream_t s);
 

@@ -252,6 +252,19 @@ def test_query_tiny_end_to_end(orc, tiny):
     assert g["hit"].sum() > 500 and g["n_queries"].max() >= 2
 
 
+@pytest.mark.parametrize("over", [dict(n_points=2), dict(n_points=1, L=16)])
+def test_query_other_point_counts(orc, over):
+    """k_query_warp derives each row's sample points from its slot (no point tile; the two
+    half-warps take points of opposite parity): n = 2 (one point per half-warp) and n = 1 (the
+    second half-warp idle in the encode), end to end against the oracle.  What this test
+    targets is the exact part (replay, and hit / leaf / query count on every ray outside the
+    ambiguity band); the band's size is a property of the random decoder, and at D_in = 32
+    it is larger than the main configurations' 1% (1.4% measured), so it is bounded at 3%."""
+    ctx, sc, tab, layers = _mk_ctx("tiny", **over)
+    g, o = _check_query(orc, ctx, tab, layers, _rays_tiny(), band_max=0.03)
+    assert g["hit"].sum() > 100 and g["n_queries"].max() >= 2
+
+
 def test_query_first_hit_mode(orc):
     ctx, sc, tab, layers = _mk_ctx("tiny", mode=1)
     _check_query(orc, ctx, tab, layers, _rays_tiny(), mode=1)

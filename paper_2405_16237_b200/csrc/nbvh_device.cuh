@@ -418,7 +418,7 @@ struct LevelSm {
     uint32_t nx, nxy;    // dense: N, N^2 (packed-cell index); hashed: 0, 0
     uint32_t coff;       // canonical entry offset (gradient / parameter layout)
     uint32_t n1, n1sq;   // dense: N+1, (N+1)^2 (canonical vertex index, C2); hashed: 0, 0
-    uint32_t pad;
+    float tops;          // 2^23 + N - 1 (exact): the cell clamp of cell_coord
 };
 
 // Stage the level table from the kernel parameter block with compile-time indices only
@@ -437,7 +437,7 @@ __device__ __forceinline__ void stage_levels(const GridDev& g, LevelSm* lv, int 
             lv[l].coff = g.offset[l];
             lv[l].n1 = dn ? n1 : 0u;
             lv[l].n1sq = dn ? n1 * n1 : 0u;
-            lv[l].pad = 0u;
+            lv[l].tops = __fadd_rn((float)g.res[l], 8388607.0f);
         }
     }
 }
@@ -485,7 +485,7 @@ __device__ __forceinline__ float cell_coord(float s, float tops, uint32_t& i) {
 __device__ __forceinline__ void level_cell_sm(const LevelSm& P, uint32_t hmask, float x0, float x1, float x2,
                                               Cell& c, uint32_t& i0, uint32_t& i1, uint32_t& i2) {
     const float s0 = __fmul_rn(x0, P.resf), s1 = __fmul_rn(x1, P.resf), s2 = __fmul_rn(x2, P.resf);
-    const float tops = __fadd_rn(P.resf, 8388607.0f);       // 2^23 + N - 1 (exact)
+    const float tops = P.tops;                              // 2^23 + N - 1 (exact)
     const float c0 = cell_coord(s0, tops, i0), c1 = cell_coord(s1, tops, i1), c2 = cell_coord(s2, tops, i2);
     const float f0 = __fsub_rn(s0, c0), f1 = __fsub_rn(s1, c1), f2 = __fsub_rn(s2, c2);
     if (P.n1) {   // canonical dense vertex index (C2)
@@ -532,7 +532,7 @@ __device__ __forceinline__ void encode_issue(const LevelSm* lv, const void* tab,
     for (int j = 0; j < NL; ++j) {
         const LevelSm P = lv[l0 + j];
         const float s0 = __fmul_rn(x0, P.resf), s1 = __fmul_rn(x1, P.resf), s2 = __fmul_rn(x2, P.resf);
-        const float tops = __fadd_rn(P.resf, 8388607.0f);   // 2^23 + N - 1 (exact)
+        const float tops = P.tops;                          // 2^23 + N - 1 (exact)
         uint32_t i0, i1, i2;
         const float c0 = cell_coord(s0, tops, i0), c1 = cell_coord(s1, tops, i1), c2 = cell_coord(s2, tops, i2);
         G.fr[j][0] = __fsub_rn(s0, c0);
